@@ -1,0 +1,310 @@
+/*
+ * blockeig_b200.h -- C ABI of the B200-native LOBPCG hot path.
+ *
+ * This is the drop-in boundary for the reference library `blockeig`
+ * (/root/reference/proj/include/blockeig/*.hpp). Every entry point below is
+ * plain C: opaque handles, raw pointers and sizes, no C++ or torch types.
+ * Each one names the reference interface it replaces (file:line relative to
+ * /root/reference/proj/include/blockeig/). The C++ mirror of the reference API
+ * (namespace blockeig, paper_2109_00485_b200/cpp/blockeig/*.hpp) is a thin
+ * header-only layer over these functions and re-throws the reference's typed
+ * exceptions from the status codes.
+ *
+ * Conventions
+ *   - Every function returns be_status; BE_OK == 0. On failure the message is
+ *     available from be_last_error() (thread-local) and, for
+ *     BE_ERR_NOT_POSITIVE_DEFINITE, the pivot index from be_last_error_pivot().
+ *   - Multivectors ("panels") are row-major n x nb, element (r, v) at
+ *     r * nb + v, exactly the BlockVector layout (block_vector.hpp:16-39).
+ *   - "_dev" pointers are CUDA device pointers; "stream" is a cudaStream_t
+ *     passed as void* (NULL = the context's own stream).
+ *   - Host-buffer variants (suffix _host) copy in/out inside the call; they
+ *     are the reference-facing Operator adapter (lobpcg.hpp:20).
+ */
+#ifndef BLOCKEIG_B200_H
+#define BLOCKEIG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* One status code per exception class of errors.hpp:11-109. */
+typedef enum be_status {
+    BE_OK = 0,
+    BE_ERR_GENERIC = 1,                 /* blockeig::Error            errors.hpp:11  */
+    BE_ERR_BLOCK_TOO_LARGE = 2,         /* BlockTooLarge              errors.hpp:18  */
+    BE_ERR_INDEX_OUT_OF_RANGE = 3,      /* IndexOutOfRange            errors.hpp:23  */
+    BE_ERR_DUPLICATE_ENTRY = 4,         /* DuplicateEntry             errors.hpp:28  */
+    BE_ERR_DIMENSION_MISMATCH = 5,      /* DimensionMismatch          errors.hpp:33  */
+    BE_ERR_NOT_STRICTLY_LOWER = 6,      /* NotStrictlyLower           errors.hpp:38  */
+    BE_ERR_MISALIGNED_TILES = 7,        /* MisalignedTiles            errors.hpp:43  */
+    BE_ERR_BAD_PARAMS = 8,              /* BadParams                  errors.hpp:48  */
+    BE_ERR_NOT_POSITIVE_DEFINITE = 9,   /* NotPositiveDefinite{pivot} errors.hpp:55  */
+    BE_ERR_SINGULAR_TRIANGULAR = 10,    /* SingularTriangular         errors.hpp:62  */
+    BE_ERR_SINGULAR_PROJECTION = 11,    /* SingularProjection         errors.hpp:67  */
+    BE_ERR_RANK_DEFICIENT = 12,         /* RankDeficient              errors.hpp:72  */
+    BE_ERR_BASIS_DEGENERATE = 13,       /* BasisDegenerate            errors.hpp:77  */
+    BE_ERR_BREAKDOWN_UNRECOVERABLE = 14,/* BreakdownUnrecoverable     errors.hpp:82  */
+    BE_ERR_EVEN_ND = 15,                /* EvenNd                     errors.hpp:89  */
+    BE_ERR_PROTOCOL_DEADLOCK = 16,      /* ProtocolDeadlock           errors.hpp:94  */
+    BE_ERR_PARSE = 17,                  /* ParseError                 errors.hpp:101 */
+    BE_ERR_NOT_SYMMETRIC_HEADER = 18,   /* NotSymmetricHeader         errors.hpp:106 */
+    /* device-side failures with no reference counterpart */
+    BE_ERR_CUDA = 32,
+    BE_ERR_NO_DEVICE = 33,
+    BE_ERR_CUSOLVER = 34,
+    BE_ERR_NCCL = 35,
+    BE_ERR_OUT_OF_MEMORY = 36
+} be_status;
+
+typedef enum be_prec { BE_F32 = 0, BE_F64 = 1 } be_prec;
+
+/* apply modes of the operator (kernels.hpp:290-371) */
+typedef enum be_apply_mode {
+    BE_APPLY_SYMMETRIC = 0,  /* out  = (L + L^T + diag D) in   SymmetricOperator::apply kernels.hpp:357 */
+    BE_APPLY_NOTRANS_ACC = 1,/* out += L in                    spmm_notrans kernels.hpp:290 */
+    BE_APPLY_TRANS_ACC = 2   /* out += L^T in                  spmm_trans   kernels.hpp:302 */
+} be_apply_mode;
+
+const char* be_last_error(void);
+int be_last_error_pivot(void);
+const char* be_version(void);
+
+/* ------------------------------------------------------------------------- */
+/* Host-side CSB_Coo storage (csb.hpp:39-63).                                 */
+/* ------------------------------------------------------------------------- */
+
+/* Triple layout of csb.hpp:20-24 (24 bytes: i64 row, i64 col, f64 value). */
+typedef struct be_triple {
+    int64_t row;
+    int64_t col;
+    double value;
+} be_triple;
+
+/* Read-only view of a CsbCooMatrix: the same arrays, same meaning. */
+typedef struct be_csb_view {
+    int64_t nrows, ncols, nrowblks, ncolblks, nnz;
+    const int64_t* row_offsets;        /* nrowblks + 1 */
+    const int64_t* col_offsets;        /* ncolblks + 1 */
+    const int64_t* block_nnz;          /* nrowblks * ncolblks, row-major */
+    const int64_t* block_nnz_offsets;  /* same shape, exclusive prefix */
+    const uint16_t* local_rows;        /* nnz */
+    const uint16_t* local_cols;        /* nnz */
+    const double* values;              /* nnz */
+} be_csb_view;
+
+typedef struct be_csb be_csb; /* owned host CSB */
+
+/* build_csb_coo (csb.hpp:100-161): block row-major grouping, input order
+ * kept inside a block, range check then duplicate check. */
+be_status be_csb_build(const be_triple* triples, int64_t count, int64_t nrows, int64_t ncols,
+                       const int64_t* row_bounds, int64_t n_row_bounds,
+                       const int64_t* col_bounds, int64_t n_col_bounds, be_csb** out);
+/* uniform_boundaries (csb.hpp:89-96); *count receives nblk + 1. out may be
+ * NULL to query the count. */
+be_status be_uniform_boundaries(int64_t n, int64_t extent, int64_t* out, int64_t* count);
+be_status be_csb_view_get(const be_csb* m, be_csb_view* view);
+/* is_strictly_lower (csb.hpp:188-202) on any view; *result = 0/1 */
+be_status be_csb_is_strictly_lower(const be_csb_view* view, int* result);
+/* to_triples (csb.hpp:165-185); out holds view->nnz triples */
+be_status be_csb_to_triples(const be_csb_view* view, be_triple* out);
+/* CSB1 binary cache (csb.hpp:204-302) plus the driver's appended diagonal
+ * section (driver.hpp:136-161); diag may be NULL/0 for the bare format. */
+be_status be_csb_save(const char* path, const be_csb_view* view, const double* diag, int64_t ndiag);
+be_status be_csb_load(const char* path, be_csb** out, double** diag, int64_t* ndiag);
+void be_free_buffer(void* p);
+void be_csb_free(be_csb* m);
+
+/* ------------------------------------------------------------------------- */
+/* Synthetic inputs (tooling, not the hot path).                              */
+/* ------------------------------------------------------------------------- */
+
+typedef enum be_synth_kind { BE_SYNTH_BANDED = 0, BE_SYNTH_BLOCKTILE = 1, BE_SYNTH_RANDOM = 2 } be_synth_kind;
+
+typedef struct be_synth_params { /* SynthParams, synth.hpp:33-56 */
+    int kind;
+    int64_t n;
+    double density;
+    int64_t bandwidth;
+    int64_t block_extent;
+    int64_t tile_min, tile_max;
+    double diag_spread;
+    double dominance;
+    uint64_t seed;
+} be_synth_params;
+
+typedef struct be_synth be_synth;
+/* generate_synthetic (synth.hpp:92-158): identical triples, diagonal and tile
+ * offsets for identical params (same mt19937_64 stream). */
+be_status be_generate_synthetic(const be_synth_params* p, be_synth** out);
+be_status be_synth_get(const be_synth* s, const be_triple** lower, int64_t* nlower,
+                       const double** diag, const int64_t** tile_offsets, int64_t* n_tile_offsets);
+void be_synth_free(be_synth* s);
+
+/* Clustered generator for the Test-1..3 shapes (new): CSB blocks
+ * of block_extent, occupied tile x tile sub-tiles at fill `fill`, counter-based
+ * RNG keyed by (seed, block, tile) so generation is parallel and
+ * deterministic. Writes a CSB directly (no triple list) plus the diagonal
+ * 0.5 + U(0, diag_spread) + dominance * sum|row| and the log-uniform
+ * preconditioner tile offsets of synth.hpp:67-83. */
+typedef struct be_cluster_params {
+    int64_t n;
+    int64_t target_nnz;     /* strictly-lower nonzeros wanted (approximate) */
+    int64_t block_extent;   /* CSB block extent (4000) */
+    int64_t tile;           /* occupied sub-tile edge (128) */
+    double fill;            /* within-tile fill (0.10) */
+    double block_occupancy; /* fraction of lower CSB blocks holding tiles (1.0 = all) */
+    int64_t tile_min, tile_max;
+    double diag_spread, dominance;
+    uint64_t seed;
+    int threads;            /* 0 = all hardware threads */
+} be_cluster_params;
+be_status be_generate_clustered(const be_cluster_params* p, be_csb** out, double** diag,
+                                int64_t** tile_offsets, int64_t* n_tile_offsets);
+
+/* ------------------------------------------------------------------------- */
+/* Device context and the symmetric operator (SymmetricOperator,             */
+/* kernels.hpp:339-378).                                                      */
+/* ------------------------------------------------------------------------- */
+
+typedef struct be_ctx be_ctx;
+be_status be_ctx_create(int device, be_ctx** out);
+be_status be_ctx_destroy(be_ctx* ctx);
+be_status be_ctx_stream(be_ctx* ctx, void** stream);
+be_status be_ctx_synchronize(be_ctx* ctx);
+/* kernel-launch counter of this context (evidence for bench gpu_launches) */
+be_status be_ctx_launches(be_ctx* ctx, int64_t* launches);
+
+typedef struct be_op be_op;
+
+enum { BE_OP_SYMMETRIC = 1 };
+/* Upload a CSB to the device and derive the tile format.
+ * flags & BE_OP_SYMMETRIC: validates square + strictly lower + diag length
+ * like the SymmetricOperator constructor (kernels.hpp:341-350); diag (host,
+ * nrows doubles) is copied. Without the flag the matrix may be rectangular
+ * and only the NOTRANS/TRANS accumulate modes are valid (diag ignored). */
+be_status be_op_create(be_ctx* ctx, const be_csb_view* L, const double* diag, int values_prec,
+                       int flags, be_op** out);
+be_status be_op_destroy(be_op* op);
+
+/* Y = op(X) on device panels of type panel_prec (BE_F32 / BE_F64),
+ * row-major nrows x nb. mode: be_apply_mode. X and Y must not alias
+ * (kernels.hpp:284). */
+be_status be_op_apply(be_op* op, const void* X_dev, void* Y_dev, int64_t nrows, int nb,
+                      int panel_prec, int mode, void* stream);
+/* Host-buffer adapter: fp64 host panels in and out (Y read for the
+ * accumulate modes), copies inside the call. */
+be_status be_op_apply_host(be_op* op, const double* X, double* Y, int64_t nrows, int nb, int mode);
+
+typedef struct be_op_info {
+    int64_t nrows, ncols, nnz;
+    int64_t ntiles;          /* device work tiles */
+    int64_t device_bytes;    /* tile-format bytes resident in HBM */
+    int64_t bytes_per_nnz_x1000;
+    int values_prec;
+    int tile_rows, tile_cols, tile_max_nnz;
+} be_op_info;
+be_status be_op_get_info(const be_op* op, be_op_info* info);
+
+/* Decode the device tile format back to global coordinates in device order
+ * (row, col, value) plus, for each entry, its index in the source CSB arrays.
+ * Used by the bit-exact indexing tests. Buffers hold info.nnz entries. */
+be_status be_op_decode(be_op* op, int64_t* rows, int64_t* cols, double* values, int64_t* csb_index);
+
+/* Average device time (ms) of the dominant SpMM kernel over the last `n`
+ * applies, measured with CUDA events on the launching stream. */
+be_status be_op_timing(be_op* op, int enable, double* last_kernel_ms, double* last_apply_ms);
+
+/* ------------------------------------------------------------------------- */
+/* Block-diagonal FOM preconditioner (precond.hpp).                           */
+/* ------------------------------------------------------------------------- */
+
+typedef struct be_tiles be_tiles;
+/* extract_tiles (precond.hpp:63-127) + upload. */
+be_status be_tiles_create(be_ctx* ctx, const be_csb_view* L, const double* diag,
+                          const int64_t* tile_offsets, int64_t n_tile_offsets, be_tiles** out);
+be_status be_tiles_destroy(be_tiles* t);
+/* Host copy of tile j in the reference's SparseTile layout (precond.hpp:18-30):
+ * query sizes with NULL buffers. */
+be_status be_tiles_get(const be_tiles* t, int64_t j, int64_t* dim, int64_t* nentries, int32_t* rows,
+                       int32_t* cols, double* values, int64_t* diag_pos);
+be_status be_tiles_count(const be_tiles* t, int64_t* count, int64_t* dim);
+/* W = K^{-1} R (apply_preconditioner, precond.hpp:287-317). Device fp64
+ * panels; shifts_dev: nb doubles on device; fallbacks_dev: one int64 on
+ * device incremented by the number of singular columns (may be NULL). */
+be_status be_precond_apply(be_tiles* t, const double* shifts_dev, const double* R_dev, double* W_dev,
+                           int64_t nrows, int nb, int m, int64_t* fallbacks_dev, void* stream);
+be_status be_precond_apply_host(be_tiles* t, const double* shifts, const double* R, double* W,
+                                int64_t nrows, int nb, int m, int64_t* fallbacks);
+
+/* ------------------------------------------------------------------------- */
+/* LOBPCG (lobpcg.hpp:291-456), device-resident.                              */
+/* ------------------------------------------------------------------------- */
+
+typedef struct be_solver_config { /* SolverConfig lobpcg.hpp:24-48 */
+    int k;
+    int nb;                 /* 0 -> k + 3 */
+    double tol;
+    int maxiter;
+    int fom_iterations;     /* FomConfig::iterations precond.hpp:51-57 */
+    uint64_t seed;
+    int observer_state;     /* 1: copy X and HX to host for the observer */
+} be_solver_config;
+
+/* Per-iteration hook (SolverConfig::observer, lobpcg.hpp:33-34, 436).
+ * x and hx are host n x nb copies when observer_state, else NULL. */
+typedef void (*be_observer_fn)(void* user, int iter, int64_t n, int nb, const double* theta,
+                               const double* residual_norms, int n_converged, const double* x,
+                               const double* hx);
+/* Generic host operator (lobpcg.hpp:20): out = H in on host panels. */
+typedef int (*be_host_operator_fn)(void* user, const double* in, double* out, int64_t n, int nb);
+
+typedef struct be_result be_result;
+/* lobpcg_solve: exactly one of op / host_op is used (op wins). precond and
+ * x0 (host, n x nb) may be NULL. */
+be_status be_lobpcg_solve(be_ctx* ctx, be_op* op, be_host_operator_fn host_op, void* host_op_user,
+                          int64_t n, be_tiles* precond, const double* x0, const be_solver_config* cfg,
+                          be_observer_fn observer, void* observer_user, be_result** out);
+
+typedef struct be_result_info {
+    int converged;
+    int iterations;
+    int k;
+    int nb;
+    int64_t n;
+    int64_t operator_calls;
+    int64_t precond_fallbacks;
+    int restarts;
+} be_result_info;
+be_status be_result_get_info(const be_result* r, be_result_info* info);
+/* lambda: k values; x: n x k row-major. */
+be_status be_result_get(const be_result* r, double* lambda, double* x);
+/* IterationRecord lobpcg.hpp:60-66 for iteration index i (0-based):
+ * theta and residual_norms hold nb values. */
+be_status be_result_get_record(const be_result* r, int i, double* theta, double* residual_norms,
+                               int* n_converged, double* t_spmm, double* t_precond, double* t_dense,
+                               double* t_total);
+void be_result_free(be_result* r);
+
+/* ------------------------------------------------------------------------- */
+/* Device dense kernels exposed for parity tests (densela.hpp).               */
+/* ------------------------------------------------------------------------- */
+
+/* out (p x q, column-major like SmallDense densela.hpp:19-47) = A^T B over
+ * device fp64 panels A (n x p) and B (n x q); symmetrised when A == B
+ * (gram, densela.hpp:70-99). out is a host buffer. */
+be_status be_gram(be_ctx* ctx, const double* A_dev, int p, const double* B_dev, int q, int64_t n,
+                  double* out);
+/* k lowest eigenpairs of (A, B) with the pivot floor (sygv_lowest,
+ * densela.hpp:357-407): host n x n column-major inputs, outputs
+ * c (n x k column-major) and d (k), computed on the device. */
+be_status be_sygv_lowest(be_ctx* ctx, const double* A, const double* B, int n, int k,
+                         double pivot_floor, double* c, double* d);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLOCKEIG_B200_H */

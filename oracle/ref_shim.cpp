@@ -1,0 +1,315 @@
+// ORACLE -- test infrastructure only. Not part of the product.
+//
+// C-ABI shim over the UNMODIFIED reference headers in
+// /root/reference/proj/include/blockeig (compiled from where they lie by
+// oracle/Makefile into oracle/_ref/libref.so; no reference source is copied
+// into this repository). It lets the tests pin the restatement in
+// oracle/oracle.cpp and lets bench.py time the reference's own CPU path
+// (cpu_baseline kind "reference").
+#include <blockeig/densela.hpp>
+#include <blockeig/kernels.hpp>
+#include <blockeig/lobpcg.hpp>
+#include <blockeig/precond.hpp>
+#include <blockeig/synth.hpp>
+
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+
+using namespace blockeig;
+
+namespace {
+thread_local std::string g_msg;
+
+int code_of(const Error& e) {
+    if (dynamic_cast<const BlockTooLarge*>(&e)) return 2;
+    if (dynamic_cast<const IndexOutOfRange*>(&e)) return 3;
+    if (dynamic_cast<const DuplicateEntry*>(&e)) return 4;
+    if (dynamic_cast<const DimensionMismatch*>(&e)) return 5;
+    if (dynamic_cast<const NotStrictlyLower*>(&e)) return 6;
+    if (dynamic_cast<const MisalignedTiles*>(&e)) return 7;
+    if (dynamic_cast<const BadParams*>(&e)) return 8;
+    if (dynamic_cast<const NotPositiveDefinite*>(&e)) return 9;
+    if (dynamic_cast<const SingularTriangular*>(&e)) return 10;
+    if (dynamic_cast<const SingularProjection*>(&e)) return 11;
+    if (dynamic_cast<const RankDeficient*>(&e)) return 12;
+    if (dynamic_cast<const BasisDegenerate*>(&e)) return 13;
+    if (dynamic_cast<const BreakdownUnrecoverable*>(&e)) return 14;
+    return 1;
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const Error& e) {
+        g_msg = e.what();
+        return code_of(e);
+    } catch (const std::exception& e) {
+        g_msg = e.what();
+        return 1;
+    }
+}
+
+struct View {
+    index_t nrows, ncols, nrb, ncb, nnz;
+    const index_t *ro, *co, *bn, *bo;
+    const std::uint16_t *lr, *lc;
+    const double* v;
+};
+
+CsbCooMatrix to_matrix(const void* p) {
+    const View* v = static_cast<const View*>(p);
+    CsbCooMatrix m;
+    m.nrows = v->nrows;
+    m.ncols = v->ncols;
+    m.nrowblks = v->nrb;
+    m.ncolblks = v->ncb;
+    m.row_offsets.assign(v->ro, v->ro + v->nrb + 1);
+    m.col_offsets.assign(v->co, v->co + v->ncb + 1);
+    m.block_nnz.assign(v->bn, v->bn + v->nrb * v->ncb);
+    m.block_nnz_offsets.assign(v->bo, v->bo + v->nrb * v->ncb);
+    m.local_rows.assign(v->lr, v->lr + v->nnz);
+    m.local_cols.assign(v->lc, v->lc + v->nnz);
+    m.values.assign(v->v, v->v + v->nnz);
+    return m;
+}
+
+std::unique_ptr<ThreadPool> pool_of(int threads) {
+    return threads > 1 ? std::make_unique<ThreadPool>(threads) : nullptr;
+}
+
+// A prepared problem kept alive across timed calls (bench cpu_baseline).
+struct Prepared {
+    CsbCooMatrix m;
+    std::vector<double> diag;
+    std::unique_ptr<ThreadPool> pool;
+    std::unique_ptr<SymmetricOperator> op;
+    std::optional<DiagonalTileSet> tiles;
+};
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_msg.c_str(); }
+
+// generate_synthetic (synth.hpp:92): counts first (buffers NULL), then data
+int ref_generate_synthetic(int kind, index_t n, double density, index_t bandwidth, index_t block_extent,
+                           std::uint64_t seed, index_t* nlower, index_t* rows, index_t* cols, double* vals,
+                           double* diag, index_t* ntoff, index_t* toff) {
+    return guarded([&] {
+        SynthParams p;
+        p.kind = kind == 0 ? SynthKind::Banded : kind == 1 ? SynthKind::BlockTile : SynthKind::Random;
+        p.n = n;
+        p.density = density;
+        p.bandwidth = bandwidth;
+        p.block_extent = block_extent;
+        p.seed = seed;
+        const auto s = generate_synthetic(p);
+        *nlower = static_cast<index_t>(s.coo.lower.size());
+        *ntoff = static_cast<index_t>(s.tile_offsets.size());
+        if (rows) {
+            for (std::size_t i = 0; i < s.coo.lower.size(); ++i) {
+                rows[i] = s.coo.lower[i].row;
+                cols[i] = s.coo.lower[i].col;
+                vals[i] = s.coo.lower[i].value;
+            }
+            std::copy(s.coo.diag.begin(), s.coo.diag.end(), diag);
+            std::copy(s.tile_offsets.begin(), s.tile_offsets.end(), toff);
+        }
+    });
+}
+
+// build_csb_coo (csb.hpp:100): outputs sized by the caller (nblocks, count)
+int ref_build_csb(const index_t* rows, const index_t* cols, const double* vals, index_t count, index_t nrows,
+                  index_t ncols, const index_t* rb, index_t nrb, const index_t* cb, index_t ncb, index_t* block_nnz,
+                  index_t* block_off, std::uint16_t* lr, std::uint16_t* lc, double* v) {
+    return guarded([&] {
+        std::vector<Triple> t(static_cast<std::size_t>(count));
+        for (index_t i = 0; i < count; ++i) t[i] = {rows[i], cols[i], vals[i]};
+        const auto m = build_csb_coo(t, nrows, ncols, std::vector<index_t>(rb, rb + nrb), std::vector<index_t>(cb, cb + ncb));
+        std::copy(m.block_nnz.begin(), m.block_nnz.end(), block_nnz);
+        std::copy(m.block_nnz_offsets.begin(), m.block_nnz_offsets.end(), block_off);
+        std::copy(m.local_rows.begin(), m.local_rows.end(), lr);
+        std::copy(m.local_cols.begin(), m.local_cols.end(), lc);
+        std::copy(m.values.begin(), m.values.end(), v);
+    });
+}
+
+// SymmetricOperator::apply / spmm_notrans / spmm_trans with a chosen variant
+int ref_spmm(const void* view, const double* diag, const double* X, double* Y, index_t nb, int mode, int variant,
+             int threads) {
+    return guarded([&] {
+        const auto m = to_matrix(view);
+        auto pool = pool_of(threads);
+        const KernelVariant kv = variant == 0 ? KernelVariant::baseline()
+                                 : variant == 1 ? KernelVariant::fused_atomic()
+                                                : KernelVariant::cache_blocked();
+        const index_t in_rows = mode == 1 ? m.ncols : m.nrows, out_rows = mode == 2 ? m.ncols : m.nrows;
+        BlockVector in(in_rows, nb), out(out_rows, nb);
+        std::copy(X, X + in_rows * nb, in.data.begin());
+        if (mode == 0) {
+            SymmetricOperator op(m, std::vector<double>(diag, diag + m.nrows), kv, pool.get());
+            op.apply(in, out);
+        } else {
+            std::copy(Y, Y + out_rows * nb, out.data.begin());
+            if (mode == 1)
+                spmm_notrans(m, in, out, kv, pool.get());
+            else
+                spmm_trans(m, in, out, kv, pool.get());
+        }
+        std::copy(out.data.begin(), out.data.end(), Y);
+    });
+}
+
+int ref_precond(const void* view, const double* diag, const index_t* off, index_t noff, const double* shifts,
+                const double* R, double* W, index_t nb, int m, index_t* fallbacks) {
+    return guarded([&] {
+        const auto mat = to_matrix(view);
+        const auto tiles = extract_tiles(mat, std::span<const double>(diag, mat.nrows), std::vector<index_t>(off, off + noff));
+        BlockVector r(mat.nrows, nb);
+        std::copy(R, R + mat.nrows * nb, r.data.begin());
+        FomConfig cfg;
+        cfg.iterations = m;
+        std::int64_t fb = 0;
+        const auto w = apply_preconditioner(tiles, std::span<const double>(shifts, nb), r, cfg, nullptr, &fb);
+        std::copy(w.data.begin(), w.data.end(), W);
+        if (fallbacks) *fallbacks = fb;
+    });
+}
+
+int ref_sygv_lowest(const double* A, const double* B, int n, int k, double floor, double* c, double* d) {
+    return guarded([&] {
+        SmallDense a(n, n), b(n, n);
+        std::copy(A, A + n * n, a.data.begin());
+        std::copy(B, B + n * n, b.data.begin());
+        const auto r = sygv_lowest(a, b, k, floor);
+        std::copy(r.c.data.begin(), r.c.data.end(), c);
+        std::copy(r.d.begin(), r.d.end(), d);
+    });
+}
+
+// lobpcg_solve through the SymmetricOperator overload (lobpcg.hpp:452)
+int ref_lobpcg(const void* view, const double* diag, const index_t* off, index_t noff, const double* x0, int k, int nb,
+               double tol, int maxiter, int fom_m, std::uint64_t seed, int variant, int threads, double* lambda,
+               double* x, double* theta_hist, double* res_hist, int* nconv_hist, double* phase_times,
+               index_t* info) {
+    return guarded([&] {
+        const auto m = to_matrix(view);
+        auto pool = pool_of(threads);
+        const KernelVariant kv = variant == 0 ? KernelVariant::baseline()
+                                 : variant == 1 ? KernelVariant::fused_atomic()
+                                                : KernelVariant::cache_blocked();
+        SymmetricOperator op(m, std::vector<double>(diag, diag + m.nrows), kv, pool.get());
+        std::optional<DiagonalTileSet> tiles;
+        if (noff > 0) tiles.emplace(extract_tiles(m, std::span<const double>(diag, m.nrows), std::vector<index_t>(off, off + noff)));
+        SolverConfig cfg;
+        cfg.k = k;
+        cfg.nb = nb;
+        cfg.tol = tol;
+        cfg.maxiter = maxiter;
+        cfg.fom.iterations = fom_m;
+        cfg.seed = seed;
+        cfg.variant = kv;
+        cfg.pool = pool.get();
+        std::optional<BlockVector> xb;
+        if (x0) {
+            xb.emplace(m.nrows, cfg.block_width());
+            std::copy(x0, x0 + m.nrows * cfg.block_width(), xb->data.begin());
+        }
+        const auto res = lobpcg_solve(op, tiles ? &*tiles : nullptr, xb ? &*xb : nullptr, cfg);
+        std::copy(res.lambda.begin(), res.lambda.end(), lambda);
+        if (x) std::copy(res.x.data.begin(), res.x.data.end(), x);
+        const int w = cfg.block_width();
+        double ts = 0, tp = 0, td = 0, tt = 0;
+        for (std::size_t i = 0; i < res.history.records.size(); ++i) {
+            const auto& r = res.history.records[i];
+            if (theta_hist) std::copy(r.theta.begin(), r.theta.end(), theta_hist + i * w);
+            if (res_hist) std::copy(r.residual_norms.begin(), r.residual_norms.end(), res_hist + i * w);
+            if (nconv_hist) nconv_hist[i] = r.n_converged;
+            ts += r.t_spmm;
+            tp += r.t_precond;
+            td += r.t_dense;
+            tt += r.t_total;
+        }
+        if (phase_times) {
+            phase_times[0] = ts;
+            phase_times[1] = tp;
+            phase_times[2] = td;
+            phase_times[3] = tt;
+        }
+        info[0] = res.converged ? 1 : 0;
+        info[1] = static_cast<index_t>(res.history.records.size());
+        info[2] = res.history.operator_calls;
+        info[3] = res.history.precond_fallbacks;
+        info[4] = res.history.restarts;
+    });
+}
+
+// ---- persistent problem for timing loops (bench.py cpu_baseline) ----------
+void* ref_prepare(const void* view, const double* diag, const index_t* off, index_t noff, int threads) {
+    try {
+        auto p = new Prepared;
+        p->m = to_matrix(view);
+        p->diag.assign(diag, diag + p->m.nrows);
+        p->pool = pool_of(threads);
+        p->op = std::make_unique<SymmetricOperator>(p->m, p->diag, KernelVariant::baseline(), p->pool.get());
+        if (noff > 0)
+            p->tiles.emplace(extract_tiles(p->m, p->diag, std::vector<index_t>(off, off + noff)));
+        return p;
+    } catch (const std::exception& e) {
+        g_msg = e.what();
+        return nullptr;
+    }
+}
+
+void ref_release(void* p) { delete static_cast<Prepared*>(p); }
+
+// time `reps` SymmetricOperator::apply calls; returns seconds per apply (median)
+double ref_time_apply(void* pp, index_t nb, std::uint64_t seed, int reps) {
+    auto* p = static_cast<Prepared*>(pp);
+    const BlockVector w = random_block(p->m.nrows, nb, seed);
+    BlockVector u(p->m.nrows, nb);
+    std::vector<double> t;
+    for (int r = 0; r < reps; ++r) {
+        const auto t0 = std::chrono::steady_clock::now();
+        p->op->apply(w, u);
+        t.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    }
+    std::sort(t.begin(), t.end());
+    return t[t.size() / 2];
+}
+
+// run `iters` LOBPCG iterations (tol=1e-300, as test_lobpcg.cpp:341) and
+// return wall seconds; phase sums into phase_times[4]
+double ref_time_lobpcg(void* pp, int k, int nb, int iters, std::uint64_t seed, int use_precond, double* phase_times) {
+    auto* p = static_cast<Prepared*>(pp);
+    SolverConfig cfg;
+    cfg.k = k;
+    cfg.nb = nb;
+    cfg.tol = 1e-300;
+    cfg.maxiter = iters;
+    cfg.seed = seed;
+    cfg.pool = p->pool.get();
+    const auto t0 = std::chrono::steady_clock::now();
+    const auto res = lobpcg_solve(*p->op, use_precond && p->tiles ? &*p->tiles : nullptr, nullptr, cfg);
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    double ts = 0, tp = 0, td = 0, tt = 0;
+    for (const auto& r : res.history.records) {
+        ts += r.t_spmm;
+        tp += r.t_precond;
+        td += r.t_dense;
+        tt += r.t_total;
+    }
+    if (phase_times) {
+        phase_times[0] = ts;
+        phase_times[1] = tp;
+        phase_times[2] = td;
+        phase_times[3] = tt;
+    }
+    return wall;
+}
+
+}  // extern "C"

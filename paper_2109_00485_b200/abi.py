@@ -1,0 +1,390 @@
+"""ctypes binding of the C ABI in include/blockeig_b200.h.
+
+Used by the tests and bench.py to drive libblockeig_b200.so exactly the way
+a foreign-language host (cgo / JNI / ctypes) would. There is no fallback:
+if the shared library is missing or a call fails, an exception is raised
+(`BlockeigError` subclasses named after errors.hpp).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libblockeig_b200.so"
+
+BE_F32, BE_F64 = 0, 1
+BE_APPLY_SYMMETRIC, BE_APPLY_NOTRANS_ACC, BE_APPLY_TRANS_ACC = 0, 1, 2
+BE_OP_SYMMETRIC = 1
+SYNTH_KINDS = {"banded": 0, "blocktile": 1, "random": 2}
+
+
+class BlockeigError(RuntimeError):
+    code = 1
+
+
+def _err(name, code):
+    return type(name, (BlockeigError,), {"code": code})
+
+
+BlockTooLarge = _err("BlockTooLarge", 2)
+IndexOutOfRange = _err("IndexOutOfRange", 3)
+DuplicateEntry = _err("DuplicateEntry", 4)
+DimensionMismatch = _err("DimensionMismatch", 5)
+NotStrictlyLower = _err("NotStrictlyLower", 6)
+MisalignedTiles = _err("MisalignedTiles", 7)
+BadParams = _err("BadParams", 8)
+NotPositiveDefinite = _err("NotPositiveDefinite", 9)
+SingularTriangular = _err("SingularTriangular", 10)
+SingularProjection = _err("SingularProjection", 11)
+RankDeficient = _err("RankDeficient", 12)
+BasisDegenerate = _err("BasisDegenerate", 13)
+BreakdownUnrecoverable = _err("BreakdownUnrecoverable", 14)
+EvenNd = _err("EvenNd", 15)
+ProtocolDeadlock = _err("ProtocolDeadlock", 16)
+ParseError = _err("ParseError", 17)
+NotSymmetricHeader = _err("NotSymmetricHeader", 18)
+CudaError = _err("CudaError", 32)
+NoDevice = _err("NoDevice", 33)
+CusolverError = _err("CusolverError", 34)
+NcclError = _err("NcclError", 35)
+OutOfMemory = _err("OutOfMemory", 36)
+_BY_CODE = {c.code: c for c in [BlockTooLarge, IndexOutOfRange, DuplicateEntry, DimensionMismatch, NotStrictlyLower,
+                                 MisalignedTiles, BadParams, NotPositiveDefinite, SingularTriangular,
+                                 SingularProjection, RankDeficient, BasisDegenerate, BreakdownUnrecoverable, EvenNd,
+                                 ProtocolDeadlock, ParseError, NotSymmetricHeader, CudaError, NoDevice,
+                                 CusolverError, NcclError, OutOfMemory]}
+
+
+class Triple(C.Structure):
+    _fields_ = [("row", C.c_int64), ("col", C.c_int64), ("value", C.c_double)]
+
+
+TRIPLE_DTYPE = np.dtype([("row", "<i8"), ("col", "<i8"), ("value", "<f8")])
+
+
+class CsbView(C.Structure):
+    _fields_ = [("nrows", C.c_int64), ("ncols", C.c_int64), ("nrowblks", C.c_int64), ("ncolblks", C.c_int64),
+                ("nnz", C.c_int64), ("row_offsets", C.c_void_p), ("col_offsets", C.c_void_p),
+                ("block_nnz", C.c_void_p), ("block_nnz_offsets", C.c_void_p), ("local_rows", C.c_void_p),
+                ("local_cols", C.c_void_p), ("values", C.c_void_p)]
+
+
+class SynthParams(C.Structure):
+    _fields_ = [("kind", C.c_int), ("n", C.c_int64), ("density", C.c_double), ("bandwidth", C.c_int64),
+                ("block_extent", C.c_int64), ("tile_min", C.c_int64), ("tile_max", C.c_int64),
+                ("diag_spread", C.c_double), ("dominance", C.c_double), ("seed", C.c_uint64)]
+
+
+class ClusterParams(C.Structure):
+    _fields_ = [("n", C.c_int64), ("target_nnz", C.c_int64), ("block_extent", C.c_int64), ("tile", C.c_int64),
+                ("fill", C.c_double), ("block_occupancy", C.c_double), ("tile_min", C.c_int64),
+                ("tile_max", C.c_int64), ("diag_spread", C.c_double), ("dominance", C.c_double),
+                ("seed", C.c_uint64), ("threads", C.c_int)]
+
+
+class OpInfo(C.Structure):
+    _fields_ = [("nrows", C.c_int64), ("ncols", C.c_int64), ("nnz", C.c_int64), ("ntiles", C.c_int64),
+                ("device_bytes", C.c_int64), ("bytes_per_nnz_x1000", C.c_int64), ("values_prec", C.c_int),
+                ("tile_rows", C.c_int), ("tile_cols", C.c_int), ("tile_max_nnz", C.c_int)]
+
+
+class SolverConfig(C.Structure):
+    _fields_ = [("k", C.c_int), ("nb", C.c_int), ("tol", C.c_double), ("maxiter", C.c_int),
+                ("fom_iterations", C.c_int), ("seed", C.c_uint64), ("observer_state", C.c_int)]
+
+
+class ResultInfo(C.Structure):
+    _fields_ = [("converged", C.c_int), ("iterations", C.c_int), ("k", C.c_int), ("nb", C.c_int), ("n", C.c_int64),
+                ("operator_calls", C.c_int64), ("precond_fallbacks", C.c_int64), ("restarts", C.c_int)]
+
+
+OBSERVER_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.c_int64, C.c_int, C.POINTER(C.c_double),
+                          C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double))
+HOST_OP_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64, C.c_int)
+
+_lib = None
+
+
+def lib():
+    """Load libblockeig_b200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise FileNotFoundError(f"{LIB_PATH} is missing: run __graft_entry__.build() first")
+        _lib = C.CDLL(str(LIB_PATH))
+        _lib.be_last_error.restype = C.c_char_p
+        _lib.be_version.restype = C.c_char_p
+        _lib.be_free_buffer.restype = None
+        _lib.be_csb_free.restype = None
+        _lib.be_synth_free.restype = None
+        if hasattr(_lib, "be_result_free"):
+            _lib.be_result_free.restype = None
+    return _lib
+
+
+def check(status: int):
+    if status != 0:
+        msg = lib().be_last_error().decode(errors="replace")
+        cls = _BY_CODE.get(status, BlockeigError)
+        e = cls(msg)
+        if status == 9:
+            e.pivot = lib().be_last_error_pivot()
+        raise e
+
+
+def _p(a):
+    return C.c_void_p(a.ctypes.data) if a is not None else C.c_void_p(0)
+
+
+# --------------------------------------------------------------------------- CSB
+class Csb:
+    """CsbCooMatrix (csb.hpp:39-63) as numpy arrays. Either owned by the
+    library (handle) or a plain set of arrays supplied by the caller."""
+
+    def __init__(self, nrows, ncols, row_offsets, col_offsets, block_nnz, block_nnz_offsets, local_rows,
+                 local_cols, values, handle=None):
+        self.nrows, self.ncols = int(nrows), int(ncols)
+        self.row_offsets = np.ascontiguousarray(row_offsets, dtype=np.int64)
+        self.col_offsets = np.ascontiguousarray(col_offsets, dtype=np.int64)
+        self.block_nnz = np.ascontiguousarray(block_nnz, dtype=np.int64)
+        self.block_nnz_offsets = np.ascontiguousarray(block_nnz_offsets, dtype=np.int64)
+        self.local_rows = np.ascontiguousarray(local_rows, dtype=np.uint16)
+        self.local_cols = np.ascontiguousarray(local_cols, dtype=np.uint16)
+        self.values = np.ascontiguousarray(values, dtype=np.float64)
+        self._handle = handle
+
+    @property
+    def nrowblks(self):
+        return len(self.row_offsets) - 1
+
+    @property
+    def ncolblks(self):
+        return len(self.col_offsets) - 1
+
+    @property
+    def nnz(self):
+        return len(self.values)
+
+    def view(self) -> CsbView:
+        return CsbView(self.nrows, self.ncols, self.nrowblks, self.ncolblks, self.nnz, _p(self.row_offsets),
+                       _p(self.col_offsets), _p(self.block_nnz), _p(self.block_nnz_offsets), _p(self.local_rows),
+                       _p(self.local_cols), _p(self.values))
+
+    @classmethod
+    def _from_handle(cls, h):
+        v = CsbView()
+        check(lib().be_csb_view_get(h, C.byref(v)))
+
+        def arr(ptr, n, dt):
+            if n == 0:
+                return np.zeros(0, dtype=dt)
+            buf = (C.c_char * (n * np.dtype(dt).itemsize)).from_address(ptr)
+            return np.frombuffer(buf, dtype=dt, count=n)
+
+        nb = v.nrowblks * v.ncolblks
+        obj = cls(v.nrows, v.ncols, arr(v.row_offsets, v.nrowblks + 1, np.int64),
+                  arr(v.col_offsets, v.ncolblks + 1, np.int64), arr(v.block_nnz, nb, np.int64),
+                  arr(v.block_nnz_offsets, nb, np.int64), arr(v.local_rows, v.nnz, np.uint16),
+                  arr(v.local_cols, v.nnz, np.uint16), arr(v.values, v.nnz, np.float64), handle=h)
+        return obj
+
+    def __del__(self):
+        if self._handle is not None and _lib is not None:
+            _lib.be_csb_free(self._handle)
+            self._handle = None
+
+    def to_triples(self) -> np.ndarray:
+        out = np.zeros(self.nnz, dtype=TRIPLE_DTYPE)
+        v = self.view()
+        check(lib().be_csb_to_triples(C.byref(v), _p(out)))
+        return out
+
+    def is_strictly_lower(self) -> bool:
+        r = C.c_int(0)
+        v = self.view()
+        check(lib().be_csb_is_strictly_lower(C.byref(v), C.byref(r)))
+        return bool(r.value)
+
+    def save(self, path, diag=None):
+        v = self.view()
+        d = None if diag is None else np.ascontiguousarray(diag, dtype=np.float64)
+        check(lib().be_csb_save(str(path).encode(), C.byref(v), _p(d), C.c_int64(0 if d is None else len(d))))
+
+    @classmethod
+    def load(cls, path):
+        h = C.c_void_p()
+        dp = C.POINTER(C.c_double)()
+        nd = C.c_int64(0)
+        check(lib().be_csb_load(str(path).encode(), C.byref(h), C.byref(dp), C.byref(nd)))
+        m = cls._from_handle(h)
+        diag = None
+        if nd.value > 0:
+            diag = np.ctypeslib.as_array(dp, shape=(nd.value,)).copy()
+            lib().be_free_buffer(dp)
+        return m, diag
+
+
+def as_triples(rows, cols, values) -> np.ndarray:
+    t = np.zeros(len(rows), dtype=TRIPLE_DTYPE)
+    t["row"], t["col"], t["value"] = rows, cols, values
+    return t
+
+
+def uniform_boundaries(n: int, extent: int) -> np.ndarray:
+    cnt = C.c_int64(0)
+    check(lib().be_uniform_boundaries(C.c_int64(n), C.c_int64(extent), None, C.byref(cnt)))
+    out = np.zeros(cnt.value, dtype=np.int64)
+    check(lib().be_uniform_boundaries(C.c_int64(n), C.c_int64(extent), _p(out), C.byref(cnt)))
+    return out
+
+
+def build_csb_coo(triples: np.ndarray, nrows: int, ncols: int, row_bounds, col_bounds) -> Csb:
+    """build_csb_coo (csb.hpp:100-161)."""
+    t = np.ascontiguousarray(triples, dtype=TRIPLE_DTYPE)
+    rb = np.ascontiguousarray(row_bounds, dtype=np.int64)
+    cb = np.ascontiguousarray(col_bounds, dtype=np.int64)
+    h = C.c_void_p()
+    check(lib().be_csb_build(_p(t), C.c_int64(len(t)), C.c_int64(nrows), C.c_int64(ncols), _p(rb),
+                             C.c_int64(len(rb)), _p(cb), C.c_int64(len(cb)), C.byref(h)))
+    return Csb._from_handle(h)
+
+
+# --------------------------------------------------------------------- generators
+class Synthetic:
+    """generate_synthetic (synth.hpp:92-158) output."""
+
+    def __init__(self, kind="random", n=1000, density=0.02, bandwidth=8, block_extent=4000, tile_min=4,
+                 tile_max=512, diag_spread=5.0, dominance=1.0, seed=1):
+        p = SynthParams(SYNTH_KINDS[kind], n, density, bandwidth, block_extent, tile_min, tile_max, diag_spread,
+                        dominance, seed)
+        self._h = C.c_void_p()
+        check(lib().be_generate_synthetic(C.byref(p), C.byref(self._h)))
+        low, nlow = C.c_void_p(), C.c_int64()
+        diag, toff, ntoff = C.c_void_p(), C.c_void_p(), C.c_int64()
+        check(lib().be_synth_get(self._h, C.byref(low), C.byref(nlow), C.byref(diag), C.byref(toff), C.byref(ntoff)))
+        self.n = n
+        self.lower = np.frombuffer((C.c_char * (24 * nlow.value)).from_address(low.value), dtype=TRIPLE_DTYPE).copy() \
+            if nlow.value else np.zeros(0, dtype=TRIPLE_DTYPE)
+        self.diag = np.frombuffer((C.c_char * (8 * n)).from_address(diag.value), dtype=np.float64).copy()
+        self.tile_offsets = np.frombuffer((C.c_char * (8 * ntoff.value)).from_address(toff.value),
+                                          dtype=np.int64).copy()
+        lib().be_synth_free(self._h)
+        self._h = None
+
+
+def generate_clustered(n, target_nnz, block_extent=4000, tile=128, fill=0.10, block_occupancy=1.0, tile_min=4,
+                       tile_max=512, diag_spread=5.0, dominance=1.0, seed=1, threads=0):
+    """Clustered CSB generator (tooling for the Test-1..3 shapes)."""
+    p = ClusterParams(n, target_nnz, block_extent, tile, fill, block_occupancy, tile_min, tile_max, diag_spread,
+                      dominance, seed, threads)
+    h = C.c_void_p()
+    dp = C.POINTER(C.c_double)()
+    tp = C.POINTER(C.c_int64)()
+    nt = C.c_int64()
+    check(lib().be_generate_clustered(C.byref(p), C.byref(h), C.byref(dp), C.byref(tp), C.byref(nt)))
+    diag = np.ctypeslib.as_array(dp, shape=(n,)).copy()
+    toff = np.ctypeslib.as_array(tp, shape=(nt.value,)).copy()
+    lib().be_free_buffer(dp)
+    lib().be_free_buffer(tp)
+    return Csb._from_handle(h), diag, toff
+
+
+# ------------------------------------------------------------------------ device
+class Context:
+    def __init__(self, device: int = 0):
+        self._h = C.c_void_p()
+        check(lib().be_ctx_create(C.c_int(device), C.byref(self._h)))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        check(lib().be_ctx_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def synchronize(self):
+        check(lib().be_ctx_synchronize(self._h))
+
+    def launches(self) -> int:
+        n = C.c_int64()
+        check(lib().be_ctx_launches(self._h, C.byref(n)))
+        return n.value
+
+    def close(self):
+        if self._h:
+            check(lib().be_ctx_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Operator:
+    """SymmetricOperator (kernels.hpp:339-378) backed by the device tile format."""
+
+    def __init__(self, ctx: Context, csb: Csb, diag=None, values_prec=BE_F32, symmetric=True):
+        self.ctx = ctx
+        self._csb = csb  # the view's arrays must outlive creation only
+        self._h = C.c_void_p()
+        d = None if diag is None else np.ascontiguousarray(diag, dtype=np.float64)
+        v = csb.view()
+        check(lib().be_op_create(ctx.handle, C.byref(v), _p(d), C.c_int(values_prec),
+                                 C.c_int(BE_OP_SYMMETRIC if symmetric else 0), C.byref(self._h)))
+        self._csb = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self) -> OpInfo:
+        i = OpInfo()
+        check(lib().be_op_get_info(self._h, C.byref(i)))
+        return i
+
+    def apply_host(self, x: np.ndarray, y: np.ndarray | None = None, mode=BE_APPLY_SYMMETRIC) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        info = self.info()
+        out_rows = info.ncols if mode == BE_APPLY_TRANS_ACC else info.nrows
+        if y is None:
+            y = np.zeros((out_rows, x.shape[1]), dtype=np.float64)
+        assert y.flags.c_contiguous and y.dtype == np.float64
+        check(lib().be_op_apply_host(self._h, _p(x), _p(y), C.c_int64(x.shape[0]), C.c_int(x.shape[1]),
+                                     C.c_int(mode)))
+        return y
+
+    def apply_dev(self, x_ptr: int, y_ptr: int, nrows: int, nb: int, panel_prec=BE_F64, mode=BE_APPLY_SYMMETRIC,
+                  stream: int = 0):
+        check(lib().be_op_apply(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), C.c_int64(nrows), C.c_int(nb),
+                                C.c_int(panel_prec), C.c_int(mode), C.c_void_p(stream)))
+
+    def decode(self):
+        n = self.info().nnz
+        rows = np.zeros(n, np.int64)
+        cols = np.zeros(n, np.int64)
+        vals = np.zeros(n, np.float64)
+        idx = np.zeros(n, np.int64)
+        check(lib().be_op_decode(self._h, _p(rows), _p(cols), _p(vals), _p(idx)))
+        return rows, cols, vals, idx
+
+    def timing(self, enable: int = -1):
+        k, a = C.c_double(), C.c_double()
+        check(lib().be_op_timing(self._h, C.c_int(enable), C.byref(k), C.byref(a)))
+        return k.value, a.value
+
+    def close(self):
+        if self._h:
+            check(lib().be_op_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,350 @@
+// C ABI edge of libblockeig_b200.so: every exported function catches the
+// library's Failure (and CUDA/std errors) and turns it into a be_status with a
+// thread-local message, mirroring the exception taxonomy of errors.hpp.
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <cstring>
+#include <string>
+
+#include "device.hpp"
+
+namespace {
+thread_local std::string g_err;
+thread_local int g_pivot = -1;
+
+template <class F>
+be_status guard(F&& f) {
+    try {
+        f();
+        return BE_OK;
+    } catch (const be::Failure& e) {
+        g_err = e.what();
+        g_pivot = e.pivot;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return BE_ERR_OUT_OF_MEMORY;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return BE_ERR_GENERIC;
+    } catch (...) {
+        g_err = "unknown error";
+        return BE_ERR_GENERIC;
+    }
+}
+}  // namespace
+
+struct be_csb {
+    std::unique_ptr<be::CsbHost> impl;
+};
+struct be_synth {
+    std::unique_ptr<be::Synth> impl;
+};
+
+extern "C" {
+
+const char* be_last_error(void) { return g_err.c_str(); }
+int be_last_error_pivot(void) { return g_pivot; }
+const char* be_version(void) { return "blockeig_b200 0.1 (sm_100a)"; }
+void be_free_buffer(void* p) { std::free(p); }
+
+// ---------------------------------------------------------------- host CSB
+be_status be_csb_build(const be_triple* triples, int64_t count, int64_t nrows, int64_t ncols,
+                       const int64_t* row_bounds, int64_t n_row_bounds, const int64_t* col_bounds,
+                       int64_t n_col_bounds, be_csb** out) {
+    return guard([&] {
+        if (!out || (count > 0 && !triples) || !row_bounds || !col_bounds) be::fail(BE_ERR_BAD_PARAMS, "be_csb_build: null argument");
+        auto m = be::build_csb(triples, count, nrows, ncols, row_bounds, n_row_bounds, col_bounds, n_col_bounds);
+        *out = new be_csb{std::move(m)};
+    });
+}
+
+be_status be_uniform_boundaries(int64_t n, int64_t extent, int64_t* out, int64_t* count) {
+    return guard([&] {
+        auto b = be::uniform_boundaries(n, extent);
+        if (count) *count = static_cast<int64_t>(b.size());
+        if (out) std::memcpy(out, b.data(), b.size() * sizeof(int64_t));
+    });
+}
+
+be_status be_csb_view_get(const be_csb* m, be_csb_view* view) {
+    return guard([&] {
+        if (!m || !view) be::fail(BE_ERR_BAD_PARAMS, "be_csb_view_get: null argument");
+        *view = m->impl->view();
+    });
+}
+
+be_status be_csb_is_strictly_lower(const be_csb_view* view, int* result) {
+    return guard([&] {
+        if (!view || !result) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        be::validate_view(*view);
+        *result = be::is_strictly_lower(*view) ? 1 : 0;
+    });
+}
+
+be_status be_csb_to_triples(const be_csb_view* view, be_triple* out) {
+    return guard([&] {
+        if (!view || (view->nnz > 0 && !out)) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        be::validate_view(*view);
+        be::to_triples(*view, out);
+    });
+}
+
+be_status be_csb_save(const char* path, const be_csb_view* view, const double* diag, int64_t ndiag) {
+    return guard([&] {
+        if (!path || !view) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        be::validate_view(*view);
+        be::save_csb1(path, *view, diag, ndiag);
+    });
+}
+
+be_status be_csb_load(const char* path, be_csb** out, double** diag, int64_t* ndiag) {
+    return guard([&] {
+        if (!path || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        std::vector<double> d;
+        auto m = be::load_csb1(path, diag ? &d : nullptr);
+        if (diag) {
+            *diag = nullptr;
+            if (!d.empty()) {
+                *diag = static_cast<double*>(std::malloc(d.size() * sizeof(double)));
+                std::memcpy(*diag, d.data(), d.size() * sizeof(double));
+            }
+            if (ndiag) *ndiag = static_cast<int64_t>(d.size());
+        }
+        *out = new be_csb{std::move(m)};
+    });
+}
+
+void be_csb_free(be_csb* m) { delete m; }
+
+// --------------------------------------------------------------- generators
+be_status be_generate_synthetic(const be_synth_params* p, be_synth** out) {
+    return guard([&] {
+        if (!p || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        *out = new be_synth{be::generate_synthetic(*p)};
+    });
+}
+
+be_status be_synth_get(const be_synth* s, const be_triple** lower, int64_t* nlower, const double** diag,
+                       const int64_t** tile_offsets, int64_t* n_tile_offsets) {
+    return guard([&] {
+        if (!s) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        if (lower) *lower = s->impl->lower.data();
+        if (nlower) *nlower = static_cast<int64_t>(s->impl->lower.size());
+        if (diag) *diag = s->impl->diag.data();
+        if (tile_offsets) *tile_offsets = s->impl->tile_offsets.data();
+        if (n_tile_offsets) *n_tile_offsets = static_cast<int64_t>(s->impl->tile_offsets.size());
+    });
+}
+
+void be_synth_free(be_synth* s) { delete s; }
+
+be_status be_generate_clustered(const be_cluster_params* p, be_csb** out, double** diag, int64_t** tile_offsets,
+                                int64_t* n_tile_offsets) {
+    return guard([&] {
+        if (!p || !out || !diag || !tile_offsets || !n_tile_offsets) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        std::vector<double> d;
+        std::vector<int64_t> t;
+        auto m = be::generate_clustered(*p, d, t);
+        *diag = static_cast<double*>(std::malloc(d.size() * sizeof(double)));
+        std::memcpy(*diag, d.data(), d.size() * sizeof(double));
+        *tile_offsets = static_cast<int64_t*>(std::malloc(t.size() * sizeof(int64_t)));
+        std::memcpy(*tile_offsets, t.data(), t.size() * sizeof(int64_t));
+        *n_tile_offsets = static_cast<int64_t>(t.size());
+        *out = new be_csb{std::move(m)};
+    });
+}
+
+// ------------------------------------------------------------------ context
+be_status be_ctx_create(int device, be_ctx** out) {
+    return guard([&] {
+        if (!out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+            cudaGetLastError();
+            be::fail(BE_ERR_NO_DEVICE, "no CUDA device available");
+        }
+        if (device < 0 || device >= ndev) be::fail(BE_ERR_NO_DEVICE, "device index out of range");
+        auto c = std::make_unique<be::Ctx>();
+        c->device = device;
+        BE_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop{};
+        BE_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10) be::fail(BE_ERR_NO_DEVICE, "blockeig_b200 needs an sm_100 (B200) device");
+        c->num_sms = prop.multiProcessorCount;
+        BE_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        *out = new be_ctx{std::move(c)};
+    });
+}
+
+be_status be_ctx_destroy(be_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        if (ctx->impl->solver) cusolverDnDestroy(ctx->impl->solver);
+        if (ctx->impl->stream) cudaStreamDestroy(ctx->impl->stream);
+        delete ctx;
+    });
+}
+
+be_status be_ctx_stream(be_ctx* ctx, void** stream) {
+    return guard([&] {
+        if (!ctx || !stream) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        *stream = ctx->impl->stream;
+    });
+}
+
+be_status be_ctx_synchronize(be_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        BE_CUDA(cudaSetDevice(ctx->impl->device));
+        BE_CUDA(cudaStreamSynchronize(ctx->impl->stream));
+    });
+}
+
+be_status be_ctx_launches(be_ctx* ctx, int64_t* launches) {
+    return guard([&] {
+        if (!ctx || !launches) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        *launches = ctx->impl->launches;
+    });
+}
+
+// ------------------------------------------------------------------ operator
+be_status be_op_create(be_ctx* ctx, const be_csb_view* L, const double* diag, int values_prec, int flags, be_op** out) {
+    return guard([&] {
+        if (!ctx || !L || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        BE_CUDA(cudaSetDevice(ctx->impl->device));
+        *out = new be_op{be::op_create(ctx->impl.get(), *L, diag, values_prec, flags)};
+    });
+}
+
+be_status be_op_destroy(be_op* op) {
+    return guard([&] { delete op; });
+}
+
+be_status be_op_apply(be_op* op, const void* X_dev, void* Y_dev, int64_t nrows, int nb, int panel_prec, int mode,
+                      void* stream) {
+    return guard([&] {
+        if (!op || !X_dev || !Y_dev) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        auto* o = op->impl.get();
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : o->ctx->stream;
+        be::op_apply(o, X_dev, Y_dev, nrows, nb, panel_prec, mode, s);
+    });
+}
+
+be_status be_op_apply_host(be_op* op, const double* X, double* Y, int64_t nrows, int nb, int mode) {
+    return guard([&] {
+        if (!op || !X || !Y) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        auto* o = op->impl.get();
+        if (X == Y) be::fail(BE_ERR_BAD_PARAMS, "spmm: W and U must not alias");
+        if (mode == BE_APPLY_SYMMETRIC && !o->symmetric) be::fail(BE_ERR_BAD_PARAMS, "apply: symmetric mode needs a symmetric operator");
+        if (mode < 0 || mode > 2) be::fail(BE_ERR_BAD_PARAMS, "apply: unknown mode");
+        const int64_t out_rows = mode == BE_APPLY_TRANS_ACC ? o->ncols : o->nrows;
+        const int64_t in_rows = mode == BE_APPLY_NOTRANS_ACC ? o->ncols : o->nrows;
+        if (nrows != in_rows) be::fail(BE_ERR_DIMENSION_MISMATCH, "apply: shape mismatch");
+        if (nb < 1) be::fail(BE_ERR_DIMENSION_MISMATCH, "apply: nb must be positive");
+        cudaStream_t s = o->ctx->stream;
+        be::DBuf<double> dx(std::max<int64_t>(in_rows * nb, 1)), dy(std::max<int64_t>(out_rows * nb, 1));
+        BE_CUDA(cudaMemcpyAsync(dx.get(), X, static_cast<std::size_t>(in_rows * nb) * 8, cudaMemcpyHostToDevice, s));
+        if (mode != BE_APPLY_SYMMETRIC)
+            BE_CUDA(cudaMemcpyAsync(dy.get(), Y, static_cast<std::size_t>(out_rows * nb) * 8, cudaMemcpyHostToDevice, s));
+        be::op_apply(o, dx.get(), dy.get(), nrows, nb, BE_F64, mode, s);
+        BE_CUDA(cudaMemcpyAsync(Y, dy.get(), static_cast<std::size_t>(out_rows * nb) * 8, cudaMemcpyDeviceToHost, s));
+        BE_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+be_status be_op_get_info(const be_op* op, be_op_info* info) {
+    return guard([&] {
+        if (!op || !info) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        const auto* o = op->impl.get();
+        std::memset(info, 0, sizeof(*info));
+        info->nrows = o->nrows;
+        info->ncols = o->ncols;
+        info->nnz = o->nnz;
+        info->ntiles = o->ntiles;
+        info->device_bytes = static_cast<int64_t>(o->tiles.bytes() + o->lens.bytes() + o->runs.bytes() + o->vals.bytes() + o->rc.bytes() + o->cperm.bytes());
+        info->bytes_per_nnz_x1000 = o->nnz ? info->device_bytes * 1000 / o->nnz : 0;
+        info->values_prec = o->values_prec;
+        info->tile_rows = be::kTile;
+        info->tile_cols = be::kTile;
+        info->tile_max_nnz = o->max_nnz;
+    });
+}
+
+be_status be_op_decode(be_op* op, int64_t* rows, int64_t* cols, double* values, int64_t* csb_index) {
+    return guard([&] {
+        if (!op) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        auto* o = op->impl.get();
+        if (o->csb_index.size() != static_cast<std::size_t>(o->padded))
+            be::fail(BE_ERR_BAD_PARAMS, "be_op_decode: source index not retained for matrices this large");
+        std::vector<be::TileHdr> h(static_cast<std::size_t>(o->ntiles));
+        std::vector<std::uint16_t> rc(static_cast<std::size_t>(o->padded)), cp(static_cast<std::size_t>(o->padded));
+        const std::size_t vsz = o->values_prec == BE_F32 ? 4 : 8;
+        std::vector<unsigned char> v(static_cast<std::size_t>(o->padded) * vsz);
+        if (o->ntiles > 0) {
+            BE_CUDA(cudaMemcpy(h.data(), o->tiles.get(), h.size() * sizeof(be::TileHdr), cudaMemcpyDeviceToHost));
+            BE_CUDA(cudaMemcpy(rc.data(), o->rc.get(), rc.size() * 2, cudaMemcpyDeviceToHost));
+            BE_CUDA(cudaMemcpy(cp.data(), o->cperm.get(), cp.size() * 2, cudaMemcpyDeviceToHost));
+            BE_CUDA(cudaMemcpy(v.data(), o->vals.get(), v.size(), cudaMemcpyDeviceToHost));
+        }
+        int64_t p = 0;
+        for (const auto& t : h) {
+            const int64_t b = static_cast<int64_t>(t.begin8) * 8;
+            const int nnz = static_cast<int>(t.packed >> 14);
+            const int nr = static_cast<int>(t.packed & 127u) + 1;
+            const int nc = static_cast<int>((t.packed >> 7) & 127u) + 1;
+            // rows and (through cperm) columns must each form one contiguous
+            // group; cperm must be a permutation of the tile's entries
+            std::vector<char> seen(static_cast<std::size_t>(nnz), 0), rdone(256, 0), cdone(256, 0);
+            int prev_r = -1, prev_c = -1;
+            for (int k = 0; k < nnz; ++k) {
+                const int q = cp[static_cast<std::size_t>(b + k)];
+                if (q >= nnz || seen[static_cast<std::size_t>(q)]) be::fail(BE_ERR_GENERIC, "decode: bad column permutation");
+                seen[static_cast<std::size_t>(q)] = 1;
+                const int c = rc[static_cast<std::size_t>(b + q)] & 255;
+                const int r = rc[static_cast<std::size_t>(b + k)] >> 8;
+                if (c != prev_c) {
+                    if (cdone[static_cast<std::size_t>(c)]) be::fail(BE_ERR_GENERIC, "decode: column order split");
+                    cdone[static_cast<std::size_t>(c)] = 1;
+                    prev_c = c;
+                }
+                if (r != prev_r) {
+                    if (rdone[static_cast<std::size_t>(r)]) be::fail(BE_ERR_GENERIC, "decode: row order split");
+                    rdone[static_cast<std::size_t>(r)] = 1;
+                    prev_r = r;
+                }
+            }
+            for (int k = 0; k < nnz; ++k) {
+                const std::uint16_t x = rc[static_cast<std::size_t>(b + k)];
+                if ((x >> 8) >= nr || (x & 255) >= nc) be::fail(BE_ERR_GENERIC, "decode: local index outside tile");
+                if (rows) rows[p] = t.row0 + (x >> 8);
+                if (cols) cols[p] = t.col0 + (x & 255);
+                if (values) {
+                    if (vsz == 4) {
+                        float f;
+                        std::memcpy(&f, v.data() + static_cast<std::size_t>(b + k) * 4, 4);
+                        values[p] = f;
+                    } else {
+                        std::memcpy(values + p, v.data() + static_cast<std::size_t>(b + k) * 8, 8);
+                    }
+                }
+                if (csb_index) csb_index[p] = o->csb_index[static_cast<std::size_t>(b + k)];
+                ++p;
+            }
+        }
+        if (p != o->nnz) be::fail(BE_ERR_GENERIC, "decode: entry count mismatch");
+    });
+}
+
+be_status be_op_timing(be_op* op, int enable, double* last_kernel_ms, double* last_apply_ms) {
+    return guard([&] {
+        if (!op) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        auto* o = op->impl.get();
+        if (enable >= 0) o->timing = enable != 0;
+        if (last_kernel_ms) *last_kernel_ms = o->last_kernel_ms;
+        if (last_apply_ms) *last_apply_ms = o->last_apply_ms;
+    });
+}
+
+}  // extern "C"

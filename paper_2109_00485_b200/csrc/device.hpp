@@ -1,0 +1,99 @@
+// Device-side objects behind the opaque C handles: context, operator (tile
+// format of the half-stored matrix), preconditioner tiles.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "host_csb.hpp"
+
+struct cusolverDnContext;
+
+namespace be {
+
+// RAII device buffer
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    index_t n = 0;
+    DBuf() = default;
+    explicit DBuf(index_t count) { reset(count); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void reset(index_t count) {
+        release();
+        n = count;
+        if (count > 0) BE_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), static_cast<std::size_t>(count) * sizeof(T)));
+    }
+    T* get() const { return p; }
+    std::size_t bytes() const { return static_cast<std::size_t>(n) * sizeof(T); }
+};
+
+struct Ctx {
+    int device = 0;
+    int num_sms = 0;
+    cudaStream_t stream = nullptr;
+    cusolverDnContext* solver = nullptr;
+    long long launches = 0;  // kernels launched through this context
+    ~Ctx();
+};
+
+// One device work tile: <= kTile rows x <= kTile cols of the lower triangle,
+// <= max_nnz entries, entries row-sorted. 16 bytes.
+struct TileHdr {
+    std::uint32_t begin8;  // entry offset / 8 (segments are 8-aligned)
+    std::int32_t row0;     // first global row of the 128-row tile-row
+    std::int32_t col0;     // first global column
+    std::uint32_t packed;  // (nr-1) | (nc-1) << 7 | nnz << 14; nr = rows of the tile-row
+};
+
+inline constexpr int kTile = 128;
+
+struct Op {
+    Ctx* ctx = nullptr;
+    index_t nrows = 0, ncols = 0, nnz = 0, ntiles = 0, padded = 0;
+    bool symmetric = false;
+    int values_prec = BE_F32;
+    int max_nnz = 2048;
+    DBuf<TileHdr> tiles;
+    DBuf<int2> runs;                 // [tile_begin, tile_end) work items
+    index_t nruns = 0;
+    DBuf<unsigned char> lens;        // 256 per tile: row / column lengths in rank order
+    DBuf<unsigned char> vals;        // float or double, rank-ordered rows within tile
+    DBuf<std::uint16_t> rc;          // (local row << 8) | local col
+    DBuf<std::uint16_t> cperm;       // column-order -> row-order position in tile
+    DBuf<double> diag;               // nrows (symmetric only)
+    DBuf<int> counter;               // persistent-kernel tile counter [2]
+    std::vector<std::int64_t> csb_index;  // device order -> CSB index (small matrices only)
+    int grid = 0;
+    // timing
+    bool timing = false;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    double last_kernel_ms = 0, last_apply_ms = 0;
+    ~Op();
+};
+
+std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag, int values_prec, int flags);
+void op_apply(Op* op, const void* X, void* Y, index_t nrows, int nb, int panel_prec, int mode, cudaStream_t s);
+
+}  // namespace be
+
+struct be_ctx {
+    std::unique_ptr<be::Ctx> impl;
+};
+struct be_op {
+    std::unique_ptr<be::Op> impl;
+};

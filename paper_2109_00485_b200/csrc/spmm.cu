@@ -1,0 +1,720 @@
+// Symmetric SpMM over the half-stored CSB_Coo Hamiltonian, sm_100a.
+//
+// Replaces SymmetricOperator::apply (kernels.hpp:357-371) = out.set_zero +
+// spmm_notrans (kernels.hpp:290) + spmm_trans (kernels.hpp:302) + the
+// diagonal pass (kernels.hpp:363-370). The reference reads every stored
+// nonzero twice (once per pass); this kernel reads it once from HBM and
+// applies it twice (A_ij X_j -> Y_i and A_ij X_i -> Y_j).
+//
+// Device format ("work tiles", built on upload from the CSB arrays):
+//   every CSB block is cut into 128 x 128 sub-tiles aligned to the block
+//   origin (a sub-tile with more than max_nnz entries is split by rows);
+//   tiles are ordered by global tile-row. Per entry the HBM stream holds the
+//   value (f32 or f64) + rc (u16: local row << 8 | local col) + cperm (u16:
+//   column-order permutation): 4 + 2 + 2 = 8 bytes per stored nonzero in f32,
+//   the reference's own "f32 value + 2 x u16" budget. Inside
+//   a tile the rows are ordered by decreasing length (rank order) and so are
+//   the columns of the column order; 256 bytes of per-tile row/column lengths
+//   (u8, rank order) complete the format.
+//
+// Kernel: persistent CTAs of 256 threads pull work items ("runs": up to 32
+//   consecutive tiles of one tile-row) from an atomic counter. Per run the
+//   CTA stages X_I once (f32, in smem) and accumulates Y_I in smem; per tile
+//   it stages X_J and the entry stream (coalesced loads, one round trip).
+//   Warps 0-3 then run pass R (Y_I += A X_J: one lane per row rank, all nb
+//   columns in registers) while warps 4-7 run pass C (Y_J += A^T X_I: one
+//   lane per column rank, flushed with REDG.E.ADD.F32x4). Rank order keeps
+//   the 32 lanes of a warp on rows of similar length (little divergence). X
+//   rows live in 128-byte smem lines holding 128 / (nb * 4) replicas; lane L
+//   reads its 16-byte chunks in the rotated order (i + L) % CH from replica
+//   (L / CH) % REP, so the 8 lanes of every quarter-warp phase hit 8 distinct
+//   bank groups whatever rows they gather.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "device.hpp"
+
+namespace be {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr index_t kRunMax = 32;  // tiles per work item
+
+template <typename TC>
+struct Meta;
+template <>
+struct __align__(8) Meta<float> {
+    float v;
+    std::uint32_t off;  // low 16: byte offset of the X_J line, high 16: of the X_I line
+};
+template <>
+struct __align__(16) Meta<double> {
+    double v;
+    std::uint32_t off;
+    std::uint32_t pad;
+};
+
+template <typename TC>
+struct Vec;
+template <>
+struct Vec<float> {
+    using T = float4;
+    static constexpr int N = 4;
+};
+template <>
+struct Vec<double> {
+    using T = double2;
+    static constexpr int N = 2;
+};
+
+__device__ __forceinline__ void vfma(float4& a, float s, const float4& x) {
+    a.x = fmaf(s, x.x, a.x);
+    a.y = fmaf(s, x.y, a.y);
+    a.z = fmaf(s, x.z, a.z);
+    a.w = fmaf(s, x.w, a.w);
+}
+__device__ __forceinline__ void vfma(double2& a, double s, const double2& x) {
+    a.x = fma(s, x.x, a.x);
+    a.y = fma(s, x.y, a.y);
+}
+__device__ __forceinline__ void vzero(float4& a) { a = make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ void vzero(double2& a) { a = make_double2(0.0, 0.0); }
+__device__ __forceinline__ void vadd(float4& a, const float4& b) {
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+}
+__device__ __forceinline__ void vadd(double2& a, const double2& b) {
+    a.x += b.x;
+    a.y += b.y;
+}
+__device__ __forceinline__ bool vnonzero(const float4& a) { return a.x != 0.f || a.y != 0.f || a.z != 0.f || a.w != 0.f; }
+__device__ __forceinline__ bool vnonzero(const double2& a) { return a.x != 0.0 || a.y != 0.0; }
+
+// Fire-and-forget global reductions (REDG, no return value).
+__device__ __forceinline__ void red_add(float* p, float v) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void red_add(double* p, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void red_add4(float* p, const float4& v) {  // REDG.E.ADD.F32x4
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+
+// Flush one 16-byte chunk (columns c0 .. c0+VEC-1 of a row) into Y.
+template <typename TX>
+__device__ __forceinline__ void flush(TX* y, const float4& a, int lim, bool vec_ok) {
+    if constexpr (sizeof(TX) == 4) {
+        if (lim >= 4 && vec_ok) {
+            red_add4(y, a);
+        } else {
+            if (lim > 0) red_add(y + 0, a.x);
+            if (lim > 1) red_add(y + 1, a.y);
+            if (lim > 2) red_add(y + 2, a.z);
+            if (lim > 3) red_add(y + 3, a.w);
+        }
+    } else {
+        if (lim > 0) red_add(y + 0, static_cast<double>(a.x));
+        if (lim > 1) red_add(y + 1, static_cast<double>(a.y));
+        if (lim > 2) red_add(y + 2, static_cast<double>(a.z));
+        if (lim > 3) red_add(y + 3, static_cast<double>(a.w));
+    }
+}
+template <typename TX>
+__device__ __forceinline__ void flush(TX* y, const double2& a, int lim, bool) {
+    if (lim > 0) red_add(y + 0, static_cast<TX>(a.x));
+    if (lim > 1) red_add(y + 1, static_cast<TX>(a.y));
+}
+
+// smem x-panel geometry for NBP padded columns of TC
+template <int NBP, typename TC>
+struct XGeom {
+    static constexpr int VEC = Vec<TC>::N;                          // elements per 16-byte chunk
+    static constexpr int CH = NBP / VEC;                            // chunks per row
+    static constexpr int RB = NBP * static_cast<int>(sizeof(TC));  // row bytes
+    static constexpr int LINEB = RB < 128 ? 128 : RB;               // bytes per smem row line
+    static constexpr int REP = LINEB / RB;                          // replicas per line
+    static_assert(NBP % VEC == 0 && CH >= 1, "bad NBP");
+};
+
+// Stage rows [row0, row0 + nr) of X (TX, row-major, nb columns) into the
+// replicated smem lines; all loads of a batch are in flight together.
+template <int NBP, typename TC, typename TX>
+__device__ __forceinline__ void stage_x(unsigned char* xs, const TX* __restrict__ X, int row0, int nr, int nb) {
+    using G = XGeom<NBP, TC>;
+    const TX* src = X + static_cast<std::int64_t>(row0) * nb;
+    constexpr int EPC = 16 / sizeof(TX);  // TX elements per 16-byte chunk
+    if constexpr ((NBP * sizeof(TX)) % 16 == 0) {
+        if (nb == NBP) {
+            constexpr int CPR = NBP / EPC;  // global chunks per row
+            const int total = nr * CPR;
+            constexpr int PER = 4;
+            for (int c0 = threadIdx.x; c0 < total; c0 += PER * kThreads) {
+                uint4 buf[PER];
+#pragma unroll
+                for (int i = 0; i < PER; ++i) {
+                    const int c = c0 + i * kThreads;
+                    if (c < total) buf[i] = __ldg(reinterpret_cast<const uint4*>(src) + c);
+                }
+#pragma unroll
+                for (int i = 0; i < PER; ++i) {
+                    const int c = c0 + i * kThreads;
+                    if (c < total) {
+                        const int r = c / CPR, v0 = (c % CPR) * EPC;
+                        const TX* e = reinterpret_cast<const TX*>(&buf[i]);
+                        TC* line = reinterpret_cast<TC*>(xs + r * G::LINEB);
+#pragma unroll
+                        for (int q = 0; q < G::REP; ++q)
+#pragma unroll
+                            for (int j = 0; j < EPC; ++j) line[q * NBP + v0 + j] = static_cast<TC>(e[j]);
+                    }
+                }
+            }
+            return;
+        }
+    }
+    const int total = nr * NBP;
+    for (int e = threadIdx.x; e < total; e += kThreads) {
+        const int r = e / NBP, v = e - r * NBP;
+        const TC x = v < nb ? static_cast<TC>(__ldg(src + static_cast<std::int64_t>(r) * nb + v)) : TC(0);
+        TC* line = reinterpret_cast<TC*>(xs + r * G::LINEB);
+#pragma unroll
+        for (int q = 0; q < G::REP; ++q) line[q * NBP + v] = x;
+    }
+}
+
+template <int NBP, typename TC>
+__device__ __forceinline__ std::uint32_t pack_off(std::uint32_t rc) {
+    using G = XGeom<NBP, TC>;
+    return ((rc & 255u) * G::LINEB) | (((rc >> 8) * G::LINEB) << 16);
+}
+
+constexpr int kEPT = 8;  // entries per thread per staging round (max_nnz <= 2048)
+
+// Gather-accumulate one segment of entries into the CH register chunks.
+// Lane L keeps accumulator chunk i for output chunk (i + L) % CH.
+template <int NBP, typename TC, bool HI>
+__device__ __forceinline__ void segment(const Meta<TC>* __restrict__ m, int k, int k1, const unsigned char* xbase,
+                                        typename Vec<TC>::T (&acc)[XGeom<NBP, TC>::CH], int lane) {
+    using G = XGeom<NBP, TC>;
+    using V = typename Vec<TC>::T;
+    const unsigned char* xb = xbase + ((lane / G::CH) % G::REP) * G::RB;
+    int coff[G::CH];
+#pragma unroll
+    for (int i = 0; i < G::CH; ++i) coff[i] = ((i + lane) % G::CH) * 16;
+    constexpr bool kPair = G::CH <= 4;  // two entries in flight unless the row is wide
+    for (; kPair && k + 1 < k1; k += 2) {
+        const Meta<TC> m0 = m[k], m1 = m[k + 1];
+        const unsigned char* p0 = xb + (HI ? (m0.off >> 16) : (m0.off & 0xFFFFu));
+        const unsigned char* p1 = xb + (HI ? (m1.off >> 16) : (m1.off & 0xFFFFu));
+        V x0[G::CH], x1[G::CH];
+#pragma unroll
+        for (int i = 0; i < G::CH; ++i) x0[i] = *reinterpret_cast<const V*>(p0 + coff[i]);
+#pragma unroll
+        for (int i = 0; i < G::CH; ++i) x1[i] = *reinterpret_cast<const V*>(p1 + coff[i]);
+#pragma unroll
+        for (int i = 0; i < G::CH; ++i) vfma(acc[i], m0.v, x0[i]);
+#pragma unroll
+        for (int i = 0; i < G::CH; ++i) vfma(acc[i], m1.v, x1[i]);
+    }
+    for (; k < k1; ++k) {
+        const Meta<TC> m0 = m[k];
+        const unsigned char* p0 = xb + (HI ? (m0.off >> 16) : (m0.off & 0xFFFFu));
+#pragma unroll
+        for (int i = 0; i < G::CH; ++i) vfma(acc[i], m0.v, *reinterpret_cast<const V*>(p0 + coff[i]));
+    }
+}
+
+template <int NBP, typename TC, typename TV, typename TX>
+__global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? 3 : 2)
+    k_sym_spmm(const int2* __restrict__ runs, int nruns, const TileHdr* __restrict__ tiles,
+               const unsigned char* __restrict__ lens, const TV* __restrict__ vals,
+               const std::uint16_t* __restrict__ rc, const std::uint16_t* __restrict__ cperm,
+               const TX* __restrict__ X, TX* __restrict__ Y, int nb, int do_r, int do_c, int max_nnz,
+               int* __restrict__ ctr) {
+    using G = XGeom<NBP, TC>;
+    using V = typename Vec<TC>::T;
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned char* xi = smem;
+    unsigned char* xj = xi + kTile * G::LINEB;
+    V* yi = reinterpret_cast<V*>(xj + kTile * G::LINEB);  // kTile x CH chunks: the run's Y_I rows
+    Meta<TC>* meta = reinterpret_cast<Meta<TC>*>(yi + kTile * G::CH);
+    Meta<TC>* cmeta = meta + max_nnz;
+    __shared__ int s_run;
+    __shared__ int s_tot[8];
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int grp = tid >> 7;  // 0: pass R (row ranks), 1: pass C (column ranks)
+    const bool vec_ok = (nb % G::VEC) == 0;
+
+    if (tid == 0) s_run = atomicAdd(ctr, 1);
+    __syncthreads();
+    int run = s_run;
+    while (run < nruns) {
+        const int2 rg = runs[run];
+        TileHdr h = tiles[rg.x];
+        const int row0 = h.row0;
+        const int nr = static_cast<int>(h.packed & 127u) + 1;
+        if (do_c) stage_x<NBP, TC, TX>(xi, X, row0, nr, nb);
+        if (do_r)
+            for (int e = tid; e < kTile * G::CH; e += kThreads) vzero(yi[e]);
+        for (int t = rg.x; t < rg.y; ++t) {
+            const std::int64_t b = static_cast<std::int64_t>(h.begin8) * 8;
+            const int nc = static_cast<int>((h.packed >> 7) & 127u) + 1;
+            const int nnz = static_cast<int>(h.packed >> 14);
+            const int col0 = h.col0;
+            // lengths (rank order) -> exclusive starts via warp scans
+            const int len = __ldg(lens + static_cast<std::int64_t>(t) * 256 + tid);
+            int incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) s_tot[warp] = incl;
+            // entry stream: coalesced, k = tid + j * kThreads
+            TV v[kEPT];
+            std::uint16_t r[kEPT], cp[kEPT];
+#pragma unroll
+            for (int j = 0; j < kEPT; ++j) {
+                const int k = tid + j * kThreads;
+                if (k < nnz) {
+                    v[j] = __ldg(vals + b + k);
+                    r[j] = __ldg(rc + b + k);
+                    if (do_c) cp[j] = __ldg(cperm + b + k);
+                }
+            }
+            if (do_r) stage_x<NBP, TC, TX>(xj, X, col0, nc, nb);
+#pragma unroll
+            for (int j = 0; j < kEPT; ++j) {
+                const int k = tid + j * kThreads;
+                if (k < nnz) {
+                    Meta<TC> m;
+                    m.v = static_cast<TC>(v[j]);
+                    m.off = pack_off<NBP, TC>(r[j]);
+                    meta[k] = m;
+                }
+            }
+            if (t + 1 < rg.y) h = tiles[t + 1];  // prefetch the next header
+            if (t == rg.y - 1 && tid == 0) s_run = atomicAdd(ctr, 1);  // and the next run
+            __syncthreads();
+            int start = incl - len;
+            for (int w = grp * 4; w < warp; ++w) start += s_tot[w];
+            if (do_c) {  // column order for pass C
+#pragma unroll
+                for (int j = 0; j < kEPT; ++j) {
+                    const int k = tid + j * kThreads;
+                    if (k < nnz) cmeta[k] = meta[cp[j]];
+                }
+                __syncthreads();
+            }
+            if (len > 0 && (grp == 0 ? do_r : do_c)) {
+                V acc[G::CH];
+#pragma unroll
+                for (int i = 0; i < G::CH; ++i) vzero(acc[i]);
+                if (grp == 0) {  // Y_I += A X_J for the row of this rank
+                    segment<NBP, TC, false>(meta, start, start + len, xj, acc, lane);
+                    const int row = static_cast<int>((meta[start].off >> 16) / G::LINEB);
+                    V* y = yi + row * G::CH;
+#pragma unroll
+                    for (int i = 0; i < G::CH; ++i) vadd(y[(i + lane) % G::CH], acc[i]);
+                } else {  // Y_J += A^T X_I for the column of this rank
+                    segment<NBP, TC, true>(cmeta, start, start + len, xi, acc, lane);
+                    const int col = static_cast<int>((cmeta[start].off & 0xFFFFu) / G::LINEB);
+                    TX* y = Y + static_cast<std::int64_t>(col0 + col) * nb;
+#pragma unroll
+                    for (int i = 0; i < G::CH; ++i) {
+                        const int c0 = ((i + lane) % G::CH) * G::VEC;
+                        if (c0 < nb) flush<TX>(y + c0, acc[i], nb - c0, vec_ok);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (do_r) {  // flush the run's rows (all-zero chunks carry no update)
+            for (int e = tid; e < nr * G::CH; e += kThreads) {
+                const int row = e / G::CH, c0 = (e % G::CH) * G::VEC;
+                if (c0 < nb && vnonzero(yi[e]))
+                    flush<TX>(Y + static_cast<std::int64_t>(row0 + row) * nb + c0, yi[e], nb - c0, vec_ok);
+            }
+        }
+        run = s_run;
+        __syncthreads();  // yi / xi / s_run are reused by the next run
+    }
+    // last CTA out resets the counter for the next launch
+    if (tid == 0) {
+        __threadfence();
+        const int done = atomicAdd(ctr + 1, 1);
+        if (done == static_cast<int>(gridDim.x) - 1) {
+            ctr[0] = 0;
+            ctr[1] = 0;
+        }
+    }
+}
+
+// Y = diag(D) X  (the diagonal pass of kernels.hpp:363-370, run first so the
+// tile kernel can accumulate straight into Y)
+template <typename TX>
+__global__ void k_diag_init(const double* __restrict__ d, const TX* __restrict__ X, TX* __restrict__ Y,
+                            std::int64_t nrows, int nb) {
+    const std::int64_t total = nrows * nb;
+    for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::int64_t r = e / nb;
+        Y[e] = static_cast<TX>(d[r] * static_cast<double>(X[e]));
+    }
+}
+
+template <int NBP, typename TC>
+std::size_t smem_bytes(int max_nnz) {
+    using G = XGeom<NBP, TC>;
+    return 2 * kTile * G::LINEB + kTile * G::CH * 16 + 2 * static_cast<std::size_t>(max_nnz) * sizeof(Meta<TC>);
+}
+
+template <int NBP, typename TC, typename TV, typename TX>
+void launch_tiles(Op* op, const TX* X, TX* Y, int nb, int do_r, int do_c, cudaStream_t s) {
+    auto kern = k_sym_spmm<NBP, TC, TV, TX>;
+    const std::size_t sm = smem_bytes<NBP, TC>(op->max_nnz);
+    static std::size_t cached_sm = 0;
+    static int per_sm = 0;
+    if (cached_sm != sm) {
+        BE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+        BE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, sm));
+        cached_sm = sm;
+    }
+    if (per_sm < 1) fail(BE_ERR_CUDA, "sym_spmm: kernel does not fit on an SM");
+    const int grid = static_cast<int>(std::min<index_t>(static_cast<index_t>(per_sm) * op->ctx->num_sms, op->nruns));
+    op->grid = grid;
+    if (grid == 0) return;
+    kern<<<grid, kThreads, sm, s>>>(op->runs.get(), static_cast<int>(op->nruns), op->tiles.get(), op->lens.get(),
+                                    reinterpret_cast<const TV*>(op->vals.get()), op->rc.get(), op->cperm.get(), X, Y,
+                                    nb, do_r, do_c, op->max_nnz, op->counter.get());
+    BE_CUDA(cudaGetLastError());
+    ++op->ctx->launches;
+}
+
+template <typename TC, typename TV, typename TX>
+void dispatch_nb(Op* op, const TX* X, TX* Y, int nb, int do_r, int do_c, cudaStream_t s) {
+    constexpr int VEC = Vec<TC>::N;
+    if (nb <= VEC) return launch_tiles<VEC, TC, TV, TX>(op, X, Y, nb, do_r, do_c, s);
+    if (nb <= 8) return launch_tiles<8, TC, TV, TX>(op, X, Y, nb, do_r, do_c, s);
+    if (nb <= 16) return launch_tiles<16, TC, TV, TX>(op, X, Y, nb, do_r, do_c, s);
+    if (nb <= 32) return launch_tiles<32, TC, TV, TX>(op, X, Y, nb, do_r, do_c, s);
+    if (nb <= 64) return launch_tiles<64, TC, TV, TX>(op, X, Y, nb, do_r, do_c, s);
+    fail(BE_ERR_BAD_PARAMS, "sym_spmm: nb > 64 is not supported by the device kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Tile-format build (host, parallel over CSB block rows).
+// ---------------------------------------------------------------------------
+
+struct RowOut {
+    std::vector<TileHdr> hdr;         // begin8 relative to this block row
+    std::vector<unsigned char> lens;  // 256 per tile: row then column lengths, rank order
+    std::vector<double> v;            // values in device order (converted on upload)
+    std::vector<std::uint16_t> rc, cp;
+    std::vector<std::int64_t> src;    // CSB index per device entry (optional)
+};
+
+// Emit one tile piece from `ent` = (local row << 56 | local col << 48 | CSB
+// index), sorted by (row, col, index).
+void emit_piece(const be_csb_view& L, const std::vector<std::uint64_t>& ent, index_t row0, index_t col0, index_t nr,
+                index_t nc, bool keep_src, index_t& pos, RowOut& out) {
+    const std::size_t n = ent.size();
+    int rlen[kTile] = {0}, clen[kTile] = {0};
+    for (std::uint64_t e : ent) {
+        ++rlen[e >> 56];
+        ++clen[(e >> 48) & 255u];
+    }
+    // rank order: decreasing length, ties by index
+    int rorder[kTile], corder[kTile], rrank[kTile], crank[kTile];
+    std::iota(rorder, rorder + kTile, 0);
+    std::iota(corder, corder + kTile, 0);
+    std::stable_sort(rorder, rorder + kTile, [&](int a, int b) { return rlen[a] > rlen[b]; });
+    std::stable_sort(corder, corder + kTile, [&](int a, int b) { return clen[a] > clen[b]; });
+    for (int i = 0; i < kTile; ++i) {
+        rrank[rorder[i]] = i;
+        crank[corder[i]] = i;
+    }
+    std::vector<std::uint64_t> ord(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        const std::uint64_t r = ent[i] >> 56, c = (ent[i] >> 48) & 255u;
+        ord[i] = (static_cast<std::uint64_t>(rrank[r]) << 56) | (c << 48) | (ent[i] & 0xFFFFFFFFFFFFULL);
+    }
+    std::sort(ord.begin(), ord.end());
+    TileHdr hd{};
+    hd.begin8 = static_cast<std::uint32_t>(pos / 8);
+    hd.row0 = static_cast<std::int32_t>(row0);
+    hd.col0 = static_cast<std::int32_t>(col0);
+    hd.packed = static_cast<std::uint32_t>(nr - 1) | (static_cast<std::uint32_t>(nc - 1) << 7) |
+                (static_cast<std::uint32_t>(n) << 14);
+    out.hdr.push_back(hd);
+    for (int i = 0; i < kTile; ++i) out.lens.push_back(static_cast<unsigned char>(rlen[rorder[i]]));
+    for (int i = 0; i < kTile; ++i) out.lens.push_back(static_cast<unsigned char>(clen[corder[i]]));
+    std::vector<std::uint64_t> ck(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        const index_t k = static_cast<index_t>(ord[i] & 0xFFFFFFFFFFFFULL);
+        const std::uint64_t r = static_cast<std::uint64_t>(rorder[ord[i] >> 56]);
+        const std::uint64_t c = (ord[i] >> 48) & 255u;
+        out.v.push_back(L.values[k]);
+        out.rc.push_back(static_cast<std::uint16_t>((r << 8) | c));
+        if (keep_src) out.src.push_back(k);
+        ck[i] = (static_cast<std::uint64_t>(crank[c]) << 40) | (r << 32) | static_cast<std::uint64_t>(i);
+    }
+    std::sort(ck.begin(), ck.end());
+    for (std::uint64_t x : ck) out.cp.push_back(static_cast<std::uint16_t>(x & 0xFFFFFFFFu));
+    pos += static_cast<index_t>(n);
+    while (pos % 8) {  // pad the segment to 8 entries
+        out.v.push_back(0.0);
+        out.rc.push_back(0);
+        out.cp.push_back(0);
+        if (keep_src) out.src.push_back(-1);
+        ++pos;
+    }
+}
+
+void build_block_row(const be_csb_view& L, index_t bi, int max_nnz, bool keep_src, RowOut& out) {
+    const index_t br = L.row_offsets[bi + 1] - L.row_offsets[bi];
+    const index_t ta = (br + kTile - 1) / kTile;
+    struct BlockBuckets {  // one CSB block's entries bucketed by (a, b) sub-tile
+        index_t bj = 0, tb = 0;
+        std::vector<std::int32_t> start;
+        std::vector<std::int64_t> idx;
+    };
+    std::vector<BlockBuckets> blocks;
+    for (index_t bj = 0; bj < L.ncolblks; ++bj) {
+        const index_t bidx = bi * L.ncolblks + bj;
+        const index_t cnt = L.block_nnz[bidx];
+        if (cnt == 0) continue;
+        const index_t k0 = L.block_nnz_offsets[bidx];
+        const index_t bc = L.col_offsets[bj + 1] - L.col_offsets[bj];
+        BlockBuckets bb;
+        bb.bj = bj;
+        bb.tb = (bc + kTile - 1) / kTile;
+        bb.start.assign(static_cast<std::size_t>(ta * bb.tb + 1), 0);
+        for (index_t k = k0; k < k0 + cnt; ++k)
+            ++bb.start[static_cast<std::size_t>((L.local_rows[k] / kTile) * bb.tb + L.local_cols[k] / kTile + 1)];
+        for (std::size_t i = 1; i < bb.start.size(); ++i) bb.start[i] += bb.start[i - 1];
+        std::vector<std::int32_t> cur(bb.start.begin(), bb.start.end() - 1);
+        bb.idx.resize(static_cast<std::size_t>(cnt));
+        for (index_t k = k0; k < k0 + cnt; ++k)
+            bb.idx[static_cast<std::size_t>(cur[static_cast<std::size_t>((L.local_rows[k] / kTile) * bb.tb + L.local_cols[k] / kTile)]++)] = k;
+        blocks.push_back(std::move(bb));
+    }
+    std::vector<std::uint64_t> keys, piece;
+    index_t pos = 0;
+    for (index_t a = 0; a < ta; ++a) {
+        for (const auto& bb : blocks) {
+            for (index_t b = 0; b < bb.tb; ++b) {
+                const std::size_t s0 = static_cast<std::size_t>(bb.start[static_cast<std::size_t>(a * bb.tb + b)]);
+                const std::size_t s1 = static_cast<std::size_t>(bb.start[static_cast<std::size_t>(a * bb.tb + b + 1)]);
+                if (s0 == s1) continue;
+                keys.clear();
+                for (std::size_t i = s0; i < s1; ++i) {
+                    const index_t k = bb.idx[i];
+                    const std::uint64_t r = L.local_rows[k] % kTile, c = L.local_cols[k] % kTile;
+                    keys.push_back((r << 56) | (c << 48) | static_cast<std::uint64_t>(k));
+                }
+                std::sort(keys.begin(), keys.end());
+                const index_t row0 = L.row_offsets[bi] + a * kTile;
+                const index_t col0 = L.col_offsets[bb.bj] + b * kTile;
+                const index_t nc = std::min<index_t>(kTile, (L.col_offsets[bb.bj + 1] - L.col_offsets[bb.bj]) - b * kTile);
+                const index_t nr = std::min<index_t>(kTile, br - a * kTile);
+                std::size_t p0 = 0;
+                while (p0 < keys.size()) {  // row pieces of <= max_nnz entries
+                    std::size_t p1 = std::min(keys.size(), p0 + static_cast<std::size_t>(max_nnz));
+                    if (p1 < keys.size()) {
+                        const std::uint64_t rcut = keys[p1] >> 56;
+                        while (p1 > p0 && (keys[p1 - 1] >> 56) == rcut) --p1;
+                        if (p1 == p0) fail(BE_ERR_BAD_PARAMS, "tile row longer than max_nnz");
+                    }
+                    piece.assign(keys.begin() + static_cast<std::ptrdiff_t>(p0), keys.begin() + static_cast<std::ptrdiff_t>(p1));
+                    emit_piece(L, piece, row0, col0, nr, nc, keep_src, pos, out);
+                    p0 = p1;
+                }
+            }
+        }
+    }
+}
+
+template <typename TV>
+void upload_values(unsigned char* dst, const std::vector<double>& v) {
+    if constexpr (sizeof(TV) == 8) {
+        BE_CUDA(cudaMemcpy(dst, v.data(), v.size() * 8, cudaMemcpyHostToDevice));
+    } else {
+        std::vector<float> f(v.size());
+        for (std::size_t i = 0; i < v.size(); ++i) f[i] = static_cast<float>(v[i]);
+        BE_CUDA(cudaMemcpy(dst, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+    }
+}
+
+}  // namespace
+
+Ctx::~Ctx() {}
+
+Op::~Op() {
+    for (auto& e : ev)
+        if (e) cudaEventDestroy(e);
+}
+
+std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag, int values_prec, int flags) {
+    validate_view(L);
+    if (values_prec != BE_F32 && values_prec != BE_F64) fail(BE_ERR_BAD_PARAMS, "values_prec must be BE_F32 or BE_F64");
+    auto op = std::make_unique<Op>();
+    op->ctx = ctx;
+    op->nrows = L.nrows;
+    op->ncols = L.ncols;
+    op->nnz = L.nnz;
+    op->values_prec = values_prec;
+    op->symmetric = (flags & BE_OP_SYMMETRIC) != 0;
+    if (op->symmetric) {  // SymmetricOperator ctor checks, kernels.hpp:341-350
+        if (L.nrows != L.ncols) fail(BE_ERR_DIMENSION_MISMATCH, "SymmetricOperator: matrix must be square");
+        if (!diag && L.nrows > 0) fail(BE_ERR_DIMENSION_MISMATCH, "SymmetricOperator: diagonal length mismatch");
+        if (!is_strictly_lower(L)) fail(BE_ERR_NOT_STRICTLY_LOWER, "SymmetricOperator: stored entry with row <= col");
+    }
+    if (L.nrows >= (index_t{1} << 31) || L.ncols >= (index_t{1} << 31))
+        fail(BE_ERR_BAD_PARAMS, "sym_spmm: dimension exceeds 2^31 rows per device");
+    op->max_nnz = values_prec == BE_F32 ? 2048 : 1024;
+    const bool keep_src = L.nnz <= (index_t{1} << 26);
+
+    std::vector<RowOut> rows(static_cast<std::size_t>(L.nrowblks));
+    parallel_for_dynamic(hw_threads(), L.nrowblks, [&](index_t bi, int) {
+        build_block_row(L, bi, op->max_nnz, keep_src, rows[static_cast<std::size_t>(bi)]);
+    });
+    index_t ntiles = 0, padded = 0;
+    for (const auto& r : rows) {
+        ntiles += static_cast<index_t>(r.hdr.size());
+        padded += static_cast<index_t>(r.v.size());
+    }
+    if (padded / 8 >= (index_t{1} << 32)) fail(BE_ERR_BAD_PARAMS, "sym_spmm: too many entries for one device");
+    op->ntiles = ntiles;
+    op->padded = padded;
+    const std::size_t vsz = values_prec == BE_F32 ? 4 : 8;
+    op->tiles.reset(std::max<index_t>(ntiles, 1));
+    op->lens.reset(std::max<index_t>(ntiles, 1) * 256);
+    op->vals.reset(std::max<index_t>(padded, 8) * static_cast<index_t>(vsz));
+    op->rc.reset(std::max<index_t>(padded, 8));
+    op->cperm.reset(std::max<index_t>(padded, 8));
+    op->counter.reset(2);
+    BE_CUDA(cudaMemset(op->counter.get(), 0, 2 * sizeof(int)));
+    if (keep_src) op->csb_index.reserve(static_cast<std::size_t>(padded));
+    std::vector<TileHdr> all_hdr;
+    all_hdr.reserve(static_cast<std::size_t>(ntiles));
+    index_t t_off = 0, e_off = 0;
+    for (auto& r : rows) {
+        if (r.hdr.empty()) continue;
+        for (auto& h : r.hdr) h.begin8 += static_cast<std::uint32_t>(e_off / 8);
+        all_hdr.insert(all_hdr.end(), r.hdr.begin(), r.hdr.end());
+        BE_CUDA(cudaMemcpy(op->lens.get() + t_off * 256, r.lens.data(), r.lens.size(), cudaMemcpyHostToDevice));
+        if (values_prec == BE_F32)
+            upload_values<float>(op->vals.get() + e_off * 4, r.v);
+        else
+            upload_values<double>(op->vals.get() + e_off * 8, r.v);
+        BE_CUDA(cudaMemcpy(op->rc.get() + e_off, r.rc.data(), r.rc.size() * 2, cudaMemcpyHostToDevice));
+        BE_CUDA(cudaMemcpy(op->cperm.get() + e_off, r.cp.data(), r.cp.size() * 2, cudaMemcpyHostToDevice));
+        if (keep_src) op->csb_index.insert(op->csb_index.end(), r.src.begin(), r.src.end());
+        t_off += static_cast<index_t>(r.hdr.size());
+        e_off += static_cast<index_t>(r.v.size());
+        r = RowOut();
+    }
+    if (ntiles > 0)
+        BE_CUDA(cudaMemcpy(op->tiles.get(), all_hdr.data(), all_hdr.size() * sizeof(TileHdr), cudaMemcpyHostToDevice));
+    {  // runs: consecutive tiles of one tile-row, at most kRunMax tiles each
+        std::vector<int2> runs;
+        for (index_t t = 0; t < ntiles;) {
+            index_t e = t + 1;
+            while (e < ntiles && e - t < kRunMax &&
+                   all_hdr[static_cast<std::size_t>(e)].row0 == all_hdr[static_cast<std::size_t>(t)].row0)
+                ++e;
+            runs.push_back(make_int2(static_cast<int>(t), static_cast<int>(e)));
+            t = e;
+        }
+        op->nruns = static_cast<index_t>(runs.size());
+        op->runs.reset(std::max<index_t>(op->nruns, 1));
+        if (!runs.empty())
+            BE_CUDA(cudaMemcpy(op->runs.get(), runs.data(), runs.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    }
+    if (op->symmetric) {
+        op->diag.reset(std::max<index_t>(L.nrows, 1));
+        if (L.nrows > 0)
+            BE_CUDA(cudaMemcpy(op->diag.get(), diag, static_cast<std::size_t>(L.nrows) * 8, cudaMemcpyHostToDevice));
+    }
+    return op;
+}
+
+void op_apply(Op* op, const void* X, void* Y, index_t in_rows, int nb, int panel_prec, int mode, cudaStream_t s) {
+    if (nb < 1) fail(BE_ERR_DIMENSION_MISMATCH, "apply: nb must be positive");
+    if (panel_prec != BE_F32 && panel_prec != BE_F64) fail(BE_ERR_BAD_PARAMS, "apply: panel_prec must be BE_F32 or BE_F64");
+    if (X == Y) fail(BE_ERR_BAD_PARAMS, "spmm: W and U must not alias");
+    int do_r = 0, do_c = 0;
+    index_t out_rows = 0;
+    switch (mode) {
+        case BE_APPLY_SYMMETRIC:
+            if (!op->symmetric) fail(BE_ERR_BAD_PARAMS, "apply: symmetric mode needs a symmetric operator");
+            if (in_rows != op->nrows) fail(BE_ERR_DIMENSION_MISMATCH, "SymmetricOperator::apply: shape mismatch");
+            do_r = do_c = 1;
+            out_rows = op->nrows;
+            break;
+        case BE_APPLY_NOTRANS_ACC:
+            if (in_rows != op->ncols) fail(BE_ERR_DIMENSION_MISMATCH, "spmm: operand shapes do not conform to the matrix");
+            do_r = 1;
+            out_rows = op->nrows;
+            break;
+        case BE_APPLY_TRANS_ACC:
+            if (in_rows != op->nrows) fail(BE_ERR_DIMENSION_MISMATCH, "spmm: operand shapes do not conform to the matrix");
+            do_c = 1;
+            out_rows = op->ncols;
+            break;
+        default:
+            fail(BE_ERR_BAD_PARAMS, "apply: unknown mode");
+    }
+    if (op->timing) {
+        for (auto& e : op->ev)
+            if (!e) BE_CUDA(cudaEventCreate(&e));
+        BE_CUDA(cudaEventRecord(op->ev[0], s));
+    }
+    if (mode == BE_APPLY_SYMMETRIC && out_rows > 0) {
+        const index_t total = out_rows * nb;
+        const int grid = static_cast<int>(std::min<index_t>((total + 255) / 256, op->ctx->num_sms * 8));
+        if (panel_prec == BE_F32)
+            k_diag_init<float><<<grid, 256, 0, s>>>(op->diag.get(), static_cast<const float*>(X), static_cast<float*>(Y), out_rows, nb);
+        else
+            k_diag_init<double><<<grid, 256, 0, s>>>(op->diag.get(), static_cast<const double*>(X), static_cast<double*>(Y), out_rows, nb);
+        BE_CUDA(cudaGetLastError());
+        ++op->ctx->launches;
+    }
+    if (op->timing) BE_CUDA(cudaEventRecord(op->ev[1], s));
+    if (op->ntiles > 0) {
+        if (op->values_prec == BE_F32) {
+            if (panel_prec == BE_F32)
+                dispatch_nb<float, float, float>(op, static_cast<const float*>(X), static_cast<float*>(Y), nb, do_r, do_c, s);
+            else
+                dispatch_nb<float, float, double>(op, static_cast<const double*>(X), static_cast<double*>(Y), nb, do_r, do_c, s);
+        } else {
+            if (panel_prec == BE_F32)
+                dispatch_nb<double, double, float>(op, static_cast<const float*>(X), static_cast<float*>(Y), nb, do_r, do_c, s);
+            else
+                dispatch_nb<double, double, double>(op, static_cast<const double*>(X), static_cast<double*>(Y), nb, do_r, do_c, s);
+        }
+    }
+    if (op->timing) {
+        BE_CUDA(cudaEventRecord(op->ev[2], s));
+        BE_CUDA(cudaEventSynchronize(op->ev[2]));
+        float a = 0, k = 0;
+        BE_CUDA(cudaEventElapsedTime(&a, op->ev[0], op->ev[2]));
+        BE_CUDA(cudaEventElapsedTime(&k, op->ev[1], op->ev[2]));
+        op->last_apply_ms = a;
+        op->last_kernel_ms = k;
+    }
+}
+
+}  // namespace be
