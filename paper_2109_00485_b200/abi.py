@@ -388,3 +388,135 @@ class Operator:
             self.close()
         except Exception:
             pass
+
+
+class Tiles:
+    """DiagonalTileSet (precond.hpp:34-48) built by extract_tiles (precond.hpp:63-127), uploaded."""
+
+    def __init__(self, ctx: Context, csb: Csb, diag, tile_offsets):
+        self.ctx = ctx
+        self._h = C.c_void_p()
+        d = np.ascontiguousarray(diag, dtype=np.float64)
+        t = np.ascontiguousarray(tile_offsets, dtype=np.int64)
+        v = csb.view()
+        check(lib().be_tiles_create(ctx.handle, C.byref(v), _p(d), _p(t), C.c_int64(len(t)), C.byref(self._h)))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def count(self):
+        c, d = C.c_int64(), C.c_int64()
+        check(lib().be_tiles_count(self._h, C.byref(c), C.byref(d)))
+        return c.value, d.value
+
+    def tile(self, j):
+        """SparseTile j in the reference layout: (dim, rows, cols, values, diag_pos)."""
+        dim, ne = C.c_int64(), C.c_int64()
+        check(lib().be_tiles_get(self._h, C.c_int64(j), C.byref(dim), C.byref(ne), None, None, None, None))
+        rows = np.zeros(ne.value, np.int32)
+        cols = np.zeros(ne.value, np.int32)
+        vals = np.zeros(ne.value)
+        dpos = np.zeros(dim.value, np.int64)
+        check(lib().be_tiles_get(self._h, C.c_int64(j), C.byref(dim), C.byref(ne), _p(rows), _p(cols), _p(vals),
+                                 _p(dpos)))
+        return dim.value, rows, cols, vals, dpos
+
+    def apply_host(self, shifts, r, m=4):
+        """apply_preconditioner (precond.hpp:287-317): returns (W, fallbacks)."""
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        sh = np.ascontiguousarray(shifts, dtype=np.float64)
+        w = np.zeros_like(r)
+        fb = C.c_int64(0)
+        check(lib().be_precond_apply_host(self._h, _p(sh), _p(r), _p(w), C.c_int64(r.shape[0]), C.c_int(r.shape[1]),
+                                          C.c_int(m), C.byref(fb)))
+        return w, fb.value
+
+    def close(self):
+        if self._h:
+            check(lib().be_tiles_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def lobpcg(ctx: Context, op=None, n=None, tiles: Tiles | None = None, x0=None, k=5, nb=0, tol=1e-6, maxiter=500,
+           fom_iterations=4, seed=1234, observer=None, observer_state=False, host_operator=None):
+    """lobpcg_solve (lobpcg.hpp:291-456) on the device. `op` is an Operator;
+    `host_operator(x) -> y` is the generic Operator closure (lobpcg.hpp:20).
+    observer(iter, theta, residual_norms, n_converged, x, hx)."""
+    if n is None:
+        n = op.info().nrows
+    cfg = SolverConfig(k, nb, tol, maxiter, fom_iterations, seed, 1 if observer_state else 0)
+    x0a = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)
+    obs_cb = OBSERVER_FN()
+    if observer is not None:
+        def _obs(user, it, nn, nbb, th, rn, nc, x, hx):
+            thv = np.ctypeslib.as_array(th, shape=(nbb,)).copy()
+            rnv = np.ctypeslib.as_array(rn, shape=(nbb,)).copy()
+            xv = np.ctypeslib.as_array(x, shape=(nn, nbb)).copy() if x else None
+            hxv = np.ctypeslib.as_array(hx, shape=(nn, nbb)).copy() if hx else None
+            observer(it, thv, rnv, nc, xv, hxv)
+        obs_cb = OBSERVER_FN(_obs)
+    hop_cb = HOST_OP_FN()
+    if host_operator is not None:
+        def _hop(user, inp, out, nn, nbb):
+            try:
+                xi = np.ctypeslib.as_array(inp, shape=(nn, nbb))
+                yo = np.ctypeslib.as_array(out, shape=(nn, nbb))
+                yo[:] = host_operator(xi)
+                return 0
+            except Exception:
+                return 1
+        hop_cb = HOST_OP_FN(_hop)
+    h = C.c_void_p()
+    check(lib().be_lobpcg_solve(ctx.handle, op.handle if op is not None else None, hop_cb, None, C.c_int64(n),
+                                tiles.handle if tiles is not None else None, _p(x0a), C.byref(cfg), obs_cb, None,
+                                C.byref(h)))
+    try:
+        info = ResultInfo()
+        check(lib().be_result_get_info(h, C.byref(info)))
+        lam = np.zeros(info.k)
+        x = np.zeros((info.n, info.k))
+        check(lib().be_result_get(h, _p(lam), _p(x)))
+        nbb = info.nb
+        th = np.zeros((info.iterations, nbb))
+        rs = np.zeros((info.iterations, nbb))
+        nc = np.zeros(info.iterations, np.int32)
+        times = np.zeros((info.iterations, 4))
+        for i in range(info.iterations):
+            c_nc = C.c_int()
+            t = [C.c_double() for _ in range(4)]
+            row_t = np.zeros(nbb)
+            row_r = np.zeros(nbb)
+            check(lib().be_result_get_record(h, C.c_int(i), _p(row_t), _p(row_r), C.byref(c_nc), *[C.byref(v) for v in t]))
+            th[i], rs[i], nc[i] = row_t, row_r, c_nc.value
+            times[i] = [v.value for v in t]
+        return dict(lambda_=lam, x=x, converged=bool(info.converged), iterations=info.iterations,
+                    operator_calls=info.operator_calls, fallbacks=info.precond_fallbacks, restarts=info.restarts,
+                    theta=th, residual_norms=rs, n_converged=nc, times=times)
+    finally:
+        lib().be_result_free(h)
+
+
+def gram_dev(ctx: Context, a_ptr: int, b_ptr: int, nb: int, n: int) -> np.ndarray:
+    out = np.zeros(nb * nb)
+    check(lib().be_gram(ctx.handle, C.c_void_p(a_ptr), C.c_int(nb), C.c_void_p(b_ptr), C.c_int(nb), C.c_int64(n),
+                        _p(out)))
+    return out.reshape((nb, nb), order="F")
+
+
+def sygv_lowest(ctx: Context, a, b, k, pivot_floor=0.0):
+    """sygv_lowest (densela.hpp:357-407) computed on the device."""
+    n = a.shape[0]
+    A = np.asfortranarray(a, dtype=np.float64).ravel(order="F")
+    B = np.asfortranarray(b, dtype=np.float64).ravel(order="F")
+    c = np.zeros(n * k)
+    d = np.zeros(k)
+    check(lib().be_sygv_lowest(ctx.handle, _p(A), _p(B), C.c_int(n), C.c_int(k), C.c_double(pivot_floor), _p(c),
+                               _p(d)))
+    return c.reshape((n, k), order="F"), d

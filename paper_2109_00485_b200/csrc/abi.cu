@@ -7,7 +7,10 @@
 #include <cstring>
 #include <string>
 
+#include "densela.cuh"
 #include "device.hpp"
+#include "lobpcg.cuh"
+#include "precond.cuh"
 
 namespace {
 thread_local std::string g_err;
@@ -344,6 +347,172 @@ be_status be_op_timing(be_op* op, int enable, double* last_kernel_ms, double* la
         if (enable >= 0) o->timing = enable != 0;
         if (last_kernel_ms) *last_kernel_ms = o->last_kernel_ms;
         if (last_apply_ms) *last_apply_ms = o->last_apply_ms;
+    });
+}
+
+// ----------------------------------------------------------- preconditioner
+be_status be_tiles_create(be_ctx* ctx, const be_csb_view* L, const double* diag, const int64_t* tile_offsets,
+                          int64_t n_tile_offsets, be_tiles** out) {
+    return guard([&] {
+        if (!ctx || !L || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        BE_CUDA(cudaSetDevice(ctx->impl->device));
+        *out = new be_tiles{be::tiles_create(ctx->impl.get(), *L, diag, tile_offsets, n_tile_offsets)};
+    });
+}
+
+be_status be_tiles_destroy(be_tiles* t) {
+    return guard([&] { delete t; });
+}
+
+be_status be_tiles_count(const be_tiles* t, int64_t* count, int64_t* dim) {
+    return guard([&] {
+        if (!t) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        if (count) *count = t->impl->ntiles;
+        if (dim) *dim = t->impl->n;
+    });
+}
+
+be_status be_tiles_get(const be_tiles* t, int64_t j, int64_t* dim, int64_t* nentries, int32_t* rows, int32_t* cols,
+                       double* values, int64_t* diag_pos) {
+    return guard([&] {
+        if (!t) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        if (j < 0 || j >= t->impl->ntiles) be::fail(BE_ERR_BAD_PARAMS, "be_tiles_get: tile index out of range");
+        const auto& T = t->impl->host[static_cast<std::size_t>(j)];
+        if (dim) *dim = T.dim;
+        if (nentries) *nentries = static_cast<int64_t>(T.vals.size());
+        if (rows) std::memcpy(rows, T.rows.data(), T.rows.size() * 4);
+        if (cols) std::memcpy(cols, T.cols.data(), T.cols.size() * 4);
+        if (values) std::memcpy(values, T.vals.data(), T.vals.size() * 8);
+        if (diag_pos) std::memcpy(diag_pos, T.diag_pos.data(), T.diag_pos.size() * 8);
+    });
+}
+
+be_status be_precond_apply(be_tiles* t, const double* shifts_dev, const double* R_dev, double* W_dev, int64_t nrows,
+                           int nb, int m, int64_t* fallbacks_dev, void* stream) {
+    return guard([&] {
+        if (!t || !shifts_dev || !R_dev || !W_dev) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->impl->ctx->stream;
+        be::precond_apply(t->impl.get(), shifts_dev, R_dev, W_dev, nrows, nb, m, fallbacks_dev, s);
+    });
+}
+
+be_status be_precond_apply_host(be_tiles* t, const double* shifts, const double* R, double* W, int64_t nrows, int nb,
+                                int m, int64_t* fallbacks) {
+    return guard([&] {
+        if (!t || !shifts || !R || !W) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        if (nrows != t->impl->n) be::fail(BE_ERR_DIMENSION_MISMATCH, "apply_preconditioner: residual rows != operator dim");
+        cudaStream_t s = t->impl->ctx->stream;
+        const std::size_t bytes = static_cast<std::size_t>(nrows * nb) * 8;
+        be::DBuf<double> dr(std::max<int64_t>(nrows * nb, 1)), dw(std::max<int64_t>(nrows * nb, 1)), ds(nb);
+        be::DBuf<int64_t> df(1);
+        BE_CUDA(cudaMemcpyAsync(dr.get(), R, bytes, cudaMemcpyHostToDevice, s));
+        BE_CUDA(cudaMemcpyAsync(ds.get(), shifts, static_cast<std::size_t>(nb) * 8, cudaMemcpyHostToDevice, s));
+        BE_CUDA(cudaMemsetAsync(df.get(), 0, 8, s));
+        be::precond_apply(t->impl.get(), ds.get(), dr.get(), dw.get(), nrows, nb, m, df.get(), s);
+        BE_CUDA(cudaMemcpyAsync(W, dw.get(), bytes, cudaMemcpyDeviceToHost, s));
+        int64_t f = 0;
+        BE_CUDA(cudaMemcpyAsync(&f, df.get(), 8, cudaMemcpyDeviceToHost, s));
+        BE_CUDA(cudaStreamSynchronize(s));
+        if (fallbacks) *fallbacks += f;
+    });
+}
+
+// ------------------------------------------------------------------- LOBPCG
+be_status be_lobpcg_solve(be_ctx* ctx, be_op* op, be_host_operator_fn host_op, void* host_op_user, int64_t n,
+                          be_tiles* precond, const double* x0, const be_solver_config* cfg, be_observer_fn observer,
+                          void* observer_user, be_result** out) {
+    return guard([&] {
+        if (!ctx || !cfg || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        auto r = be::lobpcg_solve(ctx->impl.get(), op ? op->impl.get() : nullptr, host_op, host_op_user, n,
+                                  precond ? precond->impl.get() : nullptr, x0, *cfg, observer, observer_user);
+        *out = new be_result{std::move(r)};
+    });
+}
+
+be_status be_result_get_info(const be_result* r, be_result_info* info) {
+    return guard([&] {
+        if (!r || !info) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        const auto& R = *r->impl;
+        info->converged = R.converged ? 1 : 0;
+        info->iterations = static_cast<int>(R.records.size());
+        info->k = R.k;
+        info->nb = R.nb;
+        info->n = R.n;
+        info->operator_calls = R.operator_calls;
+        info->precond_fallbacks = R.precond_fallbacks;
+        info->restarts = R.restarts;
+    });
+}
+
+be_status be_result_get(const be_result* r, double* lambda, double* x) {
+    return guard([&] {
+        if (!r) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        if (lambda) std::memcpy(lambda, r->impl->lambda.data(), r->impl->lambda.size() * 8);
+        if (x) std::memcpy(x, r->impl->x.data(), r->impl->x.size() * 8);
+    });
+}
+
+be_status be_result_get_record(const be_result* r, int i, double* theta, double* residual_norms, int* n_converged,
+                               double* t_spmm, double* t_precond, double* t_dense, double* t_total) {
+    return guard([&] {
+        if (!r) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        if (i < 0 || i >= static_cast<int>(r->impl->records.size())) be::fail(BE_ERR_BAD_PARAMS, "record index out of range");
+        const auto& rec = r->impl->records[static_cast<std::size_t>(i)];
+        if (theta) std::memcpy(theta, rec.theta.data(), rec.theta.size() * 8);
+        if (residual_norms) std::memcpy(residual_norms, rec.resn.data(), rec.resn.size() * 8);
+        if (n_converged) *n_converged = rec.nconv;
+        if (t_spmm) *t_spmm = rec.t_spmm;
+        if (t_precond) *t_precond = rec.t_precond;
+        if (t_dense) *t_dense = rec.t_dense;
+        if (t_total) *t_total = rec.t_total;
+    });
+}
+
+void be_result_free(be_result* r) { delete r; }
+
+// ------------------------------------------------------- dense parity hooks
+be_status be_gram(be_ctx* ctx, const double* A_dev, int p, const double* B_dev, int q, int64_t n, double* out) {
+    return guard([&] {
+        if (!ctx || !A_dev || !B_dev || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        if (p != q) be::fail(BE_ERR_BAD_PARAMS, "be_gram: the device kernel handles square p == q Grams");
+        auto* c = ctx->impl.get();
+        cudaStream_t s = c->stream;
+        const int64_t plen = be::dla::gram_partials_len(p, 1, c->num_sms);
+        be::DBuf<double> part(plen), o(static_cast<int64_t>(p) * q);
+        be::dla::GramJob j{};
+        j.npairs = 1;
+        j.nb = p;
+        j.a[0] = A_dev;
+        j.b[0] = B_dev;
+        j.sym[0] = A_dev == B_dev;
+        j.out[0] = o.get();
+        be::dla::gram(c, j, n, part.get(), plen, s);
+        BE_CUDA(cudaMemcpyAsync(out, o.get(), static_cast<std::size_t>(p) * q * 8, cudaMemcpyDeviceToHost, s));
+        BE_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+be_status be_sygv_lowest(be_ctx* ctx, const double* A, const double* B, int n, int k, double pivot_floor, double* c,
+                         double* d) {
+    return guard([&] {
+        if (!ctx || !A || !B || !c || !d) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        if (k < 1 || k > n) be::fail(BE_ERR_BAD_PARAMS, "sygv_lowest: k out of range");
+        auto* cx = ctx->impl.get();
+        cudaStream_t s = cx->stream;
+        const std::size_t nn = static_cast<std::size_t>(n) * n;
+        be::DBuf<double> dA(static_cast<int64_t>(nn)), dB(static_cast<int64_t>(nn)), dc(static_cast<int64_t>(n) * k), dd(k);
+        be::DBuf<be::dla::Status> st(1);
+        BE_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(be::dla::Status), s));
+        BE_CUDA(cudaMemcpyAsync(dA.get(), A, nn * 8, cudaMemcpyHostToDevice, s));
+        BE_CUDA(cudaMemcpyAsync(dB.get(), B, nn * 8, cudaMemcpyHostToDevice, s));
+        be::dla::Sygv ws;
+        be::dla::sygv_lowest(cx, ws, dA.get(), dB.get(), n, k, pivot_floor, dc.get(), dd.get(), st.get(), s);
+        be::dla::Status hs{};
+        BE_CUDA(cudaMemcpyAsync(&hs, st.get(), sizeof(hs), cudaMemcpyDeviceToHost, s));
+        BE_CUDA(cudaMemcpyAsync(c, dc.get(), static_cast<std::size_t>(n) * k * 8, cudaMemcpyDeviceToHost, s));
+        BE_CUDA(cudaMemcpyAsync(d, dd.get(), static_cast<std::size_t>(k) * 8, cudaMemcpyDeviceToHost, s));
+        BE_CUDA(cudaStreamSynchronize(s));
+        if (hs.not_pd) be::fail(BE_ERR_NOT_POSITIVE_DEFINITE, "cholesky: pivot below floor at index " + std::to_string(hs.not_pd - 1), hs.not_pd - 1);
     });
 }
 

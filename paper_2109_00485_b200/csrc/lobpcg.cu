@@ -1,0 +1,418 @@
+// Device-resident LOBPCG driver (lobpcg_solve, lobpcg.hpp:291-456).
+//
+// The control flow is the reference's, line for line: CholQR hygiene with
+// the seeded random restart (lobpcg.hpp:358-373), one operator application
+// per iteration (:376-377), Rayleigh-Ritz over [X W P] with the drop-P retry
+// (:380-396), recurrence-updated H-images (:399-406), P hygiene (:412-417),
+// residuals and the convergence test (:419-434). Every panel stays in HBM as
+// row-major fp64; the host only sees the small status words, the Ritz values
+// and the residual norms, read at three synchronisation points per iteration
+// (after the first CholQR of W, after the projected eigenproblem, after the
+// residual norms). X0 and restart blocks come from the reference's own
+// mt19937_64 stream (block_vector.hpp:47-53), generated on the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <random>
+
+#include "densela.cuh"
+#include "lobpcg.cuh"
+#include "precond.cuh"
+
+namespace be {
+
+namespace {
+
+std::vector<double> random_block(index_t n, index_t nb, std::uint64_t seed) {  // block_vector.hpp:47-53
+    std::vector<double> x(static_cast<std::size_t>(n * nb));
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> u(-1.0, 1.0);
+    for (auto& v : x) v = u(rng);
+    return x;
+}
+
+struct Events {
+    cudaEvent_t e[6] = {};
+    Events() {
+        for (auto& x : e) BE_CUDA(cudaEventCreate(&x));
+    }
+    ~Events() {
+        for (auto& x : e)
+            if (x) cudaEventDestroy(x);
+    }
+    float ms(int a, int b) const {
+        float t = 0;
+        BE_CUDA(cudaEventElapsedTime(&t, e[a], e[b]));
+        return t;
+    }
+};
+
+struct Solver {
+    Ctx* ctx;
+    cudaStream_t s;
+    index_t n;
+    int nb, k;
+    Op* op;
+    be_host_operator_fn host_op;
+    void* host_user;
+    Tiles* tiles;
+    const be_solver_config& cfg;
+    be::Result& res;
+
+    DBuf<double> X, W, P, HX, HW, HP, R, Xn, HXn, Pn, HPn;
+    DBuf<double> small, partials;
+    DBuf<dla::Status> st;
+    DBuf<std::int64_t> fallbacks;
+    dla::Sygv sygv;
+    double* blocks = nullptr;  // 12 nb x nb
+    double *G = nullptr, *O = nullptr, *C = nullptr, *theta = nullptr;
+    double *Bq = nullptr, *Rq = nullptr, *xtp = nullptr, *Bp = nullptr, *Rp = nullptr;
+    double *rn2 = nullptr, *xn2 = nullptr, *shifts = nullptr, *pn2 = nullptr;
+    std::int64_t partials_len = 0;
+    // pinned host mirror of the small readbacks
+    struct Mirror {
+        dla::Status st;
+        double theta[64];
+        double rn2[64];
+        double xn2[64];
+        double shifts[64];
+        std::int64_t fallbacks;
+    } * hm = nullptr;
+    std::vector<double> host_in, host_out;  // host-operator staging
+
+    Solver(Ctx* c, index_t n_, int nb_, int k_, Op* o, be_host_operator_fn hop, void* hu, Tiles* t,
+           const be_solver_config& cf, be::Result& r)
+        : ctx(c), s(c->stream), n(n_), nb(nb_), k(k_), op(o), host_op(hop), host_user(hu), tiles(t), cfg(cf), res(r) {
+        const index_t pn = n * nb;
+        for (auto* b : {&X, &W, &P, &HX, &HW, &HP, &R, &Xn, &HXn, &Pn, &HPn}) b->reset(std::max<index_t>(pn, 1));
+        const index_t nb2 = static_cast<index_t>(nb) * nb, dim = 3 * nb;
+        small.reset(12 * nb2 + 2 * dim * dim + dim * nb + 8 * nb2 + 8 * nb);
+        double* p = small.get();
+        blocks = p; p += 12 * nb2;
+        G = p; p += dim * dim;
+        O = p; p += dim * dim;
+        C = p; p += dim * nb;
+        Bq = p; p += nb2;
+        Rq = p; p += nb2;
+        xtp = p; p += nb2;
+        Bp = p; p += nb2;
+        Rp = p; p += nb2;
+        p += 3 * nb2;
+        theta = p; p += nb;
+        rn2 = p; p += nb;
+        xn2 = p; p += nb;
+        shifts = p; p += nb;
+        pn2 = p; p += nb;
+        partials_len = std::max<std::int64_t>(dla::gram_partials_len(nb, 12, ctx->num_sms),
+                                              static_cast<std::int64_t>(ctx->num_sms) * 4 * 2 * nb);
+        partials.reset(partials_len);
+        st.reset(1);
+        fallbacks.reset(1);
+        BE_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(dla::Status), s));
+        BE_CUDA(cudaMemsetAsync(fallbacks.get(), 0, sizeof(std::int64_t), s));
+        BE_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hm), sizeof(Mirror)));
+        sygv.ensure(ctx, dim);
+    }
+    ~Solver() {
+        if (hm) cudaFreeHost(hm);
+    }
+
+    void sync_status() {
+        BE_CUDA(cudaMemcpyAsync(&hm->st, st.get(), sizeof(dla::Status), cudaMemcpyDeviceToHost, s));
+        BE_CUDA(cudaStreamSynchronize(s));
+    }
+    void reset_qr_flags() { BE_CUDA(cudaMemsetAsync(st.get(), 0, 3 * sizeof(int), s)); }
+
+    void apply_op(const double* in, double* out) {
+        if (op) {
+            op_apply(op, in, out, n, nb, BE_F64, BE_APPLY_SYMMETRIC, s);
+        } else {
+            host_in.resize(static_cast<std::size_t>(n * nb));
+            host_out.assign(static_cast<std::size_t>(n * nb), 0.0);
+            BE_CUDA(cudaMemcpyAsync(host_in.data(), in, host_in.size() * 8, cudaMemcpyDeviceToHost, s));
+            BE_CUDA(cudaStreamSynchronize(s));
+            if (host_op(host_user, host_in.data(), host_out.data(), n, nb) != 0)
+                fail(BE_ERR_GENERIC, "lobpcg_solve: host operator callback failed");
+            BE_CUDA(cudaMemcpyAsync(out, host_out.data(), host_out.size() * 8, cudaMemcpyHostToDevice, s));
+        }
+        ++res.operator_calls;
+    }
+
+    void gram1(const double* a, const double* b, int sym, double* out) {
+        dla::GramJob j{};
+        j.npairs = 1;
+        j.nb = nb;
+        j.a[0] = a;
+        j.b[0] = b;
+        j.sym[0] = sym;
+        j.out[0] = out;
+        dla::gram(ctx, j, n, partials.get(), partials_len, s);
+    }
+
+    // qr_of_transpose (densela.hpp:412-445); returns false on RankDeficient
+    bool qr(double* A, bool check) {
+        reset_qr_flags();
+        for (int pass = 0; pass < 2; ++pass) {
+            gram1(A, A, 1, Bq);
+            dla::qr_chol(ctx, Bq, Rq, nb, st.get(), s);
+            dla::trsm(ctx, A, nullptr, Rq, nb, n, st.get(), 1, 0, s);
+        }
+        if (!check) return true;
+        sync_status();
+        if (hm->st.singular_tri) fail(BE_ERR_SINGULAR_TRIANGULAR, "trsm_right_inv: triangular factor is numerically singular");
+        return hm->st.rank_deficient == 0;
+    }
+
+    void upload_random(double* dst, std::uint64_t seed) {
+        const auto h = random_block(n, nb, seed);
+        BE_CUDA(cudaMemcpyAsync(dst, h.data(), h.size() * 8, cudaMemcpyHostToDevice, s));
+        BE_CUDA(cudaStreamSynchronize(s));
+    }
+
+    // project_out (lobpcg.hpp:243-246): w -= basis (basis^T w)
+    void project_out(double* w, const double* basis) {
+        gram1(basis, w, 0, xtp);
+        dla::MixJob m{};
+        m.nb = nb;
+        m.nout = 1;
+        m.out[0] = dla::MixOut{w, 1, 1, {{basis, xtp, 1, 0}}, -1};
+        dla::mix(ctx, m, n, s);
+    }
+
+    // rayleigh_ritz (lobpcg.hpp:113-157): false on BasisDegenerate
+    bool rayleigh_ritz(bool with_p) {
+        dla::GramJob j{};
+        j.nb = nb;
+        const double* gpairs[12][2];
+        int sym[12];
+        int np = 0;
+        auto add = [&](const double* a, const double* b, int sy) {
+            gpairs[np][0] = a;
+            gpairs[np][1] = b;
+            sym[np] = sy;
+            ++np;
+        };
+        add(X.get(), HX.get(), 0);
+        add(W.get(), HX.get(), 0);
+        add(W.get(), HW.get(), 0);
+        if (with_p) {
+            add(P.get(), HX.get(), 0);
+            add(P.get(), HW.get(), 0);
+            add(P.get(), HP.get(), 0);
+        }
+        add(X.get(), X.get(), 1);
+        add(W.get(), X.get(), 0);
+        add(W.get(), W.get(), 1);
+        if (with_p) {
+            add(P.get(), X.get(), 0);
+            add(P.get(), W.get(), 0);
+            add(P.get(), P.get(), 1);
+        }
+        j.npairs = np;
+        for (int q = 0; q < np; ++q) {
+            j.a[q] = gpairs[q][0];
+            j.b[q] = gpairs[q][1];
+            j.sym[q] = sym[q];
+            j.out[q] = blocks + static_cast<index_t>(q) * nb * nb;
+        }
+        dla::gram(ctx, j, n, partials.get(), partials_len, s);
+        const int nblk = with_p ? 3 : 2;
+        dla::rr_assemble(ctx, blocks, nb, nblk, G, O, s);
+        dla::sygv_lowest(ctx, sygv, G, O, nblk * nb, nb, 1e-10, C, theta, st.get(), s);
+        BE_CUDA(cudaMemcpyAsync(hm->theta, theta, nb * 8, cudaMemcpyDeviceToHost, s));
+        sync_status();
+        return hm->st.not_pd == 0;
+    }
+
+    void run(const double* x0) {
+        if (x0)
+            BE_CUDA(cudaMemcpyAsync(X.get(), x0, static_cast<std::size_t>(n * nb) * 8, cudaMemcpyHostToDevice, s));
+        else
+            upload_random(X.get(), cfg.seed);
+        if (!qr(X.get(), true)) fail(BE_ERR_RANK_DEFICIENT, "qr_of_transpose: Gram Cholesky failed twice");
+        apply_op(X.get(), HX.get());
+        {  // initial Rayleigh-Ritz on X alone (lobpcg.hpp:320-334)
+            dla::GramJob j{};
+            j.nb = nb;
+            j.npairs = 2;
+            j.a[0] = X.get(); j.b[0] = HX.get(); j.sym[0] = 0; j.out[0] = blocks;
+            j.a[1] = X.get(); j.b[1] = X.get(); j.sym[1] = 1; j.out[1] = blocks + static_cast<index_t>(nb) * nb;
+            dla::gram(ctx, j, n, partials.get(), partials_len, s);
+            dla::rr_assemble(ctx, blocks, nb, 1, G, O, s);
+            dla::sygv_lowest(ctx, sygv, G, O, nb, nb, 1e-10, C, theta, st.get(), s);
+            BE_CUDA(cudaMemcpyAsync(hm->theta, theta, nb * 8, cudaMemcpyDeviceToHost, s));
+            sync_status();
+            if (hm->st.not_pd) fail(BE_ERR_BREAKDOWN_UNRECOVERABLE, "lobpcg_solve: initial block is degenerate");
+            dla::MixJob m{};
+            m.nb = nb;
+            m.nout = 2;
+            m.out[0] = dla::MixOut{Xn.get(), 0, 1, {{X.get(), C, 0, nb}}, -1};
+            m.out[1] = dla::MixOut{HXn.get(), 0, 1, {{HX.get(), C, 0, nb}}, -1};
+            dla::mix(ctx, m, n, s);
+            std::swap(X, Xn);
+            std::swap(HX, HXn);
+        }
+        std::vector<double> th(hm->theta, hm->theta + nb);
+        dla::residual(ctx, HX.get(), X.get(), theta, R.get(), nb, n, partials.get(), rn2, xn2, s);
+
+        bool p_active = false, converged = false;
+        Events ev;
+        for (int iter = 1; iter <= cfg.maxiter; ++iter) {
+            const auto wall0 = std::chrono::steady_clock::now();
+            BE_CUDA(cudaEventRecord(ev.e[0], s));
+            if (tiles) {  // W = K^{-1} R, shifts theta[min(v, k-1)] (lobpcg.hpp:344-350)
+                for (int v = 0; v < nb; ++v) hm->shifts[v] = th[static_cast<std::size_t>(std::min(v, k - 1))];
+                BE_CUDA(cudaMemcpyAsync(shifts, hm->shifts, nb * 8, cudaMemcpyHostToDevice, s));
+                precond_apply(tiles, shifts, R.get(), W.get(), n, nb, cfg.fom_iterations, fallbacks.get(), s);
+            } else {
+                BE_CUDA(cudaMemcpyAsync(W.get(), R.get(), static_cast<std::size_t>(n * nb) * 8, cudaMemcpyDeviceToDevice, s));
+            }
+            BE_CUDA(cudaEventRecord(ev.e[1], s));
+            // W hygiene (lobpcg.hpp:358-373)
+            if (!qr(W.get(), true)) {
+                upload_random(W.get(), cfg.seed + static_cast<std::uint64_t>(iter) * 7919u);
+                if (!qr(W.get(), true)) fail(BE_ERR_RANK_DEFICIENT, "qr_of_transpose: Gram Cholesky failed twice");
+            }
+            project_out(W.get(), X.get());
+            if (p_active) project_out(W.get(), P.get());
+            qr(W.get(), false);  // RankDeficient swallowed: W keeps the completed passes
+            BE_CUDA(cudaEventRecord(ev.e[2], s));
+            apply_op(W.get(), HW.get());
+            BE_CUDA(cudaEventRecord(ev.e[3], s));
+            // Rayleigh-Ritz with the drop-P retry (lobpcg.hpp:380-396)
+            bool dropped = false;
+            if (!rayleigh_ritz(p_active)) {
+                if (!p_active) fail(BE_ERR_BREAKDOWN_UNRECOVERABLE, "lobpcg_solve: 2-block basis failed Cholesky");
+                dropped = true;
+                ++res.restarts;
+                if (!rayleigh_ritz(false)) fail(BE_ERR_BREAKDOWN_UNRECOVERABLE, "lobpcg_solve: basis repair failed twice");
+            }
+            const bool with_p = p_active && !dropped;
+            const int dim = (with_p ? 3 : 2) * nb;
+            {  // update_blocks (lobpcg.hpp:168-194)
+                dla::MixJob m{};
+                m.nb = nb;
+                m.nout = 4;
+                const double* c1 = C;
+                const double* c2 = C + nb;
+                const double* c3 = C + 2 * nb;
+                m.out[0] = dla::MixOut{Pn.get(), 0, with_p ? 2 : 1, {{W.get(), c2, 0, dim}, {P.get(), c3, 0, dim}}, -1};
+                m.out[1] = dla::MixOut{HPn.get(), 0, with_p ? 2 : 1, {{HW.get(), c2, 0, dim}, {HP.get(), c3, 0, dim}}, -1};
+                m.out[2] = dla::MixOut{Xn.get(), 0, 1, {{X.get(), c1, 0, dim}}, 0};
+                m.out[3] = dla::MixOut{HXn.get(), 0, 1, {{HX.get(), c1, 0, dim}}, 1};
+                dla::mix(ctx, m, n, s);
+                std::swap(X, Xn);
+                std::swap(HX, HXn);
+                std::swap(P, Pn);
+                std::swap(HP, HPn);
+            }
+            th.assign(hm->theta, hm->theta + nb);
+            p_active = true;
+            {  // P hygiene (lobpcg.hpp:412-417) + orthonormalize_pair (:254-270)
+                gram1(X.get(), P.get(), 0, xtp);
+                dla::MixJob m{};
+                m.nb = nb;
+                m.nout = 2;
+                m.out[0] = dla::MixOut{P.get(), 1, 1, {{X.get(), xtp, 1, 0}}, -1};
+                m.out[1] = dla::MixOut{HP.get(), 1, 1, {{HX.get(), xtp, 1, 0}}, -1};
+                dla::mix(ctx, m, n, s);
+                gram1(P.get(), P.get(), 1, Bp);
+                dla::chol_floored(ctx, Bp, Rp, nb, 1e-8, st.get(), s);
+                dla::trsm(ctx, P.get(), HP.get(), Rp, nb, n, st.get(), 0, 1, s);
+            }
+            dla::residual(ctx, HX.get(), X.get(), theta, R.get(), nb, n, partials.get(), rn2, xn2, s);
+            BE_CUDA(cudaMemcpyAsync(hm->rn2, rn2, nb * 8, cudaMemcpyDeviceToHost, s));
+            BE_CUDA(cudaMemcpyAsync(hm->xn2, xn2, nb * 8, cudaMemcpyDeviceToHost, s));
+            BE_CUDA(cudaEventRecord(ev.e[4], s));
+            sync_status();
+            if (hm->st.not_pd) {  // column-scaling fallback of orthonormalize_pair
+                dla::colnorm2(ctx, P.get(), nb, n, partials.get(), pn2, s);
+                dla::scale_columns(ctx, P.get(), HP.get(), pn2, nb, n, st.get(), s);
+                BE_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(dla::Status), s));
+            }
+            if (hm->st.singular_tri) fail(BE_ERR_SINGULAR_TRIANGULAR, "trsm_right_inv: triangular factor is numerically singular");
+            // convergence_check (lobpcg.hpp:216-233)
+            IterRecord rec;
+            rec.iter = iter;
+            rec.theta = th;
+            rec.resn.resize(static_cast<std::size_t>(nb));
+            int nconv = 0;
+            for (int v = 0; v < nb; ++v) {
+                const double rn = std::sqrt(hm->rn2[v]), xn = std::sqrt(hm->xn2[v]);
+                rec.resn[static_cast<std::size_t>(v)] = rn;
+                if (rn <= cfg.tol * std::max(1.0, std::abs(th[static_cast<std::size_t>(v)])) * xn && v < k) ++nconv;
+            }
+            rec.nconv = nconv;
+            rec.t_precond = ev.ms(0, 1) * 1e-3;
+            rec.t_spmm = ev.ms(2, 3) * 1e-3;
+            rec.t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+            rec.t_dense = std::max(0.0, rec.t_total - rec.t_spmm - rec.t_precond);
+            res.records.push_back(rec);
+            if (observer) {
+                const double* xh = nullptr;
+                const double* hxh = nullptr;
+                std::vector<double> xb, hxb;
+                if (cfg.observer_state) {
+                    xb.resize(static_cast<std::size_t>(n * nb));
+                    hxb.resize(static_cast<std::size_t>(n * nb));
+                    BE_CUDA(cudaMemcpyAsync(xb.data(), X.get(), xb.size() * 8, cudaMemcpyDeviceToHost, s));
+                    BE_CUDA(cudaMemcpyAsync(hxb.data(), HX.get(), hxb.size() * 8, cudaMemcpyDeviceToHost, s));
+                    BE_CUDA(cudaStreamSynchronize(s));
+                    xh = xb.data();
+                    hxh = hxb.data();
+                }
+                observer(observer_user, iter, n, nb, th.data(), rec.resn.data(), nconv, xh, hxh);
+            }
+            if (nconv >= k) {
+                converged = true;
+                break;
+            }
+        }
+        res.converged = converged;
+        res.lambda.assign(th.begin(), th.begin() + k);
+        std::vector<double> xall(static_cast<std::size_t>(n * nb));
+        BE_CUDA(cudaMemcpyAsync(xall.data(), X.get(), xall.size() * 8, cudaMemcpyDeviceToHost, s));
+        BE_CUDA(cudaMemcpyAsync(&hm->fallbacks, fallbacks.get(), 8, cudaMemcpyDeviceToHost, s));
+        BE_CUDA(cudaStreamSynchronize(s));
+        res.precond_fallbacks = hm->fallbacks;
+        res.x.resize(static_cast<std::size_t>(n * k));
+        for (index_t r = 0; r < n; ++r)
+            for (int v = 0; v < k; ++v) res.x[static_cast<std::size_t>(r * k + v)] = xall[static_cast<std::size_t>(r * nb + v)];
+    }
+
+    be_observer_fn observer = nullptr;
+    void* observer_user = nullptr;
+};
+
+}  // namespace
+
+std::unique_ptr<Result> lobpcg_solve(Ctx* ctx, Op* op, be_host_operator_fn host_op, void* host_user, index_t n,
+                                     Tiles* tiles, const double* x0, const be_solver_config& cfg,
+                                     be_observer_fn observer, void* observer_user) {
+    const int nb = cfg.nb > 0 ? cfg.nb : cfg.k + 3;
+    // SolverConfig::validate (lobpcg.hpp:38-47) + FomConfig::validate
+    if (cfg.k < 1 || cfg.k > nb) fail(BE_ERR_BAD_PARAMS, "SolverConfig: need 1 <= k <= nb");
+    if (static_cast<index_t>(nb) * 3 > n) fail(BE_ERR_BAD_PARAMS, "SolverConfig: operator dimension must be at least 3*nb");
+    if (!(cfg.tol > 0.0)) fail(BE_ERR_BAD_PARAMS, "SolverConfig: tol must be positive");
+    if (cfg.maxiter < 1) fail(BE_ERR_BAD_PARAMS, "SolverConfig: maxiter must be positive");
+    if (cfg.fom_iterations < 1) fail(BE_ERR_BAD_PARAMS, "FomConfig: iterations must be >= 1");
+    if (nb > 64) fail(BE_ERR_BAD_PARAMS, "lobpcg_solve: block width above 64 is not supported on the device");
+    if (!op && !host_op) fail(BE_ERR_BAD_PARAMS, "lobpcg_solve: no operator");
+    if (op && (!op->symmetric || op->nrows != n)) fail(BE_ERR_DIMENSION_MISMATCH, "lobpcg_solve: operator dimension mismatch");
+    if (tiles && tiles->n != n) fail(BE_ERR_DIMENSION_MISMATCH, "lobpcg_solve: preconditioner dimension mismatch");
+    BE_CUDA(cudaSetDevice(ctx->device));
+    auto res = std::make_unique<Result>();
+    res->n = n;
+    res->nb = nb;
+    res->k = cfg.k;
+    Solver sv(ctx, n, nb, cfg.k, op, host_op, host_user, tiles, cfg, *res);
+    sv.observer = observer;
+    sv.observer_user = observer_user;
+    sv.run(x0);
+    return res;
+}
+
+}  // namespace be

@@ -1,0 +1,38 @@
+// Device-resident LOBPCG (lobpcg.hpp) result objects.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "device.hpp"
+
+namespace be {
+
+struct Tiles;
+
+struct IterRecord {  // IterationRecord, lobpcg.hpp:60-66
+    int iter = 0;
+    std::vector<double> theta, resn;
+    int nconv = 0;
+    double t_spmm = 0, t_precond = 0, t_dense = 0, t_total = 0;
+};
+
+struct Result {  // SolveResult + ConvergenceHistory, lobpcg.hpp:68-80
+    index_t n = 0;
+    int nb = 0, k = 0;
+    std::vector<double> lambda, x;
+    std::vector<IterRecord> records;
+    std::int64_t operator_calls = 0, precond_fallbacks = 0;
+    int restarts = 0;
+    bool converged = false;
+};
+
+std::unique_ptr<Result> lobpcg_solve(Ctx* ctx, Op* op, be_host_operator_fn host_op, void* host_user, index_t n,
+                                     Tiles* tiles, const double* x0, const be_solver_config& cfg,
+                                     be_observer_fn observer, void* observer_user);
+
+}  // namespace be
+
+struct be_result {
+    std::unique_ptr<be::Result> impl;
+};

@@ -1,0 +1,41 @@
+// Block-diagonal FOM preconditioner objects (precond.hpp).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "device.hpp"
+
+namespace be {
+
+// SparseTile (precond.hpp:18-30), host copy in the reference layout
+struct HostTile {
+    index_t dim = 0;
+    std::vector<std::int32_t> rows, cols;
+    std::vector<double> vals;
+    std::vector<index_t> diag_pos;
+};
+
+struct Tiles {
+    Ctx* ctx = nullptr;
+    index_t n = 0, ntiles = 0, nentries = 0, max_dim = 0;
+    std::vector<index_t> offsets;
+    std::vector<HostTile> host;
+    DBuf<unsigned char> tiles;  // TileDev records
+    DBuf<std::int32_t> rowptr;
+    DBuf<std::uint16_t> cols;
+    DBuf<double> vals;
+};
+
+std::unique_ptr<Tiles> tiles_create(Ctx* ctx, const be_csb_view& L, const double* diag, const index_t* off,
+                                    index_t noff);
+void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, index_t nrows, int nb, int m,
+                   std::int64_t* fallbacks, cudaStream_t s);
+
+}  // namespace be
+
+struct be_tiles {
+    std::unique_ptr<be::Tiles> impl;
+};
