@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""LOBPCG hot path benchmark (BASELINE.json metric, Test-1 shape by default).
+
+A step is one LOBPCG iteration (preconditioner, W hygiene, the symmetric
+SpMM, Rayleigh-Ritz, updates, residuals) of the device-resident solver on the
+Test-1-shaped synthetic Hamiltonian (n = 2.9e6, 1.1e9 stored lower nonzeros,
+nev = 8, block k = nb = 16). `value` is throughput in algorithmic GB/s of
+that iteration ("Measurement"): B_iter = B_spmm + 40 n nb 8 +
+16 * (preconditioner tile entries), B_spmm = 8 nnz + 16 n nb + 8 n, divided
+by the device time of the timed iterations (CUDA events on the solver's
+stream), summed over ranks. ms_per_step is the LOBPCG iteration time. The
+`roofline` object is the SpMM (the dominant kernel) against the measured HBM
+copy bandwidth of MEASURED_PEAKS.json.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config t1|c1] [--nb 16] [--nev 8] [--precond on|off]
+                  [--no-cpu-baseline]
+
+Under torchrun (N > 1) every rank solves its own copy of the problem
+(replicas; the 2D-partitioned distributed solver is not implemented yet).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # BASELINE.json configs[1]: Test-1 shape on 1 B200 (clustered generator)
+    "t1": dict(kind="clustered", n=2_900_000, nnz=1_100_000_000, extent=4000, tile=128, fill=0.10,
+               block_occupancy=1.0),
+    # configs[0]: the reference's own CPU-runnable case (generate_synthetic Random)
+    "c1": dict(kind="random", n=100_000, nnz=50_000_000, extent=4000),
+}
+
+
+def args_parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="t1")
+    ap.add_argument("--nb", type=int, default=16)
+    ap.add_argument("--nev", type=int, default=8)
+    ap.add_argument("--precond", choices=["on", "off"], default="on")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--seed", type=int, default=1)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def build_problem(cfg, seed):
+    from paper_2109_00485_b200 import abi
+    if cfg["kind"] == "clustered":
+        m, diag, toff = abi.generate_clustered(n=cfg["n"], target_nnz=cfg["nnz"], block_extent=cfg["extent"],
+                                               tile=cfg["tile"], fill=cfg["fill"],
+                                               block_occupancy=cfg["block_occupancy"], seed=seed)
+        return m, diag, toff
+    n = cfg["n"]
+    s = abi.Synthetic("random", n=n, density=cfg["nnz"] / (n * (n - 1) / 2), block_extent=cfg["extent"], seed=seed)
+    b = abi.uniform_boundaries(n, cfg["extent"])
+    m = abi.build_csb_coo(s.lower, n, n, b, b)
+    return m, s.diag, s.tile_offsets
+
+
+def alg_bytes(n, nnz, nb, tile_ent, precond):
+    b_spmm = 8 * nnz + 2 * n * nb * 8 + 8 * n
+    b_iter = b_spmm + 40 * n * nb * 8 + (16 * tile_ent if precond else 0)
+    return b_spmm, b_iter
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for name, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(config, nb):
+    p = ROOT / "profiles" / "spmm_traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get(f"{config}_nb{nb}")
+    return None
+
+
+def cpu_reference(m, diag, toff, nev, nb, iters, seed, precond):
+    """The reference's own lobpcg_solve (oracle/_ref/libref.so) on all host
+    cores; per-iteration IterationRecord::t_total. Returns (times, cores,
+    preconditioner tile entries)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import ctypes as C
+
+    import oracle_lib as ol
+    lib = ol.ref()
+    if lib is None:
+        return None
+    cores = os.cpu_count() or 1
+    v = m.view()
+    d = np.ascontiguousarray(diag, np.float64)
+    t = np.ascontiguousarray(toff, np.int64) if precond else None
+    h = lib.ref_prepare(C.byref(v), d.ctypes.data, None if t is None else t.ctypes.data, len(t) if t is not None else 0,
+                        cores)
+    if not h:
+        raise RuntimeError(lib.ref_last_error().decode())
+    try:
+        ent = int(lib.ref_tile_entries(h))
+        times = np.zeros(iters)
+        got = lib.ref_lobpcg_iter_times(h, nev, nb, iters, seed, 1 if precond else 0, times.ctypes.data)
+        per = times[:got]
+    finally:
+        lib.ref_release(h)
+    return per, cores, ent
+
+
+def run_reference(a, rank):
+    """--impl reference: the reference's CPU LOBPCG iteration on the box's host cores."""
+    if rank != 0:
+        return
+    cfg = CONFIGS[a.config]
+    precond = a.precond == "on"
+    m, diag, toff = build_problem(cfg, a.seed)
+    res = cpu_reference(m, diag, toff, a.nev, a.nb, a.warmup + a.steps, a.seed, precond)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref.so not built"}))
+        return
+    per, cores, ent = res
+    _, b_iter = alg_bytes(m.nrows, m.nnz, a.nb, ent, precond)
+    timed = per[a.warmup:]
+    t = float(np.sum(timed))
+    value = b_iter * len(timed) / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": 0, "steps": len(timed),
+        "warmup": a.warmup, "ms_per_step": 1e3 * t / len(timed), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload(a, cfg, m),
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "reference",
+                         "sample": f"{len(timed)} timed reference lobpcg_solve iterations (tol=1e-300, baseline "
+                                   f"SpMM variant, ThreadPool({cores})) after {a.warmup} warm-up iterations"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "LOBPCG iteration time and SpMM achieved HBM GB/s (% of peak) at 1/2/4/8 B200"
+
+
+def workload(a, cfg, m):
+    return {"workload": f"{a.config}: n={m.nrows}, half-nnz={m.nnz}, nev={a.nev}, block k={a.nb}, "
+                        f"precond {a.precond}", "n": m.nrows, "nnz": m.nnz, "nb": a.nb, "nev": a.nev,
+            "precond": a.precond == "on", "generator": cfg,
+            "l2": "inputs larger than L2 (matrix stream 8 B/nnz >> 126 MB)", "values": "f32",
+            "panels": "f64"}
+
+
+def main():
+    a = args_parse()
+    rank, world, local = dist_env()
+    if a.impl == "reference":
+        return run_reference(a, rank)
+    import torch
+
+    from paper_2109_00485_b200 import abi
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS[a.config]
+    precond = a.precond == "on"
+    t0 = time.time()
+    m, diag, toff = build_problem(cfg, a.seed + rank)
+    t_gen = time.time() - t0
+    ctx = abi.Context(local)
+    t0 = time.time()
+    op = abi.Operator(ctx, m, diag, values_prec=abi.BE_F32)
+    tiles = abi.Tiles(ctx, m, diag, toff) if precond else None
+    t_up = time.time() - t0
+    n, nnz = m.nrows, m.nnz
+    ent = tiles.count()[2] if tiles else 0
+    b_spmm, b_iter = alg_bytes(n, nnz, a.nb, ent, precond)
+    stream = torch.cuda.ExternalStream(ctx.stream())
+
+    # warm-up + timed iterations of one solve (tol 1e-300 keeps it iterating)
+    solver = abi.IncrementalSolve(ctx, op, tiles=tiles, k=a.nev, nb=a.nb, tol=1e-300,
+                                  maxiter=a.warmup + a.steps + 1, seed=a.seed)
+    solver.step(a.warmup)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = ctx.launches()
+    ev0.record(stream)
+    done = solver.step(a.steps)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = ctx.launches() - l0
+    clk = clocks.stop()
+    t_ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        tt = torch.tensor([t_ms], device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    res = solver.end()
+    rec = res["times"][a.warmup:a.warmup + done]
+    spmm_ms = 1e3 * float(np.mean(rec[:, 0])) if len(rec) else float("nan")
+    ms_step = t_ms / max(done, 1)
+    value = world * b_iter * done / (t_ms * 1e-3) / 1e9
+    peak, peak_kind = measured_peak()
+    ach = b_spmm / (spmm_ms * 1e-3) / 1e9
+
+    # end to end: the reference-facing solve call with host buffers (x0 in, X out)
+    x0 = np.random.default_rng(a.seed).uniform(-1, 1, (n, a.nb))
+    torch.cuda.synchronize()
+    e0 = time.perf_counter()
+    r2 = abi.lobpcg(ctx, op, tiles=tiles, x0=x0, k=a.nev, nb=a.nb, tol=1e-300, maxiter=a.steps, seed=a.seed)
+    e_s = time.perf_counter() - e0
+    e2e_val = world * b_iter * r2["iterations"] / e_s / 1e9
+
+    cpu = None
+    if rank == 0 and not a.no_cpu_baseline:
+        got = cpu_reference(m, diag, toff, a.nev, a.nb, a.cpu_iters, a.seed, precond)
+        if got is not None:
+            per, cores, _ = got
+            cpu = {"value": b_iter / float(np.median(per)) / 1e9, "unit": "GB/s", "cores": cores, "kind": "reference",
+                   "sample": f"{len(per)} reference lobpcg_solve iterations of the same problem (tol=1e-300, "
+                             f"baseline SpMM variant, ThreadPool({cores})); median iteration "
+                             f"{1e3 * float(np.median(per)):.0f} ms"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": done, "warmup": a.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 SpMM / f64 dense", "data": "synthetic", "config": workload(a, cfg, m),
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "traffic": ncu_traffic(a.config, a.nb), "kernel": "sym_spmm (k_diag_init + k_sym_spmm)",
+                     "bytes_per_launch": b_spmm, "ms_per_launch": spmm_ms, "peak_kind": peak_kind},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": int(x0.nbytes / max(r2["iterations"], 1)),
+                "d2h_bytes_per_step": int((n * a.nev * 8 + a.nev * 8) / max(r2["iterations"], 1) + 4 * a.nb * 8),
+                "iterations": r2["iterations"], "seconds": e_s},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "lobpcg": {"iter_ms": ms_step, "spmm_ms": spmm_ms, "precond_ms": 1e3 * float(np.mean(rec[:, 1])),
+                   "setup_s": {"generate": t_gen, "upload": t_up}, "parallelism": "replicas" if world > 1 else "1 GPU"},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

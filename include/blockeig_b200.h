@@ -231,7 +231,7 @@ be_status be_tiles_destroy(be_tiles* t);
  * query sizes with NULL buffers. */
 be_status be_tiles_get(const be_tiles* t, int64_t j, int64_t* dim, int64_t* nentries, int32_t* rows,
                        int32_t* cols, double* values, int64_t* diag_pos);
-be_status be_tiles_count(const be_tiles* t, int64_t* count, int64_t* dim);
+be_status be_tiles_count(const be_tiles* t, int64_t* count, int64_t* dim, int64_t* nentries);
 /* W = K^{-1} R (apply_preconditioner, precond.hpp:287-317). Device fp64
  * panels; shifts_dev: nb doubles on device; fallbacks_dev: one int64 on
  * device incremented by the number of singular columns (may be NULL). */
@@ -268,6 +268,17 @@ typedef struct be_result be_result;
 be_status be_lobpcg_solve(be_ctx* ctx, be_op* op, be_host_operator_fn host_op, void* host_op_user,
                           int64_t n, be_tiles* precond, const double* x0, const be_solver_config* cfg,
                           be_observer_fn observer, void* observer_user, be_result** out);
+
+/* Incremental form of the same solve (bench and iteration-level timing):
+ * begin = validation + X0 CholQR + first operator call + initial
+ * Rayleigh-Ritz (lobpcg.hpp:293-335); step runs up to `count` further
+ * iterations (*done receives how many; stops at convergence or maxiter);
+ * end returns the SolveResult and releases the solver. */
+typedef struct be_solver be_solver;
+be_status be_lobpcg_begin(be_ctx* ctx, be_op* op, be_host_operator_fn host_op, void* host_op_user, int64_t n,
+                          be_tiles* precond, const double* x0, const be_solver_config* cfg, be_solver** out);
+be_status be_lobpcg_step(be_solver* s, int count, int* done);
+be_status be_lobpcg_end(be_solver* s, be_result** out);
 
 typedef struct be_result_info {
     int converged;

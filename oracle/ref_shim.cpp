@@ -267,6 +267,15 @@ void* ref_prepare(const void* view, const double* diag, const index_t* off, inde
 
 void ref_release(void* p) { delete static_cast<Prepared*>(p); }
 
+// stored entries of the prepared preconditioner tiles (both triangles + diagonal)
+index_t ref_tile_entries(void* pp) {
+    auto* p = static_cast<Prepared*>(pp);
+    index_t e = 0;
+    if (p->tiles)
+        for (const auto& t : p->tiles->tiles) e += static_cast<index_t>(t.values.size());
+    return e;
+}
+
 // time `reps` SymmetricOperator::apply calls; returns seconds per apply (median)
 double ref_time_apply(void* pp, index_t nb, std::uint64_t seed, int reps) {
     auto* p = static_cast<Prepared*>(pp);
@@ -280,6 +289,22 @@ double ref_time_apply(void* pp, index_t nb, std::uint64_t seed, int reps) {
     }
     std::sort(t.begin(), t.end());
     return t[t.size() / 2];
+}
+
+// per-iteration wall times (IterationRecord::t_total, lobpcg.hpp:432) of a
+// fixed-length run; returns the number of iterations recorded
+int ref_lobpcg_iter_times(void* pp, int k, int nb, int iters, std::uint64_t seed, int use_precond, double* times) {
+    auto* p = static_cast<Prepared*>(pp);
+    SolverConfig cfg;
+    cfg.k = k;
+    cfg.nb = nb;
+    cfg.tol = 1e-300;
+    cfg.maxiter = iters;
+    cfg.seed = seed;
+    cfg.pool = p->pool.get();
+    const auto res = lobpcg_solve(*p->op, use_precond && p->tiles ? &*p->tiles : nullptr, nullptr, cfg);
+    for (std::size_t i = 0; i < res.history.records.size(); ++i) times[i] = res.history.records[i].t_total;
+    return static_cast<int>(res.history.records.size());
 }
 
 // run `iters` LOBPCG iterations (tol=1e-300, as test_lobpcg.cpp:341) and

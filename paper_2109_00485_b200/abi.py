@@ -406,9 +406,10 @@ class Tiles:
         return self._h
 
     def count(self):
-        c, d = C.c_int64(), C.c_int64()
-        check(lib().be_tiles_count(self._h, C.byref(c), C.byref(d)))
-        return c.value, d.value
+        """(number of tiles, operator dimension, total stored tile entries)"""
+        c, d, e = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().be_tiles_count(self._h, C.byref(c), C.byref(d), C.byref(e)))
+        return c.value, d.value, e.value
 
     def tile(self, j):
         """SparseTile j in the reference layout: (dim, rows, cols, values, diag_pos)."""
@@ -520,3 +521,42 @@ def sygv_lowest(ctx: Context, a, b, k, pivot_floor=0.0):
     check(lib().be_sygv_lowest(ctx.handle, _p(A), _p(B), C.c_int(n), C.c_int(k), C.c_double(pivot_floor), _p(c),
                                _p(d)))
     return c.reshape((n, k), order="F"), d
+
+
+class IncrementalSolve:
+    """be_lobpcg_begin / be_lobpcg_step / be_lobpcg_end (iteration-level control)."""
+
+    def __init__(self, ctx: Context, op=None, n=None, tiles: Tiles | None = None, x0=None, k=5, nb=0, tol=1e-6,
+                 maxiter=500, fom_iterations=4, seed=1234):
+        if n is None:
+            n = op.info().nrows
+        self.cfg = SolverConfig(k, nb, tol, maxiter, fom_iterations, seed, 0)
+        self._x0 = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)
+        self._h = C.c_void_p()
+        check(lib().be_lobpcg_begin(ctx.handle, op.handle if op is not None else None, HOST_OP_FN(), None,
+                                    C.c_int64(n), tiles.handle if tiles is not None else None, _p(self._x0),
+                                    C.byref(self.cfg), C.byref(self._h)))
+
+    def step(self, count=1) -> int:
+        done = C.c_int(0)
+        check(lib().be_lobpcg_step(self._h, C.c_int(count), C.byref(done)))
+        return done.value
+
+    def end(self):
+        r = C.c_void_p()
+        check(lib().be_lobpcg_end(self._h, C.byref(r)))
+        self._h = None
+        try:
+            info = ResultInfo()
+            check(lib().be_result_get_info(r, C.byref(info)))
+            lam = np.zeros(info.k)
+            check(lib().be_result_get(r, _p(lam), None))
+            times = np.zeros((info.iterations, 4))
+            for i in range(info.iterations):
+                t = [C.c_double() for _ in range(4)]
+                check(lib().be_result_get_record(r, C.c_int(i), None, None, None, *[C.byref(v) for v in t]))
+                times[i] = [v.value for v in t]
+            return dict(lambda_=lam, iterations=info.iterations, converged=bool(info.converged),
+                        operator_calls=info.operator_calls, times=times)
+        finally:
+            lib().be_result_free(r)

@@ -364,11 +364,12 @@ be_status be_tiles_destroy(be_tiles* t) {
     return guard([&] { delete t; });
 }
 
-be_status be_tiles_count(const be_tiles* t, int64_t* count, int64_t* dim) {
+be_status be_tiles_count(const be_tiles* t, int64_t* count, int64_t* dim, int64_t* nentries) {
     return guard([&] {
         if (!t) be::fail(BE_ERR_BAD_PARAMS, "null argument");
         if (count) *count = t->impl->ntiles;
         if (dim) *dim = t->impl->n;
+        if (nentries) *nentries = t->impl->nentries;
     });
 }
 
@@ -426,6 +427,32 @@ be_status be_lobpcg_solve(be_ctx* ctx, be_op* op, be_host_operator_fn host_op, v
         auto r = be::lobpcg_solve(ctx->impl.get(), op ? op->impl.get() : nullptr, host_op, host_op_user, n,
                                   precond ? precond->impl.get() : nullptr, x0, *cfg, observer, observer_user);
         *out = new be_result{std::move(r)};
+    });
+}
+
+be_status be_lobpcg_begin(be_ctx* ctx, be_op* op, be_host_operator_fn host_op, void* host_op_user, int64_t n,
+                          be_tiles* precond, const double* x0, const be_solver_config* cfg, be_solver** out) {
+    return guard([&] {
+        if (!ctx || !cfg || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        *out = static_cast<be_solver*>(be::lobpcg_begin(ctx->impl.get(), op ? op->impl.get() : nullptr, host_op,
+                                                          host_op_user, n, precond ? precond->impl.get() : nullptr, x0,
+                                                          *cfg));
+    });
+}
+
+be_status be_lobpcg_step(be_solver* s, int count, int* done) {
+    be_status st = guard([&] {
+        if (!s) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        const int d = be::lobpcg_step(s, count);
+        if (done) *done = d;
+    });
+    return st;
+}
+
+be_status be_lobpcg_end(be_solver* s, be_result** out) {
+    return guard([&] {
+        if (!s || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        *out = new be_result{be::lobpcg_end(s)};
     });
 }
 

@@ -227,7 +227,12 @@ struct Solver {
         return hm->st.not_pd == 0;
     }
 
-    void run(const double* x0) {
+    std::vector<double> th;
+    bool p_active = false, converged = false;
+    int iter = 0;
+    Events ev;
+
+    void init(const double* x0) {
         if (x0)
             BE_CUDA(cudaMemcpyAsync(X.get(), x0, static_cast<std::size_t>(n * nb) * 8, cudaMemcpyHostToDevice, s));
         else
@@ -255,12 +260,17 @@ struct Solver {
             std::swap(X, Xn);
             std::swap(HX, HXn);
         }
-        std::vector<double> th(hm->theta, hm->theta + nb);
+        th.assign(hm->theta, hm->theta + nb);
         dla::residual(ctx, HX.get(), X.get(), theta, R.get(), nb, n, partials.get(), rn2, xn2, s);
+    }
 
-        bool p_active = false, converged = false;
-        Events ev;
-        for (int iter = 1; iter <= cfg.maxiter; ++iter) {
+    // run up to `count` further iterations (never past maxiter); returns the
+    // number executed. Stops at convergence.
+    int iterate(int count) {
+        int done = 0;
+        while (done < count && !converged && iter < cfg.maxiter) {
+            ++iter;
+            ++done;
             const auto wall0 = std::chrono::steady_clock::now();
             BE_CUDA(cudaEventRecord(ev.e[0], s));
             if (tiles) {  // W = K^{-1} R, shifts theta[min(v, k-1)] (lobpcg.hpp:344-350)
@@ -366,11 +376,12 @@ struct Solver {
                 }
                 observer(observer_user, iter, n, nb, th.data(), rec.resn.data(), nconv, xh, hxh);
             }
-            if (nconv >= k) {
-                converged = true;
-                break;
-            }
+            if (nconv >= k) converged = true;
         }
+        return done;
+    }
+
+    void finish() {
         res.converged = converged;
         res.lambda.assign(th.begin(), th.begin() + k);
         std::vector<double> xall(static_cast<std::size_t>(n * nb));
@@ -411,8 +422,51 @@ std::unique_ptr<Result> lobpcg_solve(Ctx* ctx, Op* op, be_host_operator_fn host_
     Solver sv(ctx, n, nb, cfg.k, op, host_op, host_user, tiles, cfg, *res);
     sv.observer = observer;
     sv.observer_user = observer_user;
-    sv.run(x0);
+    sv.init(x0);
+    sv.iterate(cfg.maxiter);
+    sv.finish();
     return res;
 }
+
+struct Incremental {
+    be_solver_config cfg;
+    std::unique_ptr<Result> res;
+    std::unique_ptr<Solver> sv;
+};
+
+void* lobpcg_begin(Ctx* ctx, Op* op, be_host_operator_fn host_op, void* host_user, index_t n, Tiles* tiles,
+                   const double* x0, const be_solver_config& cfg) {
+    const int nb = cfg.nb > 0 ? cfg.nb : cfg.k + 3;
+    if (cfg.k < 1 || cfg.k > nb) fail(BE_ERR_BAD_PARAMS, "SolverConfig: need 1 <= k <= nb");
+    if (static_cast<index_t>(nb) * 3 > n) fail(BE_ERR_BAD_PARAMS, "SolverConfig: operator dimension must be at least 3*nb");
+    if (!(cfg.tol > 0.0)) fail(BE_ERR_BAD_PARAMS, "SolverConfig: tol must be positive");
+    if (cfg.maxiter < 1) fail(BE_ERR_BAD_PARAMS, "SolverConfig: maxiter must be positive");
+    if (cfg.fom_iterations < 1) fail(BE_ERR_BAD_PARAMS, "FomConfig: iterations must be >= 1");
+    if (nb > 64) fail(BE_ERR_BAD_PARAMS, "lobpcg_solve: block width above 64 is not supported on the device");
+    if (!op && !host_op) fail(BE_ERR_BAD_PARAMS, "lobpcg_solve: no operator");
+    if (op && (!op->symmetric || op->nrows != n)) fail(BE_ERR_DIMENSION_MISMATCH, "lobpcg_solve: operator dimension mismatch");
+    if (tiles && tiles->n != n) fail(BE_ERR_DIMENSION_MISMATCH, "lobpcg_solve: preconditioner dimension mismatch");
+    BE_CUDA(cudaSetDevice(ctx->device));
+    auto inc = std::make_unique<Incremental>();
+    inc->cfg = cfg;
+    inc->res = std::make_unique<Result>();
+    inc->res->n = n;
+    inc->res->nb = nb;
+    inc->res->k = cfg.k;
+    inc->sv = std::make_unique<Solver>(ctx, n, nb, cfg.k, op, host_op, host_user, tiles, inc->cfg, *inc->res);
+    inc->sv->init(x0);
+    return inc.release();
+}
+
+int lobpcg_step(void* h, int count) { return static_cast<Incremental*>(h)->sv->iterate(count); }
+
+std::unique_ptr<Result> lobpcg_end(void* h) {
+    std::unique_ptr<Incremental> inc(static_cast<Incremental*>(h));
+    inc->sv->finish();
+    inc->sv.reset();
+    return std::move(inc->res);
+}
+
+void lobpcg_abort(void* h) { delete static_cast<Incremental*>(h); }
 
 }  // namespace be

@@ -31,6 +31,13 @@ std::unique_ptr<Result> lobpcg_solve(Ctx* ctx, Op* op, be_host_operator_fn host_
                                      Tiles* tiles, const double* x0, const be_solver_config& cfg,
                                      be_observer_fn observer, void* observer_user);
 
+// incremental driver (bench / iteration-level timing)
+void* lobpcg_begin(Ctx* ctx, Op* op, be_host_operator_fn host_op, void* host_user, index_t n, Tiles* tiles,
+                   const double* x0, const be_solver_config& cfg);
+int lobpcg_step(void* h, int count);
+std::unique_ptr<Result> lobpcg_end(void* h);
+void lobpcg_abort(void* h);
+
 }  // namespace be
 
 struct be_result {

@@ -51,6 +51,10 @@ def ref():
         _ref.ref_time_apply.argtypes = [C.c_void_p, C.c_int64, C.c_uint64, C.c_int]
         _ref.ref_time_lobpcg.restype = C.c_double
         _ref.ref_time_lobpcg.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_void_p]
+        _ref.ref_tile_entries.restype = C.c_int64
+        _ref.ref_tile_entries.argtypes = [C.c_void_p]
+        _ref.ref_lobpcg_iter_times.restype = C.c_int
+        _ref.ref_lobpcg_iter_times.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_void_p]
     return _ref
 
 
