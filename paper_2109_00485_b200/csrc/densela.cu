@@ -30,15 +30,20 @@ struct GramDev {
     int ia[12], ib[12];       // panel index of A_p / B_p
 };
 
-constexpr int kGramRows = 16;
+constexpr int kGramRows = 32;
 
-// partial[blk][combo][16]: 4x4 register block of A_p^T B_p over this CTA's rows
-__global__ void __launch_bounds__(kT) k_gram_partial(GramDev g, std::int64_t n, double* __restrict__ partial) {
-    extern __shared__ double sp[];  // nd x kGramRows x nbp
+// partial[blk][combo][16]: 4x4 register block of A_p^T B_p over this CTA's
+// rows. cpb combos per CTA slice; the rg = 256 / cpb row groups of a CTA take
+// interleaved rows of each staged chunk and are summed in smem at the end.
+__global__ void __launch_bounds__(kT) k_gram_partial(GramDev g, std::int64_t n, double* __restrict__ partial, int cpb) {
+    extern __shared__ double sp[];  // max(nd x kGramRows x nbp, rg x cpb x 16)
     const int nbp = g.nblk * 4;
-    const int combo = blockIdx.y * kT + threadIdx.x;
+    const int rg = kT / cpb;
+    const int cl = threadIdx.x % cpb, grp = threadIdx.x / cpb;
+    const int combo = blockIdx.y * cpb + cl;
+    const bool active = grp < rg && combo < g.ncombo;
     int p = 0, bi = 0, bj = 0;
-    if (combo < g.ncombo) {
+    if (active) {
         p = combo / (g.nblk * g.nblk);
         const int rem = combo % (g.nblk * g.nblk);
         bi = rem / g.nblk;
@@ -55,18 +60,28 @@ __global__ void __launch_bounds__(kT) k_gram_partial(GramDev g, std::int64_t n, 
         for (int d = 0; d < g.nd; ++d) {
             const double* src = g.panel[d] + c0 * g.nb;
             double* dst = sp + d * kGramRows * nbp;
-            for (int e = threadIdx.x; e < kGramRows * nbp; e += kT) {
-                const int r = e / nbp, v = e % nbp;
-                dst[e] = (r < rows && v < g.nb) ? src[r * g.nb + v] : 0.0;
+            if (nbp == g.nb) {  // contiguous rows: straight vector copy
+                const int tot = rows * g.nb / 2;
+                for (int e = threadIdx.x; e < tot; e += kT)
+                    reinterpret_cast<double2*>(dst)[e] = __ldg(reinterpret_cast<const double2*>(src) + e);
+            } else {
+                for (int e = threadIdx.x; e < kGramRows * nbp; e += kT) {
+                    const int r = e / nbp, v = e % nbp;
+                    dst[e] = (r < rows && v < g.nb) ? src[r * g.nb + v] : 0.0;
+                }
             }
         }
         __syncthreads();
-        if (combo < g.ncombo) {
+        if (active) {
             const double* A = sp + g.ia[p] * kGramRows * nbp + bi * 4;
             const double* B = sp + g.ib[p] * kGramRows * nbp + bj * 4;
-            for (int r = 0; r < rows; ++r) {
-                const double a0 = A[r * nbp], a1 = A[r * nbp + 1], a2 = A[r * nbp + 2], a3 = A[r * nbp + 3];
-                const double b0 = B[r * nbp], b1 = B[r * nbp + 1], b2 = B[r * nbp + 2], b3 = B[r * nbp + 3];
+            for (int r = grp; r < rows; r += rg) {
+                const double2 a01 = *reinterpret_cast<const double2*>(A + r * nbp);
+                const double2 a23 = *reinterpret_cast<const double2*>(A + r * nbp + 2);
+                const double2 b01 = *reinterpret_cast<const double2*>(B + r * nbp);
+                const double2 b23 = *reinterpret_cast<const double2*>(B + r * nbp + 2);
+                const double a0 = a01.x, a1 = a01.y, a2 = a23.x, a3 = a23.y;
+                const double b0 = b01.x, b1 = b01.y, b2 = b23.x, b3 = b23.y;
                 acc[0] += a0 * b0; acc[1] += a1 * b0; acc[2] += a2 * b0; acc[3] += a3 * b0;
                 acc[4] += a0 * b1; acc[5] += a1 * b1; acc[6] += a2 * b1; acc[7] += a3 * b1;
                 acc[8] += a0 * b2; acc[9] += a1 * b2; acc[10] += a2 * b2; acc[11] += a3 * b2;
@@ -74,10 +89,17 @@ __global__ void __launch_bounds__(kT) k_gram_partial(GramDev g, std::int64_t n, 
             }
         }
     }
-    if (combo < g.ncombo) {
-        double* out = partial + (static_cast<std::int64_t>(blockIdx.x) * g.ncombo + combo) * 16;
+    __syncthreads();
+    if (grp < rg)
 #pragma unroll
-        for (int e = 0; e < 16; ++e) out[e] = acc[e];
+        for (int e = 0; e < 16; ++e) sp[(grp * cpb + cl) * 16 + e] = acc[e];
+    __syncthreads();
+    for (int e = threadIdx.x; e < cpb * 16; e += kT) {
+        const int c = e / 16;
+        if (blockIdx.y * cpb + c >= g.ncombo) continue;
+        double s = 0.0;
+        for (int q = 0; q < rg; ++q) s += sp[(q * cpb + c) * 16 + e % 16];
+        partial[(static_cast<std::int64_t>(blockIdx.x) * g.ncombo + blockIdx.y * cpb + c) * 16 + e % 16] = s;
     }
 }
 
@@ -86,31 +108,35 @@ struct GramOut {
     int sym[12];
 };
 
-// out_p(i, j) = sum over CTAs in order; symmetrised pairs use both halves
+// out_p(i, j) = sum over CTAs (fixed lane-strided order + butterfly, so the
+// result is deterministic); symmetrised pairs average both halves. One warp
+// per output element.
 __global__ void k_gram_reduce(GramDev g, GramOut o, int nparts, const double* __restrict__ partial) {
     const int nb = g.nb;
     const int total = g.npairs * nb * nb;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < total; e += (gridDim.x * blockDim.x) >> 5) {
         const int p = e / (nb * nb), rem = e % (nb * nb);
         const int j = rem / nb, i = rem % nb;  // column-major (i, j)
+        if (o.sym[p] && i > j) continue;
         auto sum_at = [&](int ii, int jj) {
             const int combo = p * g.nblk * g.nblk + (ii / 4) * g.nblk + (jj / 4);
             const int el = (jj % 4) * 4 + (ii % 4);
             double s = 0.0;
-            for (int b = 0; b < nparts; ++b) s += partial[(static_cast<std::int64_t>(b) * g.ncombo + combo) * 16 + el];
+            for (int b = lane; b < nparts; b += 32) s += partial[(static_cast<std::int64_t>(b) * g.ncombo + combo) * 16 + el];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
             return s;
         };
-        if (o.sym[p]) {
-            if (i > j) continue;
-            if (i == j) {
-                o.out[p][j * nb + i] = sum_at(i, j);
-            } else {
-                const double s = 0.5 * (sum_at(i, j) + sum_at(j, i));
+        const double sij = sum_at(i, j);
+        if (o.sym[p] && i != j) {
+            const double s = 0.5 * (sij + sum_at(j, i));
+            if (lane == 0) {
                 o.out[p][j * nb + i] = s;
                 o.out[p][i * nb + j] = s;
             }
-        } else {
-            o.out[p][j * nb + i] = sum_at(i, j);
+        } else if (lane == 0) {
+            o.out[p][j * nb + i] = sij;
         }
     }
 }
@@ -125,78 +151,123 @@ struct MixDev {
         int accumulate, nterms, add_from;
         const double* src[3];
         int ci[3];
+        int si[3];
         double sign[3];
     } out[4];
 };
 
-// thread = (row, 4-column block); coefficients transposed into smem
-__global__ void __launch_bounds__(kT) k_mix(MixDev m, std::int64_t n) {
-    extern __shared__ double ct[];  // ncoef x nb x nbp (row i, col j) row-major
-    const int nb = m.nb, nblk = (nb + 3) / 4, nbp = nblk * 4;
+// CTA tile of RT rows: the distinct source panels' rows are staged in smem
+// with 16-byte coalesced loads (row stride nb + 1 doubles: conflict-free
+// column reads), then thread = (row, 4-column block) forms every output for
+// its row from smem and the transposed coefficients.
+constexpr int kMixRows = 64;
+struct MixSrc {
+    int nsrc;
+    const double* src[6];
+};
+__global__ void __launch_bounds__(kT) k_mix(MixDev m, MixSrc ms, const int* __restrict__ srcidx_dummy, std::int64_t n) {
+    extern __shared__ double sh[];
+    const int nb = m.nb, nblk = (nb + 3) / 4, nbp = nblk * 4, ld = nb + 1;
+    double* ct = sh;                                 // ncoef x nb x nbp
+    double* xs = sh + m.ncoef * nb * nbp;            // nsrc x kMixRows x ld
     for (int c = 0; c < m.ncoef; ++c)
         for (int e = threadIdx.x; e < nb * nbp; e += kT) {
             const int i = e / nbp, j = e % nbp;
             ct[c * nb * nbp + e] = j < nb ? m.coef[c][j * m.ld[c] + i] : 0.0;
         }
-    __syncthreads();
-    const std::int64_t total = n * nblk;
-    for (std::int64_t t = blockIdx.x * static_cast<std::int64_t>(kT) + threadIdx.x; t < total;
-         t += static_cast<std::int64_t>(gridDim.x) * kT) {
-        const std::int64_t r = t / nblk;
-        const int j0 = static_cast<int>(t % nblk) * 4;
-        double res[4][4];  // per output
-        for (int o = 0; o < m.nout; ++o) {
-            const auto& O = m.out[o];
-            double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-            double* y = O.y + r * nb;
-            if (O.accumulate) {
-                a0 = j0 < nb ? y[j0] : 0.0;
-                a1 = j0 + 1 < nb ? y[j0 + 1] : 0.0;
-                a2 = j0 + 2 < nb ? y[j0 + 2] : 0.0;
-                a3 = j0 + 3 < nb ? y[j0 + 3] : 0.0;
-            }
-            for (int tt = 0; tt < O.nterms; ++tt) {
-                const double* x = O.src[tt] + r * nb;
-                const double* C = ct + O.ci[tt] * nb * nbp + j0;
-                double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-                for (int i = 0; i < nb; ++i) {
-                    const double xi = __ldg(x + i);
-                    s0 += xi * C[i * nbp];
-                    s1 += xi * C[i * nbp + 1];
-                    s2 += xi * C[i * nbp + 2];
-                    s3 += xi * C[i * nbp + 3];
+    const int rpi = kT / nblk;  // rows computed per pass
+    for (std::int64_t r0 = static_cast<std::int64_t>(blockIdx.x) * kMixRows; r0 < n;
+         r0 += static_cast<std::int64_t>(gridDim.x) * kMixRows) {
+        const int rows = static_cast<int>(n - r0 < kMixRows ? n - r0 : kMixRows);
+        __syncthreads();
+        for (int q = 0; q < ms.nsrc; ++q) {
+            const double* src = ms.src[q] + r0 * nb;
+            double* dst = xs + q * kMixRows * ld;
+            if ((nb & 1) == 0) {
+                const int tot = rows * nb / 2;
+                for (int e = threadIdx.x; e < tot; e += kT) {
+                    const double2 v = __ldg(reinterpret_cast<const double2*>(src) + e);
+                    const int r = (2 * e) / nb, c = (2 * e) % nb;
+                    dst[r * ld + c] = v.x;
+                    dst[r * ld + c + 1] = v.y;
                 }
-                const double sg = O.sign[tt];
-                a0 += sg * s0;
-                a1 += sg * s1;
-                a2 += sg * s2;
-                a3 += sg * s3;
+            } else {
+                for (int e = threadIdx.x; e < rows * nb; e += kT) dst[(e / nb) * ld + e % nb] = __ldg(src + e);
             }
-            if (O.add_from >= 0) {
-                a0 += res[O.add_from][0];
-                a1 += res[O.add_from][1];
-                a2 += res[O.add_from][2];
-                a3 += res[O.add_from][3];
+        }
+        __syncthreads();
+        for (int rl = threadIdx.x / nblk; rl < rows; rl += rpi) {
+            if (threadIdx.x >= rpi * nblk) break;
+            const std::int64_t r = r0 + rl;
+            const int j0 = (threadIdx.x % nblk) * 4;
+            double res[4][4];
+            for (int o = 0; o < m.nout; ++o) {
+                const auto& O = m.out[o];
+                double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+                double* y = O.y + r * nb;
+                if (O.accumulate) {
+                    a0 = j0 < nb ? y[j0] : 0.0;
+                    a1 = j0 + 1 < nb ? y[j0 + 1] : 0.0;
+                    a2 = j0 + 2 < nb ? y[j0 + 2] : 0.0;
+                    a3 = j0 + 3 < nb ? y[j0 + 3] : 0.0;
+                }
+                for (int tt = 0; tt < O.nterms; ++tt) {
+                    const double* x = xs + O.si[tt] * kMixRows * ld + rl * ld;
+                    const double* C = ct + O.ci[tt] * nb * nbp + j0;
+                    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+                    for (int i = 0; i < nb; ++i) {
+                        const double xi = x[i];
+                        const double2 c01 = *reinterpret_cast<const double2*>(C + i * nbp);
+                        const double2 c23 = *reinterpret_cast<const double2*>(C + i * nbp + 2);
+                        s0 += xi * c01.x;
+                        s1 += xi * c01.y;
+                        s2 += xi * c23.x;
+                        s3 += xi * c23.y;
+                    }
+                    const double sg = O.sign[tt];
+                    a0 += sg * s0;
+                    a1 += sg * s1;
+                    a2 += sg * s2;
+                    a3 += sg * s3;
+                }
+                if (O.add_from >= 0) {
+                    a0 += res[O.add_from][0];
+                    a1 += res[O.add_from][1];
+                    a2 += res[O.add_from][2];
+                    a3 += res[O.add_from][3];
+                }
+                res[o][0] = a0;
+                res[o][1] = a1;
+                res[o][2] = a2;
+                res[o][3] = a3;
+                if (j0 + 3 < nb && (nb & 1) == 0) {
+                    reinterpret_cast<double2*>(y + j0)[0] = make_double2(a0, a1);
+                    reinterpret_cast<double2*>(y + j0)[1] = make_double2(a2, a3);
+                } else {
+                    if (j0 < nb) y[j0] = a0;
+                    if (j0 + 1 < nb) y[j0 + 1] = a1;
+                    if (j0 + 2 < nb) y[j0 + 2] = a2;
+                    if (j0 + 3 < nb) y[j0 + 3] = a3;
+                }
             }
-            res[o][0] = a0;
-            res[o][1] = a1;
-            res[o][2] = a2;
-            res[o][3] = a3;
-            if (j0 < nb) y[j0] = a0;
-            if (j0 + 1 < nb) y[j0 + 1] = a1;
-            if (j0 + 2 < nb) y[j0 + 2] = a2;
-            if (j0 + 3 < nb) y[j0 + 3] = a3;
         }
     }
 }
 
 // -------------------------------------------------------------------- trsm
+// 128 rows per CTA pass staged in smem (coalesced), one thread per row does
+// the forward substitution of trsm_right_inv (densela.hpp:137-146) from smem.
+template <int NBP>
+constexpr int trsm_rows() { return NBP <= 16 ? 128 : NBP <= 32 ? 32 : 8; }
 template <int NBP>
 __global__ void __launch_bounds__(kT) k_trsm(double* __restrict__ w0, double* __restrict__ w1,
                                             const double* __restrict__ Rg, int nb, std::int64_t n, Status* st,
                                             int skip_if_rank, int skip_if_notpd) {
     __shared__ double R[NBP * NBP];
+    constexpr int kTrsmRows = trsm_rows<NBP>();
+    __shared__ double xs[2][kTrsmRows * (NBP + 1)];
     __shared__ int skip;
+    const int ld = nb + 1;
     if (threadIdx.x == 0) {
         int sk = (skip_if_rank && st->rank_deficient) || (skip_if_notpd && st->not_pd);
         if (!sk) {  // trsm_right_inv's conditioning check (densela.hpp:129-136)
@@ -216,15 +287,23 @@ __global__ void __launch_bounds__(kT) k_trsm(double* __restrict__ w0, double* __
     for (int e = threadIdx.x; e < nb * nb; e += kT) R[e] = Rg[e];
     __syncthreads();
     if (skip) return;
-    for (std::int64_t r = blockIdx.x * static_cast<std::int64_t>(kT) + threadIdx.x; r < n;
-         r += static_cast<std::int64_t>(gridDim.x) * kT) {
-        for (int which = 0; which < 2; ++which) {
-            double* w = which == 0 ? w0 : w1;
-            if (!w) continue;
+    const int np = w1 ? 2 : 1;
+    for (std::int64_t r0 = static_cast<std::int64_t>(blockIdx.x) * kTrsmRows; r0 < n;
+         r0 += static_cast<std::int64_t>(gridDim.x) * kTrsmRows) {
+        const int rows = static_cast<int>(n - r0 < kTrsmRows ? n - r0 : kTrsmRows);
+        __syncthreads();
+        for (int q = 0; q < np; ++q) {
+            const double* src = (q == 0 ? w0 : w1) + r0 * nb;
+            for (int e = threadIdx.x; e < rows * nb; e += kT) xs[q][(e / nb) * ld + e % nb] = src[e];
+        }
+        __syncthreads();
+        const int q = threadIdx.x / kTrsmRows, rl = threadIdx.x % kTrsmRows;
+        if (q < np && rl < rows) {
+            double* xr = xs[q] + rl * ld;
             double x[NBP];
 #pragma unroll
             for (int j = 0; j < NBP; ++j)
-                if (j < nb) x[j] = w[r * nb + j];
+                if (j < nb) x[j] = xr[j];
 #pragma unroll
             for (int j = 0; j < NBP; ++j) {
                 if (j < nb) {
@@ -236,7 +315,12 @@ __global__ void __launch_bounds__(kT) k_trsm(double* __restrict__ w0, double* __
             }
 #pragma unroll
             for (int j = 0; j < NBP; ++j)
-                if (j < nb) w[r * nb + j] = x[j];
+                if (j < nb) xr[j] = x[j];
+        }
+        __syncthreads();
+        for (int qq = 0; qq < np; ++qq) {
+            double* dst = (qq == 0 ? w0 : w1) + r0 * nb;
+            for (int e = threadIdx.x; e < rows * nb; e += kT) dst[e] = xs[qq][(e / nb) * ld + e % nb];
         }
     }
 }
@@ -448,7 +532,7 @@ int grid_rows(Ctx* ctx, std::int64_t n, int per) {
 
 std::int64_t gram_partials_len(int nb, int npairs, int num_sms) {
     const int nblk = (nb + 3) / 4;
-    return static_cast<std::int64_t>(num_sms) * 2 * npairs * nblk * nblk * 16;
+    return static_cast<std::int64_t>(num_sms) * 6 * npairs * nblk * nblk * 16;
 }
 
 void gram(Ctx* ctx, const GramJob& job, std::int64_t n, double* partials, std::int64_t partials_len, cudaStream_t s) {
@@ -472,15 +556,18 @@ void gram(Ctx* ctx, const GramJob& job, std::int64_t n, double* partials, std::i
         o.out[p] = job.out[p];
         o.sym[p] = job.sym[p];
     }
-    int nparts = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 2, (n + 63) / 64)));
+    int nparts = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 6, (n + 255) / 256)));
     while (nparts > 1 && static_cast<std::int64_t>(nparts) * g.ncombo * 16 > partials_len) nparts /= 2;
-    const std::size_t sm = static_cast<std::size_t>(g.nd) * kGramRows * g.nblk * 4 * sizeof(double);
+    const int cpb = std::min(g.ncombo, kT);
+    const int rg = kT / cpb;
+    const std::size_t sm = std::max(static_cast<std::size_t>(g.nd) * kGramRows * g.nblk * 4,
+                                    static_cast<std::size_t>(rg) * cpb * 16) * sizeof(double);
     if (sm > 48 * 1024) BE_CUDA(cudaFuncSetAttribute(k_gram_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-    dim3 grid(nparts, (g.ncombo + kT - 1) / kT);
-    k_gram_partial<<<grid, kT, sm, s>>>(g, n, partials);
+    dim3 grid(nparts, (g.ncombo + cpb - 1) / cpb);
+    k_gram_partial<<<grid, kT, sm, s>>>(g, n, partials, cpb);
     BE_CUDA(cudaGetLastError());
     const int total = job.npairs * job.nb * job.nb;
-    k_gram_reduce<<<(total + 255) / 256, 256, 0, s>>>(g, o, nparts, partials);
+    k_gram_reduce<<<(total * 32 + 255) / 256, 256, 0, s>>>(g, o, nparts, partials);
     BE_CUDA(cudaGetLastError());
     ctx->launches += 2;
 }
@@ -512,20 +599,33 @@ void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
             O.sign[t] = J.term[t].neg ? -1.0 : 1.0;
         }
     }
+    MixSrc ms{};
+    for (int o = 0; o < m.nout; ++o)
+        for (int t = 0; t < m.out[o].nterms; ++t) {
+            int q = 0;
+            while (q < ms.nsrc && ms.src[q] != m.out[o].src[t]) ++q;
+            if (q == ms.nsrc) {
+                if (ms.nsrc == 6) fail(BE_ERR_BAD_PARAMS, "mix: more than 6 distinct sources");
+                ms.src[ms.nsrc++] = m.out[o].src[t];
+            }
+            m.out[o].si[t] = q;
+        }
     const int nblk = (job.nb + 3) / 4;
-    const std::size_t sm = static_cast<std::size_t>(m.ncoef) * job.nb * nblk * 4 * sizeof(double);
-    if (sm > 48 * 1024) BE_CUDA(cudaFuncSetAttribute(k_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-    const std::int64_t total = n * nblk;
-    const int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 8, (total + kT - 1) / kT)));
-    k_mix<<<grid, kT, sm, s>>>(m, n);
+    const std::size_t sm = (static_cast<std::size_t>(m.ncoef) * job.nb * nblk * 4 +
+                            static_cast<std::size_t>(ms.nsrc) * kMixRows * (job.nb + 1)) * sizeof(double);
+    BE_CUDA(cudaFuncSetAttribute(k_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    const int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 4, (n + kMixRows - 1) / kMixRows)));
+    k_mix<<<grid, kT, sm, s>>>(m, ms, nullptr, n);
     BE_CUDA(cudaGetLastError());
     ++ctx->launches;
 }
 
 void trsm(Ctx* ctx, double* w0, double* w1, const double* R, int nb, std::int64_t n, Status* st, int skip_if_rank,
           int skip_if_notpd, cudaStream_t s) {
-    const int grid = grid_rows(ctx, n, kT);
-#define BE_TRSM(NBP) k_trsm<NBP><<<grid, kT, 0, s>>>(w0, w1, R, nb, n, st, skip_if_rank, skip_if_notpd)
+#define BE_TRSM(NBP)                                                                                              \
+    k_trsm<NBP><<<static_cast<int>(std::max<std::int64_t>(                                                        \
+                      1, std::min<std::int64_t>(ctx->num_sms * 4, (n + trsm_rows<NBP>() - 1) / trsm_rows<NBP>()))), \
+                  kT, 0, s>>>(w0, w1, R, nb, n, st, skip_if_rank, skip_if_notpd)
     if (nb <= 8)
         BE_TRSM(8);
     else if (nb <= 16)

@@ -77,6 +77,7 @@ struct Op {
     DBuf<std::uint16_t> cperm;       // column-order -> row-order position in tile
     DBuf<double> diag;               // nrows (symmetric only)
     DBuf<int> counter;               // persistent-kernel tile counter [2]
+    DBuf<float> x32, y32;            // f32 staging of f64 panels (f32-values operator)
     std::vector<std::int64_t> csb_index;  // device order -> CSB index (small matrices only)
     int grid = 0;
     // timing

@@ -51,13 +51,13 @@ __global__ void __launch_bounds__(kPT) k_fom(const TileDev* __restrict__ tiles, 
                                              const std::uint16_t* __restrict__ cols, const double* __restrict__ vals,
                                              const double* __restrict__ shifts, const double* __restrict__ R,
                                              double* __restrict__ W, int nb, int m, int gc, int ngroups,
-                                             std::int64_t* fallbacks) {
+                                             std::int64_t* fallbacks, const std::int32_t* __restrict__ list) {
     extern __shared__ double sm[];
     __shared__ double red[kPT];
     __shared__ double s_dot[16], s_beta0[16], s_alpha[16][kMaxSteps], s_beta[16][kMaxSteps], s_y[16][kMaxSteps];
     __shared__ int s_steps[16], s_live[16], s_sing[16];
 
-    const int tile = blockIdx.x / ngroups;
+    const int tile = list ? list[blockIdx.x / ngroups] : static_cast<int>(blockIdx.x / ngroups);
     const int grp = blockIdx.x % ngroups;
     const TileDev td = tiles[tile];
     const int d = td.dim;
@@ -228,6 +228,237 @@ __global__ void __launch_bounds__(kPT) k_fom(const TileDev* __restrict__ tiles, 
     }
 }
 
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;  // butterfly: every lane holds the bitwise-identical total
+}
+
+// One thread group of G threads (a warp, or 4 warps) per (tile, column):
+// the m-step FOM of k_fom with the Krylov basis held in registers (each
+// thread owns rows tid, tid + G, ... up to RM rows) and only the current
+// basis vector in shared memory for the sparse gather. Reductions use warp
+// butterflies (+ a named barrier across the 4 warps when G = 128), all in a
+// fixed order.
+template <int G, int RM, int MC>
+__global__ void __launch_bounds__(256) k_fom_reg(const TileDev* __restrict__ tiles, const std::int32_t* __restrict__ list,
+                                                 int nlist, const std::int32_t* __restrict__ rowptr,
+                                                 const std::uint16_t* __restrict__ cols,
+                                                 const double* __restrict__ vals, const double* __restrict__ shifts,
+                                                 const double* __restrict__ R, double* __restrict__ W, int nb, int m,
+                                                 std::int64_t* fallbacks) {
+    constexpr int NG = 256 / G;  // items per CTA
+    constexpr int DMAX = G * RM;
+    __shared__ double s_vs[NG][DMAX];
+    __shared__ double s_red[NG][G / 32];
+    __shared__ double s_y[NG][MC];
+    __shared__ int s_sing[NG];
+    const int g = threadIdx.x / G, t = threadIdx.x % G, lane = threadIdx.x & 31, wg = t >> 5;
+    const long item = static_cast<long>(blockIdx.x) * NG + g;
+    if (item >= static_cast<long>(nlist) * nb) return;  // whole groups exit together
+    auto gsync = [&]() {
+        if constexpr (G == 32) {
+            __syncwarp();
+        } else {
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(G) : "memory");
+        }
+    };
+    auto gsum = [&](double v) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if constexpr (G == 32) {
+            return v;
+        } else {
+            if (lane == 0) s_red[g][wg] = v;
+            gsync();
+            double tot = 0.0;
+#pragma unroll
+            for (int q = 0; q < G / 32; ++q) tot += s_red[g][q];
+            gsync();
+            return tot;
+        }
+    };
+    const int col = static_cast<int>(item % nb);
+    const TileDev td = tiles[list[item / nb]];
+    const int d = td.dim;
+    const int cap = min(m, d);
+    const std::int32_t* rp = rowptr + td.ptr_off;
+    const std::uint16_t* cl = cols + td.ent_off;
+    const double* vl = vals + td.ent_off;
+    const double sigma = shifts[col];
+    const double* r = R + td.row_off * nb + col;
+    double* out = W + td.row_off * nb + col;
+    double* vs = s_vs[g];
+
+    double V[MC][RM], w[RM];
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < RM; ++k) {
+        const int i = t + k * G;
+        const double x = i < d ? r[static_cast<std::int64_t>(i) * nb] : 0.0;
+        V[0][k] = x;
+        acc += x * x;
+    }
+    const double beta0 = sqrt(gsum(acc));
+    if (beta0 == 0.0) {
+#pragma unroll
+        for (int k = 0; k < RM; ++k)
+            if (t + k * G < d) out[static_cast<std::int64_t>(t + k * G) * nb] = 0.0;
+        return;
+    }
+#pragma unroll
+    for (int k = 0; k < RM; ++k) V[0][k] /= beta0;
+    double alpha[MC], beta[MC];
+    int steps = cap;
+#pragma unroll
+    for (int s = 0; s < MC; ++s) {
+        if (s >= cap) break;
+        // w = (K - sigma I) V_s ; alpha_s = V_s . w
+#pragma unroll
+        for (int k = 0; k < RM; ++k)
+            if (t + k * G < d) vs[t + k * G] = V[s][k];
+        gsync();
+        acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < RM; ++k) {
+            const int i = t + k * G;
+            double yy = 0.0;
+            if (i < d) {
+                const int e1 = rp[i + 1] - 1;  // the diagonal slot is last
+                for (int e = rp[i]; e < e1; ++e) yy += vl[e] * vs[cl[e]];
+                yy += (vl[e1] - sigma) * V[s][k];
+            }
+            w[k] = yy;
+            acc += V[s][k] * yy;
+        }
+        const double a = gsum(acc);
+        alpha[s] = a;
+        if (s + 1 == cap) break;
+#pragma unroll
+        for (int k = 0; k < RM; ++k) {
+            double x = w[k] - a * V[s][k];
+            if (s > 0) x -= beta[s > 0 ? s - 1 : 0] * V[s > 0 ? s - 1 : 0][k];
+            w[k] = x;
+        }
+#pragma unroll
+        for (int q = 0; q < MC; ++q) {  // one reorthogonalisation pass, in order
+            if (q > s) break;
+            acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < RM; ++k) acc += V[q][k] * w[k];
+            const double pr = gsum(acc);
+#pragma unroll
+            for (int k = 0; k < RM; ++k) w[k] -= pr * V[q][k];
+        }
+        acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < RM; ++k) acc += w[k] * w[k];
+        const double nw = sqrt(gsum(acc));
+        if (nw < 1e-14 * beta0) {  // Krylov breakdown
+            steps = s + 1;
+            break;
+        }
+        beta[s] = nw;
+        if (s + 1 < MC) {
+#pragma unroll
+            for (int k = 0; k < RM; ++k) V[s + 1 < MC ? s + 1 : 0][k] = w[k] / nw;
+        }
+        gsync();  // vs is rewritten by the next step
+    }
+    if (t == 0) {  // T y = beta0 e1 by LU with partial pivoting (precond.hpp:208-249)
+        const int st = steps;
+        double T[MC][MC];
+        double tmax = 0.0;
+#pragma unroll
+        for (int i = 0; i < MC; ++i)
+#pragma unroll
+            for (int j = 0; j < MC; ++j) T[i][j] = 0.0;
+        double y[MC];
+#pragma unroll
+        for (int i = 0; i < MC; ++i) {
+            y[i] = 0.0;
+            if (i < st) {
+                T[i][i] = alpha[i];
+                tmax = fmax(tmax, fabs(alpha[i]));
+                if (i + 1 < st) {
+                    T[i][i + 1 < MC ? i + 1 : 0] = beta[i];
+                    T[i + 1 < MC ? i + 1 : 0][i] = beta[i];
+                    tmax = fmax(tmax, fabs(beta[i]));
+                }
+            }
+        }
+        const double floor = 1e-14 * fmax(1.0, tmax);
+        y[0] = beta0;
+        int sing = 0;
+#pragma unroll
+        for (int k = 0; k < MC; ++k) {
+            if (k >= st || sing) break;
+            int piv = k;
+#pragma unroll
+            for (int i = 0; i < MC; ++i)
+                if (i > k && i < st && fabs(T[i][k]) > fabs(T[piv][k])) piv = i;
+            if (fabs(T[piv][k]) < floor) {
+                sing = 1;
+                break;
+            }
+            if (piv != k) {
+#pragma unroll
+                for (int j = 0; j < MC; ++j) {
+                    const double tmp = T[k][j];
+                    T[k][j] = T[piv][j];
+                    T[piv][j] = tmp;
+                }
+                const double tmp = y[k];
+                y[k] = y[piv];
+                y[piv] = tmp;
+            }
+#pragma unroll
+            for (int i = 0; i < MC; ++i) {
+                if (i <= k || i >= st) continue;
+                const double f = T[i][k] / T[k][k];
+                if (f == 0.0) continue;
+#pragma unroll
+                for (int j = 0; j < MC; ++j)
+                    if (j >= k) T[i][j] -= f * T[k][j];
+                y[i] -= f * y[k];
+            }
+        }
+        if (!sing) {
+#pragma unroll
+            for (int i = MC - 1; i >= 0; --i) {
+                if (i >= st) continue;
+                double a2 = y[i];
+#pragma unroll
+                for (int j = 0; j < MC; ++j)
+                    if (j > i && j < st) a2 -= T[i][j] * y[j];
+                y[i] = a2 / T[i][i];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < MC; ++i) s_y[g][i] = y[i];
+        s_sing[g] = sing;
+        if (sing && fallbacks) atomicAdd(reinterpret_cast<unsigned long long*>(fallbacks), 1ull);
+    }
+    gsync();
+    const int sing = s_sing[g];
+#pragma unroll
+    for (int k = 0; k < RM; ++k) {
+        const int i = t + k * G;
+        if (i >= d) continue;
+        double o = 0.0;
+        if (sing) {
+            o = r[static_cast<std::int64_t>(i) * nb];  // unpreconditioned fallback column
+        } else {
+#pragma unroll
+            for (int j = 0; j < MC; ++j)
+                if (j < steps) o += s_y[g][j] * V[j][k];
+        }
+        out[static_cast<std::int64_t>(i) * nb] = o;
+    }
+}
+
+constexpr int kClassDims[] = {128, 512};  // warp (4 rows / lane), 4 warps (4 rows / thread)
+
 }  // namespace
 
 std::unique_ptr<Tiles> tiles_create(Ctx* ctx, const be_csb_view& L, const double* diag, const index_t* off,
@@ -327,6 +558,26 @@ std::unique_ptr<Tiles> tiles_create(Ctx* ctx, const be_csb_view& L, const double
     if (!rowptr.empty()) BE_CUDA(cudaMemcpy(t->rowptr.get(), rowptr.data(), rowptr.size() * 4, cudaMemcpyHostToDevice));
     if (!cols.empty()) BE_CUDA(cudaMemcpy(t->cols.get(), cols.data(), cols.size() * 2, cudaMemcpyHostToDevice));
     if (!vals.empty()) BE_CUDA(cudaMemcpy(t->vals.get(), vals.data(), vals.size() * 8, cudaMemcpyHostToDevice));
+    {  // size classes: warp kernel per class, CTA kernel above the last one
+        std::vector<std::int32_t> lists;
+        t->class_dim.assign(std::begin(kClassDims), std::end(kClassDims));
+        t->class_begin.clear();
+        int lo = 0;
+        for (int c = 0; c <= static_cast<int>(t->class_dim.size()); ++c) {
+            t->class_begin.push_back(static_cast<index_t>(lists.size()));
+            const int hi = c < static_cast<int>(t->class_dim.size()) ? t->class_dim[static_cast<std::size_t>(c)] : 1 << 30;
+            for (index_t j = 0; j < nt; ++j) {
+                const index_t dd = t->host[static_cast<std::size_t>(j)].dim;
+                if (dd > lo && dd <= hi) lists.push_back(static_cast<std::int32_t>(j));
+            }
+            lo = hi;
+        }
+        t->class_begin.push_back(static_cast<index_t>(lists.size()));
+        t->big_tiles = t->class_begin.back() - t->class_begin[t->class_dim.size()];
+        t->class_tiles.reset(std::max<index_t>(static_cast<index_t>(lists.size()), 1));
+        if (!lists.empty())
+            BE_CUDA(cudaMemcpy(t->class_tiles.get(), lists.data(), lists.size() * 4, cudaMemcpyHostToDevice));
+    }
     return t;
 }
 
@@ -337,6 +588,32 @@ void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, i
     if (nb < 1) fail(BE_ERR_DIMENSION_MISMATCH, "apply_preconditioner: one shift per column required");
     if (m > kMaxSteps) fail(BE_ERR_BAD_PARAMS, "apply_preconditioner: m above the device kernel's step cap (64)");
     if (t->ntiles == 0) return;
+    const auto* tdv = reinterpret_cast<const TileDev*>(t->tiles.get());
+    const int ncls = static_cast<int>(t->class_dim.size());
+    const bool reg_ok = m <= 8;
+    for (int c = 0; c < ncls && reg_ok; ++c) {
+        const index_t b0 = t->class_begin[static_cast<std::size_t>(c)], b1 = t->class_begin[static_cast<std::size_t>(c) + 1];
+        if (b1 == b0) continue;
+        const int dmax = t->class_dim[static_cast<std::size_t>(c)];
+        const index_t items = (b1 - b0) * nb;
+        const std::int32_t* list = t->class_tiles.get() + b0;
+        const int nl = static_cast<int>(b1 - b0);
+#define BE_FOMR(G, MC)                                                                                              \
+    k_fom_reg<G, 4, MC><<<static_cast<unsigned>((items + 256 / G - 1) / (256 / G)), 256, 0, s>>>(               \
+        tdv, list, nl, t->rowptr.get(), t->cols.get(), t->vals.get(), shifts, R, W, nb, m, fallbacks)
+        if (dmax <= 128) {
+            if (m <= 4) BE_FOMR(32, 4); else BE_FOMR(32, 8);
+        } else {
+            if (m <= 4) BE_FOMR(128, 4); else BE_FOMR(128, 8);
+        }
+#undef BE_FOMR
+        BE_CUDA(cudaGetLastError());
+        ++t->ctx->launches;
+    }
+    // everything the register kernel does not cover goes through the CTA kernel
+    const index_t big_begin = reg_ok ? t->class_begin[static_cast<std::size_t>(ncls)] : 0;
+    const index_t nbig = t->class_begin.back() - big_begin;
+    if (nbig == 0) return;
     const index_t cap = std::min<index_t>(m, t->max_dim);
     const std::size_t per_col = (static_cast<std::size_t>(cap + 1) * static_cast<std::size_t>(t->max_dim) +
                                  static_cast<std::size_t>(cap) * cap) * 8;
@@ -344,12 +621,12 @@ void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, i
     while (gc > 1 && (gc > nb * 2 || static_cast<std::size_t>(gc) * per_col > kSmemBudget)) gc /= 2;
     if (per_col > 200 * 1024) fail(BE_ERR_BAD_PARAMS, "apply_preconditioner: tile too large for the device kernel");
     const std::size_t sm = static_cast<std::size_t>(gc) * per_col;
-    if (sm > 48 * 1024) BE_CUDA(cudaFuncSetAttribute(k_fom, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    BE_CUDA(cudaFuncSetAttribute(k_fom, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));  // static smem counts too
     const int ngroups = (nb + gc - 1) / gc;
-    const index_t grid = t->ntiles * ngroups;
-    k_fom<<<static_cast<unsigned>(grid), kPT, sm, s>>>(reinterpret_cast<const TileDev*>(t->tiles.get()), t->rowptr.get(),
-                                                        t->cols.get(), t->vals.get(), shifts, R, W, nb, m, gc, ngroups,
-                                                        fallbacks);
+    const index_t grid = nbig * ngroups;
+    k_fom<<<static_cast<unsigned>(grid), kPT, sm, s>>>(tdv, t->rowptr.get(), t->cols.get(), t->vals.get(), shifts, R, W,
+                                                        nb, m, gc, ngroups, fallbacks,
+                                                        t->class_tiles.get() + big_begin);
     BE_CUDA(cudaGetLastError());
     ++t->ctx->launches;
 }

@@ -24,6 +24,12 @@ struct Tiles {
     std::vector<index_t> offsets;
     std::vector<HostTile> host;
     DBuf<unsigned char> tiles;  // TileDev records
+    // size classes for the warp-per-(tile, column) kernel: tiles with
+    // dim <= class_dim[c] (and > the previous class) listed in class_tiles
+    std::vector<int> class_dim;
+    std::vector<index_t> class_begin;  // into class_tiles, size = classes + 1
+    DBuf<std::int32_t> class_tiles;
+    index_t big_tiles = 0;             // tiles above the last class (CTA kernel)
     DBuf<std::int32_t> rowptr;
     DBuf<std::uint16_t> cols;
     DBuf<double> vals;

@@ -374,6 +374,32 @@ __global__ void k_diag_init(const double* __restrict__ d, const TX* __restrict__
     }
 }
 
+// f64 panel -> f32 copy for the tile kernel, and a zeroed f32 accumulator
+__global__ void k_f64_to_f32(const double* __restrict__ x, float* __restrict__ x32, std::int64_t nin,
+                             float* __restrict__ y32, std::int64_t nout) {
+    const std::int64_t total = nin > nout ? nin : nout;
+    for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        if (e < nin) x32[e] = static_cast<float>(x[e]);
+        if (e < nout) y32[e] = 0.f;
+    }
+}
+
+// Y = diag(D) X + Y32 (symmetric) or Y += Y32 (accumulate modes), in f64:
+// the diagonal pass of kernels.hpp:363-370 kept in full precision
+__global__ void k_finish_f64(const double* __restrict__ d, const double* __restrict__ X,
+                             const float* __restrict__ y32, double* __restrict__ Y, std::int64_t nrows, int nb,
+                             int symmetric) {
+    const std::int64_t total = nrows * nb;
+    for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        if (symmetric)
+            Y[e] = d[e / nb] * X[e] + static_cast<double>(y32[e]);
+        else
+            Y[e] += static_cast<double>(y32[e]);
+    }
+}
+
 template <int NBP, typename TC>
 std::size_t smem_bytes(int max_nnz) {
     using G = XGeom<NBP, TC>;
@@ -682,28 +708,53 @@ void op_apply(Op* op, const void* X, void* Y, index_t in_rows, int nb, int panel
             if (!e) BE_CUDA(cudaEventCreate(&e));
         BE_CUDA(cudaEventRecord(op->ev[0], s));
     }
-    if (mode == BE_APPLY_SYMMETRIC && out_rows > 0) {
-        const index_t total = out_rows * nb;
-        const int grid = static_cast<int>(std::min<index_t>((total + 255) / 256, op->ctx->num_sms * 8));
-        if (panel_prec == BE_F32)
-            k_diag_init<float><<<grid, 256, 0, s>>>(op->diag.get(), static_cast<const float*>(X), static_cast<float*>(Y), out_rows, nb);
-        else
-            k_diag_init<double><<<grid, 256, 0, s>>>(op->diag.get(), static_cast<const double*>(X), static_cast<double*>(Y), out_rows, nb);
+    const index_t in_tot = in_rows * nb, out_tot = out_rows * nb;
+    auto grid_for = [&](index_t total) {
+        return static_cast<int>(std::max<index_t>(1, std::min<index_t>((total + 255) / 256, op->ctx->num_sms * 8)));
+    };
+    if (panel_prec == BE_F64 && op->values_prec == BE_F32) {
+        // f32 SpMM on f64 panels: X -> f32 copy, tile kernel into a zeroed f32
+        // accumulator, then Y = D X + acc in f64 (halves the gathered and
+        // reduced vector bytes of the tile kernel)
+        const index_t need = std::max(in_tot, out_tot);
+        if (op->x32.n < need) {
+            op->x32.reset(need);
+            op->y32.reset(need);
+        }
+        k_f64_to_f32<<<grid_for(need), 256, 0, s>>>(static_cast<const double*>(X), op->x32.get(), in_tot,
+                                                       op->y32.get(), out_tot);
         BE_CUDA(cudaGetLastError());
         ++op->ctx->launches;
-    }
-    if (op->timing) BE_CUDA(cudaEventRecord(op->ev[1], s));
-    if (op->ntiles > 0) {
-        if (op->values_prec == BE_F32) {
+        if (op->timing) BE_CUDA(cudaEventRecord(op->ev[1], s));
+        if (op->ntiles > 0) dispatch_nb<float, float, float>(op, op->x32.get(), op->y32.get(), nb, do_r, do_c, s);
+        if (out_tot > 0) {
+            k_finish_f64<<<grid_for(out_tot), 256, 0, s>>>(op->diag.get(), static_cast<const double*>(X), op->y32.get(),
+                                                            static_cast<double*>(Y), out_rows, nb,
+                                                            mode == BE_APPLY_SYMMETRIC ? 1 : 0);
+            BE_CUDA(cudaGetLastError());
+            ++op->ctx->launches;
+        }
+    } else {
+        if (mode == BE_APPLY_SYMMETRIC && out_rows > 0) {
             if (panel_prec == BE_F32)
+                k_diag_init<float><<<grid_for(out_tot), 256, 0, s>>>(op->diag.get(), static_cast<const float*>(X),
+                                                                     static_cast<float*>(Y), out_rows, nb);
+            else
+                k_diag_init<double><<<grid_for(out_tot), 256, 0, s>>>(op->diag.get(), static_cast<const double*>(X),
+                                                                      static_cast<double*>(Y), out_rows, nb);
+            BE_CUDA(cudaGetLastError());
+            ++op->ctx->launches;
+        }
+        if (op->timing) BE_CUDA(cudaEventRecord(op->ev[1], s));
+        if (op->ntiles > 0) {
+            if (op->values_prec == BE_F32) {
                 dispatch_nb<float, float, float>(op, static_cast<const float*>(X), static_cast<float*>(Y), nb, do_r, do_c, s);
-            else
-                dispatch_nb<float, float, double>(op, static_cast<const double*>(X), static_cast<double*>(Y), nb, do_r, do_c, s);
-        } else {
-            if (panel_prec == BE_F32)
-                dispatch_nb<double, double, float>(op, static_cast<const float*>(X), static_cast<float*>(Y), nb, do_r, do_c, s);
-            else
-                dispatch_nb<double, double, double>(op, static_cast<const double*>(X), static_cast<double*>(Y), nb, do_r, do_c, s);
+            } else {
+                if (panel_prec == BE_F32)
+                    dispatch_nb<double, double, float>(op, static_cast<const float*>(X), static_cast<float*>(Y), nb, do_r, do_c, s);
+                else
+                    dispatch_nb<double, double, double>(op, static_cast<const double*>(X), static_cast<double*>(Y), nb, do_r, do_c, s);
+            }
         }
     }
     if (op->timing) {
