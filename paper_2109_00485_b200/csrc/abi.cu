@@ -285,7 +285,9 @@ be_status be_op_decode(be_op* op, int64_t* rows, int64_t* cols, double* values, 
         std::vector<std::uint16_t> rc(static_cast<std::size_t>(o->padded)), cp(static_cast<std::size_t>(o->padded));
         const std::size_t vsz = o->values_prec == BE_F32 ? 4 : 8;
         std::vector<unsigned char> v(static_cast<std::size_t>(o->padded) * vsz);
+        std::vector<unsigned char> lens(static_cast<std::size_t>(o->ntiles) * 256);
         if (o->ntiles > 0) {
+            BE_CUDA(cudaMemcpy(lens.data(), o->lens.get(), lens.size(), cudaMemcpyDeviceToHost));
             BE_CUDA(cudaMemcpy(h.data(), o->tiles.get(), h.size() * sizeof(be::TileHdr), cudaMemcpyDeviceToHost));
             BE_CUDA(cudaMemcpy(rc.data(), o->rc.get(), rc.size() * 2, cudaMemcpyDeviceToHost));
             BE_CUDA(cudaMemcpy(cp.data(), o->cperm.get(), cp.size() * 2, cudaMemcpyDeviceToHost));
@@ -297,25 +299,35 @@ be_status be_op_decode(be_op* op, int64_t* rows, int64_t* cols, double* values, 
             const int nnz = static_cast<int>(t.packed >> 14);
             const int nr = static_cast<int>(t.packed & 127u) + 1;
             const int nc = static_cast<int>((t.packed >> 7) & 127u) + 1;
-            // rows and (through cperm) columns must each form one contiguous
-            // group; cperm must be a permutation of the tile's entries
-            std::vector<char> seen(static_cast<std::size_t>(nnz), 0), rdone(256, 0), cdone(256, 0);
-            int prev_r = -1, prev_c = -1;
-            for (int k = 0; k < nnz; ++k) {
-                const int q = cp[static_cast<std::size_t>(b + k)];
-                if (q >= nnz || seen[static_cast<std::size_t>(q)]) be::fail(BE_ERR_GENERIC, "decode: bad column permutation");
-                seen[static_cast<std::size_t>(q)] = 1;
-                const int c = rc[static_cast<std::size_t>(b + q)] & 255;
-                const int r = rc[static_cast<std::size_t>(b + k)] >> 8;
-                if (c != prev_c) {
-                    if (cdone[static_cast<std::size_t>(c)]) be::fail(BE_ERR_GENERIC, "decode: column order split");
-                    cdone[static_cast<std::size_t>(c)] = 1;
-                    prev_c = c;
+            // JDS layout: row rank r's j-th entry sits at jd[j] + r and column
+            // rank c's j-th entry at cperm[cjd[j] + c]; every rank must map to
+            // one row (column) and cperm must be a permutation of the entries
+            const unsigned char* ln = lens.data() + static_cast<std::size_t>(&t - h.data()) * 256;
+            std::vector<char> seen(static_cast<std::size_t>(nnz), 0);
+            for (int g = 0; g < 2; ++g) {
+                int sum = 0, start = 0;
+                for (int i = 0; i < 128; ++i) {
+                    if (i > 0 && ln[g * 128 + i] > ln[g * 128 + i - 1]) be::fail(BE_ERR_GENERIC, "decode: lengths not in rank order");
+                    sum += ln[g * 128 + i];
                 }
-                if (r != prev_r) {
-                    if (rdone[static_cast<std::size_t>(r)]) be::fail(BE_ERR_GENERIC, "decode: row order split");
-                    rdone[static_cast<std::size_t>(r)] = 1;
-                    prev_r = r;
+                if (sum != nnz) be::fail(BE_ERR_GENERIC, "decode: lengths do not sum to the tile size");
+                std::vector<int> who(128, -1);
+                for (int j = 0; j < ln[g * 128]; ++j) {
+                    int cnt = 0;
+                    while (cnt < 128 && ln[g * 128 + cnt] > j) ++cnt;
+                    for (int r = 0; r < cnt; ++r) {
+                        int q = start + r;
+                        if (g == 1) {
+                            q = cp[static_cast<std::size_t>(b + q)];
+                            if (q >= nnz || seen[static_cast<std::size_t>(q)]) be::fail(BE_ERR_GENERIC, "decode: bad column permutation");
+                            seen[static_cast<std::size_t>(q)] = 1;
+                        }
+                        const std::uint16_t x = rc[static_cast<std::size_t>(b + q)];
+                        const int id = g == 0 ? (x >> 8) : (x & 255);
+                        if (who[static_cast<std::size_t>(r)] < 0) who[static_cast<std::size_t>(r)] = id;
+                        if (who[static_cast<std::size_t>(r)] != id) be::fail(BE_ERR_GENERIC, g == 0 ? "decode: row order split" : "decode: column order split");
+                    }
+                    start += cnt;
                 }
             }
             for (int k = 0; k < nnz; ++k) {

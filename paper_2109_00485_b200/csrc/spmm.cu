@@ -191,50 +191,98 @@ __device__ __forceinline__ void stage_x(unsigned char* xs, const TX* __restrict_
     }
 }
 
-template <int NBP, typename TC>
-__device__ __forceinline__ std::uint32_t pack_off(std::uint32_t rc) {
-    using G = XGeom<NBP, TC>;
-    return ((rc & 255u) * G::LINEB) | (((rc >> 8) * G::LINEB) << 16);
+// cp.async 16-byte global -> shared copy (LDGSTS), and its group fences
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-constexpr int kEPT = 8;  // entries per thread per staging round (max_nnz <= 2048)
-
-// Gather-accumulate one segment of entries into the CH register chunks.
-// Lane L keeps accumulator chunk i for output chunk (i + L) % CH.
-template <int NBP, typename TC, bool HI>
-__device__ __forceinline__ void segment(const Meta<TC>* __restrict__ m, int k, int k1, const unsigned char* xbase,
-                                        typename Vec<TC>::T (&acc)[XGeom<NBP, TC>::CH], int lane) {
-    using G = XGeom<NBP, TC>;
-    using V = typename Vec<TC>::T;
-    const unsigned char* xb = xbase + ((lane / G::CH) % G::REP) * G::RB;
-    int coff[G::CH];
-#pragma unroll
-    for (int i = 0; i < G::CH; ++i) coff[i] = ((i + lane) % G::CH) * 16;
-    constexpr bool kPair = G::CH <= 4;  // two entries in flight unless the row is wide
-    for (; kPair && k + 1 < k1; k += 2) {
-        const Meta<TC> m0 = m[k], m1 = m[k + 1];
-        const unsigned char* p0 = xb + (HI ? (m0.off >> 16) : (m0.off & 0xFFFFu));
-        const unsigned char* p1 = xb + (HI ? (m1.off >> 16) : (m1.off & 0xFFFFu));
-        V x0[G::CH], x1[G::CH];
-#pragma unroll
-        for (int i = 0; i < G::CH; ++i) x0[i] = *reinterpret_cast<const V*>(p0 + coff[i]);
-#pragma unroll
-        for (int i = 0; i < G::CH; ++i) x1[i] = *reinterpret_cast<const V*>(p1 + coff[i]);
-#pragma unroll
-        for (int i = 0; i < G::CH; ++i) vfma(acc[i], m0.v, x0[i]);
-#pragma unroll
-        for (int i = 0; i < G::CH; ++i) vfma(acc[i], m1.v, x1[i]);
-    }
-    for (; k < k1; ++k) {
-        const Meta<TC> m0 = m[k];
-        const unsigned char* p0 = xb + (HI ? (m0.off >> 16) : (m0.off & 0xFFFFu));
-#pragma unroll
-        for (int i = 0; i < G::CH; ++i) vfma(acc[i], m0.v, *reinterpret_cast<const V*>(p0 + coff[i]));
-    }
-}
-
+// Raw per-tile staging area (one of two pipeline stages): the entry stream
+// in JDS order, the column permutation, the X_J rows and the rank lengths.
 template <int NBP, typename TC, typename TV, typename TX>
-__global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? 3 : 2)
+struct Stage {
+    // raw X_J rows (staged asynchronously when small; else loaded directly)
+    static constexpr int XRAW = kTile * NBP * static_cast<int>(sizeof(TX));
+    static constexpr int XB = XRAW <= 16384 ? XRAW : 0;
+    __host__ __device__ static std::size_t bytes(int max_nnz) {
+        return static_cast<std::size_t>(max_nnz) * (sizeof(TV) + 4) + XB + 256;
+    }
+};
+
+// Issue the asynchronous copies of one tile into a stage buffer.
+template <int NBP, typename TC, typename TV, typename TX>
+__device__ __forceinline__ void stage_issue(unsigned char* st, int max_nnz, const TileHdr& h, int t,
+                                            const unsigned char* __restrict__ lens, const TV* __restrict__ vals,
+                                            const std::uint16_t* __restrict__ rc,
+                                            const std::uint16_t* __restrict__ cperm, const TX* __restrict__ X,
+                                            int nb, bool do_r, bool do_c, bool xvec) {
+    const std::int64_t b = static_cast<std::int64_t>(h.begin8) * 8;
+    const int nnz = static_cast<int>(h.packed >> 14);
+    const int nc = static_cast<int>((h.packed >> 7) & 127u) + 1;
+    const int npad = (nnz + 7) & ~7;
+    TV* sv = reinterpret_cast<TV*>(st);
+    std::uint16_t* src = reinterpret_cast<std::uint16_t*>(sv + max_nnz);
+    std::uint16_t* scp = src + max_nnz;
+    unsigned char* sx = reinterpret_cast<unsigned char*>(scp + max_nnz);
+    unsigned char* sl = sx + Stage<NBP, TC, TV, TX>::XB;
+    const int cv = npad * static_cast<int>(sizeof(TV)) / 16, cr = npad * 2 / 16;
+    const int cx = (do_r && xvec) ? nc * nb * static_cast<int>(sizeof(TX)) / 16 : 0;
+    const int total = cv + cr + (do_c ? cr : 0) + cx + 16;
+    const unsigned char* gx = reinterpret_cast<const unsigned char*>(X + static_cast<std::int64_t>(h.col0) * nb);
+    for (int c = threadIdx.x; c < total; c += kThreads) {
+        int q = c;
+        if (q < cv) { cp16(reinterpret_cast<unsigned char*>(sv) + 16 * q, reinterpret_cast<const unsigned char*>(vals + b) + 16 * q); continue; }
+        q -= cv;
+        if (q < cr) { cp16(reinterpret_cast<unsigned char*>(src) + 16 * q, reinterpret_cast<const unsigned char*>(rc + b) + 16 * q); continue; }
+        q -= cr;
+        if (do_c) {
+            if (q < cr) { cp16(reinterpret_cast<unsigned char*>(scp) + 16 * q, reinterpret_cast<const unsigned char*>(cperm + b) + 16 * q); continue; }
+            q -= cr;
+        }
+        if (q < cx) { cp16(sx + 16 * q, gx + 16 * q); continue; }
+        q -= cx;
+        cp16(sl + 16 * q, lens + static_cast<std::int64_t>(t) * 256 + 16 * q);
+    }
+}
+
+// JDS starts: for the 128 ranks of one group (rows or columns) with lengths
+// sorted in decreasing order, jd[j] = sum_r min(len_r, j) for j in [0, 128].
+// Threads 0-127 build the row table, 128-255 the column table.
+__device__ __forceinline__ void jds_starts(const unsigned char* sl, std::uint16_t* jd_r, std::uint16_t* jd_c,
+                                           int* s_tot) {
+    const int tid = threadIdx.x, grp = tid >> 7, j = tid & 127, lane = tid & 31, warp = tid >> 5;
+    const unsigned char* len = sl + grp * 128;
+    int lo = 0, hi = 128;  // count_j = #ranks with len > j (lengths are non-increasing)
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (len[mid] > j) lo = mid + 1; else hi = mid;
+    }
+    const int cnt = lo;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_tot[warp] = incl;
+    __syncthreads();
+    int start = incl - cnt;
+    for (int w = grp * 4; w < warp; ++w) start += s_tot[w];
+    std::uint16_t* jd = grp == 0 ? jd_r : jd_c;
+    jd[j] = static_cast<std::uint16_t>(start);
+    if (j == 127) jd[128] = static_cast<std::uint16_t>(start + cnt);
+}
+
+// One work item = a run of consecutive tiles of the same 128-row tile-row.
+// Per run the X_I slice is staged once (replicated lines) and Y_I rows
+// accumulate in shared memory; per tile, the raw stream of tile t + 1 is
+// copied with cp.async while tile t is computed. Pass R (warps 0-3): lane =
+// row rank, walks its row through the JDS table; pass C (warps 4-7): lane =
+// column rank, walks its column through cperm. Y_J is flushed per tile.
+template <int NBP, typename TC, typename TV, typename TX>
+__global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? 2 : 1)
     k_sym_spmm(const int2* __restrict__ runs, int nruns, const TileHdr* __restrict__ tiles,
                const unsigned char* __restrict__ lens, const TV* __restrict__ vals,
                const std::uint16_t* __restrict__ rc, const std::uint16_t* __restrict__ cperm,
@@ -242,19 +290,28 @@ __global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? 3 :
                int* __restrict__ ctr) {
     using G = XGeom<NBP, TC>;
     using V = typename Vec<TC>::T;
+    using S = Stage<NBP, TC, TV, TX>;
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned char* xi = smem;
     unsigned char* xj = xi + kTile * G::LINEB;
     V* yi = reinterpret_cast<V*>(xj + kTile * G::LINEB);  // kTile x CH chunks: the run's Y_I rows
-    Meta<TC>* meta = reinterpret_cast<Meta<TC>*>(yi + kTile * G::CH);
-    Meta<TC>* cmeta = meta + max_nnz;
+    unsigned char* stg0 = reinterpret_cast<unsigned char*>(yi + kTile * G::CH);
+    const std::size_t sbytes = (S::bytes(max_nnz) + 15) & ~static_cast<std::size_t>(15);
+    __shared__ std::uint16_t s_jd[2][129];
     __shared__ int s_run;
     __shared__ int s_tot[8];
 
     const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
+    const int lane = tid & 31;
     const int grp = tid >> 7;  // 0: pass R (row ranks), 1: pass C (column ranks)
+    const int rank = tid & 127;
     const bool vec_ok = (nb % G::VEC) == 0;
+    const bool xvec = S::XB > 0 && nb == NBP && (NBP * sizeof(TX)) % 16 == 0 &&
+                      (reinterpret_cast<std::uintptr_t>(X) & 15u) == 0;
+    const unsigned char* xbase = (grp == 0 ? xj : xi) + ((lane / G::CH) % G::REP) * G::RB;
+    int coff[G::CH];
+#pragma unroll
+    for (int i = 0; i < G::CH; ++i) coff[i] = ((i + lane) % G::CH) * 16;
 
     if (tid == 0) s_run = atomicAdd(ctr, 1);
     __syncthreads();
@@ -264,73 +321,70 @@ __global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? 3 :
         TileHdr h = tiles[rg.x];
         const int row0 = h.row0;
         const int nr = static_cast<int>(h.packed & 127u) + 1;
+        stage_issue<NBP, TC, TV, TX>(stg0, max_nnz, h, rg.x, lens, vals, rc, cperm, X, nb, do_r, do_c, xvec);
+        cp_commit();
         if (do_c) stage_x<NBP, TC, TX>(xi, X, row0, nr, nb);
         if (do_r)
             for (int e = tid; e < kTile * G::CH; e += kThreads) vzero(yi[e]);
         for (int t = rg.x; t < rg.y; ++t) {
-            const std::int64_t b = static_cast<std::int64_t>(h.begin8) * 8;
+            unsigned char* st = stg0 + ((t - rg.x) & 1) * sbytes;
             const int nc = static_cast<int>((h.packed >> 7) & 127u) + 1;
-            const int nnz = static_cast<int>(h.packed >> 14);
             const int col0 = h.col0;
-            // lengths (rank order) -> exclusive starts via warp scans
-            const int len = __ldg(lens + static_cast<std::int64_t>(t) * 256 + tid);
-            int incl = len;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
+            cp_wait_all();
+            __syncthreads();  // stage t complete and visible; stage t+1's buffer is free
+            if (t + 1 < rg.y) {
+                h = tiles[t + 1];
+                stage_issue<NBP, TC, TV, TX>(stg0 + ((t + 1 - rg.x) & 1) * sbytes, max_nnz, h, t + 1, lens, vals, rc,
+                                             cperm, X, nb, do_r, do_c, xvec);
             }
-            if (lane == 31) s_tot[warp] = incl;
-            // entry stream: coalesced, k = tid + j * kThreads
-            TV v[kEPT];
-            std::uint16_t r[kEPT], cp[kEPT];
+            cp_commit();
+            if (t == rg.y - 1 && tid == 0) s_run = atomicAdd(ctr, 1);  // next run
+            const TV* sv = reinterpret_cast<const TV*>(st);
+            const std::uint16_t* src = reinterpret_cast<const std::uint16_t*>(sv + max_nnz);
+            const std::uint16_t* scp = src + max_nnz;
+            const unsigned char* sx = reinterpret_cast<const unsigned char*>(scp + max_nnz);
+            const unsigned char* sl = sx + S::XB;
+            if (do_r) {  // X_J lines from the raw rows
+                if (xvec) {
+                    for (int e = tid; e < nc * NBP; e += kThreads) {
+                        const int r = e / NBP, v = e % NBP;
+                        const TC x = static_cast<TC>(reinterpret_cast<const TX*>(sx)[e]);
+                        TC* line = reinterpret_cast<TC*>(xj + r * G::LINEB);
 #pragma unroll
-            for (int j = 0; j < kEPT; ++j) {
-                const int k = tid + j * kThreads;
-                if (k < nnz) {
-                    v[j] = __ldg(vals + b + k);
-                    r[j] = __ldg(rc + b + k);
-                    if (do_c) cp[j] = __ldg(cperm + b + k);
+                        for (int q = 0; q < G::REP; ++q) line[q * NBP + v] = x;
+                    }
+                } else {
+                    stage_x<NBP, TC, TX>(xj, X, col0, nc, nb);
                 }
             }
-            if (do_r) stage_x<NBP, TC, TX>(xj, X, col0, nc, nb);
-#pragma unroll
-            for (int j = 0; j < kEPT; ++j) {
-                const int k = tid + j * kThreads;
-                if (k < nnz) {
-                    Meta<TC> m;
-                    m.v = static_cast<TC>(v[j]);
-                    m.off = pack_off<NBP, TC>(r[j]);
-                    meta[k] = m;
-                }
-            }
-            if (t + 1 < rg.y) h = tiles[t + 1];  // prefetch the next header
-            if (t == rg.y - 1 && tid == 0) s_run = atomicAdd(ctr, 1);  // and the next run
+            jds_starts(sl, s_jd[0], s_jd[1], s_tot);
             __syncthreads();
-            int start = incl - len;
-            for (int w = grp * 4; w < warp; ++w) start += s_tot[w];
-            if (do_c) {  // column order for pass C
-#pragma unroll
-                for (int j = 0; j < kEPT; ++j) {
-                    const int k = tid + j * kThreads;
-                    if (k < nnz) cmeta[k] = meta[cp[j]];
-                }
-                __syncthreads();
-            }
+            const int len = sl[tid];
             if (len > 0 && (grp == 0 ? do_r : do_c)) {
+                const std::uint16_t* jd = s_jd[grp];
                 V acc[G::CH];
 #pragma unroll
                 for (int i = 0; i < G::CH; ++i) vzero(acc[i]);
-                if (grp == 0) {  // Y_I += A X_J for the row of this rank
-                    segment<NBP, TC, false>(meta, start, start + len, xj, acc, lane);
-                    const int row = static_cast<int>((meta[start].off >> 16) / G::LINEB);
-                    V* y = yi + row * G::CH;
+                int first = 0;
+                for (int j = 0; j < len; ++j) {
+                    int pos = jd[j] + rank;
+                    if (grp == 1) pos = scp[pos];
+                    const TC v = static_cast<TC>(sv[pos]);
+                    const std::uint32_t x = src[pos];
+                    if (j == 0) first = x;
+                    const unsigned char* p = xbase + (grp == 0 ? (x & 255u) : (x >> 8)) * G::LINEB;
+                    V xv[G::CH];
+#pragma unroll
+                    for (int i = 0; i < G::CH; ++i) xv[i] = *reinterpret_cast<const V*>(p + coff[i]);
+#pragma unroll
+                    for (int i = 0; i < G::CH; ++i) vfma(acc[i], v, xv[i]);
+                }
+                if (grp == 0) {  // Y_I += A X_J for this row
+                    V* y = yi + (first >> 8) * G::CH;
 #pragma unroll
                     for (int i = 0; i < G::CH; ++i) vadd(y[(i + lane) % G::CH], acc[i]);
-                } else {  // Y_J += A^T X_I for the column of this rank
-                    segment<NBP, TC, true>(cmeta, start, start + len, xi, acc, lane);
-                    const int col = static_cast<int>((cmeta[start].off & 0xFFFFu) / G::LINEB);
-                    TX* y = Y + static_cast<std::int64_t>(col0 + col) * nb;
+                } else {  // Y_J += A^T X_I for this column
+                    TX* y = Y + static_cast<std::int64_t>(col0 + (first & 255)) * nb;
 #pragma unroll
                     for (int i = 0; i < G::CH; ++i) {
                         const int c0 = ((i + lane) % G::CH) * G::VEC;
@@ -338,8 +392,9 @@ __global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? 3 :
                     }
                 }
             }
-            __syncthreads();
         }
+        cp_wait_all();
+        __syncthreads();
         if (do_r) {  // flush the run's rows (all-zero chunks carry no update)
             for (int e = tid; e < nr * G::CH; e += kThreads) {
                 const int row = e / G::CH, c0 = (e % G::CH) * G::VEC;
@@ -400,16 +455,17 @@ __global__ void k_finish_f64(const double* __restrict__ d, const double* __restr
     }
 }
 
-template <int NBP, typename TC>
+template <int NBP, typename TC, typename TV, typename TX>
 std::size_t smem_bytes(int max_nnz) {
     using G = XGeom<NBP, TC>;
-    return 2 * kTile * G::LINEB + kTile * G::CH * 16 + 2 * static_cast<std::size_t>(max_nnz) * sizeof(Meta<TC>);
+    const std::size_t sb = (Stage<NBP, TC, TV, TX>::bytes(max_nnz) + 15) & ~static_cast<std::size_t>(15);
+    return 2 * kTile * G::LINEB + kTile * G::CH * 16 + 2 * sb;
 }
 
 template <int NBP, typename TC, typename TV, typename TX>
 void launch_tiles(Op* op, const TX* X, TX* Y, int nb, int do_r, int do_c, cudaStream_t s) {
     auto kern = k_sym_spmm<NBP, TC, TV, TX>;
-    const std::size_t sm = smem_bytes<NBP, TC>(op->max_nnz);
+    const std::size_t sm = smem_bytes<NBP, TC, TV, TX>(op->max_nnz);
     static std::size_t cached_sm = 0;
     static int per_sm = 0;
     if (cached_sm != sm) {
@@ -451,6 +507,11 @@ struct RowOut {
     std::vector<std::int64_t> src;    // CSB index per device entry (optional)
 };
 
+std::vector<std::uint16_t>& tls_colpos() {
+    thread_local std::vector<std::uint16_t> v;
+    return v;
+}
+
 // Emit one tile piece from `ent` = (local row << 56 | local col << 48 | CSB
 // index), sorted by (row, col, index).
 void emit_piece(const be_csb_view& L, const std::vector<std::uint64_t>& ent, index_t row0, index_t col0, index_t nr,
@@ -471,12 +532,26 @@ void emit_piece(const be_csb_view& L, const std::vector<std::uint64_t>& ent, ind
         rrank[rorder[i]] = i;
         crank[corder[i]] = i;
     }
-    std::vector<std::uint64_t> ord(n);
-    for (std::size_t i = 0; i < n; ++i) {
-        const std::uint64_t r = ent[i] >> 56, c = (ent[i] >> 48) & 255u;
-        ord[i] = (static_cast<std::uint64_t>(rrank[r]) << 56) | (c << 48) | (ent[i] & 0xFFFFFFFFFFFFULL);
+    // row-JDS order: diagonal j holds the j-th entry (by column) of every row
+    // rank with more than j entries; jd[j] = sum_r min(len_r, j)
+    int rstart[kTile + 1], cstart[kTile + 1];  // ent is (row, col)-sorted: rows are contiguous
+    rstart[0] = cstart[0] = 0;
+    for (int i = 0; i < kTile; ++i) {
+        rstart[i + 1] = rstart[i] + rlen[i];
+        cstart[i + 1] = cstart[i] + clen[corder[i]];  // by column rank
     }
-    std::sort(ord.begin(), ord.end());
+    const int rmax = rlen[rorder[0]], cmax = clen[corder[0]];
+    std::vector<int> jd(static_cast<std::size_t>(rmax) + 1, 0), cjd(static_cast<std::size_t>(cmax) + 1, 0);
+    for (int j = 0; j < rmax; ++j) {
+        int cnt = 0;
+        while (cnt < kTile && rlen[rorder[cnt]] > j) ++cnt;
+        jd[static_cast<std::size_t>(j) + 1] = jd[static_cast<std::size_t>(j)] + cnt;
+    }
+    for (int j = 0; j < cmax; ++j) {
+        int cnt = 0;
+        while (cnt < kTile && clen[corder[cnt]] > j) ++cnt;
+        cjd[static_cast<std::size_t>(j) + 1] = cjd[static_cast<std::size_t>(j)] + cnt;
+    }
     TileHdr hd{};
     hd.begin8 = static_cast<std::uint32_t>(pos / 8);
     hd.row0 = static_cast<std::int32_t>(row0);
@@ -486,18 +561,34 @@ void emit_piece(const be_csb_view& L, const std::vector<std::uint64_t>& ent, ind
     out.hdr.push_back(hd);
     for (int i = 0; i < kTile; ++i) out.lens.push_back(static_cast<unsigned char>(rlen[rorder[i]]));
     for (int i = 0; i < kTile; ++i) out.lens.push_back(static_cast<unsigned char>(clen[corder[i]]));
-    std::vector<std::uint64_t> ck(n);
-    for (std::size_t i = 0; i < n; ++i) {
-        const index_t k = static_cast<index_t>(ord[i] & 0xFFFFFFFFFFFFULL);
-        const std::uint64_t r = static_cast<std::uint64_t>(rorder[ord[i] >> 56]);
-        const std::uint64_t c = (ord[i] >> 48) & 255u;
-        out.v.push_back(L.values[k]);
-        out.rc.push_back(static_cast<std::uint16_t>((r << 8) | c));
-        if (keep_src) out.src.push_back(k);
-        ck[i] = (static_cast<std::uint64_t>(crank[c]) << 40) | (r << 32) | static_cast<std::uint64_t>(i);
+    const std::size_t base = out.v.size();
+    out.v.resize(base + n);
+    out.rc.resize(base + n);
+    out.cp.resize(base + n);
+    if (keep_src) out.src.resize(base + n);
+    std::vector<std::uint16_t>& colpos = tls_colpos();
+    colpos.resize(n);
+    int ccur[kTile];
+    std::copy(cstart, cstart + kTile, ccur);
+    for (int r = 0; r < kTile; ++r) {
+        const int row = rorder[r];
+        for (int j = 0; j < rlen[row]; ++j) {
+            const std::uint64_t e = ent[static_cast<std::size_t>(rstart[row] + j)];
+            const int q = jd[static_cast<std::size_t>(j)] + r;
+            const index_t k = static_cast<index_t>(e & 0xFFFFFFFFFFFFULL);
+            out.v[base + static_cast<std::size_t>(q)] = L.values[k];
+            out.rc[base + static_cast<std::size_t>(q)] = static_cast<std::uint16_t>(((e >> 56) << 8) | ((e >> 48) & 255u));
+            if (keep_src) out.src[base + static_cast<std::size_t>(q)] = k;
+            // column lists in (column rank, row rank) order
+            colpos[static_cast<std::size_t>(ccur[crank[(e >> 48) & 255u]]++)] = static_cast<std::uint16_t>(q);
+        }
     }
-    std::sort(ck.begin(), ck.end());
-    for (std::uint64_t x : ck) out.cp.push_back(static_cast<std::uint16_t>(x & 0xFFFFFFFFu));
+    // column-JDS order through cperm: cperm[cjd[j] + c] = row-JDS position of
+    // the j-th entry of column rank c
+    for (int c = 0; c < kTile; ++c)
+        for (int j = 0; j < cstart[c + 1] - cstart[c]; ++j)
+            out.cp[base + static_cast<std::size_t>(cjd[static_cast<std::size_t>(j)] + c)] =
+                colpos[static_cast<std::size_t>(cstart[c] + j)];
     pos += static_cast<index_t>(n);
     while (pos % 8) {  // pad the segment to 8 entries
         out.v.push_back(0.0);
