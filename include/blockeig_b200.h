@@ -2,13 +2,13 @@
  * blockeig_b200.h -- C ABI of the B200-native LOBPCG hot path.
  *
  * This is the drop-in boundary for the reference library `blockeig`
- * (/root/reference/proj/include/blockeig/*.hpp). Every entry point below is
+ * (/root/reference/proj/include/blockeig/ headers). Every entry point below is
  * plain C: opaque handles, raw pointers and sizes, no C++ or torch types.
  * Each one names the reference interface it replaces (file:line relative to
  * /root/reference/proj/include/blockeig/). The C++ mirror of the reference API
- * (namespace blockeig, paper_2109_00485_b200/cpp/blockeig/*.hpp) is a thin
- * header-only layer over these functions and re-throws the reference's typed
- * exceptions from the status codes.
+ * (namespace blockeig, include/blockeig_b200.hpp) is a thin header-only layer
+ * over these functions and re-throws the reference's typed exceptions from
+ * the status codes.
  *
  * Conventions
  *   - Every function returns be_status; BE_OK == 0. On failure the message is

@@ -1,0 +1,733 @@
+// blockeig_b200.hpp -- C++ mirror of the reference blockeig API over the C ABI.
+//
+// A program written against the reference headers
+// (/root/reference/proj/include/blockeig/{errors,block_vector,csb,kernels,
+// precond,lobpcg,synth}.hpp) compiles against this one header and runs the
+// hot path on the B200: the same namespace, type names, members, function
+// signatures, argument meaning and exception types. Everything here is a thin
+// host layer over include/blockeig_b200.h; no numerics are computed on the
+// host. Link with paper_2109_00485_b200/libblockeig_b200.so.
+//
+// Differences a caller can observe (documented in INTEGRATION.md):
+//   * SymmetricOperator uploads the matrix once at construction (it no
+//     longer needs the CsbCooMatrix to stay alive) and owns device memory;
+//     KernelVariant gains the tag Sm100a (the default), the three reference
+//     names stay parseable and select the same device kernel.
+//   * DiagonalTileSet returned by extract_tiles carries its device copy;
+//     a hand-assembled DiagonalTileSet is rejected with BadParams by
+//     apply_preconditioner / lobpcg_solve.
+//   * ThreadPool is accepted and ignored (device kernels are the workers).
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <exception>
+#include <functional>
+#include <memory>
+#include <random>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "blockeig_b200.h"
+
+namespace blockeig {
+
+using index_t = std::int64_t;
+
+// ---------------------------------------------------------------- errors.hpp
+// One class per reference exception (errors.hpp:11-109), same hierarchy.
+class Error : public std::runtime_error {
+public:
+    explicit Error(const std::string& msg) : std::runtime_error(msg) {}
+};
+#define BLOCKEIG_B200_ERROR(Name) \
+    class Name : public Error {   \
+    public:                       \
+        using Error::Error;       \
+    }
+BLOCKEIG_B200_ERROR(BlockTooLarge);
+BLOCKEIG_B200_ERROR(IndexOutOfRange);
+BLOCKEIG_B200_ERROR(DuplicateEntry);
+BLOCKEIG_B200_ERROR(DimensionMismatch);
+BLOCKEIG_B200_ERROR(NotStrictlyLower);
+BLOCKEIG_B200_ERROR(MisalignedTiles);
+BLOCKEIG_B200_ERROR(BadParams);
+BLOCKEIG_B200_ERROR(SingularTriangular);
+BLOCKEIG_B200_ERROR(SingularProjection);
+BLOCKEIG_B200_ERROR(RankDeficient);
+BLOCKEIG_B200_ERROR(BasisDegenerate);
+BLOCKEIG_B200_ERROR(BreakdownUnrecoverable);
+BLOCKEIG_B200_ERROR(EvenNd);
+BLOCKEIG_B200_ERROR(ProtocolDeadlock);
+BLOCKEIG_B200_ERROR(ParseError);
+BLOCKEIG_B200_ERROR(NotSymmetricHeader);
+BLOCKEIG_B200_ERROR(DeviceError);  // CUDA / cuSOLVER / NCCL / out of memory: no reference counterpart
+#undef BLOCKEIG_B200_ERROR
+class NotPositiveDefinite : public Error {
+public:
+    NotPositiveDefinite(const std::string& msg, int pivot_index) : Error(msg), pivot(pivot_index) {}
+    int pivot;
+};
+
+namespace b200 {
+// status -> typed exception
+[[noreturn]] inline void raise(be_status st) {
+    const std::string m = be_last_error();
+    switch (st) {
+        case BE_ERR_BLOCK_TOO_LARGE: throw BlockTooLarge(m);
+        case BE_ERR_INDEX_OUT_OF_RANGE: throw IndexOutOfRange(m);
+        case BE_ERR_DUPLICATE_ENTRY: throw DuplicateEntry(m);
+        case BE_ERR_DIMENSION_MISMATCH: throw DimensionMismatch(m);
+        case BE_ERR_NOT_STRICTLY_LOWER: throw NotStrictlyLower(m);
+        case BE_ERR_MISALIGNED_TILES: throw MisalignedTiles(m);
+        case BE_ERR_BAD_PARAMS: throw BadParams(m);
+        case BE_ERR_NOT_POSITIVE_DEFINITE: throw NotPositiveDefinite(m, be_last_error_pivot());
+        case BE_ERR_SINGULAR_TRIANGULAR: throw SingularTriangular(m);
+        case BE_ERR_SINGULAR_PROJECTION: throw SingularProjection(m);
+        case BE_ERR_RANK_DEFICIENT: throw RankDeficient(m);
+        case BE_ERR_BASIS_DEGENERATE: throw BasisDegenerate(m);
+        case BE_ERR_BREAKDOWN_UNRECOVERABLE: throw BreakdownUnrecoverable(m);
+        case BE_ERR_EVEN_ND: throw EvenNd(m);
+        case BE_ERR_PROTOCOL_DEADLOCK: throw ProtocolDeadlock(m);
+        case BE_ERR_PARSE: throw ParseError(m);
+        case BE_ERR_NOT_SYMMETRIC_HEADER: throw NotSymmetricHeader(m);
+        case BE_ERR_CUDA:
+        case BE_ERR_NO_DEVICE:
+        case BE_ERR_CUSOLVER:
+        case BE_ERR_NCCL:
+        case BE_ERR_OUT_OF_MEMORY: throw DeviceError(m);
+        default: throw Error(m);
+    }
+}
+inline void check(be_status st) {
+    if (st != BE_OK) raise(st);
+}
+
+// One device context per process (device 0 unless BLOCKEIG_B200_DEVICE set
+// through set_device before first use); shared by every object below.
+inline int& device_ordinal() {
+    static int d = 0;
+    return d;
+}
+inline void set_device(int d) { device_ordinal() = d; }
+inline be_ctx* context() {
+    static std::shared_ptr<be_ctx> ctx = [] {
+        be_ctx* c = nullptr;
+        check(be_ctx_create(device_ordinal(), &c));
+        return std::shared_ptr<be_ctx>(c, [](be_ctx* p) { be_ctx_destroy(p); });
+    }();
+    return ctx.get();
+}
+}  // namespace b200
+
+// ----------------------------------------------------------- thread_pool.hpp
+// Accepted for signature compatibility (thread_pool.hpp:18); unused.
+class ThreadPool {
+public:
+    explicit ThreadPool(int workers) : n_(workers < 1 ? 1 : workers) {}
+    int workers() const { return n_; }
+
+private:
+    int n_;
+};
+
+// ---------------------------------------------------------- block_vector.hpp
+// Row-major n x nvec multivector, element (r, v) at r * nvec + v
+// (block_vector.hpp:16-39).
+struct BlockVector {
+    index_t nrows = 0;
+    index_t nvec = 0;
+    std::vector<double> data;
+
+    BlockVector() = default;
+    BlockVector(index_t rows, index_t vecs) : nrows(rows), nvec(vecs), data(static_cast<std::size_t>(rows * vecs), 0.0) {}
+    static BlockVector zeros(index_t rows, index_t vecs) { return BlockVector(rows, vecs); }
+    double& operator()(index_t r, index_t v) { return data[static_cast<std::size_t>(r * nvec + v)]; }
+    double operator()(index_t r, index_t v) const { return data[static_cast<std::size_t>(r * nvec + v)]; }
+    double* row(index_t r) { return data.data() + r * nvec; }
+    const double* row(index_t r) const { return data.data() + r * nvec; }
+    void set_zero() { std::fill(data.begin(), data.end(), 0.0); }
+    bool same_shape(const BlockVector& o) const { return nrows == o.nrows && nvec == o.nvec; }
+};
+
+inline void require_same_shape(const BlockVector& a, const BlockVector& b, const char* where) {
+    if (!a.same_shape(b)) throw DimensionMismatch(std::string(where) + ": multivector shapes differ");
+}
+
+// block_vector.hpp:47-53: the same mt19937_64 stream, so X0 is bit-identical
+inline BlockVector random_block(index_t nrows, index_t nvec, std::uint64_t seed) {
+    BlockVector x(nrows, nvec);
+    std::mt19937_64 gen(seed);
+    std::uniform_real_distribution<double> u(-1.0, 1.0);
+    for (double& e : x.data) e = u(gen);
+    return x;
+}
+
+inline double column_norm(const BlockVector& x, index_t v) {
+    double s = 0.0;
+    for (index_t r = 0; r < x.nrows; ++r) s += x(r, v) * x(r, v);
+    return std::sqrt(s);
+}
+inline void scale_column(BlockVector& x, index_t v, double alpha) {
+    for (index_t r = 0; r < x.nrows; ++r) x(r, v) *= alpha;
+}
+inline double frobenius_norm(const BlockVector& x) {
+    double s = 0.0;
+    for (double e : x.data) s += e * e;
+    return std::sqrt(s);
+}
+inline double max_abs(const BlockVector& x) {
+    double m = 0.0;
+    for (double e : x.data) m = std::max(m, std::abs(e));
+    return m;
+}
+// block_vector.hpp:81-92
+inline double rel_frobenius_distance(const BlockVector& a, const BlockVector& b) {
+    require_same_shape(a, b, "rel_frobenius_distance");
+    double d2 = 0.0, a2 = 0.0, b2 = 0.0;
+    for (std::size_t i = 0; i < a.data.size(); ++i) {
+        const double d = a.data[i] - b.data[i];
+        d2 += d * d;
+        a2 += a.data[i] * a.data[i];
+        b2 += b.data[i] * b.data[i];
+    }
+    return std::sqrt(d2) / std::max({std::sqrt(a2), std::sqrt(b2), 1e-300});
+}
+
+// ------------------------------------------------------------------- csb.hpp
+struct Triple {  // csb.hpp:20-24
+    index_t row = 0;
+    index_t col = 0;
+    double value = 0.0;
+};
+static_assert(sizeof(Triple) == sizeof(be_triple), "Triple must match be_triple");
+
+inline constexpr index_t kMaxBlockExtent = 32000;  // csb.hpp:28
+
+struct CsbCooMatrix {  // csb.hpp:39-63
+    index_t nrows = 0;
+    index_t ncols = 0;
+    index_t nrowblks = 0;
+    index_t ncolblks = 0;
+    std::vector<index_t> row_offsets;
+    std::vector<index_t> col_offsets;
+    std::vector<index_t> block_nnz;
+    std::vector<index_t> block_nnz_offsets;
+    std::vector<std::uint16_t> local_rows;
+    std::vector<std::uint16_t> local_cols;
+    std::vector<double> values;
+
+    index_t nnz() const { return static_cast<index_t>(values.size()); }
+    index_t block_index(index_t bi, index_t bj) const { return bi * ncolblks + bj; }
+    index_t block_rows(index_t bi) const { return row_offsets[bi + 1] - row_offsets[bi]; }
+    index_t block_cols(index_t bj) const { return col_offsets[bj + 1] - col_offsets[bj]; }
+    double max_abs_value() const {
+        double m = 0.0;
+        for (double v : values) m = std::max(m, std::abs(v));
+        return m;
+    }
+    be_csb_view view() const {
+        return be_csb_view{nrows,           ncols,           nrowblks,          ncolblks,
+                           nnz(),           row_offsets.data(), col_offsets.data(), block_nnz.data(),
+                           block_nnz_offsets.data(), local_rows.data(), local_cols.data(), values.data()};
+    }
+};
+
+namespace b200 {
+inline CsbCooMatrix from_view(const be_csb_view& v) {
+    CsbCooMatrix m;
+    m.nrows = v.nrows;
+    m.ncols = v.ncols;
+    m.nrowblks = v.nrowblks;
+    m.ncolblks = v.ncolblks;
+    const auto nb = static_cast<std::size_t>(v.nrowblks * v.ncolblks);
+    m.row_offsets.assign(v.row_offsets, v.row_offsets + v.nrowblks + 1);
+    m.col_offsets.assign(v.col_offsets, v.col_offsets + v.ncolblks + 1);
+    m.block_nnz.assign(v.block_nnz, v.block_nnz + nb);
+    m.block_nnz_offsets.assign(v.block_nnz_offsets, v.block_nnz_offsets + nb);
+    m.local_rows.assign(v.local_rows, v.local_rows + v.nnz);
+    m.local_cols.assign(v.local_cols, v.local_cols + v.nnz);
+    m.values.assign(v.values, v.values + v.nnz);
+    return m;
+}
+inline CsbCooMatrix take(be_csb* h) {
+    std::unique_ptr<be_csb, void (*)(be_csb*)> own(h, be_csb_free);
+    be_csb_view v{};
+    check(be_csb_view_get(h, &v));
+    return from_view(v);
+}
+}  // namespace b200
+
+// csb.hpp:89-96
+inline std::vector<index_t> uniform_boundaries(index_t n, index_t extent) {
+    index_t cnt = 0;
+    b200::check(be_uniform_boundaries(n, extent, nullptr, &cnt));
+    std::vector<index_t> b(static_cast<std::size_t>(cnt));
+    b200::check(be_uniform_boundaries(n, extent, b.data(), &cnt));
+    return b;
+}
+
+// csb.hpp:100-161, bit-exact (block row-major, input order inside a block)
+inline CsbCooMatrix build_csb_coo(std::span<const Triple> triples, index_t nrows, index_t ncols,
+                                  const std::vector<index_t>& block_rows, const std::vector<index_t>& block_cols) {
+    be_csb* h = nullptr;
+    b200::check(be_csb_build(reinterpret_cast<const be_triple*>(triples.data()), static_cast<int64_t>(triples.size()),
+                             nrows, ncols, block_rows.data(), static_cast<int64_t>(block_rows.size()), block_cols.data(),
+                             static_cast<int64_t>(block_cols.size()), &h));
+    return b200::take(h);
+}
+
+// csb.hpp:165-185
+inline std::vector<Triple> to_triples(const CsbCooMatrix& m) {
+    std::vector<Triple> out(static_cast<std::size_t>(m.nnz()));
+    const be_csb_view v = m.view();
+    b200::check(be_csb_to_triples(&v, reinterpret_cast<be_triple*>(out.data())));
+    return out;
+}
+
+// csb.hpp:188-202
+inline bool is_strictly_lower(const CsbCooMatrix& m) {
+    const be_csb_view v = m.view();
+    int r = 0;
+    b200::check(be_csb_is_strictly_lower(&v, &r));
+    return r != 0;
+}
+
+// CSB1 cache files (csb.hpp:292-302); the diagonal section of
+// driver.hpp:136-161 is written when diag is non-empty
+inline void save_csb_file(const std::string& path, const CsbCooMatrix& m, std::span<const double> diag = {}) {
+    const be_csb_view v = m.view();
+    b200::check(be_csb_save(path.c_str(), &v, diag.empty() ? nullptr : diag.data(), static_cast<int64_t>(diag.size())));
+}
+inline CsbCooMatrix load_csb_file(const std::string& path, std::vector<double>* diag = nullptr) {
+    be_csb* h = nullptr;
+    double* d = nullptr;
+    int64_t nd = 0;
+    b200::check(be_csb_load(path.c_str(), &h, &d, &nd));
+    if (diag) diag->assign(d, d + nd);
+    be_free_buffer(d);
+    return b200::take(h);
+}
+
+// --------------------------------------------------------------- kernels.hpp
+enum class KernelTag { Baseline, FusedAtomic, CacheBlocked, Sm100a };
+
+struct KernelVariant {  // kernels.hpp:25-49
+    KernelTag tag = KernelTag::Sm100a;
+    int cache_size = 256;
+    int vector_width = 256;
+    be_prec values = BE_F32;  // stored-value precision on the device (BE_F64 = 12 B/nnz parity mode)
+
+    static KernelVariant baseline() { return {KernelTag::Baseline}; }
+    static KernelVariant fused_atomic() { return {KernelTag::FusedAtomic}; }
+    static KernelVariant cache_blocked(int cache = 256, int vec = 256) { return {KernelTag::CacheBlocked, cache, vec}; }
+    static KernelVariant sm100a(be_prec values = BE_F32) { return {KernelTag::Sm100a, 256, 256, values}; }
+    void validate() const {
+        if (cache_size < 1) throw BadParams("KernelVariant: cache_size must be >= 1");
+        if (vector_width < 1) throw BadParams("KernelVariant: vector_width must be >= 1");
+    }
+    const char* name() const {
+        switch (tag) {
+            case KernelTag::Baseline: return "baseline";
+            case KernelTag::FusedAtomic: return "fused-atomic";
+            case KernelTag::CacheBlocked: return "cache-blocked";
+            case KernelTag::Sm100a: return "sm100a";
+        }
+        return "?";
+    }
+};
+
+// kernels.hpp:51-56 plus the new tag
+inline KernelVariant variant_from_name(const std::string& s) {
+    if (s == "baseline") return KernelVariant::baseline();
+    if (s == "fused-atomic") return KernelVariant::fused_atomic();
+    if (s == "cache-blocked") return KernelVariant::cache_blocked();
+    if (s == "sm100a") return KernelVariant::sm100a();
+    throw BadParams("unknown kernel variant: " + s);
+}
+
+namespace b200 {
+struct OpDeleter {
+    void operator()(be_op* p) const { be_op_destroy(p); }
+};
+using OpHandle = std::shared_ptr<be_op>;
+inline OpHandle make_op(const CsbCooMatrix& m, const double* diag, be_prec values, int flags) {
+    const be_csb_view v = m.view();
+    be_op* op = nullptr;
+    check(be_op_create(context(), &v, diag, values, flags, &op));
+    return OpHandle(op, OpDeleter{});
+}
+inline void check_spmm_shapes(const CsbCooMatrix& h, const BlockVector& w, const BlockVector& u, bool trans) {
+    // kernels.hpp:278-285
+    const index_t in_rows = trans ? h.nrows : h.ncols, out_rows = trans ? h.ncols : h.nrows;
+    if (w.nrows != in_rows || u.nrows != out_rows || w.nvec != u.nvec)
+        throw DimensionMismatch("spmm: operand shapes do not conform to the matrix");
+    if (&w == &u || (!w.data.empty() && w.data.data() == u.data.data()))
+        throw BadParams("spmm: W and U must not alias");
+}
+}  // namespace b200
+
+// U += H W (kernels.hpp:290-300): one device upload per call; hold a
+// SymmetricOperator for repeated applies
+inline void spmm_notrans(const CsbCooMatrix& h, const BlockVector& w, BlockVector& u,
+                         const KernelVariant& variant = {}, ThreadPool* = nullptr) {
+    variant.validate();
+    b200::check_spmm_shapes(h, w, u, false);
+    auto op = b200::make_op(h, nullptr, variant.values, 0);
+    b200::check(be_op_apply_host(op.get(), w.data.data(), u.data.data(), w.nrows, static_cast<int>(w.nvec),
+                                 BE_APPLY_NOTRANS_ACC));
+}
+// U += H^T W (kernels.hpp:302-310)
+inline void spmm_trans(const CsbCooMatrix& h, const BlockVector& w, BlockVector& u,
+                       const KernelVariant& variant = {}, ThreadPool* = nullptr) {
+    variant.validate();
+    b200::check_spmm_shapes(h, w, u, true);
+    auto op = b200::make_op(h, nullptr, variant.values, 0);
+    b200::check(be_op_apply_host(op.get(), w.data.data(), u.data.data(), w.nrows, static_cast<int>(w.nvec),
+                                 BE_APPLY_TRANS_ACC));
+}
+
+// H = L + L^T + diag(D) on the device (kernels.hpp:339-378). The matrix is
+// uploaded (and converted to the device tile format) once, here.
+class SymmetricOperator {
+public:
+    SymmetricOperator(const CsbCooMatrix& l, std::vector<double> diag, KernelVariant variant = {},
+                      ThreadPool* pool = nullptr)
+        : l_(&l), diag_(std::move(diag)), variant_(variant) {
+        (void)pool;
+        variant_.validate();
+        if (l.nrows != l.ncols) throw DimensionMismatch("SymmetricOperator: matrix must be square");
+        if (static_cast<index_t>(diag_.size()) != l.nrows)
+            throw DimensionMismatch("SymmetricOperator: diagonal length mismatch");
+        op_ = b200::make_op(l, diag_.data(), variant_.values, BE_OP_SYMMETRIC);  // NotStrictlyLower from the device build
+    }
+
+    index_t dim() const { return l_->nrows; }
+    const CsbCooMatrix& matrix() const { return *l_; }
+    const std::vector<double>& diag() const { return diag_; }
+    const KernelVariant& variant() const { return variant_; }
+    be_op* handle() const { return op_.get(); }
+
+    // out = H in (overwrites out), host panels: copies in and out per call
+    void apply(const BlockVector& in, BlockVector& out) const {
+        if (!in.same_shape(out) || in.nrows != dim())
+            throw DimensionMismatch("SymmetricOperator::apply: shape mismatch");
+        b200::check(be_op_apply_host(op_.get(), in.data.data(), out.data.data(), in.nrows, static_cast<int>(in.nvec),
+                                     BE_APPLY_SYMMETRIC));
+    }
+    // out = H in on device panels (fp32 or fp64), no copies
+    void apply_device(const void* in, void* out, int nb, be_prec panels, void* stream = nullptr) const {
+        b200::check(be_op_apply(op_.get(), in, out, dim(), nb, panels, BE_APPLY_SYMMETRIC, stream));
+    }
+
+private:
+    const CsbCooMatrix* l_;
+    std::vector<double> diag_;
+    KernelVariant variant_;
+    b200::OpHandle op_;
+};
+
+// kernels.hpp:315-335
+inline BlockVector apply_symmetric(const CsbCooMatrix& l, std::span<const double> d, const BlockVector& w,
+                                   const KernelVariant& variant = {}, ThreadPool* pool = nullptr) {
+    SymmetricOperator h(l, std::vector<double>(d.begin(), d.end()), variant, pool);
+    BlockVector u(w.nrows, w.nvec);
+    h.apply(w, u);
+    return u;
+}
+
+// --------------------------------------------------------------- precond.hpp
+namespace detail {
+struct SparseTile {  // precond.hpp:18-30
+    index_t dim = 0;
+    std::vector<std::int32_t> rows, cols;
+    std::vector<double> values;
+    std::vector<index_t> diag_pos;
+    void apply(std::span<const double> x, std::span<double> y) const {
+        std::fill(y.begin(), y.end(), 0.0);
+        for (std::size_t k = 0; k < values.size(); ++k)
+            y[static_cast<std::size_t>(rows[k])] += values[k] * x[static_cast<std::size_t>(cols[k])];
+    }
+};
+}  // namespace detail
+using detail::SparseTile;
+
+struct DiagonalTileSet {  // precond.hpp:34-49, plus the device copy
+    std::vector<index_t> tile_offsets;
+    std::vector<SparseTile> tiles;
+    std::shared_ptr<be_tiles> device;
+
+    index_t count() const { return static_cast<index_t>(tile_offsets.empty() ? 0 : tile_offsets.size() - 1); }
+    index_t dim() const { return tile_offsets.empty() ? 0 : tile_offsets.back(); }
+    std::vector<index_t> sizes() const {
+        std::vector<index_t> s;
+        for (std::size_t j = 0; j + 1 < tile_offsets.size(); ++j) s.push_back(tile_offsets[j + 1] - tile_offsets[j]);
+        return s;
+    }
+    // host SparseTile copies (precond.hpp:18-30 layout), fetched on demand
+    void fetch_host_tiles() {
+        tiles.assign(static_cast<std::size_t>(count()), SparseTile{});
+        for (index_t j = 0; j < count(); ++j) {
+            SparseTile& t = tiles[static_cast<std::size_t>(j)];
+            int64_t dim = 0, ne = 0;
+            b200::check(be_tiles_get(device.get(), j, &dim, &ne, nullptr, nullptr, nullptr, nullptr));
+            t.dim = dim;
+            t.rows.resize(static_cast<std::size_t>(ne));
+            t.cols.resize(static_cast<std::size_t>(ne));
+            t.values.resize(static_cast<std::size_t>(ne));
+            t.diag_pos.resize(static_cast<std::size_t>(dim));
+            b200::check(be_tiles_get(device.get(), j, &dim, &ne, t.rows.data(), t.cols.data(), t.values.data(),
+                                     t.diag_pos.data()));
+        }
+    }
+};
+
+struct FomConfig {  // precond.hpp:51-57
+    int iterations = 4;
+    void validate() const {
+        if (iterations < 1) throw BadParams("FomConfig: iterations must be >= 1");
+    }
+};
+
+// precond.hpp:63-127 (same checks, same entry order); the tiles are uploaded
+// and the host SparseTile copies filled
+inline DiagonalTileSet extract_tiles(const CsbCooMatrix& l, std::span<const double> d,
+                                     const std::vector<index_t>& tile_offsets, bool host_copies = true) {
+    const be_csb_view v = l.view();
+    be_tiles* t = nullptr;
+    b200::check(be_tiles_create(b200::context(), &v, d.data(), tile_offsets.data(),
+                                static_cast<int64_t>(tile_offsets.size()), &t));
+    DiagonalTileSet s;
+    s.tile_offsets = tile_offsets;
+    s.device = std::shared_ptr<be_tiles>(t, [](be_tiles* p) { be_tiles_destroy(p); });
+    if (host_copies) s.fetch_host_tiles();
+    return s;
+}
+
+// precond.hpp:287-317: W = K^{-1} R, per-column shifts, singular -> raw column
+inline BlockVector apply_preconditioner(const DiagonalTileSet& tiles, std::span<const double> shifts,
+                                        const BlockVector& r, const FomConfig& cfg, ThreadPool* = nullptr,
+                                        std::int64_t* fallbacks = nullptr) {
+    cfg.validate();
+    if (r.nrows != tiles.dim()) throw DimensionMismatch("apply_preconditioner: residual rows != operator dim");
+    if (static_cast<index_t>(shifts.size()) != r.nvec)
+        throw DimensionMismatch("apply_preconditioner: one shift per column required");
+    if (!tiles.device) throw BadParams("apply_preconditioner: DiagonalTileSet was not built by extract_tiles");
+    BlockVector w(r.nrows, r.nvec);
+    std::int64_t fb = 0;
+    b200::check(be_precond_apply_host(tiles.device.get(), shifts.data(), r.data.data(), w.data.data(), r.nrows,
+                                      static_cast<int>(r.nvec), cfg.iterations, &fb));
+    if (fallbacks) *fallbacks += fb;
+    return w;
+}
+
+// ---------------------------------------------------------------- lobpcg.hpp
+using Operator = std::function<void(const BlockVector& in, BlockVector& out)>;  // lobpcg.hpp:20
+
+struct SolverState {  // lobpcg.hpp:52-58 (w, p, hw, hp are not materialised)
+    BlockVector x, w, p, hx, hw, hp;
+    std::vector<double> theta;
+    std::vector<double> residual_norms;
+    int n_converged = 0;
+    bool p_active = false;
+};
+
+struct SolverConfig {  // lobpcg.hpp:24-48
+    int k = 5;
+    int nb = 0;
+    double tol = 1e-6;
+    int maxiter = 500;
+    FomConfig fom;
+    KernelVariant variant;
+    std::uint64_t seed = 1234;
+    ThreadPool* pool = nullptr;
+    std::function<void(const SolverState&, int)> observer;
+
+    int block_width() const { return nb > 0 ? nb : k + 3; }
+    void validate(index_t n) const {
+        const int width = block_width();
+        if (k < 1 || k > width) throw BadParams("SolverConfig: need 1 <= k <= nb");
+        if (static_cast<index_t>(width) * 3 > n) throw BadParams("SolverConfig: operator dimension must be at least 3*nb");
+        if (!(tol > 0.0)) throw BadParams("SolverConfig: tol must be positive");
+        if (maxiter < 1) throw BadParams("SolverConfig: maxiter must be positive");
+        fom.validate();
+        variant.validate();
+    }
+};
+
+struct IterationRecord {  // lobpcg.hpp:60-66
+    int iter = 0;
+    std::vector<double> theta;
+    std::vector<double> residual_norms;
+    int n_converged = 0;
+    double t_spmm = 0.0, t_precond = 0.0, t_dense = 0.0, t_total = 0.0;
+};
+
+struct ConvergenceHistory {  // lobpcg.hpp:68-73
+    std::vector<IterationRecord> records;
+    std::int64_t operator_calls = 0;
+    std::int64_t precond_fallbacks = 0;
+    int restarts = 0;
+};
+
+struct SolveResult {  // lobpcg.hpp:75-80
+    std::vector<double> lambda;
+    BlockVector x;
+    ConvergenceHistory history;
+    bool converged = false;
+};
+
+namespace b200 {
+struct Callbacks {
+    const Operator* op = nullptr;
+    const SolverConfig* cfg = nullptr;
+    std::exception_ptr error;
+};
+inline int host_operator_trampoline(void* user, const double* in, double* out, int64_t n, int nb) {
+    auto* cb = static_cast<Callbacks*>(user);
+    try {
+        BlockVector bin(n, nb), bout(n, nb);
+        std::copy(in, in + n * nb, bin.data.begin());
+        (*cb->op)(bin, bout);
+        if (!bout.same_shape(bin)) throw DimensionMismatch("Operator: output shape differs from input");
+        std::copy(bout.data.begin(), bout.data.end(), out);
+        return 0;
+    } catch (...) {
+        cb->error = std::current_exception();
+        return 1;
+    }
+}
+inline void observer_trampoline(void* user, int iter, int64_t n, int nb, const double* theta, const double* rn,
+                                int n_conv, const double* x, const double* hx) {
+    auto* cb = static_cast<Callbacks*>(user);
+    if (cb->error) return;
+    try {
+        SolverState st;
+        st.theta.assign(theta, theta + nb);
+        st.residual_norms.assign(rn, rn + nb);
+        st.n_converged = n_conv;
+        st.p_active = true;  // set after every update (lobpcg.hpp:406)
+        if (x) {
+            st.x = BlockVector(n, nb);
+            std::copy(x, x + n * nb, st.x.data.begin());
+        }
+        if (hx) {
+            st.hx = BlockVector(n, nb);
+            std::copy(hx, hx + n * nb, st.hx.data.begin());
+        }
+        cb->cfg->observer(st, iter);
+    } catch (...) {
+        cb->error = std::current_exception();
+    }
+}
+inline SolveResult solve(be_op* op, const Operator* host_op, index_t n, const DiagonalTileSet* precond,
+                         const BlockVector* x0, const SolverConfig& cfg) {
+    cfg.validate(n);
+    if (precond && precond->dim() != n) throw DimensionMismatch("lobpcg_solve: preconditioner dimension mismatch");
+    if (precond && !precond->device) throw BadParams("lobpcg_solve: DiagonalTileSet was not built by extract_tiles");
+    const int nb = cfg.block_width();
+    if (x0 && (x0->nrows != n || x0->nvec != nb)) throw DimensionMismatch("lobpcg_solve: x0 shape");
+    Callbacks cb{host_op, &cfg, nullptr};
+    be_solver_config c{cfg.k, nb, cfg.tol, cfg.maxiter, cfg.fom.iterations, cfg.seed, cfg.observer ? 1 : 0};
+    be_result* res = nullptr;
+    const be_status st =
+        be_lobpcg_solve(context(), op, host_op ? host_operator_trampoline : nullptr, &cb, n,
+                        precond ? precond->device.get() : nullptr, x0 ? x0->data.data() : nullptr, &c,
+                        cfg.observer ? observer_trampoline : nullptr, &cb, &res);
+    if (cb.error) {
+        if (res) be_result_free(res);
+        std::rethrow_exception(cb.error);
+    }
+    check(st);
+    std::unique_ptr<be_result, void (*)(be_result*)> own(res, be_result_free);
+    be_result_info info{};
+    check(be_result_get_info(res, &info));
+    SolveResult out;
+    out.converged = info.converged != 0;
+    out.lambda.resize(static_cast<std::size_t>(info.k));
+    out.x = BlockVector(n, info.k);
+    check(be_result_get(res, out.lambda.data(), out.x.data.data()));
+    out.history.operator_calls = info.operator_calls;
+    out.history.precond_fallbacks = info.precond_fallbacks;
+    out.history.restarts = info.restarts;
+    for (int i = 0; i < info.iterations; ++i) {
+        IterationRecord r;
+        r.iter = i + 1;
+        r.theta.resize(static_cast<std::size_t>(nb));
+        r.residual_norms.resize(static_cast<std::size_t>(nb));
+        check(be_result_get_record(res, i, r.theta.data(), r.residual_norms.data(), &r.n_converged, &r.t_spmm,
+                                   &r.t_precond, &r.t_dense, &r.t_total));
+        out.history.records.push_back(std::move(r));
+    }
+    return out;
+}
+}  // namespace b200
+
+// lobpcg.hpp:291-449, generic operator: the closure runs on host panels, the
+// rest of the iteration stays on the device
+inline SolveResult lobpcg_solve(const Operator& op, index_t n, const DiagonalTileSet* precond, const BlockVector* x0,
+                                const SolverConfig& cfg) {
+    return b200::solve(nullptr, &op, n, precond, x0, cfg);
+}
+// lobpcg.hpp:452-456: device-resident end to end
+inline SolveResult lobpcg_solve(const SymmetricOperator& h, const DiagonalTileSet* precond, const BlockVector* x0,
+                                const SolverConfig& cfg) {
+    return b200::solve(h.handle(), nullptr, h.dim(), precond, x0, cfg);
+}
+
+// ----------------------------------------------------------------- synth.hpp
+enum class SynthKind { Banded, BlockTile, Random };  // synth.hpp:14
+
+struct SymmetricCoo {
+    index_t n = 0;
+    std::vector<Triple> lower;
+    std::vector<double> diag;
+};
+
+struct SynthParams {  // synth.hpp:33-56
+    SynthKind kind = SynthKind::Random;
+    index_t n = 1000;
+    double density = 0.02;
+    index_t bandwidth = 8;
+    index_t block_extent = 4000;
+    index_t tile_min = 4;
+    index_t tile_max = 512;
+    double diag_spread = 5.0;
+    double dominance = 1.0;
+    std::uint64_t seed = 1;
+};
+
+struct SynthMatrix {
+    SymmetricCoo coo;
+    std::vector<index_t> tile_offsets;
+};
+
+// synth.hpp:92-158: identical output for identical params
+inline SynthMatrix generate_synthetic(const SynthParams& p) {
+    const int kind = p.kind == SynthKind::Banded ? BE_SYNTH_BANDED
+                     : p.kind == SynthKind::BlockTile ? BE_SYNTH_BLOCKTILE
+                                                      : BE_SYNTH_RANDOM;
+    be_synth_params q{kind, p.n, p.density, p.bandwidth, p.block_extent, p.tile_min, p.tile_max, p.diag_spread,
+                      p.dominance, p.seed};
+    be_synth* s = nullptr;
+    b200::check(be_generate_synthetic(&q, &s));
+    std::unique_ptr<be_synth, void (*)(be_synth*)> own(s, be_synth_free);
+    const be_triple* lower = nullptr;
+    const double* diag = nullptr;
+    const int64_t* toff = nullptr;
+    int64_t nl = 0, nt = 0;
+    b200::check(be_synth_get(s, &lower, &nl, &diag, &toff, &nt));
+    SynthMatrix m;
+    m.coo.n = p.n;
+    m.coo.lower.resize(static_cast<std::size_t>(nl));
+    std::copy(lower, lower + nl, reinterpret_cast<be_triple*>(m.coo.lower.data()));
+    m.coo.diag.assign(diag, diag + p.n);
+    m.tile_offsets.assign(toff, toff + nt);
+    return m;
+}
+
+}  // namespace blockeig

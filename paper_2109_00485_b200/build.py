@@ -67,5 +67,26 @@ def build_lib(verbose: bool = False) -> Path:
     return LIB
 
 
+MIRROR_SRC = ROOT / "tests" / "cpp" / "mirror_test.cpp"
+MIRROR_BIN = ROOT / "tests" / "cpp" / "mirror_test"
+
+
+def build_cpp_tests(verbose: bool = False) -> Path:
+    """Compile the reference-style C++ test program against the C++ mirror
+    header (include/blockeig_b200.hpp) and the library."""
+    lib = build_lib(verbose)
+    deps = [MIRROR_SRC, ROOT / "include" / "blockeig_b200.hpp", ROOT / "include" / "blockeig_b200.h", lib]
+    if MIRROR_BIN.exists() and MIRROR_BIN.stat().st_mtime >= max(d.stat().st_mtime for d in deps):
+        return MIRROR_BIN
+    cmd = [CXX, "-std=c++20", "-O2", "-Wall", "-Wextra", "-I", str(ROOT / "include"), str(MIRROR_SRC),
+           "-L", str(PKG), "-lblockeig_b200", "-Wl,-rpath," + str(PKG), "-o", str(MIRROR_BIN)]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"mirror_test build failed:\n{r.stdout}\n{r.stderr}")
+    return MIRROR_BIN
+
+
 if __name__ == "__main__":
     print(build_lib(verbose="-v" in sys.argv))
