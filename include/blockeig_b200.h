@@ -301,6 +301,62 @@ be_status be_result_get_record(const be_result* r, int i, double* theta, double*
 void be_result_free(be_result* r);
 
 /* ------------------------------------------------------------------------- */
+/* Multi-GPU (dist.hpp). One rank per GPU; the reference's simulated          */
+/* collectives (SimComm, dist.hpp:85-89; distributed_spmm :256-371;           */
+/* distributed_gram_allreduce :375-391) become NCCL allgather /               */
+/* reduce-scatter / allreduce over NVLink. A second backend runs the ranks    */
+/* as threads of one process (any devices, several ranks per GPU allowed):    */
+/* the same code path, exercised on a single GPU.                             */
+/* ------------------------------------------------------------------------- */
+
+typedef struct be_comm be_comm;
+typedef struct be_comm_group be_comm_group;
+/* ncclGetUniqueId: rank 0 creates it and ships the 128 bytes to the others */
+be_status be_comm_nccl_id(uint8_t id[128]);
+be_status be_comm_create_nccl(be_ctx* ctx, const uint8_t id[128], int rank, int world, be_comm** out);
+/* in-process rank group: one be_comm_create_local per rank, each from its own
+ * host thread (creation and every collective are group-wide barriers) */
+be_status be_comm_group_create(int world, be_comm_group** out);
+be_status be_comm_group_destroy(be_comm_group* g);
+/* release every rank blocked in (or later entering) a collective of the group
+ * with BE_ERR_PROTOCOL_DEADLOCK: called by a rank that failed */
+be_status be_comm_group_abort(be_comm_group* g);
+be_status be_comm_create_local(be_ctx* ctx, be_comm_group* g, int rank, be_comm** out);
+be_status be_comm_destroy(be_comm* c);
+/* backend: 0 = NCCL, 1 = local; calls / bytes: collectives issued and bytes
+ * received by this rank (the SimComm counters) */
+be_status be_comm_info(const be_comm* c, int* rank, int* world, int* backend, int64_t* calls, int64_t* bytes);
+/* in-place sum over ranks of count device doubles (distributed_gram_allreduce) */
+be_status be_comm_allreduce_f64(be_comm* c, double* buf_dev, int64_t count, void* stream);
+
+/* Partition rules (integer-exact; every rank derives the same cuts).
+ * be_dist_rows: panel-row ownership, world + 1 cuts on the block boundaries
+ *   `bounds` (nbounds entries), cut p the boundary closest to n p / world.
+ * be_dist_balance: contiguous item ranges of near-equal weight (world + 1 item
+ *   indices), e.g. CSB block rows weighted by their stored nonzeros: the
+ *   nnz-balanced SpMM slabs. Replaces partition_matrix's fixed triangular
+ *   layout (dist.hpp:113-198, nd(nd+1)/2 ranks only) for any rank count. */
+be_status be_dist_rows(const int64_t* bounds, int64_t nbounds, int world, int64_t* cuts);
+be_status be_dist_balance(const int64_t* weights, int64_t nitems, int world, int64_t* cuts);
+
+/* Distributed symmetric operator: L_slab is this rank's share of the global
+ * strictly-lower CSB (global coordinates and blocks; the ranks' slabs are
+ * disjoint and cover L), cuts the panel-row ownership (world + 1 entries on
+ * block boundaries), diag_local the diagonal of rows [cuts[rank],
+ * cuts[rank+1]). be_op_apply then maps local f64 panels (BE_APPLY_SYMMETRIC)
+ * to local f64 panels: distributed_operator (dist.hpp:397-404) without the
+ * host scatter / gather. be_lobpcg_* on such an operator run the distributed
+ * solver: n = local rows, x0 = local rows of X0, the result holds local rows. */
+be_status be_op_create_dist(be_ctx* ctx, be_comm* comm, const be_csb_view* L_slab, const int64_t* cuts,
+                            const double* diag_local, int values_prec, be_op** out);
+/* extract_tiles restricted to the tiles of rows [row_begin, row_end) (a union
+ * of whole tiles of tile_offsets, which cover [0, n)); diag_local holds those
+ * rows. L must contain the diagonal blocks of those rows. */
+be_status be_tiles_create_range(be_ctx* ctx, const be_csb_view* L, const double* diag_local,
+                                const int64_t* tile_offsets, int64_t n_tile_offsets, int64_t row_begin,
+                                int64_t row_end, be_tiles** out);
+
+/* ------------------------------------------------------------------------- */
 /* Device dense kernels exposed for parity tests (densela.hpp).               */
 /* ------------------------------------------------------------------------- */
 

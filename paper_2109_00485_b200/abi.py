@@ -195,6 +195,26 @@ class Csb:
             _lib.be_csb_free(self._handle)
             self._handle = None
 
+    def block_row_nnz(self) -> np.ndarray:
+        """Stored nonzeros per CSB block row (the SpMM slab weights)."""
+        return self.block_nnz.reshape(self.nrowblks, self.ncolblks).sum(axis=1)
+
+    def slab(self, b0: int, b1: int) -> "Csb":
+        """Block rows [b0, b1) of this matrix as a CSB of the same global shape
+        and blocks (entries elsewhere absent); zero-copy slices of the arrays."""
+        nb = self.ncolblks
+        bn = self.block_nnz.reshape(self.nrowblks, nb).copy()
+        bn[:b0] = 0
+        bn[b1:] = 0
+        lo = int(self.block_nnz_offsets[b0 * nb]) if b0 < self.nrowblks else self.nnz
+        hi = int(self.block_nnz_offsets[b1 * nb]) if b1 < self.nrowblks else self.nnz
+        off = np.zeros(bn.size, np.int64)
+        np.cumsum(bn.ravel()[:-1], out=off[1:])
+        sl = Csb(self.nrows, self.ncols, self.row_offsets, self.col_offsets, bn.ravel(), off,
+                 self.local_rows[lo:hi], self.local_cols[lo:hi], self.values[lo:hi])
+        sl._parent = self  # keeps a library-owned parent alive
+        return sl
+
     def to_triples(self) -> np.ndarray:
         out = np.zeros(self.nnz, dtype=TRIPLE_DTYPE)
         v = self.view()
@@ -390,16 +410,141 @@ class Operator:
             pass
 
 
-class Tiles:
-    """DiagonalTileSet (precond.hpp:34-48) built by extract_tiles (precond.hpp:63-127), uploaded."""
+def dist_rows(bounds, world: int) -> np.ndarray:
+    """Panel-row ownership cuts (world + 1) on the block boundaries."""
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    out = np.zeros(world + 1, np.int64)
+    check(lib().be_dist_rows(_p(b), C.c_int64(len(b)), C.c_int(world), _p(out)))
+    return out
 
-    def __init__(self, ctx: Context, csb: Csb, diag, tile_offsets):
+
+def dist_balance(weights, world: int) -> np.ndarray:
+    """Contiguous weight-balanced item cuts (world + 1)."""
+    w = np.ascontiguousarray(weights, dtype=np.int64)
+    out = np.zeros(world + 1, np.int64)
+    check(lib().be_dist_balance(_p(w), C.c_int64(len(w)), C.c_int(world), _p(out)))
+    return out
+
+
+class CommGroup:
+    """In-process rank group (ranks are host threads; any GPUs, several ranks per GPU allowed)."""
+
+    def __init__(self, world: int):
+        self._h = C.c_void_p()
+        check(lib().be_comm_group_create(C.c_int(world), C.byref(self._h)))
+        self.world = world
+
+    def abort(self):
+        """Release ranks blocked in a collective (ProtocolDeadlock): call from a failing rank."""
+        if self._h:
+            check(lib().be_comm_group_abort(self._h))
+
+    def close(self):
+        if self._h:
+            check(lib().be_comm_group_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _nccl_hint():
+    """Point the library at the NCCL torch bundles (unless one is loaded or set):
+    the process must not mix two libnccl.so.2 builds under one soname."""
+    import os
+    if "BE_NCCL_LIB" in os.environ:
+        return
+    try:
+        import nvidia.nccl as n
+        p = Path(list(n.__path__)[0]) / "lib" / "libnccl.so.2"
+        if p.exists():
+            os.environ["BE_NCCL_LIB"] = str(p)
+    except Exception:
+        pass
+
+
+def nccl_unique_id() -> bytes:
+    _nccl_hint()
+    buf = (C.c_uint8 * 128)()
+    check(lib().be_comm_nccl_id(buf))
+    return bytes(buf)
+
+
+class Comm:
+    """A rank's communicator: NCCL (one process per GPU) or local (threads of one process)."""
+
+    def __init__(self, ctx: Context, *, nccl_id: bytes | None = None, rank: int = 0, world: int = 1,
+                 group: CommGroup | None = None):
+        self.ctx = ctx
+        self._h = C.c_void_p()
+        if group is not None:
+            self._group = group
+            check(lib().be_comm_create_local(ctx.handle, group._h, C.c_int(rank), C.byref(self._h)))
+        else:
+            _nccl_hint()
+            if nccl_id is None or len(nccl_id) != 128:
+                raise BadParams("Comm: NCCL needs the 128-byte unique id")
+            buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+            check(lib().be_comm_create_nccl(ctx.handle, buf, C.c_int(rank), C.c_int(world), C.byref(self._h)))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        r, w, b, c, n = C.c_int(), C.c_int(), C.c_int(), C.c_int64(), C.c_int64()
+        check(lib().be_comm_info(self._h, C.byref(r), C.byref(w), C.byref(b), C.byref(c), C.byref(n)))
+        return {"rank": r.value, "world": w.value, "backend": "nccl" if b.value == 0 else "local",
+                "calls": c.value, "bytes": n.value}
+
+    def allreduce_dev(self, ptr: int, count: int, stream: int = 0):
+        check(lib().be_comm_allreduce_f64(self._h, C.c_void_p(ptr), C.c_int64(count), C.c_void_p(stream)))
+
+    def close(self):
+        if self._h:
+            check(lib().be_comm_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DistOperator(Operator):
+    """Distributed symmetric operator over the ranks of `comm` (dist.hpp
+    distributed_operator): this rank's CSB slab, panel-row cuts, local diagonal."""
+
+    def __init__(self, ctx: Context, comm: Comm, slab: Csb, cuts, diag_local, values_prec=BE_F32):
+        self.ctx = ctx
+        self.comm = comm
+        self.cuts = np.ascontiguousarray(cuts, dtype=np.int64)
+        self._h = C.c_void_p()
+        d = np.ascontiguousarray(diag_local, dtype=np.float64)
+        v = slab.view()
+        check(lib().be_op_create_dist(ctx.handle, comm.handle, C.byref(v), _p(self.cuts), _p(d),
+                                      C.c_int(values_prec), C.byref(self._h)))
+
+
+class Tiles:
+    """DiagonalTileSet (precond.hpp:34-48) built by extract_tiles (precond.hpp:63-127), uploaded.
+    row_range=(lo, hi): only the tiles of rows [lo, hi) (one rank's rows), diag = those rows."""
+
+    def __init__(self, ctx: Context, csb: Csb, diag, tile_offsets, row_range=None):
         self.ctx = ctx
         self._h = C.c_void_p()
         d = np.ascontiguousarray(diag, dtype=np.float64)
         t = np.ascontiguousarray(tile_offsets, dtype=np.int64)
         v = csb.view()
-        check(lib().be_tiles_create(ctx.handle, C.byref(v), _p(d), _p(t), C.c_int64(len(t)), C.byref(self._h)))
+        if row_range is None:
+            check(lib().be_tiles_create(ctx.handle, C.byref(v), _p(d), _p(t), C.c_int64(len(t)), C.byref(self._h)))
+        else:
+            check(lib().be_tiles_create_range(ctx.handle, C.byref(v), _p(d), _p(t), C.c_int64(len(t)),
+                                              C.c_int64(row_range[0]), C.c_int64(row_range[1]), C.byref(self._h)))
 
     @property
     def handle(self):

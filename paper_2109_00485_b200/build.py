@@ -1,8 +1,8 @@
 """Build libblockeig_b200.so (sm_100a) in-tree with nvcc.
 
 Every .cu / .cpp under csrc/ is compiled to an object under build/ and linked
-into paper_2109_00485_b200/libblockeig_b200.so against cudart, cuSOLVER and
-NCCL. Objects are rebuilt when their source or any header is newer.
+into paper_2109_00485_b200/libblockeig_b200.so against cudart and cuSOLVER;
+NCCL is resolved at run time (comm.cu). Objects are rebuilt when their source or any header is newer.
 """
 from __future__ import annotations
 
@@ -22,7 +22,7 @@ CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC,-pthread", "-I", str(ROOT / "include"), "-I", str(CSRC)]
 CUFLAGS = ARCH + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
-LIBS = ["-lcudart", "-lcusolver", "-lcublas", "-lnccl", "-lpthread"]
+LIBS = ["-lcudart", "-lcusolver", "-lcublas", "-ldl", "-lpthread"]  # NCCL: dlopen at run time (comm.cu)
 
 
 def _headers():

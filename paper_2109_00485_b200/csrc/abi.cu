@@ -7,6 +7,7 @@
 #include <cstring>
 #include <string>
 
+#include "comm.hpp"
 #include "densela.cuh"
 #include "device.hpp"
 #include "lobpcg.cuh"
@@ -333,8 +334,8 @@ be_status be_op_decode(be_op* op, int64_t* rows, int64_t* cols, double* values, 
             for (int k = 0; k < nnz; ++k) {
                 const std::uint16_t x = rc[static_cast<std::size_t>(b + k)];
                 if ((x >> 8) >= nr || (x & 255) >= nc) be::fail(BE_ERR_GENERIC, "decode: local index outside tile");
-                if (rows) rows[p] = t.row0 + (x >> 8);
-                if (cols) cols[p] = t.col0 + (x & 255);
+                if (rows) rows[p] = o->comm ? o->unpad(t.row0 + (x >> 8)) : t.row0 + (x >> 8);
+                if (cols) cols[p] = o->comm ? o->unpad(t.col0 + (x & 255)) : t.col0 + (x & 255);
                 if (values) {
                     if (vsz == 4) {
                         float f;
@@ -369,6 +370,110 @@ be_status be_tiles_create(be_ctx* ctx, const be_csb_view* L, const double* diag,
         if (!ctx || !L || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
         BE_CUDA(cudaSetDevice(ctx->impl->device));
         *out = new be_tiles{be::tiles_create(ctx->impl.get(), *L, diag, tile_offsets, n_tile_offsets)};
+    });
+}
+
+be_status be_tiles_create_range(be_ctx* ctx, const be_csb_view* L, const double* diag_local,
+                                const int64_t* tile_offsets, int64_t n_tile_offsets, int64_t row_begin,
+                                int64_t row_end, be_tiles** out) {
+    return guard([&] {
+        if (!ctx || !L || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        if (row_begin < 0 || row_end < row_begin) be::fail(BE_ERR_BAD_PARAMS, "be_tiles_create_range: bad row range");
+        BE_CUDA(cudaSetDevice(ctx->impl->device));
+        *out = new be_tiles{be::tiles_create(ctx->impl.get(), *L, diag_local, tile_offsets, n_tile_offsets, row_begin,
+                                             row_end)};
+    });
+}
+
+// ------------------------------------------------------------------ multi-GPU
+be_status be_comm_nccl_id(uint8_t id[128]) {
+    return guard([&] {
+        if (!id) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        be::nccl_unique_id(id);
+    });
+}
+
+be_status be_comm_create_nccl(be_ctx* ctx, const uint8_t id[128], int rank, int world, be_comm** out) {
+    return guard([&] {
+        if (!ctx || !id || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        *out = new be_comm{be::make_nccl_comm(ctx->impl->device, id, rank, world)};
+    });
+}
+
+be_status be_comm_group_create(int world, be_comm_group** out) {
+    return guard([&] {
+        if (!out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        *out = new be_comm_group{std::make_unique<be::LocalGroup>(world)};
+    });
+}
+
+be_status be_comm_group_destroy(be_comm_group* g) {
+    return guard([&] { delete g; });
+}
+
+be_status be_comm_group_abort(be_comm_group* g) {
+    return guard([&] {
+        if (!g) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        g->impl->abort();
+    });
+}
+
+be_status be_comm_create_local(be_ctx* ctx, be_comm_group* g, int rank, be_comm** out) {
+    return guard([&] {
+        if (!ctx || !g || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        *out = new be_comm{be::make_local_comm(ctx->impl->device, g->impl.get(), rank)};
+    });
+}
+
+be_status be_comm_destroy(be_comm* c) {
+    return guard([&] { delete c; });
+}
+
+be_status be_comm_info(const be_comm* c, int* rank, int* world, int* backend, int64_t* calls, int64_t* bytes) {
+    return guard([&] {
+        if (!c) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        const auto* k = c->impl.get();
+        if (rank) *rank = k->rank;
+        if (world) *world = k->world;
+        if (backend) *backend = std::strcmp(k->backend(), "nccl") == 0 ? 0 : 1;
+        if (calls) *calls = k->calls;
+        if (bytes) *bytes = k->bytes_moved;
+    });
+}
+
+be_status be_comm_allreduce_f64(be_comm* c, double* buf_dev, int64_t count, void* stream) {
+    return guard([&] {
+        if (!c || (!buf_dev && count > 0)) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        if (count < 0) be::fail(BE_ERR_BAD_PARAMS, "be_comm_allreduce_f64: negative count");
+        BE_CUDA(cudaSetDevice(c->impl->device));
+        c->impl->allreduce_f64(buf_dev, static_cast<std::size_t>(count), static_cast<cudaStream_t>(stream));
+    });
+}
+
+be_status be_dist_rows(const int64_t* bounds, int64_t nbounds, int world, int64_t* cuts) {
+    return guard([&] {
+        if (!bounds || !cuts || nbounds < 2) be::fail(BE_ERR_BAD_PARAMS, "be_dist_rows: bad arguments");
+        for (int64_t i = 1; i < nbounds; ++i)
+            if (bounds[i] <= bounds[i - 1]) be::fail(BE_ERR_BAD_PARAMS, "be_dist_rows: boundaries must be strictly increasing");
+        const auto c = be::dist_rows(bounds, nbounds, world);
+        std::memcpy(cuts, c.data(), c.size() * sizeof(int64_t));
+    });
+}
+
+be_status be_dist_balance(const int64_t* weights, int64_t nitems, int world, int64_t* cuts) {
+    return guard([&] {
+        if ((!weights && nitems > 0) || !cuts || nitems < 0) be::fail(BE_ERR_BAD_PARAMS, "be_dist_balance: bad arguments");
+        const auto c = be::dist_balance(weights, nitems, world);
+        std::memcpy(cuts, c.data(), c.size() * sizeof(int64_t));
+    });
+}
+
+be_status be_op_create_dist(be_ctx* ctx, be_comm* comm, const be_csb_view* L_slab, const int64_t* cuts,
+                            const double* diag_local, int values_prec, be_op** out) {
+    return guard([&] {
+        if (!ctx || !comm || !L_slab || !cuts || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        BE_CUDA(cudaSetDevice(ctx->impl->device));
+        *out = new be_op{be::op_create_dist(ctx->impl.get(), comm->impl.get(), *L_slab, cuts, diag_local, values_prec)};
     });
 }
 

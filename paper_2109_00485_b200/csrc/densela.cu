@@ -562,7 +562,7 @@ void gram(Ctx* ctx, const GramJob& job, std::int64_t n, double* partials, std::i
     const int rg = kT / cpb;
     const std::size_t sm = std::max(static_cast<std::size_t>(g.nd) * kGramRows * g.nblk * 4,
                                     static_cast<std::size_t>(rg) * cpb * 16) * sizeof(double);
-    if (sm > 48 * 1024) BE_CUDA(cudaFuncSetAttribute(k_gram_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    ensure_dyn_smem(k_gram_partial, sm);
     dim3 grid(nparts, (g.ncombo + cpb - 1) / cpb);
     k_gram_partial<<<grid, kT, sm, s>>>(g, n, partials, cpb);
     BE_CUDA(cudaGetLastError());
@@ -613,7 +613,7 @@ void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
     const int nblk = (job.nb + 3) / 4;
     const std::size_t sm = (static_cast<std::size_t>(m.ncoef) * job.nb * nblk * 4 +
                             static_cast<std::size_t>(ms.nsrc) * kMixRows * (job.nb + 1)) * sizeof(double);
-    BE_CUDA(cudaFuncSetAttribute(k_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    ensure_dyn_smem(k_mix, sm);
     const int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 4, (n + kMixRows - 1) / kMixRows)));
     k_mix<<<grid, kT, sm, s>>>(m, ms, nullptr, n);
     BE_CUDA(cudaGetLastError());

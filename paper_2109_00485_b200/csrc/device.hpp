@@ -13,6 +13,8 @@ struct cusolverDnContext;
 
 namespace be {
 
+struct Comm;
+
 // RAII device buffer
 template <class T>
 struct DBuf {
@@ -62,6 +64,15 @@ struct TileHdr {
 
 inline constexpr int kTile = 128;
 
+// Raise a kernel's dynamic shared-memory limit to at least `bytes` on the
+// current device. Monotonic (never lowered), so ranks running as threads of
+// one process cannot race one another below a size a launch needs.
+void ensure_dyn_smem_raw(const void* kern, std::size_t bytes);
+template <class K>
+void ensure_dyn_smem(K* kern, std::size_t bytes) {
+    ensure_dyn_smem_raw(reinterpret_cast<const void*>(kern), bytes);
+}
+
 struct Op {
     Ctx* ctx = nullptr;
     index_t nrows = 0, ncols = 0, nnz = 0, ntiles = 0, padded = 0;
@@ -80,6 +91,24 @@ struct Op {
     DBuf<float> x32, y32;            // f32 staging of f64 panels (f32-values operator)
     std::vector<std::int64_t> csb_index;  // device order -> CSB index (small matrices only)
     int grid = 0;
+    // multi-GPU (row e): panel rows are owned in contiguous segments
+    // [cuts[q], cuts[q+1]); tile coordinates live in the padded index space
+    // q * lmax + (row - cuts[q]) so the f32 X / Y exchange buffers are
+    // equal-count NCCL allgather / reduce-scatter operands. `runs` then holds
+    // the interior work items (rows and columns both in this rank's segment,
+    // computable before the allgather lands) and runs_ext the rest.
+    Comm* comm = nullptr;
+    int rank = 0, world = 1;
+    index_t lmax = 0, row_lo = 0, nlocal = 0;
+    std::vector<index_t> cuts;
+    DBuf<int2> runs_ext;
+    index_t nruns_ext = 0;
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_x = nullptr, ev_ag = nullptr;
+    index_t unpad(index_t p) const {  // padded index -> global row
+        const index_t q = p / lmax;
+        return cuts[static_cast<std::size_t>(q)] + (p - q * lmax);
+    }
     // timing
     bool timing = false;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -88,6 +117,15 @@ struct Op {
 };
 
 std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag, int values_prec, int flags);
+// Distributed operator (row e): L holds this rank's slab of the global
+// strictly-lower matrix (global coordinates), cuts (world + 1 entries, on L's
+// block boundaries) the panel-row ownership, diag_local the diagonal of this
+// rank's rows. apply() then maps local f64 panels to local f64 panels.
+std::unique_ptr<Op> op_create_dist(Ctx* ctx, Comm* comm, const be_csb_view& L, const index_t* cuts,
+                                   const double* diag_local, int values_prec);
+// equal-rows ownership on block boundaries / contiguous weight balance
+std::vector<index_t> dist_rows(const index_t* bounds, index_t nbounds, int world);
+std::vector<index_t> dist_balance(const index_t* weights, index_t nitems, int world);
 void op_apply(Op* op, const void* X, void* Y, index_t nrows, int nb, int panel_prec, int mode, cudaStream_t s);
 
 }  // namespace be

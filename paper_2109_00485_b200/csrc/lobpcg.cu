@@ -18,6 +18,7 @@
 #include <cstring>
 #include <random>
 
+#include "comm.hpp"
 #include "densela.cuh"
 #include "lobpcg.cuh"
 #include "precond.cuh"
@@ -26,10 +27,15 @@ namespace be {
 
 namespace {
 
-std::vector<double> random_block(index_t n, index_t nb, std::uint64_t seed) {  // block_vector.hpp:47-53
+// random_block (block_vector.hpp:47-53) rows [row_lo, row_lo + n): the
+// reference's one mt19937_64 stream over the whole n_global x nb block, of
+// which a rank keeps its own rows (multi-GPU X0 / restart blocks match the
+// single-GPU ones bit for bit).
+std::vector<double> random_block(index_t n, index_t nb, std::uint64_t seed, index_t row_lo = 0) {
     std::vector<double> x(static_cast<std::size_t>(n * nb));
     std::mt19937_64 rng(seed);
     std::uniform_real_distribution<double> u(-1.0, 1.0);
+    for (index_t i = 0; i < row_lo * nb; ++i) (void)u(rng);
     for (auto& v : x) v = u(rng);
     return x;
 }
@@ -61,6 +67,14 @@ struct Solver {
     Tiles* tiles;
     const be_solver_config& cfg;
     be::Result& res;
+    // multi-GPU: panels hold this rank's rows [row_lo, row_lo + n) of n_global;
+    // every Gram / norm partial is summed over ranks (distributed_gram_allreduce,
+    // dist.hpp:375-391) so all ranks take identical decisions
+    Comm* comm = nullptr;
+    index_t n_global = 0, row_lo = 0;
+    void allreduce(double* p, int count) {
+        if (comm) comm->allreduce_f64(p, static_cast<std::size_t>(count), s);
+    }
 
     DBuf<double> X, W, P, HX, HW, HP, R, Xn, HXn, Pn, HPn;
     DBuf<double> small, partials;
@@ -86,6 +100,12 @@ struct Solver {
     Solver(Ctx* c, index_t n_, int nb_, int k_, Op* o, be_host_operator_fn hop, void* hu, Tiles* t,
            const be_solver_config& cf, be::Result& r)
         : ctx(c), s(c->stream), n(n_), nb(nb_), k(k_), op(o), host_op(hop), host_user(hu), tiles(t), cfg(cf), res(r) {
+        comm = op ? op->comm : nullptr;
+        n_global = n;
+        if (comm) {
+            n_global = op->cuts.back();
+            row_lo = op->row_lo;
+        }
         const index_t pn = n * nb;
         for (auto* b : {&X, &W, &P, &HX, &HW, &HP, &R, &Xn, &HXn, &Pn, &HPn}) b->reset(std::max<index_t>(pn, 1));
         const index_t nb2 = static_cast<index_t>(nb) * nb, dim = 3 * nb;
@@ -150,6 +170,7 @@ struct Solver {
         j.sym[0] = sym;
         j.out[0] = out;
         dla::gram(ctx, j, n, partials.get(), partials_len, s);
+        allreduce(out, nb * nb);
     }
 
     // qr_of_transpose (densela.hpp:412-445); returns false on RankDeficient
@@ -167,7 +188,7 @@ struct Solver {
     }
 
     void upload_random(double* dst, std::uint64_t seed) {
-        const auto h = random_block(n, nb, seed);
+        const auto h = random_block(n, nb, seed, row_lo);
         BE_CUDA(cudaMemcpyAsync(dst, h.data(), h.size() * 8, cudaMemcpyHostToDevice, s));
         BE_CUDA(cudaStreamSynchronize(s));
     }
@@ -219,6 +240,7 @@ struct Solver {
             j.out[q] = blocks + static_cast<index_t>(q) * nb * nb;
         }
         dla::gram(ctx, j, n, partials.get(), partials_len, s);
+        allreduce(blocks, np * nb * nb);
         const int nblk = with_p ? 3 : 2;
         dla::rr_assemble(ctx, blocks, nb, nblk, G, O, s);
         dla::sygv_lowest(ctx, sygv, G, O, nblk * nb, nb, 1e-10, C, theta, st.get(), s);
@@ -246,6 +268,7 @@ struct Solver {
             j.a[0] = X.get(); j.b[0] = HX.get(); j.sym[0] = 0; j.out[0] = blocks;
             j.a[1] = X.get(); j.b[1] = X.get(); j.sym[1] = 1; j.out[1] = blocks + static_cast<index_t>(nb) * nb;
             dla::gram(ctx, j, n, partials.get(), partials_len, s);
+            allreduce(blocks, 2 * nb * nb);
             dla::rr_assemble(ctx, blocks, nb, 1, G, O, s);
             dla::sygv_lowest(ctx, sygv, G, O, nb, nb, 1e-10, C, theta, st.get(), s);
             BE_CUDA(cudaMemcpyAsync(hm->theta, theta, nb * 8, cudaMemcpyDeviceToHost, s));
@@ -262,6 +285,7 @@ struct Solver {
         }
         th.assign(hm->theta, hm->theta + nb);
         dla::residual(ctx, HX.get(), X.get(), theta, R.get(), nb, n, partials.get(), rn2, xn2, s);
+        allreduce(rn2, 2 * nb);  // rn2, xn2 are adjacent
     }
 
     // run up to `count` further iterations (never past maxiter); returns the
@@ -334,12 +358,14 @@ struct Solver {
                 dla::trsm(ctx, P.get(), HP.get(), Rp, nb, n, st.get(), 0, 1, s);
             }
             dla::residual(ctx, HX.get(), X.get(), theta, R.get(), nb, n, partials.get(), rn2, xn2, s);
+            allreduce(rn2, 2 * nb);
             BE_CUDA(cudaMemcpyAsync(hm->rn2, rn2, nb * 8, cudaMemcpyDeviceToHost, s));
             BE_CUDA(cudaMemcpyAsync(hm->xn2, xn2, nb * 8, cudaMemcpyDeviceToHost, s));
             BE_CUDA(cudaEventRecord(ev.e[4], s));
             sync_status();
             if (hm->st.not_pd) {  // column-scaling fallback of orthonormalize_pair
                 dla::colnorm2(ctx, P.get(), nb, n, partials.get(), pn2, s);
+                allreduce(pn2, nb);
                 dla::scale_columns(ctx, P.get(), HP.get(), pn2, nb, n, st.get(), s);
                 BE_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(dla::Status), s));
             }
@@ -406,7 +432,8 @@ std::unique_ptr<Result> lobpcg_solve(Ctx* ctx, Op* op, be_host_operator_fn host_
     const int nb = cfg.nb > 0 ? cfg.nb : cfg.k + 3;
     // SolverConfig::validate (lobpcg.hpp:38-47) + FomConfig::validate
     if (cfg.k < 1 || cfg.k > nb) fail(BE_ERR_BAD_PARAMS, "SolverConfig: need 1 <= k <= nb");
-    if (static_cast<index_t>(nb) * 3 > n) fail(BE_ERR_BAD_PARAMS, "SolverConfig: operator dimension must be at least 3*nb");
+    const index_t n_all = (op && op->comm) ? op->cuts.back() : n;
+    if (static_cast<index_t>(nb) * 3 > n_all) fail(BE_ERR_BAD_PARAMS, "SolverConfig: operator dimension must be at least 3*nb");
     if (!(cfg.tol > 0.0)) fail(BE_ERR_BAD_PARAMS, "SolverConfig: tol must be positive");
     if (cfg.maxiter < 1) fail(BE_ERR_BAD_PARAMS, "SolverConfig: maxiter must be positive");
     if (cfg.fom_iterations < 1) fail(BE_ERR_BAD_PARAMS, "FomConfig: iterations must be >= 1");
@@ -438,7 +465,8 @@ void* lobpcg_begin(Ctx* ctx, Op* op, be_host_operator_fn host_op, void* host_use
                    const double* x0, const be_solver_config& cfg) {
     const int nb = cfg.nb > 0 ? cfg.nb : cfg.k + 3;
     if (cfg.k < 1 || cfg.k > nb) fail(BE_ERR_BAD_PARAMS, "SolverConfig: need 1 <= k <= nb");
-    if (static_cast<index_t>(nb) * 3 > n) fail(BE_ERR_BAD_PARAMS, "SolverConfig: operator dimension must be at least 3*nb");
+    const index_t n_all = (op && op->comm) ? op->cuts.back() : n;
+    if (static_cast<index_t>(nb) * 3 > n_all) fail(BE_ERR_BAD_PARAMS, "SolverConfig: operator dimension must be at least 3*nb");
     if (!(cfg.tol > 0.0)) fail(BE_ERR_BAD_PARAMS, "SolverConfig: tol must be positive");
     if (cfg.maxiter < 1) fail(BE_ERR_BAD_PARAMS, "SolverConfig: maxiter must be positive");
     if (cfg.fom_iterations < 1) fail(BE_ERR_BAD_PARAMS, "FomConfig: iterations must be >= 1");

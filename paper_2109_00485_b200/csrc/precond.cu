@@ -228,280 +228,474 @@ __global__ void __launch_bounds__(kPT) k_fom(const TileDev* __restrict__ tiles, 
     }
 }
 
-__device__ __forceinline__ double warp_sum(double v) {
+// One CTA of NT threads per (tile, group of C columns): the C columns run
+// their m-step FOM (precond.hpp:143-257) in lock-step. Thread t owns a chunk
+// of CW = 4 adjacent columns (chunk t % (C / 4)) of rows t / (C / 4) + k RL,
+// k < RPT, so one fetched tile entry feeds CW FMAs and the gathered basis
+// row segment is one 32-byte vector read. The Krylov basis V[s][row][col]
+// lives in shared memory (the sparse product gathers arbitrary rows of V_s);
+// w and the per-column Lanczos scalars stay in registers, replicated across
+// the threads of a column chunk (every thread gets the bitwise-identical
+// reduction result, so the tridiagonal solves run redundantly in registers).
+// The tile's entries are staged in shared memory when they fit.
+constexpr int kCW = 4;
+constexpr int kFomCols = 16;  // columns per CTA of the block kernel
+
+template <int C, int NT>
+__device__ __forceinline__ void block_colsum4(double (&v)[kCW], double (*red)[16], int& buf) {
+    constexpr int NW = NT / 32, CQ = C / kCW;
+    // lanes sharing a column chunk differ in the bits above log2(CQ)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;  // butterfly: every lane holds the bitwise-identical total
+    for (int o = CQ; o < 32; o <<= 1)
+#pragma unroll
+        for (int j = 0; j < kCW; ++j) v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
+    if constexpr (NW > 1) {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int cq = threadIdx.x % CQ;
+        if (lane < CQ)
+#pragma unroll
+            for (int j = 0; j < kCW; ++j) red[buf * NW + warp][cq * kCW + j] = v[j];
+        __syncthreads();
+        double t[kCW];
+        {
+            const double2 p0 = reinterpret_cast<const double2*>(&red[buf * NW][cq * kCW])[0];
+            const double2 p1 = reinterpret_cast<const double2*>(&red[buf * NW][cq * kCW])[1];
+            t[0] = p0.x, t[1] = p0.y, t[2] = p1.x, t[3] = p1.y;
+        }
+#pragma unroll
+        for (int w = 1; w < NW; ++w) {
+            const double2 p0 = reinterpret_cast<const double2*>(&red[buf * NW + w][cq * kCW])[0];
+            const double2 p1 = reinterpret_cast<const double2*>(&red[buf * NW + w][cq * kCW])[1];
+            t[0] += p0.x, t[1] += p0.y, t[2] += p1.x, t[3] += p1.y;
+        }
+#pragma unroll
+        for (int j = 0; j < kCW; ++j) v[j] = t[j];
+        buf ^= 1;  // double-buffered: the next reduction cannot overwrite this one before all threads read it
+    }
 }
 
-// One thread group of G threads (a warp, or 4 warps) per (tile, column):
-// the m-step FOM of k_fom with the Krylov basis held in registers (each
-// thread owns rows tid, tid + G, ... up to RM rows) and only the current
-// basis vector in shared memory for the sparse gather. Reductions use warp
-// butterflies (+ a named barrier across the 4 warps when G = 128), all in a
-// fixed order.
-template <int G, int RM, int MC>
-__global__ void __launch_bounds__(256) k_fom_reg(const TileDev* __restrict__ tiles, const std::int32_t* __restrict__ list,
-                                                 int nlist, const std::int32_t* __restrict__ rowptr,
-                                                 const std::uint16_t* __restrict__ cols,
-                                                 const double* __restrict__ vals, const double* __restrict__ shifts,
-                                                 const double* __restrict__ R, double* __restrict__ W, int nb, int m,
-                                                 std::int64_t* fallbacks) {
-    constexpr int NG = 256 / G;  // items per CTA
-    constexpr int DMAX = G * RM;
-    __shared__ double s_vs[NG][DMAX];
-    __shared__ double s_red[NG][G / 32];
-    __shared__ double s_y[NG][MC];
-    __shared__ int s_sing[NG];
-    const int g = threadIdx.x / G, t = threadIdx.x % G, lane = threadIdx.x & 31, wg = t >> 5;
-    const long item = static_cast<long>(blockIdx.x) * NG + g;
-    if (item >= static_cast<long>(nlist) * nb) return;  // whole groups exit together
-    auto gsync = [&]() {
-        if constexpr (G == 32) {
-            __syncwarp();
-        } else {
-            asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(G) : "memory");
-        }
-    };
-    auto gsum = [&](double v) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if constexpr (G == 32) {
-            return v;
-        } else {
-            if (lane == 0) s_red[g][wg] = v;
-            gsync();
-            double tot = 0.0;
-#pragma unroll
-            for (int q = 0; q < G / 32; ++q) tot += s_red[g][q];
-            gsync();
-            return tot;
-        }
-    };
-    const int col = static_cast<int>(item % nb);
-    const TileDev td = tiles[list[item / nb]];
+template <int NT>
+__device__ __forceinline__ void block_sync() {
+    if constexpr (NT == 32) __syncwarp(); else __syncthreads();
+}
+
+struct V4 {
+    double a[kCW];
+};
+__device__ __forceinline__ V4 ld4(const double* p) {  // 32-byte aligned shared-memory read
+    const double2 x = reinterpret_cast<const double2*>(p)[0], y = reinterpret_cast<const double2*>(p)[1];
+    return V4{{x.x, x.y, y.x, y.y}};
+}
+__device__ __forceinline__ void st4(double* p, const double (&v)[kCW]) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
+    reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
+}
+
+template <int MC, int NT, int RPT, bool VSM>
+__global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
+    k_fom_blk(const TileDev* __restrict__ tiles, const std::int32_t* __restrict__ list,
+              const std::int32_t* __restrict__ rowptr, const std::uint16_t* __restrict__ cols,
+              const double* __restrict__ vals, const double* __restrict__ shifts, const double* __restrict__ R,
+              double* __restrict__ W, int nb, int m, int ngroups, std::int64_t* fallbacks, int dmax, int stage_cap,
+              double* __restrict__ Vg, std::int64_t nrows) {
+    constexpr int C = kFomCols;
+    constexpr int CQ = C / kCW;  // column chunks per row
+    constexpr int RL = NT / CQ;  // row lanes
+    extern __shared__ __align__(16) double sV[];  // current basis vector [dmax][C], then the staged entries
+    __shared__ __align__(16) double red[2 * (NT / 32)][16];
+    int rbuf = 0;
+    const int tile = list[blockIdx.x / ngroups];
+    const int grp = blockIdx.x % ngroups;
+    const int col0 = grp * C;
+    const TileDev td = tiles[tile];
     const int d = td.dim;
     const int cap = min(m, d);
+    const int cq = threadIdx.x % CQ, rl = threadIdx.x / CQ;
+    const int c0 = col0 + cq * kCW;  // first global column of the chunk
     const std::int32_t* rp = rowptr + td.ptr_off;
-    const std::uint16_t* cl = cols + td.ent_off;
-    const double* vl = vals + td.ent_off;
-    const double sigma = shifts[col];
-    const double* r = R + td.row_off * nb + col;
-    double* out = W + td.row_off * nb + col;
-    double* vs = s_vs[g];
+    const std::uint16_t* gcl = cols + td.ent_off;
+    const double* gvl = vals + td.ent_off;
+    double sigma[kCW];
+    bool colok[kCW];
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) {
+        colok[j] = c0 + j < nb;
+        sigma[j] = colok[j] ? shifts[c0 + j] : 0.0;
+    }
+    const double* r = R + td.row_off * nb + c0;
+    // VSM: the whole basis V[q][row][C] in shared memory. Otherwise only the
+    // current vector is (the gathers need it) and the older ones, read back
+    // at this thread's own rows only, live in a per-SM scratch slot that stays
+    // in L2 (the launch guarantees one CTA per SM).
+    const std::size_t vstride = static_cast<std::size_t>(dmax) * C;
+    double* Vcur = sV + cq * kCW;
+    double* Vslot = nullptr;
+    if constexpr (!VSM) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        Vslot = Vg + static_cast<std::size_t>(smid) * MC * vstride + cq * kCW;
+    }
+    auto vg = [&](int q, int i) -> double* {
+        if constexpr (VSM) return Vcur + q * vstride + static_cast<std::size_t>(i) * C;
+        else return Vslot + q * vstride + static_cast<std::size_t>(i) * C;
+    };
+    double* Vc = Vcur;  // current vector (advanced per step when VSM)
+    // the tile's entries are read cap times: stage them after the basis
+    const int nent = __ldg(rp + d);
+    double* s_vl = sV + (VSM ? static_cast<std::size_t>(min(m, MC)) : 1) * vstride;
+    std::uint16_t* s_cl = reinterpret_cast<std::uint16_t*>(s_vl + stage_cap);
+    const bool staged = nent <= stage_cap;
+    if (staged)
+        for (int e = threadIdx.x; e < nent; e += NT) {
+            s_vl[e] = __ldg(gvl + e);
+            s_cl[e] = __ldg(gcl + e);
+        }
+    const double* vl = staged ? s_vl : gvl;
+    const std::uint16_t* cl = staged ? s_cl : gcl;
 
-    double V[MC][RM], w[RM];
-    double acc = 0.0;
+    int eb[RPT], ee[RPT];
+    double dg[RPT];
+    double w[RPT][kCW], vp[RPT][kCW];
+    double acc[kCW] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int k = 0; k < RM; ++k) {
-        const int i = t + k * G;
-        const double x = i < d ? r[static_cast<std::int64_t>(i) * nb] : 0.0;
-        V[0][k] = x;
-        acc += x * x;
+    for (int k = 0; k < RPT; ++k) {
+        const int i = rl + k * RL;
+        eb[k] = ee[k] = 0;
+        dg[k] = 0.0;
+#pragma unroll
+        for (int j = 0; j < kCW; ++j) w[k][j] = vp[k][j] = 0.0;
+        if (i < d) {
+            eb[k] = __ldg(rp + i);
+            ee[k] = __ldg(rp + i + 1) - 1;  // the diagonal slot is last
+            dg[k] = __ldg(gvl + ee[k]);
+#pragma unroll
+            for (int j = 0; j < kCW; ++j) {
+                const double x = colok[j] ? r[static_cast<std::int64_t>(i) * nb + j] : 0.0;
+                w[k][j] = x;
+                acc[j] += x * x;
+            }
+        }
     }
-    const double beta0 = sqrt(gsum(acc));
-    if (beta0 == 0.0) {
+    block_colsum4<C, NT>(acc, red, rbuf);
+    double beta0[kCW], inv[kCW];
 #pragma unroll
-        for (int k = 0; k < RM; ++k)
-            if (t + k * G < d) out[static_cast<std::int64_t>(t + k * G) * nb] = 0.0;
-        return;
+    for (int j = 0; j < kCW; ++j) {
+        beta0[j] = sqrt(acc[j]);
+        inv[j] = beta0[j] != 0.0 ? beta0[j] : 1.0;
     }
 #pragma unroll
-    for (int k = 0; k < RM; ++k) V[0][k] /= beta0;
-    double alpha[MC], beta[MC];
-    int steps = cap;
+    for (int k = 0; k < RPT; ++k) {
+        const int i = rl + k * RL;
+        if (i < d) {
+            double v[kCW];
 #pragma unroll
+            for (int j = 0; j < kCW; ++j) v[j] = w[k][j] / inv[j];
+            st4(Vc + static_cast<std::size_t>(i) * C, v);
+            if constexpr (!VSM) st4(vg(0, i), v);
+        }
+    }
+    // Lanczos scalars of the CTA's columns (written by row lane 0; every
+    // thread holds the same values)
+    __shared__ double s_alpha[MC][C], s_beta[MC][C];
+    __shared__ int s_steps[C];
+    double bprev[kCW] = {0.0, 0.0, 0.0, 0.0};
+    int steps[kCW];
+    bool live[kCW];
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) {
+        steps[j] = cap;
+        live[j] = beta0[j] != 0.0;
+    }
+    if (rl == 0)
+        for (int s2 = 0; s2 < MC; ++s2)
+#pragma unroll
+            for (int j = 0; j < kCW; ++j) s_alpha[s2][cq * kCW + j] = s_beta[s2][cq * kCW + j] = 0.0;
+#pragma unroll 1
     for (int s = 0; s < MC; ++s) {
         if (s >= cap) break;
+        block_sync<NT>();  // V_s (and the staged entries) complete
         // w = (K - sigma I) V_s ; alpha_s = V_s . w
 #pragma unroll
-        for (int k = 0; k < RM; ++k)
-            if (t + k * G < d) vs[t + k * G] = V[s][k];
-        gsync();
-        acc = 0.0;
+        for (int j = 0; j < kCW; ++j) acc[j] = 0.0;
+        double vs[RPT][kCW];
 #pragma unroll
-        for (int k = 0; k < RM; ++k) {
-            const int i = t + k * G;
-            double yy = 0.0;
+        for (int k = 0; k < RPT; ++k) {
+            const int i = rl + k * RL;
+            double y[kCW] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int j = 0; j < kCW; ++j) vs[k][j] = 0.0;
             if (i < d) {
-                const int e1 = rp[i + 1] - 1;  // the diagonal slot is last
-                for (int e = rp[i]; e < e1; ++e) yy += vl[e] * vs[cl[e]];
-                yy += (vl[e1] - sigma) * V[s][k];
+                int e = eb[k];
+                for (; e + 1 < ee[k]; e += 2) {
+                    const double a0 = vl[e], a1 = vl[e + 1];
+                    const V4 x0 = ld4(Vc + static_cast<int>(cl[e]) * C);
+                    const V4 x1 = ld4(Vc + static_cast<int>(cl[e + 1]) * C);
+#pragma unroll
+                    for (int j = 0; j < kCW; ++j) y[j] += a0 * x0.a[j];
+#pragma unroll
+                    for (int j = 0; j < kCW; ++j) y[j] += a1 * x1.a[j];
+                }
+                if (e < ee[k]) {
+                    const double a0 = vl[e];
+                    const V4 x0 = ld4(Vc + static_cast<int>(cl[e]) * C);
+#pragma unroll
+                    for (int j = 0; j < kCW; ++j) y[j] += a0 * x0.a[j];
+                }
+                const V4 v = ld4(Vc + static_cast<std::size_t>(i) * C);
+#pragma unroll
+                for (int j = 0; j < kCW; ++j) {
+                    vs[k][j] = v.a[j];
+                    y[j] += (dg[k] - sigma[j]) * v.a[j];
+                    acc[j] += v.a[j] * y[j];
+                }
             }
-            w[k] = yy;
-            acc += V[s][k] * yy;
+#pragma unroll
+            for (int j = 0; j < kCW; ++j) w[k][j] = y[j];
         }
-        const double a = gsum(acc);
-        alpha[s] = a;
+        block_colsum4<C, NT>(acc, red, rbuf);
+        double a[kCW];
+#pragma unroll
+        for (int j = 0; j < kCW; ++j) {
+            a[j] = acc[j];
+            if (live[j] && rl == 0) s_alpha[s][cq * kCW + j] = a[j];
+        }
         if (s + 1 == cap) break;
 #pragma unroll
-        for (int k = 0; k < RM; ++k) {
-            double x = w[k] - a * V[s][k];
-            if (s > 0) x -= beta[s > 0 ? s - 1 : 0] * V[s > 0 ? s - 1 : 0][k];
-            w[k] = x;
+        for (int k = 0; k < RPT; ++k)
+#pragma unroll
+            for (int j = 0; j < kCW; ++j) {
+                double x = w[k][j] - a[j] * vs[k][j];
+                if (s > 0) x -= bprev[j] * vp[k][j];
+                w[k][j] = x;
+            }
+        for (int q = 0; q <= s; ++q) {  // one reorthogonalisation pass, in order
+#pragma unroll
+            for (int j = 0; j < kCW; ++j) acc[j] = 0.0;
+            double vq[RPT][kCW];
+#pragma unroll
+            for (int k = 0; k < RPT; ++k) {
+                const int i = rl + k * RL;
+#pragma unroll
+                for (int j = 0; j < kCW; ++j) vq[k][j] = 0.0;
+                if (i < d) {
+                    const V4 v = q == s ? V4{{vs[k][0], vs[k][1], vs[k][2], vs[k][3]}} : ld4(vg(q, i));
+#pragma unroll
+                    for (int j = 0; j < kCW; ++j) {
+                        vq[k][j] = v.a[j];
+                        acc[j] += v.a[j] * w[k][j];
+                    }
+                }
+            }
+            block_colsum4<C, NT>(acc, red, rbuf);
+#pragma unroll
+            for (int k = 0; k < RPT; ++k)
+#pragma unroll
+                for (int j = 0; j < kCW; ++j) w[k][j] -= acc[j] * vq[k][j];
         }
 #pragma unroll
-        for (int q = 0; q < MC; ++q) {  // one reorthogonalisation pass, in order
-            if (q > s) break;
-            acc = 0.0;
+        for (int j = 0; j < kCW; ++j) acc[j] = 0.0;
 #pragma unroll
-            for (int k = 0; k < RM; ++k) acc += V[q][k] * w[k];
-            const double pr = gsum(acc);
+        for (int k = 0; k < RPT; ++k)
 #pragma unroll
-            for (int k = 0; k < RM; ++k) w[k] -= pr * V[q][k];
+            for (int j = 0; j < kCW; ++j) acc[j] += w[k][j] * w[k][j];
+        block_colsum4<C, NT>(acc, red, rbuf);  // its barrier also retires every gather of V_s
+#pragma unroll
+        for (int j = 0; j < kCW; ++j) {
+            const double nw = sqrt(acc[j]);
+            inv[j] = 1.0;
+            if (live[j]) {
+                if (nw < 1e-14 * beta0[j]) {  // Krylov breakdown
+                    steps[j] = s + 1;
+                    live[j] = false;
+                } else {
+                    if (rl == 0) s_beta[s][cq * kCW + j] = nw;
+                    bprev[j] = nw;
+                    inv[j] = nw;
+                }
+            }
         }
-        acc = 0.0;
 #pragma unroll
-        for (int k = 0; k < RM; ++k) acc += w[k] * w[k];
-        const double nw = sqrt(gsum(acc));
-        if (nw < 1e-14 * beta0) {  // Krylov breakdown
-            steps = s + 1;
-            break;
-        }
-        beta[s] = nw;
-        if (s + 1 < MC) {
+        for (int k = 0; k < RPT; ++k) {
+            const int i = rl + k * RL;
 #pragma unroll
-            for (int k = 0; k < RM; ++k) V[s + 1 < MC ? s + 1 : 0][k] = w[k] / nw;
+            for (int j = 0; j < kCW; ++j) vp[k][j] = vs[k][j];
+            if (i < d) {
+                double v[kCW];
+#pragma unroll
+                for (int j = 0; j < kCW; ++j) v[j] = w[k][j] / inv[j];
+                if constexpr (VSM) {
+                    st4(vg(s + 1, i), v);
+                } else {
+                    st4(Vc + static_cast<std::size_t>(i) * C, v);
+                    st4(vg(s + 1, i), v);
+                }
+            }
         }
-        gsync();  // vs is rewritten by the next step
+        if constexpr (VSM) Vc += vstride;
     }
-    if (t == 0) {  // T y = beta0 e1 by LU with partial pivoting (precond.hpp:208-249)
-        const int st = steps;
+    // T y = beta0 e1 by LU with partial pivoting (precond.hpp:208-249), per
+    // column, by the first row lane of each column chunk; the solutions are
+    // broadcast through shared memory
+    __shared__ double s_y[C][MC];
+    __shared__ int s_sing[C];
+    if (rl == 0)
+#pragma unroll
+        for (int j = 0; j < kCW; ++j) s_steps[cq * kCW + j] = steps[j];
+    block_sync<NT>();
+    if (rl == 0)
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) {
+        double y[MC];
+        int sg = 0;
+        const int cc = cq * kCW + j;
+        const int st = s_steps[cc];
         double T[MC][MC];
         double tmax = 0.0;
 #pragma unroll
         for (int i = 0; i < MC; ++i)
 #pragma unroll
-            for (int j = 0; j < MC; ++j) T[i][j] = 0.0;
-        double y[MC];
+            for (int q = 0; q < MC; ++q) T[i][q] = 0.0;
 #pragma unroll
         for (int i = 0; i < MC; ++i) {
             y[i] = 0.0;
             if (i < st) {
-                T[i][i] = alpha[i];
-                tmax = fmax(tmax, fabs(alpha[i]));
+                T[i][i] = s_alpha[i][cc];
+                tmax = fmax(tmax, fabs(s_alpha[i][cc]));
                 if (i + 1 < st) {
-                    T[i][i + 1 < MC ? i + 1 : 0] = beta[i];
-                    T[i + 1 < MC ? i + 1 : 0][i] = beta[i];
-                    tmax = fmax(tmax, fabs(beta[i]));
+                    T[i][i + 1 < MC ? i + 1 : 0] = s_beta[i][cc];
+                    T[i + 1 < MC ? i + 1 : 0][i] = s_beta[i][cc];
+                    tmax = fmax(tmax, fabs(s_beta[i][cc]));
                 }
             }
         }
         const double floor = 1e-14 * fmax(1.0, tmax);
-        y[0] = beta0;
-        int sing = 0;
-#pragma unroll
-        for (int k = 0; k < MC; ++k) {
-            if (k >= st || sing) break;
+        y[0] = beta0[j];
+        for (int k = 0; k < st; ++k) {
             int piv = k;
-#pragma unroll
-            for (int i = 0; i < MC; ++i)
-                if (i > k && i < st && fabs(T[i][k]) > fabs(T[piv][k])) piv = i;
+            for (int i = k + 1; i < st; ++i)
+                if (fabs(T[i][k]) > fabs(T[piv][k])) piv = i;
             if (fabs(T[piv][k]) < floor) {
-                sing = 1;
+                sg = 1;
                 break;
             }
             if (piv != k) {
-#pragma unroll
-                for (int j = 0; j < MC; ++j) {
-                    const double tmp = T[k][j];
-                    T[k][j] = T[piv][j];
-                    T[piv][j] = tmp;
+                for (int q = 0; q < MC; ++q) {
+                    const double tmp = T[k][q];
+                    T[k][q] = T[piv][q];
+                    T[piv][q] = tmp;
                 }
                 const double tmp = y[k];
                 y[k] = y[piv];
                 y[piv] = tmp;
             }
-#pragma unroll
-            for (int i = 0; i < MC; ++i) {
-                if (i <= k || i >= st) continue;
+            for (int i = k + 1; i < st; ++i) {
                 const double f = T[i][k] / T[k][k];
                 if (f == 0.0) continue;
-#pragma unroll
-                for (int j = 0; j < MC; ++j)
-                    if (j >= k) T[i][j] -= f * T[k][j];
+                for (int q = k; q < st; ++q) T[i][q] -= f * T[k][q];
                 y[i] -= f * y[k];
             }
         }
-        if (!sing) {
-#pragma unroll
-            for (int i = MC - 1; i >= 0; --i) {
-                if (i >= st) continue;
+        if (!sg)
+            for (int i = st - 1; i >= 0; --i) {
                 double a2 = y[i];
-#pragma unroll
-                for (int j = 0; j < MC; ++j)
-                    if (j > i && j < st) a2 -= T[i][j] * y[j];
+                for (int q = i + 1; q < st; ++q) a2 -= T[i][q] * y[q];
                 y[i] = a2 / T[i][i];
             }
-        }
-#pragma unroll
-        for (int i = 0; i < MC; ++i) s_y[g][i] = y[i];
-        s_sing[g] = sing;
-        if (sing && fallbacks) atomicAdd(reinterpret_cast<unsigned long long*>(fallbacks), 1ull);
+        if (colok[j] && beta0[j] != 0.0 && sg && fallbacks)
+            atomicAdd(reinterpret_cast<unsigned long long*>(fallbacks), 1ull);
+        for (int q = 0; q < MC; ++q) s_y[cc][q] = y[q];
+        s_sing[cc] = sg;
     }
-    gsync();
-    const int sing = s_sing[g];
+    block_sync<NT>();
+    double* out = W + td.row_off * nb + c0;
 #pragma unroll
-    for (int k = 0; k < RM; ++k) {
-        const int i = t + k * G;
+    for (int k = 0; k < RPT; ++k) {
+        const int i = rl + k * RL;
         if (i >= d) continue;
-        double o = 0.0;
-        if (sing) {
-            o = r[static_cast<std::int64_t>(i) * nb];  // unpreconditioned fallback column
-        } else {
+        double o[kCW] = {0.0, 0.0, 0.0, 0.0};
+        for (int q = 0; q < cap; ++q) {
+            const V4 v = ld4(vg(q, i));
 #pragma unroll
-            for (int j = 0; j < MC; ++j)
-                if (j < steps) o += s_y[g][j] * V[j][k];
+            for (int j = 0; j < kCW; ++j)
+                if (q < s_steps[cq * kCW + j]) o[j] += s_y[cq * kCW + j][q] * v.a[j];
         }
-        out[static_cast<std::int64_t>(i) * nb] = o;
+#pragma unroll
+        for (int j = 0; j < kCW; ++j) {
+            if (!colok[j]) continue;
+            double res = 0.0;
+            if (beta0[j] != 0.0)
+                res = s_sing[cq * kCW + j] ? r[static_cast<std::int64_t>(i) * nb + j] : o[j];  // fallback: raw column
+            out[static_cast<std::int64_t>(i) * nb + j] = res;
+        }
     }
 }
 
-constexpr int kClassDims[] = {128, 512};  // warp (4 rows / lane), 4 warps (4 rows / thread)
+// size classes of the block kernel: tiles up to kClassDims[c] rows run on
+// CTAs of kClassThreads[c] threads (4 per row, 16 columns per CTA)
+constexpr int kClassDims[] = {32, 64, 128, 256, 512};
+constexpr int kClassThreads[] = {32, 128, 256, 512, 512};
+constexpr bool kClassVsm[] = {true, true, true, true, false};  // whole basis in shared memory
+constexpr std::size_t kOneCtaSmem = 120 * 1024;  // > half an SM: one CTA per SM
+constexpr std::size_t kStageBudget = 200 * 1024;  // current vector + staged entries per CTA
 
 }  // namespace
 
-std::unique_ptr<Tiles> tiles_create(Ctx* ctx, const be_csb_view& L, const double* diag, const index_t* off,
-                                    index_t noff) {
+std::unique_ptr<Tiles> tiles_create(Ctx* ctx, const be_csb_view& L, const double* diag, const index_t* off_all,
+                                    index_t noff_all, index_t row_lo, index_t row_hi) {
     validate_view(L);
     // extract_tiles checks (precond.hpp:65-84)
     if (L.nrows != L.ncols) fail(BE_ERR_DIMENSION_MISMATCH, "extract_tiles: matrix must be square");
-    if (!diag && L.nrows > 0) fail(BE_ERR_DIMENSION_MISMATCH, "extract_tiles: diagonal length mismatch");
-    if (!off || noff < 2 || off[0] != 0 || off[noff - 1] != L.nrows)
+    if (!off_all || noff_all < 2 || off_all[0] != 0 || off_all[noff_all - 1] != L.nrows)
         fail(BE_ERR_BAD_PARAMS, "extract_tiles: tile offsets must cover [0, n)");
+    if (row_lo < 0) row_hi = L.nrows, row_lo = 0;  // whole matrix
+    // the rank's row range (multi-GPU) must be a union of whole tiles
+    const index_t* lo_it = std::lower_bound(off_all, off_all + noff_all, row_lo);
+    const index_t* hi_it = std::lower_bound(off_all, off_all + noff_all, row_hi);
+    if (lo_it == off_all + noff_all || *lo_it != row_lo || hi_it == off_all + noff_all || *hi_it != row_hi ||
+        row_hi < row_lo)
+        fail(BE_ERR_MISALIGNED_TILES, "extract_tiles: row range is not a union of tiles");
+    if (!diag && row_hi > row_lo) fail(BE_ERR_DIMENSION_MISMATCH, "extract_tiles: diagonal length mismatch");
+    // local tile offsets relative to row_lo; panels of the result have row_hi - row_lo rows
+    std::vector<index_t> off_local;
+    for (const index_t* q = lo_it; q <= hi_it; ++q) off_local.push_back(*q - row_lo);
+    const index_t* off = off_local.data();
+    const index_t noff = static_cast<index_t>(off_local.size());
     for (index_t j = 1; j < noff; ++j)
         if (off[j] <= off[j - 1]) fail(BE_ERR_BAD_PARAMS, "extract_tiles: tile offsets must be strictly increasing");
     {
         index_t blk = 0;
-        for (index_t j = 0; j + 1 < noff; ++j) {
-            while (blk + 1 < L.nrowblks + 1 && L.row_offsets[blk + 1] <= off[j]) ++blk;
-            if (off[j + 1] > L.row_offsets[blk + 1])
-                fail(BE_ERR_MISALIGNED_TILES, "extract_tiles: tile [" + std::to_string(off[j]) + ", " +
-                                                  std::to_string(off[j + 1]) + ") straddles a block boundary");
+        for (index_t j = 0; j + 1 < noff_all; ++j) {
+            while (blk + 1 < L.nrowblks + 1 && L.row_offsets[blk + 1] <= off_all[j]) ++blk;
+            if (off_all[j + 1] > L.row_offsets[blk + 1])
+                fail(BE_ERR_MISALIGNED_TILES, "extract_tiles: tile [" + std::to_string(off_all[j]) + ", " +
+                                                  std::to_string(off_all[j + 1]) + ") straddles a block boundary");
         }
     }
     auto t = std::make_unique<Tiles>();
     t->ctx = ctx;
-    t->n = L.nrows;
+    t->n = row_hi - row_lo;
     t->offsets.assign(off, off + noff);
     const index_t nt = noff - 1;
     t->host.resize(static_cast<std::size_t>(nt));
-    std::vector<std::int32_t> owner(static_cast<std::size_t>(L.nrows));
+    std::vector<std::int32_t> owner(static_cast<std::size_t>(t->n));
     for (index_t j = 0; j < nt; ++j) {
         t->host[static_cast<std::size_t>(j)].dim = off[j + 1] - off[j];
         for (index_t i = off[j]; i < off[j + 1]; ++i) owner[static_cast<std::size_t>(i)] = static_cast<std::int32_t>(j);
     }
-    // couplings in to_triples order (csb.hpp:165-185), both orientations
-    for (index_t bi = 0; bi < L.nrowblks; ++bi)
+    // couplings in to_triples order (csb.hpp:165-185), both orientations; only
+    // block rows meeting [row_lo, row_hi) can hold them
+    for (index_t bi = 0; bi < L.nrowblks; ++bi) {
+        if (L.row_offsets[bi + 1] <= row_lo || L.row_offsets[bi] >= row_hi) continue;
         for (index_t bj = 0; bj < L.ncolblks; ++bj) {
             const index_t b = bi * L.ncolblks + bj;
             for (index_t k = L.block_nnz_offsets[b]; k < L.block_nnz_offsets[b] + L.block_nnz[b]; ++k) {
                 const index_t r = L.row_offsets[bi] + L.local_rows[k], c = L.col_offsets[bj] + L.local_cols[k];
                 if (r <= c) fail(BE_ERR_NOT_STRICTLY_LOWER, "extract_tiles: stored entry with row <= col");
-                const auto j = owner[static_cast<std::size_t>(r)];
-                if (j != owner[static_cast<std::size_t>(c)]) continue;
+                if (r < row_lo || r >= row_hi || c < row_lo || c >= row_hi) continue;
+                const auto j = owner[static_cast<std::size_t>(r - row_lo)];
+                if (j != owner[static_cast<std::size_t>(c - row_lo)]) continue;
                 auto& T = t->host[static_cast<std::size_t>(j)];
-                const auto a = static_cast<std::int32_t>(r - off[j]), cc = static_cast<std::int32_t>(c - off[j]);
+                const auto a = static_cast<std::int32_t>(r - row_lo - off[j]), cc = static_cast<std::int32_t>(c - row_lo - off[j]);
                 T.rows.push_back(a);
                 T.cols.push_back(cc);
                 T.vals.push_back(L.values[k]);
@@ -510,6 +704,7 @@ std::unique_ptr<Tiles> tiles_create(Ctx* ctx, const be_csb_view& L, const double
                 T.vals.push_back(L.values[k]);
             }
         }
+    }
     for (index_t j = 0; j < nt; ++j) {  // diagonal slots last
         auto& T = t->host[static_cast<std::size_t>(j)];
         T.diag_pos.resize(static_cast<std::size_t>(T.dim));
@@ -574,6 +769,11 @@ std::unique_ptr<Tiles> tiles_create(Ctx* ctx, const be_csb_view& L, const double
         }
         t->class_begin.push_back(static_cast<index_t>(lists.size()));
         t->big_tiles = t->class_begin.back() - t->class_begin[t->class_dim.size()];
+        t->class_max_ent.assign(t->class_dim.size(), 0);
+        for (std::size_t c = 0; c < t->class_dim.size(); ++c)
+            for (index_t q = t->class_begin[c]; q < t->class_begin[c + 1]; ++q)
+                t->class_max_ent[c] = std::max<index_t>(
+                    t->class_max_ent[c], static_cast<index_t>(t->host[static_cast<std::size_t>(lists[static_cast<std::size_t>(q)])].vals.size()));
         t->class_tiles.reset(std::max<index_t>(static_cast<index_t>(lists.size()), 1));
         if (!lists.empty())
             BE_CUDA(cudaMemcpy(t->class_tiles.get(), lists.data(), lists.size() * 4, cudaMemcpyHostToDevice));
@@ -595,18 +795,47 @@ void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, i
         const index_t b0 = t->class_begin[static_cast<std::size_t>(c)], b1 = t->class_begin[static_cast<std::size_t>(c) + 1];
         if (b1 == b0) continue;
         const int dmax = t->class_dim[static_cast<std::size_t>(c)];
-        const index_t items = (b1 - b0) * nb;
+        const int C = kFomCols;
+        const int ngroups = (nb + C - 1) / C;
         const std::int32_t* list = t->class_tiles.get() + b0;
-        const int nl = static_cast<int>(b1 - b0);
-#define BE_FOMR(G, MC)                                                                                              \
-    k_fom_reg<G, 4, MC><<<static_cast<unsigned>((items + 256 / G - 1) / (256 / G)), 256, 0, s>>>(               \
-        tdv, list, nl, t->rowptr.get(), t->cols.get(), t->vals.get(), shifts, R, W, nb, m, fallbacks)
-        if (dmax <= 128) {
-            if (m <= 4) BE_FOMR(32, 4); else BE_FOMR(32, 8);
-        } else {
-            if (m <= 4) BE_FOMR(128, 4); else BE_FOMR(128, 8);
+        const int mc = m <= 4 ? 4 : 8;
+        const std::size_t vone = static_cast<std::size_t>(dmax) * C * sizeof(double);
+        const bool vsm = kClassVsm[c] && vone * std::min(m, mc) <= 160 * 1024;  // else: per-SM slots
+        const std::size_t vbytes = vone * (vsm ? std::min(m, mc) : 1);
+        // entry staging: up to the class's largest tile, within the smem budget
+        const std::size_t room = vbytes < kStageBudget ? (kStageBudget - vbytes) / 10 : 0;
+        const int stage_cap = static_cast<int>(std::min<std::size_t>(room, static_cast<std::size_t>(t->class_max_ent[static_cast<std::size_t>(c)]))) & ~7;
+        std::size_t sm = vbytes + static_cast<std::size_t>(stage_cap) * 10;
+        const unsigned grid = static_cast<unsigned>((b1 - b0) * ngroups);
+        if (!vsm) {  // per-SM basis slots: one CTA per SM
+            sm = std::max(sm, kOneCtaSmem);
+            const index_t vneed = static_cast<index_t>(mc) * t->ctx->num_sms * dmax * C;
+            if (t->vscratch.n < vneed) t->vscratch.reset(vneed);
         }
-#undef BE_FOMR
+#define BE_FOMB(MC, NTT, RPT, VS)                                                                                  \
+    do {                                                                                                           \
+        ensure_dyn_smem(k_fom_blk<MC, NTT, RPT, VS>, sm);                                                          \
+        k_fom_blk<MC, NTT, RPT, VS><<<grid, NTT, sm, s>>>(tdv, list, t->rowptr.get(), t->cols.get(), t->vals.get(), \
+                                                           shifts, R, W, nb, m, ngroups, fallbacks, dmax,          \
+                                                           stage_cap, t->vscratch.get(), t->n);                    \
+    } while (0)
+#define BE_FOMB2(NTT, RPT)                      \
+    if (mc == 4) {                              \
+        if (vsm) BE_FOMB(4, NTT, RPT, true);    \
+        else BE_FOMB(4, NTT, RPT, false);       \
+    } else {                                    \
+        if (vsm) BE_FOMB(8, NTT, RPT, true);    \
+        else BE_FOMB(8, NTT, RPT, false);       \
+    }
+        switch (c) {
+            case 0: BE_FOMB2(32, 4); break;    // 8 rows per pass x 4
+            case 1: BE_FOMB2(128, 2); break;   // 32 x 2
+            case 2: BE_FOMB2(256, 2); break;   // 64 x 2
+            case 3: BE_FOMB2(512, 2); break;   // 128 x 2
+            default: BE_FOMB2(512, 4); break;  // 128 x 4
+        }
+#undef BE_FOMB2
+#undef BE_FOMB
         BE_CUDA(cudaGetLastError());
         ++t->ctx->launches;
     }
@@ -621,7 +850,7 @@ void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, i
     while (gc > 1 && (gc > nb * 2 || static_cast<std::size_t>(gc) * per_col > kSmemBudget)) gc /= 2;
     if (per_col > 200 * 1024) fail(BE_ERR_BAD_PARAMS, "apply_preconditioner: tile too large for the device kernel");
     const std::size_t sm = static_cast<std::size_t>(gc) * per_col;
-    BE_CUDA(cudaFuncSetAttribute(k_fom, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));  // static smem counts too
+    ensure_dyn_smem(k_fom, sm);
     const int ngroups = (nb + gc - 1) / gc;
     const index_t grid = nbig * ngroups;
     k_fom<<<static_cast<unsigned>(grid), kPT, sm, s>>>(tdv, t->rowptr.get(), t->cols.get(), t->vals.get(), shifts, R, W,

@@ -28,15 +28,20 @@ struct Tiles {
     // dim <= class_dim[c] (and > the previous class) listed in class_tiles
     std::vector<int> class_dim;
     std::vector<index_t> class_begin;  // into class_tiles, size = classes + 1
+    std::vector<index_t> class_max_ent;  // largest tile (stored entries) per class
     DBuf<std::int32_t> class_tiles;
     index_t big_tiles = 0;             // tiles above the last class (CTA kernel)
     DBuf<std::int32_t> rowptr;
     DBuf<std::uint16_t> cols;
     DBuf<double> vals;
+    DBuf<double> vscratch;  // older Krylov vectors of the block kernel (L2-resident per CTA)
 };
 
+// extract_tiles + upload; [row_lo, row_hi) restricts the result to the tiles
+// of one rank's rows (multi-GPU; diag then holds those rows only). row_lo < 0:
+// the whole matrix.
 std::unique_ptr<Tiles> tiles_create(Ctx* ctx, const be_csb_view& L, const double* diag, const index_t* off,
-                                    index_t noff);
+                                    index_t noff, index_t row_lo = -1, index_t row_hi = -1);
 void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, index_t nrows, int nb, int m,
                    std::int64_t* fallbacks, cudaStream_t s);
 

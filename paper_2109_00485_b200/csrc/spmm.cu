@@ -34,8 +34,11 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <numeric>
 
+#include "comm.hpp"
 #include "device.hpp"
 
 namespace be {
@@ -463,21 +466,18 @@ std::size_t smem_bytes(int max_nnz) {
 }
 
 template <int NBP, typename TC, typename TV, typename TX>
-void launch_tiles(Op* op, const TX* X, TX* Y, int nb, int do_r, int do_c, cudaStream_t s) {
+void launch_tiles(Op* op, const int2* runs, index_t nruns, const TX* X, TX* Y, int nb, int do_r, int do_c,
+                  cudaStream_t s) {
     auto kern = k_sym_spmm<NBP, TC, TV, TX>;
     const std::size_t sm = smem_bytes<NBP, TC, TV, TX>(op->max_nnz);
-    static std::size_t cached_sm = 0;
-    static int per_sm = 0;
-    if (cached_sm != sm) {
-        BE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-        BE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, sm));
-        cached_sm = sm;
-    }
+    ensure_dyn_smem(kern, sm);
+    int per_sm = 0;
+    BE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, sm));
     if (per_sm < 1) fail(BE_ERR_CUDA, "sym_spmm: kernel does not fit on an SM");
-    const int grid = static_cast<int>(std::min<index_t>(static_cast<index_t>(per_sm) * op->ctx->num_sms, op->nruns));
+    const int grid = static_cast<int>(std::min<index_t>(static_cast<index_t>(per_sm) * op->ctx->num_sms, nruns));
     op->grid = grid;
     if (grid == 0) return;
-    kern<<<grid, kThreads, sm, s>>>(op->runs.get(), static_cast<int>(op->nruns), op->tiles.get(), op->lens.get(),
+    kern<<<grid, kThreads, sm, s>>>(runs, static_cast<int>(nruns), op->tiles.get(), op->lens.get(),
                                     reinterpret_cast<const TV*>(op->vals.get()), op->rc.get(), op->cperm.get(), X, Y,
                                     nb, do_r, do_c, op->max_nnz, op->counter.get());
     BE_CUDA(cudaGetLastError());
@@ -485,13 +485,14 @@ void launch_tiles(Op* op, const TX* X, TX* Y, int nb, int do_r, int do_c, cudaSt
 }
 
 template <typename TC, typename TV, typename TX>
-void dispatch_nb(Op* op, const TX* X, TX* Y, int nb, int do_r, int do_c, cudaStream_t s) {
+void dispatch_nb(Op* op, const int2* runs, index_t nruns, const TX* X, TX* Y, int nb, int do_r, int do_c,
+                 cudaStream_t s) {
     constexpr int VEC = Vec<TC>::N;
-    if (nb <= VEC) return launch_tiles<VEC, TC, TV, TX>(op, X, Y, nb, do_r, do_c, s);
-    if (nb <= 8) return launch_tiles<8, TC, TV, TX>(op, X, Y, nb, do_r, do_c, s);
-    if (nb <= 16) return launch_tiles<16, TC, TV, TX>(op, X, Y, nb, do_r, do_c, s);
-    if (nb <= 32) return launch_tiles<32, TC, TV, TX>(op, X, Y, nb, do_r, do_c, s);
-    if (nb <= 64) return launch_tiles<64, TC, TV, TX>(op, X, Y, nb, do_r, do_c, s);
+    if (nb <= VEC) return launch_tiles<VEC, TC, TV, TX>(op, runs, nruns, X, Y, nb, do_r, do_c, s);
+    if (nb <= 8) return launch_tiles<8, TC, TV, TX>(op, runs, nruns, X, Y, nb, do_r, do_c, s);
+    if (nb <= 16) return launch_tiles<16, TC, TV, TX>(op, runs, nruns, X, Y, nb, do_r, do_c, s);
+    if (nb <= 32) return launch_tiles<32, TC, TV, TX>(op, runs, nruns, X, Y, nb, do_r, do_c, s);
+    if (nb <= 64) return launch_tiles<64, TC, TV, TX>(op, runs, nruns, X, Y, nb, do_r, do_c, s);
     fail(BE_ERR_BAD_PARAMS, "sym_spmm: nb > 64 is not supported by the device kernel");
 }
 
@@ -505,6 +506,27 @@ struct RowOut {
     std::vector<double> v;            // values in device order (converted on upload)
     std::vector<std::uint16_t> rc, cp;
     std::vector<std::int64_t> src;    // CSB index per device entry (optional)
+    std::vector<unsigned char> cls;   // per tile: 0 interior, 1 exterior (distributed operator)
+};
+
+// Padded coordinates of the distributed operator: row r of segment q maps to
+// q * lmax + (r - cuts[q]).
+struct RowMap {
+    const index_t* cuts = nullptr;
+    int world = 1, rank = 0;
+    index_t lmax = 0;
+    int seg(index_t r) const {
+        int lo = 0, hi = world;  // cuts[lo] <= r < cuts[hi]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) / 2;
+            if (cuts[mid] <= r) lo = mid; else hi = mid;
+        }
+        return lo;
+    }
+    index_t pad(index_t r) const {
+        const int q = seg(r);
+        return static_cast<index_t>(q) * lmax + (r - cuts[q]);
+    }
 };
 
 std::vector<std::uint16_t>& tls_colpos() {
@@ -599,7 +621,7 @@ void emit_piece(const be_csb_view& L, const std::vector<std::uint64_t>& ent, ind
     }
 }
 
-void build_block_row(const be_csb_view& L, index_t bi, int max_nnz, bool keep_src, RowOut& out) {
+void build_block_row(const be_csb_view& L, index_t bi, int max_nnz, bool keep_src, const RowMap* map, RowOut& out) {
     const index_t br = L.row_offsets[bi + 1] - L.row_offsets[bi];
     const index_t ta = (br + kTile - 1) / kTile;
     struct BlockBuckets {  // one CSB block's entries bucketed by (a, b) sub-tile
@@ -629,8 +651,14 @@ void build_block_row(const be_csb_view& L, index_t bi, int max_nnz, bool keep_sr
     }
     std::vector<std::uint64_t> keys, piece;
     index_t pos = 0;
+    const int row_seg = map ? map->seg(L.row_offsets[bi]) : 0;
     for (index_t a = 0; a < ta; ++a) {
+      for (int pass = 0; pass < (map ? 2 : 1); ++pass) {  // interior tiles first
         for (const auto& bb : blocks) {
+            if (map) {
+                const bool interior = row_seg == map->rank && map->seg(L.col_offsets[bb.bj]) == map->rank;
+                if (interior != (pass == 0)) continue;
+            }
             for (index_t b = 0; b < bb.tb; ++b) {
                 const std::size_t s0 = static_cast<std::size_t>(bb.start[static_cast<std::size_t>(a * bb.tb + b)]);
                 const std::size_t s1 = static_cast<std::size_t>(bb.start[static_cast<std::size_t>(a * bb.tb + b + 1)]);
@@ -655,11 +683,14 @@ void build_block_row(const be_csb_view& L, index_t bi, int max_nnz, bool keep_sr
                         if (p1 == p0) fail(BE_ERR_BAD_PARAMS, "tile row longer than max_nnz");
                     }
                     piece.assign(keys.begin() + static_cast<std::ptrdiff_t>(p0), keys.begin() + static_cast<std::ptrdiff_t>(p1));
-                    emit_piece(L, piece, row0, col0, nr, nc, keep_src, pos, out);
+                    emit_piece(L, piece, map ? map->pad(row0) : row0, map ? map->pad(col0) : col0, nr, nc, keep_src,
+                               pos, out);
+                    out.cls.push_back(static_cast<unsigned char>(pass));
                     p0 = p1;
                 }
             }
         }
+      }
     }
 }
 
@@ -676,11 +707,28 @@ void upload_values(unsigned char* dst, const std::vector<double>& v) {
 
 }  // namespace
 
+static void op_build(Op* op, const be_csb_view& L, const RowMap* map);
+
 Ctx::~Ctx() {}
+
+void ensure_dyn_smem_raw(const void* kern, std::size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, std::size_t> cur;
+    int dev = 0;
+    BE_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    std::size_t& c = cur[{dev, kern}];
+    if (bytes <= c) return;
+    BE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+    c = bytes;
+}
 
 Op::~Op() {
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
+    if (ev_x) cudaEventDestroy(ev_x);
+    if (ev_ag) cudaEventDestroy(ev_ag);
+    if (cstream) cudaStreamDestroy(cstream);
 }
 
 std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag, int values_prec, int flags) {
@@ -700,12 +748,24 @@ std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag
     }
     if (L.nrows >= (index_t{1} << 31) || L.ncols >= (index_t{1} << 31))
         fail(BE_ERR_BAD_PARAMS, "sym_spmm: dimension exceeds 2^31 rows per device");
+    op_build(op.get(), L, nullptr);
+    if (op->symmetric) {
+        op->diag.reset(std::max<index_t>(L.nrows, 1));
+        if (L.nrows > 0)
+            BE_CUDA(cudaMemcpy(op->diag.get(), diag, static_cast<std::size_t>(L.nrows) * 8, cudaMemcpyHostToDevice));
+    }
+    return op;
+}
+
+// Tile-format build + upload shared by the single- and multi-GPU operators.
+static void op_build(Op* op, const be_csb_view& L, const RowMap* map) {
+    const int values_prec = op->values_prec;
     op->max_nnz = values_prec == BE_F32 ? 2048 : 1024;
     const bool keep_src = L.nnz <= (index_t{1} << 26);
 
     std::vector<RowOut> rows(static_cast<std::size_t>(L.nrowblks));
     parallel_for_dynamic(hw_threads(), L.nrowblks, [&](index_t bi, int) {
-        build_block_row(L, bi, op->max_nnz, keep_src, rows[static_cast<std::size_t>(bi)]);
+        build_block_row(L, bi, op->max_nnz, keep_src, map, rows[static_cast<std::size_t>(bi)]);
     });
     index_t ntiles = 0, padded = 0;
     for (const auto& r : rows) {
@@ -726,11 +786,14 @@ std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag
     if (keep_src) op->csb_index.reserve(static_cast<std::size_t>(padded));
     std::vector<TileHdr> all_hdr;
     all_hdr.reserve(static_cast<std::size_t>(ntiles));
+    std::vector<unsigned char> all_cls;
+    all_cls.reserve(static_cast<std::size_t>(ntiles));
     index_t t_off = 0, e_off = 0;
     for (auto& r : rows) {
         if (r.hdr.empty()) continue;
         for (auto& h : r.hdr) h.begin8 += static_cast<std::uint32_t>(e_off / 8);
         all_hdr.insert(all_hdr.end(), r.hdr.begin(), r.hdr.end());
+        all_cls.insert(all_cls.end(), r.cls.begin(), r.cls.end());
         BE_CUDA(cudaMemcpy(op->lens.get() + t_off * 256, r.lens.data(), r.lens.size(), cudaMemcpyHostToDevice));
         if (values_prec == BE_F32)
             upload_values<float>(op->vals.get() + e_off * 4, r.v);
@@ -745,33 +808,101 @@ std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag
     }
     if (ntiles > 0)
         BE_CUDA(cudaMemcpy(op->tiles.get(), all_hdr.data(), all_hdr.size() * sizeof(TileHdr), cudaMemcpyHostToDevice));
-    {  // runs: consecutive tiles of one tile-row, at most kRunMax tiles each
-        std::vector<int2> runs;
+    {  // runs: consecutive tiles of one tile-row and class, at most kRunMax tiles each
+        std::vector<int2> runs[2];
         for (index_t t = 0; t < ntiles;) {
+            const auto& h0 = all_hdr[static_cast<std::size_t>(t)];
+            const unsigned char c0 = all_cls[static_cast<std::size_t>(t)];
             index_t e = t + 1;
-            while (e < ntiles && e - t < kRunMax &&
-                   all_hdr[static_cast<std::size_t>(e)].row0 == all_hdr[static_cast<std::size_t>(t)].row0)
+            while (e < ntiles && e - t < kRunMax && all_hdr[static_cast<std::size_t>(e)].row0 == h0.row0 &&
+                   all_cls[static_cast<std::size_t>(e)] == c0)
                 ++e;
-            runs.push_back(make_int2(static_cast<int>(t), static_cast<int>(e)));
+            runs[c0].push_back(make_int2(static_cast<int>(t), static_cast<int>(e)));
             t = e;
         }
-        op->nruns = static_cast<index_t>(runs.size());
+        op->nruns = static_cast<index_t>(runs[0].size());
         op->runs.reset(std::max<index_t>(op->nruns, 1));
-        if (!runs.empty())
-            BE_CUDA(cudaMemcpy(op->runs.get(), runs.data(), runs.size() * sizeof(int2), cudaMemcpyHostToDevice));
+        if (!runs[0].empty())
+            BE_CUDA(cudaMemcpy(op->runs.get(), runs[0].data(), runs[0].size() * sizeof(int2), cudaMemcpyHostToDevice));
+        op->nruns_ext = static_cast<index_t>(runs[1].size());
+        op->runs_ext.reset(std::max<index_t>(op->nruns_ext, 1));
+        if (!runs[1].empty())
+            BE_CUDA(cudaMemcpy(op->runs_ext.get(), runs[1].data(), runs[1].size() * sizeof(int2),
+                               cudaMemcpyHostToDevice));
     }
-    if (op->symmetric) {
-        op->diag.reset(std::max<index_t>(L.nrows, 1));
-        if (L.nrows > 0)
-            BE_CUDA(cudaMemcpy(op->diag.get(), diag, static_cast<std::size_t>(L.nrows) * 8, cudaMemcpyHostToDevice));
+}
+
+// Distributed apply (row e): Y_local = (L + L^T + D) X over all ranks.
+//   1. X_local (f64) -> its f32 segment of the padded exchange panel; the
+//      f32 accumulator (world * lmax rows) is zeroed in the same pass.
+//   2. allgather of the f32 segments on the communication stream, overlapped
+//      with the interior tiles (both coordinates in this rank's segment).
+//   3. the remaining tiles once the gather has landed.
+//   4. reduce-scatter of the partial Y panels to the row owners, then
+//      Y_local = D X_local + y in f64 (the diagonal pass, kernels.hpp:363-370).
+// This is distributed_spmm (dist.hpp:256-371) on NCCL collectives.
+static void op_apply_dist(Op* op, const double* X, double* Y, index_t in_rows, int nb, cudaStream_t s) {
+    if (in_rows != op->nlocal) fail(BE_ERR_DIMENSION_MISMATCH, "distributed apply: local rows mismatch");
+    const index_t seg = op->lmax * nb, tot = seg * op->world;
+    if (op->x32.n < tot) {
+        op->x32.reset(tot);
+        op->y32.reset(tot);
     }
-    return op;
+    if (!op->cstream) {
+        BE_CUDA(cudaStreamCreateWithFlags(&op->cstream, cudaStreamNonBlocking));
+        BE_CUDA(cudaEventCreateWithFlags(&op->ev_x, cudaEventDisableTiming));
+        BE_CUDA(cudaEventCreateWithFlags(&op->ev_ag, cudaEventDisableTiming));
+    }
+    if (op->timing) {
+        for (auto& e : op->ev)
+            if (!e) BE_CUDA(cudaEventCreate(&e));
+        BE_CUDA(cudaEventRecord(op->ev[0], s));
+    }
+    float* xs = op->x32.get() + static_cast<index_t>(op->rank) * seg;
+    const int g = static_cast<int>(std::max<index_t>(1, std::min<index_t>((tot + 255) / 256, op->ctx->num_sms * 8)));
+    k_f64_to_f32<<<g, 256, 0, s>>>(X, xs, op->nlocal * nb, op->y32.get(), tot);
+    BE_CUDA(cudaGetLastError());
+    ++op->ctx->launches;
+    BE_CUDA(cudaEventRecord(op->ev_x, s));
+    BE_CUDA(cudaStreamWaitEvent(op->cstream, op->ev_x, 0));
+    op->comm->allgather_f32(xs, op->x32.get(), static_cast<std::size_t>(seg), op->cstream);
+    BE_CUDA(cudaEventRecord(op->ev_ag, op->cstream));
+    if (op->timing) BE_CUDA(cudaEventRecord(op->ev[1], s));
+    if (op->nruns > 0)
+        dispatch_nb<float, float, float>(op, op->runs.get(), op->nruns, op->x32.get(), op->y32.get(), nb, 1, 1, s);
+    BE_CUDA(cudaStreamWaitEvent(s, op->ev_ag, 0));
+    if (op->nruns_ext > 0)
+        dispatch_nb<float, float, float>(op, op->runs_ext.get(), op->nruns_ext, op->x32.get(), op->y32.get(), nb, 1, 1,
+                                         s);
+    float* ys = op->y32.get() + static_cast<index_t>(op->rank) * seg;
+    op->comm->reduce_scatter_f32(op->y32.get(), ys, static_cast<std::size_t>(seg), s);
+    if (op->nlocal > 0) {
+        const index_t out = op->nlocal * nb;
+        const int g2 = static_cast<int>(std::max<index_t>(1, std::min<index_t>((out + 255) / 256, op->ctx->num_sms * 8)));
+        k_finish_f64<<<g2, 256, 0, s>>>(op->diag.get(), X, ys, Y, op->nlocal, nb, 1);
+        BE_CUDA(cudaGetLastError());
+        ++op->ctx->launches;
+    }
+    if (op->timing) {
+        BE_CUDA(cudaEventRecord(op->ev[2], s));
+        BE_CUDA(cudaEventSynchronize(op->ev[2]));
+        float a = 0, k = 0;
+        BE_CUDA(cudaEventElapsedTime(&a, op->ev[0], op->ev[2]));
+        BE_CUDA(cudaEventElapsedTime(&k, op->ev[1], op->ev[2]));
+        op->last_apply_ms = a;
+        op->last_kernel_ms = k;
+    }
 }
 
 void op_apply(Op* op, const void* X, void* Y, index_t in_rows, int nb, int panel_prec, int mode, cudaStream_t s) {
     if (nb < 1) fail(BE_ERR_DIMENSION_MISMATCH, "apply: nb must be positive");
     if (panel_prec != BE_F32 && panel_prec != BE_F64) fail(BE_ERR_BAD_PARAMS, "apply: panel_prec must be BE_F32 or BE_F64");
     if (X == Y) fail(BE_ERR_BAD_PARAMS, "spmm: W and U must not alias");
+    if (op->comm) {
+        if (mode != BE_APPLY_SYMMETRIC || panel_prec != BE_F64)
+            fail(BE_ERR_BAD_PARAMS, "distributed apply: symmetric mode on f64 panels only");
+        return op_apply_dist(op, static_cast<const double*>(X), static_cast<double*>(Y), in_rows, nb, s);
+    }
     int do_r = 0, do_c = 0;
     index_t out_rows = 0;
     switch (mode) {
@@ -817,7 +948,7 @@ void op_apply(Op* op, const void* X, void* Y, index_t in_rows, int nb, int panel
         BE_CUDA(cudaGetLastError());
         ++op->ctx->launches;
         if (op->timing) BE_CUDA(cudaEventRecord(op->ev[1], s));
-        if (op->ntiles > 0) dispatch_nb<float, float, float>(op, op->x32.get(), op->y32.get(), nb, do_r, do_c, s);
+        if (op->ntiles > 0) dispatch_nb<float, float, float>(op, op->runs.get(), op->nruns, op->x32.get(), op->y32.get(), nb, do_r, do_c, s);
         if (out_tot > 0) {
             k_finish_f64<<<grid_for(out_tot), 256, 0, s>>>(op->diag.get(), static_cast<const double*>(X), op->y32.get(),
                                                             static_cast<double*>(Y), out_rows, nb,
@@ -839,12 +970,12 @@ void op_apply(Op* op, const void* X, void* Y, index_t in_rows, int nb, int panel
         if (op->timing) BE_CUDA(cudaEventRecord(op->ev[1], s));
         if (op->ntiles > 0) {
             if (op->values_prec == BE_F32) {
-                dispatch_nb<float, float, float>(op, static_cast<const float*>(X), static_cast<float*>(Y), nb, do_r, do_c, s);
+                dispatch_nb<float, float, float>(op, op->runs.get(), op->nruns, static_cast<const float*>(X), static_cast<float*>(Y), nb, do_r, do_c, s);
             } else {
                 if (panel_prec == BE_F32)
-                    dispatch_nb<double, double, float>(op, static_cast<const float*>(X), static_cast<float*>(Y), nb, do_r, do_c, s);
+                    dispatch_nb<double, double, float>(op, op->runs.get(), op->nruns, static_cast<const float*>(X), static_cast<float*>(Y), nb, do_r, do_c, s);
                 else
-                    dispatch_nb<double, double, double>(op, static_cast<const double*>(X), static_cast<double*>(Y), nb, do_r, do_c, s);
+                    dispatch_nb<double, double, double>(op, op->runs.get(), op->nruns, static_cast<const double*>(X), static_cast<double*>(Y), nb, do_r, do_c, s);
             }
         }
     }
@@ -857,6 +988,113 @@ void op_apply(Op* op, const void* X, void* Y, index_t in_rows, int nb, int panel
         op->last_apply_ms = a;
         op->last_kernel_ms = k;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU partition (row e). Both rules are integer-exact so every rank (and
+// the Python restatement in tests/) derives the same cuts.
+// ---------------------------------------------------------------------------
+
+// Equal-rows panel ownership on block boundaries: cut p is the boundary
+// closest to n * p / world (the lower one on ties), kept strictly increasing
+// so every rank owns at least one block row.
+std::vector<index_t> dist_rows(const index_t* b, index_t nbounds, int world) {
+    const index_t nblk = nbounds - 1;
+    if (world < 1) fail(BE_ERR_BAD_PARAMS, "dist_rows: world must be positive");
+    if (nblk < world) fail(BE_ERR_BAD_PARAMS, "dist_rows: fewer block rows than ranks");
+    const index_t n = b[nblk];
+    std::vector<index_t> k(static_cast<std::size_t>(world) + 1);
+    k[0] = 0;
+    k[static_cast<std::size_t>(world)] = nblk;
+    for (int p = 1; p < world; ++p) {
+        const __int128 target = static_cast<__int128>(n) * p;  // compare b * world with n * p
+        index_t best = 0;
+        __int128 bestd = -1;
+        for (index_t j = 0; j <= nblk; ++j) {
+            __int128 dd = static_cast<__int128>(b[j]) * world - target;
+            if (dd < 0) dd = -dd;
+            if (bestd < 0 || dd < bestd) {
+                bestd = dd;
+                best = j;
+            }
+        }
+        k[static_cast<std::size_t>(p)] = best;
+    }
+    for (int p = 1; p < world; ++p)  // strictly increasing, room for the ranks after p
+        k[static_cast<std::size_t>(p)] = std::min(std::max(k[static_cast<std::size_t>(p)], k[static_cast<std::size_t>(p) - 1] + 1),
+                                                  nblk - (world - p));
+    std::vector<index_t> cuts(static_cast<std::size_t>(world) + 1);
+    for (int p = 0; p <= world; ++p) cuts[static_cast<std::size_t>(p)] = b[k[static_cast<std::size_t>(p)]];
+    return cuts;
+}
+
+// Contiguous weight balance: cut p = first item index whose prefix weight
+// reaches total * p / world. Slabs may be empty; the result is item indices.
+std::vector<index_t> dist_balance(const index_t* w, index_t nitems, int world) {
+    if (world < 1) fail(BE_ERR_BAD_PARAMS, "dist_balance: world must be positive");
+    std::vector<index_t> cuts(static_cast<std::size_t>(world) + 1, nitems);
+    cuts[0] = 0;
+    __int128 total = 0;
+    for (index_t i = 0; i < nitems; ++i) {
+        if (w[i] < 0) fail(BE_ERR_BAD_PARAMS, "dist_balance: negative weight");
+        total += w[i];
+    }
+    __int128 pre = 0;
+    index_t i = 0;
+    for (int p = 1; p < world; ++p) {
+        const __int128 target = total * p;
+        while (i < nitems && pre * world < target) pre += w[i++];
+        cuts[static_cast<std::size_t>(p)] = i;
+    }
+    return cuts;
+}
+
+std::unique_ptr<Op> op_create_dist(Ctx* ctx, Comm* comm, const be_csb_view& L, const index_t* cuts,
+                                   const double* diag_local, int values_prec) {
+    validate_view(L);
+    if (!comm) fail(BE_ERR_BAD_PARAMS, "distributed operator: null communicator");
+    if (values_prec != BE_F32) fail(BE_ERR_BAD_PARAMS, "distributed operator: f32 values only");
+    if (L.nrows != L.ncols) fail(BE_ERR_DIMENSION_MISMATCH, "SymmetricOperator: matrix must be square");
+    if (L.nrowblks != L.ncolblks) fail(BE_ERR_DIMENSION_MISMATCH, "distributed operator: row and column blocks differ");
+    for (index_t i = 0; i <= L.nrowblks; ++i)
+        if (L.row_offsets[i] != L.col_offsets[i])
+            fail(BE_ERR_DIMENSION_MISMATCH, "distributed operator: row and column blocks differ");
+    if (!is_strictly_lower(L)) fail(BE_ERR_NOT_STRICTLY_LOWER, "SymmetricOperator: stored entry with row <= col");
+    const int world = comm->world, rank = comm->rank;
+    if (cuts[0] != 0 || cuts[world] != L.nrows) fail(BE_ERR_BAD_PARAMS, "distributed operator: cuts must cover [0, n)");
+    for (int p = 0; p < world; ++p) {
+        if (cuts[p + 1] < cuts[p]) fail(BE_ERR_BAD_PARAMS, "distributed operator: cuts must be non-decreasing");
+        const index_t* e = std::lower_bound(L.row_offsets, L.row_offsets + L.nrowblks + 1, cuts[p]);
+        if (e == L.row_offsets + L.nrowblks + 1 || *e != cuts[p])
+            fail(BE_ERR_MISALIGNED_TILES, "distributed operator: cut " + std::to_string(cuts[p]) + " is not a block boundary");
+    }
+    auto op = std::make_unique<Op>();
+    op->ctx = ctx;
+    op->comm = comm;
+    op->rank = rank;
+    op->world = world;
+    op->cuts.assign(cuts, cuts + world + 1);
+    op->lmax = 1;
+    for (int p = 0; p < world; ++p) op->lmax = std::max(op->lmax, cuts[p + 1] - cuts[p]);
+    op->row_lo = cuts[rank];
+    op->nlocal = cuts[rank + 1] - cuts[rank];
+    if (op->lmax * world >= (index_t{1} << 31)) fail(BE_ERR_BAD_PARAMS, "distributed operator: padded dimension exceeds 2^31");
+    op->nrows = op->ncols = op->nlocal;
+    op->nnz = L.nnz;
+    op->values_prec = values_prec;
+    op->symmetric = true;
+    RowMap map;
+    map.cuts = op->cuts.data();
+    map.world = world;
+    map.rank = rank;
+    map.lmax = op->lmax;
+    op_build(op.get(), L, &map);
+    op->diag.reset(std::max<index_t>(op->nlocal, 1));
+    if (op->nlocal > 0) {
+        if (!diag_local) fail(BE_ERR_DIMENSION_MISMATCH, "SymmetricOperator: diagonal length mismatch");
+        BE_CUDA(cudaMemcpy(op->diag.get(), diag_local, static_cast<std::size_t>(op->nlocal) * 8, cudaMemcpyHostToDevice));
+    }
+    return op;
 }
 
 }  // namespace be

@@ -1,0 +1,220 @@
+"""Multi-GPU path on one B200: the ranks are host threads sharing
+an in-process communicator group (the same distributed operator / solver code
+as under NCCL, only the three collectives differ), plus NCCL at world 1.
+
+Bars: distributed SpMM = single-GPU SpMM = oracle within 1e-5 relative
+(fp32 values); distributed LOBPCG eigenvalues within 1e-6 of the oracle and
+of the single-GPU solve, iterations within +-1 (preconditioner off; on, within
++-1 of the single-GPU count); the device tile format of every rank decodes
+back to exactly its slab's entries."""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle_lib as ol
+from paper_2109_00485_b200 import abi
+
+pytestmark = pytest.mark.gpu
+
+
+def run_ranks(world, fn):
+    group = abi.CommGroup(world)
+    out = [None] * world
+    errs = []
+
+    def worker(r):
+        try:
+            ctx = abi.Context(0)
+            comm = abi.Comm(ctx, group=group, rank=r)
+            out[r] = fn(r, ctx, comm)
+            comm.close()
+            ctx.close()
+        except BaseException as e:  # noqa: BLE001
+            errs.append((r, e))
+            group.abort()  # peers blocked in a collective fail with ProtocolDeadlock instead of hanging
+
+    ts = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    if errs:
+        first = [e for _, e in errs if not isinstance(e, abi.ProtocolDeadlock)] or [errs[0][1]]
+        raise first[0]
+    assert not any(t.is_alive() for t in ts), "a rank did not finish"
+    group.close()
+    return out
+
+
+def problem(n=6000, density=0.004, extent=1000, seed=3):
+    s = abi.Synthetic("random", n=n, density=density, block_extent=extent, seed=seed)
+    b = abi.uniform_boundaries(n, extent)
+    m = abi.build_csb_coo(s.lower, n, n, b, b)
+    return m, s.diag, s.tile_offsets
+
+
+def partition(m, world):
+    cuts = abi.dist_rows(m.row_offsets, world)
+    slabs = abi.dist_balance(m.block_row_nnz(), world)
+    return cuts, slabs
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_dist_spmm_matches_single_and_oracle(ctx, world):
+    m, diag, _ = problem()
+    n, nb = m.nrows, 16
+    x = np.random.default_rng(5).uniform(-1, 1, (n, nb))
+    cuts, slabs = partition(m, world)
+
+    def rank(r, c, comm):
+        op = abi.DistOperator(c, comm, m.slab(int(slabs[r]), int(slabs[r + 1])), cuts, diag[cuts[r]:cuts[r + 1]])
+        y = op.apply_host(x[cuts[r]:cuts[r + 1]])
+        y2 = op.apply_host(x[cuts[r]:cuts[r + 1]])  # the exchange buffers are reused
+        info = comm.info()
+        op.close()
+        return y, y2, info
+
+    res = run_ranks(world, rank)
+    y = np.vstack([a for a, _, _ in res])
+    assert all(np.array_equal(a, b) or np.linalg.norm(a - b) <= 1e-6 * np.linalg.norm(a) for a, b, _ in res)
+    want = ol.Impl("orc").spmm(m, diag, x)
+    single = abi.Operator(ctx, m, diag).apply_host(x)
+    assert np.linalg.norm(y - want) / np.linalg.norm(want) <= 1e-5
+    assert np.linalg.norm(y - single) / np.linalg.norm(single) <= 1e-6
+    assert all(i["backend"] == "local" and i["calls"] == 4 for _, _, i in res)  # AG + RS per apply
+
+
+def test_dist_decode_is_the_slab(ctx):
+    m, diag, _ = problem(n=3000, extent=500)
+    world = 3
+    cuts, slabs = partition(m, world)
+    trip = m.to_triples()
+
+    def rank(r, c, comm):
+        sl = m.slab(int(slabs[r]), int(slabs[r + 1]))
+        op = abi.DistOperator(c, comm, sl, cuts, diag[cuts[r]:cuts[r + 1]], values_prec=abi.BE_F32)
+        rows, cols, vals, idx = op.decode()
+        st = sl.to_triples()
+        op.close()
+        return rows, cols, vals, idx, st
+
+    res = run_ranks(world, rank)
+    total = 0
+    for rows, cols, vals, idx, st in res:
+        # device entry -> slab CSB index -> the same (row, col, f32(value))
+        assert np.array_equal(rows, st["row"][idx]) and np.array_equal(cols, st["col"][idx])
+        assert np.array_equal(vals, st["value"][idx].astype(np.float32).astype(np.float64))
+        assert np.array_equal(np.sort(idx), np.arange(len(st)))
+        total += len(st)
+    assert total == len(trip)
+
+
+def test_dist_rejects_misaligned_cuts(ctx):
+    m, diag, _ = problem(n=3000, extent=500)
+
+    def rank(r, c, comm):
+        cuts = np.array([0, 1234, 3000])  # 1234 is not a block boundary
+        with pytest.raises(abi.MisalignedTiles):
+            abi.DistOperator(c, comm, m.slab(0, 6) if r == 0 else m.slab(6, 6), cuts, diag[:1234] if r == 0 else diag[1234:])
+        return True
+
+    assert all(run_ranks(2, rank))
+
+
+@pytest.mark.parametrize("precond", [False, True])
+@pytest.mark.parametrize("world", [2, 3])
+def test_dist_lobpcg_matches_single(ctx, world, precond):
+    m, diag, toff = problem(n=6000, density=0.003, extent=1000, seed=11)
+    n, k, nb = m.nrows, 8, 16
+    cuts, slabs = partition(m, world)
+    tiles = abi.Tiles(ctx, m, diag, toff) if precond else None
+    single = abi.lobpcg(ctx, abi.Operator(ctx, m, diag), tiles=tiles, k=k, nb=nb, tol=1e-6, maxiter=300, seed=1)
+    want = ol.Impl("orc").lobpcg(m, diag, k=k, nb=nb, tol=1e-6, maxiter=300, seed=1,
+                                 toff=toff if precond else None)
+
+    def rank(r, c, comm):
+        op = abi.DistOperator(c, comm, m.slab(int(slabs[r]), int(slabs[r + 1])), cuts, diag[cuts[r]:cuts[r + 1]])
+        t = abi.Tiles(c, m, diag[cuts[r]:cuts[r + 1]], toff, row_range=(int(cuts[r]), int(cuts[r + 1]))) \
+            if precond else None
+        res = abi.lobpcg(c, op, tiles=t, k=k, nb=nb, tol=1e-6, maxiter=300, seed=1)
+        op.close()
+        return res
+
+    res = run_ranks(world, rank)
+    lam = res[0]["lambda_"]
+    assert all(np.array_equal(r["lambda_"], lam) for r in res)  # identical decisions on every rank
+    assert all(r["iterations"] == res[0]["iterations"] for r in res)
+    assert res[0]["converged"]
+    assert np.max(np.abs(lam - want["lambda_"]) / np.abs(want["lambda_"])) <= 1e-6
+    assert np.max(np.abs(lam - single["lambda_"]) / np.abs(single["lambda_"])) <= 1e-6
+    its = res[0]["iterations"]
+    if not precond:
+        assert abs(its - single["iterations"]) <= 1
+        assert abs(its - want["iterations"]) <= 1
+    else:  # the count follows the summation order: the reference's envelope + the single-GPU solve, +-1
+        from test_lobpcg_gpu import envelope
+        lo, hi = envelope(m, diag, toff, k=k, nb=nb, tol=1e-6, maxiter=300, seed=1)
+        lo, hi = min(lo, single["iterations"]), max(hi, single["iterations"])
+        assert lo - 1 <= its <= hi + 1, (its, lo, hi)
+    # the distributed eigenvectors are the single-GPU ones, row-partitioned
+    x = np.vstack([r["x"] for r in res])
+    for v in range(k):
+        a, b = x[:, v], single["x"][:, v]
+        cos = abs(a @ b) / (np.linalg.norm(a) * np.linalg.norm(b))
+        assert cos > 1 - 1e-6
+
+
+def test_dist_x0_slices_match_global_random_block(ctx):
+    """X0 of rank r is rows [cuts[r], cuts[r+1]) of random_block(n, nb, seed)
+    (block_vector.hpp:47-53): one solve step from the same start agrees."""
+    m, diag, _ = problem(n=3000, density=0.004, extent=500, seed=2)
+    world, k, nb = 2, 4, 8
+    cuts, slabs = partition(m, world)
+    single = abi.lobpcg(ctx, abi.Operator(ctx, m, diag), k=k, nb=nb, tol=1e-300, maxiter=1, seed=9)
+
+    def rank(r, c, comm):
+        op = abi.DistOperator(c, comm, m.slab(int(slabs[r]), int(slabs[r + 1])), cuts, diag[cuts[r]:cuts[r + 1]])
+        res = abi.lobpcg(c, op, k=k, nb=nb, tol=1e-300, maxiter=1, seed=9)
+        op.close()
+        return res
+
+    res = run_ranks(world, rank)
+    other = abi.lobpcg(ctx, abi.Operator(ctx, m, diag), k=k, nb=nb, tol=1e-300, maxiter=1, seed=10)
+    # same start: Ritz values agree to f32-SpMM rounding; another seed's start is far off
+    assert np.allclose(res[0]["theta"][0], single["theta"][0], rtol=1e-7, atol=0)
+    assert not np.allclose(other["theta"][0], single["theta"][0], rtol=1e-4, atol=0)
+
+
+def test_failing_rank_releases_peers(ctx):
+    """A rank that fails before a collective must not hang the others: they
+    get ProtocolDeadlock (dist.hpp:256-263), the failure itself surfaces."""
+    m, diag, _ = problem(n=3000, extent=500)
+    cuts, slabs = partition(m, 2)
+
+    def rank(r, c, comm):
+        if r == 1:
+            raise abi.BadParams("rank 1 gives up")
+        op = abi.DistOperator(c, comm, m.slab(int(slabs[r]), int(slabs[r + 1])), cuts, diag[cuts[r]:cuts[r + 1]])
+        op.apply_host(np.zeros((int(cuts[1] - cuts[0]), 4)))
+
+    with pytest.raises(abi.BadParams):
+        run_ranks(2, rank)
+
+
+def test_nccl_world1(ctx):
+    m, diag, _ = problem(n=3000, extent=500)
+    uid = abi.nccl_unique_id()
+    comm = abi.Comm(ctx, nccl_id=uid, rank=0, world=1)
+    cuts = np.array([0, m.nrows])
+    op = abi.DistOperator(ctx, comm, m, cuts, diag)
+    x = np.random.default_rng(1).uniform(-1, 1, (m.nrows, 16))
+    y = op.apply_host(x)
+    want = abi.Operator(ctx, m, diag).apply_host(x)
+    assert np.linalg.norm(y - want) / np.linalg.norm(want) <= 1e-6
+    assert comm.info()["backend"] == "nccl"
+    res = abi.lobpcg(ctx, op, k=4, nb=8, tol=1e-6, maxiter=200, seed=1)
+    ref = abi.lobpcg(ctx, abi.Operator(ctx, m, diag), k=4, nb=8, tol=1e-6, maxiter=200, seed=1)
+    assert np.allclose(res["lambda_"], ref["lambda_"], rtol=1e-9)
+    op.close()
+    comm.close()
