@@ -16,8 +16,13 @@ copy bandwidth of MEASURED_PEAKS.json.
                   [--config t1|c1] [--nb 16] [--nev 8] [--precond on|off]
                   [--no-cpu-baseline]
 
-Under torchrun (N > 1) every rank solves its own copy of the problem
-(replicas; the 2D-partitioned distributed solver is not implemented yet).
+Under torchrun (N > 1) the distributed solver runs (weak scaling):
+the Test-1-shaped problem is scaled to n = 2.9e6 N rows and 1.1e9 N stored
+nonzeros; every rank generates only its nnz-balanced slab of block rows (and
+the diagonal blocks of its panel rows for the preconditioner), the X panel is
+allgathered and partial Y panels reduce-scattered with NCCL, and the Gram /
+norm partials are allreduced. `value` is the whole-job algorithmic bytes per
+second; timing is the max over ranks of CUDA-event time.
 """
 from __future__ import annotations
 
@@ -216,18 +221,119 @@ def workload(a, cfg, m):
             "panels": "f64"}
 
 
+def run_dist(a, rank, world, local):
+    """Weak-scaled distributed LOBPCG (one rank per GPU, NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2109_00485_b200 import abi
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = dict(CONFIGS[a.config])
+    if cfg["kind"] != "clustered":
+        raise SystemExit("--gpus > 1 runs the clustered weak-scaling problem (--config t1)")
+    n, nnz = cfg["n"] * world, cfg["nnz"] * world
+    precond = a.precond == "on"
+    p = abi.clustered_params(n=n, target_nnz=nnz, block_extent=cfg["extent"], tile=cfg["tile"], fill=cfg["fill"],
+                             block_occupancy=cfg["block_occupancy"], seed=a.seed)
+    from paper_2109_00485_b200 import weak
+    ctx = abi.Context(local)
+    uid = [abi.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = abi.Comm(ctx, nccl_id=uid[0], rank=rank, world=world)
+
+    def allreduce_sum(x):
+        t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+        dist.all_reduce(t)
+        return t.cpu().numpy()
+
+    t0 = time.time()
+    rp = weak.rank_problem(ctx, comm, p, rank, world, precond, allreduce_sum)
+    t_setup = time.time() - t0
+    op, tiles, cuts, slabs, lo, hi = rp["op"], rp["tiles"], rp["cuts"], rp["slabs"], rp["lo"], rp["hi"]
+    nnz_local = rp["nnz_local"]
+    stats = allreduce_sum(np.array([float(nnz_local), float(rp["tile_entries"])]))
+    nnz_tot, ent_tot = int(stats[0]), int(stats[1])
+    b_spmm, b_iter = alg_bytes(n, nnz_tot, a.nb, ent_tot, precond)
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    solver = abi.IncrementalSolve(ctx, op, tiles=tiles, k=a.nev, nb=a.nb, tol=1e-300,
+                                  maxiter=a.warmup + a.steps + 1, seed=a.seed)
+    solver.step(a.warmup)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = ctx.launches()
+    ev0.record(stream)
+    done = solver.step(a.steps)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = ctx.launches() - l0
+    clk = clocks.stop()
+    tt = torch.tensor([ev0.elapsed_time(ev1)], device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms = float(tt.item())
+    res = solver.end()
+    rec = res["times"][a.warmup:a.warmup + done]
+    spmm_ms = 1e3 * float(np.mean(rec[:, 0])) if len(rec) else float("nan")
+    peak, peak_kind = measured_peak()
+    # roofline of this rank's share of the SpMM (its slab + its panel rows), whole distributed apply
+    b_spmm_local = 8 * nnz_local + 2 * (hi - lo) * a.nb * 8 + 8 * (hi - lo)
+    ach = b_spmm_local / (spmm_ms * 1e-3) / 1e9
+    # end to end through the solve call with host buffers (x0 in, eigenvectors out)
+    x0 = np.random.default_rng(a.seed + rank).uniform(-1, 1, (hi - lo, a.nb))
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0 = time.perf_counter()
+    r2 = abi.lobpcg(ctx, op, tiles=tiles, x0=x0, k=a.nev, nb=a.nb, tol=1e-300, maxiter=a.steps, seed=a.seed)
+    e_s = torch.tensor([time.perf_counter() - e0], device="cuda", dtype=torch.float64)
+    dist.all_reduce(e_s, op=dist.ReduceOp.MAX)
+    e_s = float(e_s.item())
+    info = comm.info()
+    line = {
+        "metric": METRIC, "value": b_iter * done / (t_ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world,
+        "steps": done, "warmup": a.warmup, "ms_per_step": t_ms / max(done, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 SpMM / f64 dense", "data": "synthetic",
+        "config": {"workload": f"t1 weak-scaled x{world}: n={n}, half-nnz={nnz_tot}, nev={a.nev}, block k={a.nb}, "
+                               f"precond {a.precond}", "n": n, "nnz": nnz_tot, "nb": a.nb, "nev": a.nev,
+                   "precond": precond, "generator": cfg, "parallelism": f"dist{world} (row panels + nnz-balanced "
+                   "SpMM slabs, NCCL allgather/reduce-scatter/allreduce)",
+                   "l2": "inputs larger than L2 (matrix stream 8 B/nnz >> 126 MB)", "values": "f32", "panels": "f64"},
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "traffic": None, "kernel": "distributed sym_spmm apply on rank 0 (slab SpMM + exchange)",
+                     "bytes_per_launch": b_spmm_local, "ms_per_launch": spmm_ms, "peak_kind": peak_kind},
+        "cpu_baseline": None,
+        "e2e": {"value": b_iter * r2["iterations"] / e_s / 1e9, "unit": "GB/s",
+                "h2d_bytes_per_step": int(x0.nbytes * world / max(r2["iterations"], 1)),
+                "d2h_bytes_per_step": int((n * a.nev * 8 + a.nev * 8 * world) / max(r2["iterations"], 1)),
+                "iterations": r2["iterations"], "seconds": e_s},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "lobpcg": {"iter_ms": t_ms / max(done, 1), "spmm_ms": spmm_ms,
+                   "precond_ms": 1e3 * float(np.mean(rec[:, 1])) if len(rec) else None,
+                   "setup_s": {"generate_and_upload": t_setup}, "parallelism": f"dist{world}",
+                   "comm": {"backend": info["backend"], "calls": info["calls"], "bytes_rank0": info["bytes"]},
+                   "cuts": [int(c) for c in cuts], "slabs": [int(c) for c in slabs]},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    op.close()
+    comm.close()
+    dist.destroy_process_group()
+
+
 def main():
     a = args_parse()
     rank, world, local = dist_env()
     if a.impl == "reference":
         return run_reference(a, rank)
+    if world > 1:
+        return run_dist(a, rank, world, local)
     import torch
 
     from paper_2109_00485_b200 import abi
     torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = CONFIGS[a.config]
     precond = a.precond == "on"
     t0 = time.time()
@@ -248,8 +354,6 @@ def main():
                                   maxiter=a.warmup + a.steps + 1, seed=a.seed)
     solver.step(a.warmup)
     torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
     clocks = ClockSampler(local)
     clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -261,10 +365,6 @@ def main():
     launches = ctx.launches() - l0
     clk = clocks.stop()
     t_ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        tt = torch.tensor([t_ms], device="cuda")
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_ms = float(tt.item())
     res = solver.end()
     rec = res["times"][a.warmup:a.warmup + done]
     spmm_ms = 1e3 * float(np.mean(rec[:, 0])) if len(rec) else float("nan")
@@ -304,12 +404,9 @@ def main():
         "gpu_launches": launches,
         "clocks": clk,
         "lobpcg": {"iter_ms": ms_step, "spmm_ms": spmm_ms, "precond_ms": 1e3 * float(np.mean(rec[:, 1])),
-                   "setup_s": {"generate": t_gen, "upload": t_up}, "parallelism": "replicas" if world > 1 else "1 GPU"},
+                   "setup_s": {"generate": t_gen, "upload": t_up}, "parallelism": "1 GPU"},
     }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

@@ -164,6 +164,18 @@ typedef struct be_cluster_params {
 } be_cluster_params;
 be_status be_generate_clustered(const be_cluster_params* p, be_csb** out, double** diag,
                                 int64_t** tile_offsets, int64_t* n_tile_offsets);
+/* One rank's part of the same matrix (multi-GPU weak scaling): block rows
+ * [brow_begin, brow_end) as a CSB of the global shape (diag_blocks_only: just
+ * their diagonal blocks), the part's contribution to sum|row| of all n rows
+ * (sum the parts over ranks, then be_clustered_diag), and the tile offsets. */
+be_status be_generate_clustered_part(const be_cluster_params* p, int64_t brow_begin, int64_t brow_end,
+                                     int diag_blocks_only, be_csb** out, double** rowabs,
+                                     int64_t** tile_offsets, int64_t* n_tile_offsets);
+/* diag[i - row_begin] = 0.5 + U_i(0, diag_spread) + dominance * rowabs[i - row_begin] */
+be_status be_clustered_diag(const be_cluster_params* p, const double* rowabs, int64_t row_begin, int64_t row_end,
+                            double* diag);
+/* expected stored nonzeros per CSB block row (the slab weights, no generation) */
+be_status be_clustered_weights(const be_cluster_params* p, int64_t* weights, int64_t* nblk);
 
 /* ------------------------------------------------------------------------- */
 /* Device context and the symmetric operator (SymmetricOperator,             */

@@ -311,6 +311,44 @@ def generate_clustered(n, target_nnz, block_extent=4000, tile=128, fill=0.10, bl
     return Csb._from_handle(h), diag, toff
 
 
+def clustered_params(n, target_nnz, block_extent=4000, tile=128, fill=0.10, block_occupancy=1.0, tile_min=4,
+                     tile_max=512, diag_spread=5.0, dominance=1.0, seed=1, threads=0):
+    return ClusterParams(n, target_nnz, block_extent, tile, fill, block_occupancy, tile_min, tile_max, diag_spread,
+                         dominance, seed, threads)
+
+
+def generate_clustered_part(params: ClusterParams, brow_begin: int, brow_end: int, diag_blocks_only=False):
+    """Block rows [brow_begin, brow_end) of the clustered matrix (global shape):
+    (csb, rowabs contribution over all n rows, tile offsets)."""
+    h = C.c_void_p()
+    rp = C.POINTER(C.c_double)()
+    tp = C.POINTER(C.c_int64)()
+    nt = C.c_int64()
+    check(lib().be_generate_clustered_part(C.byref(params), C.c_int64(brow_begin), C.c_int64(brow_end),
+                                           C.c_int(1 if diag_blocks_only else 0), C.byref(h), C.byref(rp),
+                                           C.byref(tp), C.byref(nt)))
+    rowabs = np.ctypeslib.as_array(rp, shape=(params.n,)).copy()
+    toff = np.ctypeslib.as_array(tp, shape=(nt.value,)).copy()
+    lib().be_free_buffer(rp)
+    lib().be_free_buffer(tp)
+    return Csb._from_handle(h), rowabs, toff
+
+
+def clustered_diag(params: ClusterParams, rowabs, row_begin: int, row_end: int) -> np.ndarray:
+    r = np.ascontiguousarray(rowabs, dtype=np.float64)
+    out = np.zeros(row_end - row_begin)
+    check(lib().be_clustered_diag(C.byref(params), _p(r), C.c_int64(row_begin), C.c_int64(row_end), _p(out)))
+    return out
+
+
+def clustered_weights(params: ClusterParams) -> np.ndarray:
+    nb = C.c_int64()
+    check(lib().be_clustered_weights(C.byref(params), None, C.byref(nb)))
+    w = np.zeros(nb.value, np.int64)
+    check(lib().be_clustered_weights(C.byref(params), _p(w), C.byref(nb)))
+    return w
+
+
 # ------------------------------------------------------------------------ device
 class Context:
     def __init__(self, device: int = 0):

@@ -160,6 +160,41 @@ be_status be_generate_clustered(const be_cluster_params* p, be_csb** out, double
     });
 }
 
+be_status be_generate_clustered_part(const be_cluster_params* p, int64_t brow_begin, int64_t brow_end,
+                                     int diag_blocks_only, be_csb** out, double** rowabs,
+                                     int64_t** tile_offsets, int64_t* n_tile_offsets) {
+    return guard([&] {
+        if (!p || !out || !rowabs || !tile_offsets || !n_tile_offsets) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        std::vector<double> r;
+        std::vector<int64_t> t;
+        auto m = be::generate_clustered_part(*p, brow_begin, brow_end, diag_blocks_only != 0, r, t);
+        *rowabs = static_cast<double*>(std::malloc(r.size() * sizeof(double)));
+        std::memcpy(*rowabs, r.data(), r.size() * sizeof(double));
+        *tile_offsets = static_cast<int64_t*>(std::malloc(t.size() * sizeof(int64_t)));
+        std::memcpy(*tile_offsets, t.data(), t.size() * sizeof(int64_t));
+        *n_tile_offsets = static_cast<int64_t>(t.size());
+        *out = new be_csb{std::move(m)};
+    });
+}
+
+be_status be_clustered_diag(const be_cluster_params* p, const double* rowabs, int64_t row_begin, int64_t row_end,
+                            double* diag) {
+    return guard([&] {
+        if (!p || (!rowabs && row_end > row_begin) || (!diag && row_end > row_begin)) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        if (row_begin < 0 || row_end < row_begin || row_end > p->n) be::fail(BE_ERR_BAD_PARAMS, "be_clustered_diag: bad row range");
+        for (int64_t i = row_begin; i < row_end; ++i) diag[i - row_begin] = be::clustered_diag_value(*p, i, rowabs[i - row_begin]);
+    });
+}
+
+be_status be_clustered_weights(const be_cluster_params* p, int64_t* weights, int64_t* nblk) {
+    return guard([&] {
+        if (!p || !nblk) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        const auto w = be::clustered_block_row_weights(*p);
+        *nblk = static_cast<int64_t>(w.size());
+        if (weights) std::memcpy(weights, w.data(), w.size() * sizeof(int64_t));
+    });
+}
+
 // ------------------------------------------------------------------ context
 be_status be_ctx_create(int device, be_ctx** out) {
     return guard([&] {

@@ -535,8 +535,9 @@ struct ClusterPlan {
 };
 }  // namespace
 
-std::unique_ptr<CsbHost> generate_clustered(const be_cluster_params& p, std::vector<double>& diag,
-                                            std::vector<index_t>& tile_offsets) {
+// Plan shared by the whole-matrix and the slab generators: the boundaries
+// and the occupied-tile rate p_tile that meets target_nnz on average.
+static ClusterPlan make_plan(const be_cluster_params& p) {
     if (p.n < 10) fail(BE_ERR_BAD_PARAMS, "generate_clustered: n must be at least 10");
     if (p.block_extent < 1 || p.block_extent > kMaxBlockExtent) fail(BE_ERR_BAD_PARAMS, "generate_clustered: bad block extent");
     if (p.tile < 1 || p.tile > p.block_extent) fail(BE_ERR_BAD_PARAMS, "generate_clustered: bad tile");
@@ -544,15 +545,12 @@ std::unique_ptr<CsbHost> generate_clustered(const be_cluster_params& p, std::vec
     if (!(p.block_occupancy > 0.0 && p.block_occupancy <= 1.0)) fail(BE_ERR_BAD_PARAMS, "generate_clustered: bad block occupancy");
     if (p.target_nnz < 0) fail(BE_ERR_BAD_PARAMS, "generate_clustered: negative target");
     if (p.tile_min < 1 || p.tile_max < p.tile_min) fail(BE_ERR_BAD_PARAMS, "generate_clustered: bad tile size range");
-    const int nw = p.threads > 0 ? p.threads : hw_threads();
-
     ClusterPlan plan(p);
     plan.bounds = uniform_boundaries(p.n, p.block_extent);
     plan.nblk = static_cast<index_t>(plan.bounds.size()) - 1;
     const index_t nblk = plan.nblk;
     const auto& B = plan.bounds;
     auto ntiles_of = [&](index_t len) { return (len + p.tile - 1) / p.tile; };
-
     // expected area: diagonal tiles of diagonal blocks (strict lower part)
     // always, the other lower tiles of occupied blocks at rate p_tile
     double diag_area = 0.0, other_area = 0.0;
@@ -569,7 +567,17 @@ std::unique_ptr<CsbHost> generate_clustered(const be_cluster_params& p, std::vec
     }
     const double want_area = static_cast<double>(p.target_nnz) / p.fill;
     plan.p_tile = other_area > 0 ? std::clamp((want_area - diag_area) / other_area, 0.0, 1.0) : 0.0;
+    return plan;
+}
 
+// Block rows [b0, b1) of the clustered matrix as a CSB of the global shape;
+// diag_only keeps only the diagonal blocks (a rank's preconditioner tiles).
+// The entries are exactly those of the whole-matrix generator.
+static std::unique_ptr<CsbHost> clustered_rows(const ClusterPlan& plan, index_t b0, index_t b1, bool diag_only, int nw) {
+    const auto& p = plan.p;
+    const index_t nblk = plan.nblk;
+    const auto& B = plan.bounds;
+    auto ntiles_of = [&](index_t len) { return (len + p.tile - 1) / p.tile; };
     auto m = std::make_unique<CsbHost>();
     m->nrows = m->ncols = p.n;
     m->nrowblks = m->ncolblks = nblk;
@@ -577,12 +585,13 @@ std::unique_ptr<CsbHost> generate_clustered(const be_cluster_params& p, std::vec
     m->col_offsets = B;
     m->block_nnz.assign(static_cast<std::size_t>(nblk * nblk), 0);
     m->block_nnz_offsets.assign(static_cast<std::size_t>(nblk * nblk), 0);
-
+    auto wanted = [&](index_t bi, index_t bj) { return plan.block_on(bi, bj) && (!diag_only || bi == bj); };
     // pass 1: counts per block (gap stream only)
-    parallel_for_dynamic(nw, nblk, [&](index_t bi, int) {
+    parallel_for_dynamic(nw, b1 - b0, [&](index_t q, int) {
+        const index_t bi = b0 + q;
         const index_t br = B[bi + 1] - B[bi];
         for (index_t bj = 0; bj <= bi; ++bj) {
-            if (!plan.block_on(bi, bj)) continue;
+            if (!wanted(bi, bj)) continue;
             const index_t bc = B[bj + 1] - B[bj];
             index_t c = 0;
             for (index_t a = 0; a < ntiles_of(br); ++a)
@@ -599,10 +608,11 @@ std::unique_ptr<CsbHost> generate_clustered(const be_cluster_params& p, std::vec
     }
     m->allocate(acc);
     // pass 2: fill
-    parallel_for_dynamic(nw, nblk, [&](index_t bi, int) {
+    parallel_for_dynamic(nw, b1 - b0, [&](index_t q, int) {
+        const index_t bi = b0 + q;
         const index_t br = B[bi + 1] - B[bi];
         for (index_t bj = 0; bj <= bi; ++bj) {
-            if (!plan.block_on(bi, bj)) continue;
+            if (!wanted(bi, bj)) continue;
             const index_t bc = B[bj + 1] - B[bj];
             index_t k = m->block_nnz_offsets[static_cast<std::size_t>(bi * nblk + bj)];
             for (index_t a = 0; a < ntiles_of(br); ++a)
@@ -616,34 +626,89 @@ std::unique_ptr<CsbHost> generate_clustered(const be_cluster_params& p, std::vec
                         });
         }
     });
+    return m;
+}
 
-    // diagonal: 0.5 + U(0, spread) + dominance * sum|row| (synth.hpp:147-157
-    // rule), sums in a fixed order (row part by block row, column part by
-    // block column) so the bytes never depend on the thread count
-    std::vector<double> rsum(static_cast<std::size_t>(p.n), 0.0), csum(static_cast<std::size_t>(p.n), 0.0);
-    parallel_for_dynamic(nw, nblk, [&](index_t bi, int) {
+// sum |row| of the stored entries of m, row part and column part kept apart
+// (each summed in a fixed order so the bytes never depend on the thread count)
+static void abs_sums(const CsbHost& m, index_t b0, index_t b1, std::vector<double>& rsum, std::vector<double>& csum,
+                     int nw) {
+    const index_t nblk = m.nrowblks;
+    const auto& B = m.row_offsets;
+    rsum.assign(static_cast<std::size_t>(m.nrows), 0.0);
+    csum.assign(static_cast<std::size_t>(m.nrows), 0.0);
+    parallel_for_dynamic(nw, b1 - b0, [&](index_t q, int) {
+        const index_t bi = b0 + q;
         for (index_t bj = 0; bj <= bi; ++bj) {
             const index_t b = bi * nblk + bj;
-            const index_t k0 = m->block_nnz_offsets[static_cast<std::size_t>(b)], k1 = k0 + m->block_nnz[static_cast<std::size_t>(b)];
-            for (index_t k = k0; k < k1; ++k) rsum[static_cast<std::size_t>(B[bi] + m->local_rows[k])] += std::abs(m->values[k]);
+            const index_t k0 = m.block_nnz_offsets[static_cast<std::size_t>(b)], k1 = k0 + m.block_nnz[static_cast<std::size_t>(b)];
+            for (index_t k = k0; k < k1; ++k) rsum[static_cast<std::size_t>(B[bi] + m.local_rows[k])] += std::abs(m.values[k]);
         }
     });
     parallel_for_dynamic(nw, nblk, [&](index_t bj, int) {
-        for (index_t bi = bj; bi < nblk; ++bi) {
+        for (index_t bi = std::max(bj, b0); bi < b1; ++bi) {
             const index_t b = bi * nblk + bj;
-            const index_t k0 = m->block_nnz_offsets[static_cast<std::size_t>(b)], k1 = k0 + m->block_nnz[static_cast<std::size_t>(b)];
-            for (index_t k = k0; k < k1; ++k) csum[static_cast<std::size_t>(B[bj] + m->local_cols[k])] += std::abs(m->values[k]);
+            const index_t k0 = m.block_nnz_offsets[static_cast<std::size_t>(b)], k1 = k0 + m.block_nnz[static_cast<std::size_t>(b)];
+            for (index_t k = k0; k < k1; ++k) csum[static_cast<std::size_t>(B[bj] + m.local_cols[k])] += std::abs(m.values[k]);
         }
     });
+}
+
+double clustered_diag_value(const be_cluster_params& p, index_t i, double rowabs) {
+    std::uint64_t s = hash4(p.seed, 0xD1A6, static_cast<std::uint64_t>(i), 0);
+    return 0.5 + p.diag_spread * unit(splitmix(s)) + p.dominance * rowabs;
+}
+
+std::unique_ptr<CsbHost> generate_clustered(const be_cluster_params& p, std::vector<double>& diag,
+                                            std::vector<index_t>& tile_offsets) {
+    const int nw = p.threads > 0 ? p.threads : hw_threads();
+    const ClusterPlan plan = make_plan(p);
+    auto m = clustered_rows(plan, 0, plan.nblk, false, nw);
+    // diagonal: 0.5 + U(0, spread) + dominance * sum|row| (synth.hpp:147-157 rule)
+    std::vector<double> rsum, csum;
+    abs_sums(*m, 0, plan.nblk, rsum, csum, nw);
     diag.resize(static_cast<std::size_t>(p.n));
-    for (index_t i = 0; i < p.n; ++i) {
-        std::uint64_t s = hash4(p.seed, 0xD1A6, static_cast<std::uint64_t>(i), 0);
-        diag[static_cast<std::size_t>(i)] = 0.5 + p.diag_spread * unit(splitmix(s)) +
-                                            p.dominance * (rsum[static_cast<std::size_t>(i)] + csum[static_cast<std::size_t>(i)]);
-    }
+    for (index_t i = 0; i < p.n; ++i)
+        diag[static_cast<std::size_t>(i)] = clustered_diag_value(p, i, rsum[static_cast<std::size_t>(i)] + csum[static_cast<std::size_t>(i)]);
     std::mt19937_64 trng(p.seed + 0x7157);
     tile_offsets = draw_tile_offsets(p.n, p.block_extent, p.tile_min, p.tile_max, trng);
     return m;
+}
+
+std::unique_ptr<CsbHost> generate_clustered_part(const be_cluster_params& p, index_t b0, index_t b1, bool diag_only,
+                                                 std::vector<double>& rowabs, std::vector<index_t>& tile_offsets) {
+    const int nw = p.threads > 0 ? p.threads : hw_threads();
+    const ClusterPlan plan = make_plan(p);
+    if (b0 < 0 || b1 < b0 || b1 > plan.nblk) fail(BE_ERR_BAD_PARAMS, "generate_clustered_part: bad block-row range");
+    auto m = clustered_rows(plan, b0, b1, diag_only, nw);
+    std::vector<double> rsum, csum;
+    abs_sums(*m, b0, b1, rsum, csum, nw);
+    rowabs.resize(static_cast<std::size_t>(p.n));
+    for (std::size_t i = 0; i < rowabs.size(); ++i) rowabs[i] = rsum[i] + csum[i];
+    std::mt19937_64 trng(p.seed + 0x7157);
+    tile_offsets = draw_tile_offsets(p.n, p.block_extent, p.tile_min, p.tile_max, trng);
+    return m;
+}
+
+std::vector<index_t> clustered_block_row_weights(const be_cluster_params& p) {
+    const ClusterPlan plan = make_plan(p);
+    const auto& B = plan.bounds;
+    std::vector<index_t> w(static_cast<std::size_t>(plan.nblk));
+    auto ntiles_of = [&](index_t len) { return (len + p.tile - 1) / p.tile; };
+    for (index_t bi = 0; bi < plan.nblk; ++bi) {  // expected stored entries of block row bi
+        const index_t br = B[bi + 1] - B[bi];
+        double e = 0.0;
+        for (index_t a = 0; a < ntiles_of(br); ++a) {
+            const double t = static_cast<double>(std::min(p.tile, br - a * p.tile));
+            e += t * (t - 1) / 2 * p.fill;
+            for (index_t b = 0; b < a; ++b) e += t * static_cast<double>(std::min(p.tile, br - b * p.tile)) * p.fill * plan.p_tile;
+        }
+        for (index_t bj = 0; bj < bi; ++bj)
+            if (plan.block_on(bi, bj))
+                e += static_cast<double>(br) * static_cast<double>(B[bj + 1] - B[bj]) * p.fill * plan.p_tile;
+        w[static_cast<std::size_t>(bi)] = static_cast<index_t>(std::llround(e));
+    }
+    return w;
 }
 
 }  // namespace be

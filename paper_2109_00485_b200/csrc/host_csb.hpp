@@ -69,5 +69,11 @@ std::vector<index_t> draw_tile_offsets(index_t n, index_t block_extent, index_t 
 std::unique_ptr<Synth> generate_synthetic(const be_synth_params& p);
 std::unique_ptr<CsbHost> generate_clustered(const be_cluster_params& p, std::vector<double>& diag,
                                             std::vector<index_t>& tile_offsets);
+// block rows [b0, b1) only (diag_only: their diagonal blocks only); rowabs
+// (n) receives this part's contribution to sum |row| of every row
+std::unique_ptr<CsbHost> generate_clustered_part(const be_cluster_params& p, index_t b0, index_t b1, bool diag_only,
+                                                 std::vector<double>& rowabs, std::vector<index_t>& tile_offsets);
+double clustered_diag_value(const be_cluster_params& p, index_t i, double rowabs);
+std::vector<index_t> clustered_block_row_weights(const be_cluster_params& p);
 
 }  // namespace be

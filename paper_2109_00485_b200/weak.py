@@ -1,0 +1,35 @@
+"""One rank's share of the weak-scaled clustered problem (bench.py --gpus N,
+and the threaded multi-rank tests): the SpMM slab of nnz-balanced block rows,
+the panel rows it owns (equal rows), their diagonal (the synth.hpp:147-157
+rule over sum|row| summed across the ranks' slabs) and the diagonal blocks
+its preconditioner tiles need. Every rank generates only its own part.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import abi
+
+
+def rank_problem(ctx, comm, params, rank: int, world: int, precond: bool, allreduce_sum, values_prec=abi.BE_F32):
+    """allreduce_sum(np.ndarray) -> np.ndarray summed over ranks (host-side
+    glue: torch.distributed in the bench, a thread barrier in the tests).
+    Returns dict(op, tiles, cuts, slabs, lo, hi, nnz_local, tile_entries)."""
+    n = params.n
+    bounds = abi.uniform_boundaries(n, params.block_extent)
+    cuts = abi.dist_rows(bounds, world)
+    slabs = abi.dist_balance(abi.clustered_weights(params), world)
+    slab, rowabs, toff = abi.generate_clustered_part(params, int(slabs[rank]), int(slabs[rank + 1]))
+    tot = allreduce_sum(rowabs)
+    lo, hi = int(cuts[rank]), int(cuts[rank + 1])
+    diag = abi.clustered_diag(params, tot[lo:hi], lo, hi)
+    del tot, rowabs
+    op = abi.DistOperator(ctx, comm, slab, cuts, diag, values_prec=values_prec)
+    tiles = None
+    if precond:
+        b_lo, b_hi = int(np.searchsorted(bounds, lo)), int(np.searchsorted(bounds, hi))
+        dblk = abi.generate_clustered_part(params, b_lo, b_hi, diag_blocks_only=True)[0]
+        tiles = abi.Tiles(ctx, dblk, diag, toff, row_range=(lo, hi))
+        del dblk
+    return dict(op=op, tiles=tiles, cuts=cuts, slabs=slabs, lo=lo, hi=hi, nnz_local=slab.nnz,
+                tile_entries=tiles.count()[2] if tiles else 0, diag=diag, toff=toff)

@@ -107,3 +107,31 @@ def _gloo_rank(rank, world, port, n, nb):
 def test_gloo_exchange_matches_oracle(world):
     import torch.multiprocessing as mp
     mp.spawn(_gloo_rank, args=(world, _free_port(), 1500, 8), nprocs=world, join=True)
+
+
+def test_clustered_parts_reassemble_the_matrix():
+    """Each rank generates only its block rows (weak-scaling bench): the parts
+    are exactly the whole-matrix generator's entries, the summed |row| parts
+    give its diagonal, and the expected weights track the real counts."""
+    p = abi.clustered_params(n=9000, target_nnz=2_000_000, block_extent=1000, seed=5)
+    whole, diag, toff = abi.generate_clustered(n=9000, target_nnz=2_000_000, block_extent=1000, seed=5)
+    w = abi.clustered_weights(p)
+    cuts = abi.dist_balance(w, 3)
+    parts, absum = [], np.zeros(9000)
+    for r in range(3):
+        m, rowabs, t = abi.generate_clustered_part(p, int(cuts[r]), int(cuts[r + 1]))
+        assert np.array_equal(t, toff)
+        parts.append(m.to_triples())
+        absum += rowabs
+    assert np.array_equal(np.concatenate(parts), whole.to_triples())
+    d = abi.clustered_diag(p, absum, 0, 9000)
+    assert np.allclose(d, diag, rtol=1e-13, atol=0)
+    one, rowabs, _ = abi.generate_clustered_part(p, 0, len(w))
+    assert np.array_equal(abi.clustered_diag(p, rowabs, 0, 9000), diag)  # one part: bit-exact
+    real = whole.block_row_nnz()
+    assert abs(real.sum() - w.sum()) / w.sum() < 0.02
+    dg, _, _ = abi.generate_clustered_part(p, 2, 5, diag_blocks_only=True)
+    t = dg.to_triples()
+    b = whole.row_offsets
+    blk = lambda x: np.searchsorted(b, x, side="right") - 1
+    assert np.all(blk(t["row"]) == blk(t["col"])) and np.all((blk(t["row"]) >= 2) & (blk(t["row"]) < 5))

@@ -218,3 +218,42 @@ def test_nccl_world1(ctx):
     assert np.allclose(res["lambda_"], ref["lambda_"], rtol=1e-9)
     op.close()
     comm.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_weak_scaling_glue_matches_whole_matrix(ctx, world):
+    """The bench's per-rank problem construction (weak.rank_problem: slab and
+    diagonal-block generation, the summed |row| diagonal, rank-range tiles)
+    solves the same problem as the whole matrix on one GPU."""
+    from paper_2109_00485_b200 import weak
+    kw = dict(n=24000, target_nnz=3_000_000, block_extent=2000, seed=3)
+    p = abi.clustered_params(**kw)
+    whole, diag, toff = abi.generate_clustered(**kw)
+    single = abi.lobpcg(ctx, abi.Operator(ctx, whole, diag), tiles=abi.Tiles(ctx, whole, diag, toff), k=8, nb=16,
+                        tol=1e-6, maxiter=300, seed=1)
+    box = {}
+    bar = threading.Barrier(world)
+    lock = threading.Lock()
+
+    def allreduce_sum(x):  # host-side sum over the rank threads
+        with lock:
+            box["acc"] = x.copy() if "acc" not in box or box.get("gen") != box.get("seen") else box["acc"] + x
+            box["seen"] = box.get("gen")
+        bar.wait()
+        out = box["acc"].copy()
+        bar.wait()
+        with lock:
+            box["gen"] = box.get("gen", 0) + 1
+        bar.wait()
+        return out
+
+    def rank(r, c, comm):
+        rp = weak.rank_problem(c, comm, p, r, world, True, allreduce_sum)
+        assert np.allclose(rp["diag"], diag[rp["lo"]:rp["hi"]], rtol=1e-13, atol=0)
+        res = abi.lobpcg(c, rp["op"], tiles=rp["tiles"], k=8, nb=16, tol=1e-6, maxiter=300, seed=1)
+        rp["op"].close()
+        return res
+
+    res = run_ranks(world, rank)
+    assert np.max(np.abs(res[0]["lambda_"] - single["lambda_"]) / single["lambda_"]) <= 1e-6
+    assert abs(res[0]["iterations"] - single["iterations"]) <= 2
