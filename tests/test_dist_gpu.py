@@ -231,23 +231,19 @@ def test_weak_scaling_glue_matches_whole_matrix(ctx, world):
     whole, diag, toff = abi.generate_clustered(**kw)
     single = abi.lobpcg(ctx, abi.Operator(ctx, whole, diag), tiles=abi.Tiles(ctx, whole, diag, toff), k=8, nb=16,
                         tol=1e-6, maxiter=300, seed=1)
-    box = {}
+    slots = [None] * world
     bar = threading.Barrier(world)
-    lock = threading.Lock()
-
-    def allreduce_sum(x):  # host-side sum over the rank threads
-        with lock:
-            box["acc"] = x.copy() if "acc" not in box or box.get("gen") != box.get("seen") else box["acc"] + x
-            box["seen"] = box.get("gen")
-        bar.wait()
-        out = box["acc"].copy()
-        bar.wait()
-        with lock:
-            box["gen"] = box.get("gen", 0) + 1
-        bar.wait()
-        return out
 
     def rank(r, c, comm):
+        def allreduce_sum(x):  # host-side sum over the rank threads, in rank order
+            slots[r] = x
+            bar.wait()
+            out = slots[0].copy()
+            for q in range(1, world):
+                out += slots[q]
+            bar.wait()
+            return out
+
         rp = weak.rank_problem(c, comm, p, r, world, True, allreduce_sum)
         assert np.allclose(rp["diag"], diag[rp["lo"]:rp["hi"]], rtol=1e-13, atol=0)
         res = abi.lobpcg(c, rp["op"], tiles=rp["tiles"], k=8, nb=16, tol=1e-6, maxiter=300, seed=1)
