@@ -8,6 +8,7 @@
 #include <cmath>
 
 #include "densela.cuh"
+#include "stream.cuh"
 
 namespace be {
 namespace dla {
@@ -108,6 +109,170 @@ struct GramOut {
     int sym[12];
 };
 
+// ---- streamed Gram (nb % 8 == 0): persistent CTAs, a kGS-stage ring of
+// R-row chunks of the distinct panels filled by TMA bulk copies (one per row,
+// into rows padded by 16 bytes: conflict-free shared-memory reads). Thread =
+// (8 x 8 output block of one pair, row group): per row 64 B of A and 64 B of
+// B from shared memory feed 64 FMAs. Row groups are summed in shared memory
+// in a fixed order, CTAs by k_gram_reduce8 (deterministic).
+constexpr int kGS = 3;  // pipeline stages of trsm (2 CTAs per SM, ~37 KB per stage)
+constexpr int kGG = 4;  // pipeline stages of the Gram kernel (1 CTA per SM, ~40 KB per stage)
+
+struct GramS {
+    int R;         // rows per chunk
+    int rs;        // padded row stride in doubles (nb + 2)
+    int ps;        // doubles per panel slot (R * rs + 2: a 16-byte skew between panels)
+    int ss;        // doubles per stage (nd * ps)
+    int tasks;     // npairs * B
+    int groups;    // row groups per CTA
+    int bpr;       // 8-row blocks of an nb x nb output (nb / 8)
+    int bpc;       // 4-column blocks (nb / 4)
+};
+
+// all threads fill one stage with 16-byte cp.async copies: `nsrc` panels x
+// `rows` rows into rows padded to `rs` doubles (one commit group per stage)
+__device__ __forceinline__ void cp16g(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(stream::smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void fill_stage(double* st, const double* const* src, int nsrc, int ps, int rs, int nb,
+                                           std::int64_t r0, int rows) {
+    const int pr = nb / 2;  // 16-byte pieces per row (divides the block size)
+    const int c = threadIdx.x % pr, rstep = blockDim.x / pr;
+    for (int d = 0; d < nsrc; ++d) {
+        const double* g = src[d] + r0 * nb + 2 * c;
+        double* t = st + d * ps + 2 * c;
+        for (int r = threadIdx.x / pr; r < rows; r += rstep) cp16g(t + r * rs, g + static_cast<std::int64_t>(r) * nb);
+    }
+}
+
+__global__ void __launch_bounds__(512, 1) k_gram_s(GramDev g, GramS q, std::int64_t n, double* __restrict__ partial) {
+    extern __shared__ __align__(16) double sbuf[];
+    const int tid = threadIdx.x;
+    const int nb = g.nb;
+    // this CTA's rows: contiguous chunks
+    const std::int64_t nchunk_all = (n + q.R - 1) / q.R;
+    const std::int64_t c0 = nchunk_all * blockIdx.x / gridDim.x, c1 = nchunk_all * (blockIdx.x + 1) / gridDim.x;
+    const int nch = static_cast<int>(c1 - c0);
+    auto issue = [&](int c) {  // chunk c of this CTA into stage c % kGG (one commit group, maybe empty)
+        if (c < nch) {
+            const std::int64_t r0 = (c0 + c) * q.R;
+            const int rows = static_cast<int>(min(static_cast<std::int64_t>(q.R), n - r0));
+            fill_stage(sbuf + static_cast<std::size_t>(c % kGG) * q.ss, g.panel, g.nd, q.ps, q.rs, nb, r0, rows);
+        }
+        cp_commit();
+    };
+    for (int c = 0; c < kGG - 1; ++c) issue(c);
+
+    const int task = tid % q.tasks, grp = tid / q.tasks;
+    const bool active = grp < q.groups;
+    const int B = q.bpr * q.bpc;
+    const int p = task / B, blk = task % B;
+    const int i0 = (blk / q.bpc) * 8, j0 = (blk % q.bpc) * 4;
+    const int da = g.ia[p], db = g.ib[p];
+    double acc[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) acc[e] = 0.0;
+    for (int c = 0; c < nch; ++c) {
+        issue(c + kGG - 1);  // into the stage consumed at c - 1
+        cp_wait<kGG - 1>();
+        __syncthreads();     // chunk c landed for every thread
+        const std::int64_t r0 = (c0 + c) * q.R;
+        const int rows = static_cast<int>(min(static_cast<std::int64_t>(q.R), n - r0));
+        const double* st = sbuf + static_cast<std::size_t>(c % kGG) * q.ss;
+        if (active) {
+            const double* A = st + da * q.ps + i0;
+            const double* Bp = st + db * q.ps + j0;
+            for (int r = grp; r < rows; r += q.groups) {
+                double a[8], b[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const double2 x = *reinterpret_cast<const double2*>(A + r * q.rs + 2 * k);
+                    a[2 * k] = x.x;
+                    a[2 * k + 1] = x.y;
+                }
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const double2 y = *reinterpret_cast<const double2*>(Bp + r * q.rs + 2 * k);
+                    b[2 * k] = y.x;
+                    b[2 * k + 1] = y.y;
+                }
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                    for (int ii = 0; ii < 8; ++ii) acc[jj * 8 + ii] = fma(a[ii], b[jj], acc[jj * 8 + ii]);
+            }
+        }
+        __syncthreads();  // stage c % kGG is free again
+    }
+    cp_wait<0>();
+    __syncthreads();
+    // row groups -> one partial per task (fixed order), reusing the ring
+    double* out = partial + static_cast<std::int64_t>(blockIdx.x) * q.tasks * 32;
+    if (32 % q.tasks == 0) {
+        // lanes of a warp holding the same task: butterfly, then warps in order
+        const int nw = blockDim.x / 32, warp = tid >> 5, lane = tid & 31;
+        double* red = sbuf;  // nw x tasks x 32
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+            double v = active ? acc[e] : 0.0;
+            for (int o = q.tasks; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane < q.tasks) red[(warp * q.tasks + lane) * 32 + e] = v;
+        }
+        __syncthreads();
+        for (int e = tid; e < q.tasks * 32; e += blockDim.x) {
+            double v = red[e];
+            for (int w = 1; w < nw; ++w) v += red[w * q.tasks * 32 + e];
+            out[e] = v;
+        }
+    } else {
+        double* red = sbuf;  // tasks x 32, row groups added in order
+        for (int k = 0; k < q.groups; ++k) {
+            if (active && grp == k)
+#pragma unroll
+                for (int e = 0; e < 32; ++e) red[task * 32 + e] = k == 0 ? acc[e] : red[task * 32 + e] + acc[e];
+            __syncthreads();
+        }
+        for (int e = tid; e < q.tasks * 32; e += blockDim.x) out[e] = red[e];
+    }
+}
+
+// out_p(i, j) = sum over CTAs (lane-strided + butterfly, fixed order);
+// symmetrised pairs average both halves (gram, densela.hpp:90-97)
+__global__ void k_gram_reduce8(GramDev g, GramOut o, GramS q, int nparts, const double* __restrict__ partial) {
+    const int nb = g.nb;
+    const int total = g.npairs * nb * nb;
+    const int lane = threadIdx.x & 31;
+    const int B = q.bpr * q.bpc;
+    for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < total; e += (gridDim.x * blockDim.x) >> 5) {
+        const int p = e / (nb * nb), rem = e % (nb * nb);
+        const int j = rem / nb, i = rem % nb;  // column-major (i, j)
+        if (o.sym[p] && i > j) continue;
+        auto sum_at = [&](int ii, int jj) {
+            const int task = p * B + (ii / 8) * q.bpc + (jj / 4);
+            const int el = (jj % 4) * 8 + (ii % 8);
+            double s = 0.0;
+            for (int b = lane; b < nparts; b += 32) s += partial[(static_cast<std::int64_t>(b) * q.tasks + task) * 32 + el];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            return s;
+        };
+        const double sij = sum_at(i, j);
+        if (o.sym[p] && i != j) {
+            const double s = 0.5 * (sij + sum_at(j, i));
+            if (lane == 0) {
+                o.out[p][j * nb + i] = s;
+                o.out[p][i * nb + j] = s;
+            }
+        } else if (lane == 0) {
+            o.out[p][j * nb + i] = sij;
+        }
+    }
+}
+
 // out_p(i, j) = sum over CTAs (fixed lane-strided order + butterfly, so the
 // result is deterministic); symmetrised pairs average both halves. One warp
 // per output element.
@@ -163,7 +328,7 @@ struct MixDev {
 constexpr int kMixRows = 64;
 struct MixSrc {
     int nsrc;
-    const double* src[6];
+    const double* src[8];
 };
 __global__ void __launch_bounds__(kT) k_mix(MixDev m, MixSrc ms, const int* __restrict__ srcidx_dummy, std::int64_t n) {
     extern __shared__ double sh[];
@@ -252,6 +417,105 @@ __global__ void __launch_bounds__(kT) k_mix(MixDev m, MixSrc ms, const int* __re
             }
         }
     }
+}
+
+// ---- streamed trsm (nb % 2 == 0, nb <= NBP): W <- W R^-1 for one or two
+// panels; chunk rows arrive by bulk copy, thread = (panel, row) substitutes
+// in registers (rows read / written in a lane-rotated 16-byte order), the
+// results go back through the stage and leave by one bulk store per panel.
+
+template <int NBP>
+__global__ void __launch_bounds__(256, 2) k_trsm_s(double* __restrict__ w0, double* __restrict__ w1,
+                                                  const double* __restrict__ Rg, int nb, std::int64_t n, Status* st,
+                                                  int skip_if_rank, int skip_if_notpd, int R, int ps) {
+    extern __shared__ __align__(16) double sbuf[];
+    __shared__ double Rs[NBP * NBP];
+    __shared__ double Rinv[NBP];
+    __shared__ int skip;
+    const int tid = threadIdx.x;
+    const int np = w1 ? 2 : 1;
+    const int rs = nb + 2;
+    if (tid == 0) {
+        int sk = (skip_if_rank && st->rank_deficient) || (skip_if_notpd && st->not_pd);
+        if (!sk) {  // trsm_right_inv's conditioning check (densela.hpp:129-136)
+            double dmin = INFINITY, dmax = 0.0;
+            for (int j = 0; j < nb; ++j) {
+                const double d = fabs(Rg[j * nb + j]);
+                dmin = fmin(dmin, d);
+                dmax = fmax(dmax, d);
+            }
+            if (!(dmin > 1e-14 * dmax)) {
+                sk = 1;
+                if (blockIdx.x == 0) st->singular_tri = 1;
+            }
+        }
+        skip = sk;
+    }
+    for (int e = tid; e < nb * nb; e += 256) Rs[e] = Rg[e];
+    if (tid < nb) Rinv[tid] = 1.0 / Rg[tid * nb + tid];
+    __syncthreads();
+    if (skip) return;
+    const std::int64_t nchunk_all = (n + R - 1) / R;
+    const std::int64_t c0 = nchunk_all * blockIdx.x / gridDim.x, c1 = nchunk_all * (blockIdx.x + 1) / gridDim.x;
+    const int nch = static_cast<int>(c1 - c0);
+    const std::size_t ss = static_cast<std::size_t>(np) * ps;
+    const double* srcs[2] = {w0, w1};
+    auto issue = [&](int c) {
+        if (c < nch) {
+            const std::int64_t r0 = (c0 + c) * R;
+            const int rows = static_cast<int>(min(static_cast<std::int64_t>(R), n - r0));
+            fill_stage(sbuf + (c % kGS) * ss, srcs, np, ps, rs, nb, r0, rows);
+        }
+        cp_commit();
+    };
+    for (int c = 0; c < kGS - 1; ++c) issue(c);
+    const int q = tid / R, rl = tid % R;
+    for (int c = 0; c < nch; ++c) {
+        issue(c + kGS - 1);
+        cp_wait<kGS - 1>();
+        __syncthreads();
+        const std::int64_t r0 = (c0 + c) * R;
+        const int rows = static_cast<int>(min(static_cast<std::int64_t>(R), n - r0));
+        double* stg = sbuf + (c % kGS) * ss;
+        if (q < np && rl < rows) {
+            double* xr = stg + q * ps + rl * rs;
+            double x[NBP];
+#pragma unroll
+            for (int k = 0; k < NBP / 2; ++k)
+                if (2 * k < nb) {
+                    const double2 v = reinterpret_cast<const double2*>(xr)[k];
+                    x[2 * k] = v.x;
+                    x[2 * k + 1] = v.y;
+                }
+#pragma unroll
+            for (int j = 0; j < NBP; ++j) {
+                if (j < nb) {
+                    double s = x[j];
+#pragma unroll
+                    for (int i = 0; i < j; ++i) s -= x[i] * Rs[j * nb + i];
+                    // s / R_jj: reciprocal + one residual correction (the
+                    // correctly rounded quotient but for rare last-bit
+                    // ties) instead of the ~40-instruction IEEE division
+                    const double d = Rs[j * nb + j], ri = Rinv[j];
+                    double qj = s * ri;
+                    qj = fma(fma(-qj, d, s), ri, qj);
+                    x[j] = qj;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NBP / 2; ++k)
+                if (2 * k < nb) reinterpret_cast<double2*>(xr)[k] = make_double2(x[2 * k], x[2 * k + 1]);
+        }
+        __syncthreads();  // the stage holds the chunk's results: coalesced 16-byte stores
+        const int pr = nb / 2, per = rows * pr;
+        for (int e = tid; e < per * np; e += 256) {
+            const int p = e / per, k = e % per, r = k / pr, cc = k % pr;
+            reinterpret_cast<double2*>((p == 0 ? w0 : w1) + (r0 + r) * nb)[cc] =
+                reinterpret_cast<const double2*>(stg + p * ps + r * rs)[cc];
+        }
+        __syncthreads();  // stage free for the refill at c + 1
+    }
+    cp_wait<0>();
 }
 
 // -------------------------------------------------------------------- trsm
@@ -531,8 +795,9 @@ int grid_rows(Ctx* ctx, std::int64_t n, int per) {
 }  // namespace
 
 std::int64_t gram_partials_len(int nb, int npairs, int num_sms) {
-    const int nblk = (nb + 3) / 4;
-    return static_cast<std::int64_t>(num_sms) * 6 * npairs * nblk * nblk * 16;
+    const int nblk = (nb + 3) / 4, nbp8 = (nb + 7) / 8;
+    return std::max(static_cast<std::int64_t>(num_sms) * 6 * npairs * nblk * nblk * 16,
+                    static_cast<std::int64_t>(2 * num_sms) * npairs * nbp8 * nbp8 * 64);
 }
 
 void gram(Ctx* ctx, const GramJob& job, std::int64_t n, double* partials, std::int64_t partials_len, cudaStream_t s) {
@@ -555,6 +820,34 @@ void gram(Ctx* ctx, const GramJob& job, std::int64_t n, double* partials, std::i
         g.ib[p] = idx_of(job.b[p]);
         o.out[p] = job.out[p];
         o.sym[p] = job.sym[p];
+    }
+    if (job.nb % 8 == 0 && n > 0) {  // streamed kernel (whole 8-column blocks, 16-byte rows)
+        GramS q{};
+        const int nbp = (job.nb + 7) / 8 * 8;
+        q.bpr = nbp / 8;
+        q.bpc = nbp / 4;
+        q.tasks = job.npairs * q.bpr * q.bpc;
+        if (q.tasks <= 512) {
+            q.groups = 512 / q.tasks;
+            // R rows per chunk: a stage of up to ~40 KB
+            q.rs = job.nb + 2;
+            q.R = std::max(16, std::min(256, (40 * 1024 / (g.nd * q.rs * 8)) & ~1));
+            q.ps = q.R * q.rs + 2;
+            q.ss = g.nd * q.ps;
+            const std::size_t red = static_cast<std::size_t>(32 % q.tasks == 0 ? 16 : 1) * q.tasks * 32;
+            const std::size_t sm = std::max(static_cast<std::size_t>(kGG) * q.ss, red) * 8;
+            const std::int64_t nchunks = (n + q.R - 1) / q.R;
+            const int nparts = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms, nchunks)));
+            if (static_cast<std::int64_t>(nparts) * q.tasks * 32 <= partials_len) {
+                ensure_dyn_smem(k_gram_s, sm);
+                k_gram_s<<<nparts, 512, sm, s>>>(g, q, n, partials);
+                const int total = job.npairs * job.nb * job.nb;
+                k_gram_reduce8<<<(total * 32 + 255) / 256, 256, 0, s>>>(g, o, q, nparts, partials);
+                BE_CUDA(cudaGetLastError());
+                ctx->launches += 2;
+                return;
+            }
+        }
     }
     int nparts = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 6, (n + 255) / 256)));
     while (nparts > 1 && static_cast<std::int64_t>(nparts) * g.ncombo * 16 > partials_len) nparts /= 2;
@@ -622,6 +915,26 @@ void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
 
 void trsm(Ctx* ctx, double* w0, double* w1, const double* R, int nb, std::int64_t n, Status* st, int skip_if_rank,
           int skip_if_notpd, cudaStream_t s) {
+    if (nb % 2 == 0 && nb <= 32 && n > 0) {  // streamed
+        const int np = w1 ? 2 : 1;
+        const int Rr = 256 / np;
+        const int ps = Rr * (nb + 2) + 2;
+        const std::size_t sm = static_cast<std::size_t>(kGS) * np * ps * sizeof(double);
+        const std::int64_t nchunks = (n + Rr - 1) / Rr;
+        const int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(2 * ctx->num_sms, nchunks)));
+#define BE_TRSMS(NBP)                                                                                         \
+    do {                                                                                                      \
+        ensure_dyn_smem(k_trsm_s<NBP>, sm);                                                                   \
+        k_trsm_s<NBP><<<grid, 256, sm, s>>>(w0, w1, R, nb, n, st, skip_if_rank, skip_if_notpd, Rr, ps);       \
+    } while (0)
+        if (nb <= 8) BE_TRSMS(8);
+        else if (nb <= 16) BE_TRSMS(16);
+        else BE_TRSMS(32);
+#undef BE_TRSMS
+        BE_CUDA(cudaGetLastError());
+        ++ctx->launches;
+        return;
+    }
 #define BE_TRSM(NBP)                                                                                              \
     k_trsm<NBP><<<static_cast<int>(std::max<std::int64_t>(                                                        \
                       1, std::min<std::int64_t>(ctx->num_sms * 4, (n + trsm_rows<NBP>() - 1) / trsm_rows<NBP>()))), \
