@@ -361,6 +361,26 @@ be_status be_dist_balance(const int64_t* weights, int64_t nitems, int world, int
  * solver: n = local rows, x0 = local rows of X0, the result holds local rows. */
 be_status be_op_create_dist(be_ctx* ctx, be_comm* comm, const be_csb_view* L_slab, const int64_t* cuts,
                             const double* diag_local, int values_prec, be_op** out);
+/* The same operator with segment ownership given explicitly: segment q is
+ * rows [seg_bounds[q], seg_bounds[q+1]) (world + 1 bounds on block
+ * boundaries), owned by rank seg_owner[q] (a permutation of the ranks). The
+ * reference triangular layout below uses it (parity variant). */
+be_status be_op_create_dist_owned(be_ctx* ctx, be_comm* comm, const be_csb_view* L_slab, const int64_t* seg_bounds,
+                                  const int* seg_owner, const double* diag_local, int values_prec, be_op** out);
+
+/* The reference's own layout (dist.hpp:25-198), restated bit-exactly:
+ * build_layout: blocks[3 r .. 3 r + 2] = (i, j, transposed) of rank r over
+ * n_ranks = nd (nd + 1) / 2 ranks, diagonal_ranks[g]; BE_ERR_EVEN_ND for an
+ * even or non-positive nd (any output may be NULL). */
+be_status be_tri_layout(int nd, int* blocks, int* diagonal_ranks, int* n_ranks);
+/* segment_of_rank (dist.hpp:184-196): rank r owns rows [seg_begin[r], seg_end[r]) */
+be_status be_tri_segments(int nd, const int64_t* sub_bounds, int64_t* seg_begin, int64_t* seg_end);
+/* partition_matrix's routing (dist.hpp:142-163): the stored entries of `rank`
+ * in global coordinates, in to_triples order (out NULL: *count receives the
+ * number; else *count is the capacity on entry). */
+be_status be_tri_rank_triples(const be_csb_view* L, int nd, const int64_t* sub_bounds, int rank, be_triple* out,
+                              int64_t* count);
+
 /* extract_tiles restricted to the tiles of rows [row_begin, row_end) (a union
  * of whole tiles of tile_offsets, which cover [0, n)); diag_local holds those
  * rows. L must contain the diagonal blocks of those rows. */

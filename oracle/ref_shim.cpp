@@ -7,6 +7,7 @@
 // oracle/oracle.cpp and lets bench.py time the reference's own CPU path
 // (cpu_baseline kind "reference").
 #include <blockeig/densela.hpp>
+#include <blockeig/dist.hpp>
 #include <blockeig/kernels.hpp>
 #include <blockeig/lobpcg.hpp>
 #include <blockeig/precond.hpp>
@@ -335,6 +336,56 @@ double ref_time_lobpcg(void* pp, int k, int nb, int iters, std::uint64_t seed, i
         phase_times[3] = tt;
     }
     return wall;
+}
+
+// ---- dist.hpp: the reference's triangular layout and partition (parity
+// pinning of the multi-GPU parity variant)
+int ref_build_layout(int nd, int* blocks, int* diagonal_ranks) {
+    return guarded([&] {
+        const auto lt = build_layout(nd);
+        for (int r = 0; r < lt.n_ranks; ++r) {
+            const auto& b = lt.rank_to_block[static_cast<std::size_t>(r)];
+            blocks[3 * r] = b.i;
+            blocks[3 * r + 1] = b.j;
+            blocks[3 * r + 2] = b.transposed ? 1 : 0;
+        }
+        for (int g = 0; g < nd; ++g) diagonal_ranks[g] = lt.diagonal_ranks[static_cast<std::size_t>(g)];
+    });
+}
+
+// partition_matrix of the global strictly-lower triples, then rank r's
+// stored entries mapped back to global coordinates (the reassemble rule,
+// dist.hpp:203-223) and its segment
+int ref_partition_rank(const index_t* rows, const index_t* cols, const double* vals, index_t count,
+                       const double* diag, index_t n, int nd, const index_t* sub_bounds, index_t intra_extent,
+                       int rank, index_t* out_rows, index_t* out_cols, double* out_vals, index_t* out_count,
+                       index_t* seg) {
+    return guarded([&] {
+        std::vector<Triple> lower(static_cast<std::size_t>(count));
+        for (index_t k = 0; k < count; ++k) lower[static_cast<std::size_t>(k)] = {rows[k], cols[k], vals[k]};
+        const auto lt = build_layout(nd);
+        std::vector<index_t> b(sub_bounds, sub_bounds + nd + 1);
+        const auto pb = partition_matrix(lower, std::span<const double>(diag, static_cast<std::size_t>(n)), lt, b,
+                                         intra_extent);
+        const auto& blk = lt.rank_to_block[static_cast<std::size_t>(rank)];
+        const index_t roff = b[static_cast<std::size_t>(blk.i)], coff = b[static_cast<std::size_t>(blk.j)];
+        index_t k = 0;
+        for (const Triple& t : to_triples(pb.rank_matrix[static_cast<std::size_t>(rank)])) {
+            if (k >= *out_count) throw BadParams("ref_partition_rank: buffer too small");
+            if (blk.transposed) {
+                out_rows[k] = coff + t.col;
+                out_cols[k] = roff + t.row;
+            } else {
+                out_rows[k] = roff + t.row;
+                out_cols[k] = coff + t.col;
+            }
+            out_vals[k] = t.value;
+            ++k;
+        }
+        *out_count = k;
+        seg[0] = pb.segment_of_rank[static_cast<std::size_t>(rank)].begin;
+        seg[1] = pb.segment_of_rank[static_cast<std::size_t>(rank)].end;
+    });
 }
 
 }  // extern "C"

@@ -555,17 +555,74 @@ class Comm:
 
 class DistOperator(Operator):
     """Distributed symmetric operator over the ranks of `comm` (dist.hpp
-    distributed_operator): this rank's CSB slab, panel-row cuts, local diagonal."""
+    distributed_operator): this rank's CSB slab, panel-row cuts, local diagonal.
+    owner[q] = rank owning segment q (default: segment q is rank q's)."""
 
-    def __init__(self, ctx: Context, comm: Comm, slab: Csb, cuts, diag_local, values_prec=BE_F32):
+    def __init__(self, ctx: Context, comm: Comm, slab: Csb, cuts, diag_local, values_prec=BE_F32, owner=None):
         self.ctx = ctx
         self.comm = comm
         self.cuts = np.ascontiguousarray(cuts, dtype=np.int64)
         self._h = C.c_void_p()
         d = np.ascontiguousarray(diag_local, dtype=np.float64)
         v = slab.view()
-        check(lib().be_op_create_dist(ctx.handle, comm.handle, C.byref(v), _p(self.cuts), _p(d),
-                                      C.c_int(values_prec), C.byref(self._h)))
+        if owner is None:
+            check(lib().be_op_create_dist(ctx.handle, comm.handle, C.byref(v), _p(self.cuts), _p(d),
+                                          C.c_int(values_prec), C.byref(self._h)))
+        else:
+            o = np.ascontiguousarray(owner, dtype=np.int32)
+            check(lib().be_op_create_dist_owned(ctx.handle, comm.handle, C.byref(v), _p(self.cuts), _p(o), _p(d),
+                                                C.c_int(values_prec), C.byref(self._h)))
+
+
+# ---------------------------------------------- the reference triangular layout
+def tri_layout(nd: int):
+    """build_layout (dist.hpp:49-75): (blocks[n_ranks, 3] = (i, j, transposed), diagonal_ranks[nd])."""
+    nr = C.c_int()
+    check(lib().be_tri_layout(C.c_int(nd), None, None, C.byref(nr)))
+    blocks = np.zeros((nr.value, 3), np.int32)
+    dr = np.zeros(max(nd, 1), np.int32)
+    check(lib().be_tri_layout(C.c_int(nd), _p(blocks), _p(dr), C.byref(nr)))
+    return blocks, dr[:nd]
+
+
+def tri_segments(nd: int, sub_bounds):
+    """segment_of_rank (dist.hpp:184-196): (begin[n_ranks], end[n_ranks])."""
+    b = np.ascontiguousarray(sub_bounds, dtype=np.int64)
+    nr = nd * (nd + 1) // 2
+    beg, end = np.zeros(nr, np.int64), np.zeros(nr, np.int64)
+    check(lib().be_tri_segments(C.c_int(nd), _p(b), _p(beg), _p(end)))
+    return beg, end
+
+
+def tri_rank_triples(csb: Csb, nd: int, sub_bounds, rank: int) -> np.ndarray:
+    """partition_matrix's routing: rank's stored entries in global coordinates."""
+    b = np.ascontiguousarray(sub_bounds, dtype=np.int64)
+    v = csb.view()
+    cnt = C.c_int64(0)
+    check(lib().be_tri_rank_triples(C.byref(v), C.c_int(nd), _p(b), C.c_int(rank), None, C.byref(cnt)))
+    out = np.zeros(cnt.value, dtype=TRIPLE_DTYPE)
+    check(lib().be_tri_rank_triples(C.byref(v), C.c_int(nd), _p(b), C.c_int(rank), _p(out), C.byref(cnt)))
+    return out
+
+
+def tri_rank_problem(csb: Csb, diag, nd: int, sub_bounds, rank: int, extent: int = 4000):
+    """One rank of the reference's triangular layout as a distributed-operator
+    input: (slab CSB over blocks refined at every segment cut, segment bounds in
+    row order, segment owners, this rank's diagonal)."""
+    n = csb.nrows
+    beg, end = tri_segments(nd, sub_bounds)
+    order = np.lexsort((end, beg)).astype(np.int32)
+    seg_bounds = np.concatenate([beg[order], [n]]).astype(np.int64)
+    cut = np.unique(np.concatenate([np.asarray(sub_bounds, np.int64), seg_bounds]))
+    bounds = [0]
+    for a, b in zip(cut[:-1], cut[1:]):
+        k = -(-(b - a) // extent)
+        bounds += [a + (b - a) * q // k for q in range(1, k + 1)]
+    bounds = np.asarray(bounds, np.int64)
+    t = tri_rank_triples(csb, nd, sub_bounds, rank)
+    slab = build_csb_coo(t, n, n, bounds, bounds)
+    d = np.asarray(diag)[beg[rank]:end[rank]]
+    return slab, seg_bounds, order, d
 
 
 class Tiles:

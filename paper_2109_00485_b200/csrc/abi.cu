@@ -12,6 +12,7 @@
 #include "device.hpp"
 #include "lobpcg.cuh"
 #include "precond.cuh"
+#include "tri_layout.hpp"
 
 namespace {
 thread_local std::string g_err;
@@ -508,7 +509,58 @@ be_status be_op_create_dist(be_ctx* ctx, be_comm* comm, const be_csb_view* L_sla
     return guard([&] {
         if (!ctx || !comm || !L_slab || !cuts || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
         BE_CUDA(cudaSetDevice(ctx->impl->device));
-        *out = new be_op{be::op_create_dist(ctx->impl.get(), comm->impl.get(), *L_slab, cuts, diag_local, values_prec)};
+        *out = new be_op{be::op_create_dist(ctx->impl.get(), comm->impl.get(), *L_slab, cuts, nullptr, diag_local,
+                                            values_prec)};
+    });
+}
+
+be_status be_op_create_dist_owned(be_ctx* ctx, be_comm* comm, const be_csb_view* L_slab, const int64_t* seg_bounds,
+                                  const int* seg_owner, const double* diag_local, int values_prec, be_op** out) {
+    return guard([&] {
+        if (!ctx || !comm || !L_slab || !seg_bounds || !seg_owner || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        BE_CUDA(cudaSetDevice(ctx->impl->device));
+        *out = new be_op{be::op_create_dist(ctx->impl.get(), comm->impl.get(), *L_slab, seg_bounds, seg_owner,
+                                            diag_local, values_prec)};
+    });
+}
+
+// ------------------------------------------------- reference triangular layout
+be_status be_tri_layout(int nd, int* blocks, int* diagonal_ranks, int* n_ranks) {
+    return guard([&] {
+        const auto lt = be::build_tri_layout(nd);
+        if (n_ranks) *n_ranks = lt.n_ranks;
+        if (blocks)
+            for (int r = 0; r < lt.n_ranks; ++r)
+                for (int k = 0; k < 3; ++k) blocks[3 * r + k] = lt.blocks[static_cast<std::size_t>(r)][static_cast<std::size_t>(k)];
+        if (diagonal_ranks)
+            for (int g = 0; g < nd; ++g) diagonal_ranks[g] = lt.diagonal_ranks[static_cast<std::size_t>(g)];
+    });
+}
+
+be_status be_tri_segments(int nd, const int64_t* sub_bounds, int64_t* seg_begin, int64_t* seg_end) {
+    return guard([&] {
+        if (!sub_bounds || !seg_begin || !seg_end) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        const auto lt = be::build_tri_layout(nd);
+        const auto seg = be::tri_segments(lt, sub_bounds);
+        for (int r = 0; r < lt.n_ranks; ++r) {
+            seg_begin[r] = seg[static_cast<std::size_t>(r)].first;
+            seg_end[r] = seg[static_cast<std::size_t>(r)].second;
+        }
+    });
+}
+
+be_status be_tri_rank_triples(const be_csb_view* L, int nd, const int64_t* sub_bounds, int rank, be_triple* out,
+                              int64_t* count) {
+    return guard([&] {
+        if (!L || !sub_bounds || !count) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        be::validate_view(*L);
+        const auto lt = be::build_tri_layout(nd);
+        const auto t = be::tri_rank_triples(*L, lt, sub_bounds, rank);
+        if (out) {
+            if (*count < static_cast<int64_t>(t.size())) be::fail(BE_ERR_BAD_PARAMS, "be_tri_rank_triples: buffer too small");
+            std::memcpy(out, t.data(), t.size() * sizeof(be_triple));
+        }
+        *count = static_cast<int64_t>(t.size());
     });
 }
 

@@ -105,9 +105,10 @@ struct Op {
     index_t nruns_ext = 0;
     cudaStream_t cstream = nullptr;
     cudaEvent_t ev_x = nullptr, ev_ag = nullptr;
+    std::vector<int> owner, seg_of_rank;  // segment -> rank, rank -> segment
     index_t unpad(index_t p) const {  // padded index -> global row
-        const index_t q = p / lmax;
-        return cuts[static_cast<std::size_t>(q)] + (p - q * lmax);
+        const index_t r = p / lmax;
+        return cuts[static_cast<std::size_t>(seg_of_rank[static_cast<std::size_t>(r)])] + (p - r * lmax);
     }
     // timing
     bool timing = false;
@@ -122,7 +123,7 @@ std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag
 // block boundaries) the panel-row ownership, diag_local the diagonal of this
 // rank's rows. apply() then maps local f64 panels to local f64 panels.
 std::unique_ptr<Op> op_create_dist(Ctx* ctx, Comm* comm, const be_csb_view& L, const index_t* cuts,
-                                   const double* diag_local, int values_prec);
+                                   const int* owner, const double* diag_local, int values_prec);
 // equal-rows ownership on block boundaries / contiguous weight balance
 std::vector<index_t> dist_rows(const index_t* bounds, index_t nbounds, int world);
 std::vector<index_t> dist_balance(const index_t* weights, index_t nitems, int world);

@@ -512,7 +512,8 @@ struct RowOut {
 // Padded coordinates of the distributed operator: row r of segment q maps to
 // q * lmax + (r - cuts[q]).
 struct RowMap {
-    const index_t* cuts = nullptr;
+    const index_t* cuts = nullptr;  // segment q = rows [cuts[q], cuts[q+1]), owned by rank owner[q]
+    const int* owner = nullptr;
     int world = 1, rank = 0;
     index_t lmax = 0;
     int seg(index_t r) const {
@@ -523,9 +524,10 @@ struct RowMap {
         }
         return lo;
     }
+    int owner_of(index_t r) const { return owner[seg(r)]; }
     index_t pad(index_t r) const {
         const int q = seg(r);
-        return static_cast<index_t>(q) * lmax + (r - cuts[q]);
+        return static_cast<index_t>(owner[q]) * lmax + (r - cuts[q]);
     }
 };
 
@@ -651,12 +653,12 @@ void build_block_row(const be_csb_view& L, index_t bi, int max_nnz, bool keep_sr
     }
     std::vector<std::uint64_t> keys, piece;
     index_t pos = 0;
-    const int row_seg = map ? map->seg(L.row_offsets[bi]) : 0;
+    const int row_own = map ? map->owner_of(L.row_offsets[bi]) : 0;
     for (index_t a = 0; a < ta; ++a) {
       for (int pass = 0; pass < (map ? 2 : 1); ++pass) {  // interior tiles first
         for (const auto& bb : blocks) {
             if (map) {
-                const bool interior = row_seg == map->rank && map->seg(L.col_offsets[bb.bj]) == map->rank;
+                const bool interior = row_own == map->rank && map->owner_of(L.col_offsets[bb.bj]) == map->rank;
                 if (interior != (pass == 0)) continue;
             }
             for (index_t b = 0; b < bb.tb; ++b) {
@@ -1050,7 +1052,7 @@ std::vector<index_t> dist_balance(const index_t* w, index_t nitems, int world) {
 }
 
 std::unique_ptr<Op> op_create_dist(Ctx* ctx, Comm* comm, const be_csb_view& L, const index_t* cuts,
-                                   const double* diag_local, int values_prec) {
+                                   const int* owner, const double* diag_local, int values_prec) {
     validate_view(L);
     if (!comm) fail(BE_ERR_BAD_PARAMS, "distributed operator: null communicator");
     if (values_prec != BE_F32) fail(BE_ERR_BAD_PARAMS, "distributed operator: f32 values only");
@@ -1074,10 +1076,21 @@ std::unique_ptr<Op> op_create_dist(Ctx* ctx, Comm* comm, const be_csb_view& L, c
     op->rank = rank;
     op->world = world;
     op->cuts.assign(cuts, cuts + world + 1);
+    // segment owners: a permutation of the ranks (identity when not given)
+    op->owner.resize(static_cast<std::size_t>(world));
+    op->seg_of_rank.assign(static_cast<std::size_t>(world), -1);
+    for (int q = 0; q < world; ++q) {
+        const int o = owner ? owner[q] : q;
+        if (o < 0 || o >= world || op->seg_of_rank[static_cast<std::size_t>(o)] >= 0)
+            fail(BE_ERR_BAD_PARAMS, "distributed operator: segment owners must be a permutation of the ranks");
+        op->owner[static_cast<std::size_t>(q)] = o;
+        op->seg_of_rank[static_cast<std::size_t>(o)] = q;
+    }
     op->lmax = 1;
     for (int p = 0; p < world; ++p) op->lmax = std::max(op->lmax, cuts[p + 1] - cuts[p]);
-    op->row_lo = cuts[rank];
-    op->nlocal = cuts[rank + 1] - cuts[rank];
+    const int mine = op->seg_of_rank[static_cast<std::size_t>(rank)];
+    op->row_lo = cuts[mine];
+    op->nlocal = cuts[mine + 1] - cuts[mine];
     if (op->lmax * world >= (index_t{1} << 31)) fail(BE_ERR_BAD_PARAMS, "distributed operator: padded dimension exceeds 2^31");
     op->nrows = op->ncols = op->nlocal;
     op->nnz = L.nnz;
@@ -1085,6 +1098,7 @@ std::unique_ptr<Op> op_create_dist(Ctx* ctx, Comm* comm, const be_csb_view& L, c
     op->symmetric = true;
     RowMap map;
     map.cuts = op->cuts.data();
+    map.owner = op->owner.data();
     map.world = world;
     map.rank = rank;
     map.lmax = op->lmax;

@@ -207,3 +207,32 @@ def ref_build_csb(rows, cols, vals, nrows, ncols, rb, cb):
                                        _p(rb), C.c_int64(len(rb)), _p(cb), C.c_int64(len(cb)), _p(bn), _p(bo),
                                        _p(lr), _p(lc), _p(v)))
     return bn, bo, lr, lc, v
+
+
+def ref_partition_rank(csb, diag, nd, sub_bounds, intra_extent, rank):
+    """The reference's partition_matrix (dist.hpp:113-198) for one rank:
+    (global triples of its stored block, (segment begin, end))."""
+    lib = ref()
+    t = csb.to_triples()
+    n = csb.nrows
+    cap = len(t)
+    r, c, v = np.zeros(cap, np.int64), np.zeros(cap, np.int64), np.zeros(cap)
+    cnt = np.array([cap], np.int64)
+    seg = np.zeros(2, np.int64)
+    rows = np.ascontiguousarray(t["row"]); cols = np.ascontiguousarray(t["col"]); vals = np.ascontiguousarray(t["value"])
+    d = np.ascontiguousarray(diag, np.float64)
+    b = np.ascontiguousarray(sub_bounds, np.int64)
+    st = lib.ref_partition_rank(_p(rows), _p(cols), _p(vals), C.c_int64(len(t)), _p(d), C.c_int64(n), C.c_int(nd),
+                                _p(b), C.c_int64(intra_extent), C.c_int(rank), _p(r), _p(c), _p(v), _p(cnt), _p(seg))
+    _chk(lib, "ref", st)
+    k = int(cnt[0])
+    return r[:k], c[:k], v[:k], (int(seg[0]), int(seg[1]))
+
+
+def ref_build_layout(nd):
+    lib = ref()
+    nr = nd * (nd + 1) // 2
+    blocks = np.zeros((nr, 3), np.int32)
+    dr = np.zeros(nd, np.int32)
+    _chk(lib, "ref", lib.ref_build_layout(C.c_int(nd), _p(blocks), _p(dr)))
+    return blocks, dr

@@ -135,3 +135,53 @@ def test_clustered_parts_reassemble_the_matrix():
     b = whole.row_offsets
     blk = lambda x: np.searchsorted(b, x, side="right") - 1
     assert np.all(blk(t["row"]) == blk(t["col"])) and np.all((blk(t["row"]) >= 2) & (blk(t["row"]) < 5))
+
+
+# ---- the reference's triangular layout (dist.hpp), restated bit-exactly
+def test_tri_layout_known_answers():  # test_dist.cpp:86-117
+    blocks, dr = abi.tri_layout(1)
+    assert blocks.tolist() == [[0, 0, 0]] and dr.tolist() == [0]
+    blocks, dr = abi.tri_layout(5)
+    assert len(blocks) == 15
+    assert {(i, j) for i, j, t in blocks if t} == {(0, 3), (0, 4), (1, 4)}
+    rank_of = {(int(i), int(j)): r for r, (i, j, _) in enumerate(blocks)}
+    assert [rank_of[(0, 0)], rank_of[(1, 0)], rank_of[(2, 0)], rank_of[(1, 1)], rank_of[(0, 3)], rank_of[(4, 4)]] == \
+        [0, 1, 2, 3, 9, 14]
+    for nd in (0, 2, -3):
+        with pytest.raises(abi.EvenNd):
+            abi.tri_layout(nd)
+
+
+def test_tri_layout_matches_reference():
+    import oracle_lib as ol
+    if ol.ref() is None:
+        pytest.skip("reference build absent")
+    for nd in (1, 3, 5, 7, 9):
+        b, d = abi.tri_layout(nd)
+        rb, rd = ol.ref_build_layout(nd)
+        assert np.array_equal(b, rb) and np.array_equal(d, rd)
+
+
+@pytest.mark.parametrize("nd", [1, 3, 5])
+def test_tri_partition_matches_reference(nd):
+    """Every rank's stored entries and segment equal partition_matrix's
+    (dist.hpp:113-198), entries compared as multisets in global coordinates
+    (test_dist.cpp:146-153's reassembly rule); together they are the input."""
+    import oracle_lib as ol
+    if ol.ref() is None:
+        pytest.skip("reference build absent")
+    n = 900
+    s = abi.Synthetic("random", n=n, density=0.01, block_extent=300, seed=8)
+    b = abi.uniform_boundaries(n, 300)
+    m = abi.build_csb_coo(s.lower, n, n, b, b)
+    sub = [n * g // nd for g in range(nd + 1)]
+    beg, end = abi.tri_segments(nd, sub)
+    key = lambda r, c, v: sorted(zip(r.tolist(), c.tolist(), v.tolist()))
+    total = 0
+    for rank in range(nd * (nd + 1) // 2):
+        t = abi.tri_rank_triples(m, nd, sub, rank)
+        rr, rc, rv, seg = ol.ref_partition_rank(m, s.diag, nd, sub, 64, rank)
+        assert key(t["row"], t["col"], t["value"]) == key(rr, rc, rv)
+        assert (int(beg[rank]), int(end[rank])) == seg
+        total += len(t)
+    assert total == m.nnz
