@@ -240,6 +240,145 @@ __global__ void __launch_bounds__(512, 1) k_gram_s(GramDev g, GramS q, std::int6
     }
 }
 
+// ---- Gram on the FP64 tensor cores (nb in {8, 16, 24, 32}): the same
+// cp.async row-chunk ring (rows padded to nb + 4 doubles: the m8n8k4 fragment
+// reads hit every bank twice, the minimum), then each warp owns a few pairs
+// and a row group: per 4 rows it loads the A fragments (8 x 4 of X^T) and B
+// fragments (4 x 8 of Y) of its pairs once and issues one DMMA per 8 x 8
+// output block (mma.sync m8n8k4 f64: 256 FMAs per instruction, accumulators
+// in 2 registers per block). Row groups are summed in shared memory in a
+// fixed order, CTAs by k_gram_reduce_m (deterministic).
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+struct GramM {
+    int R;      // rows per chunk (multiple of 4)
+    int rs;     // padded row stride (nb + 4)
+    int ps;     // doubles per panel slot (R * rs)
+    int ss;     // doubles per stage
+    int pw;     // pairs per warp
+    int ngrp;   // warp groups (pairs split): 8 / rg
+    int rg;     // row groups (warps sharing the same pairs)
+};
+
+template <int NBB>  // 8-blocks per dimension (nb / 8)
+__global__ void __launch_bounds__(256, 1) k_gram_m(GramDev g, GramM q, std::int64_t n, double* __restrict__ partial) {
+    constexpr int MAXPW = 16 / (NBB * NBB) > 0 ? 16 / (NBB * NBB) : 1;  // <= 16 blocks per warp
+    extern __shared__ __align__(16) double sbuf[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nb = g.nb;
+    const std::int64_t nchunk_all = (n + q.R - 1) / q.R;
+    const std::int64_t c0 = nchunk_all * blockIdx.x / gridDim.x, c1 = nchunk_all * (blockIdx.x + 1) / gridDim.x;
+    const int nch = static_cast<int>(c1 - c0);
+    auto issue = [&](int c) {
+        if (c < nch) {
+            const std::int64_t r0 = (c0 + c) * q.R;
+            const int rows = static_cast<int>(min(static_cast<std::int64_t>(q.R), n - r0));
+            fill_stage(sbuf + static_cast<std::size_t>(c % kGG) * q.ss, g.panel, g.nd, q.ps, q.rs, nb, r0, rows);
+        }
+        cp_commit();
+    };
+    for (int c = 0; c < kGG - 1; ++c) issue(c);
+    const int wg = warp / q.rg, rgi = warp % q.rg;  // pair group, row group
+    const int p0 = wg * q.pw;
+    const int m = lane >> 2, kq = lane & 3;
+    double acc[MAXPW][NBB][NBB][2];
+#pragma unroll
+    for (int a = 0; a < MAXPW; ++a)
+#pragma unroll
+        for (int i = 0; i < NBB; ++i)
+#pragma unroll
+            for (int j = 0; j < NBB; ++j) acc[a][i][j][0] = acc[a][i][j][1] = 0.0;
+    for (int c = 0; c < nch; ++c) {
+        issue(c + kGG - 1);
+        cp_wait<kGG - 1>();
+        __syncthreads();
+        const std::int64_t r0 = (c0 + c) * q.R;
+        const int rows = static_cast<int>(min(static_cast<std::int64_t>(q.R), n - r0));
+        const double* st = sbuf + static_cast<std::size_t>(c % kGG) * q.ss;
+        for (int k0 = 4 * rgi; k0 < rows; k0 += 4 * q.rg) {
+            const int r = k0 + kq;
+            const bool ok = r < rows;
+#pragma unroll
+            for (int a = 0; a < MAXPW; ++a) {
+                const int p = p0 + a;
+                if (a >= q.pw || p >= g.npairs) break;
+                const double* A = st + g.ia[p] * q.ps + r * q.rs + m;
+                const double* B = st + g.ib[p] * q.ps + r * q.rs + m;
+                double fa[NBB], fb[NBB];
+#pragma unroll
+                for (int i = 0; i < NBB; ++i) {
+                    fa[i] = ok ? A[8 * i] : 0.0;
+                    fb[i] = ok ? B[8 * i] : 0.0;
+                }
+#pragma unroll
+                for (int i = 0; i < NBB; ++i)
+#pragma unroll
+                    for (int j = 0; j < NBB; ++j) dmma884(acc[a][i][j][0], acc[a][i][j][1], fa[i], fb[j]);
+            }
+        }
+        __syncthreads();
+    }
+    cp_wait<0>();
+    __syncthreads();
+    // row groups in order -> red[pair][nb][nb] (row-major i, j), then the CTA partial
+    double* red = sbuf;
+    for (int k = 0; k < q.rg; ++k) {
+        if (rgi == k)
+#pragma unroll
+            for (int a = 0; a < MAXPW; ++a) {
+                const int p = p0 + a;
+                if (a >= q.pw || p >= g.npairs) break;
+#pragma unroll
+                for (int i = 0; i < NBB; ++i)
+#pragma unroll
+                    for (int j = 0; j < NBB; ++j)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            double* dst = red + (static_cast<std::size_t>(p) * nb + 8 * i + m) * nb + 8 * j + 2 * kq + h;
+                            *dst = k == 0 ? acc[a][i][j][h] : *dst + acc[a][i][j][h];
+                        }
+            }
+        __syncthreads();
+    }
+    double* out = partial + static_cast<std::int64_t>(blockIdx.x) * g.npairs * nb * nb;
+    for (int e = tid; e < g.npairs * nb * nb; e += blockDim.x) out[e] = red[e];
+}
+
+// out_p(i, j) = sum over CTAs (lane-strided + butterfly, fixed order);
+// symmetrised pairs average both halves (gram, densela.hpp:90-97)
+__global__ void k_gram_reduce_m(GramDev g, GramOut o, int nparts, const double* __restrict__ partial) {
+    const int nb = g.nb;
+    const int total = g.npairs * nb * nb;
+    const int lane = threadIdx.x & 31;
+    for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < total; e += (gridDim.x * blockDim.x) >> 5) {
+        const int p = e / (nb * nb), rem = e % (nb * nb);
+        const int j = rem / nb, i = rem % nb;  // column-major (i, j)
+        if (o.sym[p] && i > j) continue;
+        auto sum_at = [&](int ii, int jj) {
+            const std::int64_t el = (static_cast<std::int64_t>(p) * nb + ii) * nb + jj;
+            double s = 0.0;
+            for (int b = lane; b < nparts; b += 32) s += partial[static_cast<std::int64_t>(b) * total + el];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            return s;
+        };
+        const double sij = sum_at(i, j);
+        if (o.sym[p] && i != j) {
+            const double s = 0.5 * (sij + sum_at(j, i));
+            if (lane == 0) {
+                o.out[p][j * nb + i] = s;
+                o.out[p][i * nb + j] = s;
+            }
+        } else if (lane == 0) {
+            o.out[p][j * nb + i] = sij;
+        }
+    }
+}
+
 // out_p(i, j) = sum over CTAs (lane-strided + butterfly, fixed order);
 // symmetrised pairs average both halves (gram, densela.hpp:90-97)
 __global__ void k_gram_reduce8(GramDev g, GramOut o, GramS q, int nparts, const double* __restrict__ partial) {
@@ -313,7 +452,7 @@ struct MixDev {
     int ld[12];
     struct O {
         double* y;
-        int accumulate, nterms, add_from;
+        int accumulate, nterms, add_from, add_si, acc_si;
         const double* src[3];
         int ci[3];
         int si[3];
@@ -370,11 +509,12 @@ __global__ void __launch_bounds__(kT) k_mix(MixDev m, MixSrc ms, const int* __re
                 const auto& O = m.out[o];
                 double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
                 double* y = O.y + r * nb;
-                if (O.accumulate) {
-                    a0 = j0 < nb ? y[j0] : 0.0;
-                    a1 = j0 + 1 < nb ? y[j0 + 1] : 0.0;
-                    a2 = j0 + 2 < nb ? y[j0 + 2] : 0.0;
-                    a3 = j0 + 3 < nb ? y[j0 + 3] : 0.0;
+                if (O.accumulate) {  // the old value, staged with the sources
+                    const double* yo = xs + O.acc_si * kMixRows * ld + rl * ld + j0;
+                    a0 = j0 < nb ? yo[0] : 0.0;
+                    a1 = j0 + 1 < nb ? yo[1] : 0.0;
+                    a2 = j0 + 2 < nb ? yo[2] : 0.0;
+                    a3 = j0 + 3 < nb ? yo[3] : 0.0;
                 }
                 for (int tt = 0; tt < O.nterms; ++tt) {
                     const double* x = xs + O.si[tt] * kMixRows * ld + rl * ld;
@@ -400,6 +540,13 @@ __global__ void __launch_bounds__(kT) k_mix(MixDev m, MixSrc ms, const int* __re
                     a1 += res[O.add_from][1];
                     a2 += res[O.add_from][2];
                     a3 += res[O.add_from][3];
+                }
+                if (O.add_si >= 0) {
+                    const double* x = xs + O.add_si * kMixRows * ld + rl * ld + j0;
+                    a0 += x[0];
+                    if (j0 + 1 < nb) a1 += x[1];
+                    if (j0 + 2 < nb) a2 += x[2];
+                    if (j0 + 3 < nb) a3 += x[3];
                 }
                 res[o][0] = a0;
                 res[o][1] = a1;
@@ -821,6 +968,46 @@ void gram(Ctx* ctx, const GramJob& job, std::int64_t n, double* partials, std::i
         o.out[p] = job.out[p];
         o.sym[p] = job.sym[p];
     }
+    if (job.nb % 8 == 0 && job.nb <= 32 && n > 0) {  // tensor-core kernel
+        GramM q{};
+        const int nbb = job.nb / 8, B = nbb * nbb;
+        q.pw = std::max(1, std::min(job.npairs, 16 / B));  // <= 16 blocks per warp
+        q.ngrp = (job.npairs + q.pw - 1) / q.pw;
+        int ngrp = 1;
+        while (ngrp < q.ngrp) ngrp *= 2;
+        if (ngrp <= 8) {
+            q.ngrp = ngrp;
+            q.pw = (job.npairs + ngrp - 1) / ngrp;
+            q.rg = 8 / ngrp;
+            q.rs = job.nb + 4;
+            q.R = std::max(16, std::min(256, (40 * 1024 / (g.nd * q.rs * 8)) & ~3));
+            q.ps = q.R * q.rs;
+            q.ss = g.nd * q.ps;
+            const std::size_t sm = std::max(static_cast<std::size_t>(kGG) * q.ss,
+                                            static_cast<std::size_t>(job.npairs) * job.nb * job.nb) * 8;
+            const std::int64_t nchunks = (n + q.R - 1) / q.R;
+            const int nparts = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms, nchunks)));
+            if (static_cast<std::int64_t>(nparts) * job.npairs * job.nb * job.nb <= partials_len) {
+#define BE_GRAMM(NBB)                                                     \
+    do {                                                                  \
+        ensure_dyn_smem(k_gram_m<NBB>, sm);                               \
+        k_gram_m<NBB><<<nparts, 256, sm, s>>>(g, q, n, partials);         \
+    } while (0)
+                switch (nbb) {
+                    case 1: BE_GRAMM(1); break;
+                    case 2: BE_GRAMM(2); break;
+                    case 3: BE_GRAMM(3); break;
+                    default: BE_GRAMM(4); break;
+                }
+#undef BE_GRAMM
+                const int total = job.npairs * job.nb * job.nb;
+                k_gram_reduce_m<<<(total * 32 + 255) / 256, 256, 0, s>>>(g, o, nparts, partials);
+                BE_CUDA(cudaGetLastError());
+                ctx->launches += 2;
+                return;
+            }
+        }
+    }
     if (job.nb % 8 == 0 && n > 0) {  // streamed kernel (whole 8-column blocks, 16-byte rows)
         GramS q{};
         const int nbp = (job.nb + 7) / 8 * 8;
@@ -893,16 +1080,20 @@ void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
         }
     }
     MixSrc ms{};
-    for (int o = 0; o < m.nout; ++o)
-        for (int t = 0; t < m.out[o].nterms; ++t) {
-            int q = 0;
-            while (q < ms.nsrc && ms.src[q] != m.out[o].src[t]) ++q;
-            if (q == ms.nsrc) {
-                if (ms.nsrc == 6) fail(BE_ERR_BAD_PARAMS, "mix: more than 6 distinct sources");
-                ms.src[ms.nsrc++] = m.out[o].src[t];
-            }
-            m.out[o].si[t] = q;
+    auto sidx = [&](const double* p) {
+        int q = 0;
+        while (q < ms.nsrc && ms.src[q] != p) ++q;
+        if (q == ms.nsrc) {
+            if (ms.nsrc == 6) fail(BE_ERR_BAD_PARAMS, "mix: more than 6 distinct sources");
+            ms.src[ms.nsrc++] = p;
         }
+        return q;
+    };
+    for (int o = 0; o < m.nout; ++o) {
+        for (int t = 0; t < m.out[o].nterms; ++t) m.out[o].si[t] = sidx(m.out[o].src[t]);
+        m.out[o].add_si = job.out[o].add_src ? sidx(job.out[o].add_src) : -1;
+        m.out[o].acc_si = job.out[o].accumulate ? sidx(job.out[o].y) : -1;
+    }
     const int nblk = (job.nb + 3) / 4;
     const std::size_t sm = (static_cast<std::size_t>(m.ncoef) * job.nb * nblk * 4 +
                             static_cast<std::size_t>(ms.nsrc) * kMixRows * (job.nb + 1)) * sizeof(double);

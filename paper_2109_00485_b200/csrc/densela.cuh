@@ -37,7 +37,7 @@ std::int64_t gram_partials_len(int nb, int npairs, int num_sms);
 // Row-wise linear combinations of panels with small coefficient matrices
 // (block_times_small(_add), densela.hpp:448-484). For every output o and row r:
 //   y_o[r] = (accumulate ? y_o[r] : 0) + sum_t src_t[r] * (neg_t ? -C_t : C_t)
-//            + (add_from >= 0 ? y_{add_from}[r] (already updated) : 0)
+//            + (add_from >= 0 ? y_{add_from}[r] (already updated) : 0) + (add_src ? add_src[r] : 0)
 struct MixTerm {
     const double* src;
     const double* coef;  // nb x nb column-major with leading dimension ldc (0 = nb)
@@ -50,6 +50,7 @@ struct MixOut {
     int nterms;
     MixTerm term[3];
     int add_from;
+    const double* add_src = nullptr;  // + add_src[r] (a panel added as is, after the terms)
 };
 struct MixJob {
     int nb;

@@ -326,18 +326,23 @@ struct Solver {
             }
             const bool with_p = p_active && !dropped;
             const int dim = (with_p ? 3 : 2) * nb;
-            {  // update_blocks (lobpcg.hpp:168-194)
-                dla::MixJob m{};
-                m.nb = nb;
-                m.nout = 4;
+            {  // update_blocks (lobpcg.hpp:168-194): P+ = W C2 + P C3, X+ = X C1 + P+ (and the H-images),
+               // as two passes of <= 4 sources each (one 6-source pass runs at a fraction of HBM bandwidth)
                 const double* c1 = C;
                 const double* c2 = C + nb;
                 const double* c3 = C + 2 * nb;
+                dla::MixJob m{};
+                m.nb = nb;
+                m.nout = 2;
                 m.out[0] = dla::MixOut{Pn.get(), 0, with_p ? 2 : 1, {{W.get(), c2, 0, dim}, {P.get(), c3, 0, dim}}, -1};
                 m.out[1] = dla::MixOut{HPn.get(), 0, with_p ? 2 : 1, {{HW.get(), c2, 0, dim}, {HP.get(), c3, 0, dim}}, -1};
-                m.out[2] = dla::MixOut{Xn.get(), 0, 1, {{X.get(), c1, 0, dim}}, 0};
-                m.out[3] = dla::MixOut{HXn.get(), 0, 1, {{HX.get(), c1, 0, dim}}, 1};
                 dla::mix(ctx, m, n, s);
+                dla::MixJob m2{};
+                m2.nb = nb;
+                m2.nout = 2;
+                m2.out[0] = dla::MixOut{Xn.get(), 0, 1, {{X.get(), c1, 0, dim}}, -1, Pn.get()};
+                m2.out[1] = dla::MixOut{HXn.get(), 0, 1, {{HX.get(), c1, 0, dim}}, -1, HPn.get()};
+                dla::mix(ctx, m2, n, s);
                 std::swap(X, Xn);
                 std::swap(HX, HXn);
                 std::swap(P, Pn);

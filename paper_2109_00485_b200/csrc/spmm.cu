@@ -448,7 +448,27 @@ __global__ void k_f64_to_f32(const double* __restrict__ x, float* __restrict__ x
 __global__ void k_finish_f64(const double* __restrict__ d, const double* __restrict__ X,
                              const float* __restrict__ y32, double* __restrict__ Y, std::int64_t nrows, int nb,
                              int symmetric) {
+    // two elements per step (nb even: a row never splits a pair); 32-bit row
+    // division when the panel allows it
     const std::int64_t total = nrows * nb;
+    if (nb % 2 == 0 && total < (std::int64_t{1} << 32)) {
+        const std::uint32_t half = static_cast<std::uint32_t>(total / 2), unb = static_cast<std::uint32_t>(nb);
+        for (std::uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < half; e += gridDim.x * blockDim.x) {
+            const float2 y = reinterpret_cast<const float2*>(y32)[e];
+            double2 out;
+            if (symmetric) {
+                const double dr = d[(2u * e) / unb];
+                const double2 x = reinterpret_cast<const double2*>(X)[e];
+                out = make_double2(dr * x.x + static_cast<double>(y.x), dr * x.y + static_cast<double>(y.y));
+            } else {
+                out = reinterpret_cast<const double2*>(Y)[e];
+                out.x += static_cast<double>(y.x);
+                out.y += static_cast<double>(y.y);
+            }
+            reinterpret_cast<double2*>(Y)[e] = out;
+        }
+        return;
+    }
     for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
         if (symmetric)

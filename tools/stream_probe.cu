@@ -191,4 +191,63 @@ int main2() {
     }
     return 0;
 }
-int main() { main1(); return 0; }
+int main3() {
+    double* out;
+    cudaMalloc(&out, 8);
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    int iters = 4096;
+    for (int wps : {4, 8, 16, 32, 64}) {  // warps per SM
+        int tpb = 128, grid = sms * wps / 4;
+        k_dfma<<<grid, tpb>>>(out, iters);
+        cudaEventRecord(a);
+        k_dfma<<<grid, tpb>>>(out, iters);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        double fl = 2.0 * 16 * iters * (double)grid * tpb;
+        printf("dfma warps/SM=%d: %.1f TFLOP/s fp64 (16 indep. chains per thread)\n", wps, fl / (ms * 1e-3) / 1e12);
+    }
+    return 0;
+}
+__global__ void k_dmma(double* out, int iters) {
+    double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+    double c[8][2] = {};
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(c[q][0]), "+d"(c[q][1]) : "d"(a), "d"(b));
+    double s = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += c[q][0] + c[q][1];
+    if (s == 1.2345) out[0] = s;
+}
+int main4() {
+    double* out;
+    cudaMalloc(&out, 8);
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    int iters = 4096;
+    for (int wps : {4, 8, 16, 32}) {
+        int tpb = 128, grid = sms * wps / 4;
+        k_dmma<<<grid, tpb>>>(out, iters);
+        cudaEventRecord(a);
+        k_dmma<<<grid, tpb>>>(out, iters);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        double fl = 2.0 * 256 * 8 * iters * (double)grid * (tpb / 32);
+        printf("dmma m8n8k4 warps/SM=%d: %.1f TFLOP/s fp64  err=%s\n", wps, fl / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+    }
+    return 0;
+}
+int main() { main4(); return 0; }
