@@ -115,6 +115,11 @@ be_status be_csb_to_triples(const be_csb_view* view, be_triple* out);
  * section (driver.hpp:136-161); diag may be NULL/0 for the bare format. */
 be_status be_csb_save(const char* path, const be_csb_view* view, const double* diag, int64_t ndiag);
 be_status be_csb_load(const char* path, be_csb** out, double** diag, int64_t* ndiag);
+/* Block rows [brow_begin, brow_end) of a CSB1 cache (one rank's slab): global
+ * shape and blocks, only that slab's index / value ranges read from disk;
+ * diag (may be NULL) receives the cached diagonal of those rows. */
+be_status be_csb_load_rows(const char* path, int64_t brow_begin, int64_t brow_end, be_csb** out, double** diag,
+                           int64_t* ndiag);
 void be_free_buffer(void* p);
 void be_csb_free(be_csb* m);
 

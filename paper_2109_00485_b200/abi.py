@@ -233,6 +233,21 @@ class Csb:
         check(lib().be_csb_save(str(path).encode(), C.byref(v), _p(d), C.c_int64(0 if d is None else len(d))))
 
     @classmethod
+    def load_rows(cls, path, brow_begin: int, brow_end: int):
+        """Block rows [brow_begin, brow_end) of a CSB1 cache: (csb, diag of those rows or None)."""
+        h = C.c_void_p()
+        dp = C.POINTER(C.c_double)()
+        nd = C.c_int64(0)
+        check(lib().be_csb_load_rows(str(path).encode(), C.c_int64(brow_begin), C.c_int64(brow_end), C.byref(h),
+                                     C.byref(dp), C.byref(nd)))
+        m = cls._from_handle(h)
+        diag = None
+        if nd.value > 0:
+            diag = np.ctypeslib.as_array(dp, shape=(nd.value,)).copy()
+            lib().be_free_buffer(dp)
+        return m, diag
+
+    @classmethod
     def load(cls, path):
         h = C.c_void_p()
         dp = C.POINTER(C.c_double)()

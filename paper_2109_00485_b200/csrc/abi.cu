@@ -121,6 +121,24 @@ be_status be_csb_load(const char* path, be_csb** out, double** diag, int64_t* nd
     });
 }
 
+be_status be_csb_load_rows(const char* path, int64_t brow_begin, int64_t brow_end, be_csb** out, double** diag,
+                           int64_t* ndiag) {
+    return guard([&] {
+        if (!path || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        std::vector<double> d;
+        auto m = be::load_csb1_rows(path, brow_begin, brow_end, diag ? &d : nullptr);
+        if (diag) {
+            *diag = nullptr;
+            if (!d.empty()) {
+                *diag = static_cast<double*>(std::malloc(d.size() * sizeof(double)));
+                std::memcpy(*diag, d.data(), d.size() * sizeof(double));
+            }
+        }
+        if (ndiag) *ndiag = static_cast<int64_t>(d.size());
+        *out = new be_csb{std::move(m)};
+    });
+}
+
 void be_csb_free(be_csb* m) { delete m; }
 
 // --------------------------------------------------------------- generators

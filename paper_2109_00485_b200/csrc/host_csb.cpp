@@ -290,6 +290,86 @@ void save_csb1(const std::string& path, const be_csb_view& v, const double* diag
     if (!os) fail(BE_ERR_PARSE, "CSB1 cache: write failed for " + path);
 }
 
+// Block rows [b0, b1) of a CSB1 file (global shape and blocks kept, other
+// rows empty): the header and block tables are read, then only the slab's
+// contiguous ranges of the index and value sections (a multi-GPU rank loads
+// its own slab of a Test-3-sized cache without reading the rest). diag, when
+// given, receives the cached diagonal of those block rows' rows.
+std::unique_ptr<CsbHost> load_csb1_rows(const std::string& path, index_t b0, index_t b1, std::vector<double>* diag) {
+    std::ifstream is(path, std::ios::binary);
+    if (!is) fail(BE_ERR_PARSE, "cannot open " + path);
+    char magic[4];
+    is.read(magic, 4);
+    if (!is || std::memcmp(magic, "CSB1", 4) != 0) fail(BE_ERR_PARSE, "CSB1 cache: bad magic");
+    auto m = std::make_unique<CsbHost>();
+    m->nrows = static_cast<index_t>(get<std::uint64_t>(is));
+    m->ncols = static_cast<index_t>(get<std::uint64_t>(is));
+    m->nrowblks = static_cast<index_t>(get<std::uint64_t>(is));
+    m->ncolblks = static_cast<index_t>(get<std::uint64_t>(is));
+    if (m->nrowblks < 1 || m->ncolblks < 1 || m->nrowblks > (1 << 24) || m->ncolblks > (1 << 24))
+        fail(BE_ERR_PARSE, "CSB1 cache: implausible block counts");
+    if (b0 < 0 || b1 < b0 || b1 > m->nrowblks) fail(BE_ERR_BAD_PARAMS, "load_csb rows: bad block-row range");
+    auto get_u64s = [&](std::vector<index_t>& a, index_t n) {
+        a.resize(static_cast<std::size_t>(n));
+        for (auto& x : a) x = static_cast<index_t>(get<std::uint64_t>(is));
+    };
+    get_u64s(m->row_offsets, m->nrowblks + 1);
+    get_u64s(m->col_offsets, m->ncolblks + 1);
+    std::vector<index_t> bn, bo;
+    get_u64s(bn, m->nrowblks * m->ncolblks);
+    get_u64s(bo, m->nrowblks * m->ncolblks);
+    if (!is) fail(BE_ERR_PARSE, "CSB1 cache: truncated header");
+    const std::streamoff data0 = is.tellg();
+    const index_t nnz_all = std::accumulate(bn.begin(), bn.end(), index_t{0});
+    const index_t nb = m->ncolblks;
+    const index_t k0 = b0 < m->nrowblks ? bo[static_cast<std::size_t>(b0 * nb)] : nnz_all;
+    const index_t k1 = b1 < m->nrowblks ? bo[static_cast<std::size_t>(b1 * nb)] : nnz_all;
+    m->block_nnz.assign(bn.size(), 0);
+    m->block_nnz_offsets.assign(bn.size(), 0);
+    index_t acc = 0;
+    for (std::size_t b = 0; b < bn.size(); ++b) {
+        const index_t bi = static_cast<index_t>(b) / nb;
+        if (bi >= b0 && bi < b1) m->block_nnz[b] = bn[b];
+        m->block_nnz_offsets[b] = acc;
+        acc += m->block_nnz[b];
+    }
+    if (acc != k1 - k0) fail(BE_ERR_PARSE, "CSB1 cache: block tables are not block row-major");
+    m->allocate(acc);
+    is.seekg(data0 + static_cast<std::streamoff>(4 * k0));
+    {
+        const index_t chunk = 1 << 20;
+        std::vector<std::uint16_t> buf(static_cast<std::size_t>(2 * chunk));
+        for (index_t q0 = 0; q0 < acc; q0 += chunk) {
+            const index_t q1 = std::min(acc, q0 + chunk);
+            is.read(reinterpret_cast<char*>(buf.data()), static_cast<std::streamsize>(4 * (q1 - q0)));
+            if (!is) fail(BE_ERR_PARSE, "CSB1 cache: truncated file");
+            for (index_t k = q0; k < q1; ++k) {
+                m->local_rows[k] = buf[static_cast<std::size_t>(2 * (k - q0))];
+                m->local_cols[k] = buf[static_cast<std::size_t>(2 * (k - q0) + 1)];
+            }
+        }
+    }
+    is.seekg(data0 + static_cast<std::streamoff>(4 * nnz_all + 8 * k0));
+    is.read(reinterpret_cast<char*>(m->values.data()), static_cast<std::streamsize>(acc * 8));
+    if (!is) fail(BE_ERR_PARSE, "CSB1 cache: truncated values");
+    if (diag) {
+        diag->clear();
+        is.seekg(data0 + static_cast<std::streamoff>(12 * nnz_all));
+        std::uint64_t dlen = 0;
+        is.read(reinterpret_cast<char*>(&dlen), 8);
+        if (is && dlen > 0) {
+            if (static_cast<index_t>(dlen) != m->nrows) fail(BE_ERR_PARSE, "cache: diagonal length mismatch");
+            const index_t r0 = m->row_offsets[static_cast<std::size_t>(b0)], r1 = m->row_offsets[static_cast<std::size_t>(b1)];
+            is.seekg(data0 + static_cast<std::streamoff>(12 * nnz_all + 8 + 8 * r0));
+            diag->resize(static_cast<std::size_t>(r1 - r0));
+            is.read(reinterpret_cast<char*>(diag->data()), static_cast<std::streamsize>((r1 - r0) * 8));
+            if (!is) fail(BE_ERR_PARSE, "cache: truncated diagonal section");
+        }
+    }
+    m->nnz = acc;
+    return m;
+}
+
 std::unique_ptr<CsbHost> load_csb1(const std::string& path, std::vector<double>* diag) {
     std::ifstream is(path, std::ios::binary);
     if (!is) fail(BE_ERR_PARSE, "cannot open " + path);

@@ -185,3 +185,22 @@ def test_tri_partition_matches_reference(nd):
         assert (int(beg[rank]), int(end[rank])) == seg
         total += len(t)
     assert total == m.nnz
+
+
+def test_csb1_slab_loader(tmp_path):
+    """A rank reads only its block rows of a CSB1 cache (csb.hpp:204-302 format,
+    driver.hpp:136-161 diagonal section): same arrays as slicing the whole matrix."""
+    n = 2500
+    s = abi.Synthetic("random", n=n, density=0.01, block_extent=400, seed=12)
+    b = abi.uniform_boundaries(n, 400)
+    m = abi.build_csb_coo(s.lower, n, n, b, b)
+    path = tmp_path / "h.csb"
+    m.save(path, s.diag)
+    for b0, b1 in [(0, 7), (0, 3), (2, 5), (6, 7), (4, 4)]:
+        got, d = abi.Csb.load_rows(path, b0, b1)
+        want = m.slab(b0, b1)
+        for f in ("row_offsets", "col_offsets", "block_nnz", "block_nnz_offsets", "local_rows", "local_cols", "values"):
+            assert np.array_equal(getattr(got, f), getattr(want, f)), f
+        lo, hi = int(b[b0]), int(b[b1])
+        if hi > lo:
+            assert np.array_equal(d, s.diag[lo:hi])
