@@ -45,7 +45,11 @@ namespace be {
 
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef BE_SPMM_TPR
+#define BE_SPMM_TPR 1
+#endif
+constexpr int kTPR = BE_SPMM_TPR;          // threads per row / column rank (they split its entries)
+constexpr int kThreads = 256 * kTPR;
 constexpr index_t kRunMax = 32;  // tiles per work item
 
 template <typename TC>
@@ -143,7 +147,11 @@ struct XGeom {
     static constexpr int VEC = Vec<TC>::N;                          // elements per 16-byte chunk
     static constexpr int CH = NBP / VEC;                            // chunks per row
     static constexpr int RB = NBP * static_cast<int>(sizeof(TC));  // row bytes
+#ifdef BE_SPMM_NOREP
+    static constexpr int LINEB = RB;                                // one copy per row line
+#else
     static constexpr int LINEB = RB < 128 ? 128 : RB;               // bytes per smem row line
+#endif
     static constexpr int REP = LINEB / RB;                          // replicas per line
     static_assert(NBP % VEC == 0 && CH >= 1, "bad NBP");
 };
@@ -208,7 +216,10 @@ template <int NBP, typename TC, typename TV, typename TX>
 struct Stage {
     // raw X_J rows (staged asynchronously when small; else loaded directly)
     static constexpr int XRAW = kTile * NBP * static_cast<int>(sizeof(TX));
-    static constexpr int XB = XRAW <= 16384 ? XRAW : 0;
+#ifndef BE_SPMM_XRAW_MAX
+#define BE_SPMM_XRAW_MAX 0  // X_J rows staged raw with the tile (cp.async) up to this size (0: loaded into the lines directly, which frees the smem for a third CTA per SM)
+#endif
+    static constexpr int XB = XRAW <= BE_SPMM_XRAW_MAX ? XRAW : 0;
     __host__ __device__ static std::size_t bytes(int max_nnz) {
         return static_cast<std::size_t>(max_nnz) * (sizeof(TV) + 4) + XB + 256;
     }
@@ -255,27 +266,33 @@ __device__ __forceinline__ void stage_issue(unsigned char* st, int max_nnz, cons
 // Threads 0-127 build the row table, 128-255 the column table.
 __device__ __forceinline__ void jds_starts(const unsigned char* sl, std::uint16_t* jd_r, std::uint16_t* jd_c,
                                            int* s_tot) {
-    const int tid = threadIdx.x, grp = tid >> 7, j = tid & 127, lane = tid & 31, warp = tid >> 5;
+    // threads 0-255 work (every thread of the CTA passes the barrier)
+    const int tid = threadIdx.x, grp = (tid >> 7) & 1, j = tid & 127, lane = tid & 31, warp = tid >> 5;
     const unsigned char* len = sl + grp * 128;
-    int lo = 0, hi = 128;  // count_j = #ranks with len > j (lengths are non-increasing)
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (len[mid] > j) lo = mid + 1; else hi = mid;
-    }
-    const int cnt = lo;
-    int incl = cnt;
+    int cnt = 0, incl = 0;
+    if (tid < 256) {
+        int lo = 0, hi = 128;  // count_j = #ranks with len > j (lengths are non-increasing)
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (len[mid] > j) lo = mid + 1; else hi = mid;
+        }
+        cnt = lo;
+        incl = cnt;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_tot[warp] = incl;
     }
-    if (lane == 31) s_tot[warp] = incl;
     __syncthreads();
-    int start = incl - cnt;
-    for (int w = grp * 4; w < warp; ++w) start += s_tot[w];
-    std::uint16_t* jd = grp == 0 ? jd_r : jd_c;
-    jd[j] = static_cast<std::uint16_t>(start);
-    if (j == 127) jd[128] = static_cast<std::uint16_t>(start + cnt);
+    if (tid < 256) {
+        int start = incl - cnt;
+        for (int w = grp * 4; w < warp; ++w) start += s_tot[w];
+        std::uint16_t* jd = grp == 0 ? jd_r : jd_c;
+        jd[j] = static_cast<std::uint16_t>(start);
+        if (j == 127) jd[128] = static_cast<std::uint16_t>(start + cnt);
+    }
 }
 
 // One work item = a run of consecutive tiles of the same 128-row tile-row.
@@ -285,7 +302,10 @@ __device__ __forceinline__ void jds_starts(const unsigned char* sl, std::uint16_
 // row rank, walks its row through the JDS table; pass C (warps 4-7): lane =
 // column rank, walks its column through cperm. Y_J is flushed per tile.
 template <int NBP, typename TC, typename TV, typename TX>
-__global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? 2 : 1)
+#ifndef BE_SPMM_MINB
+#define BE_SPMM_MINB 3  // CTAs per SM (nb <= 16, f32): 80 registers, 73 KB smem
+#endif
+__global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? BE_SPMM_MINB : 1)
     k_sym_spmm(const int2* __restrict__ runs, int nruns, const TileHdr* __restrict__ tiles,
                const unsigned char* __restrict__ lens, const TV* __restrict__ vals,
                const std::uint16_t* __restrict__ rc, const std::uint16_t* __restrict__ cperm,
@@ -306,8 +326,9 @@ __global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? 2 :
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    const int grp = tid >> 7;  // 0: pass R (row ranks), 1: pass C (column ranks)
-    const int rank = tid & 127;
+    const int grp = tid / (128 * kTPR);  // 0: pass R (row ranks), 1: pass C (column ranks)
+    const int rank = (tid % (128 * kTPR)) / kTPR;
+    const int hpart = tid % kTPR;        // this thread's share of the rank's entries: j = hpart (mod kTPR)
     const bool vec_ok = (nb % G::VEC) == 0;
     const bool xvec = S::XB > 0 && nb == NBP && (NBP * sizeof(TX)) % 16 == 0 &&
                       (reinterpret_cast<std::uintptr_t>(X) & 15u) == 0;
@@ -362,36 +383,54 @@ __global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? 2 :
             }
             jds_starts(sl, s_jd[0], s_jd[1], s_tot);
             __syncthreads();
-            const int len = sl[tid];
-            if (len > 0 && (grp == 0 ? do_r : do_c)) {
+            const int len = sl[grp * 128 + rank];
+            const bool active = len > 0 && (grp == 0 ? do_r : do_c);
+            {
                 const std::uint16_t* jd = s_jd[grp];
                 V acc[G::CH];
 #pragma unroll
                 for (int i = 0; i < G::CH; ++i) vzero(acc[i]);
                 int first = 0;
-                for (int j = 0; j < len; ++j) {
-                    int pos = jd[j] + rank;
-                    if (grp == 1) pos = scp[pos];
-                    const TC v = static_cast<TC>(sv[pos]);
-                    const std::uint32_t x = src[pos];
-                    if (j == 0) first = x;
-                    const unsigned char* p = xbase + (grp == 0 ? (x & 255u) : (x >> 8)) * G::LINEB;
-                    V xv[G::CH];
+                if (active)
+                    for (int j = hpart; j < len; j += kTPR) {
+                        int pos = jd[j] + rank;
+                        if (grp == 1) pos = scp[pos];
+                        const TC v = static_cast<TC>(sv[pos]);
+                        const std::uint32_t x = src[pos];
+                        if (j == 0) first = x;
+                        const unsigned char* p = xbase + (grp == 0 ? (x & 255u) : (x >> 8)) * G::LINEB;
+                        V xv[G::CH];
 #pragma unroll
-                    for (int i = 0; i < G::CH; ++i) xv[i] = *reinterpret_cast<const V*>(p + coff[i]);
+                        for (int i = 0; i < G::CH; ++i) xv[i] = *reinterpret_cast<const V*>(p + coff[i]);
 #pragma unroll
-                    for (int i = 0; i < G::CH; ++i) vfma(acc[i], v, xv[i]);
-                }
-                if (grp == 0) {  // Y_I += A X_J for this row
-                    V* y = yi + (first >> 8) * G::CH;
-#pragma unroll
-                    for (int i = 0; i < G::CH; ++i) vadd(y[(i + lane) % G::CH], acc[i]);
-                } else {  // Y_J += A^T X_I for this column
-                    TX* y = Y + static_cast<std::int64_t>(col0 + (first & 255)) * nb;
+                        for (int i = 0; i < G::CH; ++i) vfma(acc[i], v, xv[i]);
+                    }
+                if constexpr (kTPR == 2) {  // the pair (adjacent lanes, same rank) sums its halves
 #pragma unroll
                     for (int i = 0; i < G::CH; ++i) {
-                        const int c0 = ((i + lane) % G::CH) * G::VEC;
-                        if (c0 < nb) flush<TX>(y + c0, acc[i], nb - c0, vec_ok);
+                        if constexpr (sizeof(TC) == 4) {
+                            acc[i].x += __shfl_xor_sync(0xffffffffu, acc[i].x, 1);
+                            acc[i].y += __shfl_xor_sync(0xffffffffu, acc[i].y, 1);
+                            acc[i].z += __shfl_xor_sync(0xffffffffu, acc[i].z, 1);
+                            acc[i].w += __shfl_xor_sync(0xffffffffu, acc[i].w, 1);
+                        } else {
+                            acc[i].x += __shfl_xor_sync(0xffffffffu, acc[i].x, 1);
+                            acc[i].y += __shfl_xor_sync(0xffffffffu, acc[i].y, 1);
+                        }
+                    }
+                }
+                if (active && hpart == 0) {
+                    if (grp == 0) {  // Y_I += A X_J for this row
+                        V* y = yi + (first >> 8) * G::CH;
+#pragma unroll
+                        for (int i = 0; i < G::CH; ++i) vadd(y[(i + lane) % G::CH], acc[i]);
+                    } else {  // Y_J += A^T X_I for this column
+                        TX* y = Y + static_cast<std::int64_t>(col0 + (first & 255)) * nb;
+#pragma unroll
+                        for (int i = 0; i < G::CH; ++i) {
+                            const int c0 = ((i + lane) % G::CH) * G::VEC;
+                            if (c0 < nb) flush<TX>(y + c0, acc[i], nb - c0, vec_ok);
+                        }
                     }
                 }
             }
@@ -782,7 +821,10 @@ std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag
 // Tile-format build + upload shared by the single- and multi-GPU operators.
 static void op_build(Op* op, const be_csb_view& L, const RowMap* map) {
     const int values_prec = op->values_prec;
-    op->max_nnz = values_prec == BE_F32 ? 2048 : 1024;
+#ifndef BE_SPMM_MAXNNZ
+#define BE_SPMM_MAXNNZ 2048
+#endif
+    op->max_nnz = values_prec == BE_F32 ? BE_SPMM_MAXNNZ : 1024;
     const bool keep_src = L.nnz <= (index_t{1} << 26);
 
     std::vector<RowOut> rows(static_cast<std::size_t>(L.nrowblks));

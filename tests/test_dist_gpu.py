@@ -229,8 +229,11 @@ def test_weak_scaling_glue_matches_whole_matrix(ctx, world):
     kw = dict(n=24000, target_nnz=3_000_000, block_extent=2000, seed=3)
     p = abi.clustered_params(**kw)
     whole, diag, toff = abi.generate_clustered(**kw)
+    # tol 3e-5: with the FOM preconditioner this clustered problem has a residual floor near 3e-6
+    # relative -- the reference's own preconditioned solve (oracle/_ref, f64) stalls at maxiter
+    # for tol 1e-6 too (no preconditioner: converges) -- so the tolerance sits well above it
     single = abi.lobpcg(ctx, abi.Operator(ctx, whole, diag), tiles=abi.Tiles(ctx, whole, diag, toff), k=8, nb=16,
-                        tol=1e-6, maxiter=300, seed=1)
+                        tol=3e-5, maxiter=300, seed=1)
     slots = [None] * world
     bar = threading.Barrier(world)
 
@@ -246,11 +249,12 @@ def test_weak_scaling_glue_matches_whole_matrix(ctx, world):
 
         rp = weak.rank_problem(c, comm, p, r, world, True, allreduce_sum)
         assert np.allclose(rp["diag"], diag[rp["lo"]:rp["hi"]], rtol=1e-13, atol=0)
-        res = abi.lobpcg(c, rp["op"], tiles=rp["tiles"], k=8, nb=16, tol=1e-6, maxiter=300, seed=1)
+        res = abi.lobpcg(c, rp["op"], tiles=rp["tiles"], k=8, nb=16, tol=3e-5, maxiter=300, seed=1)
         rp["op"].close()
         return res
 
     res = run_ranks(world, rank)
+    assert single["converged"] and res[0]["converged"]
     assert np.max(np.abs(res[0]["lambda_"] - single["lambda_"]) / single["lambda_"]) <= 1e-6
     assert abs(res[0]["iterations"] - single["iterations"]) <= 2
 

@@ -250,4 +250,52 @@ int main4() {
     }
     return 0;
 }
-int main() { main4(); return 0; }
+int main5() {  // cold data: rotate over 4 distinct 371 MB buffers (L2 cannot help)
+    long n = 2900000;
+    double *x[4], *out;
+    for (auto& p : x) { cudaMalloc(&p, n * 128); cudaMemset(p, 1, n * 128); }
+    cudaMalloc(&out, 8);
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (int g : {sms * 4, sms * 8, sms * 16}) {
+        k_plain<<<g, 256>>>((const double2*)x[0], n * 8, out);
+        cudaEventRecord(a);
+        for (int i = 0; i < 8; ++i) k_plain<<<g, 256>>>((const double2*)x[i % 4], n * 8, out);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        printf("cold plain grid=%d: %.0f GB/s\n", g, n * 128.0 * 8 / (ms * 1e-3) / 1e9);
+    }
+    auto ring = [&](auto kern, int S, int R, int cps, int tpb, const char* name) {
+        size_t sm = (size_t)S * (R * 18 + 2) * 8;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        int grid = sms * cps;
+        kern<<<grid, tpb, sm>>>(x[0], n, R, out);
+        cudaEventRecord(a);
+        for (int i = 0; i < 8; ++i) kern<<<grid, tpb, sm>>>(x[i % 4], n, R, out);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        printf("cold %s S=%d R=%d ctas/sm=%d tpb=%d: %.0f GB/s %s\n", name, S, R, cps, tpb, n * 128.0 * 8 / (ms * 1e-3) / 1e9,
+               cudaGetErrorString(cudaGetLastError()));
+    };
+    ring(k_ring<4, 0>, 4, 256, 1, 256, "ring");
+    ring(k_ring<6, 0>, 6, 128, 1, 256, "ring");
+    ring(k_ring<4, 0>, 4, 128, 2, 256, "ring");
+    ring(k_ring<8, 0>, 8, 64, 2, 256, "ring");
+    ring(k_ring<4, 0>, 4, 64, 4, 256, "ring");
+    ring(k_ring<4, 1>, 4, 256, 1, 256, "ring+gram");
+    ring(k_ring<4, 1>, 4, 128, 2, 256, "ring+gram");
+    ring(k_ring<4, 1>, 4, 64, 4, 256, "ring+gram");
+    ring(k_ring<3, 1>, 3, 64, 6, 256, "ring+gram");
+    ring(k_ring<4, 1>, 4, 256, 1, 512, "ring+gram");
+    ring(k_ring<4, 1>, 4, 256, 1, 1024, "ring+gram");
+    ring(k_ring<4, 1>, 4, 128, 2, 1024, "ring+gram");
+    return 0;
+}
+int main() { main5(); return 0; }
