@@ -48,6 +48,9 @@ namespace {
 #ifndef BE_SPMM_TPR
 #define BE_SPMM_TPR 1
 #endif
+#ifndef BE_SPMM_STAGES
+#define BE_SPMM_STAGES 1  // tile staging buffers per CTA (1: copy/compute overlap comes from the other CTAs of the SM)
+#endif
 constexpr int kTPR = BE_SPMM_TPR;          // threads per row / column rank (they split its entries)
 constexpr int kThreads = 256 * kTPR;
 constexpr index_t kRunMax = 32;  // tiles per work item
@@ -303,7 +306,7 @@ __device__ __forceinline__ void jds_starts(const unsigned char* sl, std::uint16_
 // column rank, walks its column through cperm. Y_J is flushed per tile.
 template <int NBP, typename TC, typename TV, typename TX>
 #ifndef BE_SPMM_MINB
-#define BE_SPMM_MINB 3  // CTAs per SM (nb <= 16, f32): 80 registers, 73 KB smem
+#define BE_SPMM_MINB 4  // CTAs per SM (nb <= 16, f32): 64 registers, 55 KB smem
 #endif
 __global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? BE_SPMM_MINB : 1)
     k_sym_spmm(const int2* __restrict__ runs, int nruns, const TileHdr* __restrict__ tiles,
@@ -351,12 +354,12 @@ __global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? BE_
         if (do_r)
             for (int e = tid; e < kTile * G::CH; e += kThreads) vzero(yi[e]);
         for (int t = rg.x; t < rg.y; ++t) {
-            unsigned char* st = stg0 + ((t - rg.x) & 1) * sbytes;
+            unsigned char* st = stg0 + (BE_SPMM_STAGES == 2 ? ((t - rg.x) & 1) * sbytes : 0);
             const int nc = static_cast<int>((h.packed >> 7) & 127u) + 1;
             const int col0 = h.col0;
             cp_wait_all();
             __syncthreads();  // stage t complete and visible; stage t+1's buffer is free
-            if (t + 1 < rg.y) {
+            if (BE_SPMM_STAGES == 2 && t + 1 < rg.y) {
                 h = tiles[t + 1];
                 stage_issue<NBP, TC, TV, TX>(stg0 + ((t + 1 - rg.x) & 1) * sbytes, max_nnz, h, t + 1, lens, vals, rc,
                                              cperm, X, nb, do_r, do_c, xvec);
@@ -433,6 +436,12 @@ __global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? BE_
                         }
                     }
                 }
+            }
+            if (BE_SPMM_STAGES == 1 && t + 1 < rg.y) {  // single buffer: refill after everyone is done with it
+                __syncthreads();
+                h = tiles[t + 1];
+                stage_issue<NBP, TC, TV, TX>(stg0, max_nnz, h, t + 1, lens, vals, rc, cperm, X, nb, do_r, do_c, xvec);
+                cp_commit();
             }
         }
         cp_wait_all();
@@ -521,7 +530,7 @@ template <int NBP, typename TC, typename TV, typename TX>
 std::size_t smem_bytes(int max_nnz) {
     using G = XGeom<NBP, TC>;
     const std::size_t sb = (Stage<NBP, TC, TV, TX>::bytes(max_nnz) + 15) & ~static_cast<std::size_t>(15);
-    return 2 * kTile * G::LINEB + kTile * G::CH * 16 + 2 * sb;
+    return 2 * kTile * G::LINEB + kTile * G::CH * 16 + BE_SPMM_STAGES * sb;
 }
 
 template <int NBP, typename TC, typename TV, typename TX>
@@ -822,7 +831,7 @@ std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag
 static void op_build(Op* op, const be_csb_view& L, const RowMap* map) {
     const int values_prec = op->values_prec;
 #ifndef BE_SPMM_MAXNNZ
-#define BE_SPMM_MAXNNZ 2048
+#define BE_SPMM_MAXNNZ 1792  // f32 entries per tile piece (keeps four CTAs per SM)
 #endif
     op->max_nnz = values_prec == BE_F32 ? BE_SPMM_MAXNNZ : 1024;
     const bool keep_src = L.nnz <= (index_t{1} << 26);
