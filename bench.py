@@ -61,6 +61,7 @@ def args_parse():
     ap.add_argument("--nev", type=int, default=8)
     ap.add_argument("--precond", choices=["on", "off"], default="on")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gate", action="store_true", help="skip the correctness gate against the reference SpMM")
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--seed", type=int, default=1)
     return ap.parse_args()
@@ -180,6 +181,24 @@ def cpu_reference(m, diag, toff, nev, nb, iters, seed, precond):
     finally:
         lib.ref_release(h)
     return per, cores, ent
+
+
+def correctness_gate(op, m, diag, nb, seed):
+    """The reference driver's gate (driver.hpp:299-373: no timing for a failing
+    output), precision-aware: one device SpMM against the reference's own
+    SymmetricOperator::apply (oracle/_ref, f64, all host threads) on the same
+    X; pass when the relative Frobenius error is <= 1e-5 (f32 values)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as ol
+    if ol.ref() is None:
+        return {"ok": None, "why": "oracle/_ref/libref.so not built"}
+    x = np.random.default_rng(seed + 3).uniform(-1, 1, (m.nrows, nb))
+    t0 = time.time()
+    y = op.apply_host(x)
+    want = ol.Impl("ref", threads=os.cpu_count() or 1).spmm(m, diag, x)
+    rel = float(np.linalg.norm(y - want) / np.linalg.norm(want))
+    return {"ok": rel <= 1e-5, "rel_frobenius": rel, "tol": 1e-5, "seconds": time.time() - t0,
+            "vs": "reference SymmetricOperator::apply (f64, oracle/_ref), X = U(-1,1) seed+3"}
 
 
 def run_reference(a, rank):
@@ -381,6 +400,7 @@ def main():
     e_s = time.perf_counter() - e0
     e2e_val = world * b_iter * r2["iterations"] / e_s / 1e9
 
+    gate = None if a.no_gate else correctness_gate(op, m, diag, a.nb, a.seed)
     cpu = None
     if rank == 0 and not a.no_cpu_baseline:
         got = cpu_reference(m, diag, toff, a.nev, a.nb, a.cpu_iters, a.seed, precond)
@@ -403,6 +423,7 @@ def main():
                 "iterations": r2["iterations"], "seconds": e_s},
         "gpu_launches": launches,
         "clocks": clk,
+        "gate": gate,
         "lobpcg": {"iter_ms": ms_step, "spmm_ms": spmm_ms, "precond_ms": 1e3 * float(np.mean(rec[:, 1])),
                    "setup_s": {"generate": t_gen, "upload": t_up}, "parallelism": "1 GPU"},
     }

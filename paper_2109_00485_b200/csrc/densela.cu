@@ -2,6 +2,7 @@
 // Memory-bound fused panel kernels (Gram, row mixes, trsm, residual norms)
 // and single-CTA kernels for the <= 3nb square projected problem; the
 // symmetric eigen-decomposition itself is cuSOLVER syevd (no host fallback).
+#include <cublas_v2.h>
 #include <cusolverDn.h>
 
 #include <algorithm>
@@ -464,7 +465,13 @@ struct MixDev {
 // with 16-byte coalesced loads (row stride nb + 1 doubles: conflict-free
 // column reads), then thread = (row, 4-column block) forms every output for
 // its row from smem and the transposed coefficients.
-constexpr int kMixRows = 64;
+#ifndef BE_MIX_ROWS
+#define BE_MIX_ROWS 64
+#endif
+#ifndef BE_MIX_CTAS
+#define BE_MIX_CTAS 4  // CTAs per SM in the grid
+#endif
+constexpr int kMixRows = BE_MIX_ROWS;
 struct MixSrc {
     int nsrc;
     const double* src[8];
@@ -806,43 +813,26 @@ __global__ void k_chol(const double* B, double* R, int n, double rel_floor, int 
     if (threadIdx.x == 0) st->not_pd = p + 1;
 }
 
-// M = R^-T A R^-1 (densela.hpp:366-390); skipped after a failed Cholesky
-__global__ void k_sygv_form(const double* A, const double* R, double* Y, double* M, int n, const Status* st) {
-    if (st->not_pd) return;
-    for (int j = threadIdx.x; j < n; j += blockDim.x)  // Y = R^-T A, column j
-        for (int i = 0; i < n; ++i) {
-            double s = A[j * n + i];
-            for (int t = 0; t < i; ++t) s -= R[i * n + t] * Y[j * n + t];
-            Y[j * n + i] = s / R[i * n + i];
-        }
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x)  // M R = Y, row i
-        for (int j = 0; j < n; ++j) {
-            double s = Y[j * n + i];
-            for (int t = 0; t < j; ++t) s -= M[t * n + i] * R[j * n + t];
-            M[j * n + i] = s / R[j * n + j];
-        }
-    __syncthreads();
+// symmetrise M in place (0.5 (M_ij + M_ji)); after a failed Cholesky the
+// pencil is meaningless (the host drops it): M = I keeps the eigensolver sane
+__global__ void k_sym_or_identity(double* M, int n, const Status* st) {
+    const bool bad = st->not_pd != 0;
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
         const int j = e / n, i = e % n;
-        if (i < j) {
-            const double s = 0.5 * (M[j * n + i] + M[i * n + j]);
-            M[j * n + i] = s;
-            M[i * n + j] = s;
+        if (bad) {
+            M[e] = i == j ? 1.0 : 0.0;
+        } else if (i < j) {
+            const double v = 0.5 * (M[j * n + i] + M[i * n + j]);
+            M[j * n + i] = v;
+            M[i * n + j] = v;
         }
     }
 }
 
-// C = R^-1 Q_k, then normalize_column_signs (densela.hpp:327-341, 393-405)
-__global__ void k_sygv_back(const double* Q, const double* w, const double* R, double* C, double* d, int n, int k,
-                            const Status* st) {
+// normalize_column_signs (densela.hpp:327-341) of C (n x k) and d = w[:k]
+__global__ void k_sign_fix(double* C, const double* w, double* d, int n, int k, const Status* st) {
     if (st->not_pd) return;
     for (int j = threadIdx.x; j < k; j += blockDim.x) {
-        for (int i = n - 1; i >= 0; --i) {
-            double s = Q[j * n + i];
-            for (int t = i + 1; t < n; ++t) s -= R[t * n + i] * C[j * n + t];
-            C[j * n + i] = s / R[i * n + i];
-        }
         int arg = 0;
         double best = -1.0;
         for (int i = 0; i < n; ++i) {
@@ -896,16 +886,31 @@ __global__ void __launch_bounds__(kT) k_residual(const double* __restrict__ hx, 
     }
 }
 
+// column sums of the per-CTA partials: 256 threads = (column, part) with the
+// parts summed in a fixed order (deterministic)
 __global__ void k_norm_reduce(const double* __restrict__ partial, int nparts, int nb, double* out_r, double* out_x) {
-    const int c = threadIdx.x;
-    if (c >= nb) return;
+    __shared__ double red[2][256];
+    const int tid = threadIdx.x;
+    const int P = blockDim.x / nb;  // parts
+    const int c = tid % nb, q = tid / nb;
     double a = 0.0, b = 0.0;
-    for (int p = 0; p < nparts; ++p) {
-        a += partial[(static_cast<std::int64_t>(p) * 2 + 0) * nb + c];
-        b += partial[(static_cast<std::int64_t>(p) * 2 + 1) * nb + c];
+    if (q < P)
+        for (int p = q; p < nparts; p += P) {
+            a += partial[(static_cast<std::int64_t>(p) * 2 + 0) * nb + c];
+            b += partial[(static_cast<std::int64_t>(p) * 2 + 1) * nb + c];
+        }
+    red[0][tid] = a;
+    red[1][tid] = b;
+    __syncthreads();
+    if (tid < nb) {
+        double sa = 0.0, sb = 0.0;
+        for (int k = 0; k < P; ++k) {
+            sa += red[0][k * nb + tid];
+            sb += red[1][k * nb + tid];
+        }
+        if (out_r) out_r[tid] = sa;
+        if (out_x) out_x[tid] = sb;
     }
-    if (out_r) out_r[c] = a;
-    if (out_x) out_x[c] = b;
 }
 
 __global__ void k_scale_columns(double* a, double* ha, const double* norm2, int nb, std::int64_t n, const Status* st) {
@@ -1098,7 +1103,7 @@ void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
     const std::size_t sm = (static_cast<std::size_t>(m.ncoef) * job.nb * nblk * 4 +
                             static_cast<std::size_t>(ms.nsrc) * kMixRows * (job.nb + 1)) * sizeof(double);
     ensure_dyn_smem(k_mix, sm);
-    const int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 4, (n + kMixRows - 1) / kMixRows)));
+    const int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * BE_MIX_CTAS, (n + kMixRows - 1) / kMixRows)));
     k_mix<<<grid, kT, sm, s>>>(m, ms, nullptr, n);
     BE_CUDA(cudaGetLastError());
     ++ctx->launches;
@@ -1162,7 +1167,7 @@ void residual(Ctx* ctx, const double* hx, const double* x, const double* theta, 
     if (nb > kT) fail(BE_ERR_BAD_PARAMS, "residual: nb too large");
     const int grid = grid_rows(ctx, n, kT / nb * 64);
     k_residual<<<grid, kT, 0, s>>>(hx, x, theta, r, nb, n, partials, 0);
-    k_norm_reduce<<<1, 64, 0, s>>>(partials, grid, nb, rnorm2, xnorm2);
+    k_norm_reduce<<<1, 256, 0, s>>>(partials, grid, nb, rnorm2, xnorm2);
     BE_CUDA(cudaGetLastError());
     ctx->launches += 2;
 }
@@ -1170,7 +1175,7 @@ void residual(Ctx* ctx, const double* hx, const double* x, const double* theta, 
 void colnorm2(Ctx* ctx, const double* a, int nb, std::int64_t n, double* partials, double* out, cudaStream_t s) {
     const int grid = grid_rows(ctx, n, kT / nb * 64);
     k_residual<<<grid, kT, 0, s>>>(nullptr, a, nullptr, nullptr, nb, n, partials, 1);
-    k_norm_reduce<<<1, 64, 0, s>>>(partials, grid, nb, nullptr, out);
+    k_norm_reduce<<<1, 256, 0, s>>>(partials, grid, nb, nullptr, out);
     BE_CUDA(cudaGetLastError());
     ctx->launches += 2;
 }
@@ -1208,8 +1213,22 @@ void sygv_lowest(Ctx* ctx, Sygv& ws, double* A, const double* B, int n, int k, d
     if (k < 1 || k > n) fail(BE_ERR_BAD_PARAMS, "sygv_lowest: k out of range");
     ws.ensure(ctx, n);
     chol_floored(ctx, B, ws.R.get(), n, pivot_floor, st, s);
-    double* Y = ws.work.get() + std::max(ws.lwork, 1);
-    k_sygv_form<<<1, 128, 0, s>>>(A, ws.R.get(), Y, ws.M.get(), n, st);
+    // M = R^-T A R^-1 (densela.hpp:366-390) as two cuBLAS triangular solves,
+    // then symmetrised (identity after a failed Cholesky: the host discards it)
+    if (!ctx->blas) {
+        cublasHandle_t h = nullptr;
+        if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) fail(BE_ERR_CUSOLVER, "cublasCreate failed");
+        ctx->blas = h;
+    }
+    BE_CUDA(cudaMemcpyAsync(ws.M.get(), A, static_cast<std::size_t>(n) * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    const double one = 1.0;
+    if (cublasSetStream(ctx->blas, s) != CUBLAS_STATUS_SUCCESS ||
+        cublasDtrsm(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, n, n, &one,
+                    ws.R.get(), n, ws.M.get(), n) != CUBLAS_STATUS_SUCCESS ||
+        cublasDtrsm(ctx->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n, n, &one,
+                    ws.R.get(), n, ws.M.get(), n) != CUBLAS_STATUS_SUCCESS)
+        fail(BE_ERR_CUSOLVER, "cublasDtrsm failed");
+    k_sym_or_identity<<<1, 256, 0, s>>>(ws.M.get(), n, st);
     BE_CUDA(cudaGetLastError());
     BE_CUSOLVER(cusolverDnSetStream(ctx->solver, s));
     int lw = 0;
@@ -1218,7 +1237,12 @@ void sygv_lowest(Ctx* ctx, Sygv& ws, double* A, const double* B, int n, int k, d
     if (lw > ws.lwork) fail(BE_ERR_CUSOLVER, "syevd workspace grew");
     BE_CUSOLVER(cusolverDnDsyevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, ws.M.get(), n,
                                  ws.w.get(), ws.work.get(), ws.lwork, ws.info.get()));
-    k_sygv_back<<<1, 64, 0, s>>>(ws.M.get(), ws.w.get(), ws.R.get(), c, d, n, k, st);
+    // C = R^-1 Q_k (densela.hpp:393-405), then normalize_column_signs
+    BE_CUDA(cudaMemcpyAsync(c, ws.M.get(), static_cast<std::size_t>(n) * k * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (cublasDtrsm(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n, k, &one,
+                    ws.R.get(), n, c, n) != CUBLAS_STATUS_SUCCESS)
+        fail(BE_ERR_CUSOLVER, "cublasDtrsm failed");
+    k_sign_fix<<<1, 64, 0, s>>>(c, ws.w.get(), d, n, k, st);
     BE_CUDA(cudaGetLastError());
     ctx->launches += 3;
 }

@@ -10,6 +10,7 @@
 #include "host_csb.hpp"
 
 struct cusolverDnContext;
+struct cublasContext;
 
 namespace be {
 
@@ -49,6 +50,7 @@ struct Ctx {
     int num_sms = 0;
     cudaStream_t stream = nullptr;
     cusolverDnContext* solver = nullptr;
+    cublasContext* blas = nullptr;  // triangular solves of the 3nb x 3nb pencil
     long long launches = 0;  // kernels launched through this context
     ~Ctx();
 };
