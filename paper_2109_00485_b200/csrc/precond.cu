@@ -250,26 +250,25 @@ __device__ __forceinline__ void block_colsum4(double (&v)[kCW], double (*red)[16
 #pragma unroll
         for (int j = 0; j < kCW; ++j) v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
     if constexpr (NW > 1) {
+        // red rows: [buf][warp] partials, then row 2 * NW + buf: the per-column totals
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         const int cq = threadIdx.x % CQ;
         if (lane < CQ)
 #pragma unroll
             for (int j = 0; j < kCW; ++j) red[buf * NW + warp][cq * kCW + j] = v[j];
         __syncthreads();
-        double t[kCW];
+        if (threadIdx.x < C) {  // one thread per column sums the warps in order
+            double t = red[buf * NW][threadIdx.x];
+#pragma unroll
+            for (int w = 1; w < NW; ++w) t += red[buf * NW + w][threadIdx.x];
+            red[2 * NW + buf][threadIdx.x] = t;
+        }
+        __syncthreads();
         {
-            const double2 p0 = reinterpret_cast<const double2*>(&red[buf * NW][cq * kCW])[0];
-            const double2 p1 = reinterpret_cast<const double2*>(&red[buf * NW][cq * kCW])[1];
-            t[0] = p0.x, t[1] = p0.y, t[2] = p1.x, t[3] = p1.y;
+            const double2 p0 = reinterpret_cast<const double2*>(&red[2 * NW + buf][cq * kCW])[0];
+            const double2 p1 = reinterpret_cast<const double2*>(&red[2 * NW + buf][cq * kCW])[1];
+            v[0] = p0.x, v[1] = p0.y, v[2] = p1.x, v[3] = p1.y;
         }
-#pragma unroll
-        for (int w = 1; w < NW; ++w) {
-            const double2 p0 = reinterpret_cast<const double2*>(&red[buf * NW + w][cq * kCW])[0];
-            const double2 p1 = reinterpret_cast<const double2*>(&red[buf * NW + w][cq * kCW])[1];
-            t[0] += p0.x, t[1] += p0.y, t[2] += p1.x, t[3] += p1.y;
-        }
-#pragma unroll
-        for (int j = 0; j < kCW; ++j) v[j] = t[j];
         buf ^= 1;  // double-buffered: the next reduction cannot overwrite this one before all threads read it
     }
 }
@@ -302,7 +301,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
     constexpr int CQ = C / kCW;  // column chunks per row
     constexpr int RL = NT / CQ;  // row lanes
     extern __shared__ __align__(16) double sV[];  // current basis vector [dmax][C], then the staged entries
-    __shared__ __align__(16) double red[2 * (NT / 32)][16];
+    __shared__ __align__(16) double red[2 * (NT / 32) + 2][16];
     int rbuf = 0;
     const int tile = list[blockIdx.x / ngroups];
     const int grp = blockIdx.x % ngroups;
