@@ -45,14 +45,10 @@ namespace be {
 
 namespace {
 
-#ifndef BE_SPMM_TPR
-#define BE_SPMM_TPR 1
-#endif
 #ifndef BE_SPMM_STAGES
 #define BE_SPMM_STAGES 1  // tile staging buffers per CTA (1: copy/compute overlap comes from the other CTAs of the SM)
 #endif
-constexpr int kTPR = BE_SPMM_TPR;          // threads per row / column rank (they split its entries)
-constexpr int kThreads = 256 * kTPR;
+constexpr int kThreads = 256;
 constexpr index_t kRunMax = 32;  // tiles per work item
 
 template <typename TC>
@@ -183,12 +179,17 @@ __device__ __forceinline__ void stage_x(unsigned char* xs, const TX* __restrict_
                     const int c = c0 + i * kThreads;
                     if (c < total) {
                         const int r = c / CPR, v0 = (c % CPR) * EPC;
-                        const TX* e = reinterpret_cast<const TX*>(&buf[i]);
                         TC* line = reinterpret_cast<TC*>(xs + r * G::LINEB);
+                        if constexpr (sizeof(TC) == sizeof(TX)) {  // 16-byte stores (one wavefront per 8 lanes)
 #pragma unroll
-                        for (int q = 0; q < G::REP; ++q)
+                            for (int q = 0; q < G::REP; ++q) *reinterpret_cast<uint4*>(line + q * NBP + v0) = buf[i];
+                        } else {
+                            const TX* e = reinterpret_cast<const TX*>(&buf[i]);
 #pragma unroll
-                            for (int j = 0; j < EPC; ++j) line[q * NBP + v0 + j] = static_cast<TC>(e[j]);
+                            for (int q = 0; q < G::REP; ++q)
+#pragma unroll
+                                for (int j = 0; j < EPC; ++j) line[q * NBP + v0 + j] = static_cast<TC>(e[j]);
+                        }
                     }
                 }
             }
@@ -329,9 +330,8 @@ __global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? BE_
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    const int grp = tid / (128 * kTPR);  // 0: pass R (row ranks), 1: pass C (column ranks)
-    const int rank = (tid % (128 * kTPR)) / kTPR;
-    const int hpart = tid % kTPR;        // this thread's share of the rank's entries: j = hpart (mod kTPR)
+    const int grp = tid >> 7;  // 0: pass R (row ranks), 1: pass C (column ranks)
+    const int rank = tid & 127;
     const bool vec_ok = (nb % G::VEC) == 0;
     const bool xvec = S::XB > 0 && nb == NBP && (NBP * sizeof(TX)) % 16 == 0 &&
                       (reinterpret_cast<std::uintptr_t>(X) & 15u) == 0;
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? BE_
                 for (int i = 0; i < G::CH; ++i) vzero(acc[i]);
                 int first = 0;
                 if (active)
-                    for (int j = hpart; j < len; j += kTPR) {
+                    for (int j = 0; j < len; ++j) {
                         int pos = jd[j] + rank;
                         if (grp == 1) pos = scp[pos];
                         const TC v = static_cast<TC>(sv[pos]);
@@ -408,21 +408,7 @@ __global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? BE_
 #pragma unroll
                         for (int i = 0; i < G::CH; ++i) vfma(acc[i], v, xv[i]);
                     }
-                if constexpr (kTPR == 2) {  // the pair (adjacent lanes, same rank) sums its halves
-#pragma unroll
-                    for (int i = 0; i < G::CH; ++i) {
-                        if constexpr (sizeof(TC) == 4) {
-                            acc[i].x += __shfl_xor_sync(0xffffffffu, acc[i].x, 1);
-                            acc[i].y += __shfl_xor_sync(0xffffffffu, acc[i].y, 1);
-                            acc[i].z += __shfl_xor_sync(0xffffffffu, acc[i].z, 1);
-                            acc[i].w += __shfl_xor_sync(0xffffffffu, acc[i].w, 1);
-                        } else {
-                            acc[i].x += __shfl_xor_sync(0xffffffffu, acc[i].x, 1);
-                            acc[i].y += __shfl_xor_sync(0xffffffffu, acc[i].y, 1);
-                        }
-                    }
-                }
-                if (active && hpart == 0) {
+                if (active) {
                     if (grp == 0) {  // Y_I += A X_J for this row
                         V* y = yi + (first >> 8) * G::CH;
 #pragma unroll
