@@ -306,10 +306,13 @@ __device__ __forceinline__ void jds_starts(const unsigned char* sl, std::uint16_
 // row rank, walks its row through the JDS table; pass C (warps 4-7): lane =
 // column rank, walks its column through cperm. Y_J is flushed per tile.
 template <int NBP, typename TC, typename TV, typename TX>
+#ifndef BE_SPMM_MINB32
+#define BE_SPMM_MINB32 3  // CTAs per SM for 17 <= nb <= 64 (f32): 80 registers
+#endif
 #ifndef BE_SPMM_MINB
 #define BE_SPMM_MINB 4  // CTAs per SM (nb <= 16, f32): 64 registers, 55 KB smem
 #endif
-__global__ void __launch_bounds__(kThreads, (NBP <= 16 && sizeof(TC) == 4) ? BE_SPMM_MINB : 1)
+__global__ void __launch_bounds__(kThreads, sizeof(TC) == 4 ? (NBP <= 16 ? BE_SPMM_MINB : BE_SPMM_MINB32) : 1)
     k_sym_spmm(const int2* __restrict__ runs, int nruns, const TileHdr* __restrict__ tiles,
                const unsigned char* __restrict__ lens, const TV* __restrict__ vals,
                const std::uint16_t* __restrict__ rc, const std::uint16_t* __restrict__ cperm,

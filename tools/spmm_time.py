@@ -17,7 +17,7 @@ m, diag, _ = abi.generate_clustered(n=2_900_000, target_nnz=1_100_000_000, block
                                     seed=1)
 ctx = abi.Context(0)
 op = abi.Operator(ctx, m, diag, values_prec=abi.BE_F32)
-n, nb = m.nrows, 16
+n, nb = m.nrows, int(os.environ.get("NB", "16"))
 x = torch.rand(n, nb, dtype=torch.float64, device="cuda") * 2 - 1
 y = torch.empty_like(x)
 op.timing(1)
