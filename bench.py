@@ -62,6 +62,7 @@ def args_parse():
     ap.add_argument("--precond", choices=["on", "off"], default="on")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gate", action="store_true", help="skip the correctness gate against the reference SpMM")
+    ap.add_argument("--dist", action="store_true", help="run the distributed (NCCL) path even on one rank")
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--seed", type=int, default=1)
     return ap.parse_args()
@@ -247,6 +248,10 @@ def run_dist(a, rank, world, local):
 
     from paper_2109_00485_b200 import abi
     torch.cuda.set_device(local)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    os.environ.setdefault("RANK", str(rank))
+    os.environ.setdefault("WORLD_SIZE", str(world))
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = dict(CONFIGS[a.config])
     if cfg["kind"] != "clustered":
@@ -347,7 +352,7 @@ def main():
     rank, world, local = dist_env()
     if a.impl == "reference":
         return run_reference(a, rank)
-    if world > 1:
+    if world > 1 or a.dist:
         return run_dist(a, rank, world, local)
     import torch
 
