@@ -266,7 +266,13 @@ struct GramM {
 };
 
 template <int NBB>  // 8-blocks per dimension (nb / 8)
-__global__ void __launch_bounds__(256, 1) k_gram_m(GramDev g, GramM q, std::int64_t n, double* __restrict__ partial) {
+#ifndef BE_GRAM_CTAS
+#define BE_GRAM_CTAS 2  // CTAs per SM of the tensor-core Gram kernel (one CTA computes while the other waits on its ring)
+#endif
+#ifndef BE_GRAM_STAGE_KB
+#define BE_GRAM_STAGE_KB 26
+#endif
+__global__ void __launch_bounds__(256, BE_GRAM_CTAS) k_gram_m(GramDev g, GramM q, std::int64_t n, double* __restrict__ partial) {
     constexpr int MAXPW = 16 / (NBB * NBB) > 0 ? 16 / (NBB * NBB) : 1;  // <= 16 blocks per warp
     extern __shared__ __align__(16) double sbuf[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -949,7 +955,7 @@ int grid_rows(Ctx* ctx, std::int64_t n, int per) {
 std::int64_t gram_partials_len(int nb, int npairs, int num_sms) {
     const int nblk = (nb + 3) / 4, nbp8 = (nb + 7) / 8;
     return std::max(static_cast<std::int64_t>(num_sms) * 6 * npairs * nblk * nblk * 16,
-                    static_cast<std::int64_t>(2 * num_sms) * npairs * nbp8 * nbp8 * 64);
+                    static_cast<std::int64_t>(4 * num_sms) * npairs * nbp8 * nbp8 * 64);
 }
 
 void gram(Ctx* ctx, const GramJob& job, std::int64_t n, double* partials, std::int64_t partials_len, cudaStream_t s) {
@@ -985,13 +991,13 @@ void gram(Ctx* ctx, const GramJob& job, std::int64_t n, double* partials, std::i
             q.pw = (job.npairs + ngrp - 1) / ngrp;
             q.rg = 8 / ngrp;
             q.rs = job.nb + 4;
-            q.R = std::max(16, std::min(256, (40 * 1024 / (g.nd * q.rs * 8)) & ~3));
+            q.R = std::max(16, std::min(256, (BE_GRAM_STAGE_KB * 1024 / (g.nd * q.rs * 8)) & ~3));
             q.ps = q.R * q.rs;
             q.ss = g.nd * q.ps;
             const std::size_t sm = std::max(static_cast<std::size_t>(kGG) * q.ss,
                                             static_cast<std::size_t>(job.npairs) * job.nb * job.nb) * 8;
             const std::int64_t nchunks = (n + q.R - 1) / q.R;
-            const int nparts = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms, nchunks)));
+            const int nparts = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(BE_GRAM_CTAS * ctx->num_sms, nchunks)));
             if (static_cast<std::int64_t>(nparts) * job.npairs * job.nb * job.nb <= partials_len) {
 #define BE_GRAMM(NBB)                                                     \
     do {                                                                  \
