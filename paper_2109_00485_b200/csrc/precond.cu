@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
               const std::int32_t* __restrict__ rowptr, const std::uint16_t* __restrict__ cols,
               const double* __restrict__ vals, const double* __restrict__ shifts, const double* __restrict__ R,
               double* __restrict__ W, int nb, int m, int ngroups, std::int64_t* fallbacks, int dmax, int stage_cap,
-              double* __restrict__ Vg, std::int64_t nrows) {
+              double* __restrict__ Vg, std::int64_t nrows, unsigned* __restrict__ slot_mask, int kslots) {
     constexpr int C = kFomCols;
     constexpr int CQ = C / kCW;  // column chunks per row
     constexpr int RL = NT / CQ;  // row lanes
@@ -329,10 +329,21 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
     const std::size_t vstride = static_cast<std::size_t>(dmax) * C;
     double* Vcur = sV + cq * kCW;
     double* Vslot = nullptr;
-    if constexpr (!VSM) {
-        unsigned smid;
+    __shared__ int s_slot;
+    unsigned smid = 0;
+    if constexpr (!VSM) {  // claim one of the SM's kslots scratch slots (released at exit)
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        Vslot = Vg + static_cast<std::size_t>(smid) * MC * vstride + cq * kCW;
+        if (threadIdx.x == 0) {
+            int k = 0;
+            for (;;) {
+                const unsigned bit = 1u << k;
+                if (!(atomicOr(slot_mask + smid, bit) & bit)) break;
+                k = k + 1 == kslots ? 0 : k + 1;
+            }
+            s_slot = static_cast<int>(smid) * kslots + k;
+        }
+        __syncthreads();
+        Vslot = Vg + static_cast<std::size_t>(s_slot) * MC * vstride + cq * kCW;
     }
     auto vg = [&](int q, int i) -> double* {
         if constexpr (VSM) return Vcur + q * vstride + static_cast<std::size_t>(i) * C;
@@ -627,14 +638,17 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
             out[static_cast<std::int64_t>(i) * nb + j] = res;
         }
     }
+    if constexpr (!VSM) {  // every thread is done with the slot: release it
+        __syncthreads();
+        if (threadIdx.x == 0) atomicAnd(slot_mask + smid, ~(1u << (s_slot - static_cast<int>(smid) * kslots)));
+    }
 }
 
 // size classes of the block kernel: tiles up to kClassDims[c] rows run on
 // CTAs of kClassThreads[c] threads (4 per row, 16 columns per CTA)
 constexpr int kClassDims[] = {32, 64, 128, 256, 512};
-constexpr int kClassThreads[] = {32, 128, 256, 512, 512};
-constexpr bool kClassVsm[] = {true, true, true, true, false};  // whole basis in shared memory
-constexpr std::size_t kOneCtaSmem = 120 * 1024;  // > half an SM: one CTA per SM
+constexpr int kClassThreads[] = {32, 128, 256, 256, 512};
+constexpr bool kClassVsm[] = {true, true, true, false, false};  // whole basis in shared memory
 constexpr std::size_t kStageBudget = 200 * 1024;  // current vector + staged entries per CTA
 
 }  // namespace
@@ -799,24 +813,33 @@ void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, i
         const std::int32_t* list = t->class_tiles.get() + b0;
         const int mc = m <= 4 ? 4 : 8;
         const std::size_t vone = static_cast<std::size_t>(dmax) * C * sizeof(double);
-        const bool vsm = kClassVsm[c] && vone * std::min(m, mc) <= 160 * 1024;  // else: per-SM slots
+        const bool vsm = kClassVsm[c] && vone * std::min(m, mc) <= 160 * 1024;  // else: scratch slots in L2
         const std::size_t vbytes = vone * (vsm ? std::min(m, mc) : 1);
         // entry staging: up to the class's largest tile, within the smem budget
         const std::size_t room = vbytes < kStageBudget ? (kStageBudget - vbytes) / 10 : 0;
         const int stage_cap = static_cast<int>(std::min<std::size_t>(room, static_cast<std::size_t>(t->class_max_ent[static_cast<std::size_t>(c)]))) & ~7;
         std::size_t sm = vbytes + static_cast<std::size_t>(stage_cap) * 10;
         const unsigned grid = static_cast<unsigned>((b1 - b0) * ngroups);
-        if (!vsm) {  // per-SM basis slots: one CTA per SM
-            sm = std::max(sm, kOneCtaSmem);
-            const index_t vneed = static_cast<index_t>(mc) * t->ctx->num_sms * dmax * C;
+        int kslots = 1;
+        auto slots_for = [&](const void* kern, int nt) {  // resident CTAs per SM = scratch slots per SM
+            int per = 0;
+            BE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, nt, sm));
+            kslots = std::max(1, std::min(per, 32));
+            const index_t vneed = static_cast<index_t>(mc) * t->ctx->num_sms * kslots * dmax * C;
             if (t->vscratch.n < vneed) t->vscratch.reset(vneed);
-        }
+            if (t->slot_mask.n < t->ctx->num_sms) {
+                t->slot_mask.reset(t->ctx->num_sms);
+                BE_CUDA(cudaMemsetAsync(t->slot_mask.get(), 0, t->slot_mask.bytes(), s));
+            }
+        };
 #define BE_FOMB(MC, NTT, RPT, VS)                                                                                  \
     do {                                                                                                           \
         ensure_dyn_smem(k_fom_blk<MC, NTT, RPT, VS>, sm);                                                          \
+        if (!(VS)) slots_for(reinterpret_cast<const void*>(k_fom_blk<MC, NTT, RPT, VS>), NTT);                    \
         k_fom_blk<MC, NTT, RPT, VS><<<grid, NTT, sm, s>>>(tdv, list, t->rowptr.get(), t->cols.get(), t->vals.get(), \
                                                            shifts, R, W, nb, m, ngroups, fallbacks, dmax,          \
-                                                           stage_cap, t->vscratch.get(), t->n);                    \
+                                                           stage_cap, t->vscratch.get(), t->n, t->slot_mask.get(), \
+                                                           kslots);                                                \
     } while (0)
 #define BE_FOMB2(NTT, RPT)                      \
     if (mc == 4) {                              \
@@ -830,7 +853,7 @@ void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, i
             case 0: BE_FOMB2(32, 4); break;    // 8 rows per pass x 4
             case 1: BE_FOMB2(128, 2); break;   // 32 x 2
             case 2: BE_FOMB2(256, 2); break;   // 64 x 2
-            case 3: BE_FOMB2(512, 2); break;   // 128 x 2
+            case 3: BE_FOMB2(256, 4); break;   // 64 x 4 (two CTAs per SM)
             default: BE_FOMB2(512, 4); break;  // 128 x 4
         }
 #undef BE_FOMB2

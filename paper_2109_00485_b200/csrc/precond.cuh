@@ -35,6 +35,7 @@ struct Tiles {
     DBuf<std::uint16_t> cols;
     DBuf<double> vals;
     DBuf<double> vscratch;  // older Krylov vectors of the block kernel (L2-resident per CTA)
+    DBuf<unsigned> slot_mask;  // per SM: which scratch slots resident CTAs hold
 };
 
 // extract_tiles + upload; [row_lo, row_hi) restricts the result to the tiles
