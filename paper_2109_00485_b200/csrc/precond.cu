@@ -363,21 +363,18 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
     const double* vl = staged ? s_vl : gvl;
     const std::uint16_t* cl = staged ? s_cl : gcl;
 
-    int eb[RPT], ee[RPT];
-    double dg[RPT];
-    double w[RPT][kCW], vp[RPT][kCW];
+    int eb[RPT], ee[RPT];  // row i's entries [eb, ee), its diagonal at ee
+    double w[RPT][kCW];  // V_s and V_{s-1} are re-read (shared memory / the CTA's slot), not held
     double acc[kCW] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
         const int i = rl + k * RL;
         eb[k] = ee[k] = 0;
-        dg[k] = 0.0;
 #pragma unroll
-        for (int j = 0; j < kCW; ++j) w[k][j] = vp[k][j] = 0.0;
+        for (int j = 0; j < kCW; ++j) w[k][j] = 0.0;
         if (i < d) {
             eb[k] = __ldg(rp + i);
             ee[k] = __ldg(rp + i + 1) - 1;  // the diagonal slot is last
-            dg[k] = __ldg(gvl + ee[k]);
 #pragma unroll
             for (int j = 0; j < kCW; ++j) {
                 const double x = colok[j] ? r[static_cast<std::int64_t>(i) * nb + j] : 0.0;
@@ -427,13 +424,10 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
         // w = (K - sigma I) V_s ; alpha_s = V_s . w
 #pragma unroll
         for (int j = 0; j < kCW; ++j) acc[j] = 0.0;
-        double vs[RPT][kCW];
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
             const int i = rl + k * RL;
             double y[kCW] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-            for (int j = 0; j < kCW; ++j) vs[k][j] = 0.0;
             if (i < d) {
                 int e = eb[k];
                 for (; e + 1 < ee[k]; e += 2) {
@@ -452,10 +446,10 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
                     for (int j = 0; j < kCW; ++j) y[j] += a0 * x0.a[j];
                 }
                 const V4 v = ld4(Vc + static_cast<std::size_t>(i) * C);
+                const double dg = vl[ee[k]];
 #pragma unroll
                 for (int j = 0; j < kCW; ++j) {
-                    vs[k][j] = v.a[j];
-                    y[j] += (dg[k] - sigma[j]) * v.a[j];
+                    y[j] += (dg - sigma[j]) * v.a[j];
                     acc[j] += v.a[j] * y[j];
                 }
             }
@@ -471,36 +465,40 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
         }
         if (s + 1 == cap) break;
 #pragma unroll
-        for (int k = 0; k < RPT; ++k)
+        for (int k = 0; k < RPT; ++k) {
+            const int i = rl + k * RL;
+            if (i >= d) continue;
+            const V4 vs = ld4(Vc + static_cast<std::size_t>(i) * C);
+            const V4 vp = s > 0 ? ld4(vg(s - 1, i)) : V4{{0.0, 0.0, 0.0, 0.0}};
 #pragma unroll
             for (int j = 0; j < kCW; ++j) {
-                double x = w[k][j] - a[j] * vs[k][j];
-                if (s > 0) x -= bprev[j] * vp[k][j];
+                double x = w[k][j] - a[j] * vs.a[j];
+                if (s > 0) x -= bprev[j] * vp.a[j];
                 w[k][j] = x;
             }
+        }
         for (int q = 0; q <= s; ++q) {  // one reorthogonalisation pass, in order
 #pragma unroll
             for (int j = 0; j < kCW; ++j) acc[j] = 0.0;
-            double vq[RPT][kCW];
 #pragma unroll
             for (int k = 0; k < RPT; ++k) {
                 const int i = rl + k * RL;
-#pragma unroll
-                for (int j = 0; j < kCW; ++j) vq[k][j] = 0.0;
                 if (i < d) {
-                    const V4 v = q == s ? V4{{vs[k][0], vs[k][1], vs[k][2], vs[k][3]}} : ld4(vg(q, i));
+                    const V4 v = ld4(q == s ? Vc + static_cast<std::size_t>(i) * C : vg(q, i));
 #pragma unroll
-                    for (int j = 0; j < kCW; ++j) {
-                        vq[k][j] = v.a[j];
-                        acc[j] += v.a[j] * w[k][j];
-                    }
+                    for (int j = 0; j < kCW; ++j) acc[j] += v.a[j] * w[k][j];
                 }
             }
             block_colsum4<C, NT>(acc, red, rbuf);
 #pragma unroll
-            for (int k = 0; k < RPT; ++k)
+            for (int k = 0; k < RPT; ++k) {  // V_q re-read (shared memory or this CTA's L1/L2 slot)
+                const int i = rl + k * RL;
+                if (i < d) {
+                    const V4 v = ld4(q == s ? Vc + static_cast<std::size_t>(i) * C : vg(q, i));
 #pragma unroll
-                for (int j = 0; j < kCW; ++j) w[k][j] -= acc[j] * vq[k][j];
+                    for (int j = 0; j < kCW; ++j) w[k][j] -= acc[j] * v.a[j];
+                }
+            }
         }
 #pragma unroll
         for (int j = 0; j < kCW; ++j) acc[j] = 0.0;
@@ -527,8 +525,6 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
             const int i = rl + k * RL;
-#pragma unroll
-            for (int j = 0; j < kCW; ++j) vp[k][j] = vs[k][j];
             if (i < d) {
                 double v[kCW];
 #pragma unroll
@@ -647,7 +643,11 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
 // size classes of the block kernel: tiles up to kClassDims[c] rows run on
 // CTAs of kClassThreads[c] threads (4 per row, 16 columns per CTA)
 constexpr int kClassDims[] = {32, 64, 128, 256, 512};
-constexpr int kClassThreads[] = {32, 128, 256, 256, 512};
+#ifndef BE_FOM_C4_NT
+#define BE_FOM_C4_NT 512
+#define BE_FOM_C4_RPT 4
+#endif
+constexpr int kClassThreads[] = {32, 128, 256, 256, BE_FOM_C4_NT};
 constexpr bool kClassVsm[] = {true, true, true, false, false};  // whole basis in shared memory
 constexpr std::size_t kStageBudget = 200 * 1024;  // current vector + staged entries per CTA
 
@@ -854,7 +854,7 @@ void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, i
             case 1: BE_FOMB2(128, 2); break;   // 32 x 2
             case 2: BE_FOMB2(256, 2); break;   // 64 x 2
             case 3: BE_FOMB2(256, 4); break;   // 64 x 4 (two CTAs per SM)
-            default: BE_FOMB2(512, 4); break;  // 128 x 4
+            default: BE_FOMB2(BE_FOM_C4_NT, BE_FOM_C4_RPT); break;  // 128 x 4
         }
 #undef BE_FOMB2
 #undef BE_FOMB
