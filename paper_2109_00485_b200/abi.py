@@ -15,7 +15,7 @@ import numpy as np
 import os as _os
 
 # BE_LIB: an alternative build of the same library (kernel-variant experiments)
-LIB_PATH = Path(_os.environ.get("BE_LIB", str(Path(__file__).resolve().parent / "libblockeig_b200.so")))
+LIB_PATH = Path(_os.environ.get("BE_LIB") or str(Path(__file__).resolve().parent / "libblockeig_b200.so"))
 
 BE_F32, BE_F64 = 0, 1
 BE_APPLY_SYMMETRIC, BE_APPLY_NOTRANS_ACC, BE_APPLY_TRANS_ACC = 0, 1, 2

@@ -181,14 +181,16 @@ __device__ __forceinline__ void stage_x(unsigned char* xs, const TX* __restrict_
                         const int r = c / CPR, v0 = (c % CPR) * EPC;
                         TC* line = reinterpret_cast<TC*>(xs + r * G::LINEB);
                         if constexpr (sizeof(TC) == sizeof(TX)) {  // 16-byte stores (one wavefront per 8 lanes)
+                            // replica order rotated by row: neighbouring rows of a phase hit different banks
 #pragma unroll
-                            for (int q = 0; q < G::REP; ++q) *reinterpret_cast<uint4*>(line + q * NBP + v0) = buf[i];
+                            for (int q = 0; q < G::REP; ++q)
+                                *reinterpret_cast<uint4*>(line + ((q + r) % G::REP) * NBP + v0) = buf[i];
                         } else {
                             const TX* e = reinterpret_cast<const TX*>(&buf[i]);
 #pragma unroll
                             for (int q = 0; q < G::REP; ++q)
 #pragma unroll
-                                for (int j = 0; j < EPC; ++j) line[q * NBP + v0 + j] = static_cast<TC>(e[j]);
+                                for (int j = 0; j < EPC; ++j) line[((q + r) % G::REP) * NBP + v0 + j] = static_cast<TC>(e[j]);
                         }
                     }
                 }
@@ -327,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(TC) == 4 ? (NBP <= 16 ? BE_SP
     V* yi = reinterpret_cast<V*>(xj + kTile * G::LINEB);  // kTile x CH chunks: the run's Y_I rows
     unsigned char* stg0 = reinterpret_cast<unsigned char*>(yi + kTile * G::CH);
     const std::size_t sbytes = (S::bytes(max_nnz) + 15) & ~static_cast<std::size_t>(15);
-    __shared__ std::uint16_t s_jd[2][129];
+    __shared__ __align__(8) std::uint16_t s_jd[2][136];  // read 4 starts at a time
     __shared__ int s_run;
     __shared__ int s_tot[8];
 
@@ -397,19 +399,36 @@ __global__ void __launch_bounds__(kThreads, sizeof(TC) == 4 ? (NBP <= 16 ? BE_SP
 #pragma unroll
                 for (int i = 0; i < G::CH; ++i) vzero(acc[i]);
                 int first = 0;
+#ifndef BE_SPMM_UNR
+#define BE_SPMM_UNR 4
+#endif
                 if (active)
-                    for (int j = 0; j < len; ++j) {
-                        int pos = jd[j] + rank;
-                        if (grp == 1) pos = scp[pos];
-                        const TC v = static_cast<TC>(sv[pos]);
-                        const std::uint32_t x = src[pos];
-                        if (j == 0) first = x;
-                        const unsigned char* p = xbase + (grp == 0 ? (x & 255u) : (x >> 8)) * G::LINEB;
-                        V xv[G::CH];
+                    for (int j0 = 0; j0 < len; j0 += BE_SPMM_UNR) {
+                        int st4[4];  // starts j0 .. j0 + BE_SPMM_UNR - 1 in one shared-memory read
+                        if constexpr (BE_SPMM_UNR == 4) {
+                            const uint2 q4 = *reinterpret_cast<const uint2*>(jd + j0);
+                            st4[0] = q4.x & 0xffffu, st4[1] = q4.x >> 16, st4[2] = q4.y & 0xffffu, st4[3] = q4.y >> 16;
+                        } else if constexpr (BE_SPMM_UNR == 2) {
+                            const unsigned q2 = *reinterpret_cast<const unsigned*>(jd + j0);
+                            st4[0] = q2 & 0xffffu, st4[1] = q2 >> 16;
+                        } else {
+                            st4[0] = jd[j0];
+                        }
 #pragma unroll
-                        for (int i = 0; i < G::CH; ++i) xv[i] = *reinterpret_cast<const V*>(p + coff[i]);
+                        for (int u = 0; u < BE_SPMM_UNR; ++u) {
+                            if (j0 + u >= len) break;
+                            int pos = st4[u] + rank;
+                            if (grp == 1) pos = scp[pos];
+                            const TC v = static_cast<TC>(sv[pos]);
+                            const std::uint32_t x = src[pos];
+                            if (j0 + u == 0) first = x;
+                            const unsigned char* p = xbase + (grp == 0 ? (x & 255u) : (x >> 8)) * G::LINEB;
+                            V xv[G::CH];
 #pragma unroll
-                        for (int i = 0; i < G::CH; ++i) vfma(acc[i], v, xv[i]);
+                            for (int i = 0; i < G::CH; ++i) xv[i] = *reinterpret_cast<const V*>(p + coff[i]);
+#pragma unroll
+                            for (int i = 0; i < G::CH; ++i) vfma(acc[i], v, xv[i]);
+                        }
                     }
                 if (active) {
                     if (grp == 0) {  // Y_I += A X_J for this row
