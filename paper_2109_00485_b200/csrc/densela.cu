@@ -579,6 +579,208 @@ __global__ void __launch_bounds__(kT) k_mix(MixDev m, MixSrc ms, const int* __re
     }
 }
 
+// Pipelined mix (nb even, nb / 2 divides the block): the CTA walks a
+// contiguous range of kMixPRows-row chunks; the distinct source rows of
+// chunk c + 1 are in flight (cp.async into the other stage, row stride nb + 2
+// doubles: 16-byte aligned and conflict-free column reads) while chunk c is
+// formed. Thread = (row, 4-column block) as in k_mix.
+#ifndef BE_MIXP_ROWS
+#define BE_MIXP_ROWS 64
+#endif
+#ifndef BE_MIXP_CTAS
+#define BE_MIXP_CTAS 2
+#endif
+constexpr int kMixPRows = BE_MIXP_ROWS;
+__global__ void __launch_bounds__(kT, BE_MIXP_CTAS) k_mix_p(MixDev m, MixSrc ms, std::int64_t n) {
+    extern __shared__ __align__(16) double sh[];
+    const int nb = m.nb, nblk = (nb + 3) / 4, nbp = nblk * 4, ld = nb + 2;
+    const int ps = kMixPRows * ld, ss = ms.nsrc * ps;
+    double* ct = sh;  // ncoef x nb x nbp (transposed coefficients)
+    double* stg = sh + ((m.ncoef * nb * nbp + 1) & ~1);
+    const std::int64_t nch_all = (n + kMixPRows - 1) / kMixPRows;
+    const std::int64_t c0 = nch_all * blockIdx.x / gridDim.x, c1 = nch_all * (blockIdx.x + 1) / gridDim.x;
+    const int nch = static_cast<int>(c1 - c0);
+    auto issue = [&](int c) {
+        if (c < nch) {
+            const std::int64_t r0 = (c0 + c) * kMixPRows;
+            const int rows = static_cast<int>(min(static_cast<std::int64_t>(kMixPRows), n - r0));
+            fill_stage(stg + (c & 1) * ss, ms.src, ms.nsrc, ps, ld, nb, r0, rows);
+        }
+        cp_commit();
+    };
+    issue(0);
+    for (int c = 0; c < m.ncoef; ++c)
+        for (int e = threadIdx.x; e < nb * nbp; e += kT) {
+            const int i = e / nbp, j = e % nbp;
+            ct[c * nb * nbp + e] = j < nb ? m.coef[c][j * m.ld[c] + i] : 0.0;
+        }
+    const int rpi = kT / nblk;  // rows computed per pass
+    for (int c = 0; c < nch; ++c) {
+        issue(c + 1);
+        cp_wait<1>();
+        __syncthreads();  // chunk c staged (and the coefficients, first time)
+        const double* xs = stg + (c & 1) * ss;
+        const std::int64_t r0 = (c0 + c) * kMixPRows;
+        const int rows = static_cast<int>(min(static_cast<std::int64_t>(kMixPRows), n - r0));
+        if (threadIdx.x < rpi * nblk)
+            for (int rl = threadIdx.x / nblk; rl < rows; rl += rpi) {
+                const std::int64_t r = r0 + rl;
+                const int j0 = (threadIdx.x % nblk) * 4;
+                double res[4][4];
+                for (int o = 0; o < m.nout; ++o) {
+                    const auto& O = m.out[o];
+                    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+                    if (O.accumulate) {
+                        const double* yo = xs + O.acc_si * ps + rl * ld + j0;
+                        a0 = j0 < nb ? yo[0] : 0.0;
+                        a1 = j0 + 1 < nb ? yo[1] : 0.0;
+                        a2 = j0 + 2 < nb ? yo[2] : 0.0;
+                        a3 = j0 + 3 < nb ? yo[3] : 0.0;
+                    }
+                    for (int tt = 0; tt < O.nterms; ++tt) {
+                        const double* x = xs + O.si[tt] * ps + rl * ld;
+                        const double* C = ct + O.ci[tt] * nb * nbp + j0;
+                        double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+                        for (int i = 0; i < nb; ++i) {
+                            const double xi = x[i];
+                            const double2 c01 = *reinterpret_cast<const double2*>(C + i * nbp);
+                            const double2 c23 = *reinterpret_cast<const double2*>(C + i * nbp + 2);
+                            s0 += xi * c01.x;
+                            s1 += xi * c01.y;
+                            s2 += xi * c23.x;
+                            s3 += xi * c23.y;
+                        }
+                        const double sg = O.sign[tt];
+                        a0 += sg * s0;
+                        a1 += sg * s1;
+                        a2 += sg * s2;
+                        a3 += sg * s3;
+                    }
+                    if (O.add_from >= 0) {
+                        a0 += res[O.add_from][0];
+                        a1 += res[O.add_from][1];
+                        a2 += res[O.add_from][2];
+                        a3 += res[O.add_from][3];
+                    }
+                    if (O.add_si >= 0) {
+                        const double* x = xs + O.add_si * ps + rl * ld + j0;
+                        a0 += x[0];
+                        if (j0 + 1 < nb) a1 += x[1];
+                        if (j0 + 2 < nb) a2 += x[2];
+                        if (j0 + 3 < nb) a3 += x[3];
+                    }
+                    res[o][0] = a0;
+                    res[o][1] = a1;
+                    res[o][2] = a2;
+                    res[o][3] = a3;
+                    double* y = O.y + r * nb;
+                    if (j0 + 3 < nb) {
+                        reinterpret_cast<double2*>(y + j0)[0] = make_double2(a0, a1);
+                        reinterpret_cast<double2*>(y + j0)[1] = make_double2(a2, a3);
+                    } else {
+                        if (j0 < nb) y[j0] = a0;
+                        if (j0 + 1 < nb) y[j0 + 1] = a1;
+                    }
+                }
+            }
+        __syncthreads();  // stage c & 1 is refilled by the next iteration's issue
+    }
+    cp_wait<0>();
+}
+
+// Tensor-core mix (nb = 8 * NBB, every output a sum of <= 4 terms): the
+// chunk pipeline of k_mix_p, then warp w forms rows 8w .. 8w + 7 of every
+// output with DMMA (m8n8k4 f64). The coefficient blocks are the B fragments,
+// loaded once per CTA into registers (sign folded in); per k-step a lane
+// loads one A element (row stride nb + 4 doubles: conflict-free). The
+// accumulate / add_src terms are added in the accumulator layout.
+struct MixT {
+    int nq;           // term slots, output-major
+    int qo[4], qs[4]; // output, staged source of each slot
+    int last[4];      // slot ends its output
+};
+template <int NBB>
+__global__ void __launch_bounds__(kT, 2) k_mix_t(MixDev m, MixSrc ms, MixT mt, std::int64_t n) {
+    constexpr int NB = NBB * 8, KS = NB / 4, LD = NB + 4, MAXT = 4;
+    static_assert(kMixPRows == 8 * (kT / 32), "one 8-row block per warp");
+    extern __shared__ __align__(16) double sh[];
+    const int ps = kMixPRows * LD, ss = ms.nsrc * ps;
+    double* stg = sh;
+    const std::int64_t nch_all = (n + kMixPRows - 1) / kMixPRows;
+    const std::int64_t c0 = nch_all * blockIdx.x / gridDim.x, c1 = nch_all * (blockIdx.x + 1) / gridDim.x;
+    const int nch = static_cast<int>(c1 - c0);
+    auto issue = [&](int c) {
+        if (c < nch) {
+            const std::int64_t r0 = (c0 + c) * kMixPRows;
+            const int rows = static_cast<int>(min(static_cast<std::int64_t>(kMixPRows), n - r0));
+            fill_stage(stg + (c & 1) * ss, ms.src, ms.nsrc, ps, LD, NB, r0, rows);
+        }
+        cp_commit();
+    };
+    issue(0);
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, rl = (threadIdx.x >> 5) * 8 + g;
+    // B fragments: B[k = t][col = g] of each slot's coefficient block
+    double bf[MAXT][KS][NBB];
+#pragma unroll
+    for (int q = 0; q < MAXT; ++q) {
+        const int o = q < mt.nq ? mt.qo[q] : 0;
+        int tt = 0;
+        for (int p = 0; p < q; ++p) tt += mt.qo[p] == o;
+        const double* cf = q < mt.nq ? m.coef[m.out[o].ci[tt]] : nullptr;
+        const int ld = q < mt.nq ? m.ld[m.out[o].ci[tt]] : 0;
+        const double sg = q < mt.nq ? m.out[o].sign[tt] : 0.0;
+#pragma unroll
+        for (int k = 0; k < KS; ++k)
+#pragma unroll
+            for (int cb = 0; cb < NBB; ++cb) bf[q][k][cb] = cf ? sg * cf[(8 * cb + g) * ld + 4 * k + t] : 0.0;
+    }
+    for (int c = 0; c < nch; ++c) {
+        issue(c + 1);
+        cp_wait<1>();
+        __syncthreads();  // chunk c staged
+        const double* xs = stg + (c & 1) * ss;
+        const std::int64_t r0 = (c0 + c) * kMixPRows;
+        const int rows = static_cast<int>(min(static_cast<std::int64_t>(kMixPRows), n - r0));
+        double acc[NBB][2];
+#pragma unroll
+        for (int cb = 0; cb < NBB; ++cb) acc[cb][0] = acc[cb][1] = 0.0;
+#pragma unroll
+        for (int q = 0; q < MAXT; ++q) {
+            if (q >= mt.nq) break;
+            const double* xa = xs + mt.qs[q] * ps + rl * LD + t;
+#pragma unroll
+            for (int k = 0; k < KS; ++k) {
+                const double a = xa[4 * k];
+#pragma unroll
+                for (int cb = 0; cb < NBB; ++cb) dmma884(acc[cb][0], acc[cb][1], a, bf[q][k][cb]);
+            }
+            if (mt.last[q]) {  // output complete: old value / added panel, store, reset
+                const auto& O = m.out[mt.qo[q]];
+#pragma unroll
+                for (int cb = 0; cb < NBB; ++cb) {
+                    const int col = 8 * cb + 2 * t;
+                    double v0 = acc[cb][0], v1 = acc[cb][1];
+                    if (O.accumulate) {
+                        const double2 yo = *reinterpret_cast<const double2*>(xs + O.acc_si * ps + rl * LD + col);
+                        v0 = yo.x + v0;
+                        v1 = yo.y + v1;
+                    }
+                    if (O.add_si >= 0) {
+                        const double2 ad = *reinterpret_cast<const double2*>(xs + O.add_si * ps + rl * LD + col);
+                        v0 += ad.x;
+                        v1 += ad.y;
+                    }
+                    if (rl < rows)
+                        *reinterpret_cast<double2*>(O.y + (r0 + rl) * NB + col) = make_double2(v0, v1);
+                    acc[cb][0] = acc[cb][1] = 0.0;
+                }
+            }
+        }
+        __syncthreads();  // stage c & 1 is refilled by the next iteration's issue
+    }
+    cp_wait<0>();
+}
+
 // ---- streamed trsm (nb % 2 == 0, nb <= NBP): W <- W R^-1 for one or two
 // panels; chunk rows arrive by bulk copy, thread = (panel, row) substitutes
 // in registers (rows read / written in a lane-rotated 16-byte order), the
@@ -1106,6 +1308,48 @@ void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
         m.out[o].acc_si = job.out[o].accumulate ? sidx(job.out[o].y) : -1;
     }
     const int nblk = (job.nb + 3) / 4;
+    {  // tensor-core path: nb in {8, 16}, <= 4 term slots, no add_from, every output has a term
+        MixT mt{};
+        bool ok = (job.nb == 8 || job.nb == 16);
+        for (int o = 0; o < m.nout && ok; ++o) {
+            if (m.out[o].add_from >= 0 || m.out[o].nterms < 1 || mt.nq + m.out[o].nterms > 4) {
+                ok = false;
+                break;
+            }
+            for (int t = 0; t < m.out[o].nterms; ++t) {
+                mt.qo[mt.nq] = o;
+                mt.qs[mt.nq] = m.out[o].si[t];
+                mt.last[mt.nq] = t + 1 == m.out[o].nterms;
+                ++mt.nq;
+            }
+        }
+        const std::size_t smt = 2 * static_cast<std::size_t>(ms.nsrc) * kMixPRows * (job.nb + 4) * sizeof(double);
+        if (ok && smt <= 200 * 1024) {
+            const int grid = static_cast<int>(
+                std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 2, (n + kMixPRows - 1) / kMixPRows)));
+            if (job.nb == 8) {
+                ensure_dyn_smem(k_mix_t<1>, smt);
+                k_mix_t<1><<<grid, kT, smt, s>>>(m, ms, mt, n);
+            } else {
+                ensure_dyn_smem(k_mix_t<2>, smt);
+                k_mix_t<2><<<grid, kT, smt, s>>>(m, ms, mt, n);
+            }
+            BE_CUDA(cudaGetLastError());
+            ++ctx->launches;
+            return;
+        }
+    }
+    const std::size_t smp = (((static_cast<std::size_t>(m.ncoef) * job.nb * nblk * 4 + 1) & ~std::size_t{1}) +
+                             2 * static_cast<std::size_t>(ms.nsrc) * kMixPRows * (job.nb + 2)) * sizeof(double);
+    if (job.nb % 2 == 0 && kT % (job.nb / 2) == 0 && smp <= 220 * 1024 / BE_MIXP_CTAS) {  // pipelined
+        ensure_dyn_smem(k_mix_p, smp);
+        const int grid = static_cast<int>(std::max<std::int64_t>(
+            1, std::min<std::int64_t>(ctx->num_sms * BE_MIXP_CTAS, (n + kMixPRows - 1) / kMixPRows)));
+        k_mix_p<<<grid, kT, smp, s>>>(m, ms, n);
+        BE_CUDA(cudaGetLastError());
+        ++ctx->launches;
+        return;
+    }
     const std::size_t sm = (static_cast<std::size_t>(m.ncoef) * job.nb * nblk * 4 +
                             static_cast<std::size_t>(ms.nsrc) * kMixRows * (job.nb + 1)) * sizeof(double);
     ensure_dyn_smem(k_mix, sm);

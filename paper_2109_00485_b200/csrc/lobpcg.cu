@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -41,7 +43,7 @@ std::vector<double> random_block(index_t n, index_t nb, std::uint64_t seed, inde
 }
 
 struct Events {
-    cudaEvent_t e[6] = {};
+    cudaEvent_t e[9] = {};
     Events() {
         for (auto& x : e) BE_CUDA(cudaEventCreate(&x));
     }
@@ -250,6 +252,7 @@ struct Solver {
     }
 
     std::vector<double> th;
+    const bool trace_segments = std::getenv("BE_TRACE_SEGMENTS") != nullptr;
     bool p_active = false, converged = false;
     int iter = 0;
     Events ev;
@@ -324,6 +327,7 @@ struct Solver {
                 ++res.restarts;
                 if (!rayleigh_ritz(false)) fail(BE_ERR_BREAKDOWN_UNRECOVERABLE, "lobpcg_solve: basis repair failed twice");
             }
+            BE_CUDA(cudaEventRecord(ev.e[5], s));
             const bool with_p = p_active && !dropped;
             const int dim = (with_p ? 3 : 2) * nb;
             {  // update_blocks (lobpcg.hpp:168-194): P+ = W C2 + P C3, X+ = X C1 + P+ (and the H-images),
@@ -348,6 +352,7 @@ struct Solver {
                 std::swap(P, Pn);
                 std::swap(HP, HPn);
             }
+            BE_CUDA(cudaEventRecord(ev.e[6], s));
             th.assign(hm->theta, hm->theta + nb);
             p_active = true;
             {  // P hygiene (lobpcg.hpp:412-417) + orthonormalize_pair (:254-270)
@@ -362,6 +367,7 @@ struct Solver {
                 dla::chol_floored(ctx, Bp, Rp, nb, 1e-8, st.get(), s);
                 dla::trsm(ctx, P.get(), HP.get(), Rp, nb, n, st.get(), 0, 1, s);
             }
+            BE_CUDA(cudaEventRecord(ev.e[7], s));
             dla::residual(ctx, HX.get(), X.get(), theta, R.get(), nb, n, partials.get(), rn2, xn2, s);
             allreduce(rn2, 2 * nb);
             BE_CUDA(cudaMemcpyAsync(hm->rn2, rn2, nb * 8, cudaMemcpyDeviceToHost, s));
@@ -391,6 +397,12 @@ struct Solver {
             rec.t_spmm = ev.ms(2, 3) * 1e-3;
             rec.t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
             rec.t_dense = std::max(0.0, rec.t_total - rec.t_spmm - rec.t_precond);
+            if (trace_segments)  // BE_TRACE_SEGMENTS=1: device time of each phase of the iteration
+                std::fprintf(stderr,
+                             "[be] iter %d ms: precond %.3f w-hygiene %.3f spmm %.3f rayleigh-ritz %.3f update %.3f "
+                             "p-hygiene %.3f residual %.3f wall %.3f\n",
+                             iter, ev.ms(0, 1), ev.ms(1, 2), ev.ms(2, 3), ev.ms(3, 5), ev.ms(5, 6), ev.ms(6, 7),
+                             ev.ms(7, 4), rec.t_total * 1e3);
             res.records.push_back(rec);
             if (observer) {
                 const double* xh = nullptr;
