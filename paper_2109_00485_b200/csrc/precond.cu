@@ -290,6 +290,165 @@ __device__ __forceinline__ void st4(double* p, const double (&v)[kCW]) {
     reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
 }
 
+// T y = beta0 e1 for one column's m x m Lanczos tridiagonal: LU with partial
+// pivoting and the singular-pivot flag (precond.hpp:208-249). UNR: every
+// index unrolled (T and y stay in registers, m <= 4); else rolled loops.
+template <int MC, bool UNR>
+__device__ __forceinline__ int tri_lu_solve(const double (*sa)[kFomCols], const double (*sb)[kFomCols], int cc, int st,
+                                            double b0, double (&y)[MC]) {
+    if constexpr (UNR) {
+        double T[MC][MC];
+        double tmax = 0.0;
+#pragma unroll
+        for (int i = 0; i < MC; ++i) {
+            y[i] = 0.0;
+#pragma unroll
+            for (int q = 0; q < MC; ++q) T[i][q] = 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < MC; ++i)
+            if (i < st) {
+                T[i][i] = sa[i][cc];
+                tmax = fmax(tmax, fabs(sa[i][cc]));
+                if (i + 1 < MC && i + 1 < st) {
+                    T[i][i + 1 < MC ? i + 1 : 0] = sb[i][cc];
+                    T[i + 1 < MC ? i + 1 : 0][i] = sb[i][cc];
+                    tmax = fmax(tmax, fabs(sb[i][cc]));
+                }
+            }
+        const double floor = 1e-14 * fmax(1.0, tmax);
+        y[0] = b0;
+        int sg = 0;
+        bool go = true;
+#pragma unroll
+        for (int k = 0; k < MC; ++k) {
+            if (!(go && k < st)) continue;
+            int piv = k;
+            double best = fabs(T[k][k]);
+#pragma unroll
+            for (int i = k + 1; i < MC; ++i)
+                if (i < st && fabs(T[i][k]) > best) {
+                    best = fabs(T[i][k]);
+                    piv = i;
+                }
+            if (best < floor) {
+                sg = 1;
+                go = false;
+                continue;
+            }
+#pragma unroll
+            for (int i = k + 1; i < MC; ++i)
+                if (i == piv) {
+#pragma unroll
+                    for (int q = 0; q < MC; ++q) {
+                        const double tmp = T[k][q];
+                        T[k][q] = T[i][q];
+                        T[i][q] = tmp;
+                    }
+                    const double tmp = y[k];
+                    y[k] = y[i];
+                    y[i] = tmp;
+                }
+#pragma unroll
+            for (int i = k + 1; i < MC; ++i) {
+                if (i >= st) continue;
+                const double f = T[i][k] / T[k][k];
+                if (f == 0.0) continue;
+#pragma unroll
+                for (int q = k; q < MC; ++q)
+                    if (q < st) T[i][q] -= f * T[k][q];
+                y[i] -= f * y[k];
+            }
+        }
+        if (!sg)
+#pragma unroll
+            for (int i = MC - 1; i >= 0; --i) {
+                if (i >= st) continue;
+                double a2 = y[i];
+#pragma unroll
+                for (int q = i + 1; q < MC; ++q)
+                    if (q < st) a2 -= T[i][q] * y[q];
+                y[i] = a2 / T[i][i];
+            }
+        return sg;
+    } else {
+        double T[MC][MC];
+        double tmax = 0.0;
+#pragma unroll 1
+        for (int i = 0; i < MC; ++i) {
+            y[i] = 0.0;
+#pragma unroll 1
+            for (int q = 0; q < MC; ++q) T[i][q] = 0.0;
+        }
+#pragma unroll 1
+        for (int i = 0; i < MC; ++i)
+            if (i < st) {
+                T[i][i] = sa[i][cc];
+                tmax = fmax(tmax, fabs(sa[i][cc]));
+                if (i + 1 < MC && i + 1 < st) {
+                    T[i][i + 1 < MC ? i + 1 : 0] = sb[i][cc];
+                    T[i + 1 < MC ? i + 1 : 0][i] = sb[i][cc];
+                    tmax = fmax(tmax, fabs(sb[i][cc]));
+                }
+            }
+        const double floor = 1e-14 * fmax(1.0, tmax);
+        y[0] = b0;
+        int sg = 0;
+        bool go = true;
+#pragma unroll 1
+        for (int k = 0; k < MC; ++k) {
+            if (!(go && k < st)) continue;
+            int piv = k;
+            double best = fabs(T[k][k]);
+#pragma unroll 1
+            for (int i = k + 1; i < MC; ++i)
+                if (i < st && fabs(T[i][k]) > best) {
+                    best = fabs(T[i][k]);
+                    piv = i;
+                }
+            if (best < floor) {
+                sg = 1;
+                go = false;
+                continue;
+            }
+#pragma unroll 1
+            for (int i = k + 1; i < MC; ++i)
+                if (i == piv) {
+#pragma unroll 1
+                    for (int q = 0; q < MC; ++q) {
+                        const double tmp = T[k][q];
+                        T[k][q] = T[i][q];
+                        T[i][q] = tmp;
+                    }
+                    const double tmp = y[k];
+                    y[k] = y[i];
+                    y[i] = tmp;
+                }
+#pragma unroll 1
+            for (int i = k + 1; i < MC; ++i) {
+                if (i >= st) continue;
+                const double f = T[i][k] / T[k][k];
+                if (f == 0.0) continue;
+#pragma unroll 1
+                for (int q = k; q < MC; ++q)
+                    if (q < st) T[i][q] -= f * T[k][q];
+                y[i] -= f * y[k];
+            }
+        }
+        if (!sg)
+#pragma unroll 1
+            for (int i = MC - 1; i >= 0; --i) {
+                if (i >= st) continue;
+                double a2 = y[i];
+#pragma unroll 1
+                for (int q = i + 1; q < MC; ++q)
+                    if (q < st) a2 -= T[i][q] * y[q];
+                y[i] = a2 / T[i][i];
+            }
+        return sg;
+    }
+}
+
 template <int MC, int NT, int RPT, bool VSM>
 __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
     k_fom_blk(const TileDev* __restrict__ tiles, const std::int32_t* __restrict__ list,
@@ -355,10 +514,26 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
     double* s_vl = sV + (VSM ? static_cast<std::size_t>(min(m, MC)) : 1) * vstride;
     std::uint16_t* s_cl = reinterpret_cast<std::uint16_t*>(s_vl + stage_cap);
     const bool staged = nent <= stage_cap;
-    if (staged)
-        for (int e = threadIdx.x; e < nent; e += NT) {
-            s_vl[e] = __ldg(gvl + e);
-            s_cl[e] = __ldg(gcl + e);
+    if (staged)  // eight loads in flight per thread before the stores
+        for (int e0 = threadIdx.x; e0 < nent; e0 += 8 * NT) {
+            double v[8];
+            std::uint16_t c[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * NT;
+                if (e < nent) {
+                    v[u] = __ldg(gvl + e);
+                    c[u] = __ldg(gcl + e);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * NT;
+                if (e < nent) {
+                    s_vl[e] = v[u];
+                    s_cl[e] = c[u];
+                }
+            }
         }
     const double* vl = staged ? s_vl : gvl;
     const std::uint16_t* cl = staged ? s_cl : gcl;
@@ -539,76 +714,30 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
         }
         if constexpr (VSM) Vc += vstride;
     }
-    // T y = beta0 e1 by LU with partial pivoting (precond.hpp:208-249), per
-    // column, by the first row lane of each column chunk; the solutions are
-    // broadcast through shared memory
+    // T y = beta0 e1 by LU with partial pivoting (precond.hpp:208-249), one
+    // thread per column (register-resident: every index is unrolled); the
+    // solutions are broadcast through shared memory
     __shared__ double s_y[C][MC];
+    __shared__ double s_b0[C];
     __shared__ int s_sing[C];
     if (rl == 0)
 #pragma unroll
-        for (int j = 0; j < kCW; ++j) s_steps[cq * kCW + j] = steps[j];
+        for (int j = 0; j < kCW; ++j) {
+            s_steps[cq * kCW + j] = steps[j];
+            s_b0[cq * kCW + j] = beta0[j];
+        }
     block_sync<NT>();
-    if (rl == 0)
-#pragma unroll
-    for (int j = 0; j < kCW; ++j) {
-        double y[MC];
-        int sg = 0;
-        const int cc = cq * kCW + j;
+    if (threadIdx.x < C) {
+        const int cc = threadIdx.x;
         const int st = s_steps[cc];
-        double T[MC][MC];
-        double tmax = 0.0;
-#pragma unroll
-        for (int i = 0; i < MC; ++i)
-#pragma unroll
-            for (int q = 0; q < MC; ++q) T[i][q] = 0.0;
-#pragma unroll
-        for (int i = 0; i < MC; ++i) {
-            y[i] = 0.0;
-            if (i < st) {
-                T[i][i] = s_alpha[i][cc];
-                tmax = fmax(tmax, fabs(s_alpha[i][cc]));
-                if (i + 1 < st) {
-                    T[i][i + 1 < MC ? i + 1 : 0] = s_beta[i][cc];
-                    T[i + 1 < MC ? i + 1 : 0][i] = s_beta[i][cc];
-                    tmax = fmax(tmax, fabs(s_beta[i][cc]));
-                }
-            }
-        }
-        const double floor = 1e-14 * fmax(1.0, tmax);
-        y[0] = beta0[j];
-        for (int k = 0; k < st; ++k) {
-            int piv = k;
-            for (int i = k + 1; i < st; ++i)
-                if (fabs(T[i][k]) > fabs(T[piv][k])) piv = i;
-            if (fabs(T[piv][k]) < floor) {
-                sg = 1;
-                break;
-            }
-            if (piv != k) {
-                for (int q = 0; q < MC; ++q) {
-                    const double tmp = T[k][q];
-                    T[k][q] = T[piv][q];
-                    T[piv][q] = tmp;
-                }
-                const double tmp = y[k];
-                y[k] = y[piv];
-                y[piv] = tmp;
-            }
-            for (int i = k + 1; i < st; ++i) {
-                const double f = T[i][k] / T[k][k];
-                if (f == 0.0) continue;
-                for (int q = k; q < st; ++q) T[i][q] -= f * T[k][q];
-                y[i] -= f * y[k];
-            }
-        }
-        if (!sg)
-            for (int i = st - 1; i >= 0; --i) {
-                double a2 = y[i];
-                for (int q = i + 1; q < st; ++q) a2 -= T[i][q] * y[q];
-                y[i] = a2 / T[i][i];
-            }
-        if (colok[j] && beta0[j] != 0.0 && sg && fallbacks)
+        const double b0 = s_b0[cc];
+        double y[MC];
+        int sg;
+        if constexpr (MC <= 4) sg = tri_lu_solve<MC, true>(s_alpha, s_beta, cc, st, b0, y);
+        else sg = tri_lu_solve<MC, false>(s_alpha, s_beta, cc, st, b0, y);
+        if (col0 + cc < nb && b0 != 0.0 && sg && fallbacks)
             atomicAdd(reinterpret_cast<unsigned long long*>(fallbacks), 1ull);
+#pragma unroll
         for (int q = 0; q < MC; ++q) s_y[cc][q] = y[q];
         s_sing[cc] = sg;
     }
@@ -619,7 +748,9 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
         const int i = rl + k * RL;
         if (i >= d) continue;
         double o[kCW] = {0.0, 0.0, 0.0, 0.0};
-        for (int q = 0; q < cap; ++q) {
+#pragma unroll
+        for (int q = 0; q < MC; ++q) {  // unrolled: the basis reads are in flight together
+            if (q >= cap) break;
             const V4 v = ld4(vg(q, i));
 #pragma unroll
             for (int j = 0; j < kCW; ++j)

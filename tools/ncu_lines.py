@@ -2,7 +2,7 @@
 import csv, subprocess, sys
 rep = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + sys.argv[3:],
                      capture_output=True, text=True).stdout.splitlines()
 r = csv.reader(out)
 next(r); next(r); h = next(r)
