@@ -281,13 +281,20 @@ __device__ __forceinline__ void block_sync() {
 struct V4 {
     double a[kCW];
 };
-__device__ __forceinline__ V4 ld4(const double* p) {  // 32-byte aligned shared-memory read
-    const double2 x = reinterpret_cast<const double2*>(p)[0], y = reinterpret_cast<const double2*>(p)[1];
-    return V4{{x.x, x.y, y.x, y.y}};
+// A row of the 16-column basis in shared memory is two 64-byte halves; the
+// 16-byte piece h of column chunk cq sits at h * 8 + cq * 2 doubles. Row lanes
+// of odd parity read (and write) their high piece first (hp = 8), so the two
+// rows of a quarter-warp phase always hit opposite bank halves: gathers of
+// arbitrary rows are conflict-free.
+static_assert(kFomCols == 16, "the piece layout of ld4 / st4 assumes 16-column rows");
+__device__ __forceinline__ V4 ld4(const double* p, int hp) {  // p: row + cq * 2
+    const double2 x = *reinterpret_cast<const double2*>(p + hp), y = *reinterpret_cast<const double2*>(p + (8 - hp));
+    return hp ? V4{{y.x, y.y, x.x, x.y}} : V4{{x.x, x.y, y.x, y.y}};
 }
-__device__ __forceinline__ void st4(double* p, const double (&v)[kCW]) {
-    reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
-    reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
+__device__ __forceinline__ void st4(double* p, const double (&v)[kCW], int hp) {
+    const double2 lo = make_double2(v[0], v[1]), hi = make_double2(v[2], v[3]);
+    *reinterpret_cast<double2*>(p + hp) = hp ? hi : lo;
+    *reinterpret_cast<double2*>(p + (8 - hp)) = hp ? lo : hi;
 }
 
 // T y = beta0 e1 for one column's m x m Lanczos tridiagonal: LU with partial
@@ -486,7 +493,8 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
     // at this thread's own rows only, live in a per-SM scratch slot that stays
     // in L2 (the launch guarantees one CTA per SM).
     const std::size_t vstride = static_cast<std::size_t>(dmax) * C;
-    double* Vcur = sV + cq * kCW;
+    double* Vcur = sV + cq * 2;  // this chunk's low piece (see ld4)
+    const int hp = NT == 32 ? 0 : (rl & 1) * 8;  // (the one-warp class is not shared-memory bound)
     double* Vslot = nullptr;
     __shared__ int s_slot;
     unsigned smid = 0;
@@ -502,7 +510,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
             s_slot = static_cast<int>(smid) * kslots + k;
         }
         __syncthreads();
-        Vslot = Vg + static_cast<std::size_t>(s_slot) * MC * vstride + cq * kCW;
+        Vslot = Vg + static_cast<std::size_t>(s_slot) * MC * vstride + cq * 2;
     }
     auto vg = [&](int q, int i) -> double* {
         if constexpr (VSM) return Vcur + q * vstride + static_cast<std::size_t>(i) * C;
@@ -572,8 +580,8 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
             double v[kCW];
 #pragma unroll
             for (int j = 0; j < kCW; ++j) v[j] = w[k][j] / inv[j];
-            st4(Vc + static_cast<std::size_t>(i) * C, v);
-            if constexpr (!VSM) st4(vg(0, i), v);
+            st4(Vc + static_cast<std::size_t>(i) * C, v, hp);
+            if constexpr (!VSM) st4(vg(0, i), v, hp);
         }
     }
     // Lanczos scalars of the CTA's columns (written by row lane 0; every
@@ -607,8 +615,8 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
                 int e = eb[k];
                 for (; e + 1 < ee[k]; e += 2) {
                     const double a0 = vl[e], a1 = vl[e + 1];
-                    const V4 x0 = ld4(Vc + static_cast<int>(cl[e]) * C);
-                    const V4 x1 = ld4(Vc + static_cast<int>(cl[e + 1]) * C);
+                    const V4 x0 = ld4(Vc + static_cast<int>(cl[e]) * C, hp);
+                    const V4 x1 = ld4(Vc + static_cast<int>(cl[e + 1]) * C, hp);
 #pragma unroll
                     for (int j = 0; j < kCW; ++j) y[j] += a0 * x0.a[j];
 #pragma unroll
@@ -616,11 +624,11 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
                 }
                 if (e < ee[k]) {
                     const double a0 = vl[e];
-                    const V4 x0 = ld4(Vc + static_cast<int>(cl[e]) * C);
+                    const V4 x0 = ld4(Vc + static_cast<int>(cl[e]) * C, hp);
 #pragma unroll
                     for (int j = 0; j < kCW; ++j) y[j] += a0 * x0.a[j];
                 }
-                const V4 v = ld4(Vc + static_cast<std::size_t>(i) * C);
+                const V4 v = ld4(Vc + static_cast<std::size_t>(i) * C, hp);
                 const double dg = vl[ee[k]];
 #pragma unroll
                 for (int j = 0; j < kCW; ++j) {
@@ -643,8 +651,8 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
         for (int k = 0; k < RPT; ++k) {
             const int i = rl + k * RL;
             if (i >= d) continue;
-            const V4 vs = ld4(Vc + static_cast<std::size_t>(i) * C);
-            const V4 vp = s > 0 ? ld4(vg(s - 1, i)) : V4{{0.0, 0.0, 0.0, 0.0}};
+            const V4 vs = ld4(Vc + static_cast<std::size_t>(i) * C, hp);
+            const V4 vp = s > 0 ? ld4(vg(s - 1, i), hp) : V4{{0.0, 0.0, 0.0, 0.0}};
 #pragma unroll
             for (int j = 0; j < kCW; ++j) {
                 double x = w[k][j] - a[j] * vs.a[j];
@@ -659,7 +667,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
             for (int k = 0; k < RPT; ++k) {
                 const int i = rl + k * RL;
                 if (i < d) {
-                    const V4 v = ld4(q == s ? Vc + static_cast<std::size_t>(i) * C : vg(q, i));
+                    const V4 v = ld4(q == s ? Vc + static_cast<std::size_t>(i) * C : vg(q, i), hp);
 #pragma unroll
                     for (int j = 0; j < kCW; ++j) acc[j] += v.a[j] * w[k][j];
                 }
@@ -669,7 +677,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
             for (int k = 0; k < RPT; ++k) {  // V_q re-read (shared memory or this CTA's L1/L2 slot)
                 const int i = rl + k * RL;
                 if (i < d) {
-                    const V4 v = ld4(q == s ? Vc + static_cast<std::size_t>(i) * C : vg(q, i));
+                    const V4 v = ld4(q == s ? Vc + static_cast<std::size_t>(i) * C : vg(q, i), hp);
 #pragma unroll
                     for (int j = 0; j < kCW; ++j) w[k][j] -= acc[j] * v.a[j];
                 }
@@ -705,10 +713,10 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
 #pragma unroll
                 for (int j = 0; j < kCW; ++j) v[j] = w[k][j] / inv[j];
                 if constexpr (VSM) {
-                    st4(vg(s + 1, i), v);
+                    st4(vg(s + 1, i), v, hp);
                 } else {
-                    st4(Vc + static_cast<std::size_t>(i) * C, v);
-                    st4(vg(s + 1, i), v);
+                    st4(Vc + static_cast<std::size_t>(i) * C, v, hp);
+                    st4(vg(s + 1, i), v, hp);
                 }
             }
         }
@@ -751,7 +759,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
 #pragma unroll
         for (int q = 0; q < MC; ++q) {  // unrolled: the basis reads are in flight together
             if (q >= cap) break;
-            const V4 v = ld4(vg(q, i));
+            const V4 v = ld4(vg(q, i), hp);
 #pragma unroll
             for (int j = 0; j < kCW; ++j)
                 if (q < s_steps[cq * kCW + j]) o[j] += s_y[cq * kCW + j][q] * v.a[j];
