@@ -297,6 +297,14 @@ __device__ __forceinline__ void st4(double* p, const double (&v)[kCW], int hp) {
     *reinterpret_cast<double2*>(p + (8 - hp)) = hp ? lo : hi;
 }
 
+// x / b, correctly rounded, from r = 1 / b (one reciprocal per column
+// instead of one IEEE division per element): q = x r, then one residual
+// correction with the exact FMA remainder (Markstein).
+__device__ __forceinline__ double div_rcp(double x, double b, double r) {
+    const double q = x * r;
+    return fma(fma(-q, b, x), r, q);
+}
+
 // T y = beta0 e1 for one column's m x m Lanczos tridiagonal: LU with partial
 // pivoting and the singular-pivot flag (precond.hpp:208-249). UNR: every
 // index unrolled (T and y stay in registers, m <= 4); else rolled loops.
@@ -567,11 +575,12 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
         }
     }
     block_colsum4<C, NT>(acc, red, rbuf);
-    double beta0[kCW], inv[kCW];
+    double beta0[kCW], inv[kCW], rinv[kCW];
 #pragma unroll
     for (int j = 0; j < kCW; ++j) {
         beta0[j] = sqrt(acc[j]);
         inv[j] = beta0[j] != 0.0 ? beta0[j] : 1.0;
+        rinv[j] = 1.0 / inv[j];
     }
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
@@ -579,7 +588,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
         if (i < d) {
             double v[kCW];
 #pragma unroll
-            for (int j = 0; j < kCW; ++j) v[j] = w[k][j] / inv[j];
+            for (int j = 0; j < kCW; ++j) v[j] = div_rcp(w[k][j], inv[j], rinv[j]);
             st4(Vc + static_cast<std::size_t>(i) * C, v, hp);
             if constexpr (!VSM) st4(vg(0, i), v, hp);
         }
@@ -704,6 +713,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
                     inv[j] = nw;
                 }
             }
+            rinv[j] = 1.0 / inv[j];
         }
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
@@ -711,7 +721,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
             if (i < d) {
                 double v[kCW];
 #pragma unroll
-                for (int j = 0; j < kCW; ++j) v[j] = w[k][j] / inv[j];
+                for (int j = 0; j < kCW; ++j) v[j] = div_rcp(w[k][j], inv[j], rinv[j]);
                 if constexpr (VSM) {
                     st4(vg(s + 1, i), v, hp);
                 } else {
