@@ -551,8 +551,6 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
                 }
             }
         }
-    const double* vl = staged ? s_vl : gvl;
-    const std::uint16_t* cl = staged ? s_cl : gcl;
 
     int eb[RPT], ee[RPT];  // row i's entries [eb, ee), its diagonal at ee
     double w[RPT][kCW];  // V_s and V_{s-1} are re-read (shared memory / the CTA's slot), not held
@@ -616,38 +614,44 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
         // w = (K - sigma I) V_s ; alpha_s = V_s . w
 #pragma unroll
         for (int j = 0; j < kCW; ++j) acc[j] = 0.0;
+        // the entries' address space is fixed per copy (a select between the
+        // staged and the global arrays would force generic loads)
+        auto matvec = [&](const double* __restrict__ vl, const std::uint16_t* __restrict__ cl) {
 #pragma unroll
-        for (int k = 0; k < RPT; ++k) {
-            const int i = rl + k * RL;
-            double y[kCW] = {0.0, 0.0, 0.0, 0.0};
-            if (i < d) {
-                int e = eb[k];
-                for (; e + 1 < ee[k]; e += 2) {
-                    const double a0 = vl[e], a1 = vl[e + 1];
-                    const V4 x0 = ld4(Vc + static_cast<int>(cl[e]) * C, hp);
-                    const V4 x1 = ld4(Vc + static_cast<int>(cl[e + 1]) * C, hp);
+            for (int k = 0; k < RPT; ++k) {
+                const int i = rl + k * RL;
+                double y[kCW] = {0.0, 0.0, 0.0, 0.0};
+                if (i < d) {
+                    int e = eb[k];
+                    for (; e + 1 < ee[k]; e += 2) {
+                        const double a0 = vl[e], a1 = vl[e + 1];
+                        const V4 x0 = ld4(Vc + static_cast<int>(cl[e]) * C, hp);
+                        const V4 x1 = ld4(Vc + static_cast<int>(cl[e + 1]) * C, hp);
 #pragma unroll
-                    for (int j = 0; j < kCW; ++j) y[j] += a0 * x0.a[j];
+                        for (int j = 0; j < kCW; ++j) y[j] += a0 * x0.a[j];
 #pragma unroll
-                    for (int j = 0; j < kCW; ++j) y[j] += a1 * x1.a[j];
+                        for (int j = 0; j < kCW; ++j) y[j] += a1 * x1.a[j];
+                    }
+                    if (e < ee[k]) {
+                        const double a0 = vl[e];
+                        const V4 x0 = ld4(Vc + static_cast<int>(cl[e]) * C, hp);
+#pragma unroll
+                        for (int j = 0; j < kCW; ++j) y[j] += a0 * x0.a[j];
+                    }
+                    const V4 v = ld4(Vc + static_cast<std::size_t>(i) * C, hp);
+                    const double dg = vl[ee[k]];
+#pragma unroll
+                    for (int j = 0; j < kCW; ++j) {
+                        y[j] += (dg - sigma[j]) * v.a[j];
+                        acc[j] += v.a[j] * y[j];
+                    }
                 }
-                if (e < ee[k]) {
-                    const double a0 = vl[e];
-                    const V4 x0 = ld4(Vc + static_cast<int>(cl[e]) * C, hp);
 #pragma unroll
-                    for (int j = 0; j < kCW; ++j) y[j] += a0 * x0.a[j];
-                }
-                const V4 v = ld4(Vc + static_cast<std::size_t>(i) * C, hp);
-                const double dg = vl[ee[k]];
-#pragma unroll
-                for (int j = 0; j < kCW; ++j) {
-                    y[j] += (dg - sigma[j]) * v.a[j];
-                    acc[j] += v.a[j] * y[j];
-                }
+                for (int j = 0; j < kCW; ++j) w[k][j] = y[j];
             }
-#pragma unroll
-            for (int j = 0; j < kCW; ++j) w[k][j] = y[j];
-        }
+        };
+        if (staged) matvec(s_vl, s_cl);
+        else matvec(gvl, gcl);
         block_colsum4<C, NT>(acc, red, rbuf);
         double a[kCW];
 #pragma unroll
@@ -676,7 +680,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
             for (int k = 0; k < RPT; ++k) {
                 const int i = rl + k * RL;
                 if (i < d) {
-                    const V4 v = ld4(q == s ? Vc + static_cast<std::size_t>(i) * C : vg(q, i), hp);
+                    const V4 v = (q == s ? ld4(Vc + static_cast<std::size_t>(i) * C, hp) : ld4(vg(q, i), hp));
 #pragma unroll
                     for (int j = 0; j < kCW; ++j) acc[j] += v.a[j] * w[k][j];
                 }
@@ -686,7 +690,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
             for (int k = 0; k < RPT; ++k) {  // V_q re-read (shared memory or this CTA's L1/L2 slot)
                 const int i = rl + k * RL;
                 if (i < d) {
-                    const V4 v = ld4(q == s ? Vc + static_cast<std::size_t>(i) * C : vg(q, i), hp);
+                    const V4 v = (q == s ? ld4(Vc + static_cast<std::size_t>(i) * C, hp) : ld4(vg(q, i), hp));
 #pragma unroll
                     for (int j = 0; j < kCW; ++j) w[k][j] -= acc[j] * v.a[j];
                 }
