@@ -8,6 +8,9 @@ if the shared library is missing or a call fails, an exception is raised
 from __future__ import annotations
 
 import ctypes as C
+import mmap
+import sys
+import time
 from pathlib import Path
 
 import numpy as np
@@ -703,6 +706,23 @@ class Tiles:
             pass
 
 
+def host_array(shape) -> np.ndarray:
+    """An uninitialised float64 host array for device -> host results, backed by an anonymous
+    mapping advised for transparent huge pages (a large result then faults in 2 MB pages instead
+    of 4 KB ones while the copy lands)."""
+    count = int(np.prod(shape))
+    nbytes = max(count * 8, 8)
+    if nbytes < (8 << 20):
+        return np.empty(shape)
+    mm = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+    if hasattr(mm, "madvise") and hasattr(mmap, "MADV_HUGEPAGE"):
+        try:
+            mm.madvise(mmap.MADV_HUGEPAGE)
+        except OSError:
+            pass
+    return np.frombuffer(mm, dtype=np.float64, count=count).reshape(shape)
+
+
 def lobpcg(ctx: Context, op=None, n=None, tiles: Tiles | None = None, x0=None, k=5, nb=0, tol=1e-6, maxiter=500,
            fom_iterations=4, seed=1234, observer=None, observer_state=False, host_operator=None):
     """lobpcg_solve (lobpcg.hpp:291-456) on the device. `op` is an Operator;
@@ -733,15 +753,20 @@ def lobpcg(ctx: Context, op=None, n=None, tiles: Tiles | None = None, x0=None, k
                 return 1
         hop_cb = HOST_OP_FN(_hop)
     h = C.c_void_p()
+    t0 = time.perf_counter()
     check(lib().be_lobpcg_solve(ctx.handle, op.handle if op is not None else None, hop_cb, None, C.c_int64(n),
                                 tiles.handle if tiles is not None else None, _p(x0a), C.byref(cfg), obs_cb, None,
                                 C.byref(h)))
     try:
+        t1 = time.perf_counter()
         info = ResultInfo()
         check(lib().be_result_get_info(h, C.byref(info)))
         lam = np.zeros(info.k)
-        x = np.zeros((info.n, info.k))
+        x = host_array((info.n, info.k))
         check(lib().be_result_get(h, _p(lam), _p(x)))
+        if _os.environ.get("BE_TRACE_SEGMENTS"):
+            print(f"[be] host: solve call {1e3 * (t1 - t0):.1f} ms, eigenvector read {1e3 * (time.perf_counter() - t1):.1f} ms",
+                  file=sys.stderr, flush=True)
         nbb = info.nb
         th = np.zeros((info.iterations, nbb))
         rs = np.zeros((info.iterations, nbb))

@@ -697,7 +697,15 @@ be_status be_result_get(const be_result* r, double* lambda, double* x) {
     return guard([&] {
         if (!r) be::fail(BE_ERR_BAD_PARAMS, "null argument");
         if (lambda) std::memcpy(lambda, r->impl->lambda.data(), r->impl->lambda.size() * 8);
-        if (x) std::memcpy(x, r->impl->x.data(), r->impl->x.size() * 8);
+        if (x) {
+            const auto& R = *r->impl;
+            if (R.xdev.p) {
+                BE_CUDA(cudaSetDevice(R.device));
+                BE_CUDA(cudaMemcpy(x, R.xdev.get(), static_cast<std::size_t>(R.n) * R.k * 8, cudaMemcpyDeviceToHost));
+            } else {
+                std::memcpy(x, R.x.data(), R.x.size() * 8);
+            }
+        }
     });
 }
 

@@ -109,7 +109,19 @@ struct Solver {
             row_lo = op->row_lo;
         }
         const index_t pn = n * nb;
-        for (auto* b : {&X, &W, &P, &HX, &HW, &HP, &R, &Xn, &HXn, &Pn, &HPn}) b->reset(std::max<index_t>(pn, 1));
+        for (auto* b : {&X, &W, &P, &HX, &HW, &HP, &R, &Xn, &HXn, &Pn, &HPn}) {  // pooled on the context
+            const index_t need = std::max<index_t>(pn, 1);
+            auto& pool = ctx->panel_pool;
+            auto it = std::find_if(pool.begin(), pool.end(), [&](const DBuf<double>& d) { return d.n >= need; });
+            if (it != pool.end()) {
+                *b = std::move(*it);
+                pool.erase(it);
+            } else {  // nothing fits: the smaller pooled panels are dropped
+                pool.erase(std::remove_if(pool.begin(), pool.end(), [&](const DBuf<double>& d) { return d.n < need; }),
+                           pool.end());
+                b->reset(need);
+            }
+        }
         const index_t nb2 = static_cast<index_t>(nb) * nb, dim = 3 * nb;
         small.reset(12 * nb2 + 2 * dim * dim + dim * nb + 8 * nb2 + 8 * nb);
         double* p = small.get();
@@ -140,6 +152,9 @@ struct Solver {
     }
     ~Solver() {
         if (hm) cudaFreeHost(hm);
+        if (cudaStreamSynchronize(s) == cudaSuccess)  // (the panels may still be in use by queued work otherwise)
+            for (auto* b : {&X, &W, &P, &HX, &HW, &HP, &R, &Xn, &HXn, &Pn, &HPn})
+                if (b->p) ctx->panel_pool.push_back(std::move(*b));
     }
 
     void sync_status() {
@@ -424,17 +439,20 @@ struct Solver {
         return done;
     }
 
+    // The first k columns of X stay on the device (compacted to n x k); the
+    // caller's be_result_get copies them straight into its buffer.
     void finish() {
         res.converged = converged;
         res.lambda.assign(th.begin(), th.begin() + k);
-        std::vector<double> xall(static_cast<std::size_t>(n * nb));
-        BE_CUDA(cudaMemcpyAsync(xall.data(), X.get(), xall.size() * 8, cudaMemcpyDeviceToHost, s));
+        res.device = ctx->device;
+        res.xdev.reset(std::max<index_t>(n * k, 1));
+        if (n > 0)
+            BE_CUDA(cudaMemcpy2DAsync(res.xdev.get(), static_cast<std::size_t>(k) * 8, X.get(),
+                                      static_cast<std::size_t>(nb) * 8, static_cast<std::size_t>(k) * 8,
+                                      static_cast<std::size_t>(n), cudaMemcpyDeviceToDevice, s));
         BE_CUDA(cudaMemcpyAsync(&hm->fallbacks, fallbacks.get(), 8, cudaMemcpyDeviceToHost, s));
         BE_CUDA(cudaStreamSynchronize(s));
         res.precond_fallbacks = hm->fallbacks;
-        res.x.resize(static_cast<std::size_t>(n * k));
-        for (index_t r = 0; r < n; ++r)
-            for (int v = 0; v < k; ++v) res.x[static_cast<std::size_t>(r * k + v)] = xall[static_cast<std::size_t>(r * nb + v)];
     }
 
     be_observer_fn observer = nullptr;
@@ -463,12 +481,24 @@ std::unique_ptr<Result> lobpcg_solve(Ctx* ctx, Op* op, be_host_operator_fn host_
     res->n = n;
     res->nb = nb;
     res->k = cfg.k;
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
     Solver sv(ctx, n, nb, cfg.k, op, host_op, host_user, tiles, cfg, *res);
     sv.observer = observer;
     sv.observer_user = observer_user;
+    const auto t1 = clk::now();
     sv.init(x0);
+    BE_CUDA(cudaStreamSynchronize(sv.s));
+    const auto t2 = clk::now();
     sv.iterate(cfg.maxiter);
+    const auto t3 = clk::now();
     sv.finish();
+    const auto t4 = clk::now();
+    if (sv.trace_segments) {
+        auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "[be] solve ms: setup %.1f init %.1f iterate %.1f finish %.1f\n", ms(t0, t1), ms(t1, t2),
+                     ms(t2, t3), ms(t3, t4));
+    }
     return res;
 }
 

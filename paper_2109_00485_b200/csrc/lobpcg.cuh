@@ -21,6 +21,8 @@ struct Result {  // SolveResult + ConvergenceHistory, lobpcg.hpp:68-80
     index_t n = 0;
     int nb = 0, k = 0;
     std::vector<double> lambda, x;
+    int device = 0;
+    DBuf<double> xdev;  // the n x k eigenvector block, kept on the device until read (x stays empty then)
     std::vector<IterRecord> records;
     std::int64_t operator_calls = 0, precond_fallbacks = 0;
     int restarts = 0;
