@@ -121,6 +121,18 @@ be_status be_csb_load(const char* path, be_csb** out, double** diag, int64_t* nd
 be_status be_csb_load_rows(const char* path, int64_t brow_begin, int64_t brow_end, be_csb** out, double** diag,
                            int64_t* ndiag);
 void be_free_buffer(void* p);
+
+/* Matrix Market ingest (ingest_matrix_market / _file, matrix_market.hpp:38-94):
+ * coordinate real|integer symmetric input; entries of either triangle become
+ * strictly-lower triples (file order), diagonal entries a dense diag[n]
+ * (0 where absent). BE_ERR_PARSE for a malformed file, BE_ERR_NOT_SYMMETRIC_HEADER
+ * for a non-symmetric header, BE_ERR_DUPLICATE_ENTRY for a repeated diagonal
+ * entry. *lower and *diag are released with be_free_buffer. */
+be_status be_mm_parse(const char* text, int64_t len, int64_t* n, be_triple** lower, int64_t* nlower, double** diag);
+be_status be_mm_read_file(const char* path, int64_t* n, be_triple** lower, int64_t* nlower, double** diag);
+/* write_matrix_market (matrix_market.hpp:98-113): NUL-terminated text, released with be_free_buffer */
+be_status be_mm_write(int64_t n, const be_triple* lower, int64_t nlower, const double* diag, char** text,
+                      int64_t* len);
 void be_csb_free(be_csb* m);
 
 /* ------------------------------------------------------------------------- */

@@ -10,12 +10,14 @@
 #include <blockeig/dist.hpp>
 #include <blockeig/kernels.hpp>
 #include <blockeig/lobpcg.hpp>
+#include <blockeig/matrix_market.hpp>
 #include <blockeig/precond.hpp>
 #include <blockeig/synth.hpp>
 
 #include <chrono>
 #include <cstring>
 #include <memory>
+#include <sstream>
 #include <string>
 
 using namespace blockeig;
@@ -37,6 +39,8 @@ int code_of(const Error& e) {
     if (dynamic_cast<const RankDeficient*>(&e)) return 12;
     if (dynamic_cast<const BasisDegenerate*>(&e)) return 13;
     if (dynamic_cast<const BreakdownUnrecoverable*>(&e)) return 14;
+    if (dynamic_cast<const NotSymmetricHeader*>(&e)) return 18;
+    if (dynamic_cast<const ParseError*>(&e)) return 17;
     return 1;
 }
 
@@ -385,6 +389,42 @@ int ref_partition_rank(const index_t* rows, const index_t* cols, const double* v
         *out_count = k;
         seg[0] = pb.segment_of_rank[static_cast<std::size_t>(rank)].begin;
         seg[1] = pb.segment_of_rank[static_cast<std::size_t>(rank)].end;
+    });
+}
+
+// ingest_matrix_market on a text buffer: n, the lower triples (file order) and diag[n]
+int ref_mm_parse(const char* text, index_t len, index_t* n, index_t* rows, index_t* cols, double* vals,
+                 index_t* count, double* diag, index_t diag_cap) {
+    return guarded([&] {
+        std::istringstream is(std::string(text, static_cast<std::size_t>(len)));
+        const auto m = ingest_matrix_market(is);
+        *n = m.n;
+        if (rows) {
+            if (static_cast<index_t>(m.lower.size()) > *count) throw BadParams("ref_mm_parse: buffer too small");
+            for (std::size_t k = 0; k < m.lower.size(); ++k) {
+                rows[k] = m.lower[k].row;
+                cols[k] = m.lower[k].col;
+                vals[k] = m.lower[k].value;
+            }
+        }
+        *count = static_cast<index_t>(m.lower.size());
+        if (diag && diag_cap >= m.n) std::memcpy(diag, m.diag.data(), m.diag.size() * sizeof(double));
+    });
+}
+
+// write_matrix_market into buf (cap bytes); *len = the text length
+int ref_mm_write(index_t n, const index_t* rows, const index_t* cols, const double* vals, index_t count,
+                 const double* diag, char* buf, index_t cap, index_t* len) {
+    return guarded([&] {
+        SymmetricCoo m;
+        m.n = n;
+        for (index_t k = 0; k < count; ++k) m.lower.push_back({rows[k], cols[k], vals[k]});
+        m.diag.assign(diag, diag + n);
+        std::ostringstream os;
+        write_matrix_market(os, m);
+        const std::string s = os.str();
+        *len = static_cast<index_t>(s.size());
+        if (buf && cap > *len) std::memcpy(buf, s.c_str(), s.size() + 1);
     });
 }
 

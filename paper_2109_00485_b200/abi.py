@@ -267,6 +267,49 @@ class Csb:
         return m, diag
 
 
+def _mm_result(call):
+    n = C.c_int64(0)
+    nl = C.c_int64(0)
+    lp = C.c_void_p()
+    dp = C.POINTER(C.c_double)()
+    check(call(C.byref(n), C.byref(lp), C.byref(nl), C.byref(dp)))
+    try:
+        lower = np.frombuffer((C.c_char * (24 * nl.value)).from_address(lp.value), dtype=TRIPLE_DTYPE).copy() \
+            if nl.value else np.zeros(0, dtype=TRIPLE_DTYPE)
+        diag = np.ctypeslib.as_array(dp, shape=(n.value,)).copy()
+    finally:
+        lib().be_free_buffer(lp)
+        lib().be_free_buffer(dp)
+    return n.value, lower, diag
+
+
+def read_matrix_market(path=None, text=None):
+    """ingest_matrix_market(_file) (matrix_market.hpp:38-94): (n, strictly-lower triples in file
+    order, dense diagonal). Raises ParseError / NotSymmetricHeader / DuplicateEntry like the reference."""
+    if (path is None) == (text is None):
+        raise ValueError("give exactly one of path / text")
+    if path is not None:
+        return _mm_result(lambda *a: lib().be_mm_read_file(str(path).encode(), *a))
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    return _mm_result(lambda *a: lib().be_mm_parse(b, C.c_int64(len(b)), *a))
+
+
+def write_matrix_market(n: int, lower: np.ndarray, diag) -> str:
+    """write_matrix_market (matrix_market.hpp:98-113)."""
+    t = np.ascontiguousarray(lower, dtype=TRIPLE_DTYPE)
+    d = np.ascontiguousarray(diag, dtype=np.float64)
+    if d.shape != (n,):
+        raise ValueError("diag must have n entries")
+    tp = C.c_void_p()
+    ln = C.c_int64(0)
+    check(lib().be_mm_write(C.c_int64(n), _p(t) if len(t) else None, C.c_int64(len(t)), _p(d), C.byref(tp),
+                            C.byref(ln)))
+    try:
+        return C.string_at(tp.value, ln.value).decode()
+    finally:
+        lib().be_free_buffer(tp)
+
+
 def as_triples(rows, cols, values) -> np.ndarray:
     t = np.zeros(len(rows), dtype=TRIPLE_DTYPE)
     t["row"], t["col"], t["value"] = rows, cols, values

@@ -11,6 +11,7 @@
 #include "densela.cuh"
 #include "device.hpp"
 #include "lobpcg.cuh"
+#include "matrix_market.hpp"
 #include "precond.cuh"
 #include "tri_layout.hpp"
 
@@ -140,6 +141,51 @@ be_status be_csb_load_rows(const char* path, int64_t brow_begin, int64_t brow_en
 }
 
 void be_csb_free(be_csb* m) { delete m; }
+
+// ----------------------------------------------------------- Matrix Market
+namespace {
+void mm_out(be::MmMatrix&& m, int64_t* n, be_triple** lower, int64_t* nlower, double** diag) {
+    if (n) *n = m.n;
+    if (nlower) *nlower = static_cast<int64_t>(m.lower.size());
+    if (lower) {
+        *lower = static_cast<be_triple*>(std::malloc(std::max<std::size_t>(m.lower.size(), 1) * sizeof(be_triple)));
+        if (!*lower) be::fail(BE_ERR_OUT_OF_MEMORY, "matrix market: host allocation failed");
+        if (!m.lower.empty()) std::memcpy(*lower, m.lower.data(), m.lower.size() * sizeof(be_triple));
+    }
+    if (diag) {
+        *diag = static_cast<double*>(std::malloc(std::max<std::size_t>(m.diag.size(), 1) * sizeof(double)));
+        if (!*diag) be::fail(BE_ERR_OUT_OF_MEMORY, "matrix market: host allocation failed");
+        if (!m.diag.empty()) std::memcpy(*diag, m.diag.data(), m.diag.size() * sizeof(double));
+    }
+}
+}  // namespace
+
+be_status be_mm_parse(const char* text, int64_t len, int64_t* n, be_triple** lower, int64_t* nlower, double** diag) {
+    return guard([&] {
+        if (!text || len < 0) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        mm_out(be::parse_matrix_market(text, static_cast<std::size_t>(len)), n, lower, nlower, diag);
+    });
+}
+
+be_status be_mm_read_file(const char* path, int64_t* n, be_triple** lower, int64_t* nlower, double** diag) {
+    return guard([&] {
+        if (!path) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        mm_out(be::read_matrix_market_file(path), n, lower, nlower, diag);
+    });
+}
+
+be_status be_mm_write(int64_t n, const be_triple* lower, int64_t nlower, const double* diag, char** text,
+                      int64_t* len) {
+    return guard([&] {
+        if ((!lower && nlower > 0) || (!diag && n > 0) || !text || n < 0 || nlower < 0)
+            be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        const std::string s = be::write_matrix_market(n, lower, nlower, diag);
+        *text = static_cast<char*>(std::malloc(s.size() + 1));
+        if (!*text) be::fail(BE_ERR_OUT_OF_MEMORY, "matrix market: host allocation failed");
+        std::memcpy(*text, s.c_str(), s.size() + 1);
+        if (len) *len = static_cast<int64_t>(s.size());
+    });
+}
 
 // --------------------------------------------------------------- generators
 be_status be_generate_synthetic(const be_synth_params* p, be_synth** out) {
