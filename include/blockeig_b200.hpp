@@ -24,6 +24,9 @@
 #include <cstdint>
 #include <exception>
 #include <functional>
+#include <istream>
+#include <iterator>
+#include <ostream>
 #include <memory>
 #include <random>
 #include <span>
@@ -311,6 +314,51 @@ inline CsbCooMatrix load_csb_file(const std::string& path, std::vector<double>* 
     if (diag) diag->assign(d, d + nd);
     be_free_buffer(d);
     return b200::take(h);
+}
+
+// --------------------------------------------------------- matrix_market.hpp
+struct SymmetricCoo {  // matrix_market.hpp:20-24
+    index_t n = 0;
+    std::vector<Triple> lower;
+    std::vector<double> diag;
+};
+
+namespace b200 {
+inline SymmetricCoo take_mm(int64_t n, be_triple* lower, int64_t nlower, double* diag) {
+    SymmetricCoo m;
+    m.n = n;
+    m.lower.resize(static_cast<std::size_t>(nlower));
+    for (int64_t k = 0; k < nlower; ++k) m.lower[static_cast<std::size_t>(k)] = {lower[k].row, lower[k].col, lower[k].value};
+    m.diag.assign(diag, diag + n);
+    be_free_buffer(lower);
+    be_free_buffer(diag);
+    return m;
+}
+}  // namespace b200
+
+inline SymmetricCoo ingest_matrix_market(std::istream& is) {  // matrix_market.hpp:38
+    const std::string text((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+    int64_t n = 0, nl = 0;
+    be_triple* lo = nullptr;
+    double* d = nullptr;
+    b200::check(be_mm_parse(text.data(), static_cast<int64_t>(text.size()), &n, &lo, &nl, &d));
+    return b200::take_mm(n, lo, nl, d);
+}
+inline SymmetricCoo ingest_matrix_market_file(const std::string& path) {  // matrix_market.hpp:90
+    int64_t n = 0, nl = 0;
+    be_triple* lo = nullptr;
+    double* d = nullptr;
+    b200::check(be_mm_read_file(path.c_str(), &n, &lo, &nl, &d));
+    return b200::take_mm(n, lo, nl, d);
+}
+inline void write_matrix_market(std::ostream& os, const SymmetricCoo& m) {  // matrix_market.hpp:98
+    std::vector<be_triple> t(m.lower.size());
+    for (std::size_t k = 0; k < t.size(); ++k) t[k] = {m.lower[k].row, m.lower[k].col, m.lower[k].value};
+    char* text = nullptr;
+    int64_t len = 0;
+    b200::check(be_mm_write(m.n, t.data(), static_cast<int64_t>(t.size()), m.diag.data(), &text, &len));
+    os.write(text, len);
+    be_free_buffer(text);
 }
 
 // --------------------------------------------------------------- kernels.hpp
@@ -681,12 +729,6 @@ inline SolveResult lobpcg_solve(const SymmetricOperator& h, const DiagonalTileSe
 
 // ----------------------------------------------------------------- synth.hpp
 enum class SynthKind { Banded, BlockTile, Random };  // synth.hpp:14
-
-struct SymmetricCoo {
-    index_t n = 0;
-    std::vector<Triple> lower;
-    std::vector<double> diag;
-};
 
 struct SynthParams {  // synth.hpp:33-56
     SynthKind kind = SynthKind::Random;

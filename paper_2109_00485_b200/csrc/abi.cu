@@ -9,6 +9,7 @@
 
 #include "comm.hpp"
 #include "densela.cuh"
+#include "hostcopy.hpp"
 #include "device.hpp"
 #include "lobpcg.cuh"
 #include "matrix_market.hpp"
@@ -747,7 +748,7 @@ be_status be_result_get(const be_result* r, double* lambda, double* x) {
             const auto& R = *r->impl;
             if (R.xdev.p) {
                 BE_CUDA(cudaSetDevice(R.device));
-                BE_CUDA(cudaMemcpy(x, R.xdev.get(), static_cast<std::size_t>(R.n) * R.k * 8, cudaMemcpyDeviceToHost));
+                be::d2h_large(x, R.xdev.get(), static_cast<std::size_t>(R.n) * R.k * 8, nullptr);
             } else {
                 std::memcpy(x, R.x.data(), R.x.size() * 8);
             }

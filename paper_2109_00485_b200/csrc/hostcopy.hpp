@@ -1,0 +1,16 @@
+// Staged, multi-threaded copies between pageable host memory and the device.
+#pragma once
+
+#include <cstddef>
+
+#include <cuda_runtime.h>
+
+#include "device.hpp"
+
+namespace be {
+
+// Both return with the copy complete (src / dst may be reused immediately).
+void h2d_large(void* dst, const void* src, std::size_t bytes, cudaStream_t s);
+void d2h_large(void* dst, const void* src, std::size_t bytes, cudaStream_t s);
+
+}  // namespace be

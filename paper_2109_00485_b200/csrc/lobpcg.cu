@@ -22,6 +22,7 @@
 
 #include "comm.hpp"
 #include "densela.cuh"
+#include "hostcopy.hpp"
 #include "lobpcg.cuh"
 #include "precond.cuh"
 
@@ -274,7 +275,7 @@ struct Solver {
 
     void init(const double* x0) {
         if (x0)
-            BE_CUDA(cudaMemcpyAsync(X.get(), x0, static_cast<std::size_t>(n * nb) * 8, cudaMemcpyHostToDevice, s));
+            h2d_large(X.get(), x0, static_cast<std::size_t>(n * nb) * 8, s);
         else
             upload_random(X.get(), cfg.seed);
         if (!qr(X.get(), true)) fail(BE_ERR_RANK_DEFICIENT, "qr_of_transpose: Gram Cholesky failed twice");

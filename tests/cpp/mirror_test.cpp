@@ -4,6 +4,7 @@
 // Built by __graft_entry__.build(); run by tests/test_mirror_gpu.py.
 #include <cmath>
 #include <cstdio>
+#include <sstream>
 #include <cstdlib>
 #include <string>
 
@@ -56,6 +57,23 @@ int main() {
     const auto b = uniform_boundaries(p.n, 700);
     CsbCooMatrix l = build_csb_coo(s.coo.lower, p.n, p.n, b, b);
     CHECK(is_strictly_lower(l));
+    {  // Matrix Market (matrix_market.hpp:38-113) through the mirror
+        std::stringstream mm;
+        SymmetricCoo c;
+        c.n = p.n;
+        c.lower = s.coo.lower;
+        c.diag = s.coo.diag;
+        write_matrix_market(mm, c);
+        const SymmetricCoo r = ingest_matrix_market(mm);
+        CHECK(r.n == c.n && r.lower.size() == c.lower.size() && r.diag == c.diag);
+        bool same = true;
+        for (std::size_t k = 0; k < r.lower.size(); ++k)
+            same = same && r.lower[k].row == c.lower[k].row && r.lower[k].col == c.lower[k].col &&
+                   r.lower[k].value == c.lower[k].value;
+        CHECK(same);
+        std::istringstream bad("%%MatrixMarket matrix coordinate real general\n1 1 0\n");
+        CHECK(throws<NotSymmetricHeader>([&] { ingest_matrix_market(bad); }));
+    }
     CHECK(l.nnz() == static_cast<index_t>(s.coo.lower.size()));
     {
         auto back = to_triples(l);
