@@ -17,7 +17,8 @@ sp = [i for i, (n, _) in enumerate(ls) if 'k_sym_spmm' in n]
 a, b = sp[-2], sp[-1]
 agg = collections.OrderedDict()
 for n, v in ls[a:b]:
-    short = re.sub(r'\(.*', '', n).replace('void ', '').replace('unnamed>::', '')
+    short = re.sub(r'\(.*', '', n).replace('void ', '')
+    short = re.sub(r'^.*(unnamed>::|dla::|be::)', '', short)
     if not short.startswith('k_'):
         short = 'library: ' + short[:40]
     e = agg.setdefault(short, [0, 0.0]); e[0] += 1; e[1] += v
