@@ -279,3 +279,28 @@ def test_gram_matches_numpy(ctx):
     assert np.allclose(g, want, rtol=1e-12, atol=1e-10)
     gs = abi.gram_dev(ctx, a.data_ptr(), a.data_ptr(), 16, 12345)
     assert np.array_equal(gs, gs.T)
+
+
+def test_repeated_solves_reuse_the_context_panels(ctx):
+    """Solves on one context take their panels from the context's pool (Ctx::panel_pool): the same
+    solve twice is bit-identical, a larger problem in between re-allocates, host x0 in and eigenvectors
+    out go through the pinned staging path (the 140000-row problem: x0 and the eigenvectors are above
+    the 8 MB staging threshold)."""
+    m, d = make_test_matrix(1500, 30000, 7)
+    op = abi.Operator(ctx, m, d, values_prec=abi.BE_F64)
+    a = abi.lobpcg(ctx, op, k=4, nb=8, tol=1e-8, maxiter=300, seed=3)
+    mb, db = make_test_matrix(140000, 400000, 8)
+    opb = abi.Operator(ctx, mb, db, values_prec=abi.BE_F32)
+    x0 = np.random.default_rng(2).uniform(-1, 1, (140000, 16))
+    big = abi.lobpcg(ctx, opb, x0=x0, k=8, nb=16, tol=1e-300, maxiter=3, seed=3)
+    assert big["x"].shape == (140000, 8) and np.all(np.isfinite(big["x"]))
+    # X is orthonormal after the Rayleigh-Ritz update: the staged read-back must be too
+    g = big["x"].T @ big["x"]
+    assert np.max(np.abs(g - np.eye(8))) < 1e-8
+    # (the SpMM's transposed pass reduces with atomics, so repeated solves agree to rounding, not bitwise)
+    b = abi.lobpcg(ctx, op, k=4, nb=8, tol=1e-8, maxiter=300, seed=3)
+    assert abs(a["iterations"] - b["iterations"]) <= 1
+    assert np.max(np.abs(a["lambda_"] - b["lambda_"]) / np.abs(a["lambda_"])) < 1e-10
+    assert np.max(np.abs(a["x"] - b["x"])) < 1e-6
+    big2 = abi.lobpcg(ctx, opb, x0=x0, k=8, nb=16, tol=1e-300, maxiter=3, seed=3)
+    assert np.max(np.abs(big["x"] - big2["x"])) < 1e-8
