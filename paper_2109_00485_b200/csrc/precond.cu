@@ -927,10 +927,18 @@ std::unique_ptr<Tiles> tiles_create(Ctx* ctx, const be_csb_view& L, const double
         for (int c = 0; c <= static_cast<int>(t->class_dim.size()); ++c) {
             t->class_begin.push_back(static_cast<index_t>(lists.size()));
             const int hi = c < static_cast<int>(t->class_dim.size()) ? t->class_dim[static_cast<std::size_t>(c)] : 1 << 30;
+            const std::size_t b0 = lists.size();
             for (index_t j = 0; j < nt; ++j) {
                 const index_t dd = t->host[static_cast<std::size_t>(j)].dim;
                 if (dd > lo && dd <= hi) lists.push_back(static_cast<std::int32_t>(j));
             }
+            // largest tiles first (entries + rows): the last wave of CTAs is the short one
+            auto work = [&](std::int32_t j) {
+                const auto& h = t->host[static_cast<std::size_t>(j)];
+                return static_cast<index_t>(h.vals.size()) + 8 * h.dim;
+            };
+            std::stable_sort(lists.begin() + static_cast<std::ptrdiff_t>(b0), lists.end(),
+                             [&](std::int32_t a, std::int32_t b) { return work(a) > work(b); });
             lo = hi;
         }
         t->class_begin.push_back(static_cast<index_t>(lists.size()));
