@@ -965,9 +965,29 @@ void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, i
     const auto* tdv = reinterpret_cast<const TileDev*>(t->tiles.get());
     const int ncls = static_cast<int>(t->class_dim.size());
     const bool reg_ok = m <= 8;
-    for (int c = 0; c < ncls && reg_ok; ++c) {
+    // The classes write disjoint rows of W: the largest class runs on s, launched
+    // first, the others on side streams, so small-tile CTAs fill the SMs around
+    // the large-tile ones (one 512-thread CTA per SM leaves room).
+    static_assert(sizeof(kClassDims) / sizeof(kClassDims[0]) <= 8, "class arrays");
+    if (!t->fork) {
+        BE_CUDA(cudaEventCreateWithFlags(&t->fork, cudaEventDisableTiming));
+        for (int c = 0; c < ncls; ++c) {
+            BE_CUDA(cudaStreamCreateWithFlags(&t->side[c], cudaStreamNonBlocking));
+            BE_CUDA(cudaEventCreateWithFlags(&t->join[c], cudaEventDisableTiming));
+        }
+    }
+    BE_CUDA(cudaEventRecord(t->fork, s));
+    bool joined[8] = {};
+    for (int ci = 0; ci < ncls && reg_ok; ++ci) {
+        const int c = ncls - 1 - ci;  // largest class first
         const index_t b0 = t->class_begin[static_cast<std::size_t>(c)], b1 = t->class_begin[static_cast<std::size_t>(c) + 1];
         if (b1 == b0) continue;
+        cudaStream_t cs = s;
+        if (ci > 0) {
+            cs = t->side[c];
+            BE_CUDA(cudaStreamWaitEvent(cs, t->fork, 0));
+            joined[c] = true;
+        }
         const int dmax = t->class_dim[static_cast<std::size_t>(c)];
         const int C = kFomCols;
         const int ngroups = (nb + C - 1) / C;
@@ -987,20 +1007,20 @@ void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, i
             BE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, nt, sm));
             kslots = std::max(1, std::min(per, 32));
             const index_t vneed = static_cast<index_t>(mc) * t->ctx->num_sms * kslots * dmax * C;
-            if (t->vscratch.n < vneed) t->vscratch.reset(vneed);
-            if (t->slot_mask.n < t->ctx->num_sms) {
-                t->slot_mask.reset(t->ctx->num_sms);
-                BE_CUDA(cudaMemsetAsync(t->slot_mask.get(), 0, t->slot_mask.bytes(), s));
+            if (t->vscratch[c].n < vneed) t->vscratch[c].reset(vneed);
+            if (t->slot_mask[c].n < t->ctx->num_sms) {
+                t->slot_mask[c].reset(t->ctx->num_sms);
+                BE_CUDA(cudaMemsetAsync(t->slot_mask[c].get(), 0, t->slot_mask[c].bytes(), cs));
             }
         };
 #define BE_FOMB(MC, NTT, RPT, VS)                                                                                  \
     do {                                                                                                           \
         ensure_dyn_smem(k_fom_blk<MC, NTT, RPT, VS>, sm);                                                          \
         if (!(VS)) slots_for(reinterpret_cast<const void*>(k_fom_blk<MC, NTT, RPT, VS>), NTT);                    \
-        k_fom_blk<MC, NTT, RPT, VS><<<grid, NTT, sm, s>>>(tdv, list, t->rowptr.get(), t->cols.get(), t->vals.get(), \
-                                                           shifts, R, W, nb, m, ngroups, fallbacks, dmax,          \
-                                                           stage_cap, t->vscratch.get(), t->n, t->slot_mask.get(), \
-                                                           kslots);                                                \
+        k_fom_blk<MC, NTT, RPT, VS><<<grid, NTT, sm, cs>>>(tdv, list, t->rowptr.get(), t->cols.get(), t->vals.get(), \
+                                                            shifts, R, W, nb, m, ngroups, fallbacks, dmax,         \
+                                                            stage_cap, t->vscratch[c].get(), t->n,                 \
+                                                            t->slot_mask[c].get(), kslots);                        \
     } while (0)
 #define BE_FOMB2(NTT, RPT)                      \
     if (mc == 4) {                              \
@@ -1021,7 +1041,10 @@ void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, i
 #undef BE_FOMB
         BE_CUDA(cudaGetLastError());
         ++t->ctx->launches;
+        if (joined[c]) BE_CUDA(cudaEventRecord(t->join[c], cs));
     }
+    for (int c = 0; c < ncls; ++c)
+        if (joined[c]) BE_CUDA(cudaStreamWaitEvent(s, t->join[c], 0));
     // everything the register kernel does not cover goes through the CTA kernel
     const index_t big_begin = reg_ok ? t->class_begin[static_cast<std::size_t>(ncls)] : 0;
     const index_t nbig = t->class_begin.back() - big_begin;

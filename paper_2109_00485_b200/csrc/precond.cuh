@@ -34,8 +34,20 @@ struct Tiles {
     DBuf<std::int32_t> rowptr;
     DBuf<std::uint16_t> cols;
     DBuf<double> vals;
-    DBuf<double> vscratch;  // older Krylov vectors of the block kernel (L2-resident per CTA)
-    DBuf<unsigned> slot_mask;  // per SM: which scratch slots resident CTAs hold
+    // per size class: older Krylov vectors of the block kernel (L2-resident
+    // scratch slots) and the per-SM mask of the slots resident CTAs hold
+    DBuf<double> vscratch[8];
+    DBuf<unsigned> slot_mask[8];
+    // the size classes run concurrently: side streams joined back by events
+    cudaStream_t side[8] = {};
+    cudaEvent_t fork = nullptr, join[8] = {};
+    ~Tiles() {
+        for (auto& x : side)
+            if (x) cudaStreamDestroy(x);
+        for (auto& x : join)
+            if (x) cudaEventDestroy(x);
+        if (fork) cudaEventDestroy(fork);
+    }
 };
 
 // extract_tiles + upload; [row_lo, row_hi) restricts the result to the tiles
