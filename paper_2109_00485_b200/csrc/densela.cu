@@ -312,6 +312,14 @@ __global__ void __launch_bounds__(256, BE_GRAM_CTAS) k_gram_m(GramDev g, GramM q
     const int wg = warp / q.rg, rgi = warp % q.rg;  // pair group, row group
     const int p0 = wg * q.pw;
     const int m = lane >> 2, kq = lane & 3;
+    // this warp's pairs: count and panel offsets in a stage, hoisted out of the row loop
+    const int npw = max(0, min(q.pw, g.npairs - p0));
+    int aoff[MAXPW], boff[MAXPW];
+#pragma unroll
+    for (int a = 0; a < MAXPW; ++a) {
+        aoff[a] = a < npw ? g.ia[p0 + a] * q.ps : 0;
+        boff[a] = a < npw ? g.ib[p0 + a] * q.ps : 0;
+    }
     double acc[MAXPW][NBB][NBB][2];
 #pragma unroll
     for (int a = 0; a < MAXPW; ++a)
@@ -329,12 +337,12 @@ __global__ void __launch_bounds__(256, BE_GRAM_CTAS) k_gram_m(GramDev g, GramM q
         for (int k0 = 4 * rgi; k0 < rows; k0 += 4 * q.rg) {
             const int r = k0 + kq;
             const bool ok = r < rows;
+            const double* sr = st + r * q.rs + m;
 #pragma unroll
             for (int a = 0; a < MAXPW; ++a) {
-                const int p = p0 + a;
-                if (a >= q.pw || p >= g.npairs) break;
-                const double* A = st + g.ia[p] * q.ps + r * q.rs + m;
-                const double* B = st + g.ib[p] * q.ps + r * q.rs + m;
+                if (a >= npw) break;
+                const double* A = sr + aoff[a];
+                const double* B = sr + boff[a];
                 double fa[NBB], fb[NBB];
 #pragma unroll
                 for (int i = 0; i < NBB; ++i) {
