@@ -900,11 +900,23 @@ __global__ void __launch_bounds__(256, 2) k_trsm_s(double* __restrict__ w0, doub
                 if (2 * k < nb) reinterpret_cast<double2*>(xr)[k] = make_double2(x[2 * k], x[2 * k + 1]);
         }
         __syncthreads();  // the stage holds the chunk's results: coalesced 16-byte stores
-        const int pr = nb / 2, per = rows * pr;
-        for (int e = tid; e < per * np; e += 256) {
-            const int p = e / per, k = e % per, r = k / pr, cc = k % pr;
-            reinterpret_cast<double2*>((p == 0 ? w0 : w1) + (r0 + r) * nb)[cc] =
-                reinterpret_cast<const double2*>(stg + p * ps + r * rs)[cc];
+        if (nb == NBP) {  // compile-time piece count: no integer division per store
+            constexpr int PR = NBP / 2;
+            for (int p = 0; p < np; ++p) {
+                double* w = (p == 0 ? w0 : w1) + r0 * NBP;
+                const double* sp = stg + p * ps;
+                for (int e = tid; e < rows * PR; e += 256) {
+                    const int r = e / PR, cc = e % PR;
+                    reinterpret_cast<double2*>(w + r * NBP)[cc] = reinterpret_cast<const double2*>(sp + r * rs)[cc];
+                }
+            }
+        } else {
+            const int pr = nb / 2, per = rows * pr;
+            for (int e = tid; e < per * np; e += 256) {
+                const int p = e / per, k = e % per, r = k / pr, cc = k % pr;
+                reinterpret_cast<double2*>((p == 0 ? w0 : w1) + (r0 + r) * nb)[cc] =
+                    reinterpret_cast<const double2*>(stg + p * ps + r * rs)[cc];
+            }
         }
         __syncthreads();  // stage free for the refill at c + 1
     }
