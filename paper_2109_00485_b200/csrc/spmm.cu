@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -402,7 +403,9 @@ __global__ void __launch_bounds__(kThreads, sizeof(TC) == 4 ? (NBP <= 16 ? BE_SP
 #ifndef BE_SPMM_UNR
 #define BE_SPMM_UNR 4
 #endif
-                if (active)
+                // the pass is warp-uniform: one copy of the walk per pass (no per-entry selects)
+                auto walk = [&](auto pass) {
+                    constexpr int GP = decltype(pass)::value;
                     for (int j0 = 0; j0 < len; j0 += BE_SPMM_UNR) {
                         int st4[4];  // starts j0 .. j0 + BE_SPMM_UNR - 1 in one shared-memory read
                         if constexpr (BE_SPMM_UNR == 4) {
@@ -418,11 +421,11 @@ __global__ void __launch_bounds__(kThreads, sizeof(TC) == 4 ? (NBP <= 16 ? BE_SP
                         for (int u = 0; u < BE_SPMM_UNR; ++u) {
                             if (j0 + u >= len) break;
                             int pos = st4[u] + rank;
-                            if (grp == 1) pos = scp[pos];
+                            if constexpr (GP == 1) pos = scp[pos];
                             const TC v = static_cast<TC>(sv[pos]);
                             const std::uint32_t x = src[pos];
                             if (j0 + u == 0) first = x;
-                            const unsigned char* p = xbase + (grp == 0 ? (x & 255u) : (x >> 8)) * G::LINEB;
+                            const unsigned char* p = xbase + (GP == 0 ? (x & 255u) : (x >> 8)) * G::LINEB;
                             V xv[G::CH];
 #pragma unroll
                             for (int i = 0; i < G::CH; ++i) xv[i] = *reinterpret_cast<const V*>(p + coff[i]);
@@ -430,6 +433,11 @@ __global__ void __launch_bounds__(kThreads, sizeof(TC) == 4 ? (NBP <= 16 ? BE_SP
                             for (int i = 0; i < G::CH; ++i) vfma(acc[i], v, xv[i]);
                         }
                     }
+                };
+                if (active) {
+                    if (grp == 0) walk(std::integral_constant<int, 0>{});
+                    else walk(std::integral_constant<int, 1>{});
+                }
                 if (active) {
                     if (grp == 0) {  // Y_I += A X_J for this row
                         V* y = yi + (first >> 8) * G::CH;
