@@ -810,6 +810,7 @@ def lobpcg(ctx: Context, op=None, n=None, tiles: Tiles | None = None, x0=None, k
         if _os.environ.get("BE_TRACE_SEGMENTS"):
             print(f"[be] host: solve call {1e3 * (t1 - t0):.1f} ms, eigenvector read {1e3 * (time.perf_counter() - t1):.1f} ms",
                   file=sys.stderr, flush=True)
+            t1 = time.perf_counter()
         nbb = info.nb
         th = np.zeros((info.iterations, nbb))
         rs = np.zeros((info.iterations, nbb))
@@ -828,6 +829,8 @@ def lobpcg(ctx: Context, op=None, n=None, tiles: Tiles | None = None, x0=None, k
                     theta=th, residual_norms=rs, n_converged=nc, times=times)
     finally:
         lib().be_result_free(h)
+        if _os.environ.get("BE_TRACE_SEGMENTS"):
+            print(f"[be] host: records + result free {1e3 * (time.perf_counter() - t1):.1f} ms", file=sys.stderr, flush=True)
 
 
 def gram_dev(ctx: Context, a_ptr: int, b_ptr: int, nb: int, n: int) -> np.ndarray:

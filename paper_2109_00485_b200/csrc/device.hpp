@@ -4,7 +4,9 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "host_csb.hpp"
@@ -45,6 +47,31 @@ struct DBuf {
     std::size_t bytes() const { return static_cast<std::size_t>(n) * sizeof(T); }
 };
 
+// Device panels kept for reuse; shared by a context and the results it
+// produced (a result returns its eigenvector block here when freed).
+struct PanelPool {
+    std::mutex mu;
+    std::vector<DBuf<double>> bufs;
+    DBuf<double> take(index_t need) {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto it = bufs.begin(); it != bufs.end(); ++it)
+            if (it->n >= need) {
+                DBuf<double> b = std::move(*it);
+                bufs.erase(it);
+                return b;
+            }
+        // nothing fits: the smaller pooled panels are dropped
+        bufs.erase(std::remove_if(bufs.begin(), bufs.end(), [&](const DBuf<double>& d) { return d.n < need; }),
+                   bufs.end());
+        return DBuf<double>(need);
+    }
+    void give(DBuf<double>&& b) {
+        if (!b.p) return;
+        std::lock_guard<std::mutex> lk(mu);
+        bufs.push_back(std::move(b));
+    }
+};
+
 struct Ctx {
     int device = 0;
     int num_sms = 0;
@@ -52,9 +79,11 @@ struct Ctx {
     cusolverDnContext* solver = nullptr;
     cublasContext* blas = nullptr;  // triangular solves of the 3nb x 3nb pencil
     long long launches = 0;  // kernels launched through this context
-    // n x nb panels of finished solves, reused by the next solve on this
-    // context (no cudaMalloc / cudaFree of ~11 panels per call)
-    std::vector<DBuf<double>> panel_pool;
+    // n x nb panels of finished solves (and of freed results), reused by the
+    // next solve on this context: no cudaMalloc / cudaFree per call
+    std::shared_ptr<PanelPool> panels = std::make_shared<PanelPool>();
+    // the small device / pinned buffers of the last finished solve (lobpcg.cu)
+    std::shared_ptr<void> solver_keep;
     ~Ctx();
 };
 

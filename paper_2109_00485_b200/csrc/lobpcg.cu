@@ -43,6 +43,20 @@ std::vector<double> random_block(index_t n, index_t nb, std::uint64_t seed, inde
     return x;
 }
 
+// the small device / pinned buffers a finished solve leaves on its context
+struct Keep {
+    int nb = 0;
+    std::int64_t partials_len = 0;
+    DBuf<double> small, partials;
+    DBuf<dla::Status> st;
+    DBuf<std::int64_t> fallbacks;
+    dla::Sygv sygv;
+    void* hm = nullptr;  // pinned Solver::Mirror
+    ~Keep() {
+        if (hm) cudaFreeHost(hm);
+    }
+};
+
 struct Events {
     cudaEvent_t e[9] = {};
     Events() {
@@ -110,21 +124,25 @@ struct Solver {
             row_lo = op->row_lo;
         }
         const index_t pn = n * nb;
-        for (auto* b : {&X, &W, &P, &HX, &HW, &HP, &R, &Xn, &HXn, &Pn, &HPn}) {  // pooled on the context
-            const index_t need = std::max<index_t>(pn, 1);
-            auto& pool = ctx->panel_pool;
-            auto it = std::find_if(pool.begin(), pool.end(), [&](const DBuf<double>& d) { return d.n >= need; });
-            if (it != pool.end()) {
-                *b = std::move(*it);
-                pool.erase(it);
-            } else {  // nothing fits: the smaller pooled panels are dropped
-                pool.erase(std::remove_if(pool.begin(), pool.end(), [&](const DBuf<double>& d) { return d.n < need; }),
-                           pool.end());
-                b->reset(need);
-            }
-        }
+        for (auto* b : {&X, &W, &P, &HX, &HW, &HP, &R, &Xn, &HXn, &Pn, &HPn})  // pooled on the context
+            *b = ctx->panels->take(std::max<index_t>(pn, 1));
         const index_t nb2 = static_cast<index_t>(nb) * nb, dim = 3 * nb;
-        small.reset(12 * nb2 + 2 * dim * dim + dim * nb + 8 * nb2 + 8 * nb);
+        partials_len = std::max<std::int64_t>(dla::gram_partials_len(nb, 12, ctx->num_sms),
+                                              static_cast<std::int64_t>(ctx->num_sms) * 4 * 2 * nb);
+        // the small buffers of the previous solve on this context, when they fit
+        auto keep = std::static_pointer_cast<Keep>(ctx->solver_keep);
+        ctx->solver_keep.reset();
+        if (keep && keep->nb == nb && keep->partials_len == partials_len) {
+            small = std::move(keep->small);
+            partials = std::move(keep->partials);
+            st = std::move(keep->st);
+            fallbacks = std::move(keep->fallbacks);
+            sygv = std::move(keep->sygv);
+            hm = static_cast<Mirror*>(keep->hm);
+            keep->hm = nullptr;
+        }
+        keep.reset();
+        if (!small.p) small.reset(12 * nb2 + 2 * dim * dim + dim * nb + 8 * nb2 + 8 * nb);
         double* p = small.get();
         blocks = p; p += 12 * nb2;
         G = p; p += dim * dim;
@@ -141,21 +159,31 @@ struct Solver {
         xn2 = p; p += nb;
         shifts = p; p += nb;
         pn2 = p; p += nb;
-        partials_len = std::max<std::int64_t>(dla::gram_partials_len(nb, 12, ctx->num_sms),
-                                              static_cast<std::int64_t>(ctx->num_sms) * 4 * 2 * nb);
-        partials.reset(partials_len);
-        st.reset(1);
-        fallbacks.reset(1);
+        if (!partials.p) partials.reset(partials_len);
+        if (!st.p) st.reset(1);
+        if (!fallbacks.p) fallbacks.reset(1);
         BE_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(dla::Status), s));
         BE_CUDA(cudaMemsetAsync(fallbacks.get(), 0, sizeof(std::int64_t), s));
-        BE_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hm), sizeof(Mirror)));
+        if (!hm) BE_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hm), sizeof(Mirror)));
         sygv.ensure(ctx, dim);
     }
     ~Solver() {
-        if (hm) cudaFreeHost(hm);
-        if (cudaStreamSynchronize(s) == cudaSuccess)  // (the panels may still be in use by queued work otherwise)
-            for (auto* b : {&X, &W, &P, &HX, &HW, &HP, &R, &Xn, &HXn, &Pn, &HPn})
-                if (b->p) ctx->panel_pool.push_back(std::move(*b));
+        if (cudaStreamSynchronize(s) != cudaSuccess) {  // queued work may still use the buffers: plain release
+            if (hm) cudaFreeHost(hm);
+            return;
+        }
+        for (auto* b : {&X, &W, &P, &HX, &HW, &HP, &R, &Xn, &HXn, &Pn, &HPn}) ctx->panels->give(std::move(*b));
+        auto keep = std::make_shared<Keep>();
+        keep->nb = nb;
+        keep->partials_len = partials_len;
+        keep->small = std::move(small);
+        keep->partials = std::move(partials);
+        keep->st = std::move(st);
+        keep->fallbacks = std::move(fallbacks);
+        keep->sygv = std::move(sygv);
+        keep->hm = hm;
+        hm = nullptr;
+        ctx->solver_keep = std::move(keep);
     }
 
     void sync_status() {
@@ -446,7 +474,8 @@ struct Solver {
         res.converged = converged;
         res.lambda.assign(th.begin(), th.begin() + k);
         res.device = ctx->device;
-        res.xdev.reset(std::max<index_t>(n * k, 1));
+        res.pool = ctx->panels;
+        res.xdev = ctx->panels->take(std::max<index_t>(n * k, 1));
         if (n > 0)
             BE_CUDA(cudaMemcpy2DAsync(res.xdev.get(), static_cast<std::size_t>(k) * 8, X.get(),
                                       static_cast<std::size_t>(nb) * 8, static_cast<std::size_t>(k) * 8,
@@ -484,21 +513,24 @@ std::unique_ptr<Result> lobpcg_solve(Ctx* ctx, Op* op, be_host_operator_fn host_
     res->k = cfg.k;
     using clk = std::chrono::steady_clock;
     const auto t0 = clk::now();
-    Solver sv(ctx, n, nb, cfg.k, op, host_op, host_user, tiles, cfg, *res);
-    sv.observer = observer;
-    sv.observer_user = observer_user;
+    auto sv = std::make_unique<Solver>(ctx, n, nb, cfg.k, op, host_op, host_user, tiles, cfg, *res);
+    sv->observer = observer;
+    sv->observer_user = observer_user;
     const auto t1 = clk::now();
-    sv.init(x0);
-    BE_CUDA(cudaStreamSynchronize(sv.s));
+    sv->init(x0);
+    BE_CUDA(cudaStreamSynchronize(sv->s));
     const auto t2 = clk::now();
-    sv.iterate(cfg.maxiter);
+    sv->iterate(cfg.maxiter);
     const auto t3 = clk::now();
-    sv.finish();
+    sv->finish();
     const auto t4 = clk::now();
-    if (sv.trace_segments) {
+    const bool trace = sv->trace_segments;
+    sv.reset();
+    const auto t5 = clk::now();
+    if (trace) {
         auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-        std::fprintf(stderr, "[be] solve ms: setup %.1f init %.1f iterate %.1f finish %.1f\n", ms(t0, t1), ms(t1, t2),
-                     ms(t2, t3), ms(t3, t4));
+        std::fprintf(stderr, "[be] solve ms: setup %.1f init %.1f iterate %.1f finish %.1f teardown %.1f\n", ms(t0, t1),
+                     ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, t5));
     }
     return res;
 }

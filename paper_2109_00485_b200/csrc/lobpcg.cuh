@@ -22,7 +22,14 @@ struct Result {  // SolveResult + ConvergenceHistory, lobpcg.hpp:68-80
     int nb = 0, k = 0;
     std::vector<double> lambda, x;
     int device = 0;
-    DBuf<double> xdev;  // the n x k eigenvector block, kept on the device until read (x stays empty then)
+    DBuf<double> xdev;
+    std::shared_ptr<PanelPool> pool;  // xdev goes back here when the result is freed
+    Result() = default;
+    Result(const Result&) = delete;
+    Result& operator=(const Result&) = delete;
+    ~Result() {
+        if (pool && xdev.p) pool->give(std::move(xdev));  // (no CUDA call: the pool keeps it)
+    }  // the n x k eigenvector block, kept on the device until read (x stays empty then)
     std::vector<IterRecord> records;
     std::int64_t operator_calls = 0, precond_fallbacks = 0;
     int restarts = 0;
