@@ -1106,8 +1106,52 @@ __global__ void __launch_bounds__(kT) k_residual(const double* __restrict__ hx, 
                                                  std::int64_t n, double* __restrict__ partial, int mode) {
     // mode 0: r = hx - x*theta, sums of r^2 and x^2; mode 1: sums of x^2 only
     __shared__ double red[2][kT];
-    const int rpi = kT / nb;  // rows per iteration
     const int tid = threadIdx.x;
+    if (nb == 16) {  // 16-byte accesses: thread = (row, column pair)
+        constexpr int CP = 8, RPI = kT / CP;
+        const int cp = tid % CP, rl = tid / CP;
+        double sr0 = 0.0, sr1 = 0.0, sx0 = 0.0, sx1 = 0.0;
+        const double th0 = mode == 0 ? theta[2 * cp] : 0.0, th1 = mode == 0 ? theta[2 * cp + 1] : 0.0;
+        for (std::int64_t row = blockIdx.x * static_cast<std::int64_t>(RPI) + rl; row < n;
+             row += static_cast<std::int64_t>(gridDim.x) * RPI) {
+            const double2 xv = reinterpret_cast<const double2*>(x + row * 16)[cp];
+            sx0 += xv.x * xv.x;
+            sx1 += xv.y * xv.y;
+            if (mode == 0) {
+                const double2 hv = reinterpret_cast<const double2*>(hx + row * 16)[cp];
+                const double r0 = hv.x - th0 * xv.x, r1 = hv.y - th1 * xv.y;
+                reinterpret_cast<double2*>(r + row * 16)[cp] = make_double2(r0, r1);
+                sr0 += r0 * r0;
+                sr1 += r1 * r1;
+            }
+        }
+        // the 4 row groups of a warp (lanes 8 apart) by butterfly, then red[.][warp * 16 + column]
+        for (int o = 8; o < 32; o <<= 1) {
+            sr0 += __shfl_xor_sync(0xffffffffu, sr0, o);
+            sr1 += __shfl_xor_sync(0xffffffffu, sr1, o);
+            sx0 += __shfl_xor_sync(0xffffffffu, sx0, o);
+            sx1 += __shfl_xor_sync(0xffffffffu, sx1, o);
+        }
+        const int lane = tid & 31, warp = tid >> 5;
+        if (lane < CP) {
+            red[0][warp * 16 + 2 * cp] = sr0;
+            red[0][warp * 16 + 2 * cp + 1] = sr1;
+            red[1][warp * 16 + 2 * cp] = sx0;
+            red[1][warp * 16 + 2 * cp + 1] = sx1;
+        }
+        __syncthreads();
+        if (tid < 16) {
+            double a = 0.0, b = 0.0;
+            for (int q = 0; q < kT / 32; ++q) {
+                a += red[0][q * 16 + tid];
+                b += red[1][q * 16 + tid];
+            }
+            partial[(static_cast<std::int64_t>(blockIdx.x) * 2 + 0) * 16 + tid] = a;
+            partial[(static_cast<std::int64_t>(blockIdx.x) * 2 + 1) * 16 + tid] = b;
+        }
+        return;
+    }
+    const int rpi = kT / nb;  // rows per iteration
     const int c = tid % nb, rl = tid / nb;
     double s_r = 0.0, s_x = 0.0;
     if (rl < rpi) {

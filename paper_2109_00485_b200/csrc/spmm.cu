@@ -521,7 +521,8 @@ __global__ void k_finish_f64(const double* __restrict__ d, const double* __restr
             const float2 y = reinterpret_cast<const float2*>(y32)[e];
             double2 out;
             if (symmetric) {
-                const double dr = d[(2u * e) / unb];
+                const std::uint32_t row = (unb & (unb - 1)) == 0 ? (2u * e) >> (__ffs(unb) - 1) : (2u * e) / unb;
+                const double dr = d[row];
                 const double2 x = reinterpret_cast<const double2*>(X)[e];
                 out = make_double2(dr * x.x + static_cast<double>(y.x), dr * x.y + static_cast<double>(y.y));
             } else {
