@@ -998,7 +998,7 @@ __global__ void __launch_bounds__(kT) k_trsm(double* __restrict__ w0, double* __
 // Block-cooperative floored Cholesky (densela.hpp:103-121 / 155-175): upper R
 // with B = R^T R. floored=false reproduces cholesky() (pivot must be > 0).
 // Returns the failing pivot index or -1. All threads of the CTA participate.
-__device__ int dev_chol(const double* B, double* R, int n, double rel_floor, bool floored) {
+__device__ int dev_chol_g(const double* B, double* R, int n, double rel_floor, bool floored) {
     __shared__ double s_floor, s_rjj;
     __shared__ int s_fail;
     if (threadIdx.x == 0) {
@@ -1031,6 +1031,56 @@ __device__ int dev_chol(const double* B, double* R, int n, double rel_floor, boo
         __syncthreads();
     }
     return -1;
+}
+
+// The same factorisation on shared-memory copies for n <= kCholS (the
+// per-step pivot sums then read shared memory, not L2): identical arithmetic.
+constexpr int kCholS = 48;
+__device__ int dev_chol(const double* B, double* R, int n, double rel_floor, bool floored) {
+    if (n > kCholS) return dev_chol_g(B, R, n, rel_floor, floored);
+    __shared__ double sB[kCholS * kCholS], sR[kCholS * kCholS];
+    __shared__ double s_floor, s_rjj;
+    __shared__ int s_fail;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        sB[e] = B[e];
+        sR[e] = 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double dmax = 0.0;
+        for (int i = 0; i < n; ++i) dmax = fmax(dmax, fabs(sB[i * n + i]));
+        s_floor = floored ? rel_floor * fmax(dmax, 1e-300) : 0.0;
+        s_fail = -1;
+    }
+    __syncthreads();
+    int fail_at = -1;
+    for (int j = 0; j < n; ++j) {
+        if (threadIdx.x == 0) {
+            double piv = sB[j * n + j];
+            for (int k = 0; k < j; ++k) piv -= sR[j * n + k] * sR[j * n + k];
+            if (!(piv > s_floor)) {
+                s_fail = j;
+            } else {
+                s_rjj = sqrt(piv);
+                sR[j * n + j] = s_rjj;
+            }
+        }
+        __syncthreads();
+        if (s_fail >= 0) {
+            fail_at = s_fail;
+            break;
+        }
+        const double rjj = s_rjj;
+        for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) {
+            double sacc = sB[i * n + j];  // B(j, i)
+            for (int k = 0; k < j; ++k) sacc -= sR[j * n + k] * sR[i * n + k];
+            sR[i * n + j] = sacc / rjj;  // R(j, i)
+        }
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) R[e] = sR[e];
+    __syncthreads();
+    return fail_at;
 }
 
 __global__ void k_qr_chol(double* B, double* R, int nb, Status* st) {
