@@ -766,6 +766,18 @@ def host_array(shape) -> np.ndarray:
     return np.frombuffer(mm, dtype=np.float64, count=count).reshape(shape)
 
 
+def _x0_checked(x0, n, k, nb):
+    """X0 must be n x nb (nb = k + 3 when 0), as lobpcg_solve checks
+    (lobpcg.hpp:308-310): the C side reads n*nb doubles from the pointer."""
+    if x0 is None:
+        return None
+    x0a = np.ascontiguousarray(x0, dtype=np.float64)
+    nb_eff = nb or k + 3
+    if x0a.ndim != 2 or x0a.shape != (int(n), int(nb_eff)):
+        raise DimensionMismatch(f"lobpcg_solve: X0 must be n x nb ({n} x {nb_eff}), got {x0a.shape}")
+    return x0a
+
+
 def lobpcg(ctx: Context, op=None, n=None, tiles: Tiles | None = None, x0=None, k=5, nb=0, tol=1e-6, maxiter=500,
            fom_iterations=4, seed=1234, observer=None, observer_state=False, host_operator=None):
     """lobpcg_solve (lobpcg.hpp:291-456) on the device. `op` is an Operator;
@@ -774,7 +786,7 @@ def lobpcg(ctx: Context, op=None, n=None, tiles: Tiles | None = None, x0=None, k
     if n is None:
         n = op.info().nrows
     cfg = SolverConfig(k, nb, tol, maxiter, fom_iterations, seed, 1 if observer_state else 0)
-    x0a = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)
+    x0a = _x0_checked(x0, n, k, nb)
     obs_cb = OBSERVER_FN()
     if observer is not None:
         def _obs(user, it, nn, nbb, th, rn, nc, x, hx):
@@ -860,7 +872,7 @@ class IncrementalSolve:
         if n is None:
             n = op.info().nrows
         self.cfg = SolverConfig(k, nb, tol, maxiter, fom_iterations, seed, 0)
-        self._x0 = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)
+        self._x0 = _x0_checked(x0, n, k, nb)
         self._h = C.c_void_p()
         check(lib().be_lobpcg_begin(ctx.handle, op.handle if op is not None else None, HOST_OP_FN(), None,
                                     C.c_int64(n), tiles.handle if tiles is not None else None, _p(self._x0),

@@ -2,6 +2,7 @@
 // library's Failure (and CUDA/std errors) and turns it into a be_status with a
 // thread-local message, mirroring the exception taxonomy of errors.hpp.
 #include <cuda_runtime.h>
+#include <cublas_v2.h>
 #include <cusolverDn.h>
 
 #include <cstring>
@@ -287,6 +288,7 @@ be_status be_ctx_destroy(be_ctx* ctx) {
     return guard([&] {
         if (!ctx) return;
         if (ctx->impl->solver) cusolverDnDestroy(ctx->impl->solver);
+        if (ctx->impl->blas) cublasDestroy(ctx->impl->blas);
         if (ctx->impl->stream) cudaStreamDestroy(ctx->impl->stream);
         delete ctx;
     });

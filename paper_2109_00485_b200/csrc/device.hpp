@@ -75,6 +75,7 @@ struct PanelPool {
 struct Ctx {
     int device = 0;
     int num_sms = 0;
+    int nsmid = 0;  // %nsmid (upper bound of %smid; may exceed num_sms), queried on first use
     cudaStream_t stream = nullptr;
     cusolverDnContext* solver = nullptr;
     cublasContext* blas = nullptr;  // triangular solves of the 3nb x 3nb pencil

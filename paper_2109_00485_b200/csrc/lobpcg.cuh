@@ -23,12 +23,15 @@ struct Result {  // SolveResult + ConvergenceHistory, lobpcg.hpp:68-80
     std::vector<double> lambda, x;
     int device = 0;
     DBuf<double> xdev;
-    std::shared_ptr<PanelPool> pool;  // xdev goes back here when the result is freed
+    // xdev goes back to the context's pool when the result is freed; a weak reference, so a result
+    // outliving its context does not keep the context's pooled panels allocated (xdev is freed then)
+    std::weak_ptr<PanelPool> pool;
     Result() = default;
     Result(const Result&) = delete;
     Result& operator=(const Result&) = delete;
     ~Result() {
-        if (pool && xdev.p) pool->give(std::move(xdev));  // (no CUDA call: the pool keeps it)
+        if (!xdev.p) return;
+        if (auto p = pool.lock()) p->give(std::move(xdev));  // (no CUDA call: the pool keeps it)
     }  // the n x k eigenvector block, kept on the device until read (x stays empty then)
     std::vector<IterRecord> records;
     std::int64_t operator_calls = 0, precond_fallbacks = 0;

@@ -804,6 +804,27 @@ constexpr int kClassThreads[] = {32, 128, 256, 256, BE_FOM_C4_NT};
 constexpr bool kClassVsm[] = {true, true, true, false, false};  // whole basis in shared memory
 constexpr std::size_t kStageBudget = 200 * 1024;  // current vector + staged entries per CTA
 
+
+__global__ void k_nsmid(int* out) {
+    unsigned v;
+    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(v));
+    *out = static_cast<int>(v);
+}
+
+// Scratch slots are indexed by %smid, which PTX bounds by %nsmid, not by the
+// multiprocessor count (floorswept / MIG parts can have holes in the SM ids).
+int smid_bound(Ctx* ctx, cudaStream_t cs) {
+    if (ctx->nsmid <= 0) {
+        DBuf<int> d(1);
+        k_nsmid<<<1, 1, 0, cs>>>(d.get());
+        int h = 0;
+        BE_CUDA(cudaMemcpyAsync(&h, d.get(), sizeof(int), cudaMemcpyDeviceToHost, cs));
+        BE_CUDA(cudaStreamSynchronize(cs));
+        ctx->nsmid = std::max(h, ctx->num_sms);
+    }
+    return ctx->nsmid;
+}
+
 }  // namespace
 
 std::unique_ptr<Tiles> tiles_create(Ctx* ctx, const be_csb_view& L, const double* diag, const index_t* off_all,
@@ -1002,14 +1023,15 @@ void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, i
         std::size_t sm = vbytes + static_cast<std::size_t>(stage_cap) * 10;
         const unsigned grid = static_cast<unsigned>((b1 - b0) * ngroups);
         int kslots = 1;
+        const int nslot_sm = smid_bound(t->ctx, cs);
         auto slots_for = [&](const void* kern, int nt) {  // resident CTAs per SM = scratch slots per SM
             int per = 0;
             BE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, nt, sm));
             kslots = std::max(1, std::min(per, 32));
-            const index_t vneed = static_cast<index_t>(mc) * t->ctx->num_sms * kslots * dmax * C;
+            const index_t vneed = static_cast<index_t>(mc) * nslot_sm * kslots * dmax * C;
             if (t->vscratch[c].n < vneed) t->vscratch[c].reset(vneed);
-            if (t->slot_mask[c].n < t->ctx->num_sms) {
-                t->slot_mask[c].reset(t->ctx->num_sms);
+            if (t->slot_mask[c].n < nslot_sm) {
+                t->slot_mask[c].reset(nslot_sm);
                 BE_CUDA(cudaMemsetAsync(t->slot_mask[c].get(), 0, t->slot_mask[c].bytes(), cs));
             }
         };

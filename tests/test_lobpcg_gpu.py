@@ -303,4 +303,9 @@ def test_repeated_solves_reuse_the_context_panels(ctx):
     assert np.max(np.abs(a["lambda_"] - b["lambda_"]) / np.abs(a["lambda_"])) < 1e-10
     assert np.max(np.abs(a["x"] - b["x"])) < 1e-6
     big2 = abi.lobpcg(ctx, opb, x0=x0, k=8, nb=16, tol=1e-300, maxiter=3, seed=3)
-    assert np.max(np.abs(big["x"] - big2["x"])) < 1e-8
+    # f32 values + an unordered red.global transpose pass: the two runs agree to f32 rounding
+    # amplified by three unconverged iterations, so compare the spanned subspaces (singular values
+    # of X1^T X2 are the cosines of the principal angles) and the Ritz values, not bits
+    cos = np.linalg.svd(big["x"].T @ big2["x"], compute_uv=False)
+    assert 1.0 - cos.min() < 1e-6, cos
+    assert np.max(np.abs(big["lambda_"] - big2["lambda_"]) / np.abs(big["lambda_"])) < 1e-6
