@@ -106,6 +106,10 @@ be_status be_csb_build(const be_triple* triples, int64_t count, int64_t nrows, i
 /* uniform_boundaries (csb.hpp:89-96); *count receives nblk + 1. out may be
  * NULL to query the count. */
 be_status be_uniform_boundaries(int64_t n, int64_t extent, int64_t* out, int64_t* count);
+/* random_block (block_vector.hpp:47-53): rows [row_lo, row_lo + n) of the
+ * reference's mt19937_64(seed) U(-1, 1) n_global x nb block, row-major; the
+ * solver's X0 / restart blocks (bit-identical to the reference's). */
+be_status be_random_block(int64_t n, int64_t nb, uint64_t seed, int64_t row_lo, double* out);
 be_status be_csb_view_get(const be_csb* m, be_csb_view* view);
 /* is_strictly_lower (csb.hpp:188-202) on any view; *result = 0/1 */
 be_status be_csb_is_strictly_lower(const be_csb_view* view, int* result);

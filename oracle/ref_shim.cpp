@@ -253,6 +253,14 @@ int ref_lobpcg(const void* view, const double* diag, const index_t* off, index_t
     });
 }
 
+// random_block (block_vector.hpp:47-53), the reference's own
+int ref_random_block(index_t n, index_t nb, std::uint64_t seed, double* out) {
+    return guarded([&] {
+        const BlockVector b = random_block(n, nb, seed);
+        std::copy(b.data.begin(), b.data.end(), out);
+    });
+}
+
 // ---- persistent problem for timing loops (bench.py cpu_baseline) ----------
 void* ref_prepare(const void* view, const double* diag, const index_t* off, index_t noff, int threads) {
     try {

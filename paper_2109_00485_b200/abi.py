@@ -316,6 +316,14 @@ def as_triples(rows, cols, values) -> np.ndarray:
     return t
 
 
+def random_block(n: int, nb: int, seed: int, row_lo: int = 0) -> np.ndarray:
+    """random_block (block_vector.hpp:47-53): rows [row_lo, row_lo + n) of the
+    reference's mt19937_64 U(-1, 1) block -- the solver's X0."""
+    out = np.zeros((n, nb))
+    check(lib().be_random_block(C.c_int64(n), C.c_int64(nb), C.c_uint64(seed), C.c_int64(row_lo), _p(out)))
+    return out
+
+
 def uniform_boundaries(n: int, extent: int) -> np.ndarray:
     cnt = C.c_int64(0)
     check(lib().be_uniform_boundaries(C.c_int64(n), C.c_int64(extent), None, C.byref(cnt)))

@@ -76,6 +76,14 @@ be_status be_uniform_boundaries(int64_t n, int64_t extent, int64_t* out, int64_t
     });
 }
 
+be_status be_random_block(int64_t n, int64_t nb, uint64_t seed, int64_t row_lo, double* out) {
+    return guard([&] {
+        if (!out || n < 0 || nb < 1 || row_lo < 0) be::fail(BE_ERR_BAD_PARAMS, "be_random_block: bad argument");
+        const auto x = be::random_block(n, nb, seed, row_lo);
+        std::memcpy(out, x.data(), x.size() * sizeof(double));
+    });
+}
+
 be_status be_csb_view_get(const be_csb* m, be_csb_view* view) {
     return guard([&] {
         if (!m || !view) be::fail(BE_ERR_BAD_PARAMS, "be_csb_view_get: null argument");

@@ -28,13 +28,11 @@
 
 namespace be {
 
-namespace {
-
 // random_block (block_vector.hpp:47-53) rows [row_lo, row_lo + n): the
 // reference's one mt19937_64 stream over the whole n_global x nb block, of
 // which a rank keeps its own rows (multi-GPU X0 / restart blocks match the
 // single-GPU ones bit for bit).
-std::vector<double> random_block(index_t n, index_t nb, std::uint64_t seed, index_t row_lo = 0) {
+std::vector<double> random_block(index_t n, index_t nb, std::uint64_t seed, index_t row_lo) {
     std::vector<double> x(static_cast<std::size_t>(n * nb));
     std::mt19937_64 rng(seed);
     std::uniform_real_distribution<double> u(-1.0, 1.0);
@@ -42,6 +40,9 @@ std::vector<double> random_block(index_t n, index_t nb, std::uint64_t seed, inde
     for (auto& v : x) v = u(rng);
     return x;
 }
+
+namespace {
+
 
 // the small device / pinned buffers a finished solve leaves on its context
 struct Keep {

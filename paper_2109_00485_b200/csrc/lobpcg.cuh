@@ -10,6 +10,10 @@ namespace be {
 
 struct Tiles;
 
+// random_block (block_vector.hpp:47-53): rows [row_lo, row_lo + n) of the reference's
+// mt19937_64 U(-1, 1) block (host; X0 and restart blocks are generated here and copied)
+std::vector<double> random_block(index_t n, index_t nb, std::uint64_t seed, index_t row_lo = 0);
+
 struct IterRecord {  // IterationRecord, lobpcg.hpp:60-66
     int iter = 0;
     std::vector<double> theta, resn;

@@ -1,0 +1,125 @@
+"""LOBPCG parity on the BASELINE.json configs themselves (slow GPU tests).
+
+C1 = configs[0], the reference's own CPU-runnable case: generate_synthetic
+Random, n = 1e5, 5e7 stored lower nonzeros, extent 4000, tiles 4..512, seed 1
+(synth.hpp:33-158), SolverConfig{k = 8, nb = 16, tol = 1e-6, maxiter = 500,
+FOM m = 4, seed = 1} (lobpcg.hpp:24-48), the pattern of
+test_lobpcg.cpp:286-303 (solver vs an independent answer). The reference's
+results on the same bytes are committed in tests/golden/c1_reference.json
+(tests/golden/make_golden_c1.py runs oracle/_ref/libref.so, the unmodified
+reference headers): precondition off 51 iterations under every summation
+order, on 65 (serial) / 66 (8-thread baseline and fused-atomic).
+
+T1 = configs[1] shape (clustered generator, n = 2.9e6, 1.1e9 lower
+nonzeros): the first 10 iterations' Ritz values against the reference's
+(tests/golden/t1_reference.json, tests/golden/make_golden_t1.py).
+
+Bars (BASELINE.json north star): eigenvalues within 1e-6 relative; the same
+iteration count +-1 with the preconditioner off, and +-1 of the reference's
+own summation-order envelope with it on.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2109_00485_b200 import abi
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+def digest(m, diag):
+    h = hashlib.sha256()
+    for a in (m.block_nnz, m.block_nnz_offsets, m.local_rows, m.local_cols, m.values, diag):
+        h.update(memoryview(np.ascontiguousarray(a)).cast("B"))
+    return h.hexdigest()
+
+
+@pytest.fixture(scope="module")
+def c1():
+    g = json.loads((GOLD / "c1_reference.json").read_text())
+    n = g["n"]
+    s = abi.Synthetic("random", n=n, density=g["density"], block_extent=g["extent"], seed=g["seed"])
+    b = abi.uniform_boundaries(n, g["extent"])
+    m = abi.build_csb_coo(s.lower, n, n, b, b)
+    # the library's generator + CSB build reproduce the reference's bytes at full C1 size
+    assert m.nnz == g["nnz"] and len(s.tile_offsets) - 1 == g["ntiles"]
+    assert digest(m, s.diag) == g["csb_sha256"]
+    return g, m, s
+
+
+def _runs(g, tag):
+    return {k.split("_", 1)[1]: v for k, v in g["runs"].items() if k.startswith(tag + "_")}
+
+
+@pytest.mark.parametrize("values", ["f32", "f64"])
+def test_c1_precond_off_matches_reference(ctx, c1, values):
+    g, m, s = c1
+    ref = _runs(g, "off")
+    op = abi.Operator(ctx, m, s.diag, values_prec=abi.BE_F32 if values == "f32" else abi.BE_F64)
+    got = abi.lobpcg(ctx, op, k=g["k"], nb=g["nb"], tol=g["tol"], maxiter=g["maxiter"], fom_iterations=g["fom_m"],
+                     seed=g["seed"])
+    assert got["converged"]
+    want_it = {r["iterations"] for r in ref.values()}
+    assert want_it == {51}
+    assert abs(got["iterations"] - 51) <= 1, got["iterations"]
+    lam = np.array(ref["serial"]["lambda_"])
+    rel = np.max(np.abs(got["lambda_"] - lam) / np.abs(lam))
+    assert rel <= 1e-6, rel
+    # the trajectory: Ritz values of the first 10 iterations
+    th = np.array(ref["serial"]["theta_first10"])
+    relth = np.max(np.abs(got["theta"][:10] - th) / np.abs(th))
+    assert relth <= 1e-6, relth
+    assert got["operator_calls"] == got["iterations"] + 1
+    op.close()
+
+
+@pytest.mark.parametrize("values", ["f64", "f32"])
+def test_c1_precond_on_within_reference_envelope(ctx, c1, values):
+    g, m, s = c1
+    ref = _runs(g, "on")
+    lo = min(r["iterations"] for r in ref.values())
+    hi = max(r["iterations"] for r in ref.values())
+    assert (lo, hi) == (65, 66)
+    op = abi.Operator(ctx, m, s.diag, values_prec=abi.BE_F32 if values == "f32" else abi.BE_F64)
+    tiles = abi.Tiles(ctx, m, s.diag, s.tile_offsets)
+    got = abi.lobpcg(ctx, op, tiles=tiles, k=g["k"], nb=g["nb"], tol=g["tol"], maxiter=g["maxiter"],
+                     fom_iterations=g["fom_m"], seed=g["seed"])
+    assert got["converged"]
+    lam = np.array(ref["serial"]["lambda_"])
+    rel = np.max(np.abs(got["lambda_"] - lam) / np.abs(lam))
+    assert rel <= 1e-6, rel
+    if values == "f64":  # the parity mode for the chaotic precond-on count
+        assert lo - 1 <= got["iterations"] <= hi + 1, (got["iterations"], lo, hi)
+    else:  # f32 values: reported, bounded loosely (SURVEY 8c measured 67-69 with fp32 emulation)
+        assert lo - 1 <= got["iterations"] <= hi + 5, (got["iterations"], lo, hi)
+    tiles.close()
+    op.close()
+
+
+def test_t1_ritz_trace_matches_reference(ctx):
+    path = GOLD / "t1_reference.json"
+    if not path.exists():
+        pytest.skip("t1_reference.json not generated")
+    g = json.loads(path.read_text())
+    m, diag, toff = abi.generate_clustered(**g["params"])
+    assert m.nnz == g["nnz"]
+    assert digest(m, diag) == g["csb_sha256"]
+    op = abi.Operator(ctx, m, diag, values_prec=abi.BE_F32)
+    tiles = abi.Tiles(ctx, m, diag, toff)
+    it = g["iterations"]
+    got = abi.lobpcg(ctx, op, tiles=tiles, k=g["k"], nb=g["nb"], tol=1e-300, maxiter=it, fom_iterations=g["fom_m"],
+                     seed=g["seed"])
+    assert got["iterations"] == it and got["operator_calls"] == g["operator_calls"]
+    th = np.array(g["theta"])
+    rel = np.abs(got["theta"] - th) / np.abs(th)
+    # the wanted (lowest k) Ritz values track the reference's to 1e-6 every iteration
+    assert np.max(rel[:, :g["k"]]) <= 1e-6, np.max(rel[:, :g["k"]], axis=1)
+    tiles.close()
+    op.close()
