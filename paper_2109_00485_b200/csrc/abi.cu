@@ -5,7 +5,10 @@
 #include <cublas_v2.h>
 #include <cusolverDn.h>
 
+#include <algorithm>
 #include <cstring>
+#include <tuple>
+#include <vector>
 #include <string>
 
 #include "comm.hpp"
@@ -378,7 +381,7 @@ be_status be_op_get_info(const be_op* op, be_op_info* info) {
         info->ncols = o->ncols;
         info->nnz = o->nnz;
         info->ntiles = o->ntiles;
-        info->device_bytes = static_cast<int64_t>(o->tiles.bytes() + o->lens.bytes() + o->runs.bytes() + o->vals.bytes() + o->rc.bytes() + o->cperm.bytes());
+        info->device_bytes = static_cast<int64_t>(o->tiles.bytes() + o->runs.bytes() + o->runs_ext.bytes() + o->blobs.bytes());
         info->bytes_per_nnz_x1000 = o->nnz ? info->device_bytes * 1000 / o->nnz : 0;
         info->values_prec = o->values_prec;
         info->tile_rows = be::kTile;
@@ -391,74 +394,81 @@ be_status be_op_decode(be_op* op, int64_t* rows, int64_t* cols, double* values, 
     return guard([&] {
         if (!op) be::fail(BE_ERR_BAD_PARAMS, "null argument");
         auto* o = op->impl.get();
-        if (o->csb_index.size() != static_cast<std::size_t>(o->padded))
+        if (o->csb_index.size() != static_cast<std::size_t>(o->padded) || (o->padded == 0 && o->nnz > 0))
             be::fail(BE_ERR_BAD_PARAMS, "be_op_decode: source index not retained for matrices this large");
         std::vector<be::TileHdr> h(static_cast<std::size_t>(o->ntiles));
-        std::vector<std::uint16_t> rc(static_cast<std::size_t>(o->padded)), cp(static_cast<std::size_t>(o->padded));
+        std::vector<unsigned char> blob(static_cast<std::size_t>(o->blob_total));
         const std::size_t vsz = o->values_prec == BE_F32 ? 4 : 8;
-        std::vector<unsigned char> v(static_cast<std::size_t>(o->padded) * vsz);
-        std::vector<unsigned char> lens(static_cast<std::size_t>(o->ntiles) * 256);
         if (o->ntiles > 0) {
-            BE_CUDA(cudaMemcpy(lens.data(), o->lens.get(), lens.size(), cudaMemcpyDeviceToHost));
             BE_CUDA(cudaMemcpy(h.data(), o->tiles.get(), h.size() * sizeof(be::TileHdr), cudaMemcpyDeviceToHost));
-            BE_CUDA(cudaMemcpy(rc.data(), o->rc.get(), rc.size() * 2, cudaMemcpyDeviceToHost));
-            BE_CUDA(cudaMemcpy(cp.data(), o->cperm.get(), cp.size() * 2, cudaMemcpyDeviceToHost));
-            BE_CUDA(cudaMemcpy(v.data(), o->vals.get(), v.size(), cudaMemcpyDeviceToHost));
+            BE_CUDA(cudaMemcpy(blob.data(), o->blobs.get(), blob.size(), cudaMemcpyDeviceToHost));
         }
-        int64_t p = 0;
+        auto val = [&](const unsigned char* p) {
+            if (vsz == 4) {
+                float f;
+                std::memcpy(&f, p, 4);
+                return static_cast<double>(f);
+            }
+            double d;
+            std::memcpy(&d, p, 8);
+            return d;
+        };
+        // Blob layout (spmm.cu): meta 1056 B = jr u16[136] | jc u16[136] | rank->row u8[128] |
+        // rank->col u8[128] | row lengths | column lengths; then values + columns in row-JDS
+        // order and values + rows in column-JDS order, npad = nnz rounded up to 16 each.
+        // Both orders are validated (ranks by decreasing length, starts = prefix sums of
+        // min(len, d), both orders the same entry set); entries come out in row order.
+        int64_t p = 0, slot = 0;
         for (const auto& t : h) {
-            const int64_t b = static_cast<int64_t>(t.begin8) * 8;
-            const int nnz = static_cast<int>(t.packed >> 14);
+            const int nnz = static_cast<int>(t.packed >> 14), npad = (nnz + 15) & ~15;
             const int nr = static_cast<int>(t.packed & 127u) + 1;
             const int nc = static_cast<int>((t.packed >> 7) & 127u) + 1;
-            // JDS layout: row rank r's j-th entry sits at jd[j] + r and column
-            // rank c's j-th entry at cperm[cjd[j] + c]; every rank must map to
-            // one row (column) and cperm must be a permutation of the entries
-            const unsigned char* ln = lens.data() + static_cast<std::size_t>(&t - h.data()) * 256;
-            std::vector<char> seen(static_cast<std::size_t>(nnz), 0);
+            const unsigned char* b = blob.data() + static_cast<std::size_t>(t.begin16) * 16;
+            const std::uint16_t* jd[2] = {reinterpret_cast<const std::uint16_t*>(b), reinterpret_cast<const std::uint16_t*>(b + 272)};
+            const unsigned char* perm[2] = {b + 544, b + 672};
+            const unsigned char* len[2] = {b + 800, b + 928};
+            const unsigned char* sv[2] = {b + 1056, b + 1056 + static_cast<std::size_t>(npad) * (vsz + 1)};
+            const unsigned char* si[2] = {b + 1056 + static_cast<std::size_t>(npad) * vsz,
+                                          b + 1056 + static_cast<std::size_t>(npad) * (2 * vsz + 1)};
+            std::vector<std::tuple<int, int, std::uint64_t>> got[2];
             for (int g = 0; g < 2; ++g) {
-                int sum = 0, start = 0;
+                int sum = 0;
+                std::vector<char> used(128, 0);
                 for (int i = 0; i < 128; ++i) {
-                    if (i > 0 && ln[g * 128 + i] > ln[g * 128 + i - 1]) be::fail(BE_ERR_GENERIC, "decode: lengths not in rank order");
-                    sum += ln[g * 128 + i];
+                    if (i > 0 && len[g][i] > len[g][i - 1]) be::fail(BE_ERR_GENERIC, "decode: lengths not in rank order");
+                    if (used[perm[g][i]]) be::fail(BE_ERR_GENERIC, "decode: rank map is not a permutation");
+                    used[perm[g][i]] = 1;
+                    sum += len[g][i];
                 }
                 if (sum != nnz) be::fail(BE_ERR_GENERIC, "decode: lengths do not sum to the tile size");
-                std::vector<int> who(128, -1);
-                for (int j = 0; j < ln[g * 128]; ++j) {
-                    int cnt = 0;
-                    while (cnt < 128 && ln[g * 128 + cnt] > j) ++cnt;
-                    for (int r = 0; r < cnt; ++r) {
-                        int q = start + r;
-                        if (g == 1) {
-                            q = cp[static_cast<std::size_t>(b + q)];
-                            if (q >= nnz || seen[static_cast<std::size_t>(q)]) be::fail(BE_ERR_GENERIC, "decode: bad column permutation");
-                            seen[static_cast<std::size_t>(q)] = 1;
+                for (int d = 0; d <= 128; ++d) {
+                    int s = 0;
+                    for (int i = 0; i < 128; ++i) s += std::min<int>(len[g][i], d);
+                    if (jd[g][d] != s) be::fail(BE_ERR_GENERIC, "decode: JDS starts inconsistent with the lengths");
+                }
+                for (int r = 0; r < 128; ++r)
+                    for (int d = 0; d < len[g][r]; ++d) {
+                        const int q = jd[g][d] + r;
+                        const int other = si[g][q];
+                        const int row = g == 0 ? perm[g][r] : other, col = g == 0 ? other : perm[g][r];
+                        if (row >= nr || col >= nc) be::fail(BE_ERR_GENERIC, "decode: local index outside tile");
+                        std::uint64_t bits = 0;
+                        const double v = val(sv[g] + static_cast<std::size_t>(q) * vsz);
+                        std::memcpy(&bits, &v, 8);
+                        got[g].emplace_back(row, col, bits);
+                        if (g == 0) {
+                            if (rows) rows[p] = o->comm ? o->unpad(t.row0 + row) : t.row0 + row;
+                            if (cols) cols[p] = o->comm ? o->unpad(t.col0 + col) : t.col0 + col;
+                            if (values) values[p] = v;
+                            if (csb_index) csb_index[p] = o->csb_index[static_cast<std::size_t>(slot + q)];
+                            ++p;
                         }
-                        const std::uint16_t x = rc[static_cast<std::size_t>(b + q)];
-                        const int id = g == 0 ? (x >> 8) : (x & 255);
-                        if (who[static_cast<std::size_t>(r)] < 0) who[static_cast<std::size_t>(r)] = id;
-                        if (who[static_cast<std::size_t>(r)] != id) be::fail(BE_ERR_GENERIC, g == 0 ? "decode: row order split" : "decode: column order split");
                     }
-                    start += cnt;
-                }
             }
-            for (int k = 0; k < nnz; ++k) {
-                const std::uint16_t x = rc[static_cast<std::size_t>(b + k)];
-                if ((x >> 8) >= nr || (x & 255) >= nc) be::fail(BE_ERR_GENERIC, "decode: local index outside tile");
-                if (rows) rows[p] = o->comm ? o->unpad(t.row0 + (x >> 8)) : t.row0 + (x >> 8);
-                if (cols) cols[p] = o->comm ? o->unpad(t.col0 + (x & 255)) : t.col0 + (x & 255);
-                if (values) {
-                    if (vsz == 4) {
-                        float f;
-                        std::memcpy(&f, v.data() + static_cast<std::size_t>(b + k) * 4, 4);
-                        values[p] = f;
-                    } else {
-                        std::memcpy(values + p, v.data() + static_cast<std::size_t>(b + k) * 8, 8);
-                    }
-                }
-                if (csb_index) csb_index[p] = o->csb_index[static_cast<std::size_t>(b + k)];
-                ++p;
-            }
+            std::sort(got[0].begin(), got[0].end());
+            std::sort(got[1].begin(), got[1].end());
+            if (got[0] != got[1]) be::fail(BE_ERR_GENERIC, "decode: row and column orders hold different entries");
+            slot += npad;
         }
         if (p != o->nnz) be::fail(BE_ERR_GENERIC, "decode: entry count mismatch");
     });

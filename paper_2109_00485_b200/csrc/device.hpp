@@ -89,9 +89,9 @@ struct Ctx {
 };
 
 // One device work tile: <= kTile rows x <= kTile cols of the lower triangle,
-// <= max_nnz entries, entries row-sorted. 16 bytes.
+// <= max_nnz entries; its data is one 16-byte aligned blob (spmm.cu). 16 bytes.
 struct TileHdr {
-    std::uint32_t begin8;  // entry offset / 8 (segments are 8-aligned)
+    std::uint32_t begin16;  // blob byte offset / 16
     std::int32_t row0;     // first global row of the 128-row tile-row
     std::int32_t col0;     // first global column
     std::uint32_t packed;  // (nr-1) | (nc-1) << 7 | nnz << 14; nr = rows of the tile-row
@@ -117,14 +117,13 @@ struct Op {
     DBuf<TileHdr> tiles;
     DBuf<int2> runs;                 // [tile_begin, tile_end) work items
     index_t nruns = 0;
-    DBuf<unsigned char> lens;        // 256 per tile: row / column lengths in rank order
-    DBuf<unsigned char> vals;        // float or double, rank-ordered rows within tile
-    DBuf<std::uint16_t> rc;          // (local row << 8) | local col
-    DBuf<std::uint16_t> cperm;       // column-order -> row-order position in tile
+    DBuf<unsigned char> blobs;       // per tile: JDS meta + row-order and column-order entry streams
+    index_t blob_total = 0;          // bytes of all blobs
+    int blob_max = 0;                // bytes of the largest possible blob (one stage buffer)
     DBuf<double> diag;               // nrows (symmetric only)
     DBuf<int> counter;               // persistent-kernel tile counter [2]
     DBuf<float> x32, y32;            // f32 staging of f64 panels (f32-values operator)
-    std::vector<std::int64_t> csb_index;  // device order -> CSB index (small matrices only)
+    std::vector<std::int64_t> csb_index;  // row-order device slot -> CSB index, -1 = padding (small matrices only)
     int grid = 0;
     // multi-GPU (row e): panel rows are owned in contiguous segments
     // [cuts[q], cuts[q+1]); tile coordinates live in the padded index space

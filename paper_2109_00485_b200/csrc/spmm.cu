@@ -2,38 +2,50 @@
 //
 // Replaces SymmetricOperator::apply (kernels.hpp:357-371) = out.set_zero +
 // spmm_notrans (kernels.hpp:290) + spmm_trans (kernels.hpp:302) + the
-// diagonal pass (kernels.hpp:363-370). The reference reads every stored
-// nonzero twice (once per pass); this kernel reads it once from HBM and
-// applies it twice (A_ij X_j -> Y_i and A_ij X_i -> Y_j).
+// diagonal pass (kernels.hpp:363-370). The reference walks the stored
+// nonzeros twice (once per pass); this kernel streams every 128 x 128 work
+// tile from HBM once and applies each entry twice (A_ij X_j -> Y_i and
+// A_ij X_i -> Y_j).
 //
-// Device format ("work tiles", built on upload from the CSB arrays):
-//   every CSB block is cut into 128 x 128 sub-tiles aligned to the block
-//   origin (a sub-tile with more than max_nnz entries is split by rows);
-//   tiles are ordered by global tile-row. Per entry the HBM stream holds the
-//   value (f32 or f64) + rc (u16: local row << 8 | local col) + cperm (u16:
-//   column-order permutation): 4 + 2 + 2 = 8 bytes per stored nonzero in f32,
-//   the reference's own "f32 value + 2 x u16" budget. Inside
-//   a tile the rows are ordered by decreasing length (rank order) and so are
-//   the columns of the column order; 256 bytes of per-tile row/column lengths
-//   (u8, rank order) complete the format.
+// Device format ("work tiles", built on upload from the CSB arrays): every
+// CSB block is cut into 128 x 128 sub-tiles aligned to the block origin (a
+// sub-tile with more than max_nnz entries is split by rows). Each tile is ONE
+// contiguous, 16-byte aligned blob, fetched with a single cp.async.bulk:
+//   meta (1056 B): row-JDS starts jr[129] | column-JDS starts jc[129] (u16,
+//     padded to 136) | rank -> local row (u8[128]) | rank -> local column |
+//     row lengths by rank | column lengths by rank
+//   row stream:    values[npad] (f32 or f64) | local column u8[npad]
+//   column stream: values[npad]              | local row    u8[npad]
+// "JDS" = jagged diagonals: diagonal d holds the d-th entry of every row
+// (column) rank whose length exceeds d, ranks sorted by decreasing length, so
+// lane r of a warp reads word jr[d] + r -- consecutive words, one shared-
+// memory wavefront per 32 entries, in both passes (no indirection). In f32
+// that is 10 B per stored entry (the value is stored once per pass order).
 //
-// Kernel: persistent CTAs of 256 threads pull work items ("runs": up to 32
-//   consecutive tiles of one tile-row) from an atomic counter. Per run the
-//   CTA stages X_I once (f32, in smem) and accumulates Y_I in smem; per tile
-//   it stages X_J and the entry stream (coalesced loads, one round trip).
-//   Warps 0-3 then run pass R (Y_I += A X_J: one lane per row rank, all nb
-//   columns in registers) while warps 4-7 run pass C (Y_J += A^T X_I: one
-//   lane per column rank, flushed with REDG.E.ADD.F32x4). Rank order keeps
-//   the 32 lanes of a warp on rows of similar length (little divergence). X
-//   rows live in 128-byte smem lines holding 128 / (nb * 4) replicas; lane L
-//   reads its 16-byte chunks in the rotated order (i + L) % CH from replica
-//   (L / CH) % REP, so the 8 lanes of every quarter-warp phase hit 8 distinct
-//   bank groups whatever rows they gather.
+// Kernel: persistent CTAs of 256 threads (2 per SM) pull work items ("runs":
+// up to 32 consecutive tiles of one tile-row inside one L2 column band) from
+// an atomic counter, and run the next tile's blob (bulk copy, mbarrier) and
+// X_J rows (registers) one tile ahead, across run boundaries, so one
+// __syncthreads per tile remains. Per run X_I is staged once and Y_I
+// accumulates in shared memory. Warps 0-3 run pass R (Y_I += A X_J: lane =
+// row rank, all nb columns in registers), warps 4-7 pass C (Y_J += A^T X_I:
+// lane = column rank, flushed with red.global.add.v4.f32). X rows live in
+// 128-byte smem lines holding 128 / (nb * 4) replicas; lane L reads its
+// 16-byte chunks in the rotated order (i + L) % CH from replica (L / CH) %
+// REP, so the 8 lanes of every quarter-warp phase hit 8 distinct bank groups
+// whatever rows they gather. Row ranks are assigned so that lanes L and L + 4
+// of a quarter-warp own rows of opposite parity where lengths allow, which
+// makes the Y_I read-modify-write conflict-free too (64-byte rows at nb = 16).
+//
+// Runs are ordered by L2 column band (about 64 MB of f32 X_J and Y_J rows per
+// band), so the gathered X_J rows and the reduced Y_J rows of one band stay
+// L2-resident while every tile-row that touches the band streams past.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <type_traits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -41,30 +53,23 @@
 
 #include "comm.hpp"
 #include "device.hpp"
+#include "stream.cuh"
 
 namespace be {
 
 namespace {
 
-#ifndef BE_SPMM_STAGES
-#define BE_SPMM_STAGES 1  // tile staging buffers per CTA (1: copy/compute overlap comes from the other CTAs of the SM)
-#endif
 constexpr int kThreads = 256;
 constexpr index_t kRunMax = 32;  // tiles per work item
 
-template <typename TC>
-struct Meta;
-template <>
-struct __align__(8) Meta<float> {
-    float v;
-    std::uint32_t off;  // low 16: byte offset of the X_J line, high 16: of the X_I line
-};
-template <>
-struct __align__(16) Meta<double> {
-    double v;
-    std::uint32_t off;
-    std::uint32_t pad;
-};
+// blob layout (bytes)
+constexpr int kMetaJr = 0, kMetaJc = 272, kMetaRperm = 544, kMetaCperm = 672, kMetaRlen = 800, kMetaClen = 928;
+constexpr int kMetaBytes = 1056;
+__host__ __device__ constexpr int pad16(int n) { return (n + 15) & ~15; }
+template <typename TV>
+__host__ __device__ constexpr std::size_t blob_bytes(int nnz) {
+    return kMetaBytes + static_cast<std::size_t>(pad16(nnz)) * (2 * sizeof(TV) + 2);
+}
 
 template <typename TC>
 struct Vec;
@@ -147,11 +152,7 @@ struct XGeom {
     static constexpr int VEC = Vec<TC>::N;                          // elements per 16-byte chunk
     static constexpr int CH = NBP / VEC;                            // chunks per row
     static constexpr int RB = NBP * static_cast<int>(sizeof(TC));  // row bytes
-#ifdef BE_SPMM_NOREP
-    static constexpr int LINEB = RB;                                // one copy per row line
-#else
     static constexpr int LINEB = RB < 128 ? 128 : RB;               // bytes per smem row line
-#endif
     static constexpr int REP = LINEB / RB;                          // replicas per line
     static_assert(NBP % VEC == 0 && CH >= 1, "bad NBP");
 };
@@ -159,12 +160,12 @@ struct XGeom {
 // Stage rows [row0, row0 + nr) of X (TX, row-major, nb columns) into the
 // replicated smem lines; all loads of a batch are in flight together.
 template <int NBP, typename TC, typename TX>
-__device__ __forceinline__ void stage_x(unsigned char* xs, const TX* __restrict__ X, int row0, int nr, int nb) {
+__device__ __forceinline__ void stage_x(unsigned char* xs, const TX* __restrict__ X, int row0, int nr, int nb, int ld) {
     using G = XGeom<NBP, TC>;
-    const TX* src = X + static_cast<std::int64_t>(row0) * nb;
+    const TX* src = X + static_cast<std::int64_t>(row0) * ld;
     constexpr int EPC = 16 / sizeof(TX);  // TX elements per 16-byte chunk
     if constexpr ((NBP * sizeof(TX)) % 16 == 0) {
-        if (nb == NBP) {
+        if (nb == NBP && ld == NBP) {
             constexpr int CPR = NBP / EPC;  // global chunks per row
             const int total = nr * CPR;
             constexpr int PER = 4;
@@ -202,275 +203,315 @@ __device__ __forceinline__ void stage_x(unsigned char* xs, const TX* __restrict_
     const int total = nr * NBP;
     for (int e = threadIdx.x; e < total; e += kThreads) {
         const int r = e / NBP, v = e - r * NBP;
-        const TC x = v < nb ? static_cast<TC>(__ldg(src + static_cast<std::int64_t>(r) * nb + v)) : TC(0);
+        const TC x = v < nb ? static_cast<TC>(__ldg(src + static_cast<std::int64_t>(r) * ld + v)) : TC(0);
         TC* line = reinterpret_cast<TC*>(xs + r * G::LINEB);
 #pragma unroll
         for (int q = 0; q < G::REP; ++q) line[q * NBP + v] = x;
     }
 }
 
-// cp.async 16-byte global -> shared copy (LDGSTS), and its group fences
-__device__ __forceinline__ void cp16(void* dst, const void* src) {
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-// Raw per-tile staging area (one of two pipeline stages): the entry stream
-// in JDS order, the column permutation, the X_J rows and the rank lengths.
-template <int NBP, typename TC, typename TV, typename TX>
-struct Stage {
-    // raw X_J rows (staged asynchronously when small; else loaded directly)
-    static constexpr int XRAW = kTile * NBP * static_cast<int>(sizeof(TX));
-#ifndef BE_SPMM_XRAW_MAX
-#define BE_SPMM_XRAW_MAX 0  // X_J rows staged raw with the tile (cp.async) up to this size (0: loaded into the lines directly, which frees the smem for a third CTA per SM)
-#endif
-    static constexpr int XB = XRAW <= BE_SPMM_XRAW_MAX ? XRAW : 0;
-    __host__ __device__ static std::size_t bytes(int max_nnz) {
-        return static_cast<std::size_t>(max_nnz) * (sizeof(TV) + 4) + XB + 256;
+// X_J rows of the next tile, held in registers while the current tile is
+// computed (fast path: TX == TC, nb == NBP, 16-byte aligned X).
+template <int NBP, typename TC>
+struct XPre {
+    static constexpr int CPR = NBP * static_cast<int>(sizeof(TC)) / 16;
+    static constexpr int PER = (kTile * CPR + kThreads - 1) / kThreads;
+    uint4 v[PER];
+    __device__ __forceinline__ void load(const TC* __restrict__ X, int row0, int nr) {
+        const uint4* src = reinterpret_cast<const uint4*>(X + static_cast<std::int64_t>(row0) * NBP);
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int c = threadIdx.x + i * kThreads;
+            if (c < nr * CPR) v[i] = __ldg(src + c);
+        }
+    }
+    __device__ __forceinline__ void store(unsigned char* xs, int nr) const {
+        using G = XGeom<NBP, TC>;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int c = threadIdx.x + i * kThreads;
+            if (c < nr * CPR) {
+                const int r = c / CPR, v0 = (c % CPR) * (16 / static_cast<int>(sizeof(TC)));
+                TC* line = reinterpret_cast<TC*>(xs + r * G::LINEB);
+#pragma unroll
+                for (int q = 0; q < G::REP; ++q) *reinterpret_cast<uint4*>(line + ((q + r) % G::REP) * NBP + v0) = v[i];
+            }
+        }
     }
 };
 
-// Issue the asynchronous copies of one tile into a stage buffer.
-template <int NBP, typename TC, typename TV, typename TX>
-__device__ __forceinline__ void stage_issue(unsigned char* st, int max_nnz, const TileHdr& h, int t,
-                                            const unsigned char* __restrict__ lens, const TV* __restrict__ vals,
-                                            const std::uint16_t* __restrict__ rc,
-                                            const std::uint16_t* __restrict__ cperm, const TX* __restrict__ X,
-                                            int nb, bool do_r, bool do_c, bool xvec) {
-    const std::int64_t b = static_cast<std::int64_t>(h.begin8) * 8;
-    const int nnz = static_cast<int>(h.packed >> 14);
-    const int nc = static_cast<int>((h.packed >> 7) & 127u) + 1;
-    const int npad = (nnz + 7) & ~7;
-    TV* sv = reinterpret_cast<TV*>(st);
-    std::uint16_t* src = reinterpret_cast<std::uint16_t*>(sv + max_nnz);
-    std::uint16_t* scp = src + max_nnz;
-    unsigned char* sx = reinterpret_cast<unsigned char*>(scp + max_nnz);
-    unsigned char* sl = sx + Stage<NBP, TC, TV, TX>::XB;
-    const int cv = npad * static_cast<int>(sizeof(TV)) / 16, cr = npad * 2 / 16;
-    const int cx = (do_r && xvec) ? nc * nb * static_cast<int>(sizeof(TX)) / 16 : 0;
-    const int total = cv + cr + (do_c ? cr : 0) + cx + 16;
-    const unsigned char* gx = reinterpret_cast<const unsigned char*>(X + static_cast<std::int64_t>(h.col0) * nb);
-    for (int c = threadIdx.x; c < total; c += kThreads) {
-        int q = c;
-        if (q < cv) { cp16(reinterpret_cast<unsigned char*>(sv) + 16 * q, reinterpret_cast<const unsigned char*>(vals + b) + 16 * q); continue; }
-        q -= cv;
-        if (q < cr) { cp16(reinterpret_cast<unsigned char*>(src) + 16 * q, reinterpret_cast<const unsigned char*>(rc + b) + 16 * q); continue; }
-        q -= cr;
-        if (do_c) {
-            if (q < cr) { cp16(reinterpret_cast<unsigned char*>(scp) + 16 * q, reinterpret_cast<const unsigned char*>(cperm + b) + 16 * q); continue; }
-            q -= cr;
-        }
-        if (q < cx) { cp16(sx + 16 * q, gx + 16 * q); continue; }
-        q -= cx;
-        cp16(sl + 16 * q, lens + static_cast<std::int64_t>(t) * 256 + 16 * q);
-    }
-}
-
-// JDS starts: for the 128 ranks of one group (rows or columns) with lengths
-// sorted in decreasing order, jd[j] = sum_r min(len_r, j) for j in [0, 128].
-// Threads 0-127 build the row table, 128-255 the column table.
-__device__ __forceinline__ void jds_starts(const unsigned char* sl, std::uint16_t* jd_r, std::uint16_t* jd_c,
-                                           int* s_tot) {
-    // threads 0-255 work (every thread of the CTA passes the barrier)
-    const int tid = threadIdx.x, grp = (tid >> 7) & 1, j = tid & 127, lane = tid & 31, warp = tid >> 5;
-    const unsigned char* len = sl + grp * 128;
-    int cnt = 0, incl = 0;
-    if (tid < 256) {
-        int lo = 0, hi = 128;  // count_j = #ranks with len > j (lengths are non-increasing)
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (len[mid] > j) lo = mid + 1; else hi = mid;
-        }
-        cnt = lo;
-        incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        if (lane == 31) s_tot[warp] = incl;
-    }
-    __syncthreads();
-    if (tid < 256) {
-        int start = incl - cnt;
-        for (int w = grp * 4; w < warp; ++w) start += s_tot[w];
-        std::uint16_t* jd = grp == 0 ? jd_r : jd_c;
-        jd[j] = static_cast<std::uint16_t>(start);
-        if (j == 127) jd[128] = static_cast<std::uint16_t>(start + cnt);
-    }
-}
-
-// One work item = a run of consecutive tiles of the same 128-row tile-row.
-// Per run the X_I slice is staged once (replicated lines) and Y_I rows
-// accumulate in shared memory; per tile, the raw stream of tile t + 1 is
-// copied with cp.async while tile t is computed. Pass R (warps 0-3): lane =
-// row rank, walks its row through the JDS table; pass C (warps 4-7): lane =
-// column rank, walks its column through cperm. Y_J is flushed per tile.
-template <int NBP, typename TC, typename TV, typename TX>
-#ifndef BE_SPMM_MINB32
-#define BE_SPMM_MINB32 3  // CTAs per SM for 17 <= nb <= 64 (f32): 80 registers
-#endif
-#ifndef BE_SPMM_MINB
-#define BE_SPMM_MINB 4  // CTAs per SM (nb <= 16, f32): 64 registers, 55 KB smem
-#endif
-__global__ void __launch_bounds__(kThreads, sizeof(TC) == 4 ? (NBP <= 16 ? BE_SPMM_MINB : BE_SPMM_MINB32) : 1)
-    k_sym_spmm(const int2* __restrict__ runs, int nruns, const TileHdr* __restrict__ tiles,
-               const unsigned char* __restrict__ lens, const TV* __restrict__ vals,
-               const std::uint16_t* __restrict__ rc, const std::uint16_t* __restrict__ cperm,
-               const TX* __restrict__ X, TX* __restrict__ Y, int nb, int do_r, int do_c, int max_nnz,
-               int* __restrict__ ctr) {
+// One pass of one tile: lane = rank (row rank for pass R, column rank for
+// pass C); walks diagonals [d_begin, len) of its jagged row (column) through
+// the JDS starts, gathering the matching X line of the other side for every
+// entry. Full groups of U entries are branch-free, so the U index / value
+// reads and the U x CH gathers of a group are all in flight together.
+template <int NBP, typename TC, typename TV>
+__device__ __forceinline__ void jds_walk(const std::uint16_t* __restrict__ jd, int d_begin, int len, int rank,
+                                         const TV* __restrict__ sv, const unsigned char* __restrict__ sidx,
+                                         const unsigned char* __restrict__ xbase, const int* coff,
+                                         typename Vec<TC>::T* acc) {
     using G = XGeom<NBP, TC>;
     using V = typename Vec<TC>::T;
-    using S = Stage<NBP, TC, TV, TX>;
-    extern __shared__ __align__(16) unsigned char smem[];
-    unsigned char* xi = smem;
-    unsigned char* xj = xi + kTile * G::LINEB;
-    V* yi = reinterpret_cast<V*>(xj + kTile * G::LINEB);  // kTile x CH chunks: the run's Y_I rows
-    unsigned char* stg0 = reinterpret_cast<unsigned char*>(yi + kTile * G::CH);
-    const std::size_t sbytes = (S::bytes(max_nnz) + 15) & ~static_cast<std::size_t>(15);
-    __shared__ __align__(8) std::uint16_t s_jd[2][136];  // read 4 starts at a time
-    __shared__ int s_run;
-    __shared__ int s_tot[8];
+    constexpr int U = G::CH <= 4 ? 4 : (G::CH <= 8 ? 2 : 1);
+    int d = d_begin;  // a multiple of 4: the starts of a group are one broadcast 8-byte read
+    for (; d + U <= len; d += U) {
+        int pos[U];
+        if constexpr (U == 4) {
+            const uint2 q = *reinterpret_cast<const uint2*>(jd + d);
+            pos[0] = static_cast<int>(q.x & 0xffffu) + rank;
+            pos[1] = static_cast<int>(q.x >> 16) + rank;
+            pos[2] = static_cast<int>(q.y & 0xffffu) + rank;
+            pos[3] = static_cast<int>(q.y >> 16) + rank;
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) pos[u] = static_cast<int>(jd[d + u]) + rank;
+        }
+        TC v[U];
+        const unsigned char* p[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            v[u] = static_cast<TC>(sv[pos[u]]);
+            p[u] = xbase + static_cast<int>(sidx[pos[u]]) * G::LINEB;
+        }
+        V xv[U][G::CH];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int i = 0; i < G::CH; ++i) xv[u][i] = *reinterpret_cast<const V*>(p[u] + coff[i]);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int i = 0; i < G::CH; ++i) vfma(acc[i], v[u], xv[u][i]);
+    }
+    for (; d < len; ++d) {
+        const int pos = static_cast<int>(jd[d]) + rank;
+        const TC v = static_cast<TC>(sv[pos]);
+        const unsigned char* p = xbase + static_cast<int>(sidx[pos]) * G::LINEB;
+        V xv[G::CH];
+#pragma unroll
+        for (int i = 0; i < G::CH; ++i) xv[i] = *reinterpret_cast<const V*>(p + coff[i]);
+#pragma unroll
+        for (int i = 0; i < G::CH; ++i) vfma(acc[i], v, xv[i]);
+    }
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// Tail split (load balance inside a pass): ranks are sorted by decreasing
+// length, so the first warp of a pass owns the longest rows (columns). Its
+// diagonals [D, len) -- D stored at jd[130] -- go to the last warp of the pass,
+// which runs them after its own ranks and hands the partial sums over through
+// shared memory (named barrier 1 for pass R, 2 for pass C).
+constexpr int kSplitSlot = 130;
+
+template <int NBP, typename TC, typename TV, typename TX>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_sym_spmm(const int2* __restrict__ runs, int nruns, const TileHdr* __restrict__ tiles,
+               const unsigned char* __restrict__ blobs, const TX* __restrict__ X, TX* __restrict__ Y, int nb, int ld,
+               int do_r, int do_c, int blob_max, int* __restrict__ ctr) {
+    using G = XGeom<NBP, TC>;
+    using V = typename Vec<TC>::T;
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char* xi = smem;                              // X_I lines of the current run
+    unsigned char* xjb = xi + kTile * G::LINEB;            // X_J lines, two buffers
+    V* yi = reinterpret_cast<V*>(xjb + 2 * kTile * G::LINEB);  // kTile x CH chunks: the run's Y_I rows
+    V* tail = yi + kTile * G::CH;                          // 2 x 32 x CH: tail-split partial sums
+    unsigned char* stg = reinterpret_cast<unsigned char*>(tail + 2 * 32 * G::CH);  // two blob buffers
+    __shared__ __align__(8) std::uint64_t bars[2];
+    __shared__ TileHdr s_hdr[2][kRunMax];  // headers of the current and the next run
+    __shared__ int2 s_rg[2];               // their tile ranges (x >= y: no run)
+    __shared__ int s_pend;                 // id of the run after next (its headers are fetched during this run)
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
+    const int warp = tid >> 5;
     const int grp = tid >> 7;  // 0: pass R (row ranks), 1: pass C (column ranks)
     const int rank = tid & 127;
-    const bool vec_ok = (nb % G::VEC) == 0;
-    const bool xvec = S::XB > 0 && nb == NBP && (NBP * sizeof(TX)) % 16 == 0 &&
-                      (reinterpret_cast<std::uintptr_t>(X) & 15u) == 0;
-    const unsigned char* xbase = (grp == 0 ? xj : xi) + ((lane / G::CH) % G::REP) * G::RB;
+    const int wq = warp & 3;   // warp of the pass
+    const bool vec_ok = (nb % G::VEC) == 0 && (ld % G::VEC) == 0 && (reinterpret_cast<std::uintptr_t>(Y) & 15u) == 0;
+    const bool fast_x = sizeof(TC) == sizeof(TX) && nb == NBP && ld == NBP && (NBP * sizeof(TX)) % 16 == 0 &&
+                        (reinterpret_cast<std::uintptr_t>(X) & 15u) == 0;
+    const unsigned char* xrep = ((lane / G::CH) % G::REP) * G::RB + (grp == 0 ? xjb : xi);
+    const unsigned char* xrep_c = ((lane / G::CH) % G::REP) * G::RB + xi;
     int coff[G::CH];
 #pragma unroll
     for (int i = 0; i < G::CH; ++i) coff[i] = ((i + lane) % G::CH) * 16;
+    std::uint64_t policy;  // the blob stream is read once: keep the X / Y bands in L2 instead
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
 
-    if (tid == 0) s_run = atomicAdd(ctr, 1);
+    // a run's range and headers (warp 0): load into registers, store into the cache later
+    auto fetch_run = [&](int id, int2& rg, TileHdr& hd) {
+        rg = id < nruns ? runs[id] : make_int2(0, 0);
+        if (lane < rg.y - rg.x) hd = tiles[rg.x + lane];
+    };
+    auto store_run = [&](int slot, const int2& rg, const TileHdr& hd) {
+        if (lane == 0) s_rg[slot] = rg;
+        if (lane < rg.y - rg.x) s_hdr[slot][lane] = hd;
+    };
+    if (warp == 0) {
+        int id0 = 0, id1 = 0, id2 = 0;
+        if (lane == 0) {
+            stream::mbar_init(&bars[0], 1);
+            stream::mbar_init(&bars[1], 1);
+            stream::mbar_init_fence();
+            id0 = atomicAdd(ctr, 1);
+            id1 = id0 < nruns ? atomicAdd(ctr, 1) : nruns;
+            id2 = id1 < nruns ? atomicAdd(ctr, 1) : nruns;
+            s_pend = id2;
+        }
+        id0 = __shfl_sync(0xffffffffu, id0, 0);
+        id1 = __shfl_sync(0xffffffffu, id1, 0);
+        int2 r0, r1;
+        TileHdr h0, h1;
+        fetch_run(id0, r0, h0);
+        fetch_run(id1, r1, h1);
+        store_run(0, r0, h0);
+        store_run(1, r1, h1);
+    }
     __syncthreads();
-    int run = s_run;
-    while (run < nruns) {
-        const int2 rg = runs[run];
-        TileHdr h = tiles[rg.x];
-        const int row0 = h.row0;
-        const int nr = static_cast<int>(h.packed & 127u) + 1;
-        stage_issue<NBP, TC, TV, TX>(stg0, max_nnz, h, rg.x, lens, vals, rc, cperm, X, nb, do_r, do_c, xvec);
-        cp_commit();
-        if (do_c) stage_x<NBP, TC, TX>(xi, X, row0, nr, nb);
-        if (do_r)
-            for (int e = tid; e < kTile * G::CH; e += kThreads) vzero(yi[e]);
-        for (int t = rg.x; t < rg.y; ++t) {
-            unsigned char* st = stg0 + (BE_SPMM_STAGES == 2 ? ((t - rg.x) & 1) * sbytes : 0);
-            const int nc = static_cast<int>((h.packed >> 7) & 127u) + 1;
-            const int col0 = h.col0;
-            cp_wait_all();
-            __syncthreads();  // stage t complete and visible; stage t+1's buffer is free
-            if (BE_SPMM_STAGES == 2 && t + 1 < rg.y) {
-                h = tiles[t + 1];
-                stage_issue<NBP, TC, TV, TX>(stg0 + ((t + 1 - rg.x) & 1) * sbytes, max_nnz, h, t + 1, lens, vals, rc,
-                                             cperm, X, nb, do_r, do_c, xvec);
+    int cur = 0;  // run-cache slot of the current run
+    int2 rg = s_rg[0];
+    if (rg.x < rg.y) {
+        int t = rg.x;
+        auto issue = [&](const TileHdr& hh, int slot) {  // one thread: the blob of a tile -> stage slot
+            const std::uint32_t bytes = static_cast<std::uint32_t>(blob_bytes<TV>(static_cast<int>(hh.packed >> 14)));
+            stream::fence_proxy_async();
+            stream::mbar_arrive_expect_tx(&bars[slot], bytes);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                    stream::smem_u32(stg + slot * blob_max)),
+                "l"(blobs + static_cast<std::size_t>(hh.begin16) * 16), "r"(bytes), "r"(stream::smem_u32(&bars[slot])),
+                "l"(policy)
+                : "memory");
+        };
+        {  // first tile of the first run: synchronous staging
+            const TileHdr h0 = s_hdr[0][0];
+            if (tid == 0) issue(h0, 0);
+            if (do_r) stage_x<NBP, TC, TX>(xjb, X, h0.col0, static_cast<int>((h0.packed >> 7) & 127u) + 1, nb, ld);
+            if (do_c) stage_x<NBP, TC, TX>(xi, X, h0.row0, static_cast<int>(h0.packed & 127u) + 1, nb, ld);
+            if (do_r)
+                for (int e = tid; e < kTile * G::CH; e += kThreads) vzero(yi[e]);
+        }
+        std::uint32_t phase = 0;  // bit s: parity of stage s's next completion
+        int s = 0;
+        int2 prg = make_int2(0, 0);  // warp 0: the run after next, fetched during this run
+        TileHdr phd{};
+        bool run_start = true;
+        for (;;) {
+            stream::mbar_wait(&bars[s], (phase >> s) & 1u);
+            phase ^= 1u << s;
+            __syncthreads();  // blob t, X_J(t), X_I, Y_I, run cache visible; stage s^1 and X_J buffer s^1 free
+            if (run_start && warp == 0) fetch_run(s_pend, prg, phd);
+            run_start = false;
+            const TileHdr h = s_hdr[cur][t - rg.x];
+            int tn = -1;
+            TileHdr hn{};
+            if (t + 1 < rg.y) {
+                tn = t + 1;
+                hn = s_hdr[cur][t + 1 - rg.x];
+            } else if (s_rg[cur ^ 1].x < s_rg[cur ^ 1].y) {
+                tn = s_rg[cur ^ 1].x;
+                hn = s_hdr[cur ^ 1][0];
             }
-            cp_commit();
-            if (t == rg.y - 1 && tid == 0) s_run = atomicAdd(ctr, 1);  // next run
-            const TV* sv = reinterpret_cast<const TV*>(st);
-            const std::uint16_t* src = reinterpret_cast<const std::uint16_t*>(sv + max_nnz);
-            const std::uint16_t* scp = src + max_nnz;
-            const unsigned char* sx = reinterpret_cast<const unsigned char*>(scp + max_nnz);
-            const unsigned char* sl = sx + S::XB;
-            if (do_r) {  // X_J lines from the raw rows
-                if (xvec) {
-                    for (int e = tid; e < nc * NBP; e += kThreads) {
-                        const int r = e / NBP, v = e % NBP;
-                        const TC x = static_cast<TC>(reinterpret_cast<const TX*>(sx)[e]);
-                        TC* line = reinterpret_cast<TC*>(xj + r * G::LINEB);
-#pragma unroll
-                        for (int q = 0; q < G::REP; ++q) line[q * NBP + v] = x;
-                    }
-                } else {
-                    stage_x<NBP, TC, TX>(xj, X, col0, nc, nb);
-                }
+            XPre<NBP, TC> pre, prei;
+            const bool run_end = t == rg.y - 1;
+            if (tn >= 0) {
+                if (tid == 0) issue(hn, s ^ 1);
+                if (do_r && fast_x)
+                    pre.load(reinterpret_cast<const TC*>(X), hn.col0, static_cast<int>((hn.packed >> 7) & 127u) + 1);
+                if (run_end && do_c && fast_x)  // the next run's X_I, stored after the end-of-run barrier
+                    prei.load(reinterpret_cast<const TC*>(X), hn.row0, static_cast<int>(hn.packed & 127u) + 1);
             }
-            jds_starts(sl, s_jd[0], s_jd[1], s_tot);
-            __syncthreads();
-            const int len = sl[grp * 128 + rank];
-            const bool active = len > 0 && (grp == 0 ? do_r : do_c);
+            // ---- compute tile t
             {
-                const std::uint16_t* jd = s_jd[grp];
-                V acc[G::CH];
+                const unsigned char* st = stg + s * blob_max;
+                const int npad = pad16(static_cast<int>(h.packed >> 14));
+                if (grp == 0 ? do_r : do_c) {
+                    const std::uint16_t* jd = reinterpret_cast<const std::uint16_t*>(st + (grp == 0 ? kMetaJr : kMetaJc));
+                    const unsigned char* lens = st + (grp == 0 ? kMetaRlen : kMetaClen);
+                    const TV* sv = reinterpret_cast<const TV*>(st + kMetaBytes + (grp == 0 ? 0 : npad * (static_cast<int>(sizeof(TV)) + 1)));
+                    const unsigned char* sx = st + kMetaBytes + npad * (grp == 0 ? static_cast<int>(sizeof(TV)) : 2 * static_cast<int>(sizeof(TV)) + 1);
+                    const unsigned char* xb = grp == 0 ? xrep + s * kTile * G::LINEB : xrep_c;
+                    const int split = jd[kSplitSlot];                  // tail of warp 0's ranks: diagonals [split, len)
+                    const bool has_tail = split < lens[0];
+                    const int len = lens[rank];
+                    V acc[G::CH];
 #pragma unroll
-                for (int i = 0; i < G::CH; ++i) vzero(acc[i]);
-                int first = 0;
-#ifndef BE_SPMM_UNR
-#define BE_SPMM_UNR 4
-#endif
-                // the pass is warp-uniform: one copy of the walk per pass (no per-entry selects)
-                auto walk = [&](auto pass) {
-                    constexpr int GP = decltype(pass)::value;
-                    for (int j0 = 0; j0 < len; j0 += BE_SPMM_UNR) {
-                        int st4[4];  // starts j0 .. j0 + BE_SPMM_UNR - 1 in one shared-memory read
-                        if constexpr (BE_SPMM_UNR == 4) {
-                            const uint2 q4 = *reinterpret_cast<const uint2*>(jd + j0);
-                            st4[0] = q4.x & 0xffffu, st4[1] = q4.x >> 16, st4[2] = q4.y & 0xffffu, st4[3] = q4.y >> 16;
-                        } else if constexpr (BE_SPMM_UNR == 2) {
-                            const unsigned q2 = *reinterpret_cast<const unsigned*>(jd + j0);
-                            st4[0] = q2 & 0xffffu, st4[1] = q2 >> 16;
+                    for (int i = 0; i < G::CH; ++i) vzero(acc[i]);
+                    jds_walk<NBP, TC, TV>(jd, 0, wq == 0 ? min(len, split) : len, rank, sv, sx, xb, coff, acc);
+                    auto out = [&](int rk, V* a) {  // Y_I += A X_J (row rk) / Y_J += A^T X_I (column rk)
+                        if (grp == 0) {
+                            V* y = yi + static_cast<int>(st[kMetaRperm + rk]) * G::CH;
+#pragma unroll
+                            for (int i = 0; i < G::CH; ++i) vadd(y[(i + lane) % G::CH], a[i]);
                         } else {
-                            st4[0] = jd[j0];
+                            TX* y = Y + static_cast<std::int64_t>(h.col0 + st[kMetaCperm + rk]) * ld;
+#pragma unroll
+                            for (int i = 0; i < G::CH; ++i) {
+                                const int c0 = ((i + lane) % G::CH) * G::VEC;
+                                if (c0 < nb) flush<TX>(y + c0, a[i], nb - c0, vec_ok);
+                            }
                         }
+                    };
+                    V* tl = tail + (grp * 32 + lane) * G::CH;
+                    if (wq == 3) {
+                        if (len > 0) out(rank, acc);
+                        if (has_tail) {  // the tail of ranks 0..31, handed to warp 0 of the pass
+                            const int l0 = lens[lane];
 #pragma unroll
-                        for (int u = 0; u < BE_SPMM_UNR; ++u) {
-                            if (j0 + u >= len) break;
-                            int pos = st4[u] + rank;
-                            if constexpr (GP == 1) pos = scp[pos];
-                            const TC v = static_cast<TC>(sv[pos]);
-                            const std::uint32_t x = src[pos];
-                            if (j0 + u == 0) first = x;
-                            const unsigned char* p = xbase + (GP == 0 ? (x & 255u) : (x >> 8)) * G::LINEB;
-                            V xv[G::CH];
+                            for (int i = 0; i < G::CH; ++i) vzero(acc[i]);
+                            jds_walk<NBP, TC, TV>(jd, split, l0, lane, sv, sx, xb, coff, acc);
 #pragma unroll
-                            for (int i = 0; i < G::CH; ++i) xv[i] = *reinterpret_cast<const V*>(p + coff[i]);
-#pragma unroll
-                            for (int i = 0; i < G::CH; ++i) vfma(acc[i], v, xv[i]);
+                            for (int i = 0; i < G::CH; ++i) tl[(i + lane) % G::CH] = acc[i];  // rotated: conflict-free
+                            __threadfence_block();
+                            named_bar_arrive(1 + grp, 64);
                         }
-                    }
-                };
-                if (active) {
-                    if (grp == 0) walk(std::integral_constant<int, 0>{});
-                    else walk(std::integral_constant<int, 1>{});
-                }
-                if (active) {
-                    if (grp == 0) {  // Y_I += A X_J for this row
-                        V* y = yi + (first >> 8) * G::CH;
+                    } else {
+                        if (wq == 0 && has_tail) {
+                            named_bar_sync(1 + grp, 64);
 #pragma unroll
-                        for (int i = 0; i < G::CH; ++i) vadd(y[(i + lane) % G::CH], acc[i]);
-                    } else {  // Y_J += A^T X_I for this column
-                        TX* y = Y + static_cast<std::int64_t>(col0 + (first & 255)) * nb;
-#pragma unroll
-                        for (int i = 0; i < G::CH; ++i) {
-                            const int c0 = ((i + lane) % G::CH) * G::VEC;
-                            if (c0 < nb) flush<TX>(y + c0, acc[i], nb - c0, vec_ok);
+                            for (int i = 0; i < G::CH; ++i) vadd(acc[i], tl[(i + lane) % G::CH]);
                         }
+                        if (len > 0) out(rank, acc);
                     }
                 }
             }
-            if (BE_SPMM_STAGES == 1 && t + 1 < rg.y) {  // single buffer: refill after everyone is done with it
+            if (tn >= 0 && do_r) {  // X_J of the next tile into the other buffer
+                unsigned char* xn = xjb + (s ^ 1) * kTile * G::LINEB;
+                const int ncn = static_cast<int>((hn.packed >> 7) & 127u) + 1;
+                if (fast_x) pre.store(xn, ncn);
+                else stage_x<NBP, TC, TX>(xn, X, hn.col0, ncn, nb, ld);
+            }
+            if (run_end) {  // end of the run: flush Y_I, stage the next run's X_I, refill the run cache
                 __syncthreads();
-                h = tiles[t + 1];
-                stage_issue<NBP, TC, TV, TX>(stg0, max_nnz, h, t + 1, lens, vals, rc, cperm, X, nb, do_r, do_c, xvec);
-                cp_commit();
+                if (do_r) {
+                    const int nr = static_cast<int>(h.packed & 127u) + 1;
+                    for (int e = tid; e < nr * G::CH; e += kThreads) {
+                        const int row = e / G::CH, c0 = (e % G::CH) * G::VEC;
+                        if (c0 < nb && vnonzero(yi[e]))
+                            flush<TX>(Y + static_cast<std::int64_t>(h.row0 + row) * ld + c0, yi[e], nb - c0, vec_ok);
+                        vzero(yi[e]);
+                    }
+                }
+                if (tn >= 0) {
+                    if (do_c) {
+                        if (fast_x) prei.store(xi, static_cast<int>(hn.packed & 127u) + 1);
+                        else stage_x<NBP, TC, TX>(xi, X, hn.row0, static_cast<int>(hn.packed & 127u) + 1, nb, ld);
+                    }
+                    if (warp == 0) {
+                        store_run(cur, prg, phd);  // the run after next replaces the finished one
+                        if (lane == 0) s_pend = s_pend < nruns ? atomicAdd(ctr, 1) : nruns;
+                    }
+                }
+                cur ^= 1;
+                rg = s_rg[cur];  // (unchanged by the store above: that went to the other slot)
+                run_start = true;
             }
+            if (tn < 0) break;
+            t = tn;
+            s ^= 1;
         }
-        cp_wait_all();
-        __syncthreads();
-        if (do_r) {  // flush the run's rows (all-zero chunks carry no update)
-            for (int e = tid; e < nr * G::CH; e += kThreads) {
-                const int row = e / G::CH, c0 = (e % G::CH) * G::VEC;
-                if (c0 < nb && vnonzero(yi[e]))
-                    flush<TX>(Y + static_cast<std::int64_t>(row0 + row) * nb + c0, yi[e], nb - c0, vec_ok);
-            }
-        }
-        run = s_run;
-        __syncthreads();  // yi / xi / s_run are reused by the next run
     }
     // last CTA out resets the counter for the next launch
     if (tid == 0) {
@@ -544,17 +585,16 @@ __global__ void k_finish_f64(const double* __restrict__ d, const double* __restr
 }
 
 template <int NBP, typename TC, typename TV, typename TX>
-std::size_t smem_bytes(int max_nnz) {
+std::size_t smem_bytes(int blob_max) {
     using G = XGeom<NBP, TC>;
-    const std::size_t sb = (Stage<NBP, TC, TV, TX>::bytes(max_nnz) + 15) & ~static_cast<std::size_t>(15);
-    return 2 * kTile * G::LINEB + kTile * G::CH * 16 + BE_SPMM_STAGES * sb;
+    return 3 * kTile * G::LINEB + (kTile + 64) * G::CH * 16 + 2 * static_cast<std::size_t>(blob_max);
 }
 
 template <int NBP, typename TC, typename TV, typename TX>
-void launch_tiles(Op* op, const int2* runs, index_t nruns, const TX* X, TX* Y, int nb, int do_r, int do_c,
+void launch_tiles(Op* op, const int2* runs, index_t nruns, const TX* X, TX* Y, int nb, int ld, int do_r, int do_c,
                   cudaStream_t s) {
     auto kern = k_sym_spmm<NBP, TC, TV, TX>;
-    const std::size_t sm = smem_bytes<NBP, TC, TV, TX>(op->max_nnz);
+    const std::size_t sm = smem_bytes<NBP, TC, TV, TX>(op->blob_max);
     ensure_dyn_smem(kern, sm);
     int per_sm = 0;
     BE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, sm));
@@ -562,9 +602,8 @@ void launch_tiles(Op* op, const int2* runs, index_t nruns, const TX* X, TX* Y, i
     const int grid = static_cast<int>(std::min<index_t>(static_cast<index_t>(per_sm) * op->ctx->num_sms, nruns));
     op->grid = grid;
     if (grid == 0) return;
-    kern<<<grid, kThreads, sm, s>>>(runs, static_cast<int>(nruns), op->tiles.get(), op->lens.get(),
-                                    reinterpret_cast<const TV*>(op->vals.get()), op->rc.get(), op->cperm.get(), X, Y,
-                                    nb, do_r, do_c, op->max_nnz, op->counter.get());
+    kern<<<grid, kThreads, sm, s>>>(runs, static_cast<int>(nruns), op->tiles.get(), op->blobs.get(), X, Y, nb, ld,
+                                    do_r, do_c, op->blob_max, op->counter.get());
     BE_CUDA(cudaGetLastError());
     ++op->ctx->launches;
 }
@@ -573,12 +612,19 @@ template <typename TC, typename TV, typename TX>
 void dispatch_nb(Op* op, const int2* runs, index_t nruns, const TX* X, TX* Y, int nb, int do_r, int do_c,
                  cudaStream_t s) {
     constexpr int VEC = Vec<TC>::N;
-    if (nb <= VEC) return launch_tiles<VEC, TC, TV, TX>(op, runs, nruns, X, Y, nb, do_r, do_c, s);
-    if (nb <= 8) return launch_tiles<8, TC, TV, TX>(op, runs, nruns, X, Y, nb, do_r, do_c, s);
-    if (nb <= 16) return launch_tiles<16, TC, TV, TX>(op, runs, nruns, X, Y, nb, do_r, do_c, s);
-    if (nb <= 32) return launch_tiles<32, TC, TV, TX>(op, runs, nruns, X, Y, nb, do_r, do_c, s);
-    if (nb <= 64) return launch_tiles<64, TC, TV, TX>(op, runs, nruns, X, Y, nb, do_r, do_c, s);
-    fail(BE_ERR_BAD_PARAMS, "sym_spmm: nb > 64 is not supported by the device kernel");
+    // widest panel slice whose X_I / X_J / Y_I lines fit the shared memory of an SM next to the
+    // two stage buffers: 64 f32 or 32 f64 columns; wider panels run as column slices (row stride nb)
+    constexpr int WMAX = sizeof(TC) == 4 ? 64 : 32;
+    for (int c0 = 0; c0 < nb; c0 += WMAX) {
+        const int w = std::min(WMAX, nb - c0);
+        const TX* x = X + c0;
+        TX* y = Y + c0;
+        if (w <= VEC) launch_tiles<VEC, TC, TV, TX>(op, runs, nruns, x, y, w, nb, do_r, do_c, s);
+        else if (w <= 8) launch_tiles<8, TC, TV, TX>(op, runs, nruns, x, y, w, nb, do_r, do_c, s);
+        else if (w <= 16) launch_tiles<16, TC, TV, TX>(op, runs, nruns, x, y, w, nb, do_r, do_c, s);
+        else if (w <= 32) launch_tiles<32, TC, TV, TX>(op, runs, nruns, x, y, w, nb, do_r, do_c, s);
+        else if constexpr (sizeof(TC) == 4) launch_tiles<64, TC, TV, TX>(op, runs, nruns, x, y, w, nb, do_r, do_c, s);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -586,11 +632,9 @@ void dispatch_nb(Op* op, const int2* runs, index_t nruns, const TX* X, TX* Y, in
 // ---------------------------------------------------------------------------
 
 struct RowOut {
-    std::vector<TileHdr> hdr;         // begin8 relative to this block row
-    std::vector<unsigned char> lens;  // 256 per tile: row then column lengths, rank order
-    std::vector<double> v;            // values in device order (converted on upload)
-    std::vector<std::uint16_t> rc, cp;
-    std::vector<std::int64_t> src;    // CSB index per device entry (optional)
+    std::vector<TileHdr> hdr;         // begin16 relative to this block row's blob bytes
+    std::vector<unsigned char> blob;  // the block row's tile blobs (values as f32 or f64)
+    std::vector<std::int64_t> src;    // CSB index per row-order device entry (optional, npad per tile)
     std::vector<unsigned char> cls;   // per tile: 0 interior, 1 exterior (distributed operator)
 };
 
@@ -616,98 +660,122 @@ struct RowMap {
     }
 };
 
-std::vector<std::uint16_t>& tls_colpos() {
-    thread_local std::vector<std::uint16_t> v;
-    return v;
+// Rank order of one side (rows or columns) of a tile: decreasing length, ties
+// by index. For rows, lanes L and L + 4 of every quarter-warp (ranks 8q + j
+// and 8q + j + 4) then get rows of opposite parity where a row of the same
+// length allows it: their 64-byte Y_I rows then sit in opposite bank halves
+// and the per-tile Y_I read-modify-write is conflict-free (nb = 16, f32).
+void rank_order(const int* len, int* order, bool parity) {
+    std::iota(order, order + kTile, 0);
+    std::stable_sort(order, order + kTile, [&](int a, int b) { return len[a] > len[b]; });
+    if (!parity) return;
+    for (int p = 0; p < kTile; ++p) {
+        if ((p & 7) < 4 || len[order[p]] == 0) continue;
+        const int partner = order[p - 4];
+        if (((order[p] ^ partner) & 1) != 0) continue;
+        for (int q = p + 1; q < kTile && len[order[q]] == len[order[p]]; ++q)
+            if (((order[q] ^ partner) & 1) != 0) {
+                std::swap(order[p], order[q]);
+                break;
+            }
+    }
 }
 
 // Emit one tile piece from `ent` = (local row << 56 | local col << 48 | CSB
-// index), sorted by (row, col, index).
+// index), sorted by (row, col, index), as a blob (see the format above).
+template <typename TV>
 void emit_piece(const be_csb_view& L, const std::vector<std::uint64_t>& ent, index_t row0, index_t col0, index_t nr,
-                index_t nc, bool keep_src, index_t& pos, RowOut& out) {
-    const std::size_t n = ent.size();
+                index_t nc, bool keep_src, RowOut& out) {
+    const int n = static_cast<int>(ent.size());
+    const int npad = pad16(n);
     int rlen[kTile] = {0}, clen[kTile] = {0};
     for (std::uint64_t e : ent) {
         ++rlen[e >> 56];
         ++clen[(e >> 48) & 255u];
     }
-    // rank order: decreasing length, ties by index
-    int rorder[kTile], corder[kTile], rrank[kTile], crank[kTile];
-    std::iota(rorder, rorder + kTile, 0);
-    std::iota(corder, corder + kTile, 0);
-    std::stable_sort(rorder, rorder + kTile, [&](int a, int b) { return rlen[a] > rlen[b]; });
-    std::stable_sort(corder, corder + kTile, [&](int a, int b) { return clen[a] > clen[b]; });
-    for (int i = 0; i < kTile; ++i) {
-        rrank[rorder[i]] = i;
-        crank[corder[i]] = i;
+    int rorder[kTile], corder[kTile];
+    rank_order(rlen, rorder, true);
+    rank_order(clen, corder, false);
+    // JDS starts: jd[d] = sum over ranks of min(len, d)
+    std::uint16_t jr[136] = {0}, jc[136] = {0};
+    for (int d = 0; d < kTile; ++d) {
+        int cr = 0, cc = 0;
+        for (int i = 0; i < kTile; ++i) {
+            cr += rlen[i] > d;
+            cc += clen[i] > d;
+        }
+        jr[d + 1] = static_cast<std::uint16_t>(jr[d] + cr);
+        jc[d + 1] = static_cast<std::uint16_t>(jc[d] + cc);
     }
-    // row-JDS order: diagonal j holds the j-th entry (by column) of every row
-    // rank with more than j entries; jd[j] = sum_r min(len_r, j)
-    int rstart[kTile + 1], cstart[kTile + 1];  // ent is (row, col)-sorted: rows are contiguous
-    rstart[0] = cstart[0] = 0;
-    for (int i = 0; i < kTile; ++i) {
-        rstart[i + 1] = rstart[i] + rlen[i];
-        cstart[i + 1] = cstart[i] + clen[corder[i]];  // by column rank
+    for (int d = kTile + 1; d < 136; ++d) {
+        jr[d] = jr[kTile];
+        jc[d] = jc[kTile];
     }
-    const int rmax = rlen[rorder[0]], cmax = clen[corder[0]];
-    std::vector<int> jd(static_cast<std::size_t>(rmax) + 1, 0), cjd(static_cast<std::size_t>(cmax) + 1, 0);
-    for (int j = 0; j < rmax; ++j) {
-        int cnt = 0;
-        while (cnt < kTile && rlen[rorder[cnt]] > j) ++cnt;
-        jd[static_cast<std::size_t>(j) + 1] = jd[static_cast<std::size_t>(j)] + cnt;
-    }
-    for (int j = 0; j < cmax; ++j) {
-        int cnt = 0;
-        while (cnt < kTile && clen[corder[cnt]] > j) ++cnt;
-        cjd[static_cast<std::size_t>(j) + 1] = cjd[static_cast<std::size_t>(j)] + cnt;
-    }
+    // tail split (see k_sym_spmm): warp 0 of a pass stops at diagonal D, warp 3 takes [D, len)
+    auto split_at = [](const int* len, const int* order) -> std::uint16_t {
+        const int t0 = len[order[0]], t1 = len[order[32]], t2 = len[order[64]], t3 = len[order[96]];
+        const int d = (std::max({t1, t2, (t0 + t3 + 1) / 2}) + 2) & ~3;  // nearest multiple of 4 (aligned starts)
+        return static_cast<std::uint16_t>(d >= t0 || d == 0 ? 0xFFFF : d);
+    };
+    jr[kSplitSlot] = split_at(rlen, rorder);
+    jc[kSplitSlot] = split_at(clen, corder);
     TileHdr hd{};
-    hd.begin8 = static_cast<std::uint32_t>(pos / 8);
+    hd.begin16 = static_cast<std::uint32_t>(out.blob.size() / 16);
     hd.row0 = static_cast<std::int32_t>(row0);
     hd.col0 = static_cast<std::int32_t>(col0);
     hd.packed = static_cast<std::uint32_t>(nr - 1) | (static_cast<std::uint32_t>(nc - 1) << 7) |
                 (static_cast<std::uint32_t>(n) << 14);
     out.hdr.push_back(hd);
-    for (int i = 0; i < kTile; ++i) out.lens.push_back(static_cast<unsigned char>(rlen[rorder[i]]));
-    for (int i = 0; i < kTile; ++i) out.lens.push_back(static_cast<unsigned char>(clen[corder[i]]));
-    const std::size_t base = out.v.size();
-    out.v.resize(base + n);
-    out.rc.resize(base + n);
-    out.cp.resize(base + n);
-    if (keep_src) out.src.resize(base + n);
-    std::vector<std::uint16_t>& colpos = tls_colpos();
-    colpos.resize(n);
-    int ccur[kTile];
-    std::copy(cstart, cstart + kTile, ccur);
+    const std::size_t base = out.blob.size();
+    out.blob.resize(base + blob_bytes<TV>(n), 0);
+    unsigned char* b = out.blob.data() + base;
+    std::memcpy(b + kMetaJr, jr, sizeof(jr));
+    std::memcpy(b + kMetaJc, jc, sizeof(jc));
+    for (int i = 0; i < kTile; ++i) {
+        b[kMetaRperm + i] = static_cast<unsigned char>(rorder[i]);
+        b[kMetaCperm + i] = static_cast<unsigned char>(corder[i]);
+        b[kMetaRlen + i] = static_cast<unsigned char>(rlen[rorder[i]]);
+        b[kMetaClen + i] = static_cast<unsigned char>(clen[corder[i]]);
+    }
+    TV* rv = reinterpret_cast<TV*>(b + kMetaBytes);
+    unsigned char* rcol = b + kMetaBytes + static_cast<std::size_t>(npad) * sizeof(TV);
+    TV* cv = reinterpret_cast<TV*>(b + kMetaBytes + static_cast<std::size_t>(npad) * (sizeof(TV) + 1));
+    unsigned char* crow = b + kMetaBytes + static_cast<std::size_t>(npad) * (2 * sizeof(TV) + 1);
+    const std::size_t sbase = out.src.size();
+    if (keep_src) out.src.resize(sbase + static_cast<std::size_t>(npad), -1);
+    // rows: ent is (row, col)-sorted, so row `row`'s entries are contiguous
+    int rstart[kTile + 1];
+    rstart[0] = 0;
+    for (int i = 0; i < kTile; ++i) rstart[i + 1] = rstart[i] + rlen[i];
+    int crank[kTile];
+    for (int i = 0; i < kTile; ++i) crank[corder[i]] = i;
+    int cnext[kTile] = {0};  // per column: entries placed so far (rows ascend through the row loop)
     for (int r = 0; r < kTile; ++r) {
         const int row = rorder[r];
         for (int j = 0; j < rlen[row]; ++j) {
             const std::uint64_t e = ent[static_cast<std::size_t>(rstart[row] + j)];
-            const int q = jd[static_cast<std::size_t>(j)] + r;
+            const int col = static_cast<int>((e >> 48) & 255u);
             const index_t k = static_cast<index_t>(e & 0xFFFFFFFFFFFFULL);
-            out.v[base + static_cast<std::size_t>(q)] = L.values[k];
-            out.rc[base + static_cast<std::size_t>(q)] = static_cast<std::uint16_t>(((e >> 56) << 8) | ((e >> 48) & 255u));
-            if (keep_src) out.src[base + static_cast<std::size_t>(q)] = k;
-            // column lists in (column rank, row rank) order
-            colpos[static_cast<std::size_t>(ccur[crank[(e >> 48) & 255u]]++)] = static_cast<std::uint16_t>(q);
+            const TV v = static_cast<TV>(L.values[k]);
+            const int q = jr[j] + r;
+            rv[q] = v;
+            rcol[q] = static_cast<unsigned char>(col);
+            if (keep_src) out.src[sbase + static_cast<std::size_t>(q)] = k;
         }
     }
-    // column-JDS order through cperm: cperm[cjd[j] + c] = row-JDS position of
-    // the j-th entry of column rank c
-    for (int c = 0; c < kTile; ++c)
-        for (int j = 0; j < cstart[c + 1] - cstart[c]; ++j)
-            out.cp[base + static_cast<std::size_t>(cjd[static_cast<std::size_t>(j)] + c)] =
-                colpos[static_cast<std::size_t>(cstart[c] + j)];
-    pos += static_cast<index_t>(n);
-    while (pos % 8) {  // pad the segment to 8 entries
-        out.v.push_back(0.0);
-        out.rc.push_back(0);
-        out.cp.push_back(0);
-        if (keep_src) out.src.push_back(-1);
-        ++pos;
-    }
+    // columns: the j-th entry (by row) of column rank c at jc[j] + c
+    for (int row = 0; row < kTile; ++row)
+        for (int j = 0; j < rlen[row]; ++j) {
+            const std::uint64_t e = ent[static_cast<std::size_t>(rstart[row] + j)];
+            const int col = static_cast<int>((e >> 48) & 255u);
+            const index_t k = static_cast<index_t>(e & 0xFFFFFFFFFFFFULL);
+            const int q = jc[cnext[col]++] + crank[col];
+            cv[q] = static_cast<TV>(L.values[k]);
+            crow[q] = static_cast<unsigned char>(row);
+        }
 }
 
+template <typename TV>
 void build_block_row(const be_csb_view& L, index_t bi, int max_nnz, bool keep_src, const RowMap* map, RowOut& out) {
     const index_t br = L.row_offsets[bi + 1] - L.row_offsets[bi];
     const index_t ta = (br + kTile - 1) / kTile;
@@ -737,7 +805,6 @@ void build_block_row(const be_csb_view& L, index_t bi, int max_nnz, bool keep_sr
         blocks.push_back(std::move(bb));
     }
     std::vector<std::uint64_t> keys, piece;
-    index_t pos = 0;
     const int row_own = map ? map->owner_of(L.row_offsets[bi]) : 0;
     for (index_t a = 0; a < ta; ++a) {
       for (int pass = 0; pass < (map ? 2 : 1); ++pass) {  // interior tiles first
@@ -770,25 +837,14 @@ void build_block_row(const be_csb_view& L, index_t bi, int max_nnz, bool keep_sr
                         if (p1 == p0) fail(BE_ERR_BAD_PARAMS, "tile row longer than max_nnz");
                     }
                     piece.assign(keys.begin() + static_cast<std::ptrdiff_t>(p0), keys.begin() + static_cast<std::ptrdiff_t>(p1));
-                    emit_piece(L, piece, map ? map->pad(row0) : row0, map ? map->pad(col0) : col0, nr, nc, keep_src,
-                               pos, out);
+                    emit_piece<TV>(L, piece, map ? map->pad(row0) : row0, map ? map->pad(col0) : col0, nr, nc,
+                                   keep_src, out);
                     out.cls.push_back(static_cast<unsigned char>(pass));
                     p0 = p1;
                 }
             }
         }
       }
-    }
-}
-
-template <typename TV>
-void upload_values(unsigned char* dst, const std::vector<double>& v) {
-    if constexpr (sizeof(TV) == 8) {
-        BE_CUDA(cudaMemcpy(dst, v.data(), v.size() * 8, cudaMemcpyHostToDevice));
-    } else {
-        std::vector<float> f(v.size());
-        for (std::size_t i = 0; i < v.size(); ++i) f[i] = static_cast<float>(v[i]);
-        BE_CUDA(cudaMemcpy(dst, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
     }
 }
 
@@ -844,72 +900,89 @@ std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag
     return op;
 }
 
+// Rows of one L2 column band: the f32 X_J and Y_J rows of a band at nb = 16
+// (2 x 64 B per row) take about half of the 126 MB L2.
+#ifndef BE_SPMM_BAND_ROWS
+#define BE_SPMM_BAND_ROWS 500000
+#endif
+
 // Tile-format build + upload shared by the single- and multi-GPU operators.
 static void op_build(Op* op, const be_csb_view& L, const RowMap* map) {
     const int values_prec = op->values_prec;
 #ifndef BE_SPMM_MAXNNZ
-#define BE_SPMM_MAXNNZ 1792  // f32 entries per tile piece (keeps four CTAs per SM)
+#define BE_SPMM_MAXNNZ 2048  // f32 entries per tile piece (two CTAs per SM)
 #endif
     op->max_nnz = values_prec == BE_F32 ? BE_SPMM_MAXNNZ : 1024;
+    op->blob_max = static_cast<int>(values_prec == BE_F32 ? blob_bytes<float>(op->max_nnz) : blob_bytes<double>(op->max_nnz));
     const bool keep_src = L.nnz <= (index_t{1} << 26);
 
     std::vector<RowOut> rows(static_cast<std::size_t>(L.nrowblks));
     parallel_for_dynamic(hw_threads(), L.nrowblks, [&](index_t bi, int) {
-        build_block_row(L, bi, op->max_nnz, keep_src, map, rows[static_cast<std::size_t>(bi)]);
+        if (values_prec == BE_F32)
+            build_block_row<float>(L, bi, op->max_nnz, keep_src, map, rows[static_cast<std::size_t>(bi)]);
+        else
+            build_block_row<double>(L, bi, op->max_nnz, keep_src, map, rows[static_cast<std::size_t>(bi)]);
     });
-    index_t ntiles = 0, padded = 0;
+    index_t ntiles = 0, bytes = 0, padded = 0;
     for (const auto& r : rows) {
         ntiles += static_cast<index_t>(r.hdr.size());
-        padded += static_cast<index_t>(r.v.size());
+        bytes += static_cast<index_t>(r.blob.size());
+        padded += static_cast<index_t>(r.src.size());
     }
-    if (padded / 8 >= (index_t{1} << 32)) fail(BE_ERR_BAD_PARAMS, "sym_spmm: too many entries for one device");
+    if (bytes / 16 >= (index_t{1} << 32)) fail(BE_ERR_BAD_PARAMS, "sym_spmm: tile blobs exceed 64 GB on one device");
     op->ntiles = ntiles;
-    op->padded = padded;
-    const std::size_t vsz = values_prec == BE_F32 ? 4 : 8;
+    op->blob_total = bytes;
+    op->padded = keep_src ? padded : 0;
     op->tiles.reset(std::max<index_t>(ntiles, 1));
-    op->lens.reset(std::max<index_t>(ntiles, 1) * 256);
-    op->vals.reset(std::max<index_t>(padded, 8) * static_cast<index_t>(vsz));
-    op->rc.reset(std::max<index_t>(padded, 8));
-    op->cperm.reset(std::max<index_t>(padded, 8));
+    op->blobs.reset(std::max<index_t>(bytes, 16));
     op->counter.reset(2);
     BE_CUDA(cudaMemset(op->counter.get(), 0, 2 * sizeof(int)));
+    op->csb_index.clear();
     if (keep_src) op->csb_index.reserve(static_cast<std::size_t>(padded));
     std::vector<TileHdr> all_hdr;
     all_hdr.reserve(static_cast<std::size_t>(ntiles));
     std::vector<unsigned char> all_cls;
     all_cls.reserve(static_cast<std::size_t>(ntiles));
-    index_t t_off = 0, e_off = 0;
+    index_t b_off = 0;
     for (auto& r : rows) {
         if (r.hdr.empty()) continue;
-        for (auto& h : r.hdr) h.begin8 += static_cast<std::uint32_t>(e_off / 8);
+        for (auto& h : r.hdr) h.begin16 += static_cast<std::uint32_t>(b_off / 16);
         all_hdr.insert(all_hdr.end(), r.hdr.begin(), r.hdr.end());
         all_cls.insert(all_cls.end(), r.cls.begin(), r.cls.end());
-        BE_CUDA(cudaMemcpy(op->lens.get() + t_off * 256, r.lens.data(), r.lens.size(), cudaMemcpyHostToDevice));
-        if (values_prec == BE_F32)
-            upload_values<float>(op->vals.get() + e_off * 4, r.v);
-        else
-            upload_values<double>(op->vals.get() + e_off * 8, r.v);
-        BE_CUDA(cudaMemcpy(op->rc.get() + e_off, r.rc.data(), r.rc.size() * 2, cudaMemcpyHostToDevice));
-        BE_CUDA(cudaMemcpy(op->cperm.get() + e_off, r.cp.data(), r.cp.size() * 2, cudaMemcpyHostToDevice));
+        BE_CUDA(cudaMemcpy(op->blobs.get() + b_off, r.blob.data(), r.blob.size(), cudaMemcpyHostToDevice));
         if (keep_src) op->csb_index.insert(op->csb_index.end(), r.src.begin(), r.src.end());
-        t_off += static_cast<index_t>(r.hdr.size());
-        e_off += static_cast<index_t>(r.v.size());
+        b_off += static_cast<index_t>(r.blob.size());
         r = RowOut();
     }
     if (ntiles > 0)
         BE_CUDA(cudaMemcpy(op->tiles.get(), all_hdr.data(), all_hdr.size() * sizeof(TileHdr), cudaMemcpyHostToDevice));
-    {  // runs: consecutive tiles of one tile-row and class, at most kRunMax tiles each
-        std::vector<int2> runs[2];
+    {  // runs: consecutive tiles of one tile-row, class and L2 column band, at most kRunMax tiles each,
+       // ordered by (class, band, tile-row)
+        struct R {
+            int cls;
+            index_t band;
+            int b, e;
+        };
+        std::vector<R> all;
+        index_t band_rows = BE_SPMM_BAND_ROWS;
+        if (const char* e = std::getenv("BE_SPMM_BAND_ROWS")) band_rows = std::atoll(e);  // (experiments)
+        band_rows = std::max<index_t>(kTile, band_rows);
         for (index_t t = 0; t < ntiles;) {
             const auto& h0 = all_hdr[static_cast<std::size_t>(t)];
             const unsigned char c0 = all_cls[static_cast<std::size_t>(t)];
+            const index_t band = h0.col0 / band_rows;
             index_t e = t + 1;
             while (e < ntiles && e - t < kRunMax && all_hdr[static_cast<std::size_t>(e)].row0 == h0.row0 &&
-                   all_cls[static_cast<std::size_t>(e)] == c0)
+                   all_cls[static_cast<std::size_t>(e)] == c0 && all_hdr[static_cast<std::size_t>(e)].col0 / band_rows == band)
                 ++e;
-            runs[c0].push_back(make_int2(static_cast<int>(t), static_cast<int>(e)));
+            all.push_back(R{c0, band, static_cast<int>(t), static_cast<int>(e)});
             t = e;
         }
+        std::stable_sort(all.begin(), all.end(), [](const R& a, const R& b) {
+            return a.cls != b.cls ? a.cls < b.cls : a.band < b.band;
+        });
+        std::vector<int2> runs[2];
+        for (const auto& x : all) runs[x.cls].push_back(make_int2(x.b, x.e));
         op->nruns = static_cast<index_t>(runs[0].size());
         op->runs.reset(std::max<index_t>(op->nruns, 1));
         if (!runs[0].empty())
