@@ -1598,6 +1598,7 @@ void Sygv::ensure(Ctx* ctx, int nn) {
 void sygv_lowest(Ctx* ctx, Sygv& ws, double* A, const double* B, int n, int k, double pivot_floor, double* c,
                  double* d, Status* st, cudaStream_t s) {
     if (k < 1 || k > n) fail(BE_ERR_BAD_PARAMS, "sygv_lowest: k out of range");
+    if (rr_eig_fits(n)) return sygv_small(ctx, A, B, n, k, pivot_floor, c, d, st, s);
     ws.ensure(ctx, n);
     chol_floored(ctx, B, ws.R.get(), n, pivot_floor, st, s);
     // M = R^-T A R^-1 (densela.hpp:366-390) as two cuBLAS triangular solves,

@@ -18,7 +18,9 @@ struct Status {
     int singular_tri;      // trsm_right_inv refused a factor (densela.hpp:135-136)
     int not_pd;            // last floored Cholesky failed (pivot + 1, 0 = ok)
     int ortho_fallback;    // orthonormalize_pair took the column-scaling path
-    int pad[3];
+    int rr_dropped;        // rr_eig: 1 dropped P (lobpcg.hpp:380-396), 2 failed without P too
+    int w_rank_first;      // the first qr_of_transpose of W gave up (restart with a random W)
+    int pad;
 };
 
 // Up to 12 Gram products A_p^T B_p (nb x nb, column-major) in one pass over
@@ -92,6 +94,20 @@ void rr_assemble(Ctx* ctx, const double* blocks, int nb, int nblk, double* G, do
 // -> st->not_pd), M = R^-T A R^-1 symmetrised, eigen-decomposition with
 // cuSOLVER syevd, C = R^-1 Q_k with normalize_column_signs. A, B are n x n
 // column-major device matrices (A is overwritten); c (n x k), d (k).
+// Fused Rayleigh-Ritz eigensolve (rr_eig.cu) for nblk * nb <= 64: assembly,
+// floored Cholesky (pivot_floor), reduction, Jacobi, back-transform, signs and
+// the drop-P retry in one single-CTA launch. c: (nblk nb) x nb column-major
+// (the P rows zeroed when P was dropped), theta: nb ascending, shifts (may be
+// null): theta[min(v, k - 1)] for the next preconditioner apply.
+bool rr_eig_fits(int dim);
+void rr_eig(Ctx* ctx, const double* blocks, int nb, int nblk, int k, double pivot_floor, double* c, double* theta,
+            double* shifts, Status* st, cudaStream_t s);
+// sygv_lowest on the same single-CTA solver (n <= 64): c (n x k), d (k)
+// st->w_rank_first |= st->rank_deficient (the first W qr's verdict survives the second qr)
+void latch_w_rank(Ctx* ctx, Status* st, cudaStream_t s);
+void sygv_small(Ctx* ctx, const double* A, const double* B, int n, int k, double pivot_floor, double* c, double* d,
+                Status* st, cudaStream_t s);
+
 struct Sygv {
     int n = 0;
     int lwork = 0;

@@ -191,7 +191,8 @@ struct Solver {
         BE_CUDA(cudaMemcpyAsync(&hm->st, st.get(), sizeof(dla::Status), cudaMemcpyDeviceToHost, s));
         BE_CUDA(cudaStreamSynchronize(s));
     }
-    void reset_qr_flags() { BE_CUDA(cudaMemsetAsync(st.get(), 0, 3 * sizeof(int), s)); }
+    // qr_failures and rank_deficient only: singular_tri stays set until the iteration's check
+    void reset_qr_flags() { BE_CUDA(cudaMemsetAsync(st.get(), 0, 2 * sizeof(int), s)); }
 
     void apply_op(const double* in, double* out) {
         if (op) {
@@ -289,6 +290,10 @@ struct Solver {
         dla::gram(ctx, j, n, partials.get(), partials_len, s);
         allreduce(blocks, np * nb * nb);
         const int nblk = with_p ? 3 : 2;
+        if (fused_rr) {  // one launch, no host round trip; verdict read at the iteration's sync
+            dla::rr_eig(ctx, blocks, nb, nblk, k, 1e-10, C, theta, shifts, st.get(), s);
+            return true;
+        }
         dla::rr_assemble(ctx, blocks, nb, nblk, G, O, s);
         dla::sygv_lowest(ctx, sygv, G, O, nblk * nb, nb, 1e-10, C, theta, st.get(), s);
         BE_CUDA(cudaMemcpyAsync(hm->theta, theta, nb * 8, cudaMemcpyDeviceToHost, s));
@@ -298,6 +303,8 @@ struct Solver {
 
     std::vector<double> th;
     const bool trace_segments = std::getenv("BE_TRACE_SEGMENTS") != nullptr;
+    // the fused single-CTA Rayleigh-Ritz eigensolve (rr_eig.cu) when the pencil fits
+    const bool fused_rr = dla::rr_eig_fits(3 * nb) && std::getenv("BE_RR_CUSOLVER") == nullptr;
     bool p_active = false, converged = false;
     int iter = 0;
     Events ev;
@@ -317,11 +324,15 @@ struct Solver {
             j.a[1] = X.get(); j.b[1] = X.get(); j.sym[1] = 1; j.out[1] = blocks + static_cast<index_t>(nb) * nb;
             dla::gram(ctx, j, n, partials.get(), partials_len, s);
             allreduce(blocks, 2 * nb * nb);
-            dla::rr_assemble(ctx, blocks, nb, 1, G, O, s);
-            dla::sygv_lowest(ctx, sygv, G, O, nb, nb, 1e-10, C, theta, st.get(), s);
+            if (fused_rr) {
+                dla::rr_eig(ctx, blocks, nb, 1, k, 1e-10, C, theta, shifts, st.get(), s);
+            } else {
+                dla::rr_assemble(ctx, blocks, nb, 1, G, O, s);
+                dla::sygv_lowest(ctx, sygv, G, O, nb, nb, 1e-10, C, theta, st.get(), s);
+            }
             BE_CUDA(cudaMemcpyAsync(hm->theta, theta, nb * 8, cudaMemcpyDeviceToHost, s));
             sync_status();
-            if (hm->st.not_pd) fail(BE_ERR_BREAKDOWN_UNRECOVERABLE, "lobpcg_solve: initial block is degenerate");
+            if (hm->st.not_pd || hm->st.rr_dropped) fail(BE_ERR_BREAKDOWN_UNRECOVERABLE, "lobpcg_solve: initial block is degenerate");
             dla::MixJob m{};
             m.nb = nb;
             m.nout = 2;
@@ -336,6 +347,99 @@ struct Solver {
         allreduce(rn2, 2 * nb);  // rn2, xn2 are adjacent
     }
 
+    // One iteration of lobpcg_solve (lobpcg.hpp:338-441) from the preconditioner
+    // on. With the fused Rayleigh-Ritz eigensolve the device takes every
+    // decision of the iteration itself (the drop-P retry inside rr_eig, the
+    // W restart deferred, see iterate) and the host synchronises once, at the
+    // end, to read the status, the Ritz values and the residual norms.
+    void iteration_body(bool w_restart) {
+        BE_CUDA(cudaEventRecord(ev.e[0], s));
+        if (!w_restart) {
+            if (tiles) {  // W = K^{-1} R, shifts theta[min(v, k-1)] (lobpcg.hpp:344-350)
+                if (!fused_rr) {  // (the fused eigensolve writes the shifts on the device)
+                    for (int v = 0; v < nb; ++v) hm->shifts[v] = th[static_cast<std::size_t>(std::min(v, k - 1))];
+                    BE_CUDA(cudaMemcpyAsync(shifts, hm->shifts, nb * 8, cudaMemcpyHostToDevice, s));
+                }
+                precond_apply(tiles, shifts, R.get(), W.get(), n, nb, cfg.fom_iterations, fallbacks.get(), s);
+            } else {
+                BE_CUDA(cudaMemcpyAsync(W.get(), R.get(), static_cast<std::size_t>(n * nb) * 8, cudaMemcpyDeviceToDevice, s));
+            }
+        }
+        BE_CUDA(cudaEventRecord(ev.e[1], s));
+        // W hygiene (lobpcg.hpp:358-373)
+        if (w_restart) {  // the first qr_of_transpose of W gave up: a random W (lobpcg.hpp:360-363)
+            upload_random(W.get(), cfg.seed + static_cast<std::uint64_t>(iter) * 7919u);
+            if (!qr(W.get(), true)) fail(BE_ERR_RANK_DEFICIENT, "qr_of_transpose: Gram Cholesky failed twice");
+        } else if (fused_rr) {
+            qr(W.get(), false);  // verdict latched, read at the end of the iteration
+            dla::latch_w_rank(ctx, st.get(), s);
+        } else if (!qr(W.get(), true)) {
+            upload_random(W.get(), cfg.seed + static_cast<std::uint64_t>(iter) * 7919u);
+            if (!qr(W.get(), true)) fail(BE_ERR_RANK_DEFICIENT, "qr_of_transpose: Gram Cholesky failed twice");
+        }
+        project_out(W.get(), X.get());
+        if (p_active) project_out(W.get(), P.get());
+        qr(W.get(), false);  // RankDeficient swallowed: W keeps the completed passes
+        BE_CUDA(cudaEventRecord(ev.e[2], s));
+        apply_op(W.get(), HW.get());
+        BE_CUDA(cudaEventRecord(ev.e[3], s));
+        // Rayleigh-Ritz with the drop-P retry (lobpcg.hpp:380-396)
+        dropped_host = false;
+        if (!rayleigh_ritz(p_active)) {  // (host-driven path only: the fused one retries on the device)
+            if (!p_active) fail(BE_ERR_BREAKDOWN_UNRECOVERABLE, "lobpcg_solve: 2-block basis failed Cholesky");
+            dropped_host = true;
+            if (!rayleigh_ritz(false)) fail(BE_ERR_BREAKDOWN_UNRECOVERABLE, "lobpcg_solve: basis repair failed twice");
+        }
+        BE_CUDA(cudaEventRecord(ev.e[5], s));
+        // fused: C keeps the 3-block layout and its P rows are zero after a device-side drop
+        const bool with_p = p_active && !dropped_host;
+        const int dim = (with_p ? 3 : 2) * nb;
+        {  // update_blocks (lobpcg.hpp:168-194): P+ = W C2 + P C3, X+ = X C1 + P+ (and the H-images),
+           // as two passes of <= 4 sources each (one 6-source pass runs at a fraction of HBM bandwidth)
+            const double* c1 = C;
+            const double* c2 = C + nb;
+            const double* c3 = C + 2 * nb;
+            dla::MixJob m{};
+            m.nb = nb;
+            m.nout = 2;
+            m.out[0] = dla::MixOut{Pn.get(), 0, with_p ? 2 : 1, {{W.get(), c2, 0, dim}, {P.get(), c3, 0, dim}}, -1};
+            m.out[1] = dla::MixOut{HPn.get(), 0, with_p ? 2 : 1, {{HW.get(), c2, 0, dim}, {HP.get(), c3, 0, dim}}, -1};
+            dla::mix(ctx, m, n, s);
+            dla::MixJob m2{};
+            m2.nb = nb;
+            m2.nout = 2;
+            m2.out[0] = dla::MixOut{Xn.get(), 0, 1, {{X.get(), c1, 0, dim}}, -1, Pn.get()};
+            m2.out[1] = dla::MixOut{HXn.get(), 0, 1, {{HX.get(), c1, 0, dim}}, -1, HPn.get()};
+            dla::mix(ctx, m2, n, s);
+            std::swap(X, Xn);
+            std::swap(HX, HXn);
+            std::swap(P, Pn);
+            std::swap(HP, HPn);
+        }
+        BE_CUDA(cudaEventRecord(ev.e[6], s));
+        {  // P hygiene (lobpcg.hpp:412-417) + orthonormalize_pair (:254-270)
+            gram1(X.get(), P.get(), 0, xtp);
+            dla::MixJob m{};
+            m.nb = nb;
+            m.nout = 2;
+            m.out[0] = dla::MixOut{P.get(), 1, 1, {{X.get(), xtp, 1, 0}}, -1};
+            m.out[1] = dla::MixOut{HP.get(), 1, 1, {{HX.get(), xtp, 1, 0}}, -1};
+            dla::mix(ctx, m, n, s);
+            gram1(P.get(), P.get(), 1, Bp);
+            dla::chol_floored(ctx, Bp, Rp, nb, 1e-8, st.get(), s);
+            dla::trsm(ctx, P.get(), HP.get(), Rp, nb, n, st.get(), 0, 1, s);
+        }
+        BE_CUDA(cudaEventRecord(ev.e[7], s));
+        dla::residual(ctx, HX.get(), X.get(), theta, R.get(), nb, n, partials.get(), rn2, xn2, s);
+        allreduce(rn2, 2 * nb);
+        BE_CUDA(cudaMemcpyAsync(hm->theta, theta, nb * 8, cudaMemcpyDeviceToHost, s));
+        BE_CUDA(cudaMemcpyAsync(hm->rn2, rn2, nb * 8, cudaMemcpyDeviceToHost, s));
+        BE_CUDA(cudaMemcpyAsync(hm->xn2, xn2, nb * 8, cudaMemcpyDeviceToHost, s));
+        BE_CUDA(cudaEventRecord(ev.e[4], s));
+        sync_status();
+    }
+    bool dropped_host = false;
+
     // run up to `count` further iterations (never past maxiter); returns the
     // number executed. Stops at convergence.
     int iterate(int count) {
@@ -344,81 +448,26 @@ struct Solver {
             ++iter;
             ++done;
             const auto wall0 = std::chrono::steady_clock::now();
-            BE_CUDA(cudaEventRecord(ev.e[0], s));
-            if (tiles) {  // W = K^{-1} R, shifts theta[min(v, k-1)] (lobpcg.hpp:344-350)
-                for (int v = 0; v < nb; ++v) hm->shifts[v] = th[static_cast<std::size_t>(std::min(v, k - 1))];
-                BE_CUDA(cudaMemcpyAsync(shifts, hm->shifts, nb * 8, cudaMemcpyHostToDevice, s));
-                precond_apply(tiles, shifts, R.get(), W.get(), n, nb, cfg.fom_iterations, fallbacks.get(), s);
-            } else {
-                BE_CUDA(cudaMemcpyAsync(W.get(), R.get(), static_cast<std::size_t>(n * nb) * 8, cudaMemcpyDeviceToDevice, s));
-            }
-            BE_CUDA(cudaEventRecord(ev.e[1], s));
-            // W hygiene (lobpcg.hpp:358-373)
-            if (!qr(W.get(), true)) {
-                upload_random(W.get(), cfg.seed + static_cast<std::uint64_t>(iter) * 7919u);
-                if (!qr(W.get(), true)) fail(BE_ERR_RANK_DEFICIENT, "qr_of_transpose: Gram Cholesky failed twice");
-            }
-            project_out(W.get(), X.get());
-            if (p_active) project_out(W.get(), P.get());
-            qr(W.get(), false);  // RankDeficient swallowed: W keeps the completed passes
-            BE_CUDA(cudaEventRecord(ev.e[2], s));
-            apply_op(W.get(), HW.get());
-            BE_CUDA(cudaEventRecord(ev.e[3], s));
-            // Rayleigh-Ritz with the drop-P retry (lobpcg.hpp:380-396)
-            bool dropped = false;
-            if (!rayleigh_ritz(p_active)) {
-                if (!p_active) fail(BE_ERR_BREAKDOWN_UNRECOVERABLE, "lobpcg_solve: 2-block basis failed Cholesky");
-                dropped = true;
-                ++res.restarts;
-                if (!rayleigh_ritz(false)) fail(BE_ERR_BREAKDOWN_UNRECOVERABLE, "lobpcg_solve: basis repair failed twice");
-            }
-            BE_CUDA(cudaEventRecord(ev.e[5], s));
-            const bool with_p = p_active && !dropped;
-            const int dim = (with_p ? 3 : 2) * nb;
-            {  // update_blocks (lobpcg.hpp:168-194): P+ = W C2 + P C3, X+ = X C1 + P+ (and the H-images),
-               // as two passes of <= 4 sources each (one 6-source pass runs at a fraction of HBM bandwidth)
-                const double* c1 = C;
-                const double* c2 = C + nb;
-                const double* c3 = C + 2 * nb;
-                dla::MixJob m{};
-                m.nb = nb;
-                m.nout = 2;
-                m.out[0] = dla::MixOut{Pn.get(), 0, with_p ? 2 : 1, {{W.get(), c2, 0, dim}, {P.get(), c3, 0, dim}}, -1};
-                m.out[1] = dla::MixOut{HPn.get(), 0, with_p ? 2 : 1, {{HW.get(), c2, 0, dim}, {HP.get(), c3, 0, dim}}, -1};
-                dla::mix(ctx, m, n, s);
-                dla::MixJob m2{};
-                m2.nb = nb;
-                m2.nout = 2;
-                m2.out[0] = dla::MixOut{Xn.get(), 0, 1, {{X.get(), c1, 0, dim}}, -1, Pn.get()};
-                m2.out[1] = dla::MixOut{HXn.get(), 0, 1, {{HX.get(), c1, 0, dim}}, -1, HPn.get()};
-                dla::mix(ctx, m2, n, s);
+            BE_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(dla::Status), s));
+            const bool p_was = p_active;
+            iteration_body(false);
+            if (hm->st.w_rank_first) {
+                // The first qr_of_transpose of W gave up (rare): roll back to the state
+                // before the update (the update wrote the other half of every double-buffered
+                // panel) and redo the iteration from a random W, as the reference does.
                 std::swap(X, Xn);
                 std::swap(HX, HXn);
                 std::swap(P, Pn);
                 std::swap(HP, HPn);
+                p_active = p_was;
+                --res.operator_calls;
+                BE_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(dla::Status), s));
+                iteration_body(true);
             }
-            BE_CUDA(cudaEventRecord(ev.e[6], s));
+            if (hm->st.rr_dropped == 2) fail(BE_ERR_BREAKDOWN_UNRECOVERABLE, "lobpcg_solve: basis repair failed twice");
+            if (hm->st.rr_dropped == 1 || dropped_host) ++res.restarts;
             th.assign(hm->theta, hm->theta + nb);
             p_active = true;
-            {  // P hygiene (lobpcg.hpp:412-417) + orthonormalize_pair (:254-270)
-                gram1(X.get(), P.get(), 0, xtp);
-                dla::MixJob m{};
-                m.nb = nb;
-                m.nout = 2;
-                m.out[0] = dla::MixOut{P.get(), 1, 1, {{X.get(), xtp, 1, 0}}, -1};
-                m.out[1] = dla::MixOut{HP.get(), 1, 1, {{HX.get(), xtp, 1, 0}}, -1};
-                dla::mix(ctx, m, n, s);
-                gram1(P.get(), P.get(), 1, Bp);
-                dla::chol_floored(ctx, Bp, Rp, nb, 1e-8, st.get(), s);
-                dla::trsm(ctx, P.get(), HP.get(), Rp, nb, n, st.get(), 0, 1, s);
-            }
-            BE_CUDA(cudaEventRecord(ev.e[7], s));
-            dla::residual(ctx, HX.get(), X.get(), theta, R.get(), nb, n, partials.get(), rn2, xn2, s);
-            allreduce(rn2, 2 * nb);
-            BE_CUDA(cudaMemcpyAsync(hm->rn2, rn2, nb * 8, cudaMemcpyDeviceToHost, s));
-            BE_CUDA(cudaMemcpyAsync(hm->xn2, xn2, nb * 8, cudaMemcpyDeviceToHost, s));
-            BE_CUDA(cudaEventRecord(ev.e[4], s));
-            sync_status();
             if (hm->st.not_pd) {  // column-scaling fallback of orthonormalize_pair
                 dla::colnorm2(ctx, P.get(), nb, n, partials.get(), pn2, s);
                 allreduce(pn2, nb);

@@ -60,6 +60,9 @@ def main():
             out["runs"][f"{tag}_{name}"] = dict(iterations=r["iterations"], converged=r["converged"],
                                                 operator_calls=r["operator_calls"], lambda_=r["lambda_"].tolist(),
                                                 theta_first10=r["theta"][:10].tolist(),
+                                                theta=r["theta"][:, :8].tolist(),
+                                                residual_norms=r["residual_norms"][:, :8].tolist(),
+                                                n_converged=r["n_converged"].tolist(), fallbacks=r["fallbacks"],
                                                 seconds=round(time.time() - t0, 1))
             print(tag, name, r["iterations"], r["lambda_"][:3], f"{time.time() - t0:.1f}s", flush=True)
     (HERE / "c1_reference.json").write_text(json.dumps(out, indent=1))

@@ -82,23 +82,32 @@ def test_c1_precond_off_matches_reference(ctx, c1, values):
 
 @pytest.mark.parametrize("values", ["f64", "f32"])
 def test_c1_precond_on_within_reference_envelope(ctx, c1, values):
+    """With the FOM preconditioner the iteration is chaotic: the reference itself, run with
+    ThreadPool(T) for T = 1..8 (different Gram / SpMM partial-sum orders, densela.hpp:74-89),
+    takes 59..69 iterations (tests/golden/make_golden_envelope.py), and its serial and 8-thread
+    Ritz values drift apart ~1000x per iteration (1e-11, 3e-8, 9e-6, 2e-3 at iterations 1-4)
+    before converging to the same eigenvalues. The bars: the same final eigenvalues (1e-6),
+    an iteration count inside the reference's own envelope +-1, and the same early trajectory
+    as the reference's own order-to-order spread."""
     g, m, s = c1
-    ref = _runs(g, "on")
-    lo = min(r["iterations"] for r in ref.values())
-    hi = max(r["iterations"] for r in ref.values())
-    assert (lo, hi) == (65, 66)
+    env = [int(v) for v in g["envelope_on"].values()]
+    lo, hi = min(env), max(env)
+    assert (lo, hi) == (59, 69) and len(env) == 8
     op = abi.Operator(ctx, m, s.diag, values_prec=abi.BE_F32 if values == "f32" else abi.BE_F64)
     tiles = abi.Tiles(ctx, m, s.diag, s.tile_offsets)
     got = abi.lobpcg(ctx, op, tiles=tiles, k=g["k"], nb=g["nb"], tol=g["tol"], maxiter=g["maxiter"],
                      fom_iterations=g["fom_m"], seed=g["seed"])
     assert got["converged"]
-    lam = np.array(ref["serial"]["lambda_"])
+    ser = g["runs"]["on_serial"]
+    lam = np.array(ser["lambda_"])
     rel = np.max(np.abs(got["lambda_"] - lam) / np.abs(lam))
     assert rel <= 1e-6, rel
-    if values == "f64":  # the parity mode for the chaotic precond-on count
-        assert lo - 1 <= got["iterations"] <= hi + 1, (got["iterations"], lo, hi)
-    else:  # f32 values: reported, bounded loosely (SURVEY 8c measured 67-69 with fp32 emulation)
-        assert lo - 1 <= got["iterations"] <= hi + 5, (got["iterations"], lo, hi)
+    assert lo - 1 <= got["iterations"] <= hi + 1, (got["iterations"], lo, hi)
+    # early trajectory: within 10x the reference's own serial-vs-8-thread spread (floor 1e-9)
+    a, b = np.array(ser["theta"]), np.array(g["runs"]["on_baseline8"]["theta"])
+    spread = np.max(np.abs(a[:3] - b[:3]) / np.abs(a[:3]), axis=1)
+    ours = np.max(np.abs(got["theta"][:3, :8] - a[:3]) / np.abs(a[:3]), axis=1)
+    assert np.all(ours <= np.maximum(10 * spread, 1e-9)), (ours, spread)
     tiles.close()
     op.close()
 
@@ -117,9 +126,14 @@ def test_t1_ritz_trace_matches_reference(ctx):
     got = abi.lobpcg(ctx, op, tiles=tiles, k=g["k"], nb=g["nb"], tol=1e-300, maxiter=it, fom_iterations=g["fom_m"],
                      seed=g["seed"])
     assert got["iterations"] == it and got["operator_calls"] == g["operator_calls"]
-    th = np.array(g["theta"])
-    rel = np.abs(got["theta"] - th) / np.abs(th)
-    # the wanted (lowest k) Ritz values track the reference's to 1e-6 every iteration
-    assert np.max(rel[:, :g["k"]]) <= 1e-6, np.max(rel[:, :g["k"]], axis=1)
+    th = np.array(g["theta"])[:, :g["k"]]
+    rel = np.max(np.abs(got["theta"][:, :g["k"]] - th) / np.abs(th), axis=1)
+    # the wanted (lowest k) Ritz values track the reference's (8 threads) within the reference's
+    # own spread between ThreadPool(4) and ThreadPool(8) (x10, floor 1e-6): with the preconditioner
+    # on, the trajectory amplifies rounding differences ~1000x per iteration (see the C1 test)
+    t4 = np.array(g["theta_t4"])[:, :g["k"]]
+    spread = np.max(np.abs(t4 - th) / np.abs(th), axis=1)
+    assert np.all(rel <= np.maximum(10 * spread, 1e-6)), (rel, spread)
+    assert rel[0] <= 1e-6
     tiles.close()
     op.close()
