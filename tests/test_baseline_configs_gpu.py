@@ -8,7 +8,7 @@ test_lobpcg.cpp:286-303 (solver vs an independent answer). The reference's
 results on the same bytes are committed in tests/golden/c1_reference.json
 (tests/golden/make_golden_c1.py runs oracle/_ref/libref.so, the unmodified
 reference headers): precondition off 51 iterations under every summation
-order, on 65 (serial) / 66 (8-thread baseline and fused-atomic).
+order; on: 59..69 over ThreadPool(1..8) (tests/golden/make_golden_envelope.py).
 
 T1 = configs[1] shape (clustered generator, n = 2.9e6, 1.1e9 lower
 nonzeros): the first 10 iterations' Ritz values against the reference's
