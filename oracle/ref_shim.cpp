@@ -15,6 +15,7 @@
 #include <blockeig/synth.hpp>
 
 #include <chrono>
+#include <fstream>
 #include <cstring>
 #include <memory>
 #include <sstream>
@@ -277,6 +278,43 @@ void* ref_prepare(const void* view, const double* diag, const index_t* off, inde
         return nullptr;
     }
 }
+
+// The same, from a CSB1 cache file as the reference driver reads it
+// (driver.hpp:136-161): load_csb (csb.hpp:264-290), then the u64 length and
+// the f64 diagonal section; tile offsets from a plain i64 sidecar (count, then
+// offsets), or none (preconditioner off) when tiles_path is NULL.
+void* ref_prepare_file(const char* path, const char* tiles_path, int threads) {
+    try {
+        auto p = new Prepared;
+        std::ifstream is(path, std::ios::binary);
+        if (!is) throw ParseError(std::string("cannot open cache ") + path);
+        p->m = load_csb(is);
+        std::uint64_t dlen = 0;
+        is.read(reinterpret_cast<char*>(&dlen), sizeof(dlen));
+        p->diag.resize(dlen);
+        is.read(reinterpret_cast<char*>(p->diag.data()), static_cast<std::streamsize>(dlen * sizeof(double)));
+        if (!is) throw ParseError("cache: truncated diagonal section");
+        if (static_cast<index_t>(dlen) != p->m.nrows) throw ParseError("cache: dimensions do not match the input matrix");
+        p->pool = pool_of(threads);
+        p->op = std::make_unique<SymmetricOperator>(p->m, p->diag, KernelVariant::baseline(), p->pool.get());
+        if (tiles_path) {
+            std::ifstream ts(tiles_path, std::ios::binary);
+            std::int64_t cnt = 0;
+            ts.read(reinterpret_cast<char*>(&cnt), sizeof(cnt));
+            std::vector<index_t> off(static_cast<std::size_t>(cnt));
+            ts.read(reinterpret_cast<char*>(off.data()), static_cast<std::streamsize>(cnt * sizeof(index_t)));
+            if (!ts) throw ParseError("tile offsets sidecar truncated");
+            p->tiles.emplace(extract_tiles(p->m, p->diag, off));
+        }
+        return p;
+    } catch (const std::exception& e) {
+        g_msg = e.what();
+        return nullptr;
+    }
+}
+
+index_t ref_prepared_nrows(void* pp) { return static_cast<Prepared*>(pp)->m.nrows; }
+index_t ref_prepared_nnz(void* pp) { return static_cast<index_t>(static_cast<Prepared*>(pp)->m.values.size()); }
 
 void ref_release(void* p) { delete static_cast<Prepared*>(p); }
 

@@ -32,4 +32,4 @@ def rank_problem(ctx, comm, params, rank: int, world: int, precond: bool, allred
         tiles = abi.Tiles(ctx, dblk, diag, toff, row_range=(lo, hi))
         del dblk
     return dict(op=op, tiles=tiles, cuts=cuts, slabs=slabs, lo=lo, hi=hi, nnz_local=slab.nnz,
-                tile_entries=tiles.count()[2] if tiles else 0, diag=diag, toff=toff)
+                tile_entries=tiles.count()[2] if tiles else 0, diag=diag, toff=toff, slab_csb=slab)
