@@ -1,7 +1,10 @@
 """Golden Ritz-value trace of the REFERENCE on the Test-1-shaped problem
 (BASELINE.json configs[1]: n = 2.9e6, 1.1e9 stored lower nonzeros, nev = 8,
-block k = 16, preconditioner on), 10 fixed iterations (tol = 1e-300, the
-pattern of test_lobpcg.cpp:341), for the slow GPU parity test.
+block k = 16), 10 fixed iterations (tol = 1e-300, the pattern of
+test_lobpcg.cpp:341), for the slow GPU parity test: with the preconditioner
+on under ThreadPool(8) ("theta") and ThreadPool(4) ("theta_t4": the
+reference's own summation-order spread), and with it off ("theta_off",
+ThreadPool(8)), where the trajectory is not chaotic.
 
 The matrix is the clustered generator's (counter-based, so the GPU
 box regenerates the same bytes -- the fixture stores a SHA-256 of the CSB
@@ -51,6 +54,17 @@ def main():
     out = dict(params=T1, nnz=int(m.nnz), csb_sha256=dg, k=8, nb=16, fom_m=4, seed=1, iterations=r["iterations"],
                theta=r["theta"].tolist(), residual_norms=r["residual_norms"].tolist(),
                operator_calls=r["operator_calls"], fallbacks=r["fallbacks"])
+    t0 = time.time()
+    r4 = ol.Impl("ref", threads=4, variant=0).lobpcg(m, diag, toff, k=8, nb=16, tol=1e-300, maxiter=ITERS, fom_m=4,
+                                                    seed=1)
+    out["theta_t4"] = r4["theta"].tolist()
+    print(f"reference (4 threads) {ITERS} iterations in {time.time() - t0:.1f}s", flush=True)
+    t0 = time.time()
+    ro = ol.Impl("ref", threads=8, variant=0).lobpcg(m, diag, None, k=8, nb=16, tol=1e-300, maxiter=ITERS, fom_m=4,
+                                                    seed=1)
+    out["theta_off"] = ro["theta"].tolist()
+    out["residual_norms_off"] = ro["residual_norms"].tolist()
+    print(f"reference (precond off) {ITERS} iterations in {time.time() - t0:.1f}s", flush=True)
     (HERE / "t1_reference.json").write_text(json.dumps(out, indent=1))
 
 
