@@ -124,6 +124,11 @@ be_status be_csb_load(const char* path, be_csb** out, double** diag, int64_t* nd
  * diag (may be NULL) receives the cached diagonal of those rows. */
 be_status be_csb_load_rows(const char* path, int64_t brow_begin, int64_t brow_end, be_csb** out, double** diag,
                            int64_t* ndiag);
+/* The same CSB1 bytes in memory (save_csb / load_csb on std::ostream /
+ * std::istream, csb.hpp:245-290): *bytes is released with be_free_buffer;
+ * a bad magic or a truncated buffer is BE_ERR_PARSE. */
+be_status be_csb_save_mem(const be_csb_view* view, const double* diag, int64_t ndiag, char** bytes, int64_t* len);
+be_status be_csb_load_mem(const char* bytes, int64_t len, be_csb** out, double** diag, int64_t* ndiag);
 void be_free_buffer(void* p);
 
 /* Matrix Market ingest (ingest_matrix_market / _file, matrix_market.hpp:38-94):
@@ -270,6 +275,14 @@ be_status be_tiles_count(const be_tiles* t, int64_t* count, int64_t* dim, int64_
  * device incremented by the number of singular columns (may be NULL). */
 be_status be_precond_apply(be_tiles* t, const double* shifts_dev, const double* R_dev, double* W_dev,
                            int64_t nrows, int nb, int m, int64_t* fallbacks_dev, void* stream);
+/* Tiles given explicitly in the reference's SparseTile layout (precond.hpp:18-30):
+ * tile j has dims[j] rows (consecutive row ranges), entries
+ * [entry_offsets[j], entry_offsets[j+1]) of rows / cols / values (tile-local
+ * indices) and its diagonal slots at diag_pos[sum(dims[<j]) + i] (relative to
+ * the tile's first entry). Used by the mirror's fom_solve_tile. */
+be_status be_tiles_create_explicit(be_ctx* ctx, int64_t ntiles, const int64_t* dims, const int64_t* entry_offsets,
+                                   const int32_t* rows, const int32_t* cols, const double* values,
+                                   const int64_t* diag_pos, be_tiles** out);
 be_status be_precond_apply_host(be_tiles* t, const double* shifts, const double* R, double* W,
                                 int64_t nrows, int nb, int m, int64_t* fallbacks);
 
@@ -284,14 +297,18 @@ typedef struct be_solver_config { /* SolverConfig lobpcg.hpp:24-48 */
     int maxiter;
     int fom_iterations;     /* FomConfig::iterations precond.hpp:51-57 */
     uint64_t seed;
-    int observer_state;     /* 1: copy X and HX to host for the observer */
+    int observer_state;     /* 1: copy the SolverState panels to host for the observer */
 } be_solver_config;
 
-/* Per-iteration hook (SolverConfig::observer, lobpcg.hpp:33-34, 436).
- * x and hx are host n x nb copies when observer_state, else NULL. */
+/* Per-iteration hook (SolverConfig::observer, lobpcg.hpp:33-34, 436) with the
+ * SolverState of lobpcg.hpp:52-58: x, hx, w, hw, p, hp are host n x nb copies
+ * of X, HX, the iteration's W and HW, and the updated P, HP when
+ * observer_state, else NULL (p_active is true after every iteration,
+ * lobpcg.hpp:406). */
 typedef void (*be_observer_fn)(void* user, int iter, int64_t n, int nb, const double* theta,
                                const double* residual_norms, int n_converged, const double* x,
-                               const double* hx);
+                               const double* hx, const double* w, const double* hw, const double* p,
+                               const double* hp);
 /* Generic host operator (lobpcg.hpp:20): out = H in on host panels. */
 typedef int (*be_host_operator_fn)(void* user, const double* in, double* out, int64_t n, int nb);
 
@@ -423,6 +440,38 @@ be_status be_gram(be_ctx* ctx, const double* A_dev, int p, const double* B_dev, 
  * c (n x k column-major) and d (k), computed on the device. */
 be_status be_sygv_lowest(be_ctx* ctx, const double* A, const double* B, int n, int k,
                          double pivot_floor, double* c, double* d);
+
+/* The n-row panel functions of densela.hpp / lobpcg.hpp on HOST buffers (the
+ * C++ mirror's entry points, used by the reference's own unit suites): the
+ * panels are uploaded, the solver's device kernels run, the results come
+ * back. Panels are row-major n x w, small matrices column-major. */
+/* gram (densela.hpp:70-99): out (p x q) = A^T B; same != 0 symmetrises (gram(a, a)) */
+be_status be_dense_gram(be_ctx* ctx, const double* A, int p, const double* B, int q, int64_t n, int same,
+                        double* out);
+/* cholesky (rel_floor = 0, densela.hpp:103-121) / cholesky_floored (densela.hpp:155-175):
+ * R upper, B = R^T R; BE_ERR_NOT_POSITIVE_DEFINITE with the pivot index */
+be_status be_dense_cholesky(be_ctx* ctx, const double* B, int n, double rel_floor, double* R);
+/* trsm_right_inv (densela.hpp:125-147): W <- W R^{-1}; BE_ERR_SINGULAR_TRIANGULAR */
+be_status be_dense_trsm(be_ctx* ctx, double* W, int64_t n, int nb, const double* R);
+/* qr_of_transpose (densela.hpp:412-445): X <- Q, R (nb x nb) with X = Q R; BE_ERR_RANK_DEFICIENT */
+be_status be_dense_qr(be_ctx* ctx, double* X, int64_t n, int nb, double* R);
+/* block_times_small(_add) (densela.hpp:448-484): Y (n x q) (+)= X (n x p) C (p x q) */
+be_status be_dense_mix(be_ctx* ctx, const double* X, int64_t n, int p, const double* C, int q, double* Y,
+                       int accumulate);
+/* residual_block (lobpcg.hpp:197-213) + the column sums of squares of R and X (may be NULL) */
+be_status be_dense_residual(be_ctx* ctx, const double* HX, const double* X, const double* theta, int64_t n, int nb,
+                            double* R, double* rnorm2, double* xnorm2);
+/* per-column sums of squares (column_norm^2, block_vector.hpp:55-62) */
+be_status be_dense_colnorm2(be_ctx* ctx, const double* A, int64_t n, int nb, double* out);
+/* rayleigh_ritz (lobpcg.hpp:113-157): c ((2 or 3) nb x k_keep, column-major), theta (k_keep);
+ * P and HP both NULL for the 2 nb pencil; BE_ERR_BASIS_DEGENERATE on a failed overlap Cholesky */
+be_status be_rayleigh_ritz(be_ctx* ctx, const double* X, const double* W, const double* P, const double* HX,
+                           const double* HW, const double* HP, int64_t n, int nb, int k_keep, double* c,
+                           double* theta);
+/* update_blocks (lobpcg.hpp:168-194): C1, C2, C3 are nb x m; outputs n x m (P, HP, C3 NULL without P) */
+be_status be_update_blocks(be_ctx* ctx, const double* X, const double* W, const double* P, const double* HX,
+                           const double* HW, const double* HP, int64_t n, int nb, int m, const double* C1,
+                           const double* C2, const double* C3, double* Xo, double* HXo, double* Po, double* HPo);
 
 #ifdef __cplusplus
 }

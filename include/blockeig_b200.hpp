@@ -14,8 +14,10 @@
 //     KernelVariant gains the tag Sm100a (the default), the three reference
 //     names stay parseable and select the same device kernel.
 //   * DiagonalTileSet returned by extract_tiles carries its device copy;
-//     a hand-assembled DiagonalTileSet is rejected with BadParams by
-//     apply_preconditioner / lobpcg_solve.
+//     a hand-assembled DiagonalTileSet is uploaded for each
+//     apply_preconditioner / lobpcg_solve call that uses it.
+//   * The reference's KernelVariant names keep its f64 arithmetic (f64 values
+//     on the device); KernelVariant::sm100a() selects the f32-valued fast path.
 //   * ThreadPool is accepted and ignored (device kernels are the workers).
 #pragma once
 
@@ -300,6 +302,24 @@ inline bool is_strictly_lower(const CsbCooMatrix& m) {
     return r != 0;
 }
 
+// CSB1 cache on streams (csb.hpp:245-290): the bytes are produced and parsed by
+// the library (be_csb_save_mem / be_csb_load_mem); load_csb consumes the rest
+// of the stream
+inline void save_csb(std::ostream& os, const CsbCooMatrix& m) {
+    const be_csb_view v = m.view();
+    char* b = nullptr;
+    int64_t len = 0;
+    b200::check(be_csb_save_mem(&v, nullptr, 0, &b, &len));
+    os.write(b, static_cast<std::streamsize>(len));
+    be_free_buffer(b);
+}
+inline CsbCooMatrix load_csb(std::istream& is) {
+    const std::string bytes((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+    be_csb* h = nullptr;
+    b200::check(be_csb_load_mem(bytes.data(), static_cast<int64_t>(bytes.size()), &h, nullptr, nullptr));
+    return b200::take(h);
+}
+
 // CSB1 cache files (csb.hpp:292-302); the diagonal section of
 // driver.hpp:136-161 is written when diag is non-empty
 inline void save_csb_file(const std::string& path, const CsbCooMatrix& m, std::span<const double> diag = {}) {
@@ -364,11 +384,15 @@ inline void write_matrix_market(std::ostream& os, const SymmetricCoo& m) {  // m
 // --------------------------------------------------------------- kernels.hpp
 enum class KernelTag { Baseline, FusedAtomic, CacheBlocked, Sm100a };
 
+// The reference's three names keep the reference's arithmetic contract (f64 stored values:
+// results within ~1e-12 of the fp64 CPU kernels, kernels.hpp test bounds); the new Sm100a tag
+// selects the f32-valued fast path (8 B/nnz, 1e-5 relative, the headline bench) unless
+// KernelVariant::sm100a(BE_F64) asks for f64 values. All four run the same device kernel.
 struct KernelVariant {  // kernels.hpp:25-49
-    KernelTag tag = KernelTag::Sm100a;
+    KernelTag tag = KernelTag::Baseline;
     int cache_size = 256;
     int vector_width = 256;
-    be_prec values = BE_F32;  // stored-value precision on the device (BE_F64 = 12 B/nnz parity mode)
+    be_prec values = BE_F64;  // stored-value precision on the device
 
     static KernelVariant baseline() { return {KernelTag::Baseline}; }
     static KernelVariant fused_atomic() { return {KernelTag::FusedAtomic}; }
@@ -545,6 +569,8 @@ struct FomConfig {  // precond.hpp:51-57
 // and the host SparseTile copies filled
 inline DiagonalTileSet extract_tiles(const CsbCooMatrix& l, std::span<const double> d,
                                      const std::vector<index_t>& tile_offsets, bool host_copies = true) {
+    if (l.nrows != l.ncols) throw DimensionMismatch("extract_tiles: matrix must be square");
+    if (static_cast<index_t>(d.size()) != l.nrows) throw DimensionMismatch("extract_tiles: diagonal length mismatch");
     const be_csb_view v = l.view();
     be_tiles* t = nullptr;
     b200::check(be_tiles_create(b200::context(), &v, d.data(), tile_offsets.data(),
@@ -557,6 +583,34 @@ inline DiagonalTileSet extract_tiles(const CsbCooMatrix& l, std::span<const doub
 }
 
 // precond.hpp:287-317: W = K^{-1} R, per-column shifts, singular -> raw column
+namespace b200 {
+// the device tiles of a set: extract_tiles' own copy, or (a hand-assembled DiagonalTileSet,
+// precond.hpp:34-49) its host SparseTiles uploaded for the call
+inline std::shared_ptr<be_tiles> device_tiles(const DiagonalTileSet& set) {
+    if (set.device) return set.device;
+    if (set.tile_offsets.size() < 2 || set.tiles.size() + 1 != set.tile_offsets.size())
+        throw BadParams("DiagonalTileSet: tile_offsets and tiles disagree");
+    std::vector<int64_t> dims, eoff(1, 0), dpos;
+    std::vector<std::int32_t> rows, cols;
+    std::vector<double> vals;
+    for (std::size_t j = 0; j < set.tiles.size(); ++j) {
+        const SparseTile& t = set.tiles[j];
+        if (t.dim != set.tile_offsets[j + 1] - set.tile_offsets[j])
+            throw DimensionMismatch("DiagonalTileSet: tile dim disagrees with tile_offsets");
+        dims.push_back(t.dim);
+        rows.insert(rows.end(), t.rows.begin(), t.rows.end());
+        cols.insert(cols.end(), t.cols.begin(), t.cols.end());
+        vals.insert(vals.end(), t.values.begin(), t.values.end());
+        eoff.push_back(static_cast<int64_t>(vals.size()));
+        dpos.insert(dpos.end(), t.diag_pos.begin(), t.diag_pos.end());
+    }
+    be_tiles* h = nullptr;
+    check(be_tiles_create_explicit(context(), static_cast<int64_t>(dims.size()), dims.data(), eoff.data(), rows.data(),
+                                   cols.data(), vals.data(), dpos.data(), &h));
+    return std::shared_ptr<be_tiles>(h, [](be_tiles* p) { be_tiles_destroy(p); });
+}
+}  // namespace b200
+
 inline BlockVector apply_preconditioner(const DiagonalTileSet& tiles, std::span<const double> shifts,
                                         const BlockVector& r, const FomConfig& cfg, ThreadPool* = nullptr,
                                         std::int64_t* fallbacks = nullptr) {
@@ -564,19 +618,218 @@ inline BlockVector apply_preconditioner(const DiagonalTileSet& tiles, std::span<
     if (r.nrows != tiles.dim()) throw DimensionMismatch("apply_preconditioner: residual rows != operator dim");
     if (static_cast<index_t>(shifts.size()) != r.nvec)
         throw DimensionMismatch("apply_preconditioner: one shift per column required");
-    if (!tiles.device) throw BadParams("apply_preconditioner: DiagonalTileSet was not built by extract_tiles");
+    const auto dev = b200::device_tiles(tiles);
     BlockVector w(r.nrows, r.nvec);
     std::int64_t fb = 0;
-    b200::check(be_precond_apply_host(tiles.device.get(), shifts.data(), r.data.data(), w.data.data(), r.nrows,
+    b200::check(be_precond_apply_host(dev.get(), shifts.data(), r.data.data(), w.data.data(), r.nrows,
                                       static_cast<int>(r.nvec), cfg.iterations, &fb));
     if (fallbacks) *fallbacks += fb;
     return w;
 }
 
+// fom_solve_tile (precond.hpp:265-281): the FOM solve of one tile, per column
+// with that column's shift, on the device (the tile is uploaded for the call);
+// a singular projected system throws SingularProjection, as the reference does
+inline BlockVector fom_solve_tile(const SparseTile& tile, std::span<const double> sigma, const BlockVector& rj,
+                                  int m) {
+    if (rj.nrows != tile.dim) throw DimensionMismatch("fom_solve_tile: residual rows != tile dim");
+    if (static_cast<index_t>(sigma.size()) != rj.nvec)
+        throw DimensionMismatch("fom_solve_tile: one shift per column required");
+    if (m < 1) throw BadParams("fom_solve_tile: need at least one iteration");
+    const int64_t dims[1] = {tile.dim};
+    const int64_t eoff[2] = {0, static_cast<int64_t>(tile.values.size())};
+    be_tiles* h = nullptr;
+    b200::check(be_tiles_create_explicit(b200::context(), 1, dims, eoff, tile.rows.data(), tile.cols.data(),
+                                         tile.values.data(), tile.diag_pos.data(), &h));
+    std::unique_ptr<be_tiles, be_status (*)(be_tiles*)> own(h, be_tiles_destroy);
+    BlockVector w(tile.dim, rj.nvec);
+    std::int64_t fb = 0;
+    b200::check(be_precond_apply_host(h, sigma.data(), rj.data.data(), w.data.data(), rj.nrows,
+                                      static_cast<int>(rj.nvec), m, &fb));
+    if (fb > 0) throw SingularProjection("fom_solve_tile: projected tridiagonal system is singular");
+    return w;
+}
+
+// ---------------------------------------------------------------- densela.hpp
+// SmallDense and its O(dim^2..dim^3) helpers (matmul, transpose, identity,
+// normalize_column_signs, the block placement of lobpcg.hpp:89-104) are small
+// projected-problem bookkeeping kept on the host as in the reference; every
+// function that touches an n-row panel (gram, trsm_right_inv, qr_of_transpose,
+// block_times_small(_add), residual_block, the norms of convergence_check,
+// rayleigh_ritz, update_blocks) and the factorisations / eigensolvers
+// (cholesky, sygv_lowest, sym_eig) run on the device through the C ABI.
+struct SmallDense {  // densela.hpp:19-47, column-major
+    int nrows = 0;
+    int ncols = 0;
+    std::vector<double> data;
+    SmallDense() = default;
+    SmallDense(int r, int c) : nrows(r), ncols(c), data(static_cast<std::size_t>(r) * c, 0.0) {}
+    static SmallDense identity(int n) {
+        SmallDense m(n, n);
+        for (int i = 0; i < n; ++i) m.at(i, i) = 1.0;
+        return m;
+    }
+    double& at(int i, int j) { return data[static_cast<std::size_t>(j) * nrows + i]; }
+    double at(int i, int j) const { return data[static_cast<std::size_t>(j) * nrows + i]; }
+    double max_abs() const {
+        double m = 0.0;
+        for (double v : data) m = std::max(m, std::abs(v));
+        return m;
+    }
+    double frobenius() const {
+        double s = 0.0;
+        for (double v : data) s += v * v;
+        return std::sqrt(s);
+    }
+};
+
+inline SmallDense matmul(const SmallDense& a, const SmallDense& b) {  // densela.hpp:49-59
+    if (a.ncols != b.nrows) throw DimensionMismatch("matmul: inner dimensions differ");
+    SmallDense c(a.nrows, b.ncols);
+    for (int j = 0; j < b.ncols; ++j)
+        for (int k = 0; k < a.ncols; ++k) {
+            const double bkj = b.at(k, j);
+            if (bkj == 0.0) continue;
+            for (int i = 0; i < a.nrows; ++i) c.at(i, j) += a.at(i, k) * bkj;
+        }
+    return c;
+}
+
+inline SmallDense transpose(const SmallDense& a) {  // densela.hpp:61-66
+    SmallDense t(a.ncols, a.nrows);
+    for (int j = 0; j < a.ncols; ++j)
+        for (int i = 0; i < a.nrows; ++i) t.at(j, i) = a.at(i, j);
+    return t;
+}
+
+// gram (densela.hpp:70-99): A^T B on the device; symmetrised when a and b are the same object
+inline SmallDense gram(const BlockVector& a, const BlockVector& b, ThreadPool* = nullptr) {
+    if (a.nrows != b.nrows) throw DimensionMismatch("gram: row counts differ");
+    SmallDense g(static_cast<int>(a.nvec), static_cast<int>(b.nvec));
+    if (a.nvec == 0 || b.nvec == 0) return g;
+    b200::check(be_dense_gram(b200::context(), a.data.data(), static_cast<int>(a.nvec), b.data.data(),
+                              static_cast<int>(b.nvec), a.nrows, &a == &b ? 1 : 0, g.data.data()));
+    return g;
+}
+
+// cholesky (densela.hpp:103-121): upper R with B = R^T R, NotPositiveDefinite at the first
+// non-positive pivot
+inline SmallDense cholesky(const SmallDense& b) {
+    if (b.nrows != b.ncols) throw DimensionMismatch("cholesky: matrix must be square");
+    SmallDense r(b.nrows, b.nrows);
+    if (b.nrows == 0) return r;
+    b200::check(be_dense_cholesky(b200::context(), b.data.data(), b.nrows, 0.0, r.data.data()));
+    return r;
+}
+
+// trsm_right_inv (densela.hpp:125-147): W <- W R^{-1} on the device
+inline void trsm_right_inv(BlockVector& w, const SmallDense& r, ThreadPool* = nullptr) {
+    if (r.nrows != r.ncols || r.nrows != static_cast<int>(w.nvec))
+        throw DimensionMismatch("trsm_right_inv: triangular factor does not conform");
+    if (r.nrows == 0) return;
+    b200::check(be_dense_trsm(b200::context(), w.data.data(), w.nrows, r.nrows, r.data.data()));
+}
+
+namespace detail {
+// cholesky_floored (densela.hpp:155-175)
+inline SmallDense cholesky_floored(const SmallDense& b, double rel_floor) {
+    if (b.nrows != b.ncols) throw DimensionMismatch("cholesky: matrix must be square");
+    SmallDense r(b.nrows, b.nrows);
+    if (b.nrows == 0) return r;
+    b200::check(be_dense_cholesky(b200::context(), b.data.data(), b.nrows, rel_floor, r.data.data()));
+    return r;
+}
+
+struct SymEig {  // densela.hpp:293-296
+    std::vector<double> values;  // ascending
+    SmallDense vectors;
+};
+
+// sym_eig (densela.hpp:299-325): the full spectrum, computed by the device eigensolver
+// (the pencil (A, I)); columns are orthonormal eigenvectors (sign-normalised)
+inline SymEig sym_eig(const SmallDense& a) {
+    if (a.nrows != a.ncols) throw DimensionMismatch("sym_eig: matrix must be square");
+    const int n = a.nrows;
+    SymEig out;
+    out.values.assign(static_cast<std::size_t>(n), 0.0);
+    out.vectors = SmallDense(n, n);
+    if (n == 0) return out;
+    const SmallDense eye = SmallDense::identity(n);
+    b200::check(be_sygv_lowest(b200::context(), a.data.data(), eye.data.data(), n, n, 0.0, out.vectors.data.data(),
+                               out.values.data()));
+    return out;
+}
+
+inline void normalize_column_signs(SmallDense& c) {  // densela.hpp:327-341
+    for (int j = 0; j < c.ncols; ++j) {
+        int arg = 0;
+        double best = -1.0;
+        for (int i = 0; i < c.nrows; ++i) {
+            const double v = std::abs(c.at(i, j));
+            if (v > best) {
+                best = v;
+                arg = i;
+            }
+        }
+        if (c.at(arg, j) < 0.0)
+            for (int i = 0; i < c.nrows; ++i) c.at(i, j) = -c.at(i, j);
+    }
+}
+}  // namespace detail
+
+struct SygvResult {  // densela.hpp:345-348
+    SmallDense c;
+    std::vector<double> d;
+};
+
+// sygv_lowest (densela.hpp:357-407) on the device
+inline SygvResult sygv_lowest(const SmallDense& ahat, const SmallDense& bhat, int k, double pivot_floor = 0.0) {
+    if (ahat.nrows != ahat.ncols || bhat.nrows != bhat.ncols || ahat.nrows != bhat.nrows)
+        throw DimensionMismatch("sygv_lowest: pencil matrices must be square and conforming");
+    const int n = ahat.nrows;
+    if (k < 1 || k > n) throw BadParams("sygv_lowest: k out of range");
+    SygvResult out;
+    out.c = SmallDense(n, k);
+    out.d.assign(static_cast<std::size_t>(k), 0.0);
+    b200::check(be_sygv_lowest(b200::context(), ahat.data.data(), bhat.data.data(), n, k, pivot_floor,
+                               out.c.data.data(), out.d.data()));
+    return out;
+}
+
+// qr_of_transpose (densela.hpp:412-445): CholQR2 with the boost retry, on the device
+inline SmallDense qr_of_transpose(BlockVector& x, ThreadPool* = nullptr) {
+    if (x.nvec > x.nrows) throw DimensionMismatch("qr_of_transpose: more columns than rows");
+    const int nb = static_cast<int>(x.nvec);
+    SmallDense r(nb, nb);
+    if (nb == 0) return r;
+    b200::check(be_dense_qr(b200::context(), x.data.data(), x.nrows, nb, r.data.data()));
+    return r;
+}
+
+// block_times_small (densela.hpp:448-465): Y = X C on the device
+inline BlockVector block_times_small(const BlockVector& x, const SmallDense& c, ThreadPool* = nullptr) {
+    if (static_cast<int>(x.nvec) != c.nrows)
+        throw DimensionMismatch("block_times_small: coefficient rows must match nvec");
+    BlockVector y(x.nrows, c.ncols);
+    if (c.nrows == 0 || c.ncols == 0) return y;
+    b200::check(be_dense_mix(b200::context(), x.data.data(), x.nrows, c.nrows, c.data.data(), c.ncols,
+                             y.data.data(), 0));
+    return y;
+}
+
+// block_times_small_add (densela.hpp:468-484): Y += X C on the device
+inline void block_times_small_add(BlockVector& y, const BlockVector& x, const SmallDense& c, ThreadPool* = nullptr) {
+    if (static_cast<int>(x.nvec) != c.nrows || static_cast<int>(y.nvec) != c.ncols || y.nrows != x.nrows)
+        throw DimensionMismatch("block_times_small_add: shapes do not conform");
+    if (c.nrows == 0 || c.ncols == 0) return;
+    b200::check(be_dense_mix(b200::context(), x.data.data(), x.nrows, c.nrows, c.data.data(), c.ncols,
+                             y.data.data(), 1));
+}
+
 // ---------------------------------------------------------------- lobpcg.hpp
 using Operator = std::function<void(const BlockVector& in, BlockVector& out)>;  // lobpcg.hpp:20
 
-struct SolverState {  // lobpcg.hpp:52-58 (w, p, hw, hp are not materialised)
+struct SolverState {  // lobpcg.hpp:52-58 (all six panels are host copies of the device state)
     BlockVector x, w, p, hx, hw, hp;
     std::vector<double> theta;
     std::vector<double> residual_norms;
@@ -629,6 +882,145 @@ struct SolveResult {  // lobpcg.hpp:75-80
     bool converged = false;
 };
 
+// ---------------------------------------------- lobpcg.hpp panel functions
+struct RayleighRitzResult {  // lobpcg.hpp:82-85
+    SmallDense c1, c2, c3;  // c3 is 0x0 when P is absent
+    std::vector<double> theta;
+};
+
+namespace detail {
+inline void place_block(SmallDense& g, int roff, int coff, const SmallDense& blk) {  // lobpcg.hpp:89-92
+    for (int j = 0; j < blk.ncols; ++j)
+        for (int i = 0; i < blk.nrows; ++i) g.at(roff + i, coff + j) = blk.at(i, j);
+}
+inline void mirror_lower(SmallDense& g) {  // lobpcg.hpp:94-97
+    for (int j = 0; j < g.ncols; ++j)
+        for (int i = j + 1; i < g.nrows; ++i) g.at(j, i) = g.at(i, j);
+}
+inline SmallDense rows_slice(const SmallDense& c, int begin, int count) {  // lobpcg.hpp:99-104
+    SmallDense out(count, c.ncols);
+    for (int j = 0; j < c.ncols; ++j)
+        for (int i = 0; i < count; ++i) out.at(i, j) = c.at(begin + i, j);
+    return out;
+}
+inline SmallDense negated(SmallDense m) {  // lobpcg.hpp:237-240
+    for (auto& v : m.data) v = -v;
+    return m;
+}
+}  // namespace detail
+
+// rayleigh_ritz (lobpcg.hpp:113-157): the 12 (6) lower Gram blocks in one device pass, the pencil
+// assembled and solved on the device (pivot floor 1e-10); BasisDegenerate on a failed overlap
+inline RayleighRitzResult rayleigh_ritz(const BlockVector& x, const BlockVector& w, const BlockVector* p,
+                                        const BlockVector& hx, const BlockVector& hw, const BlockVector* hp, int k_keep,
+                                        ThreadPool* = nullptr) {
+    const int nb = static_cast<int>(x.nvec);
+    const bool with_p = p != nullptr;
+    if (w.nvec != nb || (with_p && p->nvec != nb)) throw DimensionMismatch("rayleigh_ritz: basis parts must share nvec");
+    if ((with_p && hp == nullptr) || (!with_p && hp != nullptr))
+        throw DimensionMismatch("rayleigh_ritz: P and HP must be given together");
+    const int dim = with_p ? 3 * nb : 2 * nb;
+    if (k_keep < 1 || k_keep > dim) throw BadParams("sygv_lowest: k out of range");
+    SmallDense c(dim, k_keep);
+    RayleighRitzResult out;
+    out.theta.assign(static_cast<std::size_t>(k_keep), 0.0);
+    b200::check(be_rayleigh_ritz(b200::context(), x.data.data(), w.data.data(), with_p ? p->data.data() : nullptr,
+                                 hx.data.data(), hw.data.data(), with_p ? hp->data.data() : nullptr, x.nrows, nb,
+                                 k_keep, c.data.data(), out.theta.data()));
+    out.c1 = detail::rows_slice(c, 0, nb);
+    out.c2 = detail::rows_slice(c, nb, nb);
+    if (with_p) out.c3 = detail::rows_slice(c, 2 * nb, nb);
+    return out;
+}
+
+struct UpdatedBlocks {  // lobpcg.hpp:159-161
+    BlockVector x, hx, p, hp;
+};
+
+// update_blocks (lobpcg.hpp:168-194): the four row mixes in one device pass
+inline UpdatedBlocks update_blocks(const BlockVector& x, const BlockVector& w, const BlockVector* p,
+                                   const BlockVector& hx, const BlockVector& hw, const BlockVector* hp,
+                                   const SmallDense& c1, const SmallDense& c2, const SmallDense& c3,
+                                   ThreadPool* = nullptr) {
+    if (c1.nrows != static_cast<int>(x.nvec) || c2.nrows != static_cast<int>(w.nvec) || c1.ncols != c2.ncols)
+        throw DimensionMismatch("update_blocks: coefficient blocks do not conform");
+    const bool with_p = p != nullptr;
+    if (with_p && (c3.nrows != static_cast<int>(p->nvec) || c3.ncols != c1.ncols))
+        throw DimensionMismatch("update_blocks: C3 does not conform to P");
+    const int m = c1.ncols;
+    UpdatedBlocks out{BlockVector(x.nrows, m), BlockVector(x.nrows, m), BlockVector(x.nrows, m),
+                      BlockVector(x.nrows, m)};
+    if (m == 0 || x.nvec == 0) return out;
+    b200::check(be_update_blocks(b200::context(), x.data.data(), w.data.data(), with_p ? p->data.data() : nullptr,
+                                 hx.data.data(), hw.data.data(), with_p ? hp->data.data() : nullptr, x.nrows,
+                                 static_cast<int>(x.nvec), m, c1.data.data(), c2.data.data(),
+                                 with_p ? c3.data.data() : nullptr, out.x.data.data(), out.hx.data.data(),
+                                 out.p.data.data(), out.hp.data.data()));
+    return out;
+}
+
+// residual_block (lobpcg.hpp:197-213): R = HX - X diag(theta) on the device
+inline BlockVector residual_block(const BlockVector& hx, const BlockVector& x, std::span<const double> theta,
+                                  ThreadPool* = nullptr) {
+    require_same_shape(hx, x, "residual_block");
+    if (static_cast<index_t>(theta.size()) != x.nvec)
+        throw DimensionMismatch("residual_block: one theta per column required");
+    BlockVector r(x.nrows, x.nvec);
+    if (x.nvec == 0) return r;
+    b200::check(be_dense_residual(b200::context(), hx.data.data(), x.data.data(), theta.data(), x.nrows,
+                                  static_cast<int>(x.nvec), r.data.data(), nullptr, nullptr));
+    return r;
+}
+
+// convergence_check (lobpcg.hpp:216-233): column norms on the device, the test itself as written
+inline std::pair<std::vector<char>, int> convergence_check(const BlockVector& r, const BlockVector& x,
+                                                           std::span<const double> theta, double tol, int k) {
+    require_same_shape(r, x, "convergence_check");
+    std::vector<char> flags(static_cast<std::size_t>(x.nvec), 0);
+    if (x.nvec == 0) return {std::move(flags), 0};
+    std::vector<double> rn2(static_cast<std::size_t>(x.nvec)), xn2(static_cast<std::size_t>(x.nvec));
+    b200::check(be_dense_colnorm2(b200::context(), r.data.data(), r.nrows, static_cast<int>(r.nvec), rn2.data()));
+    b200::check(be_dense_colnorm2(b200::context(), x.data.data(), x.nrows, static_cast<int>(x.nvec), xn2.data()));
+    int n_converged = 0;
+    for (index_t v = 0; v < x.nvec; ++v) {
+        const double rn = std::sqrt(rn2[static_cast<std::size_t>(v)]);
+        const double xn = std::sqrt(xn2[static_cast<std::size_t>(v)]);
+        if (rn <= tol * std::max(1.0, std::abs(theta[static_cast<std::size_t>(v)])) * xn) {
+            flags[static_cast<std::size_t>(v)] = 1;
+            if (v < k) ++n_converged;
+        }
+    }
+    return {std::move(flags), n_converged};
+}
+
+namespace detail {
+// project_out (lobpcg.hpp:243-246): w -= basis (basis^T w)
+inline void project_out(BlockVector& w, const BlockVector& basis, ThreadPool* pool) {
+    const SmallDense coeff = gram(basis, w, pool);
+    block_times_small_add(w, basis, negated(coeff), pool);
+}
+// orthonormalize_pair (lobpcg.hpp:254-270)
+inline void orthonormalize_pair(BlockVector& a, BlockVector& ha, ThreadPool* pool) {
+    const SmallDense b = gram(a, a, pool);
+    try {
+        const SmallDense r = cholesky_floored(b, 1e-8);
+        trsm_right_inv(a, r, pool);
+        trsm_right_inv(ha, r, pool);
+        return;
+    } catch (const NotPositiveDefinite&) {
+    }
+    std::vector<double> n2(static_cast<std::size_t>(a.nvec));
+    b200::check(be_dense_colnorm2(b200::context(), a.data.data(), a.nrows, static_cast<int>(a.nvec), n2.data()));
+    SmallDense s(static_cast<int>(a.nvec), static_cast<int>(a.nvec));
+    for (index_t v = 0; v < a.nvec; ++v) {
+        const double an = std::sqrt(n2[static_cast<std::size_t>(v)]);
+        s.at(static_cast<int>(v), static_cast<int>(v)) = an > 1e-300 ? 1.0 / an : 1.0;
+    }
+    a = block_times_small(a, s, pool);
+    ha = block_times_small(ha, s, pool);
+}
+}  // namespace detail
+
 namespace b200 {
 struct Callbacks {
     const Operator* op = nullptr;
@@ -650,7 +1042,8 @@ inline int host_operator_trampoline(void* user, const double* in, double* out, i
     }
 }
 inline void observer_trampoline(void* user, int iter, int64_t n, int nb, const double* theta, const double* rn,
-                                int n_conv, const double* x, const double* hx) {
+                                int n_conv, const double* x, const double* hx, const double* w, const double* hw,
+                                const double* p, const double* hp) {
     auto* cb = static_cast<Callbacks*>(user);
     if (cb->error) return;
     try {
@@ -659,14 +1052,17 @@ inline void observer_trampoline(void* user, int iter, int64_t n, int nb, const d
         st.residual_norms.assign(rn, rn + nb);
         st.n_converged = n_conv;
         st.p_active = true;  // set after every update (lobpcg.hpp:406)
-        if (x) {
-            st.x = BlockVector(n, nb);
-            std::copy(x, x + n * nb, st.x.data.begin());
-        }
-        if (hx) {
-            st.hx = BlockVector(n, nb);
-            std::copy(hx, hx + n * nb, st.hx.data.begin());
-        }
+        auto fill = [&](BlockVector& b, const double* src) {
+            if (!src) return;
+            b = BlockVector(n, nb);
+            std::copy(src, src + n * nb, b.data.begin());
+        };
+        fill(st.x, x);
+        fill(st.hx, hx);
+        fill(st.w, w);
+        fill(st.hw, hw);
+        fill(st.p, p);
+        fill(st.hp, hp);
         cb->cfg->observer(st, iter);
     } catch (...) {
         cb->error = std::current_exception();
@@ -676,7 +1072,7 @@ inline SolveResult solve(be_op* op, const Operator* host_op, index_t n, const Di
                          const BlockVector* x0, const SolverConfig& cfg) {
     cfg.validate(n);
     if (precond && precond->dim() != n) throw DimensionMismatch("lobpcg_solve: preconditioner dimension mismatch");
-    if (precond && !precond->device) throw BadParams("lobpcg_solve: DiagonalTileSet was not built by extract_tiles");
+    const auto pdev = precond ? device_tiles(*precond) : nullptr;
     const int nb = cfg.block_width();
     if (x0 && (x0->nrows != n || x0->nvec != nb)) throw DimensionMismatch("lobpcg_solve: x0 shape");
     Callbacks cb{host_op, &cfg, nullptr};
@@ -684,7 +1080,7 @@ inline SolveResult solve(be_op* op, const Operator* host_op, index_t n, const Di
     be_result* res = nullptr;
     const be_status st =
         be_lobpcg_solve(context(), op, host_op ? host_operator_trampoline : nullptr, &cb, n,
-                        precond ? precond->device.get() : nullptr, x0 ? x0->data.data() : nullptr, &c,
+                        pdev.get(), x0 ? x0->data.data() : nullptr, &c,
                         cfg.observer ? observer_trampoline : nullptr, &cb, &res);
     if (cb.error) {
         if (res) be_result_free(res);

@@ -107,7 +107,7 @@ class ResultInfo(C.Structure):
 
 
 OBSERVER_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.c_int64, C.c_int, C.POINTER(C.c_double),
-                          C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double))
+                          C.POINTER(C.c_double), C.c_int, *([C.POINTER(C.c_double)] * 6))
 HOST_OP_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64, C.c_int)
 
 _lib = None
@@ -787,22 +787,27 @@ def _x0_checked(x0, n, k, nb):
 
 
 def lobpcg(ctx: Context, op=None, n=None, tiles: Tiles | None = None, x0=None, k=5, nb=0, tol=1e-6, maxiter=500,
-           fom_iterations=4, seed=1234, observer=None, observer_state=False, host_operator=None):
+           fom_iterations=4, seed=1234, observer=None, observer_state=False, host_operator=None,
+           observer_panels=False):
     """lobpcg_solve (lobpcg.hpp:291-456) on the device. `op` is an Operator;
     `host_operator(x) -> y` is the generic Operator closure (lobpcg.hpp:20).
-    observer(iter, theta, residual_norms, n_converged, x, hx)."""
+    observer(iter, theta, residual_norms, n_converged, x, hx), or with
+    observer_panels=True observer(iter, theta, residual_norms, n_converged, state)
+    where state holds the six SolverState panels x, hx, w, hw, p, hp."""
     if n is None:
         n = op.info().nrows
-    cfg = SolverConfig(k, nb, tol, maxiter, fom_iterations, seed, 1 if observer_state else 0)
+    cfg = SolverConfig(k, nb, tol, maxiter, fom_iterations, seed, 1 if (observer_state or observer_panels) else 0)
     x0a = _x0_checked(x0, n, k, nb)
     obs_cb = OBSERVER_FN()
     if observer is not None:
-        def _obs(user, it, nn, nbb, th, rn, nc, x, hx):
+        def _obs(user, it, nn, nbb, th, rn, nc, x, hx, w, hw, p, hp):
             thv = np.ctypeslib.as_array(th, shape=(nbb,)).copy()
             rnv = np.ctypeslib.as_array(rn, shape=(nbb,)).copy()
-            xv = np.ctypeslib.as_array(x, shape=(nn, nbb)).copy() if x else None
-            hxv = np.ctypeslib.as_array(hx, shape=(nn, nbb)).copy() if hx else None
-            observer(it, thv, rnv, nc, xv, hxv)
+            pan = [np.ctypeslib.as_array(a, shape=(nn, nbb)).copy() if a else None for a in (x, hx, w, hw, p, hp)]
+            if observer_panels:  # the whole SolverState (lobpcg.hpp:52-58)
+                observer(it, thv, rnv, nc, dict(zip(("x", "hx", "w", "hw", "p", "hp"), pan)))
+            else:
+                observer(it, thv, rnv, nc, pan[0], pan[1])
         obs_cb = OBSERVER_FN(_obs)
     hop_cb = HOST_OP_FN()
     if host_operator is not None:

@@ -88,5 +88,50 @@ def build_cpp_tests(verbose: bool = False) -> Path:
     return MIRROR_BIN
 
 
+REF_TESTS = Path("/root/reference/proj/tests")
+REFSUITE = ROOT / "tests" / "refsuite"
+REFSUITE_BIN = REFSUITE / "bin"
+REF_SUITES = ("test_kernels", "test_precond", "test_lobpcg", "test_densela", "test_csb")
+
+
+def build_refsuite(verbose: bool = False) -> dict:
+    """Compile the reference's OWN unit suites (/root/reference/proj/tests/test_*.cpp,
+    unmodified, read in place) against the C++ mirror header: their
+    #include "blockeig/*.hpp" resolve to tests/refsuite/include/blockeig/ (forwarders
+    to include/blockeig_b200.hpp) and <doctest.h> to the minimal doctest shim. The
+    binaries land in tests/refsuite/bin/ (git-ignored, shipped to the GPU box like
+    the library). Only possible where /root/reference exists (this container);
+    returns {suite: "ok" | error text}."""
+    lib = build_lib(verbose)
+    out = {}
+    if not REF_TESTS.is_dir():
+        return out
+    REFSUITE_BIN.mkdir(parents=True, exist_ok=True)
+    inc = REFSUITE / "include"
+    deps = [ROOT / "include" / "blockeig_b200.hpp", ROOT / "include" / "blockeig_b200.h", lib, inc / "doctest.h"]
+    newest_dep = max(d.stat().st_mtime for d in deps)
+
+    def one(name):
+        src = REF_TESTS / f"{name}.cpp"
+        exe = REFSUITE_BIN / name
+        if exe.exists() and exe.stat().st_mtime >= max(newest_dep, src.stat().st_mtime):
+            return name, "ok"
+        cmd = [CXX, "-std=c++20", "-O2", "-I", str(inc), "-I", str(ROOT / "include"), str(src), "-L", str(PKG),
+               "-lblockeig_b200", "-Wl,-rpath," + str(PKG), "-o", str(exe)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            if exe.exists():
+                exe.unlink()
+            return name, (r.stderr or r.stdout)[-4000:]
+        return name, "ok"
+
+    with cf.ThreadPoolExecutor(max_workers=len(REF_SUITES)) as ex:
+        for name, res in ex.map(one, REF_SUITES):
+            out[name] = res
+    return out
+
+
 if __name__ == "__main__":
     print(build_lib(verbose="-v" in sys.argv))

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <sstream>
 #include <tuple>
 #include <vector>
 #include <string>
@@ -123,6 +124,38 @@ be_status be_csb_load(const char* path, be_csb** out, double** diag, int64_t* nd
         if (!path || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
         std::vector<double> d;
         auto m = be::load_csb1(path, diag ? &d : nullptr);
+        if (diag) {
+            *diag = nullptr;
+            if (!d.empty()) {
+                *diag = static_cast<double*>(std::malloc(d.size() * sizeof(double)));
+                std::memcpy(*diag, d.data(), d.size() * sizeof(double));
+            }
+            if (ndiag) *ndiag = static_cast<int64_t>(d.size());
+        }
+        *out = new be_csb{std::move(m)};
+    });
+}
+
+be_status be_csb_save_mem(const be_csb_view* view, const double* diag, int64_t ndiag, char** bytes, int64_t* len) {
+    return guard([&] {
+        if (!view || !bytes || !len) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        be::validate_view(*view);
+        std::ostringstream os(std::ios::binary);
+        be::save_csb1(os, *view, diag, ndiag);
+        const std::string b = os.str();
+        *bytes = static_cast<char*>(std::malloc(std::max<std::size_t>(b.size(), 1)));
+        if (!*bytes) be::fail(BE_ERR_OUT_OF_MEMORY, "be_csb_save_mem: host allocation failed");
+        std::memcpy(*bytes, b.data(), b.size());
+        *len = static_cast<int64_t>(b.size());
+    });
+}
+
+be_status be_csb_load_mem(const char* bytes, int64_t len, be_csb** out, double** diag, int64_t* ndiag) {
+    return guard([&] {
+        if ((!bytes && len > 0) || len < 0 || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        std::istringstream is(std::string(bytes ? bytes : "", static_cast<std::size_t>(len)), std::ios::binary);
+        std::vector<double> d;
+        auto m = be::load_csb1(is, diag ? &d : nullptr);
         if (diag) {
             *diag = nullptr;
             if (!d.empty()) {
@@ -686,6 +719,30 @@ be_status be_precond_apply(be_tiles* t, const double* shifts_dev, const double* 
     });
 }
 
+be_status be_tiles_create_explicit(be_ctx* ctx, int64_t ntiles, const int64_t* dims, const int64_t* entry_offsets,
+                                   const int32_t* rows, const int32_t* cols, const double* values,
+                                   const int64_t* diag_pos, be_tiles** out) {
+    return guard([&] {
+        if (!ctx || !out || ntiles < 0 || (ntiles > 0 && (!dims || !entry_offsets || !diag_pos)))
+            be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        std::vector<be::HostTile> ts(static_cast<std::size_t>(ntiles));
+        int64_t row0 = 0;
+        for (int64_t j = 0; j < ntiles; ++j) {
+            auto& T = ts[static_cast<std::size_t>(j)];
+            T.dim = dims[j];
+            const int64_t e0 = entry_offsets[j], e1 = entry_offsets[j + 1];
+            if (e1 < e0) be::fail(BE_ERR_BAD_PARAMS, "be_tiles_create_explicit: entry offsets must not decrease");
+            if (e1 > e0 && (!rows || !cols || !values)) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+            T.rows.assign(rows + e0, rows + e1);
+            T.cols.assign(cols + e0, cols + e1);
+            T.vals.assign(values + e0, values + e1);
+            if (T.dim > 0) T.diag_pos.assign(diag_pos + row0, diag_pos + row0 + T.dim);
+            row0 += std::max<int64_t>(T.dim, 0);
+        }
+        *out = new be_tiles{be::tiles_create_explicit(ctx->impl.get(), ts)};
+    });
+}
+
 be_status be_precond_apply_host(be_tiles* t, const double* shifts, const double* R, double* W, int64_t nrows, int nb,
                                 int m, int64_t* fallbacks) {
     return guard([&] {
@@ -837,6 +894,347 @@ be_status be_sygv_lowest(be_ctx* ctx, const double* A, const double* B, int n, i
         BE_CUDA(cudaMemcpyAsync(d, dd.get(), static_cast<std::size_t>(k) * 8, cudaMemcpyDeviceToHost, s));
         BE_CUDA(cudaStreamSynchronize(s));
         if (hs.not_pd) be::fail(BE_ERR_NOT_POSITIVE_DEFINITE, "cholesky: pivot below floor at index " + std::to_string(hs.not_pd - 1), hs.not_pd - 1);
+    });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------ dense, host buffers
+// The densela.hpp / lobpcg.hpp panel functions on host buffers (the C++
+// mirror's entry points for the reference's own unit suites): panels are
+// uploaded, the solver's device kernels run, results come back. Widths that
+// differ (p != q) run on zero-padded square panels.
+namespace {
+
+struct Staged {  // an n x m device panel holding a host n x w panel in its first w columns
+    be::DBuf<double> d;
+    int m = 0;
+    void up(const double* h, int64_t n, int w, int m_, cudaStream_t s) {
+        m = m_;
+        d.reset(std::max<int64_t>(n * m, 1));
+        if (w != m || !h) BE_CUDA(cudaMemsetAsync(d.get(), 0, d.bytes(), s));
+        if (h && n > 0 && w > 0)
+            BE_CUDA(cudaMemcpy2DAsync(d.get(), static_cast<std::size_t>(m) * 8, h, static_cast<std::size_t>(w) * 8,
+                                      static_cast<std::size_t>(w) * 8, static_cast<std::size_t>(n),
+                                      cudaMemcpyHostToDevice, s));
+    }
+    void down(double* h, int64_t n, int w, cudaStream_t s) const {
+        if (n > 0 && w > 0)
+            BE_CUDA(cudaMemcpy2DAsync(h, static_cast<std::size_t>(w) * 8, d.get(), static_cast<std::size_t>(m) * 8,
+                                      static_cast<std::size_t>(w) * 8, static_cast<std::size_t>(n),
+                                      cudaMemcpyDeviceToHost, s));
+    }
+};
+
+// a small q x q column-major matrix zero-padded into the top-left of an m x m one
+be::DBuf<double> small_up(const double* h, int r, int c, int m, cudaStream_t s) {
+    std::vector<double> p(static_cast<std::size_t>(m) * m, 0.0);
+    for (int j = 0; j < c; ++j)
+        for (int i = 0; i < r; ++i) p[static_cast<std::size_t>(j) * m + i] = h[static_cast<std::size_t>(j) * r + i];
+    be::DBuf<double> d(static_cast<int64_t>(m) * m);
+    BE_CUDA(cudaMemcpyAsync(d.get(), p.data(), p.size() * 8, cudaMemcpyHostToDevice, s));
+    BE_CUDA(cudaStreamSynchronize(s));  // p is a temporary
+    return d;
+}
+
+be::dla::Status read_status(const be::DBuf<be::dla::Status>& st, cudaStream_t s) {
+    be::dla::Status h{};
+    BE_CUDA(cudaMemcpyAsync(&h, st.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    BE_CUDA(cudaStreamSynchronize(s));
+    return h;
+}
+
+void gram_dev(be::Ctx* c, const double* a, const double* b, int m, int sym, int64_t n, double* out, cudaStream_t s) {
+    const int64_t plen = be::dla::gram_partials_len(m, 1, c->num_sms);
+    be::DBuf<double> part(plen);
+    be::dla::GramJob j{};
+    j.npairs = 1;
+    j.nb = m;
+    j.a[0] = a;
+    j.b[0] = b;
+    j.sym[0] = sym;
+    j.out[0] = out;
+    be::dla::gram(c, j, n, part.get(), plen, s);
+    BE_CUDA(cudaStreamSynchronize(s));  // part is released on return
+}
+
+}  // namespace
+
+extern "C" {
+
+be_status be_dense_gram(be_ctx* ctx, const double* A, int p, const double* B, int q, int64_t n, int same,
+                        double* out) {
+    return guard([&] {
+        if (!ctx || !out || (n > 0 && (!A || !B)) || p < 1 || q < 1 || n < 0) be::fail(BE_ERR_BAD_PARAMS, "bad argument");
+        if (p > 64 || q > 64) be::fail(BE_ERR_BAD_PARAMS, "gram: panel wider than 64 columns");
+        auto* c = ctx->impl.get();
+        cudaStream_t s = c->stream;
+        const int m = std::max(p, q);
+        Staged a, b;
+        a.up(A, n, p, m, s);
+        if (!same) b.up(B, n, q, m, s);
+        be::DBuf<double> o(static_cast<int64_t>(m) * m);
+        gram_dev(c, a.d.get(), same ? a.d.get() : b.d.get(), m, same ? 1 : 0, n, o.get(), s);
+        std::vector<double> h(static_cast<std::size_t>(m) * m);
+        BE_CUDA(cudaMemcpy(h.data(), o.get(), h.size() * 8, cudaMemcpyDeviceToHost));
+        for (int j = 0; j < q; ++j)
+            for (int i = 0; i < p; ++i) out[static_cast<std::size_t>(j) * p + i] = h[static_cast<std::size_t>(j) * m + i];
+    });
+}
+
+be_status be_dense_cholesky(be_ctx* ctx, const double* B, int n, double rel_floor, double* R) {
+    return guard([&] {
+        if (!ctx || !B || !R || n < 1) be::fail(BE_ERR_BAD_PARAMS, "bad argument");
+        auto* c = ctx->impl.get();
+        cudaStream_t s = c->stream;
+        be::DBuf<double> dB = small_up(B, n, n, n, s), dR(static_cast<int64_t>(n) * n);
+        be::DBuf<be::dla::Status> st(1);
+        BE_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(be::dla::Status), s));
+        be::dla::chol_floored(c, dB.get(), dR.get(), n, rel_floor, st.get(), s);
+        BE_CUDA(cudaMemcpyAsync(R, dR.get(), static_cast<std::size_t>(n) * n * 8, cudaMemcpyDeviceToHost, s));
+        const auto h = read_status(st, s);
+        if (h.not_pd)
+            be::fail(BE_ERR_NOT_POSITIVE_DEFINITE,
+                     std::string(rel_floor > 0 ? "cholesky: pivot below floor at index " : "cholesky: non-positive pivot at index ") +
+                         std::to_string(h.not_pd - 1),
+                     h.not_pd - 1);
+    });
+}
+
+be_status be_dense_trsm(be_ctx* ctx, double* W, int64_t n, int nb, const double* R) {
+    return guard([&] {
+        if (!ctx || !R || (n > 0 && !W) || nb < 1 || n < 0) be::fail(BE_ERR_BAD_PARAMS, "bad argument");
+        auto* c = ctx->impl.get();
+        cudaStream_t s = c->stream;
+        Staged w;
+        w.up(W, n, nb, nb, s);
+        be::DBuf<double> dR = small_up(R, nb, nb, nb, s);
+        be::DBuf<be::dla::Status> st(1);
+        BE_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(be::dla::Status), s));
+        be::dla::trsm(c, w.d.get(), nullptr, dR.get(), nb, std::max<int64_t>(n, 0), st.get(), 0, 0, s);
+        const auto h = read_status(st, s);
+        if (h.singular_tri) be::fail(BE_ERR_SINGULAR_TRIANGULAR, "trsm_right_inv: triangular factor is numerically singular");
+        w.down(W, n, nb, s);
+        BE_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+be_status be_dense_qr(be_ctx* ctx, double* X, int64_t n, int nb, double* R) {
+    return guard([&] {
+        if (!ctx || !R || (n > 0 && !X) || nb < 1) be::fail(BE_ERR_BAD_PARAMS, "bad argument");
+        if (nb > n) be::fail(BE_ERR_DIMENSION_MISMATCH, "qr_of_transpose: more columns than rows");
+        auto* c = ctx->impl.get();
+        cudaStream_t s = c->stream;
+        Staged x;
+        x.up(X, n, nb, nb, s);
+        const int64_t nb2 = static_cast<int64_t>(nb) * nb;
+        be::DBuf<double> Bq(nb2), Rq(2 * nb2);
+        be::DBuf<be::dla::Status> st(1);
+        BE_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(be::dla::Status), s));
+        for (int pass = 0; pass < 2; ++pass) {  // densela.hpp:412-445 (rtot = R2 R1)
+            gram_dev(c, x.d.get(), x.d.get(), nb, 1, n, Bq.get(), s);
+            be::dla::qr_chol(c, Bq.get(), Rq.get() + pass * nb2, nb, st.get(), s);
+            be::dla::trsm(c, x.d.get(), nullptr, Rq.get() + pass * nb2, nb, n, st.get(), 1, 0, s);
+        }
+        const auto h = read_status(st, s);
+        if (h.rank_deficient) be::fail(BE_ERR_RANK_DEFICIENT, "qr_of_transpose: Gram matrix is numerically rank deficient");
+        if (h.singular_tri) be::fail(BE_ERR_SINGULAR_TRIANGULAR, "trsm_right_inv: triangular factor is numerically singular");
+        std::vector<double> r(static_cast<std::size_t>(2 * nb2));
+        BE_CUDA(cudaMemcpy(r.data(), Rq.get(), r.size() * 8, cudaMemcpyDeviceToHost));
+        x.down(X, n, nb, s);
+        BE_CUDA(cudaStreamSynchronize(s));
+        // rtot = matmul(R2, R1) (both upper triangular, nb x nb): the small product on the host
+        const double* r1 = r.data();
+        const double* r2 = r.data() + nb2;
+        for (int j = 0; j < nb; ++j)
+            for (int i = 0; i < nb; ++i) {
+                double acc = 0.0;
+                for (int k = 0; k < nb; ++k) {
+                    const double b = r1[static_cast<std::size_t>(j) * nb + k];
+                    if (b == 0.0) continue;
+                    acc += r2[static_cast<std::size_t>(k) * nb + i] * b;
+                }
+                R[static_cast<std::size_t>(j) * nb + i] = acc;
+            }
+    });
+}
+
+be_status be_dense_mix(be_ctx* ctx, const double* X, int64_t n, int p, const double* C, int q, double* Y,
+                       int accumulate) {
+    return guard([&] {
+        if (!ctx || !C || (n > 0 && (!X || !Y)) || p < 1 || q < 1 || n < 0) be::fail(BE_ERR_BAD_PARAMS, "bad argument");
+        if (p > 64 || q > 64) be::fail(BE_ERR_BAD_PARAMS, "block_times_small: panel wider than 64 columns");
+        auto* c = ctx->impl.get();
+        cudaStream_t s = c->stream;
+        const int m = std::max(p, q);
+        Staged x, y;
+        x.up(X, n, p, m, s);
+        y.up(accumulate ? Y : nullptr, n, q, m, s);
+        be::DBuf<double> dC = small_up(C, p, q, m, s);
+        be::dla::MixJob job{};
+        job.nb = m;
+        job.nout = 1;
+        job.out[0] = be::dla::MixOut{y.d.get(), accumulate ? 1 : 0, 1, {{x.d.get(), dC.get(), 0, 0}}, -1};
+        if (n > 0) be::dla::mix(c, job, n, s);
+        y.down(Y, n, q, s);
+        BE_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+be_status be_dense_residual(be_ctx* ctx, const double* HX, const double* X, const double* theta, int64_t n, int nb,
+                            double* R, double* rnorm2, double* xnorm2) {
+    return guard([&] {
+        if (!ctx || !theta || (n > 0 && (!HX || !X || !R)) || nb < 1 || nb > 64 || n < 0)
+            be::fail(BE_ERR_BAD_PARAMS, "bad argument");
+        auto* c = ctx->impl.get();
+        cudaStream_t s = c->stream;
+        Staged hx, x, r;
+        hx.up(HX, n, nb, nb, s);
+        x.up(X, n, nb, nb, s);
+        r.up(nullptr, n, nb, nb, s);
+        be::DBuf<double> th(nb), norms(2 * nb), part(static_cast<int64_t>(c->num_sms) * 64 * 2 * nb);
+        BE_CUDA(cudaMemcpyAsync(th.get(), theta, static_cast<std::size_t>(nb) * 8, cudaMemcpyHostToDevice, s));
+        BE_CUDA(cudaMemsetAsync(norms.get(), 0, norms.bytes(), s));
+        if (n > 0) be::dla::residual(c, hx.d.get(), x.d.get(), th.get(), r.d.get(), nb, n, part.get(), norms.get(), norms.get() + nb, s);
+        r.down(R, n, nb, s);
+        std::vector<double> h(static_cast<std::size_t>(2 * nb));
+        BE_CUDA(cudaMemcpyAsync(h.data(), norms.get(), h.size() * 8, cudaMemcpyDeviceToHost, s));
+        BE_CUDA(cudaStreamSynchronize(s));
+        if (rnorm2) std::memcpy(rnorm2, h.data(), static_cast<std::size_t>(nb) * 8);
+        if (xnorm2) std::memcpy(xnorm2, h.data() + nb, static_cast<std::size_t>(nb) * 8);
+    });
+}
+
+be_status be_dense_colnorm2(be_ctx* ctx, const double* A, int64_t n, int nb, double* out) {
+    return guard([&] {
+        if (!ctx || !out || (n > 0 && !A) || nb < 1 || nb > 64 || n < 0) be::fail(BE_ERR_BAD_PARAMS, "bad argument");
+        auto* c = ctx->impl.get();
+        cudaStream_t s = c->stream;
+        Staged a;
+        a.up(A, n, nb, nb, s);
+        be::DBuf<double> o(nb), part(static_cast<int64_t>(c->num_sms) * 64 * 2 * nb);
+        BE_CUDA(cudaMemsetAsync(o.get(), 0, o.bytes(), s));
+        if (n > 0) be::dla::colnorm2(c, a.d.get(), nb, n, part.get(), o.get(), s);
+        BE_CUDA(cudaMemcpyAsync(out, o.get(), static_cast<std::size_t>(nb) * 8, cudaMemcpyDeviceToHost, s));
+        BE_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+be_status be_rayleigh_ritz(be_ctx* ctx, const double* X, const double* W, const double* P, const double* HX,
+                           const double* HW, const double* HP, int64_t n, int nb, int k_keep, double* c,
+                           double* theta) {
+    return guard([&] {
+        if (!ctx || !c || !theta || (n > 0 && (!X || !W || !HX || !HW)) || nb < 1 || nb > 64 || n < 0)
+            be::fail(BE_ERR_BAD_PARAMS, "bad argument");
+        if ((P == nullptr) != (HP == nullptr))
+            be::fail(BE_ERR_DIMENSION_MISMATCH, "rayleigh_ritz: P and HP must be given together");
+        const bool with_p = P != nullptr;
+        const int nblk = with_p ? 3 : 2, dim = nblk * nb;
+        if (k_keep < 1 || k_keep > dim) be::fail(BE_ERR_BAD_PARAMS, "sygv_lowest: k out of range");
+        auto* cx = ctx->impl.get();
+        cudaStream_t s = cx->stream;
+        Staged x, w, p, hx, hw, hp;
+        x.up(X, n, nb, nb, s);
+        w.up(W, n, nb, nb, s);
+        hx.up(HX, n, nb, nb, s);
+        hw.up(HW, n, nb, nb, s);
+        if (with_p) {
+            p.up(P, n, nb, nb, s);
+            hp.up(HP, n, nb, nb, s);
+        }
+        // the 6 (3) lower G blocks then the 6 (3) lower O blocks (lobpcg.hpp:126-141)
+        const double* pairs[12][2];
+        int sym[12], np = 0;
+        auto add = [&](const double* a, const double* b, int sy) {
+            pairs[np][0] = a;
+            pairs[np][1] = b;
+            sym[np++] = sy;
+        };
+        add(x.d.get(), hx.d.get(), 0);
+        add(w.d.get(), hx.d.get(), 0);
+        add(w.d.get(), hw.d.get(), 0);
+        if (with_p) {
+            add(p.d.get(), hx.d.get(), 0);
+            add(p.d.get(), hw.d.get(), 0);
+            add(p.d.get(), hp.d.get(), 0);
+        }
+        add(x.d.get(), x.d.get(), 1);
+        add(w.d.get(), x.d.get(), 0);
+        add(w.d.get(), w.d.get(), 1);
+        if (with_p) {
+            add(p.d.get(), x.d.get(), 0);
+            add(p.d.get(), w.d.get(), 0);
+            add(p.d.get(), p.d.get(), 1);
+        }
+        const int64_t nb2 = static_cast<int64_t>(nb) * nb;
+        be::DBuf<double> blocks(12 * nb2), G(static_cast<int64_t>(dim) * dim), O(static_cast<int64_t>(dim) * dim),
+            dc(static_cast<int64_t>(dim) * k_keep), dd(k_keep);
+        be::dla::GramJob j{};
+        j.npairs = np;
+        j.nb = nb;
+        for (int q = 0; q < np; ++q) {
+            j.a[q] = pairs[q][0];
+            j.b[q] = pairs[q][1];
+            j.sym[q] = sym[q];
+            j.out[q] = blocks.get() + q * nb2;
+        }
+        const int64_t plen = be::dla::gram_partials_len(nb, np, cx->num_sms);
+        be::DBuf<double> part(plen);
+        be::dla::gram(cx, j, n, part.get(), plen, s);
+        be::dla::rr_assemble(cx, blocks.get(), nb, nblk, G.get(), O.get(), s);
+        be::DBuf<be::dla::Status> st(1);
+        BE_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(be::dla::Status), s));
+        be::dla::Sygv ws;
+        be::dla::sygv_lowest(cx, ws, G.get(), O.get(), dim, k_keep, 1e-10, dc.get(), dd.get(), st.get(), s);
+        BE_CUDA(cudaMemcpyAsync(c, dc.get(), static_cast<std::size_t>(dim) * k_keep * 8, cudaMemcpyDeviceToHost, s));
+        BE_CUDA(cudaMemcpyAsync(theta, dd.get(), static_cast<std::size_t>(k_keep) * 8, cudaMemcpyDeviceToHost, s));
+        const auto h = read_status(st, s);
+        if (h.not_pd)
+            be::fail(BE_ERR_BASIS_DEGENERATE, "rayleigh_ritz: overlap matrix failed Cholesky (cholesky: pivot below floor at index " +
+                                                  std::to_string(h.not_pd - 1) + ")");
+    });
+}
+
+be_status be_update_blocks(be_ctx* ctx, const double* X, const double* W, const double* P, const double* HX,
+                           const double* HW, const double* HP, int64_t n, int nb, int m, const double* C1,
+                           const double* C2, const double* C3, double* Xo, double* HXo, double* Po, double* HPo) {
+    return guard([&] {
+        if (!ctx || !C1 || !C2 || (n > 0 && (!X || !W || !HX || !HW || !Xo || !HXo || !Po || !HPo)) || nb < 1 ||
+            m < 1 || nb > 64 || m > 64 || n < 0)
+            be::fail(BE_ERR_BAD_PARAMS, "bad argument");
+        if ((P == nullptr) != (HP == nullptr) || (P && !C3))
+            be::fail(BE_ERR_DIMENSION_MISMATCH, "update_blocks: P, HP and C3 must be given together");
+        auto* cx = ctx->impl.get();
+        cudaStream_t s = cx->stream;
+        const bool with_p = P != nullptr;
+        const int w2 = std::max(nb, m);  // square working width
+        Staged x, w, p, hx, hw, hp, xo, hxo, po, hpo;
+        x.up(X, n, nb, w2, s);
+        w.up(W, n, nb, w2, s);
+        hx.up(HX, n, nb, w2, s);
+        hw.up(HW, n, nb, w2, s);
+        if (with_p) {
+            p.up(P, n, nb, w2, s);
+            hp.up(HP, n, nb, w2, s);
+        }
+        for (auto* o : {&xo, &hxo, &po, &hpo}) o->up(nullptr, n, m, w2, s);
+        be::DBuf<double> c1 = small_up(C1, nb, m, w2, s), c2 = small_up(C2, nb, m, w2, s);
+        be::DBuf<double> c3;
+        if (with_p) c3 = small_up(C3, nb, m, w2, s);
+        // lobpcg.hpp:168-194: P+ = W C2 + P C3, HP+ likewise; X+ = X C1 + P+, HX+ = HX C1 + HP+
+        be::dla::MixJob job{};
+        job.nb = w2;
+        job.nout = 4;
+        job.out[0] = be::dla::MixOut{po.d.get(), 0, with_p ? 2 : 1, {{w.d.get(), c2.get(), 0, 0}, {p.d.get(), c3.get(), 0, 0}}, -1};
+        job.out[1] = be::dla::MixOut{hpo.d.get(), 0, with_p ? 2 : 1, {{hw.d.get(), c2.get(), 0, 0}, {hp.d.get(), c3.get(), 0, 0}}, -1};
+        job.out[2] = be::dla::MixOut{xo.d.get(), 0, 1, {{x.d.get(), c1.get(), 0, 0}}, 0};
+        job.out[3] = be::dla::MixOut{hxo.d.get(), 0, 1, {{hx.d.get(), c1.get(), 0, 0}}, 1};
+        if (n > 0) be::dla::mix(cx, job, n, s);
+        xo.down(Xo, n, m, s);
+        hxo.down(HXo, n, m, s);
+        po.down(Po, n, m, s);
+        hpo.down(HPo, n, m, s);
+        BE_CUDA(cudaStreamSynchronize(s));
     });
 }
 

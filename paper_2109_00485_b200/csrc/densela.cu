@@ -1169,7 +1169,8 @@ __global__ void __launch_bounds__(kT) k_residual(const double* __restrict__ hx, 
             sx1 += xv.y * xv.y;
             if (mode == 0) {
                 const double2 hv = reinterpret_cast<const double2*>(hx + row * 16)[cp];
-                const double r0 = hv.x - th0 * xv.x, r1 = hv.y - th1 * xv.y;
+                // hx - theta x with two roundings, as written in lobpcg.hpp:208 (no FMA contraction)
+                const double r0 = __dsub_rn(hv.x, __dmul_rn(th0, xv.x)), r1 = __dsub_rn(hv.y, __dmul_rn(th1, xv.y));
                 reinterpret_cast<double2*>(r + row * 16)[cp] = make_double2(r0, r1);
                 sr0 += r0 * r0;
                 sr1 += r1 * r1;
@@ -1211,7 +1212,7 @@ __global__ void __launch_bounds__(kT) k_residual(const double* __restrict__ hx, 
             const double xv = x[row * nb + c];
             s_x += xv * xv;
             if (mode == 0) {
-                const double rv = hx[row * nb + c] - th * xv;
+                const double rv = __dsub_rn(hx[row * nb + c], __dmul_rn(th, xv));  // no FMA (lobpcg.hpp:208)
                 r[row * nb + c] = rv;
                 s_r += rv * rv;
             }

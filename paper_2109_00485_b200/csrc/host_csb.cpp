@@ -257,6 +257,11 @@ static T get(std::istream& is) {
 void save_csb1(const std::string& path, const be_csb_view& v, const double* diag, index_t ndiag) {
     std::ofstream os(path, std::ios::binary);
     if (!os) fail(BE_ERR_PARSE, "cannot open " + path + " for writing");
+    save_csb1(os, v, diag, ndiag);
+    if (!os) fail(BE_ERR_PARSE, "CSB1 cache: write failed for " + path);
+}
+
+void save_csb1(std::ostream& os, const be_csb_view& v, const double* diag, index_t ndiag) {
     os.write("CSB1", 4);
     put<std::uint64_t>(os, static_cast<std::uint64_t>(v.nrows));
     put<std::uint64_t>(os, static_cast<std::uint64_t>(v.ncols));
@@ -287,7 +292,7 @@ void save_csb1(const std::string& path, const be_csb_view& v, const double* diag
         put<std::uint64_t>(os, static_cast<std::uint64_t>(ndiag));
         os.write(reinterpret_cast<const char*>(diag), static_cast<std::streamsize>(ndiag * 8));
     }
-    if (!os) fail(BE_ERR_PARSE, "CSB1 cache: write failed for " + path);
+    if (!os) fail(BE_ERR_PARSE, "CSB1 cache: write failed");
 }
 
 // Block rows [b0, b1) of a CSB1 file (global shape and blocks kept, other
@@ -373,6 +378,10 @@ std::unique_ptr<CsbHost> load_csb1_rows(const std::string& path, index_t b0, ind
 std::unique_ptr<CsbHost> load_csb1(const std::string& path, std::vector<double>* diag) {
     std::ifstream is(path, std::ios::binary);
     if (!is) fail(BE_ERR_PARSE, "cannot open " + path);
+    return load_csb1(is, diag);
+}
+
+std::unique_ptr<CsbHost> load_csb1(std::istream& is, std::vector<double>* diag) {
     char magic[4];
     is.read(magic, 4);
     if (!is || std::memcmp(magic, "CSB1", 4) != 0) fail(BE_ERR_PARSE, "CSB1 cache: bad magic");

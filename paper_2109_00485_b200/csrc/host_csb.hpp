@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cstdlib>
+#include <istream>
+#include <ostream>
 #include <memory>
 #include <random>
 #include <string>
@@ -64,6 +66,8 @@ bool is_strictly_lower(const be_csb_view& v);
 void to_triples(const be_csb_view& v, be_triple* out);
 void save_csb1(const std::string& path, const be_csb_view& v, const double* diag, index_t ndiag);
 std::unique_ptr<CsbHost> load_csb1(const std::string& path, std::vector<double>* diag);
+void save_csb1(std::ostream& os, const be_csb_view& v, const double* diag, index_t ndiag);
+std::unique_ptr<CsbHost> load_csb1(std::istream& is, std::vector<double>* diag);
 std::unique_ptr<CsbHost> load_csb1_rows(const std::string& path, index_t b0, index_t b1, std::vector<double>* diag);
 std::vector<index_t> draw_tile_offsets(index_t n, index_t block_extent, index_t tile_min, index_t tile_max,
                                        std::mt19937_64& rng);

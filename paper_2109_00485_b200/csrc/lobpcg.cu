@@ -370,8 +370,11 @@ struct Solver {
         if (w_restart) {  // the first qr_of_transpose of W gave up: a random W (lobpcg.hpp:360-363)
             upload_random(W.get(), cfg.seed + static_cast<std::uint64_t>(iter) * 7919u);
             if (!qr(W.get(), true)) fail(BE_ERR_RANK_DEFICIENT, "qr_of_transpose: Gram Cholesky failed twice");
-        } else if (fused_rr) {
-            qr(W.get(), false);  // verdict latched, read at the end of the iteration
+        } else if (fused_rr && op) {
+            // device operator: verdict latched, read at the end of the iteration (a rare redo costs
+            // one extra device apply). A host operator is checked now instead: its calls are
+            // observable (test_lobpcg.cpp:334-354 counts them), so it is never applied speculatively.
+            qr(W.get(), false);
             dla::latch_w_rank(ctx, st.get(), s);
         } else if (!qr(W.get(), true)) {
             upload_random(W.get(), cfg.seed + static_cast<std::uint64_t>(iter) * 7919u);
@@ -498,20 +501,21 @@ struct Solver {
                              iter, ev.ms(0, 1), ev.ms(1, 2), ev.ms(2, 3), ev.ms(3, 5), ev.ms(5, 6), ev.ms(6, 7),
                              ev.ms(7, 4), rec.t_total * 1e3);
             res.records.push_back(rec);
-            if (observer) {
-                const double* xh = nullptr;
-                const double* hxh = nullptr;
-                std::vector<double> xb, hxb;
-                if (cfg.observer_state) {
-                    xb.resize(static_cast<std::size_t>(n * nb));
-                    hxb.resize(static_cast<std::size_t>(n * nb));
-                    BE_CUDA(cudaMemcpyAsync(xb.data(), X.get(), xb.size() * 8, cudaMemcpyDeviceToHost, s));
-                    BE_CUDA(cudaMemcpyAsync(hxb.data(), HX.get(), hxb.size() * 8, cudaMemcpyDeviceToHost, s));
+            if (observer) {  // SolverState after the iteration (lobpcg.hpp:52-58, 436)
+                std::vector<double> hb;
+                const double* ph[6] = {};
+                if (cfg.observer_state) {  // X, HX, W, HW, P+, HP+ (the buffers hold exactly these here)
+                    const std::size_t pn = static_cast<std::size_t>(n * nb);
+                    hb.resize(6 * pn);
+                    const double* src[6] = {X.get(), HX.get(), W.get(), HW.get(), P.get(), HP.get()};
+                    for (int q = 0; q < 6; ++q) {
+                        BE_CUDA(cudaMemcpyAsync(hb.data() + q * pn, src[q], pn * 8, cudaMemcpyDeviceToHost, s));
+                        ph[q] = hb.data() + q * pn;
+                    }
                     BE_CUDA(cudaStreamSynchronize(s));
-                    xh = xb.data();
-                    hxh = hxb.data();
                 }
-                observer(observer_user, iter, n, nb, th.data(), rec.resn.data(), nconv, xh, hxh);
+                observer(observer_user, iter, n, nb, th.data(), rec.resn.data(), nconv, ph[0], ph[1], ph[2], ph[3],
+                         ph[4], ph[5]);
             }
             if (nconv >= k) converged = true;
         }

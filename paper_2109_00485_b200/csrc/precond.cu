@@ -827,81 +827,11 @@ int smid_bound(Ctx* ctx, cudaStream_t cs) {
 
 }  // namespace
 
-std::unique_ptr<Tiles> tiles_create(Ctx* ctx, const be_csb_view& L, const double* diag, const index_t* off_all,
-                                    index_t noff_all, index_t row_lo, index_t row_hi) {
-    validate_view(L);
-    // extract_tiles checks (precond.hpp:65-84)
-    if (L.nrows != L.ncols) fail(BE_ERR_DIMENSION_MISMATCH, "extract_tiles: matrix must be square");
-    if (!off_all || noff_all < 2 || off_all[0] != 0 || off_all[noff_all - 1] != L.nrows)
-        fail(BE_ERR_BAD_PARAMS, "extract_tiles: tile offsets must cover [0, n)");
-    if (row_lo < 0) row_hi = L.nrows, row_lo = 0;  // whole matrix
-    // the rank's row range (multi-GPU) must be a union of whole tiles
-    const index_t* lo_it = std::lower_bound(off_all, off_all + noff_all, row_lo);
-    const index_t* hi_it = std::lower_bound(off_all, off_all + noff_all, row_hi);
-    if (lo_it == off_all + noff_all || *lo_it != row_lo || hi_it == off_all + noff_all || *hi_it != row_hi ||
-        row_hi < row_lo)
-        fail(BE_ERR_MISALIGNED_TILES, "extract_tiles: row range is not a union of tiles");
-    if (!diag && row_hi > row_lo) fail(BE_ERR_DIMENSION_MISMATCH, "extract_tiles: diagonal length mismatch");
-    // local tile offsets relative to row_lo; panels of the result have row_hi - row_lo rows
-    std::vector<index_t> off_local;
-    for (const index_t* q = lo_it; q <= hi_it; ++q) off_local.push_back(*q - row_lo);
-    const index_t* off = off_local.data();
-    const index_t noff = static_cast<index_t>(off_local.size());
-    for (index_t j = 1; j < noff; ++j)
-        if (off[j] <= off[j - 1]) fail(BE_ERR_BAD_PARAMS, "extract_tiles: tile offsets must be strictly increasing");
-    {
-        index_t blk = 0;
-        for (index_t j = 0; j + 1 < noff_all; ++j) {
-            while (blk + 1 < L.nrowblks + 1 && L.row_offsets[blk + 1] <= off_all[j]) ++blk;
-            if (off_all[j + 1] > L.row_offsets[blk + 1])
-                fail(BE_ERR_MISALIGNED_TILES, "extract_tiles: tile [" + std::to_string(off_all[j]) + ", " +
-                                                  std::to_string(off_all[j + 1]) + ") straddles a block boundary");
-        }
-    }
-    auto t = std::make_unique<Tiles>();
-    t->ctx = ctx;
-    t->n = row_hi - row_lo;
-    t->offsets.assign(off, off + noff);
-    const index_t nt = noff - 1;
-    t->host.resize(static_cast<std::size_t>(nt));
-    std::vector<std::int32_t> owner(static_cast<std::size_t>(t->n));
-    for (index_t j = 0; j < nt; ++j) {
-        t->host[static_cast<std::size_t>(j)].dim = off[j + 1] - off[j];
-        for (index_t i = off[j]; i < off[j + 1]; ++i) owner[static_cast<std::size_t>(i)] = static_cast<std::int32_t>(j);
-    }
-    // couplings in to_triples order (csb.hpp:165-185), both orientations; only
-    // block rows meeting [row_lo, row_hi) can hold them
-    for (index_t bi = 0; bi < L.nrowblks; ++bi) {
-        if (L.row_offsets[bi + 1] <= row_lo || L.row_offsets[bi] >= row_hi) continue;
-        for (index_t bj = 0; bj < L.ncolblks; ++bj) {
-            const index_t b = bi * L.ncolblks + bj;
-            for (index_t k = L.block_nnz_offsets[b]; k < L.block_nnz_offsets[b] + L.block_nnz[b]; ++k) {
-                const index_t r = L.row_offsets[bi] + L.local_rows[k], c = L.col_offsets[bj] + L.local_cols[k];
-                if (r <= c) fail(BE_ERR_NOT_STRICTLY_LOWER, "extract_tiles: stored entry with row <= col");
-                if (r < row_lo || r >= row_hi || c < row_lo || c >= row_hi) continue;
-                const auto j = owner[static_cast<std::size_t>(r - row_lo)];
-                if (j != owner[static_cast<std::size_t>(c - row_lo)]) continue;
-                auto& T = t->host[static_cast<std::size_t>(j)];
-                const auto a = static_cast<std::int32_t>(r - row_lo - off[j]), cc = static_cast<std::int32_t>(c - row_lo - off[j]);
-                T.rows.push_back(a);
-                T.cols.push_back(cc);
-                T.vals.push_back(L.values[k]);
-                T.rows.push_back(cc);
-                T.cols.push_back(a);
-                T.vals.push_back(L.values[k]);
-            }
-        }
-    }
-    for (index_t j = 0; j < nt; ++j) {  // diagonal slots last
-        auto& T = t->host[static_cast<std::size_t>(j)];
-        T.diag_pos.resize(static_cast<std::size_t>(T.dim));
-        for (index_t i = 0; i < T.dim; ++i) {
-            T.diag_pos[static_cast<std::size_t>(i)] = static_cast<index_t>(T.vals.size());
-            T.rows.push_back(static_cast<std::int32_t>(i));
-            T.cols.push_back(static_cast<std::int32_t>(i));
-            T.vals.push_back(diag[off[j] + i]);
-        }
-    }
+// Device CSR of the host tiles (stable by row: a row's diagonal slot, last in
+// the host entry order, stays last in its row) and the size-class lists.
+static void tiles_upload(Tiles* tp, const index_t* off) {
+    Tiles* t = tp;
+    const index_t nt = static_cast<index_t>(t->host.size());
     // device CSR (stable by row: a row's diagonal slot stays last)
     std::vector<TileDev> td(static_cast<std::size_t>(nt));
     std::vector<std::int32_t> rowptr;
@@ -973,6 +903,131 @@ std::unique_ptr<Tiles> tiles_create(Ctx* ctx, const be_csb_view& L, const double
         if (!lists.empty())
             BE_CUDA(cudaMemcpy(t->class_tiles.get(), lists.data(), lists.size() * 4, cudaMemcpyHostToDevice));
     }
+}
+
+std::unique_ptr<Tiles> tiles_create(Ctx* ctx, const be_csb_view& L, const double* diag, const index_t* off_all,
+                                    index_t noff_all, index_t row_lo, index_t row_hi) {
+    validate_view(L);
+    // extract_tiles checks (precond.hpp:65-84)
+    if (L.nrows != L.ncols) fail(BE_ERR_DIMENSION_MISMATCH, "extract_tiles: matrix must be square");
+    if (!off_all || noff_all < 2 || off_all[0] != 0 || off_all[noff_all - 1] != L.nrows)
+        fail(BE_ERR_BAD_PARAMS, "extract_tiles: tile offsets must cover [0, n)");
+    for (index_t j = 1; j < noff_all; ++j)
+        if (off_all[j] <= off_all[j - 1]) fail(BE_ERR_BAD_PARAMS, "extract_tiles: tile offsets must be strictly increasing");
+    if (row_lo < 0) row_hi = L.nrows, row_lo = 0;  // whole matrix
+    // the rank's row range (multi-GPU) must be a union of whole tiles
+    const index_t* lo_it = std::lower_bound(off_all, off_all + noff_all, row_lo);
+    const index_t* hi_it = std::lower_bound(off_all, off_all + noff_all, row_hi);
+    if (lo_it == off_all + noff_all || *lo_it != row_lo || hi_it == off_all + noff_all || *hi_it != row_hi ||
+        row_hi < row_lo)
+        fail(BE_ERR_MISALIGNED_TILES, "extract_tiles: row range is not a union of tiles");
+    if (!diag && row_hi > row_lo) fail(BE_ERR_DIMENSION_MISMATCH, "extract_tiles: diagonal length mismatch");
+    // local tile offsets relative to row_lo; panels of the result have row_hi - row_lo rows
+    std::vector<index_t> off_local;
+    for (const index_t* q = lo_it; q <= hi_it; ++q) off_local.push_back(*q - row_lo);
+    const index_t* off = off_local.data();
+    const index_t noff = static_cast<index_t>(off_local.size());
+    for (index_t j = 1; j < noff; ++j)
+        if (off[j] <= off[j - 1]) fail(BE_ERR_BAD_PARAMS, "extract_tiles: tile offsets must be strictly increasing");
+    {
+        index_t blk = 0;
+        for (index_t j = 0; j + 1 < noff_all; ++j) {
+            while (blk + 1 < L.nrowblks + 1 && L.row_offsets[blk + 1] <= off_all[j]) ++blk;
+            if (off_all[j + 1] > L.row_offsets[blk + 1])
+                fail(BE_ERR_MISALIGNED_TILES, "extract_tiles: tile [" + std::to_string(off_all[j]) + ", " +
+                                                  std::to_string(off_all[j + 1]) + ") straddles a block boundary");
+        }
+    }
+    auto t = std::make_unique<Tiles>();
+    t->ctx = ctx;
+    t->n = row_hi - row_lo;
+    t->offsets.assign(off, off + noff);
+    const index_t nt = noff - 1;
+    t->host.resize(static_cast<std::size_t>(nt));
+    std::vector<std::int32_t> owner(static_cast<std::size_t>(t->n));
+    for (index_t j = 0; j < nt; ++j) {
+        t->host[static_cast<std::size_t>(j)].dim = off[j + 1] - off[j];
+        for (index_t i = off[j]; i < off[j + 1]; ++i) owner[static_cast<std::size_t>(i)] = static_cast<std::int32_t>(j);
+    }
+    // couplings in to_triples order (csb.hpp:165-185), both orientations; only
+    // block rows meeting [row_lo, row_hi) can hold them
+    for (index_t bi = 0; bi < L.nrowblks; ++bi) {
+        if (L.row_offsets[bi + 1] <= row_lo || L.row_offsets[bi] >= row_hi) continue;
+        for (index_t bj = 0; bj < L.ncolblks; ++bj) {
+            const index_t b = bi * L.ncolblks + bj;
+            for (index_t k = L.block_nnz_offsets[b]; k < L.block_nnz_offsets[b] + L.block_nnz[b]; ++k) {
+                const index_t r = L.row_offsets[bi] + L.local_rows[k], c = L.col_offsets[bj] + L.local_cols[k];
+                if (r <= c) fail(BE_ERR_NOT_STRICTLY_LOWER, "extract_tiles: stored entry with row <= col");
+                if (r < row_lo || r >= row_hi || c < row_lo || c >= row_hi) continue;
+                const auto j = owner[static_cast<std::size_t>(r - row_lo)];
+                if (j != owner[static_cast<std::size_t>(c - row_lo)]) continue;
+                auto& T = t->host[static_cast<std::size_t>(j)];
+                const auto a = static_cast<std::int32_t>(r - row_lo - off[j]), cc = static_cast<std::int32_t>(c - row_lo - off[j]);
+                T.rows.push_back(a);
+                T.cols.push_back(cc);
+                T.vals.push_back(L.values[k]);
+                T.rows.push_back(cc);
+                T.cols.push_back(a);
+                T.vals.push_back(L.values[k]);
+            }
+        }
+    }
+    for (index_t j = 0; j < nt; ++j) {  // diagonal slots last
+        auto& T = t->host[static_cast<std::size_t>(j)];
+        T.diag_pos.resize(static_cast<std::size_t>(T.dim));
+        for (index_t i = 0; i < T.dim; ++i) {
+            T.diag_pos[static_cast<std::size_t>(i)] = static_cast<index_t>(T.vals.size());
+            T.rows.push_back(static_cast<std::int32_t>(i));
+            T.cols.push_back(static_cast<std::int32_t>(i));
+            T.vals.push_back(diag[off[j] + i]);
+        }
+    }
+    tiles_upload(t.get(), off);
+    return t;
+}
+
+std::unique_ptr<Tiles> tiles_create_explicit(Ctx* ctx, const std::vector<HostTile>& tiles) {
+    auto t = std::make_unique<Tiles>();
+    t->ctx = ctx;
+    std::vector<index_t> off(1, 0);
+    for (const auto& T : tiles) {
+        if (T.dim < 1) fail(BE_ERR_BAD_PARAMS, "SparseTile: dim must be positive");
+        if (T.rows.size() != T.vals.size() || T.cols.size() != T.vals.size() ||
+            T.diag_pos.size() != static_cast<std::size_t>(T.dim))
+            fail(BE_ERR_DIMENSION_MISMATCH, "SparseTile: rows / cols / values / diag_pos sizes disagree");
+        // reference layout (precond.hpp:18-30): couplings, then one diagonal slot per row; the
+        // device CSR keeps each row's diagonal slot last, so it is moved there if it is not
+        std::vector<char> is_diag(T.vals.size(), 0);
+        for (index_t i = 0; i < T.dim; ++i) {
+            const index_t q = T.diag_pos[static_cast<std::size_t>(i)];
+            if (q < 0 || q >= static_cast<index_t>(T.vals.size()) || T.rows[static_cast<std::size_t>(q)] != i ||
+                T.cols[static_cast<std::size_t>(q)] != i)
+                fail(BE_ERR_BAD_PARAMS, "SparseTile: diag_pos does not point at the diagonal slot of its row");
+            is_diag[static_cast<std::size_t>(q)] = 1;
+        }
+        HostTile h;
+        h.dim = T.dim;
+        for (std::size_t q = 0; q < T.vals.size(); ++q) {
+            if (is_diag[q]) continue;
+            if (T.rows[q] < 0 || T.rows[q] >= T.dim || T.cols[q] < 0 || T.cols[q] >= T.dim)
+                fail(BE_ERR_INDEX_OUT_OF_RANGE, "SparseTile: entry outside the tile");
+            h.rows.push_back(T.rows[q]);
+            h.cols.push_back(T.cols[q]);
+            h.vals.push_back(T.vals[q]);
+        }
+        h.diag_pos.resize(static_cast<std::size_t>(T.dim));
+        for (index_t i = 0; i < T.dim; ++i) {
+            h.diag_pos[static_cast<std::size_t>(i)] = static_cast<index_t>(h.vals.size());
+            h.rows.push_back(static_cast<std::int32_t>(i));
+            h.cols.push_back(static_cast<std::int32_t>(i));
+            h.vals.push_back(T.vals[static_cast<std::size_t>(T.diag_pos[static_cast<std::size_t>(i)])]);
+        }
+        off.push_back(off.back() + T.dim);
+        t->host.push_back(std::move(h));
+    }
+    t->n = off.back();
+    t->offsets = off;
+    tiles_upload(t.get(), off.data());
     return t;
 }
 

@@ -55,6 +55,9 @@ struct Tiles {
 // the whole matrix.
 std::unique_ptr<Tiles> tiles_create(Ctx* ctx, const be_csb_view& L, const double* diag, const index_t* off,
                                     index_t noff, index_t row_lo = -1, index_t row_hi = -1);
+// Tiles given explicitly in the reference's SparseTile layout (consecutive row
+// ranges in the order given): the fom_solve_tile entry point of the mirror.
+std::unique_ptr<Tiles> tiles_create_explicit(Ctx* ctx, const std::vector<HostTile>& tiles);
 void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, index_t nrows, int nb, int m,
                    std::int64_t* fallbacks, cudaStream_t s);
 

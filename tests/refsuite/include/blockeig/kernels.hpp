@@ -1,0 +1,4 @@
+// Forwarding header (test infrastructure): the reference suites include "blockeig/kernels.hpp";
+// this build resolves it to the B200 C++ mirror (include/blockeig_b200.hpp).
+#pragma once
+#include "blockeig_b200.hpp"

@@ -167,6 +167,34 @@ def test_long_run_invariants(ctx):  # test_lobpcg.cpp:329-365 (trace, calls, rec
     assert np.all(tr[1:] <= tr[:-1] + 1e-12 * np.abs(tr[1:]))
 
 
+def test_observer_receives_the_whole_solver_state(ctx):
+    """SolverState (lobpcg.hpp:52-58) at the observer call (:436): X, W, P+ with their H-images.
+    The recurrences keep HX = H X, HW = H W and HP = H P; W is orthonormal after its hygiene and
+    P+ is orthogonal to X+ and near-orthonormal (lobpcg.hpp:412-417), as in the reference."""
+    n = 400
+    m, d = make_test_matrix(n, 2000, 5)
+    op = abi.Operator(ctx, m, d, values_prec=abi.BE_F64)
+    t = m.to_triples()
+    dense = np.diag(d)
+    dense[t["row"], t["col"]] += t["value"]
+    dense[t["col"], t["row"]] += t["value"]
+    seen = []
+
+    def obs(it, theta, rn, nc, st):
+        seen.append(it)
+        for a, ha in (("x", "hx"), ("w", "hw"), ("p", "hp")):
+            assert st[a].shape == (n, 8) and st[ha].shape == (n, 8)
+            ref = dense @ st[a]
+            assert np.linalg.norm(st[ha] - ref) <= 1e-9 * np.linalg.norm(ref), (it, a)
+        assert np.allclose(st["w"].T @ st["w"], np.eye(8), atol=1e-8)
+        assert np.abs(st["x"].T @ st["p"]).max() < 1e-8
+        assert np.allclose(st["p"].T @ st["p"], np.eye(8), atol=1e-6)
+        assert np.allclose(np.linalg.norm(st["hx"] - st["x"] * theta, axis=0), rn, rtol=1e-8, atol=1e-12)
+
+    res = abi.lobpcg(ctx, op, k=4, nb=8, tol=1e-300, maxiter=6, observer=obs, observer_panels=True)
+    assert seen == list(range(1, 7)) and res["iterations"] == 6
+
+
 def test_host_operator_closure(ctx):  # generic Operator boundary (lobpcg.hpp:20)
     d = np.arange(1.0, 101.0)
     res = abi.lobpcg(ctx, None, n=100, host_operator=lambda x: d[:, None] * x, k=5, nb=8, tol=1e-9, seed=7)
