@@ -218,12 +218,17 @@ be_status be_ctx_launches(be_ctx* ctx, int64_t* launches);
 
 typedef struct be_op be_op;
 
-enum { BE_OP_SYMMETRIC = 1 };
+enum { BE_OP_SYMMETRIC = 1, BE_OP_DETERMINISTIC = 2 };
 /* Upload a CSB to the device and derive the tile format.
  * flags & BE_OP_SYMMETRIC: validates square + strictly lower + diag length
  * like the SymmetricOperator constructor (kernels.hpp:341-350); diag (host,
  * nrows doubles) is copied. Without the flag the matrix may be rectangular
- * and only the NOTRANS/TRANS accumulate modes are valid (diag ignored). */
+ * and only the NOTRANS/TRANS accumulate modes are valid (diag ignored).
+ * flags & BE_OP_DETERMINISTIC: f64 values, every output element summed by one
+ * thread in the reference's serial order (run_baseline, kernels.hpp:253-276:
+ * L's entries of the row in CSB order, then L^T's, then the diagonal; no FMA
+ * contraction) -- bit-reproducible and bit-identical to the serial reference
+ * on f64 panels; reads each stored entry twice (the reference's two passes). */
 be_status be_op_create(be_ctx* ctx, const be_csb_view* L, const double* diag, int values_prec,
                        int flags, be_op** out);
 be_status be_op_destroy(be_op* op);

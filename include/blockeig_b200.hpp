@@ -384,10 +384,11 @@ inline void write_matrix_market(std::ostream& os, const SymmetricCoo& m) {  // m
 // --------------------------------------------------------------- kernels.hpp
 enum class KernelTag { Baseline, FusedAtomic, CacheBlocked, Sm100a };
 
-// The reference's three names keep the reference's arithmetic contract (f64 stored values:
-// results within ~1e-12 of the fp64 CPU kernels, kernels.hpp test bounds); the new Sm100a tag
-// selects the f32-valued fast path (8 B/nnz, 1e-5 relative, the headline bench) unless
-// KernelVariant::sm100a(BE_F64) asks for f64 values. All four run the same device kernel.
+// The reference's three names keep the reference's arithmetic contract: f64 values summed in the
+// serial reference's order (BE_OP_DETERMINISTIC: bit-reproducible, bit-identical to the serial
+// CPU kernels on f64 panels). The new Sm100a tag selects the one-pass tile kernel (f32 values,
+// 8 B/nnz, 1e-5 relative, the headline bench) unless KernelVariant::sm100a(BE_F64) asks for
+// f64 values.
 struct KernelVariant {  // kernels.hpp:25-49
     KernelTag tag = KernelTag::Baseline;
     int cache_size = 256;
@@ -398,6 +399,8 @@ struct KernelVariant {  // kernels.hpp:25-49
     static KernelVariant fused_atomic() { return {KernelTag::FusedAtomic}; }
     static KernelVariant cache_blocked(int cache = 256, int vec = 256) { return {KernelTag::CacheBlocked, cache, vec}; }
     static KernelVariant sm100a(be_prec values = BE_F32) { return {KernelTag::Sm100a, 256, 256, values}; }
+    // the reference's names run the deterministic device mode (its serial summation order)
+    int op_flags() const { return tag == KernelTag::Sm100a ? 0 : BE_OP_DETERMINISTIC; }
     void validate() const {
         if (cache_size < 1) throw BadParams("KernelVariant: cache_size must be >= 1");
         if (vector_width < 1) throw BadParams("KernelVariant: vector_width must be >= 1");
@@ -449,7 +452,7 @@ inline void spmm_notrans(const CsbCooMatrix& h, const BlockVector& w, BlockVecto
                          const KernelVariant& variant = {}, ThreadPool* = nullptr) {
     variant.validate();
     b200::check_spmm_shapes(h, w, u, false);
-    auto op = b200::make_op(h, nullptr, variant.values, 0);
+    auto op = b200::make_op(h, nullptr, variant.values, variant.op_flags());
     b200::check(be_op_apply_host(op.get(), w.data.data(), u.data.data(), w.nrows, static_cast<int>(w.nvec),
                                  BE_APPLY_NOTRANS_ACC));
 }
@@ -458,7 +461,7 @@ inline void spmm_trans(const CsbCooMatrix& h, const BlockVector& w, BlockVector&
                        const KernelVariant& variant = {}, ThreadPool* = nullptr) {
     variant.validate();
     b200::check_spmm_shapes(h, w, u, true);
-    auto op = b200::make_op(h, nullptr, variant.values, 0);
+    auto op = b200::make_op(h, nullptr, variant.values, variant.op_flags());
     b200::check(be_op_apply_host(op.get(), w.data.data(), u.data.data(), w.nrows, static_cast<int>(w.nvec),
                                  BE_APPLY_TRANS_ACC));
 }
@@ -475,7 +478,7 @@ public:
         if (l.nrows != l.ncols) throw DimensionMismatch("SymmetricOperator: matrix must be square");
         if (static_cast<index_t>(diag_.size()) != l.nrows)
             throw DimensionMismatch("SymmetricOperator: diagonal length mismatch");
-        op_ = b200::make_op(l, diag_.data(), variant_.values, BE_OP_SYMMETRIC);  // NotStrictlyLower from the device build
+        op_ = b200::make_op(l, diag_.data(), variant_.values, BE_OP_SYMMETRIC | variant_.op_flags());  // NotStrictlyLower from the device build
     }
 
     index_t dim() const { return l_->nrows; }

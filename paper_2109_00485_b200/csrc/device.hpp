@@ -124,6 +124,13 @@ struct Op {
     DBuf<int> counter;               // persistent-kernel tile counter [2]
     DBuf<float> x32, y32;            // f32 staging of f64 panels (f32-values operator)
     std::vector<std::int64_t> csb_index;  // row-order device slot -> CSB index, -1 = padding (small matrices only)
+    // deterministic mode (BE_OP_DETERMINISTIC): row lists in the reference's serial summation
+    // order instead of the tile format -- L's entries of each output row (det_ptr_n, nrows + 1)
+    // and L^T's (det_ptr_t, ncols + 1) over one (column, f64 value) array
+    bool det = false;
+    DBuf<std::int64_t> det_ptr_n, det_ptr_t;
+    DBuf<std::int32_t> det_col;
+    DBuf<double> det_val;
     int grid = 0;
     // multi-GPU (row e): panel rows are owned in contiguous segments
     // [cuts[q], cuts[q+1]); tile coordinates live in the padded index space

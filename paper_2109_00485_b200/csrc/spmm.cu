@@ -524,6 +524,34 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
 }
 
+// Deterministic symmetric SpMM (BE_OP_DETERMINISTIC): one warp per output
+// row, lane = panel column; the row's entries are summed sequentially in the
+// reference's serial order (run_baseline, kernels.hpp:253-276 + the diagonal
+// pass :363-370) with separately rounded products and sums (the reference's
+// u += v * w compiles without FMA), so the result is bit-reproducible and
+// bit-identical to the serial reference on f64 panels.
+template <typename TX>
+__global__ void k_det_spmm(const std::int64_t* __restrict__ pa, const std::int64_t* __restrict__ pb,
+                           const std::int32_t* __restrict__ col, const double* __restrict__ val,
+                           const double* __restrict__ diag, const TX* __restrict__ X, TX* __restrict__ Y,
+                           std::int64_t nout, int nb, int init_zero) {
+    const int lane = threadIdx.x & 31;
+    const std::int64_t w0 = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const std::int64_t nw = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (std::int64_t r = w0; r < nout; r += nw) {
+        for (int v = lane; v < nb; v += 32) {
+            double y = init_zero ? 0.0 : static_cast<double>(Y[r * nb + v]);
+            for (std::int64_t e = pa[r]; e < pa[r + 1]; ++e)
+                y = __dadd_rn(y, __dmul_rn(val[e], static_cast<double>(X[static_cast<std::int64_t>(col[e]) * nb + v])));
+            if (pb)
+                for (std::int64_t e = pb[r]; e < pb[r + 1]; ++e)
+                    y = __dadd_rn(y, __dmul_rn(val[e], static_cast<double>(X[static_cast<std::int64_t>(col[e]) * nb + v])));
+            if (diag) y = __dadd_rn(y, __dmul_rn(diag[r], static_cast<double>(X[r * nb + v])));
+            Y[r * nb + v] = static_cast<TX>(y);
+        }
+    }
+}
+
 // Y = diag(D) X  (the diagonal pass of kernels.hpp:363-370, run first so the
 // tile kernel can accumulate straight into Y)
 template <typename TX>
@@ -874,6 +902,56 @@ Op::~Op() {
     if (cstream) cudaStreamDestroy(cstream);
 }
 
+// Row lists of the deterministic mode (see k_det_spmm): a stable counting sort
+// of the CSB storage order (blocks row-major, entries in stored order) by
+// global row gives each row's L entries in run_baseline's notrans order (column
+// blocks ascending, stored order within a block); by global column, each
+// column's entries in its trans order (row blocks ascending).
+static void op_build_det(Op* op, const be_csb_view& L) {
+    const index_t n = L.nrows, m = L.ncols, nnz = L.nnz;
+    if (nnz >= (index_t{1} << 40)) fail(BE_ERR_BAD_PARAMS, "deterministic operator too large");
+    std::vector<std::int64_t> pn(static_cast<std::size_t>(n) + 1, 0), pt(static_cast<std::size_t>(m) + 1, 0);
+    std::vector<std::int32_t> grow(static_cast<std::size_t>(nnz)), gcol(static_cast<std::size_t>(nnz));
+    for (index_t bi = 0; bi < L.nrowblks; ++bi)
+        for (index_t bj = 0; bj < L.ncolblks; ++bj) {
+            const index_t b = bi * L.ncolblks + bj;
+            for (index_t k = L.block_nnz_offsets[b]; k < L.block_nnz_offsets[b] + L.block_nnz[b]; ++k) {
+                grow[static_cast<std::size_t>(k)] = static_cast<std::int32_t>(L.row_offsets[bi] + L.local_rows[k]);
+                gcol[static_cast<std::size_t>(k)] = static_cast<std::int32_t>(L.col_offsets[bj] + L.local_cols[k]);
+                ++pn[static_cast<std::size_t>(grow[static_cast<std::size_t>(k)]) + 1];
+                ++pt[static_cast<std::size_t>(gcol[static_cast<std::size_t>(k)]) + 1];
+            }
+        }
+    for (std::size_t i = 1; i < pn.size(); ++i) pn[i] += pn[i - 1];
+    for (std::size_t i = 1; i < pt.size(); ++i) pt[i] += pt[i - 1];
+    std::vector<std::int32_t> col(static_cast<std::size_t>(2 * nnz));
+    std::vector<double> val(static_cast<std::size_t>(2 * nnz));
+    std::vector<std::int64_t> cn(pn.begin(), pn.end() - 1), ct(pt.begin(), pt.end() - 1);
+    for (auto& c : ct) c += nnz;  // the L^T lists follow the L lists
+    for (index_t b = 0; b < L.nrowblks * L.ncolblks; ++b)  // blocks row-major, entries in stored order
+        for (index_t k = L.block_nnz_offsets[b]; k < L.block_nnz_offsets[b] + L.block_nnz[b]; ++k) {
+            const auto r = grow[static_cast<std::size_t>(k)], c = gcol[static_cast<std::size_t>(k)];
+            const auto qn = cn[static_cast<std::size_t>(r)]++;
+            col[static_cast<std::size_t>(qn)] = c;
+            val[static_cast<std::size_t>(qn)] = L.values[k];
+            const auto qt = ct[static_cast<std::size_t>(c)]++;
+            col[static_cast<std::size_t>(qt)] = r;
+            val[static_cast<std::size_t>(qt)] = L.values[k];
+        }
+    for (auto& x : pt) x += nnz;
+    op->det = true;
+    op->det_ptr_n.reset(n + 1);
+    op->det_ptr_t.reset(m + 1);
+    op->det_col.reset(std::max<index_t>(2 * nnz, 1));
+    op->det_val.reset(std::max<index_t>(2 * nnz, 1));
+    BE_CUDA(cudaMemcpy(op->det_ptr_n.get(), pn.data(), pn.size() * 8, cudaMemcpyHostToDevice));
+    BE_CUDA(cudaMemcpy(op->det_ptr_t.get(), pt.data(), pt.size() * 8, cudaMemcpyHostToDevice));
+    if (nnz > 0) {
+        BE_CUDA(cudaMemcpy(op->det_col.get(), col.data(), col.size() * 4, cudaMemcpyHostToDevice));
+        BE_CUDA(cudaMemcpy(op->det_val.get(), val.data(), val.size() * 8, cudaMemcpyHostToDevice));
+    }
+}
+
 std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag, int values_prec, int flags) {
     validate_view(L);
     if (values_prec != BE_F32 && values_prec != BE_F64) fail(BE_ERR_BAD_PARAMS, "values_prec must be BE_F32 or BE_F64");
@@ -891,7 +969,12 @@ std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag
     }
     if (L.nrows >= (index_t{1} << 31) || L.ncols >= (index_t{1} << 31))
         fail(BE_ERR_BAD_PARAMS, "sym_spmm: dimension exceeds 2^31 rows per device");
-    op_build(op.get(), L, nullptr);
+    if (flags & BE_OP_DETERMINISTIC) {
+        op->values_prec = BE_F64;
+        op_build_det(op.get(), L);
+    } else {
+        op_build(op.get(), L, nullptr);
+    }
     if (op->symmetric) {
         op->diag.reset(std::max<index_t>(L.nrows, 1));
         if (L.nrows > 0)
@@ -1097,7 +1180,26 @@ void op_apply(Op* op, const void* X, void* Y, index_t in_rows, int nb, int panel
     auto grid_for = [&](index_t total) {
         return static_cast<int>(std::max<index_t>(1, std::min<index_t>((total + 255) / 256, op->ctx->num_sms * 8)));
     };
-    if (panel_prec == BE_F64 && op->values_prec == BE_F32) {
+    if (op->det) {  // deterministic mode: one pass over the row lists
+        if (op->timing) BE_CUDA(cudaEventRecord(op->ev[1], s));
+        const std::int64_t* pa = mode == BE_APPLY_TRANS_ACC ? op->det_ptr_t.get() : op->det_ptr_n.get();
+        const std::int64_t* pb = mode == BE_APPLY_SYMMETRIC ? op->det_ptr_t.get() : nullptr;
+        const double* dg = mode == BE_APPLY_SYMMETRIC ? op->diag.get() : nullptr;
+        const int zero = mode == BE_APPLY_SYMMETRIC ? 1 : 0;
+        if (out_rows > 0) {
+            const int g = grid_for(out_rows * 32);
+            if (panel_prec == BE_F64)
+                k_det_spmm<double><<<g, 256, 0, s>>>(pa, pb, op->det_col.get(), op->det_val.get(), dg,
+                                                     static_cast<const double*>(X), static_cast<double*>(Y), out_rows,
+                                                     nb, zero);
+            else
+                k_det_spmm<float><<<g, 256, 0, s>>>(pa, pb, op->det_col.get(), op->det_val.get(), dg,
+                                                    static_cast<const float*>(X), static_cast<float*>(Y), out_rows, nb,
+                                                    zero);
+            BE_CUDA(cudaGetLastError());
+            ++op->ctx->launches;
+        }
+    } else if (panel_prec == BE_F64 && op->values_prec == BE_F32) {
         // f32 SpMM on f64 panels: X -> f32 copy, tile kernel into a zeroed f32
         // accumulator, then Y = D X + acc in f64 (halves the gathered and
         // reduced vector bytes of the tile kernel)

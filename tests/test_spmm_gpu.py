@@ -216,3 +216,36 @@ def test_config1_random_spmm_parity(ctx):
     want = ol.Impl("orc").spmm(m, s.diag, x)
     got = abi.Operator(ctx, m, s.diag).apply_host(x)
     assert relf(got, want) <= 1e-5
+
+
+# --- deterministic mode (BE_OP_DETERMINISTIC, the mirror's reference variant names) -----
+@pytest.mark.parametrize("nb", [1, 5, 16, 40])
+def test_deterministic_mode_is_bit_exact_with_the_serial_reference(ctx, nb):
+    """f64 values summed in run_baseline's serial order (kernels.hpp:253-276) without FMA
+    contraction: bit-identical to the reference itself (oracle/_ref, ThreadPool-free baseline)
+    in all three apply modes, and bit-reproducible."""
+    try:
+        ref = ol.Impl("ref", threads=1, variant=0)
+    except FileNotFoundError:
+        pytest.skip("oracle/_ref/libref.so not built")
+    m, diag = sym_problem(2000, 30000, 700, 11)
+    op = abi.Operator(ctx, m, diag, values_prec=abi.BE_F64, deterministic=True)
+    x = np.random.default_rng(nb).uniform(-1, 1, (2000, nb))
+    got = op.apply_host(x)
+    assert np.array_equal(got, ref.spmm(m, diag, x))
+    assert np.array_equal(got, op.apply_host(x))
+    y0 = np.random.default_rng(99).uniform(-1, 1, (2000, nb))
+    for mode in (abi.BE_APPLY_NOTRANS_ACC, abi.BE_APPLY_TRANS_ACC):
+        assert np.array_equal(op.apply_host(x, y0.copy(), mode=mode), ref.spmm(m, None, x, y0, mode=mode))
+
+
+def test_deterministic_solve_is_bit_reproducible(ctx):
+    """test_lobpcg.cpp:389-407 (identical history for an identical seed) on the device: the
+    deterministic operator plus the fixed-order dense reductions."""
+    m, diag = sym_problem(1500, 9000, 500, 3)
+    op = abi.Operator(ctx, m, diag, values_prec=abi.BE_F64, deterministic=True)
+    r1 = abi.lobpcg(ctx, op, k=3, nb=6, tol=1e-8, seed=42)
+    r2 = abi.lobpcg(ctx, op, k=3, nb=6, tol=1e-8, seed=42)
+    assert r1["iterations"] == r2["iterations"]
+    assert np.array_equal(r1["lambda_"], r2["lambda_"]) and np.array_equal(r1["x"], r2["x"])
+    assert np.array_equal(r1["theta"], r2["theta"]) and np.array_equal(r1["residual_norms"], r2["residual_norms"])
