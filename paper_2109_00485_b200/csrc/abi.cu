@@ -449,7 +449,7 @@ be_status be_op_decode(be_op* op, int64_t* rows, int64_t* cols, double* values, 
             std::memcpy(&d, p, 8);
             return d;
         };
-        // Blob layout (spmm.cu): meta 1056 B = jr u16[136] | jc u16[136] | rank->row u8[128] |
+        // Blob layout (spmm.cu): meta kBlobMeta B = jr u16[136] | jc u16[136] | rank->row u8[128] |
         // rank->col u8[128] | row lengths | column lengths; then values + columns in row-JDS
         // order and values + rows in column-JDS order, npad = nnz rounded up to 16 each.
         // Both orders are validated (ranks by decreasing length, starts = prefix sums of
@@ -463,9 +463,9 @@ be_status be_op_decode(be_op* op, int64_t* rows, int64_t* cols, double* values, 
             const std::uint16_t* jd[2] = {reinterpret_cast<const std::uint16_t*>(b), reinterpret_cast<const std::uint16_t*>(b + 272)};
             const unsigned char* perm[2] = {b + 544, b + 672};
             const unsigned char* len[2] = {b + 800, b + 928};
-            const unsigned char* sv[2] = {b + 1056, b + 1056 + static_cast<std::size_t>(npad) * (vsz + 1)};
-            const unsigned char* si[2] = {b + 1056 + static_cast<std::size_t>(npad) * vsz,
-                                          b + 1056 + static_cast<std::size_t>(npad) * (2 * vsz + 1)};
+            const unsigned char* sv[2] = {b + be::kBlobMeta, b + be::kBlobMeta + static_cast<std::size_t>(npad) * (vsz + 1)};
+            const unsigned char* si[2] = {b + be::kBlobMeta + static_cast<std::size_t>(npad) * vsz,
+                                          b + be::kBlobMeta + static_cast<std::size_t>(npad) * (2 * vsz + 1)};
             std::vector<std::tuple<int, int, std::uint64_t>> got[2];
             for (int g = 0; g < 2; ++g) {
                 int sum = 0;

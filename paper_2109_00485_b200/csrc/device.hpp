@@ -98,6 +98,9 @@ struct TileHdr {
 };
 
 inline constexpr int kTile = 128;
+// tile blob metadata (spmm.cu): jr u16[136] | jc u16[136] | rank->row u8[128] | rank->col u8[128] |
+// row lengths u8[128] | column lengths u8[128] | work split u16[9] (+ padding) = 1088 bytes
+inline constexpr int kBlobMeta = 1088;
 
 // Raise a kernel's dynamic shared-memory limit to at least `bytes` on the
 // current device. Monotonic (never lowered), so ranks running as threads of
