@@ -141,8 +141,9 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 
 __device__ __forceinline__ void fill_stage(double* st, const double* const* src, int nsrc, int ps, int rs, int nb,
                                            std::int64_t r0, int rows) {
-    const int pr = nb / 2;  // 16-byte pieces per row (divides the block size)
+    const int pr = nb / 2;  // 16-byte pieces per row
     const int c = threadIdx.x % pr, rstep = blockDim.x / pr;
+    if (static_cast<int>(threadIdx.x) >= rstep * pr) return;  // pr need not divide the block: no duplicate rows
     for (int d = 0; d < nsrc; ++d) {
         const double* g = src[d] + r0 * nb + 2 * c;
         double* t = st + d * ps + 2 * c;

@@ -763,6 +763,8 @@ __global__ void __launch_bounds__(kWsThreads, kWsStages <= 2 ? 2 : 1)
             ++un;
             d = 0;
         }
+        // this warp's generic-proxy reads of the stage before the producer's next bulk (async-proxy) writes
+        stream::fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(stream::smem_u32(&empty[s])) : "memory");
