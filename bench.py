@@ -81,6 +81,7 @@ def args_parse():
     ap.add_argument("--values", choices=["f32", "f64"], default="f32",
                     help="stored matrix values on the device: f32 (8 B/nnz budget) or f64 (12 B/nnz, the reference's precision)")
     ap.add_argument("--no-tts", action="store_true", help="skip the time-to-solution solve (tol 1e-6)")
+    ap.add_argument("--report", help="write the time-to-solution solve's run report (blockeig/run-report/v1) here")
     ap.add_argument("--write-cache", help=argparse.SUPPRESS)  # internal: generate the input file in a child process
     return ap.parse_args()
 
@@ -568,6 +569,19 @@ def main():
         if cpu is not None:
             tts["reference_estimated_s"] = r3["iterations"] * cpu["ms_per_step"] * 1e-3
             tts["reference_estimate"] = "our iteration count x the reference's measured median iteration time"
+        if a.report and rank == 0:  # the reference driver's solve report (driver.hpp:242-281)
+            from paper_2109_00485_b200 import report
+            rcfg = report.config_echo(k=a.nev, nb=a.nb, tol=1e-6, maxiter=500, fom_iters=4, seed=a.seed,
+                                      no_precond=not precond, nd=world, variant="sm100a",
+                                      input_echo={"gen": cfg["kind"], "n": cfg["n"], "nnz": cfg["nnz"],
+                                                  "block_extent": cfg["extent"], "cache": inp.get("file"),
+                                                  "cache_hit": True})
+            sizes = None
+            if tiles is not None:
+                sizes = list(np.diff(np.fromfile(inp["tiles"], dtype=np.int64)[1:]))
+            Path(a.report).write_text(report.dumps(report.solve_report(r3, n=n, nnz_lower=nnz, config=rcfg,
+                                                                       tile_sizes=sizes)))
+            tts["run_report"] = a.report
     traffic = ncu_traffic(a.config, a.nb) if a.values == "f32" else None
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": done, "warmup": a.warmup,

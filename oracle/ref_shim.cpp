@@ -7,6 +7,7 @@
 // oracle/oracle.cpp and lets bench.py time the reference's own CPU path
 // (cpu_baseline kind "reference").
 #include <blockeig/densela.hpp>
+#include <blockeig/driver.hpp>
 #include <blockeig/dist.hpp>
 #include <blockeig/kernels.hpp>
 #include <blockeig/lobpcg.hpp>
@@ -471,6 +472,39 @@ int ref_mm_write(index_t n, const index_t* rows, const index_t* cols, const doub
         const std::string s = os.str();
         *len = static_cast<index_t>(s.size());
         if (buf && cap > *len) std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
+}
+
+// the reference CLI's `solve` command (driver.hpp:200-290) on a generated
+// problem: runs it and keeps its run report ("blockeig/run-report/v1");
+// *len receives the report's length, ref_last_report copies it out
+static std::string g_last_report;
+int ref_cmd_solve(const char* gen, index_t n, double density, index_t block_extent, int k, int nb, double tol,
+                  int maxiter, std::uint64_t seed, int no_precond, index_t* len) {
+    return guarded([&] {
+        DriverArgs a;
+        a.gen = gen;
+        a.n = n;
+        a.density = density;
+        a.block_extent = block_extent;
+        a.k = k;
+        a.nb = nb;
+        a.tol = tol;
+        a.maxiter = maxiter;
+        a.seed = seed;
+        a.no_precond = no_precond != 0;
+        a.threads = 1;
+        std::ostringstream os, es;
+        const int rc = cmd_solve(a, os, es);
+        if (rc != kExitOk) throw std::runtime_error("cmd_solve exit " + std::to_string(rc) + ": " + es.str());
+        g_last_report = os.str();
+        *len = static_cast<index_t>(g_last_report.size());
+    });
+}
+int ref_last_report(char* out, index_t cap) {
+    return guarded([&] {
+        if (cap < static_cast<index_t>(g_last_report.size())) throw std::runtime_error("ref_last_report: buffer too small");
+        std::memcpy(out, g_last_report.data(), g_last_report.size());
     });
 }
 
