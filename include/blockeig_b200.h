@@ -218,7 +218,7 @@ be_status be_ctx_launches(be_ctx* ctx, int64_t* launches);
 
 typedef struct be_op be_op;
 
-enum { BE_OP_SYMMETRIC = 1, BE_OP_DETERMINISTIC = 2 };
+enum { BE_OP_SYMMETRIC = 1, BE_OP_DETERMINISTIC = 2, BE_OP_FORMAT_TILES = 4, BE_OP_FORMAT_ROWS = 8 };
 /* Upload a CSB to the device and derive the tile format.
  * flags & BE_OP_SYMMETRIC: validates square + strictly lower + diag length
  * like the SymmetricOperator constructor (kernels.hpp:341-350); diag (host,
@@ -228,7 +228,14 @@ enum { BE_OP_SYMMETRIC = 1, BE_OP_DETERMINISTIC = 2 };
  * thread in the reference's serial order (run_baseline, kernels.hpp:253-276:
  * L's entries of the row in CSB order, then L^T's, then the diagonal; no FMA
  * contraction) -- bit-reproducible and bit-identical to the serial reference
- * on f64 panels; reads each stored entry twice (the reference's two passes). */
+ * on f64 panels; reads each stored entry twice (the reference's two passes).
+ * Device format of the fast path (f32 values): BE_OP_FORMAT_TILES forces the
+ * 128 x 128 tile format (dense clustered matrices: each entry read once and
+ * applied twice, X rows staged in shared memory), BE_OP_FORMAT_ROWS the
+ * row-list format (L and L^T rows, X rows gathered from L2: very sparse
+ * matrices, where a 128 x 128 tile holds too few entries to amortise its
+ * staging); neither flag: chosen from the matrix (rows when it has >= 2^22
+ * entries and fewer than 384 per occupied 128 x 128 sub-tile). */
 be_status be_op_create(be_ctx* ctx, const be_csb_view* L, const double* diag, int values_prec,
                        int flags, be_op** out);
 be_status be_op_destroy(be_op* op);

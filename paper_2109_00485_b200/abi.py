@@ -24,6 +24,8 @@ BE_F32, BE_F64 = 0, 1
 BE_APPLY_SYMMETRIC, BE_APPLY_NOTRANS_ACC, BE_APPLY_TRANS_ACC = 0, 1, 2
 BE_OP_SYMMETRIC = 1
 BE_OP_DETERMINISTIC = 2  # f64 values, the serial reference summation order (bit-reproducible)
+BE_OP_FORMAT_TILES = 4  # force the 128 x 128 tile format
+BE_OP_FORMAT_ROWS = 8  # force the row-list format (very sparse matrices)
 SYNTH_KINDS = {"banded": 0, "blocktile": 1, "random": 2}
 
 
@@ -460,14 +462,16 @@ class Context:
 class Operator:
     """SymmetricOperator (kernels.hpp:339-378) backed by the device tile format."""
 
-    def __init__(self, ctx: Context, csb: Csb, diag=None, values_prec=BE_F32, symmetric=True, deterministic=False):
+    def __init__(self, ctx: Context, csb: Csb, diag=None, values_prec=BE_F32, symmetric=True, deterministic=False,
+                 fmt=None):
         self.ctx = ctx
         self._csb = csb  # the view's arrays must outlive creation only
         self._h = C.c_void_p()
         d = None if diag is None else np.ascontiguousarray(diag, dtype=np.float64)
         v = csb.view()
         check(lib().be_op_create(ctx.handle, C.byref(v), _p(d), C.c_int(values_prec),
-                                 C.c_int((BE_OP_SYMMETRIC if symmetric else 0) | (BE_OP_DETERMINISTIC if deterministic else 0)),
+                                 C.c_int((BE_OP_SYMMETRIC if symmetric else 0) | (BE_OP_DETERMINISTIC if deterministic else 0)
+                                         | {None: 0, "tiles": BE_OP_FORMAT_TILES, "rows": BE_OP_FORMAT_ROWS}[fmt]),
                                  C.byref(self._h)))
         self._csb = None
 

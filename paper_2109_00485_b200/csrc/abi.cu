@@ -416,7 +416,7 @@ be_status be_op_get_info(const be_op* op, be_op_info* info) {
         info->ntiles = o->ntiles;
         info->device_bytes = static_cast<int64_t>(o->tiles.bytes() + o->runs.bytes() + o->runs_ext.bytes() + o->blobs.bytes() +
                                                   o->det_ptr_n.bytes() + o->det_ptr_t.bytes() + o->det_col.bytes() +
-                                                  o->det_val.bytes());
+                                                  o->det_val.bytes() + o->rows_val.bytes());
         info->bytes_per_nnz_x1000 = o->nnz ? info->device_bytes * 1000 / o->nnz : 0;
         info->values_prec = o->values_prec;
         info->tile_rows = be::kTile;
@@ -429,7 +429,7 @@ be_status be_op_decode(be_op* op, int64_t* rows, int64_t* cols, double* values, 
     return guard([&] {
         if (!op) be::fail(BE_ERR_BAD_PARAMS, "null argument");
         auto* o = op->impl.get();
-        if (o->det) be::fail(BE_ERR_BAD_PARAMS, "be_op_decode: a deterministic operator has no tile format");
+        if (o->det || o->rows) be::fail(BE_ERR_BAD_PARAMS, "be_op_decode: operator has no tile format (row-list format)");
         if (o->csb_index.size() != static_cast<std::size_t>(o->padded) || (o->padded == 0 && o->nnz > 0))
             be::fail(BE_ERR_BAD_PARAMS, "be_op_decode: source index not retained for matrices this large");
         std::vector<be::TileHdr> h(static_cast<std::size_t>(o->ntiles));

@@ -134,6 +134,9 @@ struct Op {
     DBuf<std::int64_t> det_ptr_n, det_ptr_t;
     DBuf<std::int32_t> det_col;
     DBuf<double> det_val;
+    // row-list format for sparse matrices (k_rows_spmm): the same L / L^T row lists with f32 values
+    bool rows = false;
+    DBuf<float> rows_val;
     int grid = 0;
     // multi-GPU (row e): panel rows are owned in contiguous segments
     // [cuts[q], cuts[q+1]); tile coordinates live in the padded index space

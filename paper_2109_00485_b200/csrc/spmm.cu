@@ -818,9 +818,9 @@ bool launch_ws(Op* op, const int2* runs, index_t nruns, const float* X, float* Y
 // pass :363-370) with separately rounded products and sums (the reference's
 // u += v * w compiles without FMA), so the result is bit-reproducible and
 // bit-identical to the serial reference on f64 panels.
-template <typename TX>
+template <typename TX, typename TV = double>
 __global__ void k_det_spmm(const std::int64_t* __restrict__ pa, const std::int64_t* __restrict__ pb,
-                           const std::int32_t* __restrict__ col, const double* __restrict__ val,
+                           const std::int32_t* __restrict__ col, const TV* __restrict__ val,
                            const double* __restrict__ diag, const TX* __restrict__ X, TX* __restrict__ Y,
                            std::int64_t nout, int nb, int init_zero) {
     const int lane = threadIdx.x & 31;
@@ -830,13 +830,64 @@ __global__ void k_det_spmm(const std::int64_t* __restrict__ pa, const std::int64
         for (int v = lane; v < nb; v += 32) {
             double y = init_zero ? 0.0 : static_cast<double>(Y[r * nb + v]);
             for (std::int64_t e = pa[r]; e < pa[r + 1]; ++e)
-                y = __dadd_rn(y, __dmul_rn(val[e], static_cast<double>(X[static_cast<std::int64_t>(col[e]) * nb + v])));
+                y = __dadd_rn(y, __dmul_rn(static_cast<double>(val[e]), static_cast<double>(X[static_cast<std::int64_t>(col[e]) * nb + v])));
             if (pb)
                 for (std::int64_t e = pb[r]; e < pb[r + 1]; ++e)
-                    y = __dadd_rn(y, __dmul_rn(val[e], static_cast<double>(X[static_cast<std::int64_t>(col[e]) * nb + v])));
+                    y = __dadd_rn(y, __dmul_rn(static_cast<double>(val[e]), static_cast<double>(X[static_cast<std::int64_t>(col[e]) * nb + v])));
             if (diag) y = __dadd_rn(y, __dmul_rn(diag[r], static_cast<double>(X[r * nb + v])));
             Y[r * nb + v] = static_cast<TX>(y);
         }
+    }
+}
+
+// Row-list SpMM for sparse matrices (the BE_OP_FORMAT_ROWS device format):
+// output row r = its L entries, then its L^T entries (the same lists as the
+// deterministic mode, f32 values), summed by a group of G = NBP / 4 lanes that
+// each own 16 bytes of the row; the X rows are gathered straight from L2 (one
+// 64-byte line segment per group and entry at nb = 16) -- no shared-memory
+// staging, which a 128 x 128 tile holding a few hundred entries cannot
+// amortise. The group's lanes load G entries at once and broadcast them with
+// shuffles; every output row is written once, no atomics (deterministic).
+// init: 0 = Y <- sum, 1 = Y += sum, 2 = Y <- diag X + sum.
+template <int NBP>
+__global__ void __launch_bounds__(256) k_rows_spmm(const std::int64_t* __restrict__ pa, const std::int64_t* __restrict__ pb,
+                                                   const std::int32_t* __restrict__ col, const float* __restrict__ val,
+                                                   const double* __restrict__ diag, const float* __restrict__ X,
+                                                   float* __restrict__ Y, std::int64_t nout, int init) {
+    constexpr int G = NBP / 4, RPW = 32 / G;
+    const int lane = threadIdx.x & 31, sub = lane % G;
+    const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (lane - sub);
+    const std::int64_t w0 = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const std::int64_t nw = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (std::int64_t rb = w0 * RPW; rb < nout; rb += nw * RPW) {
+        const std::int64_t r = rb + lane / G;
+        const bool live = r < nout;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (live && init == 1) acc = reinterpret_cast<const float4*>(Y + r * NBP)[sub];
+        if (live && init == 2) {
+            const float d = static_cast<float>(diag[r]);
+            const float4 x = reinterpret_cast<const float4*>(X + r * NBP)[sub];
+            acc = make_float4(d * x.x, d * x.y, d * x.z, d * x.w);
+        }
+        for (int list = 0; list < (pb ? 2 : 1); ++list) {
+            const std::int64_t* ptr = list == 0 ? pa : pb;
+            std::int64_t e = live ? ptr[r] : 0;
+            const std::int64_t e1 = live ? ptr[r + 1] : 0;
+            for (; e < e1; e += G) {  // (lanes of different groups run their own trip counts)
+                const bool ok = e + sub < e1;
+                const int c = ok ? col[e + sub] : 0;
+                const float v = ok ? val[e + sub] : 0.f;
+                const int cnt = e1 - e < G ? static_cast<int>(e1 - e) : G;
+#pragma unroll 4
+                for (int k = 0; k < cnt; ++k) {
+                    const int ck = __shfl_sync(gmask, c, k, G);
+                    const float vk = __shfl_sync(gmask, v, k, G);
+                    const float4 x = __ldg(reinterpret_cast<const float4*>(X + static_cast<std::int64_t>(ck) * NBP) + sub);
+                    vfma(acc, vk, x);
+                }
+            }
+        }
+        if (live) reinterpret_cast<float4*>(Y + r * NBP)[sub] = acc;
     }
 }
 
@@ -1236,7 +1287,8 @@ Op::~Op() {
 // global row gives each row's L entries in run_baseline's notrans order (column
 // blocks ascending, stored order within a block); by global column, each
 // column's entries in its trans order (row blocks ascending).
-static void op_build_det(Op* op, const be_csb_view& L) {
+template <typename TV>
+static void op_build_lists(Op* op, const be_csb_view& L, DBuf<TV>& vals_out) {
     const index_t n = L.nrows, m = L.ncols, nnz = L.nnz;
     if (nnz >= (index_t{1} << 40)) fail(BE_ERR_BAD_PARAMS, "deterministic operator too large");
     std::vector<std::int64_t> pn(static_cast<std::size_t>(n) + 1, 0), pt(static_cast<std::size_t>(m) + 1, 0);
@@ -1254,7 +1306,7 @@ static void op_build_det(Op* op, const be_csb_view& L) {
     for (std::size_t i = 1; i < pn.size(); ++i) pn[i] += pn[i - 1];
     for (std::size_t i = 1; i < pt.size(); ++i) pt[i] += pt[i - 1];
     std::vector<std::int32_t> col(static_cast<std::size_t>(2 * nnz));
-    std::vector<double> val(static_cast<std::size_t>(2 * nnz));
+    std::vector<TV> val(static_cast<std::size_t>(2 * nnz));
     std::vector<std::int64_t> cn(pn.begin(), pn.end() - 1), ct(pt.begin(), pt.end() - 1);
     for (auto& c : ct) c += nnz;  // the L^T lists follow the L lists
     for (index_t b = 0; b < L.nrowblks * L.ncolblks; ++b)  // blocks row-major, entries in stored order
@@ -1262,23 +1314,47 @@ static void op_build_det(Op* op, const be_csb_view& L) {
             const auto r = grow[static_cast<std::size_t>(k)], c = gcol[static_cast<std::size_t>(k)];
             const auto qn = cn[static_cast<std::size_t>(r)]++;
             col[static_cast<std::size_t>(qn)] = c;
-            val[static_cast<std::size_t>(qn)] = L.values[k];
+            val[static_cast<std::size_t>(qn)] = static_cast<TV>(L.values[k]);
             const auto qt = ct[static_cast<std::size_t>(c)]++;
             col[static_cast<std::size_t>(qt)] = r;
-            val[static_cast<std::size_t>(qt)] = L.values[k];
+            val[static_cast<std::size_t>(qt)] = static_cast<TV>(L.values[k]);
         }
     for (auto& x : pt) x += nnz;
-    op->det = true;
     op->det_ptr_n.reset(n + 1);
     op->det_ptr_t.reset(m + 1);
     op->det_col.reset(std::max<index_t>(2 * nnz, 1));
-    op->det_val.reset(std::max<index_t>(2 * nnz, 1));
+    vals_out.reset(std::max<index_t>(2 * nnz, 1));
     BE_CUDA(cudaMemcpy(op->det_ptr_n.get(), pn.data(), pn.size() * 8, cudaMemcpyHostToDevice));
     BE_CUDA(cudaMemcpy(op->det_ptr_t.get(), pt.data(), pt.size() * 8, cudaMemcpyHostToDevice));
     if (nnz > 0) {
         BE_CUDA(cudaMemcpy(op->det_col.get(), col.data(), col.size() * 4, cudaMemcpyHostToDevice));
-        BE_CUDA(cudaMemcpy(op->det_val.get(), val.data(), val.size() * 8, cudaMemcpyHostToDevice));
+        BE_CUDA(cudaMemcpy(vals_out.get(), val.data(), val.size() * sizeof(TV), cudaMemcpyHostToDevice));
     }
+}
+
+// Occupied 128 x 128 sub-tiles of L (the tile format's work units), exactly.
+static index_t occupied_subtiles(const be_csb_view& L) {
+    std::vector<index_t> per(static_cast<std::size_t>(L.nrowblks), 0);
+    parallel_for_dynamic(hw_threads(), L.nrowblks, [&](index_t bi, int) {
+        std::vector<std::uint64_t> bits;
+        index_t c = 0;
+        for (index_t bj = 0; bj < L.ncolblks; ++bj) {
+            const index_t b = bi * L.ncolblks + bj, cnt = L.block_nnz[b];
+            if (cnt == 0) continue;
+            const index_t tb = (L.col_offsets[bj + 1] - L.col_offsets[bj] + kTile - 1) / kTile;
+            const index_t ta = (L.row_offsets[bi + 1] - L.row_offsets[bi] + kTile - 1) / kTile;
+            bits.assign(static_cast<std::size_t>((ta * tb + 63) / 64), 0);
+            for (index_t k = L.block_nnz_offsets[b]; k < L.block_nnz_offsets[b] + cnt; ++k) {
+                const index_t q = (L.local_rows[k] / kTile) * tb + L.local_cols[k] / kTile;
+                bits[static_cast<std::size_t>(q >> 6)] |= std::uint64_t{1} << (q & 63);
+            }
+            for (auto w : bits) c += __builtin_popcountll(w);
+        }
+        per[static_cast<std::size_t>(bi)] = c;
+    });
+    index_t tot = 0;
+    for (auto c : per) tot += c;
+    return tot;
 }
 
 std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag, int values_prec, int flags) {
@@ -1300,9 +1376,21 @@ std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag
         fail(BE_ERR_BAD_PARAMS, "sym_spmm: dimension exceeds 2^31 rows per device");
     if (flags & BE_OP_DETERMINISTIC) {
         op->values_prec = BE_F64;
-        op_build_det(op.get(), L);
+        op_build_lists<double>(op.get(), L, op->det_val);
+        op->det = true;
     } else {
-        op_build(op.get(), L, nullptr);
+        bool rows = false;
+        if (values_prec == BE_F32 && !(flags & BE_OP_FORMAT_TILES)) {
+            if (flags & BE_OP_FORMAT_ROWS) rows = true;
+            else if (const char* e = std::getenv("BE_SPMM_FORMAT")) rows = std::strcmp(e, "rows") == 0;  // (experiments)
+            else if (L.nnz >= (index_t{1} << 22)) rows = L.nnz < 384 * occupied_subtiles(L);
+        }
+        if (rows) {
+            op_build_lists<float>(op.get(), L, op->rows_val);
+            op->rows = true;
+        } else {
+            op_build(op.get(), L, nullptr);
+        }
     }
     if (op->symmetric) {
         op->diag.reset(std::max<index_t>(L.nrows, 1));
@@ -1509,7 +1597,61 @@ void op_apply(Op* op, const void* X, void* Y, index_t in_rows, int nb, int panel
     auto grid_for = [&](index_t total) {
         return static_cast<int>(std::max<index_t>(1, std::min<index_t>((total + 255) / 256, op->ctx->num_sms * 8)));
     };
-    if (op->det) {  // deterministic mode: one pass over the row lists
+    if (op->rows) {  // row-list format (sparse matrices, f32 values)
+        if (op->timing) BE_CUDA(cudaEventRecord(op->ev[1], s));
+        const std::int64_t* pa = mode == BE_APPLY_TRANS_ACC ? op->det_ptr_t.get() : op->det_ptr_n.get();
+        const std::int64_t* pb = mode == BE_APPLY_SYMMETRIC ? op->det_ptr_t.get() : nullptr;
+        const bool f64p = panel_prec == BE_F64;
+        const float* xs = static_cast<const float*>(X);
+        float* ys = static_cast<float*>(Y);
+        if (f64p) {  // f32 copy of X; the f32 sums land in y32 and the finish adds them (and D X) in f64
+            const index_t need = std::max(in_tot, out_tot);
+            if (op->x32.n < need) {
+                op->x32.reset(need);
+                op->y32.reset(need);
+            }
+            k_f64_to_f32<<<grid_for(in_tot), 256, 0, s>>>(static_cast<const double*>(X), op->x32.get(), in_tot, nullptr, 0);
+            BE_CUDA(cudaGetLastError());
+            ++op->ctx->launches;
+            xs = op->x32.get();
+            ys = op->y32.get();
+        }
+        const int init = f64p ? 0 : (mode == BE_APPLY_SYMMETRIC ? 2 : 1);
+        const double* dg = init == 2 ? op->diag.get() : nullptr;
+        const bool a16 = (reinterpret_cast<std::uintptr_t>(xs) & 15u) == 0 && (reinterpret_cast<std::uintptr_t>(ys) & 15u) == 0;
+        if (out_rows > 0) {
+            auto launch = [&](auto kern, int rows_per_warp) {
+                const index_t warps = (out_rows + rows_per_warp - 1) / rows_per_warp;
+                const int g = static_cast<int>(std::max<index_t>(1, std::min<index_t>((warps * 32 + 255) / 256, op->ctx->num_sms * 16)));
+                kern<<<g, 256, 0, s>>>(pa, pb, op->det_col.get(), op->rows_val.get(), dg, xs, ys, out_rows, init);
+            };
+            if (a16 && nb == 16) launch(k_rows_spmm<16>, 8);
+            else if (a16 && nb == 8) launch(k_rows_spmm<8>, 16);
+            else if (a16 && nb == 32) launch(k_rows_spmm<32>, 4);
+            else if (a16 && nb == 4) launch(k_rows_spmm<4>, 32);
+            else if (init == 1) {  // other widths: one warp per row, lane = column
+                k_det_spmm<float, float><<<grid_for(out_rows * 32), 256, 0, s>>>(pa, pb, op->det_col.get(), op->rows_val.get(),
+                                                                              nullptr, xs, ys, out_rows, nb, 0);
+            } else {
+                if (init == 2) {  // Y = D X first, then the lists accumulate
+                    k_diag_init<float><<<grid_for(out_tot), 256, 0, s>>>(op->diag.get(), xs, ys, out_rows, nb);
+                    BE_CUDA(cudaGetLastError());
+                    ++op->ctx->launches;
+                }
+                k_det_spmm<float, float><<<grid_for(out_rows * 32), 256, 0, s>>>(pa, pb, op->det_col.get(), op->rows_val.get(),
+                                                                              nullptr, xs, ys, out_rows, nb, init == 0 ? 1 : 0);
+            }
+            BE_CUDA(cudaGetLastError());
+            ++op->ctx->launches;
+        }
+        if (f64p && out_tot > 0) {
+            k_finish_f64<<<grid_for(out_tot), 256, 0, s>>>(op->diag.get(), static_cast<const double*>(X), op->y32.get(),
+                                                            static_cast<double*>(Y), out_rows, nb,
+                                                            mode == BE_APPLY_SYMMETRIC ? 1 : 0);
+            BE_CUDA(cudaGetLastError());
+            ++op->ctx->launches;
+        }
+    } else if (op->det) {  // deterministic mode: one pass over the row lists
         if (op->timing) BE_CUDA(cudaEventRecord(op->ev[1], s));
         const std::int64_t* pa = mode == BE_APPLY_TRANS_ACC ? op->det_ptr_t.get() : op->det_ptr_n.get();
         const std::int64_t* pb = mode == BE_APPLY_SYMMETRIC ? op->det_ptr_t.get() : nullptr;

@@ -249,3 +249,43 @@ def test_deterministic_solve_is_bit_reproducible(ctx):
     assert r1["iterations"] == r2["iterations"]
     assert np.array_equal(r1["lambda_"], r2["lambda_"]) and np.array_equal(r1["x"], r2["x"])
     assert np.array_equal(r1["theta"], r2["theta"]) and np.array_equal(r1["residual_norms"], r2["residual_norms"])
+
+
+# --- row-list format (BE_OP_FORMAT_ROWS: very sparse matrices, X gathered from L2) ----------
+@pytest.mark.parametrize("nb", [1, 3, 4, 8, 16, 32, 48])
+def test_row_list_format_matches_oracle(ctx, nb):
+    m, diag = sym_problem(2500, 20000, 800, 21)
+    op = abi.Operator(ctx, m, diag, values_prec=abi.BE_F32, fmt="rows")
+    orc = ol.Impl("orc")
+    x = np.random.default_rng(nb).uniform(-1, 1, (2500, nb))
+    assert relf(op.apply_host(x), orc.spmm(m, diag, x)) <= 1e-5
+    y0 = np.random.default_rng(7).uniform(-1, 1, (2500, nb))
+    for mode in (abi.BE_APPLY_NOTRANS_ACC, abi.BE_APPLY_TRANS_ACC):
+        assert relf(op.apply_host(x, y0.copy(), mode=mode), orc.spmm(m, None, x, y0, mode=mode)) <= 1e-5
+
+
+@pytest.mark.parametrize("nb", [8, 16])
+def test_row_list_format_f32_panels_and_determinism(ctx, nb):
+    import torch
+    m, diag = sym_problem(3000, 40000, 1000, 5)
+    op = abi.Operator(ctx, m, diag, values_prec=abi.BE_F32, fmt="rows")
+    x = torch.rand(3000, nb, dtype=torch.float32, device="cuda") * 2 - 1
+    y1 = torch.empty_like(x)
+    y2 = torch.empty_like(x)
+    op.apply_dev(x.data_ptr(), y1.data_ptr(), 3000, nb, abi.BE_F32, abi.BE_APPLY_SYMMETRIC, ctx.stream())
+    op.apply_dev(x.data_ptr(), y2.data_ptr(), 3000, nb, abi.BE_F32, abi.BE_APPLY_SYMMETRIC, ctx.stream())
+    ctx.synchronize()
+    assert torch.equal(y1, y2)  # no atomics: every output row is summed by one lane group
+    want = ol.Impl("orc").spmm(m, diag, x.double().cpu().numpy())
+    assert relf(y1.double().cpu().numpy(), want) <= 1e-5
+
+
+def test_auto_format_choice(ctx):
+    """Large and sparse (C1-like density) -> row lists; the clustered generator -> tiles."""
+    s = abi.Synthetic("random", n=40000, density=0.006, block_extent=4000, seed=3)
+    b = abi.uniform_boundaries(40000, 4000)
+    m = abi.build_csb_coo(s.lower, 40000, 40000, b, b)
+    assert m.nnz >= 1 << 22
+    assert abi.Operator(ctx, m, s.diag).info().ntiles == 0
+    mc, dc, _ = abi.generate_clustered(n=200000, target_nnz=1 << 23, seed=2)
+    assert abi.Operator(ctx, mc, dc).info().ntiles > 0
