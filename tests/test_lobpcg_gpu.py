@@ -105,12 +105,13 @@ def test_matches_oracle(ctx, seed, n, nnz, k, nb, precond):
 
 
 def envelope(m, d, toff, **kw):
-    """min / max iterations of the reference over summation orders: serial,
-    4- and 8-thread baseline and fused-atomic; oracle alone when
-    the reference build is absent."""
+    """min / max iterations of the reference over summation orders: serial and
+    ThreadPool(2..8) with the baseline and fused-atomic SpMM variants (SURVEY
+    8c; the C1 test uses the same 1..8 thread sweep); oracle alone when the
+    reference build is absent."""
     its = [ol.Impl("orc").lobpcg(m, d, toff, **kw)["iterations"]]
     if ol.ref() is not None:
-        for threads, variant in ((1, 0), (4, 0), (4, 1), (8, 0), (8, 1)):
+        for threads, variant in [(1, 0)] + [(t, v) for t in range(2, 9) for v in (0, 1)]:
             its.append(ol.Impl("ref", threads=threads, variant=variant).lobpcg(m, d, toff, **kw)["iterations"])
     return min(its), max(its)
 
