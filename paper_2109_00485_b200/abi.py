@@ -864,6 +864,18 @@ def lobpcg(ctx: Context, op=None, n=None, tiles: Tiles | None = None, x0=None, k
             print(f"[be] host: records + result free {1e3 * (time.perf_counter() - t1):.1f} ms", file=sys.stderr, flush=True)
 
 
+def dense_mix(ctx: Context, x: np.ndarray, c: np.ndarray, y: np.ndarray | None = None) -> np.ndarray:
+    """block_times_small(_add) (densela.hpp:448-484) on the device: Y (+)= X C for host panels."""
+    x = np.ascontiguousarray(x, np.float64)
+    cc = np.asfortranarray(c, np.float64)
+    n, p = x.shape
+    q = cc.shape[1]
+    acc = y is not None
+    out = np.ascontiguousarray(y, np.float64).copy() if acc else np.zeros((n, q))
+    check(lib().be_dense_mix(ctx.handle, _p(x), C.c_int64(n), C.c_int(p), _p(cc), C.c_int(q), _p(out), C.c_int(int(acc))))
+    return out
+
+
 def gram_dev(ctx: Context, a_ptr: int, b_ptr: int, nb: int, n: int) -> np.ndarray:
     out = np.zeros(nb * nb)
     check(lib().be_gram(ctx.handle, C.c_void_p(a_ptr), C.c_int(nb), C.c_void_p(b_ptr), C.c_int(nb), C.c_int64(n),

@@ -728,8 +728,11 @@ struct MixT {
     int qo[4], qs[4]; // output, staged source of each slot
     int last[4];      // slot ends its output
 };
-template <int NBB>
-__global__ void __launch_bounds__(kT, 2) k_mix_t(MixDev m, MixSrc ms, MixT mt, std::int64_t n) {
+// BSM (nb = 24, 32): the B fragments no longer fit the registers and are read
+// from shared memory instead, laid out fragment-major so a warp's 32 loads of
+// one fragment are one contiguous 256-byte read.
+template <int NBB, bool BSM = false>
+__global__ void __launch_bounds__(kT, BSM ? 1 : 2) k_mix_t(MixDev m, MixSrc ms, MixT mt, std::int64_t n) {
     constexpr int NB = NBB * 8, KS = NB / 4, LD = NB + 4, MAXT = 4;
     static_assert(kMixPRows == 8 * (kT / 32), "one 8-row block per warp");
     extern __shared__ __align__(16) double sh[];
@@ -749,19 +752,36 @@ __global__ void __launch_bounds__(kT, 2) k_mix_t(MixDev m, MixSrc ms, MixT mt, s
     issue(0);
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, rl = (threadIdx.x >> 5) * 8 + g;
     // B fragments: B[k = t][col = g] of each slot's coefficient block
-    double bf[MAXT][KS][NBB];
+    double bf[BSM ? 1 : MAXT][BSM ? 1 : KS][BSM ? 1 : NBB];
+    double* bsm = sh + 2 * static_cast<std::size_t>(ss);  // (BSM) [slot][k][cb][lane]
+    if constexpr (BSM) {
+        for (int e = threadIdx.x; e < MAXT * KS * NBB * 32; e += kT) {
+            const int ln = e & 31, cb = (e >> 5) % NBB, k = (e >> 5) / NBB % KS, q = (e >> 5) / (NBB * KS);
+            const int gg = ln >> 2, tq = ln & 3;
+            double v = 0.0;
+            if (q < mt.nq) {
+                const int o = mt.qo[q];
+                int tt = 0;
+                for (int p = 0; p < q; ++p) tt += mt.qo[p] == o;
+                const double* cf = m.coef[m.out[o].ci[tt]];
+                v = m.out[o].sign[tt] * cf[(8 * cb + gg) * m.ld[m.out[o].ci[tt]] + 4 * k + tq];
+            }
+            bsm[e] = v;
+        }  // (visible after the first chunk's barrier below)
+    } else {
 #pragma unroll
-    for (int q = 0; q < MAXT; ++q) {
-        const int o = q < mt.nq ? mt.qo[q] : 0;
-        int tt = 0;
-        for (int p = 0; p < q; ++p) tt += mt.qo[p] == o;
-        const double* cf = q < mt.nq ? m.coef[m.out[o].ci[tt]] : nullptr;
-        const int ld = q < mt.nq ? m.ld[m.out[o].ci[tt]] : 0;
-        const double sg = q < mt.nq ? m.out[o].sign[tt] : 0.0;
+        for (int q = 0; q < MAXT; ++q) {
+            const int o = q < mt.nq ? mt.qo[q] : 0;
+            int tt = 0;
+            for (int p = 0; p < q; ++p) tt += mt.qo[p] == o;
+            const double* cf = q < mt.nq ? m.coef[m.out[o].ci[tt]] : nullptr;
+            const int ld = q < mt.nq ? m.ld[m.out[o].ci[tt]] : 0;
+            const double sg = q < mt.nq ? m.out[o].sign[tt] : 0.0;
 #pragma unroll
-        for (int k = 0; k < KS; ++k)
+            for (int k = 0; k < KS; ++k)
 #pragma unroll
-            for (int cb = 0; cb < NBB; ++cb) bf[q][k][cb] = cf ? sg * cf[(8 * cb + g) * ld + 4 * k + t] : 0.0;
+                for (int cb = 0; cb < NBB; ++cb) bf[q][k][cb] = cf ? sg * cf[(8 * cb + g) * ld + 4 * k + t] : 0.0;
+        }
     }
     for (int c = 0; c < nch; ++c) {
         issue(c + 1);
@@ -781,7 +801,10 @@ __global__ void __launch_bounds__(kT, 2) k_mix_t(MixDev m, MixSrc ms, MixT mt, s
             for (int k = 0; k < KS; ++k) {
                 const double a = xa[4 * k];
 #pragma unroll
-                for (int cb = 0; cb < NBB; ++cb) dmma884(acc[cb][0], acc[cb][1], a, bf[q][k][cb]);
+                for (int cb = 0; cb < NBB; ++cb) {
+                    if constexpr (BSM) dmma884(acc[cb][0], acc[cb][1], a, bsm[((q * KS + k) * NBB + cb) * 32 + lane]);
+                    else dmma884(acc[cb][0], acc[cb][1], a, bf[q][k][cb]);
+                }
             }
             if (mt.last[q]) {  // output complete: old value / added panel, store, reset
                 const auto& O = m.out[mt.qo[q]];
@@ -1449,7 +1472,7 @@ void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
     const int nblk = (job.nb + 3) / 4;
     {  // tensor-core path: nb in {8, 16}, <= 4 term slots, no add_from, every output has a term
         MixT mt{};
-        bool ok = (job.nb == 8 || job.nb == 16);
+        bool ok = (job.nb == 8 || job.nb == 16 || job.nb == 24 || job.nb == 32);
         for (int o = 0; o < m.nout && ok; ++o) {
             if (m.out[o].add_from >= 0 || m.out[o].nterms < 1 || mt.nq + m.out[o].nterms > 4) {
                 ok = false;
@@ -1462,16 +1485,24 @@ void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
                 ++mt.nq;
             }
         }
-        const std::size_t smt = 2 * static_cast<std::size_t>(ms.nsrc) * kMixPRows * (job.nb + 4) * sizeof(double);
+        const bool bsm = job.nb > 16;
+        const std::size_t smt = 2 * static_cast<std::size_t>(ms.nsrc) * kMixPRows * (job.nb + 4) * sizeof(double) +
+                                (bsm ? 4 * static_cast<std::size_t>(job.nb / 4) * (job.nb / 8) * 32 * sizeof(double) : 0);
         if (ok && smt <= 200 * 1024) {
             const int grid = static_cast<int>(
                 std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 2, (n + kMixPRows - 1) / kMixPRows)));
             if (job.nb == 8) {
                 ensure_dyn_smem(k_mix_t<1>, smt);
                 k_mix_t<1><<<grid, kT, smt, s>>>(m, ms, mt, n);
-            } else {
+            } else if (job.nb == 16) {
                 ensure_dyn_smem(k_mix_t<2>, smt);
                 k_mix_t<2><<<grid, kT, smt, s>>>(m, ms, mt, n);
+            } else if (job.nb == 24) {
+                ensure_dyn_smem(k_mix_t<3, true>, smt);
+                k_mix_t<3, true><<<grid, kT, smt, s>>>(m, ms, mt, n);
+            } else {
+                ensure_dyn_smem(k_mix_t<4, true>, smt);
+                k_mix_t<4, true><<<grid, kT, smt, s>>>(m, ms, mt, n);
             }
             BE_CUDA(cudaGetLastError());
             ++ctx->launches;

@@ -85,7 +85,8 @@ def test_config_validation(ctx):  # test_lobpcg.cpp:409-421
         abi.lobpcg(ctx, op, k=5, nb=8, tol=0.0)
 
 
-@pytest.mark.parametrize("seed,n,nnz,k,nb,precond", [(88, 200, 800, 3, 6, False),
+@pytest.mark.parametrize("seed,n,nnz,k,nb,precond", [(88, 200, 800, 3, 6, False), (7, 3000, 60000, 16, 32, False),
+                                                     (8, 3000, 60000, 12, 24, False),
                                                       (99, 1500, 30000, 5, 8, False), (5, 2000, 40000, 8, 16, False)])
 def test_matches_oracle(ctx, seed, n, nnz, k, nb, precond):
     m, d = make_test_matrix(n, nnz, seed)
@@ -308,6 +309,20 @@ def test_gram_matches_numpy(ctx):
     assert np.allclose(g, want, rtol=1e-12, atol=1e-10)
     gs = abi.gram_dev(ctx, a.data_ptr(), a.data_ptr(), 16, 12345)
     assert np.array_equal(gs, gs.T)
+
+
+@pytest.mark.parametrize("nb", [8, 12, 16, 24, 32])
+def test_block_times_small_matches_numpy(ctx, nb):
+    """block_times_small(_add) (densela.hpp:448-484): the tensor-core mix (nb = 8, 16; 24, 32 with the
+    coefficient fragments in shared memory) and the FFMA kernel (other widths), f64 to ~1e-14."""
+    rng = np.random.default_rng(nb)
+    x = rng.uniform(-1, 1, (5000, nb))
+    c = rng.uniform(-1, 1, (nb, nb))
+    y0 = rng.uniform(-1, 1, (5000, nb))
+    got = abi.dense_mix(ctx, x, c)
+    assert np.max(np.abs(got - x @ c)) <= 1e-13 * nb
+    got = abi.dense_mix(ctx, x, c, y0)
+    assert np.max(np.abs(got - (y0 + x @ c))) <= 1e-13 * nb
 
 
 def test_repeated_solves_reuse_the_context_panels(ctx):
