@@ -7,11 +7,15 @@
 
 #include <chrono>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
+#include <thread>
 
 #include "comm.hpp"
 
 namespace be {
+
+void Comm::sync(cudaStream_t s) { BE_CUDA(cudaStreamSynchronize(s)); }
 
 namespace {
 
@@ -27,6 +31,8 @@ struct NcclApi {
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
 };
 
 const NcclApi& nccl() {
@@ -55,6 +61,8 @@ const NcclApi& nccl() {
         api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
         api.ReduceScatter = reinterpret_cast<decltype(api.ReduceScatter)>(sym("ncclReduceScatter"));
         api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+        api.CommGetAsyncError = reinterpret_cast<decltype(api.CommGetAsyncError)>(sym("ncclCommGetAsyncError"));
+        api.CommAbort = reinterpret_cast<decltype(api.CommAbort)>(sym("ncclCommAbort"));
     });
     if (!err.empty()) fail(BE_ERR_NCCL, err);
     return api;
@@ -102,6 +110,28 @@ class NcclComm final : public Comm {
     }
     ~NcclComm() override {
         if (comm_) nccl().CommDestroy(comm_);
+    }
+    void sync(cudaStream_t s) override {
+        const auto t0 = std::chrono::steady_clock::now();
+        double limit = 600.0;
+        if (const char* e = std::getenv("BE_COMM_TIMEOUT_S")) limit = std::atof(e);
+        for (int spin = 0;; ++spin) {
+            const cudaError_t q = cudaStreamQuery(s);
+            if (q == cudaSuccess) return;
+            if (q != cudaErrorNotReady) BE_CUDA(q);
+            ncclResult_t ae = ncclSuccess;
+            BE_NCCL(nccl().CommGetAsyncError(comm_, &ae));
+            const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if ((ae != ncclSuccess && ae != ncclInProgress) || el > limit) {
+                const std::string why = ae != ncclSuccess && ae != ncclInProgress
+                                            ? std::string("asynchronous NCCL error: ") + nccl().GetErrorString(ae)
+                                            : "no progress in " + std::to_string(limit) + " s";
+                nccl().CommAbort(comm_);
+                comm_ = nullptr;
+                fail(BE_ERR_PROTOCOL_DEADLOCK, "distributed collective: a rank is missing (" + why + ")");
+            }
+            if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
     }
     void allreduce_f64(double* buf, std::size_t count, cudaStream_t s) override {
         BE_NCCL(nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, comm_, s));

@@ -40,6 +40,12 @@ struct Comm {
     // (send holds world * count floats). In place when recv == send + rank * count.
     virtual void reduce_scatter_f32(const float* send, float* recv, std::size_t count, cudaStream_t s) = 0;
     virtual const char* backend() const = 0;
+    // Wait for stream s while watching the group (NCCL: ncclCommGetAsyncError; a failed
+    // or vanished peer leaves the collective pending forever): an asynchronous error, or
+    // no progress within BE_COMM_TIMEOUT_S seconds (default 600), aborts the
+    // communicator and throws ProtocolDeadlock -- the reference's "a rank is missing from
+    // the collective" (dist.hpp:256-263, 273-282).
+    virtual void sync(cudaStream_t s);
     std::int64_t calls = 0;       // collectives issued
     std::int64_t bytes_moved = 0; // bytes this rank received (flat model, like SimComm::volume_doubles)
 };

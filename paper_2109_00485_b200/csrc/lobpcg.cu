@@ -187,9 +187,14 @@ struct Solver {
         ctx->solver_keep = std::move(keep);
     }
 
+    // host wait on the solver stream; with a communicator it watches the group (Comm::sync)
+    void wait() {
+        if (comm) comm->sync(s);
+        else BE_CUDA(cudaStreamSynchronize(s));
+    }
     void sync_status() {
         BE_CUDA(cudaMemcpyAsync(&hm->st, st.get(), sizeof(dla::Status), cudaMemcpyDeviceToHost, s));
-        BE_CUDA(cudaStreamSynchronize(s));
+        wait();
     }
     // qr_failures and rank_deficient only: singular_tri stays set until the iteration's check
     void reset_qr_flags() { BE_CUDA(cudaMemsetAsync(st.get(), 0, 2 * sizeof(int), s)); }
