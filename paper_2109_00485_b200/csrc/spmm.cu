@@ -533,13 +533,17 @@ __global__ void __launch_bounds__(kThreads, 2)
 // per SM: a producer warp streams each tile's blob, its X_J rows and its X_I
 // rows into a ring of kWsStages shared-memory stages with 1-D bulk copies
 // (cp.async.bulk, completion on a per-stage "full" mbarrier); eight consumer
-// warps each run a precomputed, equal-entry piece of the tile's work (the
-// blob's work split: pass-R and pass-C rank groups cut by diagonal), flush
-// every partial row with red.global.add.v4.f32 and release the stage on a
+// warps each run one unit of the tile's work -- a pass (R: Y_I += A X_J,
+// C: Y_J += A^T X_I) over one group of 32 rank lanes -- warp w taking unit
+// (w + tile) mod 8, so over eight tiles every warp runs every unit once; they
+// flush each row with red.global.add.v4.f32 and release the stage on a
 // per-stage "empty" mbarrier. No CTA-wide barrier: a warp that finishes its
-// piece early starts on the next tile (up to kWsStages - 1 tiles ahead), so
-// the per-tile imbalance between passes and rank groups no longer idles the
-// shared-memory crossbar. The staged X rows are REP = 128 / (4 nb) plain
+// unit early starts on the next tile (up to kWsStages - 1 tiles ahead), so the
+// per-tile imbalance between units (the longest rank group carries ~2x the
+// entries of the shortest) averages out instead of idling the shared-memory
+// crossbar, and no rank is split between warps (one flush per rank and pass;
+// the blob's equal-entry work split, BE_SPMM_WS_ROT=0, costs ~20 % more in
+// split-rank flushes). The staged X rows are REP = 128 / (4 nb) plain
 // copies, copy q placed at q * 129 rows so that row r of copy q sits in the
 // 128-byte bank line slot (q + r) mod REP: lane L reads the copy that puts its
 // row in slot (L / CH) mod REP, so a quarter-warp's eight 16-byte reads are
@@ -616,7 +620,7 @@ template <int NBP, int kWsStages>
 __global__ void __launch_bounds__(kWsThreads, kWsStages <= 2 ? 2 : 1)
     k_sym_spmm_ws(const int2* __restrict__ runs, int nruns, const TileHdr* __restrict__ tiles,
                   const unsigned char* __restrict__ blobs, const float* __restrict__ X, float* __restrict__ Y,
-                  int do_r, int do_c, int blob_max, int stage_bytes, int* __restrict__ ctr) {
+                  int do_r, int do_c, int blob_max, int stage_bytes, int rot, int* __restrict__ ctr) {
     using G = WsGeom<NBP>;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) std::uint64_t full[kWsStages], empty[kWsStages], xfull[2], xempty[2];
@@ -714,7 +718,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsStages <= 2 ? 2 : 1)
 #pragma unroll
     for (int i = 0; i < G::CH; ++i) coff[i] = ((i + lane) % G::CH) * 16;
     const int slot = (lane / G::CH) % G::REP;
-    int s = 0;
+    int s = 0, tcount = 0;
     std::uint32_t fph = 0, xph = 0;
     for (;;) {
         stream::mbar_wait(&full[s], (fph >> s) & 1u);
@@ -729,7 +733,16 @@ __global__ void __launch_bounds__(kWsThreads, kWsStages <= 2 ? 2 : 1)
         const unsigned char* st = smem + static_cast<std::size_t>(s) * stage_bytes;
         const int npad = pad16(static_cast<int>(h.packed >> 14));
         const std::uint16_t* seg = reinterpret_cast<const std::uint16_t*>(st + kMetaSeg);
-        const int b0 = seg[warp], b1 = seg[warp + 1];
+        int b0, b1;
+        if (rot) {  // whole units, rotated by tile: warp w runs unit (w + tile) mod 8, no split ranks
+            const int un0 = (warp + tcount) & 7;
+            b0 = un0 << 8;
+            b1 = (un0 + 1) << 8;
+        } else {  // the blob's equal-entry pieces
+            b0 = seg[warp];
+            b1 = seg[warp + 1];
+        }
+        ++tcount;
         int un = b0 >> 8, d = b0 & 255;
         const int ue = b1 >> 8, de = b1 & 255;
         while (un < ue || (un == ue && d < de)) {
@@ -792,8 +805,12 @@ bool launch_ws_s(Op* op, const int2* runs, index_t nruns, const float* X, float*
     const int grid = static_cast<int>(std::min<index_t>(static_cast<index_t>(per_sm) * op->ctx->num_sms, nruns));
     op->grid = grid;
     if (grid == 0) return true;
+    static const int rot = [] {  // whole units rotated by tile (default) or the blob's equal-entry pieces
+        const char* e = std::getenv("BE_SPMM_WS_ROT");
+        return e ? std::atoi(e) : 1;
+    }();
     kern<<<grid, kWsThreads, sm, s>>>(runs, static_cast<int>(nruns), op->tiles.get(), op->blobs.get(), X, Y, do_r, do_c,
-                                      op->blob_max, stage, op->counter.get());
+                                      op->blob_max, stage, rot, op->counter.get());
     BE_CUDA(cudaGetLastError());
     ++op->ctx->launches;
     return true;
@@ -979,12 +996,12 @@ template <typename TC, typename TV, typename TX>
 void dispatch_nb(Op* op, const int2* runs, index_t nruns, const TX* X, TX* Y, int nb, int do_r, int do_c,
                  cudaStream_t s) {
     if constexpr (std::is_same_v<TC, float> && std::is_same_v<TV, float> && std::is_same_v<TX, float>) {
-        // the warp-specialised kernel where it is measured faster (nb = 8: 5.4 vs 6.3 ms, nb = 32:
-        // 17.9 vs 32.5 ms at T1); at nb = 16 the two are within 2 % and the classic kernel stays.
-        // BE_SPMM_WS=1 / 0 forces it on / off for every width (experiments).
+        // the warp-specialised kernel for the widths it covers (T1: nb = 8 4.7 vs 6.3 ms, nb = 16
+        // 8.0 vs 9.4 ms, nb = 32 14.9 vs 32.5 ms against the classic kernel); BE_SPMM_WS=0 selects
+        // the classic kernel (experiments)
         static const int ws_mode = [] {
             const char* e = std::getenv("BE_SPMM_WS");
-            return e ? (e[0] == '0' ? 0 : 2) : 1;
+            return e && e[0] == '0' ? 0 : 2;
         }();
         const bool aligned = (reinterpret_cast<std::uintptr_t>(X) & 15u) == 0 && (reinterpret_cast<std::uintptr_t>(Y) & 15u) == 0;
         if (ws_mode > 0 && aligned) {
