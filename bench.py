@@ -588,7 +588,7 @@ def main():
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": f"{a.values} SpMM / f64 dense", "data": "synthetic", "config": workload(a, cfg, n, nnz, a.values),
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                     "traffic": traffic, "kernel": "sym_spmm (k_f64_to_f32 + k_sym_spmm + k_finish_f64)",
+                     "traffic": traffic, "kernel": "sym_spmm (k_f64_to_f32 + tile or row-list SpMM kernel + k_finish_f64)",
                      "bytes_per_launch": b_spmm, "ms_per_launch": spmm_ms, "peak_kind": peak_kind},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": int(x0.nbytes / max(r2["iterations"], 1)),
