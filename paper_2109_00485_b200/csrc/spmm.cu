@@ -1307,36 +1307,37 @@ Op::~Op() {
 template <typename TV>
 static void op_build_lists(Op* op, const be_csb_view& L, DBuf<TV>& vals_out) {
     const index_t n = L.nrows, m = L.ncols, nnz = L.nnz;
-    if (nnz >= (index_t{1} << 40)) fail(BE_ERR_BAD_PARAMS, "deterministic operator too large");
+    if (nnz >= (index_t{1} << 40)) fail(BE_ERR_BAD_PARAMS, "row-list operator too large");
     std::vector<std::int64_t> pn(static_cast<std::size_t>(n) + 1, 0), pt(static_cast<std::size_t>(m) + 1, 0);
-    std::vector<std::int32_t> grow(static_cast<std::size_t>(nnz)), gcol(static_cast<std::size_t>(nnz));
-    for (index_t bi = 0; bi < L.nrowblks; ++bi)
-        for (index_t bj = 0; bj < L.ncolblks; ++bj) {
-            const index_t b = bi * L.ncolblks + bj;
-            for (index_t k = L.block_nnz_offsets[b]; k < L.block_nnz_offsets[b] + L.block_nnz[b]; ++k) {
-                grow[static_cast<std::size_t>(k)] = static_cast<std::int32_t>(L.row_offsets[bi] + L.local_rows[k]);
-                gcol[static_cast<std::size_t>(k)] = static_cast<std::int32_t>(L.col_offsets[bj] + L.local_cols[k]);
-                ++pn[static_cast<std::size_t>(grow[static_cast<std::size_t>(k)]) + 1];
-                ++pt[static_cast<std::size_t>(gcol[static_cast<std::size_t>(k)]) + 1];
+    auto each = [&](auto&& f) {  // blocks row-major, entries in stored order (the CSB storage order)
+        for (index_t bi = 0; bi < L.nrowblks; ++bi)
+            for (index_t bj = 0; bj < L.ncolblks; ++bj) {
+                const index_t b = bi * L.ncolblks + bj;
+                const index_t r0 = L.row_offsets[bi], c0 = L.col_offsets[bj];
+                for (index_t k = L.block_nnz_offsets[b]; k < L.block_nnz_offsets[b] + L.block_nnz[b]; ++k)
+                    f(k, r0 + L.local_rows[k], c0 + L.local_cols[k]);
             }
-        }
+    };
+    each([&](index_t, index_t r, index_t c) {
+        ++pn[static_cast<std::size_t>(r) + 1];
+        ++pt[static_cast<std::size_t>(c) + 1];
+    });
     for (std::size_t i = 1; i < pn.size(); ++i) pn[i] += pn[i - 1];
     for (std::size_t i = 1; i < pt.size(); ++i) pt[i] += pt[i - 1];
+    for (auto& x : pt) x += nnz;  // the L^T lists follow the L lists
     std::vector<std::int32_t> col(static_cast<std::size_t>(2 * nnz));
     std::vector<TV> val(static_cast<std::size_t>(2 * nnz));
-    std::vector<std::int64_t> cn(pn.begin(), pn.end() - 1), ct(pt.begin(), pt.end() - 1);
-    for (auto& c : ct) c += nnz;  // the L^T lists follow the L lists
-    for (index_t b = 0; b < L.nrowblks * L.ncolblks; ++b)  // blocks row-major, entries in stored order
-        for (index_t k = L.block_nnz_offsets[b]; k < L.block_nnz_offsets[b] + L.block_nnz[b]; ++k) {
-            const auto r = grow[static_cast<std::size_t>(k)], c = gcol[static_cast<std::size_t>(k)];
+    {
+        std::vector<std::int64_t> cn(pn.begin(), pn.end() - 1), ct(pt.begin(), pt.end() - 1);
+        each([&](index_t k, index_t r, index_t c) {
             const auto qn = cn[static_cast<std::size_t>(r)]++;
-            col[static_cast<std::size_t>(qn)] = c;
+            col[static_cast<std::size_t>(qn)] = static_cast<std::int32_t>(c);
             val[static_cast<std::size_t>(qn)] = static_cast<TV>(L.values[k]);
             const auto qt = ct[static_cast<std::size_t>(c)]++;
-            col[static_cast<std::size_t>(qt)] = r;
+            col[static_cast<std::size_t>(qt)] = static_cast<std::int32_t>(r);
             val[static_cast<std::size_t>(qt)] = static_cast<TV>(L.values[k]);
-        }
-    for (auto& x : pt) x += nnz;
+        });
+    }
     op->det_ptr_n.reset(n + 1);
     op->det_ptr_t.reset(m + 1);
     op->det_col.reset(std::max<index_t>(2 * nnz, 1));
