@@ -553,21 +553,30 @@ __global__ void __launch_bounds__(kThreads, 2)
 constexpr int kWsThreads = 288;  // 8 consumer warps + 1 producer warp
 constexpr std::uint32_t kWsEnd = 0xFFFFFFFFu;
 
-template <int NBP>
+template <int NBP, typename T = float>
 struct WsGeom {
-    static constexpr int RB = NBP * 4;          // bytes per X row
-    static constexpr int REP = 128 / RB;         // shifted copies per staged panel
-    static constexpr int CH = NBP / 4;           // 16-byte chunks per row
-    static constexpr int COPY = (kTile + 1) * RB;  // bytes per copy (one row of shift)
-    static constexpr int XREG = REP * COPY;      // one staged panel
-    static_assert(REP >= 1 && (REP & (REP - 1)) == 0, "nb must be 8, 16 or 32");
+    static constexpr int RB = NBP * static_cast<int>(sizeof(T));  // bytes per X row
+    static constexpr int REP = RB >= 128 ? 1 : 128 / RB;            // shifted copies per staged panel
+    static constexpr int CH = RB / 16;                              // 16-byte chunks per row
+    static constexpr int EPC = 16 / static_cast<int>(sizeof(T));    // elements per chunk
+    static constexpr int COPY = (kTile + 1) * RB;                   // bytes per copy (one row of shift)
+    static constexpr int XREG = REP * COPY;                         // one staged panel
+    static_assert(REP >= 1 && (REP & (REP - 1)) == 0 && RB % 16 == 0, "nb must be 8, 16 or 32");
 };
 
-template <int NBP>
+__device__ __forceinline__ void red_vec(float* y, const float4& a) { red_add4(y, a); }
+__device__ __forceinline__ void red_vec(double* y, const double2& a) {
+    red_add(y, a.x);
+    red_add(y + 1, a.y);
+}
+
+template <int NBP, typename T>
 __device__ __forceinline__ void ws_walk(const std::uint16_t* __restrict__ jd, int d, int hi, int rank,
-                                        const float* __restrict__ sv, const unsigned char* __restrict__ sidx,
-                                        const unsigned char* __restrict__ xreg, int slot, const int* coff, float4* acc) {
-    using G = WsGeom<NBP>;
+                                        const T* __restrict__ sv, const unsigned char* __restrict__ sidx,
+                                        const unsigned char* __restrict__ xreg, int slot, const int* coff,
+                                        typename Vec<T>::T* acc) {
+    using G = WsGeom<NBP, T>;
+    using V = typename Vec<T>::T;
     constexpr int U = G::CH <= 4 ? 4 : 2;
     auto row_ptr = [&](int idx) {  // 16-byte aligned by construction (stage, COPY and RB are multiples of 16)
         return static_cast<const unsigned char*>(
@@ -586,19 +595,19 @@ __device__ __forceinline__ void ws_walk(const std::uint16_t* __restrict__ jd, in
             pos[0] = static_cast<int>(q & 0xffffu) + rank;
             pos[1] = static_cast<int>(q >> 16) + rank;
         }
-        float v[U];
+        T v[U];
         const unsigned char* p[U];
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             v[k] = sv[pos[k]];
             p[k] = row_ptr(static_cast<int>(sidx[pos[k]]));
         }
-        float4 xv[U][G::CH];
+        V xv[U][G::CH];
 #pragma unroll
         for (int k = 0; k < U; ++k)
 #pragma unroll
             for (int i = 0; i < G::CH; ++i)
-                xv[k][i] = *static_cast<const float4*>(__builtin_assume_aligned(p[k] + coff[i], 16));
+                xv[k][i] = *static_cast<const V*>(__builtin_assume_aligned(p[k] + coff[i], 16));
 #pragma unroll
         for (int k = 0; k < U; ++k)
 #pragma unroll
@@ -606,22 +615,24 @@ __device__ __forceinline__ void ws_walk(const std::uint16_t* __restrict__ jd, in
     }
     for (; d < hi; ++d) {
         const int pos = static_cast<int>(jd[d]) + rank;
-        const float v = sv[pos];
+        const T v = sv[pos];
         const unsigned char* p = row_ptr(static_cast<int>(sidx[pos]));
-        float4 xv[G::CH];
+        V xv[G::CH];
 #pragma unroll
-        for (int i = 0; i < G::CH; ++i) xv[i] = *static_cast<const float4*>(__builtin_assume_aligned(p + coff[i], 16));
+        for (int i = 0; i < G::CH; ++i) xv[i] = *static_cast<const V*>(__builtin_assume_aligned(p + coff[i], 16));
 #pragma unroll
         for (int i = 0; i < G::CH; ++i) vfma(acc[i], v, xv[i]);
     }
 }
 
-template <int NBP, int kWsStages>
+template <int NBP, int kWsStages, typename T = float>
 __global__ void __launch_bounds__(kWsThreads, kWsStages <= 2 ? 2 : 1)
     k_sym_spmm_ws(const int2* __restrict__ runs, int nruns, const TileHdr* __restrict__ tiles,
-                  const unsigned char* __restrict__ blobs, const float* __restrict__ X, float* __restrict__ Y,
+                  const unsigned char* __restrict__ blobs, const T* __restrict__ X, T* __restrict__ Y,
                   int do_r, int do_c, int blob_max, int stage_bytes, int rot, int* __restrict__ ctr) {
-    using G = WsGeom<NBP>;
+    using G = WsGeom<NBP, T>;
+    using V = typename Vec<T>::T;
+    constexpr int TS = static_cast<int>(sizeof(T));
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) std::uint64_t full[kWsStages], empty[kWsStages], xfull[2], xempty[2];
     __shared__ TileHdr shdr[kWsStages];
@@ -681,7 +692,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsStages <= 2 ? 2 : 1)
                     sflag[s] = (i == 0 ? 1 : 0) | (i == cnt - 1 ? 2 : 0) | (xs << 2);
                     const int nnz = static_cast<int>(h.packed >> 14);
                     const int nr = static_cast<int>(h.packed & 127u) + 1, nc = static_cast<int>((h.packed >> 7) & 127u) + 1;
-                    const std::uint32_t bb = static_cast<std::uint32_t>(blob_bytes<float>(nnz));
+                    const std::uint32_t bb = static_cast<std::uint32_t>(blob_bytes<T>(nnz));
                     const std::uint32_t bytes = bb + (do_r ? G::REP * nc * G::RB : 0);
                     unsigned char* st = smem + static_cast<std::size_t>(s) * stage_bytes;
                     stream::mbar_arrive_expect_tx(&full[s], bytes);
@@ -754,23 +765,17 @@ __global__ void __launch_bounds__(kWsThreads, kWsStages <= 2 ? 2 : 1)
                 const int len = st[(pass == 0 ? kMetaRlen : kMetaClen) + rank];
                 const int hi = min(dend, len);
                 if (d < hi) {
-                    const float* sv = reinterpret_cast<const float*>(st + kMetaBytes + (pass == 0 ? 0 : npad * 5));
-                    const unsigned char* sx = st + kMetaBytes + npad * (pass == 0 ? 4 : 9);
+                    const T* sv = reinterpret_cast<const T*>(st + kMetaBytes + (pass == 0 ? 0 : npad * (TS + 1)));
+                    const unsigned char* sx = st + kMetaBytes + npad * (pass == 0 ? TS : 2 * TS + 1);
                     const unsigned char* xreg = pass == 0 ? st + blob_max : xis + xs * G::XREG;
-                    float4 acc[G::CH];
+                    V acc[G::CH];
 #pragma unroll
-                    for (int i = 0; i < G::CH; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    ws_walk<NBP>(jd, d, hi, rank, sv, sx, xreg, slot, coff, acc);
+                    for (int i = 0; i < G::CH; ++i) vzero(acc[i]);
+                    ws_walk<NBP, T>(jd, d, hi, rank, sv, sx, xreg, slot, coff, acc);
                     const int row = pass == 0 ? h.row0 + st[kMetaRperm + rank] : h.col0 + st[kMetaCperm + rank];
-                    float* y = Y + static_cast<std::int64_t>(row) * NBP;
+                    T* y = Y + static_cast<std::int64_t>(row) * NBP;
 #pragma unroll
-                    for (int i = 0; i < G::CH; ++i) {
-#ifdef BE_WS_NO_RED  // (experiment: plain stores instead of reductions -- wrong results, timing only)
-                        *reinterpret_cast<float4*>(y + ((i + lane) % G::CH) * 4) = acc[i];
-#else
-                        red_add4(y + ((i + lane) % G::CH) * 4, acc[i]);
-#endif
-                    }
+                    for (int i = 0; i < G::CH; ++i) red_vec(y + ((i + lane) % G::CH) * G::EPC, acc[i]);
                 }
             }
             ++un;
@@ -788,16 +793,16 @@ __global__ void __launch_bounds__(kWsThreads, kWsStages <= 2 ? 2 : 1)
     }
 }
 
-template <int NBP, int S>
-bool launch_ws_s(Op* op, const int2* runs, index_t nruns, const float* X, float* Y, int do_r, int do_c, cudaStream_t s) {
-    using G = WsGeom<NBP>;
+template <int NBP, int S, typename T = float>
+bool launch_ws_s(Op* op, const int2* runs, index_t nruns, const T* X, T* Y, int do_r, int do_c, cudaStream_t s) {
+    using G = WsGeom<NBP, T>;
     const int stage = ((op->blob_max + G::XREG) + 127) & ~127;
     const std::size_t sm = static_cast<std::size_t>(stage) * S + 2 * G::XREG;
     int dev = 0, optin = 0;
     BE_CUDA(cudaGetDevice(&dev));
     BE_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     if (sm + 1024 > static_cast<std::size_t>(optin)) return false;
-    auto kern = k_sym_spmm_ws<NBP, S>;
+    auto kern = k_sym_spmm_ws<NBP, S, T>;
     ensure_dyn_smem(kern, sm);
     int per_sm = 0;
     BE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWsThreads, sm));
@@ -818,15 +823,15 @@ bool launch_ws_s(Op* op, const int2* runs, index_t nruns, const float* X, float*
 
 // stages per CTA: 2 (two CTAs per SM: 16 consumer warps, measured fastest) or 3 / 4 (one CTA per
 // SM); BE_SPMM_WS_STAGES overrides (experiments)
-template <int NBP>
-bool launch_ws(Op* op, const int2* runs, index_t nruns, const float* X, float* Y, int do_r, int do_c, cudaStream_t s) {
+template <int NBP, typename T = float>
+bool launch_ws(Op* op, const int2* runs, index_t nruns, const T* X, T* Y, int do_r, int do_c, cudaStream_t s) {
     static const int stages = [] {
         const char* e = std::getenv("BE_SPMM_WS_STAGES");
         return e ? std::atoi(e) : 2;
     }();
-    if (stages == 2) return launch_ws_s<NBP, 2>(op, runs, nruns, X, Y, do_r, do_c, s);
-    if (stages == 3) return launch_ws_s<NBP, 3>(op, runs, nruns, X, Y, do_r, do_c, s);
-    return launch_ws_s<NBP, 4>(op, runs, nruns, X, Y, do_r, do_c, s);
+    if (stages == 3) return launch_ws_s<NBP, 3, T>(op, runs, nruns, X, Y, do_r, do_c, s);
+    if (stages == 4) return launch_ws_s<NBP, 4, T>(op, runs, nruns, X, Y, do_r, do_c, s);
+    return launch_ws_s<NBP, 2, T>(op, runs, nruns, X, Y, do_r, do_c, s);
 }
 
 // Deterministic symmetric SpMM (BE_OP_DETERMINISTIC): one warp per output
@@ -995,6 +1000,18 @@ void launch_tiles(Op* op, const int2* runs, index_t nruns, const TX* X, TX* Y, i
 template <typename TC, typename TV, typename TX>
 void dispatch_nb(Op* op, const int2* runs, index_t nruns, const TX* X, TX* Y, int nb, int do_r, int do_c,
                  cudaStream_t s) {
+    if constexpr (std::is_same_v<TC, double> && std::is_same_v<TV, double> && std::is_same_v<TX, double>) {
+        // f64 values and panels (the 12 B/nnz parity mode): the warp-specialised kernel for nb 8 / 16
+        static const bool ws64 = [] {
+            const char* e = std::getenv("BE_SPMM_WS");
+            return !(e && e[0] == '0');
+        }();
+        const bool aligned = (reinterpret_cast<std::uintptr_t>(X) & 15u) == 0 && (reinterpret_cast<std::uintptr_t>(Y) & 15u) == 0;
+        if (ws64 && aligned) {
+            if (nb == 16 && launch_ws<16, double>(op, runs, nruns, X, Y, do_r, do_c, s)) return;
+            if (nb == 8 && launch_ws<8, double>(op, runs, nruns, X, Y, do_r, do_c, s)) return;
+        }
+    }
     if constexpr (std::is_same_v<TC, float> && std::is_same_v<TV, float> && std::is_same_v<TX, float>) {
         // the warp-specialised kernel for the widths it covers (T1: nb = 8 4.7 vs 6.3 ms, nb = 16
         // 8.0 vs 9.4 ms, nb = 32 14.9 vs 32.5 ms against the classic kernel); BE_SPMM_WS=0 selects
