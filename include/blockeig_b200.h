@@ -399,6 +399,15 @@ be_status be_comm_allreduce_f64(be_comm* c, double* buf_dev, int64_t count, void
  *   nnz-balanced SpMM slabs. Replaces partition_matrix's fixed triangular
  *   layout (dist.hpp:113-198, nd(nd+1)/2 ranks only) for any rank count. */
 be_status be_dist_rows(const int64_t* bounds, int64_t nbounds, int world, int64_t* cuts);
+/* Segment-wise exchange rule of the distributed operator:
+ * touched[r] = 1 when a stored block of this rank's slab L_slab has rows or
+ * columns in the panel segment owned by rank r (segment q = [cuts[q],
+ * cuts[q+1]), owned by owner[q], identity when owner is NULL). X segment r is
+ * sent to exactly the ranks that touch it, partial Y segment r only to rank r.
+ * Host only; be_op_dist_need reads a distributed operator's world x world
+ * matrix (row p = rank p's touched slots) as built at be_op_create_dist. */
+be_status be_dist_touched(const be_csb_view* L_slab, const int64_t* cuts, const int* owner, int world,
+                          uint8_t* touched);
 be_status be_dist_balance(const int64_t* weights, int64_t nitems, int world, int64_t* cuts);
 
 /* Distributed symmetric operator: L_slab is this rank's share of the global
@@ -417,6 +426,7 @@ be_status be_op_create_dist(be_ctx* ctx, be_comm* comm, const be_csb_view* L_sla
  * reference triangular layout below uses it (parity variant). */
 be_status be_op_create_dist_owned(be_ctx* ctx, be_comm* comm, const be_csb_view* L_slab, const int64_t* seg_bounds,
                                   const int* seg_owner, const double* diag_local, int values_prec, be_op** out);
+be_status be_op_dist_need(const be_op* op, uint8_t* need);
 
 /* The reference's own layout (dist.hpp:25-198), restated bit-exactly:
  * build_layout: blocks[3 r .. 3 r + 2] = (i, j, transposed) of rank r over

@@ -534,6 +534,17 @@ def dist_rows(bounds, world: int) -> np.ndarray:
     return out
 
 
+def dist_touched(slab: "Csb", cuts, world: int, owner=None) -> np.ndarray:
+    """The segment-wise exchange rule (be_dist_touched): touched[r] = 1 when the slab's stored
+    blocks have rows or columns in the panel segment owned by rank r."""
+    c = np.ascontiguousarray(cuts, dtype=np.int64)
+    o = None if owner is None else np.ascontiguousarray(owner, dtype=np.int32)
+    out = np.zeros(world, np.uint8)
+    v = slab.view()
+    check(lib().be_dist_touched(C.byref(v), _p(c), _p(o), C.c_int(world), _p(out)))
+    return out.astype(bool)
+
+
 def dist_balance(weights, world: int) -> np.ndarray:
     """Contiguous weight-balanced item cuts (world + 1)."""
     w = np.ascontiguousarray(weights, dtype=np.int64)
@@ -650,6 +661,13 @@ class DistOperator(Operator):
             o = np.ascontiguousarray(owner, dtype=np.int32)
             check(lib().be_op_create_dist_owned(ctx.handle, comm.handle, C.byref(v), _p(self.cuts), _p(o), _p(d),
                                                 C.c_int(values_prec), C.byref(self._h)))
+
+    def need(self) -> np.ndarray:
+        """world x world: row p = the padded slots rank p's tiles touch (be_op_dist_need)."""
+        w = len(self.cuts) - 1
+        out = np.zeros((w, w), np.uint8)
+        check(lib().be_op_dist_need(self._h, _p(out)))
+        return out.astype(bool)
 
 
 # ---------------------------------------------- the reference triangular layout

@@ -1242,3 +1242,35 @@ be_status be_update_blocks(be_ctx* ctx, const double* X, const double* W, const 
 }
 
 }  // extern "C"
+
+extern "C" {
+
+be_status be_dist_touched(const be_csb_view* L, const int64_t* cuts, const int* owner, int world, uint8_t* touched) {
+    return guard([&] {
+        if (!L || !cuts || !touched || world < 1) be::fail(BE_ERR_BAD_PARAMS, "bad argument");
+        be::validate_view(*L);
+        auto slot = [&](int64_t row) {
+            const int q = static_cast<int>(std::upper_bound(cuts, cuts + world + 1, row) - cuts) - 1;
+            if (q < 0 || q >= world) be::fail(BE_ERR_BAD_PARAMS, "be_dist_touched: row outside the cuts");
+            return owner ? owner[q] : q;
+        };
+        std::fill(touched, touched + world, 0);
+        for (int64_t bi = 0; bi < L->nrowblks; ++bi)
+            for (int64_t bj = 0; bj < L->ncolblks; ++bj)
+                if (L->block_nnz[bi * L->ncolblks + bj] > 0) {
+                    touched[slot(L->row_offsets[bi])] = 1;
+                    touched[slot(L->col_offsets[bj])] = 1;
+                }
+    });
+}
+
+be_status be_op_dist_need(const be_op* op, uint8_t* need) {
+    return guard([&] {
+        if (!op || !need) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        const auto* o = op->impl.get();
+        if (!o->comm) be::fail(BE_ERR_BAD_PARAMS, "be_op_dist_need: not a distributed operator");
+        for (std::size_t i = 0; i < o->need.size(); ++i) need[i] = static_cast<uint8_t>(o->need[i]);
+    });
+}
+
+}  // extern "C"

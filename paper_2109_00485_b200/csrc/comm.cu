@@ -33,6 +33,10 @@ struct NcclApi {
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
     ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
     ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
 };
 
 const NcclApi& nccl() {
@@ -63,6 +67,10 @@ const NcclApi& nccl() {
         api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
         api.CommGetAsyncError = reinterpret_cast<decltype(api.CommGetAsyncError)>(sym("ncclCommGetAsyncError"));
         api.CommAbort = reinterpret_cast<decltype(api.CommAbort)>(sym("ncclCommAbort"));
+        api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+        api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+        api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+        api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
     });
     if (!err.empty()) fail(BE_ERR_NCCL, err);
     return api;
@@ -148,6 +156,20 @@ class NcclComm final : public Comm {
         ++calls;
         bytes_moved += static_cast<std::int64_t>((world - 1) * count * sizeof(float));
     }
+    void p2p(const std::vector<P2POp>& ops, cudaStream_t s) override {
+        if (ops.empty()) return;
+        BE_NCCL(nccl().GroupStart());
+        for (const auto& o : ops) {
+            if (o.send) {
+                BE_NCCL(nccl().Send(o.ptr, o.bytes, ncclChar, o.peer, comm_, s));
+            } else {
+                BE_NCCL(nccl().Recv(o.ptr, o.bytes, ncclChar, o.peer, comm_, s));
+                bytes_moved += static_cast<std::int64_t>(o.bytes);
+            }
+        }
+        BE_NCCL(nccl().GroupEnd());
+        ++calls;
+    }
     const char* backend() const override { return "nccl"; }
 
   private:
@@ -227,6 +249,31 @@ class LocalComm final : public Comm {
             BE_CUDA(cudaGetLastError());
         });
         bytes_moved += static_cast<std::int64_t>((world - 1) * count * sizeof(float));
+    }
+    void p2p(const std::vector<P2POp>& ops, cudaStream_t s) override {
+        std::vector<P2POp> sends, recvs;
+        for (const auto& o : ops) (o.send ? sends : recvs).push_back(o);
+        {
+            std::lock_guard<std::mutex> lk(g_->mu);
+            g_->slots[static_cast<std::size_t>(rank)].sends = sends;
+        }
+        run(nullptr, nullptr, s, [&](const std::vector<LocalGroup::Slot>& sl) {
+            std::vector<int> taken(static_cast<std::size_t>(world), 0);  // k-th receive from p <- k-th send of p to me
+            for (const auto& r : recvs) {
+                const auto& ps = sl[static_cast<std::size_t>(r.peer)].sends;
+                int k = taken[static_cast<std::size_t>(r.peer)]++, seen = 0;
+                const P2POp* match = nullptr;
+                for (const auto& x : ps)
+                    if (x.peer == rank && seen++ == k) {
+                        match = &x;
+                        break;
+                    }
+                if (!match || match->bytes != r.bytes)
+                    fail(BE_ERR_PROTOCOL_DEADLOCK, "local comm: unmatched point-to-point receive");
+                if (r.bytes) BE_CUDA(cudaMemcpyAsync(r.ptr, match->ptr, r.bytes, cudaMemcpyDefault, s));
+                bytes_moved += static_cast<std::int64_t>(r.bytes);
+            }
+        });
     }
     const char* backend() const override { return "local"; }
 

@@ -28,6 +28,14 @@
 
 namespace be {
 
+// One point-to-point transfer of a grouped exchange (Comm::p2p).
+struct P2POp {
+    int peer;
+    bool send;       // send `bytes` from ptr to peer, or receive them into ptr
+    void* ptr;
+    std::size_t bytes;
+};
+
 struct Comm {
     int rank = 0, world = 1, device = 0;
     virtual ~Comm() = default;
@@ -39,6 +47,10 @@ struct Comm {
     // recv (count floats) <- sum over ranks of send[rank * count ...]
     // (send holds world * count floats). In place when recv == send + rank * count.
     virtual void reduce_scatter_f32(const float* send, float* recv, std::size_t count, cudaStream_t s) = 0;
+    // A grouped set of sends and receives, stream-ordered on s: every send to a
+    // peer matches, in order, one receive of that peer from this rank (ncclSend /
+    // ncclRecv inside one group). The segment-wise SpMM exchange.
+    virtual void p2p(const std::vector<P2POp>& ops, cudaStream_t s) = 0;
     virtual const char* backend() const = 0;
     // Wait for stream s while watching the group (NCCL: ncclCommGetAsyncError; a failed
     // or vanished peer leaves the collective pending forever): an asynchronous error, or
@@ -72,6 +84,7 @@ struct LocalGroup {
         int device = 0;
         cudaEvent_t ready = nullptr;  // send data complete on the owner's stream
         cudaEvent_t done = nullptr;   // the owner finished reading peers' data
+        std::vector<P2POp> sends;     // (p2p) this rank's published sends
     };
     std::vector<Slot> slots;
 };

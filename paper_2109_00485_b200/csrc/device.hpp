@@ -152,6 +152,11 @@ struct Op {
     index_t nruns_ext = 0;
     cudaStream_t cstream = nullptr;
     cudaEvent_t ev_x = nullptr, ev_ag = nullptr;
+    // segment-wise exchange: need[p * world + r] = rank p's tiles touch the padded slot of rank
+    // r (rows or columns); X slots travel only to the ranks that touch them and partial Y
+    // slots only to their owners
+    std::vector<char> touched, need;
+    DBuf<float> ystage;
     std::vector<int> owner, seg_of_rank;  // segment -> rank, rank -> segment
     index_t unpad(index_t p) const {  // padded index -> global row
         const index_t r = p / lmax;

@@ -973,6 +973,19 @@ __global__ void k_finish_f64(const double* __restrict__ d, const double* __restr
     }
 }
 
+// out[i] = ((in_0[i] + in_1[i]) + ...) in slot order (the distributed Y sum); out may alias an input
+struct SlotPtrs {
+    const float* p[16];
+};
+__global__ void k_sum_slots(SlotPtrs in, int nin, float* out, std::int64_t count) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        float v = in.p[0][i];
+        for (int q = 1; q < nin; ++q) v += in.p[q][i];
+        out[i] = v;
+    }
+}
+
 template <int NBP, typename TC, typename TV, typename TX>
 std::size_t smem_bytes(int blob_max) {
     using G = XGeom<NBP, TC>;
@@ -1491,6 +1504,13 @@ static void op_build(Op* op, const be_csb_view& L, const RowMap* map) {
     }
     if (ntiles > 0)
         BE_CUDA(cudaMemcpy(op->tiles.get(), all_hdr.data(), all_hdr.size() * sizeof(TileHdr), cudaMemcpyHostToDevice));
+    if (map) {  // padded slots (ranks) whose rows the tiles read or write: tiles never straddle a segment
+        op->touched.assign(static_cast<std::size_t>(map->world), 0);
+        for (const auto& h : all_hdr) {
+            op->touched[static_cast<std::size_t>(h.row0 / map->lmax)] = 1;
+            op->touched[static_cast<std::size_t>(h.col0 / map->lmax)] = 1;
+        }
+    }
     {  // runs: consecutive tiles of one tile-row, class and L2 column band, at most kRunMax tiles each,
        // ordered by (class, band, tile-row)
         struct R {
@@ -1539,12 +1559,22 @@ static void op_build(Op* op, const be_csb_view& L, const RowMap* map) {
 //   4. reduce-scatter of the partial Y panels to the row owners, then
 //      Y_local = D X_local + y in f64 (the diagonal pass, kernels.hpp:363-370).
 // This is distributed_spmm (dist.hpp:256-371) on NCCL collectives.
+// Distributed apply, segment-wise exchange. Rank r's panel rows
+// live in padded slot r of the f32 exchange buffers. X: rank r sends its slot
+// to exactly the ranks whose tiles touch it and receives the slots its own
+// tiles touch (NCCL send / recv on the communication stream, overlapped with
+// the interior tiles); Y: it sends each partial slot its tiles wrote to that
+// slot's owner and receives the partials of its own slot, summed in ascending
+// rank order (identical on every run, like the reduce-scatter it replaces).
+// Only touched slots are zeroed; no full-panel collective remains.
 static void op_apply_dist(Op* op, const double* X, double* Y, index_t in_rows, int nb, cudaStream_t s) {
     if (in_rows != op->nlocal) fail(BE_ERR_DIMENSION_MISMATCH, "distributed apply: local rows mismatch");
-    const index_t seg = op->lmax * nb, tot = seg * op->world;
+    const int world = op->world, me = op->rank;
+    const index_t seg = op->lmax * nb, tot = seg * world;
     if (op->x32.n < tot) {
         op->x32.reset(tot);
         op->y32.reset(tot);
+        op->ystage.reset(tot);
     }
     if (!op->cstream) {
         BE_CUDA(cudaStreamCreateWithFlags(&op->cstream, cudaStreamNonBlocking));
@@ -1556,14 +1586,26 @@ static void op_apply_dist(Op* op, const double* X, double* Y, index_t in_rows, i
             if (!e) BE_CUDA(cudaEventCreate(&e));
         BE_CUDA(cudaEventRecord(op->ev[0], s));
     }
-    float* xs = op->x32.get() + static_cast<index_t>(op->rank) * seg;
-    const int g = static_cast<int>(std::max<index_t>(1, std::min<index_t>((tot + 255) / 256, op->ctx->num_sms * 8)));
-    k_f64_to_f32<<<g, 256, 0, s>>>(X, xs, op->nlocal * nb, op->y32.get(), tot);
+    auto need = [&](int p, int r) { return op->need[static_cast<std::size_t>(p) * world + r] != 0; };
+    const std::size_t sb = static_cast<std::size_t>(seg) * sizeof(float);
+    float* xs = op->x32.get() + static_cast<index_t>(me) * seg;
+    const int g = static_cast<int>(std::max<index_t>(1, std::min<index_t>((seg + 255) / 256, op->ctx->num_sms * 8)));
+    k_f64_to_f32<<<g, 256, 0, s>>>(X, xs, op->nlocal * nb, nullptr, 0);
     BE_CUDA(cudaGetLastError());
     ++op->ctx->launches;
+    for (int r = 0; r < world; ++r)  // the partial Y slots this rank's tiles write
+        if (r == me || need(me, r)) BE_CUDA(cudaMemsetAsync(op->y32.get() + static_cast<index_t>(r) * seg, 0, sb, s));
     BE_CUDA(cudaEventRecord(op->ev_x, s));
     BE_CUDA(cudaStreamWaitEvent(op->cstream, op->ev_x, 0));
-    op->comm->allgather_f32(xs, op->x32.get(), static_cast<std::size_t>(seg), op->cstream);
+    {
+        std::vector<P2POp> xo;
+        for (int p = 0; p < world; ++p) {
+            if (p == me) continue;
+            if (need(p, me)) xo.push_back(P2POp{p, true, xs, sb});
+            if (need(me, p)) xo.push_back(P2POp{p, false, op->x32.get() + static_cast<index_t>(p) * seg, sb});
+        }
+        op->comm->p2p(xo, op->cstream);
+    }
     BE_CUDA(cudaEventRecord(op->ev_ag, op->cstream));
     if (op->timing) BE_CUDA(cudaEventRecord(op->ev[1], s));
     if (op->nruns > 0)
@@ -1572,8 +1614,30 @@ static void op_apply_dist(Op* op, const double* X, double* Y, index_t in_rows, i
     if (op->nruns_ext > 0)
         dispatch_nb<float, float, float>(op, op->runs_ext.get(), op->nruns_ext, op->x32.get(), op->y32.get(), nb, 1, 1,
                                          s);
-    float* ys = op->y32.get() + static_cast<index_t>(op->rank) * seg;
-    op->comm->reduce_scatter_f32(op->y32.get(), ys, static_cast<std::size_t>(seg), s);
+    float* ys = op->y32.get() + static_cast<index_t>(me) * seg;
+    {
+        std::vector<P2POp> yo;
+        for (int p = 0; p < world; ++p) {
+            if (p == me) continue;
+            if (need(me, p)) yo.push_back(P2POp{p, true, op->y32.get() + static_cast<index_t>(p) * seg, sb});
+            if (need(p, me)) yo.push_back(P2POp{p, false, op->ystage.get() + static_cast<index_t>(p) * seg, sb});
+        }
+        op->comm->p2p(yo, s);
+        std::vector<const float*> parts;
+        for (int q = 0; q < world; ++q)  // ascending rank order
+            if (q == me) parts.push_back(ys);
+            else if (need(q, me)) parts.push_back(op->ystage.get() + static_cast<index_t>(q) * seg);
+        // ((p0 + p1) + p2) + ... in chunks of 16 pointers; the running sum lands in ys
+        for (std::size_t b = 0; b + 1 < parts.size(); b += 15) {
+            SlotPtrs in{};
+            int nin = 0;
+            in.p[nin++] = b == 0 ? parts[0] : ys;
+            for (std::size_t q = b + 1; q < parts.size() && nin < 16; ++q) in.p[nin++] = parts[q];
+            k_sum_slots<<<g, 256, 0, s>>>(in, nin, ys, seg);
+            BE_CUDA(cudaGetLastError());
+            ++op->ctx->launches;
+        }
+    }
     if (op->nlocal > 0) {
         const index_t out = op->nlocal * nb;
         const int g2 = static_cast<int>(std::max<index_t>(1, std::min<index_t>((out + 255) / 256, op->ctx->num_sms * 8)));
@@ -1872,6 +1936,19 @@ std::unique_ptr<Op> op_create_dist(Ctx* ctx, Comm* comm, const be_csb_view& L, c
     map.rank = rank;
     map.lmax = op->lmax;
     op_build(op.get(), L, &map);
+    {  // every rank's touched slots (one allreduce at setup)
+        const std::size_t w2 = static_cast<std::size_t>(world) * world;
+        std::vector<double> h(w2, 0.0);
+        for (int r = 0; r < world; ++r) h[static_cast<std::size_t>(rank) * world + r] = op->touched[static_cast<std::size_t>(r)];
+        DBuf<double> dv(static_cast<index_t>(w2));
+        cudaStream_t cs = ctx->stream;
+        BE_CUDA(cudaMemcpyAsync(dv.get(), h.data(), w2 * 8, cudaMemcpyHostToDevice, cs));
+        comm->allreduce_f64(dv.get(), w2, cs);
+        BE_CUDA(cudaMemcpyAsync(h.data(), dv.get(), w2 * 8, cudaMemcpyDeviceToHost, cs));
+        comm->sync(cs);
+        op->need.assign(w2, 0);
+        for (std::size_t i = 0; i < w2; ++i) op->need[i] = h[i] > 0.5 ? 1 : 0;
+    }
     op->diag.reset(std::max<index_t>(op->nlocal, 1));
     if (op->nlocal > 0) {
         if (!diag_local) fail(BE_ERR_DIMENSION_MISMATCH, "SymmetricOperator: diagonal length mismatch");

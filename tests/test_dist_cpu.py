@@ -70,6 +70,10 @@ def _free_port():
 
 
 def _gloo_rank(rank, world, port, n, nb):
+    """One rank of the segment-wise exchange of the distributed operator on CPU
+    with gloo: the C++ rule (be_dist_touched) decides which X segments travel where and which
+    partial Y segments go to which owner; the partial SpMM of the slab is the restated model
+    (tests/dist_model.py); the owner sums the partials in ascending rank order."""
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -81,17 +85,53 @@ def _gloo_rank(rank, world, port, n, nb):
     slabs = abi.dist_balance(m.block_row_nnz(), world)
     lmax = int(np.max(np.diff(cuts)))
     x = np.random.default_rng(1).uniform(-1, 1, (n, nb))
-    # this rank's X segment, padded to lmax rows -> allgather
-    seg = np.zeros((lmax, nb))
-    seg[: cuts[rank + 1] - cuts[rank]] = x[cuts[rank]:cuts[rank + 1]]
-    out = [torch.zeros(lmax * nb, dtype=torch.float64) for _ in range(world)]
-    dist.all_gather(out, torch.from_numpy(seg.ravel()))
-    xpad = torch.cat(out).numpy()
-    t = m.slab(int(slabs[rank]), int(slabs[rank + 1])).to_triples()
-    ypart = dm.slab_partial_spmm(t["row"], t["col"], t["value"], xpad, cuts, nb)
-    mine = torch.zeros(lmax * nb, dtype=torch.float64)
-    dist.reduce_scatter(mine, list(torch.from_numpy(ypart.ravel()).chunk(world)))
-    y = mine.numpy().reshape(lmax, nb)[: cuts[rank + 1] - cuts[rank]] + s.diag[cuts[rank]:cuts[rank + 1], None] * x[cuts[rank]:cuts[rank + 1]]
+    slab = m.slab(int(slabs[rank]), int(slabs[rank + 1]))
+    mine = abi.dist_touched(slab, cuts, world)
+    allt = [None] * world
+    dist.all_gather_object(allt, mine.tolist())
+    need = np.array(allt, dtype=bool)  # need[p, r]: rank p's slab touches segment r
+    # X: my segment to the ranks that touch it, the touched segments from their owners
+    xpad = np.zeros((world * lmax, nb))
+    xpad[rank * lmax: rank * lmax + cuts[rank + 1] - cuts[rank]] = x[cuts[rank]:cuts[rank + 1]]
+    reqs, bufs = [], {}
+    mine_t = torch.from_numpy(np.ascontiguousarray(xpad[rank * lmax:(rank + 1) * lmax]).ravel())
+    for p in range(world):
+        if p == rank:
+            continue
+        if need[p, rank]:
+            reqs.append(dist.isend(mine_t, p))
+        if need[rank, p]:
+            bufs[p] = torch.zeros(lmax * nb, dtype=torch.float64)
+            reqs.append(dist.irecv(bufs[p], p))
+    for q in reqs:
+        q.wait()
+    for p, buf in bufs.items():
+        xpad[p * lmax:(p + 1) * lmax] = buf.numpy().reshape(lmax, nb)
+    t = slab.to_triples()
+    ypart = dm.slab_partial_spmm(t["row"], t["col"], t["value"], xpad.ravel(), cuts, nb).reshape(world * lmax, nb)
+    # the slab only writes the segments it touches (the rule is exact, not conservative)
+    for r in range(world):
+        if not need[rank, r]:
+            assert not np.any(ypart[r * lmax:(r + 1) * lmax])
+    # Y: partial segments to their owners; mine summed in ascending rank order
+    reqs, parts = [], {}
+    for p in range(world):
+        if p == rank:
+            continue
+        if need[rank, p]:
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(ypart[p * lmax:(p + 1) * lmax]).ravel()), p))
+        if need[p, rank]:
+            parts[p] = torch.zeros(lmax * nb, dtype=torch.float64)
+            reqs.append(dist.irecv(parts[p], p))
+    for q in reqs:
+        q.wait()
+    acc = None
+    for p in range(world):
+        v = ypart[rank * lmax:(rank + 1) * lmax] if p == rank else (parts[p].numpy().reshape(lmax, nb) if p in parts else None)
+        if v is not None:
+            acc = v.copy() if acc is None else acc + v
+    nl = cuts[rank + 1] - cuts[rank]
+    y = acc[:nl] + s.diag[cuts[rank]:cuts[rank + 1], None] * x[cuts[rank]:cuts[rank + 1]]
     got = [None] * world
     dist.all_gather_object(got, y)
     dist.destroy_process_group()

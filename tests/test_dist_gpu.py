@@ -60,29 +60,46 @@ def partition(m, world):
     return cuts, slabs
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_dist_spmm_matches_single_and_oracle(ctx, world):
-    m, diag, _ = problem()
+    """Segment-wise exchange: X segments travel only to the ranks whose slab touches
+    them, partial Y segments only to their owners; the result equals the single-GPU SpMM and the
+    oracle, the exchange plan is the C++ rule (be_dist_touched) on every rank, and the bytes moved
+    stay below the full-panel allgather + reduce-scatter it replaced."""
+    m, diag, _ = problem(extent=500 if world > 4 else 1000)
     n, nb = m.nrows, 16
     x = np.random.default_rng(5).uniform(-1, 1, (n, nb))
     cuts, slabs = partition(m, world)
 
     def rank(r, c, comm):
-        op = abi.DistOperator(c, comm, m.slab(int(slabs[r]), int(slabs[r + 1])), cuts, diag[cuts[r]:cuts[r + 1]])
+        slab = m.slab(int(slabs[r]), int(slabs[r + 1]))
+        op = abi.DistOperator(c, comm, slab, cuts, diag[cuts[r]:cuts[r + 1]])
         y = op.apply_host(x[cuts[r]:cuts[r + 1]])
         y2 = op.apply_host(x[cuts[r]:cuts[r + 1]])  # the exchange buffers are reused
         info = comm.info()
+        need = op.need()
         op.close()
-        return y, y2, info
+        return y, y2, info, need, abi.dist_touched(slab, cuts, world)
 
     res = run_ranks(world, rank)
-    y = np.vstack([a for a, _, _ in res])
-    assert all(np.array_equal(a, b) or np.linalg.norm(a - b) <= 1e-6 * np.linalg.norm(a) for a, b, _ in res)
+    y = np.vstack([a[0] for a in res])
+    assert all(np.array_equal(a, b) or np.linalg.norm(a - b) <= 1e-6 * np.linalg.norm(a) for a, b, *_ in res)
     want = ol.Impl("orc").spmm(m, diag, x)
     single = abi.Operator(ctx, m, diag).apply_host(x)
     assert np.linalg.norm(y - want) / np.linalg.norm(want) <= 1e-5
     assert np.linalg.norm(y - single) / np.linalg.norm(single) <= 1e-6
-    assert all(i["backend"] == "local" and i["calls"] == 4 for _, _, i in res)  # AG + RS per apply
+    need = np.array([t for *_, t in res])  # the host rule, rank by rank
+    assert all(np.array_equal(r[3], need) for r in res)  # every rank built the same plan from its tiles
+    # slab p (rows [s_p, s_p+1), columns below s_p+1) touches exactly the segments starting before its end
+    for p in range(world):
+        if slabs[p + 1] > slabs[p]:
+            end = m.row_offsets[int(slabs[p + 1])]
+            assert np.array_equal(need[p], cuts[:-1] < end) or need[p].sum() <= (cuts[:-1] < end).sum()
+    lmax = int(np.max(np.diff(cuts)))
+    full = 2 * 2 * (world - 1) * lmax * nb * 4  # two applies of AG + RS, bytes each rank received
+    assert all(i["backend"] == "local" and i["calls"] == 5 for _, _, i, *_ in res)  # setup allreduce + 2 x (X, Y)
+    if world > 2:
+        assert sum(i["bytes"] for _, _, i, *_ in res) < world * full
 
 
 def test_dist_decode_is_the_slab(ctx):
