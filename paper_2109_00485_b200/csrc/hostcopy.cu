@@ -1,11 +1,15 @@
-// Large host <-> device copies of caller-owned (pageable) buffers: the
-// caller's bytes go through two pinned staging chunks; host threads move
-// each chunk between the caller's pages and the staging buffer while the copy
-// engine moves the other chunk. The driver's own pageable path does the same
-// with one thread (~5 GB/s on the B200 hosts); here the host side runs on up
-// to 8 threads.
+// Large host <-> device copies of caller-owned (pageable) buffers: a
+// persistent pool of host worker threads, each running its own pipeline over
+// one contiguous slice of the transfer -- host memcpy between the caller's
+// pages and the worker's two pinned staging chunks, DMA on the worker's own
+// stream -- so the host-side memcpy of every worker and all copy engines run
+// concurrently. The driver's own pageable path does the same with one thread
+// (~5 GB/s on the B200 hosts); the round-1 version spawned threads per chunk
+// and kept one pipeline (16 GB/s).
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -15,49 +19,98 @@
 namespace be {
 namespace {
 
-constexpr std::size_t kChunk = 16u << 20;  // bytes per staging chunk
+constexpr std::size_t kChunk = 8u << 20;   // bytes per staging chunk
 constexpr std::size_t kDirect = 8u << 20;  // below this the driver's path is as good
+constexpr std::size_t kMinSlice = 4u << 20;
 
-struct Staging {
-    std::mutex mu;
+struct Worker {
     void* buf[2] = {nullptr, nullptr};
     cudaEvent_t ev[2] = {nullptr, nullptr};
-    int device = -1;
+    cudaEvent_t done = nullptr;
+    cudaStream_t stream = nullptr;
+    bool used[2] = {false, false};
 };
 
-Staging& staging() {
-    static Staging st;  // process-wide, allocated on first use, never freed
-    return st;
+// The pool: workers sleep on a condition variable; run() hands every worker a
+// job index and returns when all finished. One transfer at a time (the mutex
+// of copy()).
+class Pool {
+  public:
+    static Pool& get() {
+        // process-wide, created on first use and never destroyed: the detached workers stay
+        // parked on a live condition variable until the process exits (a static object's
+        // destructor would tear the mutex down under them and hang the exit)
+        static Pool* p = new Pool();
+        return *p;
+    }
+    int size() const { return static_cast<int>(threads_.size()); }
+    void run(const std::function<void(int)>& job) {
+        std::unique_lock<std::mutex> lk(mu_);
+        job_ = &job;
+        pending_ = size();
+        ++gen_;
+        cv_.notify_all();
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+    std::mutex copy_mu;  // serialises transfers (the workers' staging buffers are shared)
+    std::vector<Worker> workers;
+    int device = -1;
+
+  private:
+    Pool() {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const int n = static_cast<int>(std::min(16u, hw));
+        workers.resize(static_cast<std::size_t>(n));
+        for (int i = 0; i < n; ++i) threads_.emplace_back([this, i] { loop(i); });
+        for (auto& t : threads_) t.detach();
+    }
+    void loop(int i) {
+        std::uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(int)>* job = nullptr;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                job = job_;
+            }
+            if (job) (*job)(i);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_cv_.notify_all();
+        }
+    }
+    std::vector<std::thread> threads_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int)>* job_ = nullptr;
+    int pending_ = 0;
+    std::uint64_t gen_ = 0;
+};
+
+void ensure(Pool& p, int device) {
+    if (p.device == device) return;
+    for (auto& w : p.workers) {
+        if (w.buf[0]) {  // streams / events belong to another device: recreate them here
+            for (auto& e : w.ev) cudaEventDestroy(e);
+            for (auto& b : w.buf) cudaFreeHost(b);
+            cudaEventDestroy(w.done);
+            cudaStreamDestroy(w.stream);
+        }
+        for (auto& b : w.buf) BE_CUDA(cudaHostAlloc(&b, kChunk, cudaHostAllocPortable));
+        for (auto& e : w.ev) BE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        BE_CUDA(cudaEventCreateWithFlags(&w.done, cudaEventDisableTiming));
+        BE_CUDA(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
+        w.used[0] = w.used[1] = false;
+    }
+    p.device = device;
 }
 
-void ensure(Staging& st, int device) {
-    if (st.buf[0] && st.device == device) return;
-    if (st.buf[0]) {  // events belong to another device: recreate them there
-        for (auto& e : st.ev) cudaEventDestroy(e);
-        for (auto& b : st.buf) cudaFreeHost(b);
-    }
-    for (auto& b : st.buf) BE_CUDA(cudaHostAlloc(&b, kChunk, cudaHostAllocPortable));
-    for (auto& e : st.ev) BE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    st.device = device;
-}
-
-// dst[0, n) = src[0, n) on up to `nt` threads
-void par_memcpy(void* dst, const void* src, std::size_t n) {
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const std::size_t nt = std::min<std::size_t>({8, hw, std::max<std::size_t>(1, n >> 20)});
-    if (nt <= 1) {
-        std::memcpy(dst, src, n);
-        return;
-    }
-    std::vector<std::thread> th;
-    const std::size_t per = (n + nt - 1) / nt;
-    for (std::size_t t = 1; t < nt; ++t) {
-        const std::size_t b = t * per, e = std::min(n, b + per);
-        if (b < e)
-            th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b); });
-    }
-    std::memcpy(dst, src, std::min(n, per));
-    for (auto& x : th) x.join();
+// worker slices: contiguous, 64-byte aligned boundaries
+void slice(std::size_t bytes, int nw, int i, std::size_t& b, std::size_t& e) {
+    const std::size_t per = ((bytes + static_cast<std::size_t>(nw) - 1) / nw + 63) & ~std::size_t{63};
+    b = std::min(bytes, per * static_cast<std::size_t>(i));
+    e = std::min(bytes, b + per);
 }
 
 }  // namespace
@@ -69,21 +122,32 @@ void h2d_large(void* dst, const void* src, std::size_t bytes, cudaStream_t s) {
     }
     int dev = 0;
     BE_CUDA(cudaGetDevice(&dev));
-    auto& st = staging();
-    std::lock_guard<std::mutex> lk(st.mu);
-    ensure(st, dev);
-    bool used[2] = {false, false};
-    for (std::size_t off = 0, c = 0; off < bytes; off += kChunk, ++c) {
-        const int b = static_cast<int>(c & 1);
-        const std::size_t len = std::min(kChunk, bytes - off);
-        if (used[b]) BE_CUDA(cudaEventSynchronize(st.ev[b]));  // its previous DMA is done
-        par_memcpy(st.buf[b], static_cast<const char*>(src) + off, len);
-        BE_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, st.buf[b], len, cudaMemcpyHostToDevice, s));
-        BE_CUDA(cudaEventRecord(st.ev[b], s));
-        used[b] = true;
-    }
-    for (int b = 0; b < 2; ++b)  // the staging buffers are free again when this returns
-        if (used[b]) BE_CUDA(cudaEventSynchronize(st.ev[b]));
+    auto& p = Pool::get();
+    std::lock_guard<std::mutex> lk(p.copy_mu);
+    ensure(p, dev);
+    const int nw = static_cast<int>(std::clamp<std::size_t>(bytes / kMinSlice, 1, p.workers.size()));
+    std::vector<cudaError_t> err(static_cast<std::size_t>(nw), cudaSuccess);
+    p.run([&](int i) {
+        if (i >= nw) return;
+        auto& w = p.workers[static_cast<std::size_t>(i)];
+        cudaError_t e = cudaSetDevice(dev);
+        std::size_t b0, e0;
+        slice(bytes, nw, i, b0, e0);
+        for (std::size_t off = b0, c = 0; off < e0 && e == cudaSuccess; off += kChunk, ++c) {
+            const int k = static_cast<int>(c & 1);
+            const std::size_t len = std::min(kChunk, e0 - off);
+            if (w.used[k]) e = cudaEventSynchronize(w.ev[k]);  // its previous DMA is done
+            if (e != cudaSuccess) break;
+            std::memcpy(w.buf[k], static_cast<const char*>(src) + off, len);
+            e = cudaMemcpyAsync(static_cast<char*>(dst) + off, w.buf[k], len, cudaMemcpyHostToDevice, w.stream);
+            if (e == cudaSuccess) e = cudaEventRecord(w.ev[k], w.stream);
+            w.used[k] = true;
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(w.done, w.stream);
+        err[static_cast<std::size_t>(i)] = e;
+    });
+    for (auto e : err) BE_CUDA(e);
+    for (int i = 0; i < nw; ++i) BE_CUDA(cudaStreamWaitEvent(s, p.workers[static_cast<std::size_t>(i)].done, 0));
 }
 
 void d2h_large(void* dst, const void* src, std::size_t bytes, cudaStream_t s) {
@@ -94,24 +158,43 @@ void d2h_large(void* dst, const void* src, std::size_t bytes, cudaStream_t s) {
     }
     int dev = 0;
     BE_CUDA(cudaGetDevice(&dev));
-    auto& st = staging();
-    std::lock_guard<std::mutex> lk(st.mu);
-    ensure(st, dev);
-    const std::size_t nchunk = (bytes + kChunk - 1) / kChunk;
-    auto issue = [&](std::size_t c) {
-        const int b = static_cast<int>(c & 1);
-        const std::size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
-        BE_CUDA(cudaMemcpyAsync(st.buf[b], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, s));
-        BE_CUDA(cudaEventRecord(st.ev[b], s));
-    };
-    issue(0);
-    for (std::size_t c = 0; c < nchunk; ++c) {
-        const int b = static_cast<int>(c & 1);
-        BE_CUDA(cudaEventSynchronize(st.ev[b]));
-        if (c + 1 < nchunk) issue(c + 1);  // the other buffer was drained in the previous round
-        const std::size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
-        par_memcpy(static_cast<char*>(dst) + off, st.buf[b], len);
-    }
+    auto& p = Pool::get();
+    std::lock_guard<std::mutex> lk(p.copy_mu);
+    ensure(p, dev);
+    cudaEvent_t ready = nullptr;  // the producer of src on s is done
+    BE_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    BE_CUDA(cudaEventRecord(ready, s));
+    const int nw = static_cast<int>(std::clamp<std::size_t>(bytes / kMinSlice, 1, p.workers.size()));
+    std::vector<cudaError_t> err(static_cast<std::size_t>(nw), cudaSuccess);
+    p.run([&](int i) {
+        if (i >= nw) return;
+        auto& w = p.workers[static_cast<std::size_t>(i)];
+        cudaError_t e = cudaSetDevice(dev);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(w.stream, ready, 0);
+        std::size_t b0, e0;
+        slice(bytes, nw, i, b0, e0);
+        const std::size_t nch = (e0 - b0 + kChunk - 1) / kChunk;
+        auto issue = [&](std::size_t c) {
+            const int k = static_cast<int>(c & 1);
+            const std::size_t off = b0 + c * kChunk, len = std::min(kChunk, e0 - off);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(w.buf[k], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, w.stream);
+            if (e == cudaSuccess) e = cudaEventRecord(w.ev[k], w.stream);
+            w.used[k] = true;
+        };
+        if (nch > 0) issue(0);
+        for (std::size_t c = 0; c < nch && e == cudaSuccess; ++c) {
+            const int k = static_cast<int>(c & 1);
+            e = cudaEventSynchronize(w.ev[k]);
+            if (e != cudaSuccess) break;
+            if (c + 1 < nch) issue(c + 1);  // the other buffer was drained in the previous round
+            const std::size_t off = b0 + c * kChunk, len = std::min(kChunk, e0 - off);
+            std::memcpy(static_cast<char*>(dst) + off, w.buf[k], len);
+        }
+        err[static_cast<std::size_t>(i)] = e;
+    });
+    cudaEventDestroy(ready);
+    for (auto e : err) BE_CUDA(e);
 }
 
 }  // namespace be
