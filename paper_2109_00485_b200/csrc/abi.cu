@@ -324,6 +324,7 @@ be_status be_ctx_create(int device, be_ctx** out) {
         if (prop.major < 10) be::fail(BE_ERR_NO_DEVICE, "blockeig_b200 needs an sm_100 (B200) device");
         c->num_sms = prop.multiProcessorCount;
         BE_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        be::hostcopy_prepare(device);  // pinned staging for the host-buffer calls, allocated once
         *out = new be_ctx{std::move(c)};
     });
 }

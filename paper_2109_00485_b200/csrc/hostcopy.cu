@@ -19,7 +19,7 @@
 namespace be {
 namespace {
 
-constexpr std::size_t kChunk = 8u << 20;   // bytes per staging chunk
+constexpr std::size_t kChunk = 4u << 20;   // bytes per staging chunk (x2 per worker: 128 MB pinned for 16 workers)
 constexpr std::size_t kDirect = 8u << 20;  // below this the driver's path is as good
 constexpr std::size_t kMinSlice = 4u << 20;
 
@@ -114,6 +114,12 @@ void slice(std::size_t bytes, int nw, int i, std::size_t& b, std::size_t& e) {
 }
 
 }  // namespace
+
+void hostcopy_prepare(int device) {
+    auto& p = Pool::get();
+    std::lock_guard<std::mutex> lk(p.copy_mu);
+    ensure(p, device);
+}
 
 void h2d_large(void* dst, const void* src, std::size_t bytes, cudaStream_t s) {
     if (bytes < kDirect) {
