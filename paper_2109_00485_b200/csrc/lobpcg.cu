@@ -20,6 +20,8 @@
 #include <cstring>
 #include <random>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "comm.hpp"
 #include "densela.cuh"
 #include "hostcopy.hpp"
@@ -55,6 +57,22 @@ struct Keep {
     void* hm = nullptr;  // pinned Solver::Mirror
     ~Keep() {
         if (hm) cudaFreeHost(hm);
+    }
+};
+
+// NVTX ranges of the iteration phases (the same boundaries as the CUDA events
+// of BE_TRACE_SEGMENTS): visible in nsys / Nsight next to the kernels, free
+// without an attached tool (NVTX v3 is header-only).
+struct NvtxPhases {
+    bool open = false;
+    void to(const char* name) {
+        if (open) nvtxRangePop();
+        nvtxRangePushA(name);
+        open = true;
+    }
+    void end() {
+        if (open) nvtxRangePop();
+        open = false;
     }
 };
 
@@ -313,6 +331,7 @@ struct Solver {
     bool p_active = false, converged = false;
     int iter = 0;
     Events ev;
+    NvtxPhases nv;
 
     void init(const double* x0) {
         if (x0)
@@ -358,6 +377,7 @@ struct Solver {
     // W restart deferred, see iterate) and the host synchronises once, at the
     // end, to read the status, the Ritz values and the residual norms.
     void iteration_body(bool w_restart) {
+        nv.to("precond");
         BE_CUDA(cudaEventRecord(ev.e[0], s));
         if (!w_restart) {
             if (tiles) {  // W = K^{-1} R, shifts theta[min(v, k-1)] (lobpcg.hpp:344-350)
@@ -370,6 +390,7 @@ struct Solver {
                 BE_CUDA(cudaMemcpyAsync(W.get(), R.get(), static_cast<std::size_t>(n * nb) * 8, cudaMemcpyDeviceToDevice, s));
             }
         }
+        nv.to("w-hygiene");
         BE_CUDA(cudaEventRecord(ev.e[1], s));
         // W hygiene (lobpcg.hpp:358-373)
         if (w_restart) {  // the first qr_of_transpose of W gave up: a random W (lobpcg.hpp:360-363)
@@ -388,8 +409,10 @@ struct Solver {
         project_out(W.get(), X.get());
         if (p_active) project_out(W.get(), P.get());
         qr(W.get(), false);  // RankDeficient swallowed: W keeps the completed passes
+        nv.to("spmm");
         BE_CUDA(cudaEventRecord(ev.e[2], s));
         apply_op(W.get(), HW.get());
+        nv.to("rayleigh-ritz");
         BE_CUDA(cudaEventRecord(ev.e[3], s));
         // Rayleigh-Ritz with the drop-P retry (lobpcg.hpp:380-396)
         dropped_host = false;
@@ -398,6 +421,7 @@ struct Solver {
             dropped_host = true;
             if (!rayleigh_ritz(false)) fail(BE_ERR_BREAKDOWN_UNRECOVERABLE, "lobpcg_solve: basis repair failed twice");
         }
+        nv.to("update");
         BE_CUDA(cudaEventRecord(ev.e[5], s));
         // fused: C keeps the 3-block layout and its P rows are zero after a device-side drop
         const bool with_p = p_active && !dropped_host;
@@ -424,6 +448,7 @@ struct Solver {
             std::swap(P, Pn);
             std::swap(HP, HPn);
         }
+        nv.to("p-hygiene");
         BE_CUDA(cudaEventRecord(ev.e[6], s));
         {  // P hygiene (lobpcg.hpp:412-417) + orthonormalize_pair (:254-270)
             gram1(X.get(), P.get(), 0, xtp);
@@ -437,6 +462,7 @@ struct Solver {
             dla::chol_floored(ctx, Bp, Rp, nb, 1e-8, st.get(), s);
             dla::trsm(ctx, P.get(), HP.get(), Rp, nb, n, st.get(), 0, 1, s);
         }
+        nv.to("residual");
         BE_CUDA(cudaEventRecord(ev.e[7], s));
         dla::residual(ctx, HX.get(), X.get(), theta, R.get(), nb, n, partials.get(), rn2, xn2, s);
         allreduce(rn2, 2 * nb);
@@ -444,6 +470,7 @@ struct Solver {
         BE_CUDA(cudaMemcpyAsync(hm->rn2, rn2, nb * 8, cudaMemcpyDeviceToHost, s));
         BE_CUDA(cudaMemcpyAsync(hm->xn2, xn2, nb * 8, cudaMemcpyDeviceToHost, s));
         BE_CUDA(cudaEventRecord(ev.e[4], s));
+        nv.end();
         sync_status();
     }
     bool dropped_host = false;

@@ -52,6 +52,8 @@
 #include <mutex>
 #include <numeric>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "comm.hpp"
 #include "device.hpp"
 #include "stream.cuh"
@@ -1604,7 +1606,9 @@ static void op_apply_dist(Op* op, const double* X, double* Y, index_t in_rows, i
             if (need(p, me)) xo.push_back(P2POp{p, true, xs, sb});
             if (need(me, p)) xo.push_back(P2POp{p, false, op->x32.get() + static_cast<index_t>(p) * seg, sb});
         }
+        nvtxRangePushA("x-exchange");
         op->comm->p2p(xo, op->cstream);
+        nvtxRangePop();
     }
     BE_CUDA(cudaEventRecord(op->ev_ag, op->cstream));
     if (op->timing) BE_CUDA(cudaEventRecord(op->ev[1], s));
@@ -1622,7 +1626,9 @@ static void op_apply_dist(Op* op, const double* X, double* Y, index_t in_rows, i
             if (need(me, p)) yo.push_back(P2POp{p, true, op->y32.get() + static_cast<index_t>(p) * seg, sb});
             if (need(p, me)) yo.push_back(P2POp{p, false, op->ystage.get() + static_cast<index_t>(p) * seg, sb});
         }
+        nvtxRangePushA("y-exchange");
         op->comm->p2p(yo, s);
+        nvtxRangePop();
         std::vector<const float*> parts;
         for (int q = 0; q < world; ++q)  // ascending rank order
             if (q == me) parts.push_back(ys);
