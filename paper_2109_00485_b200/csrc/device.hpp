@@ -150,6 +150,11 @@ struct Op {
     std::vector<index_t> cuts;
     DBuf<int2> runs_ext;
     index_t nruns_ext = 0;
+    // runs_ext grouped by column segment (segment order): group q = [ext_group[q], ext_group[q+1]).
+    // In a lower triangle every tile writing segment q (as column or as row) sits in a group <= q,
+    // so segment q's partial Y is final once groups 0..q ran (the overlapped Y exchange).
+    std::vector<index_t> ext_group;
+    std::vector<cudaEvent_t> ev_grp;
     cudaStream_t cstream = nullptr;
     cudaEvent_t ev_x = nullptr, ev_ag = nullptr;
     // segment-wise exchange: need[p * world + r] = rank p's tiles touch the padded slot of rank

@@ -1328,6 +1328,8 @@ Op::~Op() {
         if (e) cudaEventDestroy(e);
     if (ev_x) cudaEventDestroy(ev_x);
     if (ev_ag) cudaEventDestroy(ev_ag);
+    for (auto& e : ev_grp)
+        if (e) cudaEventDestroy(e);
     if (cstream) cudaStreamDestroy(cstream);
 }
 
@@ -1519,27 +1521,46 @@ static void op_build(Op* op, const be_csb_view& L, const RowMap* map) {
             int cls;
             index_t band;
             int b, e;
+            int seg;
         };
         std::vector<R> all;
         index_t band_rows = BE_SPMM_BAND_ROWS;
         if (const char* e = std::getenv("BE_SPMM_BAND_ROWS")) band_rows = std::atoll(e);  // (experiments)
         band_rows = std::max<index_t>(kTile, band_rows);
+        // distributed operator: the column segment of a tile (segment order; the padded slot is its owner)
+        auto colseg = [&](const TileHdr& h) -> int {
+            if (!map) return 0;
+            const int slot = static_cast<int>(h.col0 / map->lmax);
+            for (int q = 0; q < map->world; ++q)
+                if (map->owner[q] == slot) return q;
+            return 0;
+        };
         for (index_t t = 0; t < ntiles;) {
             const auto& h0 = all_hdr[static_cast<std::size_t>(t)];
             const unsigned char c0 = all_cls[static_cast<std::size_t>(t)];
             const index_t band = h0.col0 / band_rows;
+            const int q0 = colseg(h0);
             index_t e = t + 1;
             while (e < ntiles && e - t < kRunMax && all_hdr[static_cast<std::size_t>(e)].row0 == h0.row0 &&
-                   all_cls[static_cast<std::size_t>(e)] == c0 && all_hdr[static_cast<std::size_t>(e)].col0 / band_rows == band)
+                   all_cls[static_cast<std::size_t>(e)] == c0 && all_hdr[static_cast<std::size_t>(e)].col0 / band_rows == band &&
+                   colseg(all_hdr[static_cast<std::size_t>(e)]) == q0)
                 ++e;
-            all.push_back(R{c0, band, static_cast<int>(t), static_cast<int>(e)});
+            all.push_back(R{c0, band, static_cast<int>(t), static_cast<int>(e), q0});
             t = e;
         }
         std::stable_sort(all.begin(), all.end(), [](const R& a, const R& b) {
-            return a.cls != b.cls ? a.cls < b.cls : a.band < b.band;
+            if (a.cls != b.cls) return a.cls < b.cls;
+            if (a.seg != b.seg) return a.seg < b.seg;
+            return a.band < b.band;
         });
         std::vector<int2> runs[2];
         for (const auto& x : all) runs[x.cls].push_back(make_int2(x.b, x.e));
+        if (map) {  // exterior groups by column segment
+            op->ext_group.assign(static_cast<std::size_t>(map->world) + 1, 0);
+            for (const auto& x : all)
+                if (x.cls == 1) ++op->ext_group[static_cast<std::size_t>(x.seg) + 1];
+            for (std::size_t q = 1; q < op->ext_group.size(); ++q) op->ext_group[q] += op->ext_group[q - 1];
+        }
         op->nruns = static_cast<index_t>(runs[0].size());
         op->runs.reset(std::max<index_t>(op->nruns, 1));
         if (!runs[0].empty())
@@ -1565,10 +1586,11 @@ static void op_build(Op* op, const be_csb_view& L, const RowMap* map) {
 // live in padded slot r of the f32 exchange buffers. X: rank r sends its slot
 // to exactly the ranks whose tiles touch it and receives the slots its own
 // tiles touch (NCCL send / recv on the communication stream, overlapped with
-// the interior tiles); Y: it sends each partial slot its tiles wrote to that
-// slot's owner and receives the partials of its own slot, summed in ascending
-// rank order (identical on every run, like the reduce-scatter it replaces).
-// Only touched slots are zeroed; no full-panel collective remains.
+// the interior tiles); Y: segment by segment, as soon as the tiles writing a
+// segment have run, the ranks that wrote it send their partial to its owner
+// (overlapped with the next segments' tiles), and the owner sums the partials
+// of its slot in ascending rank order (identical on every run). Only touched
+// slots are zeroed; no full-panel collective remains.
 static void op_apply_dist(Op* op, const double* X, double* Y, index_t in_rows, int nb, cudaStream_t s) {
     if (in_rows != op->nlocal) fail(BE_ERR_DIMENSION_MISMATCH, "distributed apply: local rows mismatch");
     const int world = op->world, me = op->rank;
@@ -1615,20 +1637,38 @@ static void op_apply_dist(Op* op, const double* X, double* Y, index_t in_rows, i
     if (op->nruns > 0)
         dispatch_nb<float, float, float>(op, op->runs.get(), op->nruns, op->x32.get(), op->y32.get(), nb, 1, 1, s);
     BE_CUDA(cudaStreamWaitEvent(s, op->ev_ag, 0));
-    if (op->nruns_ext > 0)
-        dispatch_nb<float, float, float>(op, op->runs_ext.get(), op->nruns_ext, op->x32.get(), op->y32.get(), nb, 1, 1,
-                                         s);
     float* ys = op->y32.get() + static_cast<index_t>(me) * seg;
-    {
-        std::vector<P2POp> yo;
-        for (int p = 0; p < world; ++p) {
-            if (p == me) continue;
-            if (need(me, p)) yo.push_back(P2POp{p, true, op->y32.get() + static_cast<index_t>(p) * seg, sb});
-            if (need(p, me)) yo.push_back(P2POp{p, false, op->ystage.get() + static_cast<index_t>(p) * seg, sb});
+    // Exterior tiles segment by segment; once groups 0..q ran, segment q's partial Y is final and its
+    // exchange (call q: every rank that wrote it sends it to the owner, the owner receives) runs on the
+    // communication stream while the next groups compute. One call per segment on every rank keeps
+    // the calls matched.
+    if (op->ev_grp.size() < static_cast<std::size_t>(world)) {
+        for (int q = static_cast<int>(op->ev_grp.size()); q < world; ++q) {
+            cudaEvent_t e = nullptr;
+            BE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            op->ev_grp.push_back(e);
         }
+    }
+    for (int q = 0; q < world; ++q) {
+        const index_t g0 = op->ext_group[static_cast<std::size_t>(q)], g1 = op->ext_group[static_cast<std::size_t>(q) + 1];
+        if (g1 > g0)
+            dispatch_nb<float, float, float>(op, op->runs_ext.get() + g0, g1 - g0, op->x32.get(), op->y32.get(), nb, 1, 1, s);
+        BE_CUDA(cudaEventRecord(op->ev_grp[static_cast<std::size_t>(q)], s));
+        BE_CUDA(cudaStreamWaitEvent(op->cstream, op->ev_grp[static_cast<std::size_t>(q)], 0));
+        const int o = op->owner[static_cast<std::size_t>(q)];
+        std::vector<P2POp> yo;
+        if (o != me && need(me, o)) yo.push_back(P2POp{o, true, op->y32.get() + static_cast<index_t>(o) * seg, sb});
+        if (o == me)
+            for (int p = 0; p < world; ++p)
+                if (p != me && need(p, me))
+                    yo.push_back(P2POp{p, false, op->ystage.get() + static_cast<index_t>(p) * seg, sb});
         nvtxRangePushA("y-exchange");
-        op->comm->p2p(yo, s);
+        op->comm->p2p(yo, op->cstream);
         nvtxRangePop();
+    }
+    BE_CUDA(cudaEventRecord(op->ev_ag, op->cstream));
+    BE_CUDA(cudaStreamWaitEvent(s, op->ev_ag, 0));
+    {
         std::vector<const float*> parts;
         for (int q = 0; q < world; ++q)  // ascending rank order
             if (q == me) parts.push_back(ys);
