@@ -173,10 +173,8 @@ def test_dist_lobpcg_matches_single(ctx, world, precond):
         from test_lobpcg_gpu import envelope
         lo, hi = envelope(m, diag, toff, k=k, nb=nb, tol=1e-6, maxiter=300, seed=1)
         lo, hi = min(lo, single["iterations"]), max(hi, single["iterations"])
-        # the distributed reduction order is yet another order (atomics + the rank split): measured
-        # spread up to ~2 iterations beyond the sampled envelope on a 36-38 envelope
-        slack = max(2, int(0.1 * hi))
-        assert lo - slack <= its <= hi + slack, (its, lo, hi)
+        # (the envelope samples the reference over ThreadPool(1..8) x {baseline, fused-atomic})
+        assert lo - 1 <= its <= hi + 1, (its, lo, hi)
     # the distributed eigenvectors are the single-GPU ones, row-partitioned
     x = np.vstack([r["x"] for r in res])
     for v in range(k):
@@ -276,9 +274,12 @@ def test_weak_scaling_glue_matches_whole_matrix(ctx, world):
     res = run_ranks(world, rank)
     assert single["converged"] and res[0]["converged"]
     assert np.max(np.abs(res[0]["lambda_"] - single["lambda_"]) / single["lambda_"]) <= 1e-6
-    # preconditioned iteration counts follow the summation order: the reference's own
-    # serial / 4- / 8-thread runs of this problem take 52-54, f32-valued runs 47-55
-    assert abs(res[0]["iterations"] - single["iterations"]) <= max(3, 0.15 * single["iterations"])
+    # preconditioned iteration counts follow the summation order: both counts inside the
+    # reference's own ThreadPool(1..8) x variant envelope of this problem, +-1
+    from test_lobpcg_gpu import envelope
+    lo, hi = envelope(whole, diag, toff, k=8, nb=16, tol=3e-5, maxiter=300, seed=1)
+    assert lo - 1 <= res[0]["iterations"] <= hi + 1, (res[0]["iterations"], lo, hi)
+    assert lo - 1 <= single["iterations"] <= hi + 1, (single["iterations"], lo, hi)
 
 
 @pytest.mark.parametrize("nd", [1, 3])
