@@ -56,6 +56,7 @@
 
 #include "comm.hpp"
 #include "device.hpp"
+#include "hostcopy.hpp"
 #include "stream.cuh"
 
 namespace be {
@@ -1501,11 +1502,13 @@ static void op_build(Op* op, const be_csb_view& L, const RowMap* map) {
         for (auto& h : r.hdr) h.begin16 += static_cast<std::uint32_t>(b_off / 16);
         all_hdr.insert(all_hdr.end(), r.hdr.begin(), r.hdr.end());
         all_cls.insert(all_cls.end(), r.cls.begin(), r.cls.end());
-        BE_CUDA(cudaMemcpy(op->blobs.get() + b_off, r.blob.data(), r.blob.size(), cudaMemcpyHostToDevice));
+        // the copy pool (pinned pipelines on 16 host threads) instead of the driver's pageable path
+        h2d_large(op->blobs.get() + b_off, r.blob.data(), r.blob.size(), op->ctx->stream);
         if (keep_src) op->csb_index.insert(op->csb_index.end(), r.src.begin(), r.src.end());
         b_off += static_cast<index_t>(r.blob.size());
         r = RowOut();
     }
+    BE_CUDA(cudaStreamSynchronize(op->ctx->stream));
     if (ntiles > 0)
         BE_CUDA(cudaMemcpy(op->tiles.get(), all_hdr.data(), all_hdr.size() * sizeof(TileHdr), cudaMemcpyHostToDevice));
     if (map) {  // padded slots (ranks) whose rows the tiles read or write: tiles never straddle a segment
