@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsStages <= 2 ? 2 : 1)
                 const std::uint32_t p0 = __shfl_sync(1u, hd.packed, 0);
                 const int r0 = __shfl_sync(1u, hd.row0, 0);
                 const int nr = static_cast<int>(p0 & 127u) + 1;
-                stream::mbar_wait(&xempty[xs], (xeph >> xs) & 1u);
+                stream::mbar_wait_parked(&xempty[xs], (xeph >> xs) & 1u);
                 xeph ^= 1u << xs;
                 stream::mbar_arrive_expect_tx(&xfull[xs], static_cast<std::uint32_t>(G::REP * nr * G::RB));
 #pragma unroll
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsStages <= 2 ? 2 : 1)
                 h.col0 = __shfl_sync(0xffffffffu, hd.col0, i);
                 h.packed = __shfl_sync(0xffffffffu, hd.packed, i);
                 if (lane == 0) {
-                    stream::mbar_wait(&empty[s], (eph >> s) & 1u);
+                    stream::mbar_wait_parked(&empty[s], (eph >> s) & 1u);
                     eph ^= 1u << s;
                     shdr[s] = h;
                     sflag[s] = (i == 0 ? 1 : 0) | (i == cnt - 1 ? 2 : 0) | (xs << 2);
@@ -715,7 +715,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsStages <= 2 ? 2 : 1)
             }
         }
         if (lane == 0) {  // end of stream; then the last producer out resets the counter
-            stream::mbar_wait(&empty[s], (eph >> s) & 1u);
+            stream::mbar_wait_parked(&empty[s], (eph >> s) & 1u);
             shdr[s].packed = kWsEnd;
             stream::mbar_arrive_expect_tx(&full[s], 0);
             __threadfence();
@@ -735,13 +735,13 @@ __global__ void __launch_bounds__(kWsThreads, kWsStages <= 2 ? 2 : 1)
     int s = 0, tcount = 0;
     std::uint32_t fph = 0, xph = 0;
     for (;;) {
-        stream::mbar_wait(&full[s], (fph >> s) & 1u);
+        stream::mbar_wait_parked(&full[s], (fph >> s) & 1u);
         fph ^= 1u << s;
         const TileHdr h = shdr[s];
         if (h.packed == kWsEnd) break;
         const int fl = sflag[s], xs = (fl >> 2) & 1;
         if (do_c && (fl & 1)) {
-            stream::mbar_wait(&xfull[xs], (xph >> xs) & 1u);
+            stream::mbar_wait_parked(&xfull[xs], (xph >> xs) & 1u);
             xph ^= 1u << xs;
         }
         const unsigned char* st = smem + static_cast<std::size_t>(s) * stage_bytes;

@@ -40,6 +40,21 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* b, std::uint32_t phase)
         : "memory");
 }
 
+// The same wait with a suspend-time hint: the warp is parked by the hardware
+// until the phase completes (or the hint elapses) instead of spinning through
+// try_wait / branch, so waiting warps stop competing for issue slots.
+__device__ __forceinline__ void mbar_wait_parked(std::uint64_t* b, std::uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(phase), "r"(1000000u)
+        : "memory");
+}
+
 // order this thread's earlier generic-proxy shared-memory accesses before
 // later async-proxy (TMA) writes to the same buffer
 __device__ __forceinline__ void fence_proxy_async() {
