@@ -748,8 +748,11 @@ __global__ void __launch_bounds__(kWsThreads, kWsStages <= 2 ? 2 : 1)
         const int npad = pad16(static_cast<int>(h.packed >> 14));
         const std::uint16_t* seg = reinterpret_cast<const std::uint16_t*>(st + kMetaSeg);
         int b0, b1;
-        if (rot) {  // whole units, rotated by tile: warp w runs unit (w + tile) mod 8, no split ranks
-            const int un0 = (warp + tcount) & 7;
+        if (rot) {  // whole units, rotated by tile, no split ranks: warp w runs unit kRotSeq[(w + tile) mod 8]
+            // -- the sequence alternates heavy and light rank groups (R0, C3, R1, C2, R2, C1, R3, C0), so
+            // a warp never meets two long-row units in a row and its lead / lag stays within the ring
+            constexpr unsigned kRotSeq = 0x43526170u;  // nibbles, lowest first: 0 7 1 6 2 5 3 4
+            const int un0 = static_cast<int>((kRotSeq >> (4 * ((warp + tcount) & 7))) & 15u);
             b0 = un0 << 8;
             b1 = (un0 + 1) << 8;
         } else {  // the blob's equal-entry pieces
