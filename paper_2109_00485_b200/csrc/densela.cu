@@ -833,6 +833,103 @@ __global__ void __launch_bounds__(kT, BSM ? 1 : 2) k_mix_t(MixDev m, MixSrc ms, 
     cp_wait<0>();
 }
 
+// Register-direct tensor-core mix (nb = 8 or 16, <= 4 term slots, <= 4 panel
+// loads): no shared-memory staging and no CTA barrier in the row loop. Warp w
+// forms 8-row blocks w, w + W, ... (W = warps of the grid) on its own: lane
+// (g, t) loads row g of every panel with 16-byte loads -- term-slot panels
+// at columns KS t .. KS t + KS - 1 (KS = nb / 4), the k index of the m8n8k4
+// products permuted so that k-step kk uses column KS t + kk (the same
+// products, regrouped); accumulated / added panels in the accumulator layout
+// (columns 8 cb + 2 t, + 1) -- then forms and stores every output. Four CTAs
+// of eight warps per SM keep ~128 KB of loads in flight, like k_residual. The
+// B fragments (sign folded) sit in shared memory, fragment-major.
+struct MixR {
+    int nq;             // term slots (loads 0 .. nq - 1 are their panels)
+    const double* src[4];
+    int qo[4], last[4];  // output of each slot, slot ends its output
+    int accl[4], addl[4];  // per output: load index of the old value / the added panel, or -1
+    double* y[4];
+};
+
+template <int L, int KS>
+__device__ __forceinline__ double pick_load(const double (&x)[L][KS], int l, int i) {
+    double v = 0.0;
+#pragma unroll
+    for (int j = 0; j < L; ++j)
+        if (j == l) v = x[j][i];
+    return v;
+}
+
+template <int NBB, int L>
+__global__ void __launch_bounds__(256, 4) k_mix_r(MixDev m, MixR r, std::int64_t n) {
+    constexpr int NB = 8 * NBB, KS = NB / 4;
+    __shared__ __align__(16) double bsm[4 * KS * NBB * 32];  // [slot][kk][cb][lane]
+    for (int e = threadIdx.x; e < 4 * KS * NBB * 32; e += blockDim.x) {
+        const int ln = e & 31, cb = (e >> 5) % NBB, kk = (e >> 5) / NBB % KS, q = (e >> 5) / (NBB * KS);
+        double v = 0.0;
+        if (q < r.nq) {
+            const int o = r.qo[q];
+            int tt = 0;
+            for (int p = 0; p < q; ++p) tt += r.qo[p] == o;
+            const int ci = m.out[o].ci[tt];
+            v = m.out[o].sign[tt] * m.coef[ci][(8 * cb + (ln >> 2)) * m.ld[ci] + KS * (ln & 3) + kk];
+        }
+        bsm[e] = v;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const std::int64_t nblk = (n + 7) / 8;
+    const std::int64_t wstride = static_cast<std::int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (std::int64_t b = static_cast<std::int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nblk;
+         b += wstride) {
+        const std::int64_t row = b * 8 + g;
+        const bool ok = row < n;
+        double x[L][KS];
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            const bool cl = l >= r.nq;  // accumulator layout
+#pragma unroll
+            for (int h = 0; h < KS / 2; ++h) {
+                const int col = cl ? 8 * h + 2 * t : KS * t + 2 * h;
+                double2 v = make_double2(0.0, 0.0);
+                if (ok) v = *reinterpret_cast<const double2*>(r.src[l] + row * NB + col);
+                x[l][2 * h] = v.x;
+                x[l][2 * h + 1] = v.y;
+            }
+        }
+        double acc[NBB][2];
+#pragma unroll
+        for (int cb = 0; cb < NBB; ++cb) acc[cb][0] = acc[cb][1] = 0.0;
+#pragma unroll
+        for (int q = 0; q < L; ++q) {
+            if (q >= r.nq) break;
+#pragma unroll
+            for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+                for (int cb = 0; cb < NBB; ++cb)
+                    dmma884(acc[cb][0], acc[cb][1], x[q][kk], bsm[((q * KS + kk) * NBB + cb) * 32 + lane]);
+            if (r.last[q]) {  // output complete: old value / added panel, store, reset
+                const int o = r.qo[q], al = r.accl[o], dl = r.addl[o];
+                double* y = r.y[o] + row * NB + 2 * t;
+#pragma unroll
+                for (int cb = 0; cb < NBB; ++cb) {
+                    double v0 = acc[cb][0], v1 = acc[cb][1];
+                    if (al >= 0) {
+                        v0 = pick_load(x, al, 2 * cb) + v0;
+                        v1 = pick_load(x, al, 2 * cb + 1) + v1;
+                    }
+                    if (dl >= 0) {
+                        v0 += pick_load(x, dl, 2 * cb);
+                        v1 += pick_load(x, dl, 2 * cb + 1);
+                    }
+                    if (ok) *reinterpret_cast<double2*>(y + 8 * cb) = make_double2(v0, v1);
+                    acc[cb][0] = acc[cb][1] = 0.0;
+                }
+            }
+        }
+    }
+}
+
 // ---- streamed trsm (nb % 2 == 0, nb <= NBP): W <- W R^-1 for one or two
 // panels; chunk rows arrive by bulk copy, thread = (panel, row) substitutes
 // in registers (rows read / written in a lane-rotated 16-byte order), the
@@ -1485,8 +1582,57 @@ void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
                 ++mt.nq;
             }
         }
+        static const bool mix_r_on = [] {
+            const char* e = std::getenv("BE_MIX_R");
+            return !(e && e[0] == '0');
+        }();
+        if (ok && mix_r_on && (job.nb == 8 || job.nb == 16)) {  // register-direct kernel
+            MixR r{};
+            r.nq = mt.nq;
+            int nl = mt.nq;
+            for (int q = 0; q < mt.nq; ++q) {
+                r.src[q] = ms.src[mt.qs[q]];
+                r.qo[q] = mt.qo[q];
+                r.last[q] = mt.last[q];
+            }
+            bool fits = true;
+            for (int o = 0; o < m.nout; ++o) {
+                r.y[o] = m.out[o].y;
+                r.accl[o] = r.addl[o] = -1;
+                if (m.out[o].accumulate) {
+                    if (nl == 4) fits = false;
+                    else r.src[r.accl[o] = nl++] = m.out[o].y;
+                }
+                if (m.out[o].add_si >= 0) {
+                    if (nl == 4) fits = false;
+                    else r.src[r.addl[o] = nl++] = ms.src[m.out[o].add_si];
+                }
+            }
+            if (fits) {
+                const std::int64_t nblk = (n + 7) / 8;
+                const int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 4, (nblk + 7) / 8)));
+#define BE_MIXR(NBB, L) k_mix_r<NBB, L><<<grid, 256, 0, s>>>(m, r, n)
+#define BE_MIXR_L(NBB)                 \
+    switch (nl) {                      \
+        case 1: BE_MIXR(NBB, 1); break; \
+        case 2: BE_MIXR(NBB, 2); break; \
+        case 3: BE_MIXR(NBB, 3); break; \
+        default: BE_MIXR(NBB, 4); break; \
+    }
+                if (job.nb == 8) {
+                    BE_MIXR_L(1)
+                } else {
+                    BE_MIXR_L(2)
+                }
+#undef BE_MIXR_L
+#undef BE_MIXR
+                BE_CUDA(cudaGetLastError());
+                ++ctx->launches;
+                return;
+            }
+        }
         const bool bsm = job.nb > 16;
-        const std::size_t smt = 2 * static_cast<std::size_t>(ms.nsrc) * kMixPRows * (job.nb + 4) * sizeof(double) +
+        const std::size_t smt =2 * static_cast<std::size_t>(ms.nsrc) * kMixPRows * (job.nb + 4) * sizeof(double) +
                                 (bsm ? 4 * static_cast<std::size_t>(job.nb / 4) * (job.nb / 8) * 32 * sizeof(double) : 0);
         if (ok && smt <= 200 * 1024) {
             const int grid = static_cast<int>(

@@ -464,6 +464,21 @@ __device__ __forceinline__ int tri_lu_solve(const double (*sa)[kFomCols], const 
     }
 }
 
+#ifdef BE_FOM_PROF  // development probe: per-phase clock cycles of thread 0, summed per size class
+__device__ unsigned long long g_fom_prof[5][8];
+#define BE_FOM_MARK(k)                                                                                     \
+    do {                                                                                                   \
+        if (threadIdx.x == 0) {                                                                            \
+            const long long t_ = clock64();                                                                \
+            atomicAdd(&g_fom_prof[NT == 32 ? 0 : NT == 128 ? 1 : (NT == 256 && RPT == 2) ? 2 : NT == 256 ? 3 : 4][k], \
+                      static_cast<unsigned long long>(t_ - prof_t));                                       \
+            prof_t = t_;                                                                                   \
+        }                                                                                                  \
+    } while (0)
+#else
+#define BE_FOM_MARK(k) do {} while (0)
+#endif
+
 template <int MC, int NT, int RPT, bool VSM>
 __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
     k_fom_blk(const TileDev* __restrict__ tiles, const std::int32_t* __restrict__ list,
@@ -477,6 +492,9 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
     extern __shared__ __align__(16) double sV[];  // current basis vector [dmax][C], then the staged entries
     __shared__ __align__(16) double red[2 * (NT / 32) + 2][16];
     int rbuf = 0;
+#ifdef BE_FOM_PROF
+    long long prof_t = clock64();
+#endif
     const int tile = list[blockIdx.x / ngroups];
     const int grp = blockIdx.x % ngroups;
     const int col0 = grp * C;
@@ -573,6 +591,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
         }
     }
     block_colsum4<C, NT>(acc, red, rbuf);
+    BE_FOM_MARK(0);
     double beta0[kCW], inv[kCW], rinv[kCW];
 #pragma unroll
     for (int j = 0; j < kCW; ++j) {
@@ -653,6 +672,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
         if (staged) matvec(s_vl, s_cl);
         else matvec(gvl, gcl);
         block_colsum4<C, NT>(acc, red, rbuf);
+        BE_FOM_MARK(1);
         double a[kCW];
 #pragma unroll
         for (int j = 0; j < kCW; ++j) {
@@ -696,6 +716,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
                 }
             }
         }
+        BE_FOM_MARK(2);
 #pragma unroll
         for (int j = 0; j < kCW; ++j) acc[j] = 0.0;
 #pragma unroll
@@ -735,6 +756,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
             }
         }
         if constexpr (VSM) Vc += vstride;
+        BE_FOM_MARK(3);
     }
     // T y = beta0 e1 by LU with partial pivoting (precond.hpp:208-249), one
     // thread per column (register-resident: every index is unrolled); the
@@ -787,6 +809,10 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
             out[static_cast<std::int64_t>(i) * nb + j] = res;
         }
     }
+    BE_FOM_MARK(4);
+#ifdef BE_FOM_PROF
+    if (threadIdx.x == 0) atomicAdd(&g_fom_prof[NT == 32 ? 0 : NT == 128 ? 1 : (NT == 256 && RPT == 2) ? 2 : NT == 256 ? 3 : 4][5], 1ull);
+#endif
     if constexpr (!VSM) {  // every thread is done with the slot: release it
         __syncthreads();
         if (threadIdx.x == 0) atomicAnd(slot_mask + smid, ~(1u << (s_slot - static_cast<int>(smid) * kslots)));
@@ -1144,3 +1170,14 @@ void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, i
 }
 
 }  // namespace be
+
+#ifdef BE_FOM_PROF
+extern "C" int be_fom_prof_read(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, be::g_fom_prof, sizeof(be::g_fom_prof)) != cudaSuccess) return 1;
+    if (reset) {
+        static const unsigned long long z[5][8] = {};
+        if (cudaMemcpyToSymbol(be::g_fom_prof, z, sizeof(z)) != cudaSuccess) return 1;
+    }
+    return 0;
+}
+#endif

@@ -311,14 +311,16 @@ def test_gram_matches_numpy(ctx):
     assert np.array_equal(gs, gs.T)
 
 
+@pytest.mark.parametrize("rows", [5000, 4997])
 @pytest.mark.parametrize("nb", [8, 12, 16, 24, 32])
-def test_block_times_small_matches_numpy(ctx, nb):
-    """block_times_small(_add) (densela.hpp:448-484): the tensor-core mix (nb = 8, 16; 24, 32 with the
-    coefficient fragments in shared memory) and the FFMA kernel (other widths), f64 to ~1e-14."""
+def test_block_times_small_matches_numpy(ctx, nb, rows):
+    """block_times_small(_add) (densela.hpp:448-484): the tensor-core mixes (nb = 8, 16: register-direct,
+    a partial last 8-row block at 4997 rows; 24, 32: staged, coefficient fragments in shared memory) and
+    the FFMA kernel (other widths), f64 to ~1e-14."""
     rng = np.random.default_rng(nb)
-    x = rng.uniform(-1, 1, (5000, nb))
+    x = rng.uniform(-1, 1, (rows, nb))
     c = rng.uniform(-1, 1, (nb, nb))
-    y0 = rng.uniform(-1, 1, (5000, nb))
+    y0 = rng.uniform(-1, 1, (rows, nb))
     got = abi.dense_mix(ctx, x, c)
     assert np.max(np.abs(got - x @ c)) <= 1e-13 * nb
     got = abi.dense_mix(ctx, x, c, y0)
