@@ -35,17 +35,20 @@ namespace {
 constexpr int kN = 64;  // largest pencil
 constexpr int kLD = kN + 1;  // leading dimension: columns 130 words apart, so a warp walking
                              // across columns hits every bank pair once (no 32-way conflicts)
-constexpr int kRT = 512;
+#ifndef BE_RR_THREADS
+#define BE_RR_THREADS 256  // 8 warps: every warp recomputes a round's rotations, so more warps cost issue slots
+#endif
+constexpr int kRT = BE_RR_THREADS;
 
 struct Smem {
     double M[kN * kLD];  // column-major, leading dimension kLD
+    double M2[kN * kLD];  // Jacobi: the other half of the ping-pong pair
     double R[kN * kLD];
     double V[kN * kLD];
     double w[kN];
-    double cs[kN / 2][2];
-    int pq[kN / 2][2];
+    int pq[(kN - 1) * (kN / 2)][2];  // Jacobi pair table [round][pair]
     double floor_, red[kRT / 32];
-    int fail;
+    int fail, sweeps;
 };
 
 __device__ __forceinline__ int pair_of(int round, int i, int np, int& p, int& q) {
@@ -145,16 +148,61 @@ __device__ void reduce_pencil(Smem& S, int n) {
     __syncthreads();
 }
 
+// f64 reciprocal / reciprocal square root: the hardware approximation (~2^-23)
+// refined by Newton steps (each doubles the correct bits), no special-case
+// branches -- callers keep the arguments finite, positive and normal.
+template <int STEPS>
+__device__ __forceinline__ double rcp_nr(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+    for (int i = 0; i < STEPS; ++i) y = fma(y, fma(-x, y, 1.0), y);
+    return y;
+}
+template <int STEPS>
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+    for (int i = 0; i < STEPS; ++i) {
+        const double hx = 0.5 * x;
+        y = fma(y, fma(-hx * y, y, 0.5), y);  // y (3 - x y^2) / 2
+    }
+    return y;
+}
+
 // Parallel cyclic Jacobi on S.M (n x n, symmetric): S.V = eigenvectors,
 // S.w = eigenvalues (unsorted). np = n rounded up to even (a zero pad index).
+// Round-robin pairing (circle method), P = np / 2 disjoint pairs per round.
+// Every warp computes all P rotations of a round itself (lane b: pair b) from
+// the current M and writes its share of J^T M J into the other buffer of a
+// ping-pong pair (the pairs partition the indices: every entry is written
+// once per round), so a round costs one CTA barrier: rotations -> the warp's
+// 2 x 2 blocks of J^T M J and rows of V J (operands of other pairs by
+// shuffle) -> barrier -> swap. The rotation takes
+// one square root, one division and one reciprocal square root:
+//   d = a_qq - a_pp, t = sign(d) 2 a_pq / (|d| + sqrt(d^2 + 4 a_pq^2)),
+//   c = 1 / sqrt(1 + t^2), s = t c
+// (t the smaller root of t^2 + 2 (d / 2 a_pq) t - 1 = 0, as in the classical
+// formula th = d / (2 a_pq), t = sign(th) / (|th| + sqrt(1 + th^2))).
 __device__ void jacobi(Smem& S, int n) {
     const int tid = threadIdx.x;
     const int np = n + (n & 1);
     const int P = np / 2;
+    const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+    double* Mc = S.M;
+    double* Mn = S.M2;
     for (int e = tid; e < np * np; e += blockDim.x) {
         const int j = e / np, i = e % np;
         S.V[j * kLD + i] = i == j ? 1.0 : 0.0;
         if (i >= n || j >= n) S.M[j * kLD + i] = 0.0;
+    }
+    for (int e = tid; e < (np - 1) * P; e += blockDim.x) {  // pair table [round][pair]
+        const int round = e / P, i = e % P;
+        int p, q;
+        pair_of(round, i, np, p, q);
+        S.pq[e][0] = p;
+        S.pq[e][1] = q;
     }
     __syncthreads();
     for (int sweep = 0; sweep < 30; ++sweep) {
@@ -163,63 +211,101 @@ __device__ void jacobi(Smem& S, int n) {
         double off = 0.0, all = 0.0;
         for (int e = tid; e < n * n; e += blockDim.x) {
             const int j = e / n, i = e % n;
-            const double v = S.M[j * kLD + i];
+            const double v = Mc[j * kLD + i];
             all += v * v;
             if (i != j) off += v * v;
         }
         off = block_sum(off, S);
         all = block_sum(all, S);
+        if (tid == 0) S.sweeps = sweep;
         if (off <= 1e-28 * all) break;
         for (int round = 0; round < np - 1; ++round) {
-            if (tid < P) {  // this round's pairs and rotations
-                int p, q;
-                pair_of(round, tid, np, p, q);
-                const double apq = S.M[q * kLD + p];
-                double c = 1.0, s = 0.0;
-                if (q < n && fabs(apq) > 1e-300 &&
-                    fabs(apq) > 1e-17 * sqrt(fabs(S.M[p * kLD + p]) * fabs(S.M[q * kLD + q]))) {
-                    const double app = S.M[p * kLD + p], aqq = S.M[q * kLD + q];
-                    const double th = (aqq - app) / (2.0 * apq);
-                    // t = tan of the rotation angle, the smaller root; 1 / (2 th) when th^2 would overflow
-                    const double t = fabs(th) > 1e150 ? 0.5 / th
-                                                      : (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(1.0 + th * th));
-                    c = 1.0 / sqrt(1.0 + t * t);
-                    s = t * c;
+            int pb = 0, qb = 0;
+            double cb = 1.0, sb = 0.0;
+            if (lane < P) {  // this lane's pair of the round and its rotation (every warp alike)
+                pb = S.pq[round * P + lane][0];
+                qb = S.pq[round * P + lane][1];
+                const double apq = Mc[qb * kLD + pb];
+                if (qb < n) {
+                    const double app = Mc[pb * kLD + pb], aqq = Mc[qb * kLD + qb];
+                    if (apq * apq > 1e-34 * fabs(app * aqq) && fabs(apq) > 1e-300) {
+                        const double d = aqq - app, h = 2.0 * apq;
+                        // t needs only to annihilate a_pq to first order (the rotation stays exactly
+                        // orthogonal through c, s): approximate sqrt / division refined once; c to
+                        // full precision. The library routines outside the safe range.
+                        const double q2 = d * d + h * h;
+                        double t;
+                        if (q2 > 1e-280 && q2 < 1e280) {
+                            const double r = q2 * rsqrt_nr<1>(q2);
+                            t = copysign(1.0, d) * h * rcp_nr<1>(fabs(d) + r);
+                        } else {
+                            t = fabs(d) > 1e150 ? apq / d : copysign(1.0, d) * h / (fabs(d) + sqrt(q2));
+                        }
+                        cb = rsqrt_nr<2>(1.0 + t * t);
+                        sb = t * cb;
+                    }
                 }
-                S.cs[tid][0] = c;
-                S.cs[tid][1] = s;
-                S.pq[tid][0] = p;
-                S.pq[tid][1] = q;
             }
-            __syncthreads();
-            // M <- J^T M J: one 2 x 2 block per (warp row a, lane b); V <- V J: one row per warp step, lane b
-            const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+            // M <- J^T M J: 2 x 2 block (row pair a, column pair lane); V <- V J: rows of the warp,
+            // pair lane. All of a warp's loads are issued before its first store (fully unrolled).
+            constexpr int AMAX = (kN / 2 + kRT / 32 - 1) / (kRT / 32), IMAX = (kN + kRT / 32 - 1) / (kRT / 32);
+            {
+                int pa[AMAX], qa[AMAX];
+                double ca[AMAX], sa[AMAX], mv[AMAX][4];
+#pragma unroll
+                for (int j = 0; j < AMAX; ++j) {
+                    const int a = warp + j * nw;
+                    pa[j] = __shfl_sync(0xffffffffu, pb, a & 31);
+                    qa[j] = __shfl_sync(0xffffffffu, qb, a & 31);
+                    ca[j] = __shfl_sync(0xffffffffu, cb, a & 31);
+                    sa[j] = __shfl_sync(0xffffffffu, sb, a & 31);
+                    if (a < P && lane < P) {
+                        mv[j][0] = Mc[pb * kLD + pa[j]];
+                        mv[j][1] = Mc[qb * kLD + pa[j]];
+                        mv[j][2] = Mc[pb * kLD + qa[j]];
+                        mv[j][3] = Mc[qb * kLD + qa[j]];
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < AMAX; ++j) {
+                    const int a = warp + j * nw;
+                    if (a < P && lane < P) {
+                        // rows: p' = c p - s q, q' = s p + c q (J = [[c, s], [-s, c]])
+                        const double r_pp = ca[j] * mv[j][0] - sa[j] * mv[j][2], r_pq = ca[j] * mv[j][1] - sa[j] * mv[j][3];
+                        const double r_qp = sa[j] * mv[j][0] + ca[j] * mv[j][2], r_qq = sa[j] * mv[j][1] + ca[j] * mv[j][3];
+                        Mn[pb * kLD + pa[j]] = cb * r_pp - sb * r_pq;  // columns
+                        Mn[qb * kLD + pa[j]] = sb * r_pp + cb * r_pq;
+                        Mn[pb * kLD + qa[j]] = cb * r_qp - sb * r_qq;
+                        Mn[qb * kLD + qa[j]] = sb * r_qp + cb * r_qq;
+                    }
+                }
+            }
             if (lane < P) {
-                const int pb = S.pq[lane][0], qb = S.pq[lane][1];
-                const double cb = S.cs[lane][0], sb = S.cs[lane][1];
-                for (int a = warp; a < P; a += nw) {
-                    const int pa = S.pq[a][0], qa = S.pq[a][1];
-                    const double ca = S.cs[a][0], sa = S.cs[a][1];
-                    const double m_pp = S.M[pb * kLD + pa], m_pq = S.M[qb * kLD + pa];
-                    const double m_qp = S.M[pb * kLD + qa], m_qq = S.M[qb * kLD + qa];
-                    // rows: p' = c p - s q, q' = s p + c q (J = [[c, s], [-s, c]])
-                    const double r_pp = ca * m_pp - sa * m_qp, r_pq = ca * m_pq - sa * m_qq;
-                    const double r_qp = sa * m_pp + ca * m_qp, r_qq = sa * m_pq + ca * m_qq;
-                    S.M[pb * kLD + pa] = cb * r_pp - sb * r_pq;  // columns
-                    S.M[qb * kLD + pa] = sb * r_pp + cb * r_pq;
-                    S.M[pb * kLD + qa] = cb * r_qp - sb * r_qq;
-                    S.M[qb * kLD + qa] = sb * r_qp + cb * r_qq;
+                double vp[IMAX], vq[IMAX];
+#pragma unroll
+                for (int j = 0; j < IMAX; ++j) {
+                    const int i = warp + j * nw;
+                    if (i < np) {
+                        vp[j] = S.V[pb * kLD + i];
+                        vq[j] = S.V[qb * kLD + i];
+                    }
                 }
-                for (int i = warp; i < np; i += nw) {
-                    const double vp = S.V[pb * kLD + i], vq = S.V[qb * kLD + i];
-                    S.V[pb * kLD + i] = cb * vp - sb * vq;
-                    S.V[qb * kLD + i] = sb * vp + cb * vq;
+#pragma unroll
+                for (int j = 0; j < IMAX; ++j) {
+                    const int i = warp + j * nw;
+                    if (i < np) {
+                        S.V[pb * kLD + i] = cb * vp[j] - sb * vq[j];
+                        S.V[qb * kLD + i] = sb * vp[j] + cb * vq[j];
+                    }
                 }
             }
             __syncthreads();
+            double* const tmp = Mc;
+            Mc = Mn;
+            Mn = tmp;
         }
     }
-    for (int i = tid; i < n; i += blockDim.x) S.w[i] = S.M[i * kLD + i];
+    for (int i = tid; i < n; i += blockDim.x) S.w[i] = Mc[i * kLD + i];
     __syncthreads();
 }
 
@@ -287,6 +373,9 @@ __global__ void __launch_bounds__(kRT, 1) k_rr_eig(const double* __restrict__ bl
     Smem& S = *reinterpret_cast<Smem*>(raw);
     const int ng = nblk * (nblk + 1) / 2;
     const int ldc = nblk * nb;
+#ifdef BE_RR_PROF
+    long long t0 = clock64();
+#endif
     int use = nblk;
     for (;;) {
         assemble(S, blocks, nb, use, ng);
@@ -300,9 +389,24 @@ __global__ void __launch_bounds__(kRT, 1) k_rr_eig(const double* __restrict__ bl
     }
     if (threadIdx.x == 0 && use != nblk) st->rr_dropped = 1;
     const int n = use * nb;
+#ifdef BE_RR_PROF
+    long long t1 = clock64();
+#endif
     reduce_pencil(S, n);
+#ifdef BE_RR_PROF
+    long long t2 = clock64();
+#endif
     jacobi(S, n);
+#ifdef BE_RR_PROF
+    long long t3 = clock64();
+#endif
     back_transform(S, n, nb, c, ldc, theta);
+#ifdef BE_RR_PROF
+    long long t4 = clock64();
+    if (threadIdx.x == 0)
+        printf("[rr_eig] n %d chol %lld reduce %lld jacobi %lld (sweeps %d) back %lld cycles\n", n, t1 - t0, t2 - t1,
+               t3 - t2, S.sweeps, t4 - t3);
+#endif
     if (shifts)
         for (int v = threadIdx.x; v < nb; v += blockDim.x) shifts[v] = theta[min(v, k - 1)];
 }
