@@ -239,7 +239,6 @@ __global__ void __launch_bounds__(kPT) k_fom(const TileDev* __restrict__ tiles, 
 // reduction result, so the tridiagonal solves run redundantly in registers).
 // The tile's entries are staged in shared memory when they fit.
 constexpr int kCW = 4;
-constexpr int kFomCols = 16;  // columns per CTA of the block kernel
 
 template <int C, int NT>
 __device__ __forceinline__ void block_colsum4(double (&v)[kCW], double (*red)[16], int& buf) {
@@ -281,20 +280,22 @@ __device__ __forceinline__ void block_sync() {
 struct V4 {
     double a[kCW];
 };
-// A row of the 16-column basis in shared memory is two 64-byte halves; the
-// 16-byte piece h of column chunk cq sits at h * 8 + cq * 2 doubles. Row lanes
-// of odd parity read (and write) their high piece first (hp = 8), so the two
-// rows of a quarter-warp phase always hit opposite bank halves: gathers of
-// arbitrary rows are conflict-free.
-static_assert(kFomCols == 16, "the piece layout of ld4 / st4 assumes 16-column rows");
+// A row of the C-column basis in shared memory is two halves of H = C / 2
+// doubles; the 16-byte piece h of column chunk cq sits at h * H + cq * 2
+// doubles. Row lanes of odd parity read (and write) their high piece first
+// (hp = H), so the two rows of a quarter-warp phase hit opposite bank halves:
+// gathers of arbitrary rows are conflict-free for C = 16 (64-byte halves);
+// for C = 8 (32-byte halves) two of the four rows of a phase can share one.
+template <int H>
 __device__ __forceinline__ V4 ld4(const double* p, int hp) {  // p: row + cq * 2
-    const double2 x = *reinterpret_cast<const double2*>(p + hp), y = *reinterpret_cast<const double2*>(p + (8 - hp));
+    const double2 x = *reinterpret_cast<const double2*>(p + hp), y = *reinterpret_cast<const double2*>(p + (H - hp));
     return hp ? V4{{y.x, y.y, x.x, x.y}} : V4{{x.x, x.y, y.x, y.y}};
 }
+template <int H>
 __device__ __forceinline__ void st4(double* p, const double (&v)[kCW], int hp) {
     const double2 lo = make_double2(v[0], v[1]), hi = make_double2(v[2], v[3]);
     *reinterpret_cast<double2*>(p + hp) = hp ? hi : lo;
-    *reinterpret_cast<double2*>(p + (8 - hp)) = hp ? lo : hi;
+    *reinterpret_cast<double2*>(p + (H - hp)) = hp ? lo : hi;
 }
 
 // x / b, correctly rounded, from r = 1 / b (one reciprocal per column
@@ -308,8 +309,8 @@ __device__ __forceinline__ double div_rcp(double x, double b, double r) {
 // T y = beta0 e1 for one column's m x m Lanczos tridiagonal: LU with partial
 // pivoting and the singular-pivot flag (precond.hpp:208-249). UNR: every
 // index unrolled (T and y stay in registers, m <= 4); else rolled loops.
-template <int MC, bool UNR>
-__device__ __forceinline__ int tri_lu_solve(const double (*sa)[kFomCols], const double (*sb)[kFomCols], int cc, int st,
+template <int MC, bool UNR, int C>
+__device__ __forceinline__ int tri_lu_solve(const double (*sa)[C], const double (*sb)[C], int cc, int st,
                                             double b0, double (&y)[MC]) {
     if constexpr (UNR) {
         double T[MC][MC];
@@ -470,7 +471,7 @@ __device__ unsigned long long g_fom_prof[5][8];
     do {                                                                                                   \
         if (threadIdx.x == 0) {                                                                            \
             const long long t_ = clock64();                                                                \
-            atomicAdd(&g_fom_prof[NT == 32 ? 0 : NT == 128 ? 1 : (NT == 256 && RPT == 2) ? 2 : NT == 256 ? 3 : 4][k], \
+            atomicAdd(&g_fom_prof[NT == 32 ? 0 : NT == 128 ? 1 : (NT == 256 && RPT == 2) ? 2 : (NT == 256 && C == 16) ? 3 : 4][k], \
                       static_cast<unsigned long long>(t_ - prof_t));                                       \
             prof_t = t_;                                                                                   \
         }                                                                                                  \
@@ -479,15 +480,15 @@ __device__ unsigned long long g_fom_prof[5][8];
 #define BE_FOM_MARK(k) do {} while (0)
 #endif
 
-template <int MC, int NT, int RPT, bool VSM>
+template <int MC, int NT, int RPT, bool VSM, int C>
 __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
     k_fom_blk(const TileDev* __restrict__ tiles, const std::int32_t* __restrict__ list,
               const std::int32_t* __restrict__ rowptr, const std::uint16_t* __restrict__ cols,
               const double* __restrict__ vals, const double* __restrict__ shifts, const double* __restrict__ R,
               double* __restrict__ W, int nb, int m, int ngroups, std::int64_t* fallbacks, int dmax, int stage_cap,
               double* __restrict__ Vg, std::int64_t nrows, unsigned* __restrict__ slot_mask, int kslots) {
-    constexpr int C = kFomCols;
     constexpr int CQ = C / kCW;  // column chunks per row
+    constexpr int H = C / 2;     // half-row of the basis layout (ld4 / st4)
     constexpr int RL = NT / CQ;  // row lanes
     extern __shared__ __align__(16) double sV[];  // current basis vector [dmax][C], then the staged entries
     __shared__ __align__(16) double red[2 * (NT / 32) + 2][16];
@@ -520,7 +521,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
     // in L2 (the launch guarantees one CTA per SM).
     const std::size_t vstride = static_cast<std::size_t>(dmax) * C;
     double* Vcur = sV + cq * 2;  // this chunk's low piece (see ld4)
-    const int hp = NT == 32 ? 0 : (rl & 1) * 8;  // (the one-warp class is not shared-memory bound)
+    const int hp = NT == 32 ? 0 : (rl & 1) * H;  // (the one-warp class is not shared-memory bound)
     double* Vslot = nullptr;
     __shared__ int s_slot;
     unsigned smid = 0;
@@ -606,8 +607,8 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
             double v[kCW];
 #pragma unroll
             for (int j = 0; j < kCW; ++j) v[j] = div_rcp(w[k][j], inv[j], rinv[j]);
-            st4(Vc + static_cast<std::size_t>(i) * C, v, hp);
-            if constexpr (!VSM) st4(vg(0, i), v, hp);
+            st4<H>(Vc + static_cast<std::size_t>(i) * C, v, hp);
+            if constexpr (!VSM) st4<H>(vg(0, i), v, hp);
         }
     }
     // Lanczos scalars of the CTA's columns (written by row lane 0; every
@@ -644,8 +645,8 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
                     int e = eb[k];
                     for (; e + 1 < ee[k]; e += 2) {
                         const double a0 = vl[e], a1 = vl[e + 1];
-                        const V4 x0 = ld4(Vc + static_cast<int>(cl[e]) * C, hp);
-                        const V4 x1 = ld4(Vc + static_cast<int>(cl[e + 1]) * C, hp);
+                        const V4 x0 = ld4<H>(Vc + static_cast<int>(cl[e]) * C, hp);
+                        const V4 x1 = ld4<H>(Vc + static_cast<int>(cl[e + 1]) * C, hp);
 #pragma unroll
                         for (int j = 0; j < kCW; ++j) y[j] += a0 * x0.a[j];
 #pragma unroll
@@ -653,11 +654,11 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
                     }
                     if (e < ee[k]) {
                         const double a0 = vl[e];
-                        const V4 x0 = ld4(Vc + static_cast<int>(cl[e]) * C, hp);
+                        const V4 x0 = ld4<H>(Vc + static_cast<int>(cl[e]) * C, hp);
 #pragma unroll
                         for (int j = 0; j < kCW; ++j) y[j] += a0 * x0.a[j];
                     }
-                    const V4 v = ld4(Vc + static_cast<std::size_t>(i) * C, hp);
+                    const V4 v = ld4<H>(Vc + static_cast<std::size_t>(i) * C, hp);
                     const double dg = vl[ee[k]];
 #pragma unroll
                     for (int j = 0; j < kCW; ++j) {
@@ -684,8 +685,8 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
         for (int k = 0; k < RPT; ++k) {
             const int i = rl + k * RL;
             if (i >= d) continue;
-            const V4 vs = ld4(Vc + static_cast<std::size_t>(i) * C, hp);
-            const V4 vp = s > 0 ? ld4(vg(s - 1, i), hp) : V4{{0.0, 0.0, 0.0, 0.0}};
+            const V4 vs = ld4<H>(Vc + static_cast<std::size_t>(i) * C, hp);
+            const V4 vp = s > 0 ? ld4<H>(vg(s - 1, i), hp) : V4{{0.0, 0.0, 0.0, 0.0}};
 #pragma unroll
             for (int j = 0; j < kCW; ++j) {
                 double x = w[k][j] - a[j] * vs.a[j];
@@ -700,7 +701,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
             for (int k = 0; k < RPT; ++k) {
                 const int i = rl + k * RL;
                 if (i < d) {
-                    const V4 v = (q == s ? ld4(Vc + static_cast<std::size_t>(i) * C, hp) : ld4(vg(q, i), hp));
+                    const V4 v = (q == s ? ld4<H>(Vc + static_cast<std::size_t>(i) * C, hp) : ld4<H>(vg(q, i), hp));
 #pragma unroll
                     for (int j = 0; j < kCW; ++j) acc[j] += v.a[j] * w[k][j];
                 }
@@ -710,7 +711,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
             for (int k = 0; k < RPT; ++k) {  // V_q re-read (shared memory or this CTA's L1/L2 slot)
                 const int i = rl + k * RL;
                 if (i < d) {
-                    const V4 v = (q == s ? ld4(Vc + static_cast<std::size_t>(i) * C, hp) : ld4(vg(q, i), hp));
+                    const V4 v = (q == s ? ld4<H>(Vc + static_cast<std::size_t>(i) * C, hp) : ld4<H>(vg(q, i), hp));
 #pragma unroll
                     for (int j = 0; j < kCW; ++j) w[k][j] -= acc[j] * v.a[j];
                 }
@@ -748,10 +749,10 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
 #pragma unroll
                 for (int j = 0; j < kCW; ++j) v[j] = div_rcp(w[k][j], inv[j], rinv[j]);
                 if constexpr (VSM) {
-                    st4(vg(s + 1, i), v, hp);
+                    st4<H>(vg(s + 1, i), v, hp);
                 } else {
-                    st4(Vc + static_cast<std::size_t>(i) * C, v, hp);
-                    st4(vg(s + 1, i), v, hp);
+                    st4<H>(Vc + static_cast<std::size_t>(i) * C, v, hp);
+                    st4<H>(vg(s + 1, i), v, hp);
                 }
             }
         }
@@ -777,8 +778,8 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
         const double b0 = s_b0[cc];
         double y[MC];
         int sg;
-        if constexpr (MC <= 4) sg = tri_lu_solve<MC, true>(s_alpha, s_beta, cc, st, b0, y);
-        else sg = tri_lu_solve<MC, false>(s_alpha, s_beta, cc, st, b0, y);
+        if constexpr (MC <= 4) sg = tri_lu_solve<MC, true, C>(s_alpha, s_beta, cc, st, b0, y);
+        else sg = tri_lu_solve<MC, false, C>(s_alpha, s_beta, cc, st, b0, y);
         if (col0 + cc < nb && b0 != 0.0 && sg && fallbacks)
             atomicAdd(reinterpret_cast<unsigned long long*>(fallbacks), 1ull);
 #pragma unroll
@@ -795,7 +796,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
 #pragma unroll
         for (int q = 0; q < MC; ++q) {  // unrolled: the basis reads are in flight together
             if (q >= cap) break;
-            const V4 v = ld4(vg(q, i), hp);
+            const V4 v = ld4<H>(vg(q, i), hp);
 #pragma unroll
             for (int j = 0; j < kCW; ++j)
                 if (q < s_steps[cq * kCW + j]) o[j] += s_y[cq * kCW + j][q] * v.a[j];
@@ -811,7 +812,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
     }
     BE_FOM_MARK(4);
 #ifdef BE_FOM_PROF
-    if (threadIdx.x == 0) atomicAdd(&g_fom_prof[NT == 32 ? 0 : NT == 128 ? 1 : (NT == 256 && RPT == 2) ? 2 : NT == 256 ? 3 : 4][5], 1ull);
+    if (threadIdx.x == 0) atomicAdd(&g_fom_prof[NT == 32 ? 0 : NT == 128 ? 1 : (NT == 256 && RPT == 2) ? 2 : (NT == 256 && C == 16) ? 3 : 4][5], 1ull);
 #endif
     if constexpr (!VSM) {  // every thread is done with the slot: release it
         __syncthreads();
@@ -820,15 +821,26 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
 }
 
 // size classes of the block kernel: tiles up to kClassDims[c] rows run on
-// CTAs of kClassThreads[c] threads (4 per row, 16 columns per CTA)
+// CTAs of the thread count in precond_apply's launch switch, kClassCols[c] columns per CTA (a tile is
+// split over nb / C CTAs), every thread 4 adjacent columns of RPT rows, the
+// dynamic shared memory (current vector + staged entries) held to
+// kClassBudget[c]. Measured at T1 (profiles/r02_dense_precond_ncu.md): the
+// 257..512-row class as two 8-column CTAs of 256 threads per SM (budget
+// 104 KB) is 5 % slower than one 16-column CTA of 512 threads -- the same
+// threads per SM either way (128 registers each fill the register file), and
+// each CTA's Lanczos step costs as long at half the columns.
 constexpr int kClassDims[] = {32, 64, 128, 256, 512};
 #ifndef BE_FOM_C4_NT
 #define BE_FOM_C4_NT 512
 #define BE_FOM_C4_RPT 4
+#define BE_FOM_C4_C 16
+#define BE_FOM_C4_BUDGET_KB 200
 #endif
-constexpr int kClassThreads[] = {32, 128, 256, 256, BE_FOM_C4_NT};
+constexpr int kClassCols[] = {16, 16, 16, 16, BE_FOM_C4_C};
 constexpr bool kClassVsm[] = {true, true, true, false, false};  // whole basis in shared memory
 constexpr std::size_t kStageBudget = 200 * 1024;  // current vector + staged entries per CTA
+constexpr std::size_t kClassBudget[] = {kStageBudget, kStageBudget, kStageBudget, kStageBudget,
+                                        static_cast<std::size_t>(BE_FOM_C4_BUDGET_KB) * 1024};
 
 
 __global__ void k_nsmid(int* out) {
@@ -1091,7 +1103,7 @@ void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, i
             joined[c] = true;
         }
         const int dmax = t->class_dim[static_cast<std::size_t>(c)];
-        const int C = kFomCols;
+        const int C = kClassCols[c];
         const int ngroups = (nb + C - 1) / C;
         const std::int32_t* list = t->class_tiles.get() + b0;
         const int mc = m <= 4 ? 4 : 8;
@@ -1099,7 +1111,8 @@ void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, i
         const bool vsm = kClassVsm[c] && vone * std::min(m, mc) <= 160 * 1024;  // else: scratch slots in L2
         const std::size_t vbytes = vone * (vsm ? std::min(m, mc) : 1);
         // entry staging: up to the class's largest tile, within the smem budget
-        const std::size_t room = vbytes < kStageBudget ? (kStageBudget - vbytes) / 10 : 0;
+        const std::size_t budget = kClassBudget[c];
+        const std::size_t room = vbytes < budget ? (budget - vbytes) / 10 : 0;
         const int stage_cap = static_cast<int>(std::min<std::size_t>(room, static_cast<std::size_t>(t->class_max_ent[static_cast<std::size_t>(c)]))) & ~7;
         std::size_t sm = vbytes + static_cast<std::size_t>(stage_cap) * 10;
         const unsigned grid = static_cast<unsigned>((b1 - b0) * ngroups);
@@ -1116,29 +1129,30 @@ void precond_apply(Tiles* t, const double* shifts, const double* R, double* W, i
                 BE_CUDA(cudaMemsetAsync(t->slot_mask[c].get(), 0, t->slot_mask[c].bytes(), cs));
             }
         };
-#define BE_FOMB(MC, NTT, RPT, VS)                                                                                  \
-    do {                                                                                                           \
-        ensure_dyn_smem(k_fom_blk<MC, NTT, RPT, VS>, sm);                                                          \
-        if (!(VS)) slots_for(reinterpret_cast<const void*>(k_fom_blk<MC, NTT, RPT, VS>), NTT);                    \
-        k_fom_blk<MC, NTT, RPT, VS><<<grid, NTT, sm, cs>>>(tdv, list, t->rowptr.get(), t->cols.get(), t->vals.get(), \
-                                                            shifts, R, W, nb, m, ngroups, fallbacks, dmax,         \
-                                                            stage_cap, t->vscratch[c].get(), t->n,                 \
-                                                            t->slot_mask[c].get(), kslots);                        \
+#define BE_FOMB(MC, NTT, RPT, VS, CC)                                                                              \
+    do {                                                                                                               \
+        ensure_dyn_smem(k_fom_blk<MC, NTT, RPT, VS, CC>, sm);                                                          \
+        if (!(VS)) slots_for(reinterpret_cast<const void*>(k_fom_blk<MC, NTT, RPT, VS, CC>), NTT);                    \
+        k_fom_blk<MC, NTT, RPT, VS, CC><<<grid, NTT, sm, cs>>>(tdv, list, t->rowptr.get(), t->cols.get(), t->vals.get(), \
+                                                                shifts, R, W, nb, m, ngroups, fallbacks, dmax,         \
+                                                                stage_cap, t->vscratch[c].get(), t->n,                 \
+                                                                t->slot_mask[c].get(), kslots);                        \
     } while (0)
-#define BE_FOMB2(NTT, RPT)                      \
-    if (mc == 4) {                              \
-        if (vsm) BE_FOMB(4, NTT, RPT, true);    \
-        else BE_FOMB(4, NTT, RPT, false);       \
-    } else {                                    \
-        if (vsm) BE_FOMB(8, NTT, RPT, true);    \
-        else BE_FOMB(8, NTT, RPT, false);       \
+#define BE_FOMB2(NTT, RPT, CC)                      \
+    if (mc == 4) {                                  \
+        if (vsm) BE_FOMB(4, NTT, RPT, true, CC);    \
+        else BE_FOMB(4, NTT, RPT, false, CC);       \
+    } else {                                        \
+        if (vsm) BE_FOMB(8, NTT, RPT, true, CC);    \
+        else BE_FOMB(8, NTT, RPT, false, CC);       \
     }
+        static_assert(BE_FOM_C4_NT / (BE_FOM_C4_C / kCW) * BE_FOM_C4_RPT >= 512, "class 4 rows per CTA");
         switch (c) {
-            case 0: BE_FOMB2(32, 4); break;    // 8 rows per pass x 4
-            case 1: BE_FOMB2(128, 2); break;   // 32 x 2
-            case 2: BE_FOMB2(256, 2); break;   // 64 x 2
-            case 3: BE_FOMB2(256, 4); break;   // 64 x 4 (two CTAs per SM)
-            default: BE_FOMB2(BE_FOM_C4_NT, BE_FOM_C4_RPT); break;  // 128 x 4
+            case 0: BE_FOMB2(32, 4, 16); break;    // 8 rows per pass x 4
+            case 1: BE_FOMB2(128, 2, 16); break;   // 32 x 2
+            case 2: BE_FOMB2(256, 2, 16); break;   // 64 x 2
+            case 3: BE_FOMB2(256, 4, 16); break;   // 64 x 4 (two CTAs per SM)
+            default: BE_FOMB2(BE_FOM_C4_NT, BE_FOM_C4_RPT, BE_FOM_C4_C); break;  // 128 x 4, 8 columns
         }
 #undef BE_FOMB2
 #undef BE_FOMB

@@ -27,7 +27,8 @@ R = torch.rand(n, nb, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
 W = torch.zeros_like(R)
 sh = torch.linspace(0.5, 2.0, nb, dtype=torch.float64, device="cuda")
 lib = abi.lib()
-st = torch.cuda.current_stream().cuda_stream
+st = ctx.stream()  # the context stream (torch's legacy default stream is 0 = "use the context's")
+es = torch.cuda.ExternalStream(st)
 
 
 def run():
@@ -41,9 +42,9 @@ for _ in range(3):
 ts = []
 for _ in range(10):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
+    a.record(es)
     run()
-    b.record()
+    b.record(es)
     torch.cuda.synchronize()
     ts.append(a.elapsed_time(b))
 print(f"precond {cfg}: median {np.median(ts):.3f} ms, min {min(ts):.3f} ms", flush=True)
