@@ -1044,6 +1044,130 @@ __global__ void __launch_bounds__(256, 2) k_trsm_s(double* __restrict__ w0, doub
     cp_wait<0>();
 }
 
+// ---- warp-independent trsm (nb = NB, 8 or 16): W <- W R^-1 for one or two
+// panels. A warp takes 32-row blocks w, w + W, ... on its own: 16-byte
+// cp.async copies (coalesced, the next block's in flight while this one is
+// solved) into a double-buffered warp-private shared-memory tile (rows padded
+// to NB + 2 doubles: the row-major copies and the row-per-lane reads are both
+// conflict-free), lane l substitutes row l in registers exactly as k_trsm_s,
+// the results go back with coalesced 16-byte stores. No CTA barrier after the
+// setup.
+constexpr int kTrsmWarps = 4;
+// shared-memory loads the compiler may not hoist out of the row loop (the
+// 120 factor entries would otherwise be kept in registers and spill)
+__device__ __forceinline__ double2 lds2_nohoist(const double* p) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(stream::smem_u32(p)));
+    return v;
+}
+__device__ __forceinline__ double lds_nohoist(const double* p) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(stream::smem_u32(p)));
+    return v;
+}
+template <int NB>
+__global__ void __launch_bounds__(kTrsmWarps * 32) k_trsm_r(double* __restrict__ w0, double* __restrict__ w1,
+                                                           const double* __restrict__ Rg, std::int64_t n, Status* st,
+                                                           int skip_if_rank, int skip_if_notpd) {
+    constexpr int RS = NB + 2, PR = NB / 2;  // padded row stride (doubles), 16-byte pieces per row
+    constexpr int RPI = 32 / PR;             // rows per coalesced warp copy
+    constexpr int LPP = NB / 2;              // 16-byte pieces per lane per panel block
+    extern __shared__ __align__(16) double sbuf[];
+    __shared__ __align__(16) double Rs[NB * NB];
+    __shared__ double Rinv[NB];
+    __shared__ int skip;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int np = w1 ? 2 : 1;
+    if (tid == 0) {
+        int sk = (skip_if_rank && st->rank_deficient) || (skip_if_notpd && st->not_pd);
+        if (!sk) {  // trsm_right_inv's conditioning check (densela.hpp:129-136)
+            double dmin = INFINITY, dmax = 0.0;
+            for (int j = 0; j < NB; ++j) {
+                const double d = fabs(Rg[j * NB + j]);
+                dmin = fmin(dmin, d);
+                dmax = fmax(dmax, d);
+            }
+            if (!(dmin > 1e-14 * dmax)) {
+                sk = 1;
+                if (blockIdx.x == 0) st->singular_tri = 1;
+            }
+        }
+        skip = sk;
+    }
+    for (int e = tid; e < NB * NB; e += blockDim.x) Rs[e] = Rg[e];
+    if (tid < NB) Rinv[tid] = 1.0 / Rg[tid * NB + tid];
+    __syncthreads();
+    if (skip) return;
+    const int tstride = np * 32 * RS;                                        // one buffer: [panel][row][RS]
+    double* tiles = sbuf + static_cast<std::size_t>(warp) * 2 * tstride;  // two buffers per warp
+    const std::int64_t nblk = (n + 31) / 32;
+    const std::int64_t wstride = static_cast<std::int64_t>(gridDim.x) * kTrsmWarps;
+    const int lr = lane / PR, lc = lane % PR;  // coalesced piece: row lr + RPI k, piece lc
+    auto issue = [&](std::int64_t b, double* t) {
+        if (b < nblk) {
+            const std::int64_t r0 = b * 32;
+            for (int p = 0; p < np; ++p) {
+                const double* w = (p == 0 ? w0 : w1) + r0 * NB;
+#pragma unroll
+                for (int k = 0; k < LPP; ++k) {
+                    const int r = lr + RPI * k;
+                    if (r0 + r < n) cp16g(t + p * 32 * RS + r * RS + 2 * lc, w + r * NB + 2 * lc);
+                }
+            }
+        }
+        cp_commit();
+    };
+    std::int64_t b = static_cast<std::int64_t>(blockIdx.x) * kTrsmWarps + warp;
+    issue(b, tiles);
+    for (int it = 0; b < nblk; b += wstride, ++it) {
+        double* t = tiles + (it & 1) * tstride;
+        issue(b + wstride, tiles + ((it + 1) & 1) * tstride);  // next block in flight during the solve
+        cp_wait<1>();
+        __syncwarp();
+        const std::int64_t r0 = b * 32;
+        for (int p = 0; p < np; ++p) {
+            double* xr = t + p * 32 * RS + lane * RS;
+            double x[NB];
+#pragma unroll
+            for (int k = 0; k < NB / 2; ++k) {
+                const double2 v = reinterpret_cast<const double2*>(xr)[k];
+                x[2 * k] = v.x;
+                x[2 * k + 1] = v.y;
+            }
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                double s = x[j];
+#pragma unroll
+                for (int i = 0; i + 1 < j; i += 2) {  // i ascending, as k_trsm_s
+                    const double2 rr = lds2_nohoist(Rs + j * NB + i);
+                    s -= x[i] * rr.x;
+                    s -= x[i + 1] * rr.y;
+                }
+                if (j & 1) s -= x[j - 1] * lds_nohoist(Rs + j * NB + j - 1);
+                const double d = lds_nohoist(Rs + j * NB + j), ri = lds_nohoist(Rinv + j);
+                double qj = s * ri;
+                qj = fma(fma(-qj, d, s), ri, qj);
+                x[j] = qj;
+            }
+#pragma unroll
+            for (int k = 0; k < NB / 2; ++k) reinterpret_cast<double2*>(xr)[k] = make_double2(x[2 * k], x[2 * k + 1]);
+        }
+        __syncwarp();
+        for (int p = 0; p < np; ++p) {
+            double* w = (p == 0 ? w0 : w1) + r0 * NB;
+#pragma unroll
+            for (int k = 0; k < LPP; ++k) {
+                const int r = lr + RPI * k;
+                if (r0 + r < n)
+                    reinterpret_cast<double2*>(w + r * NB)[lc] =
+                        reinterpret_cast<const double2*>(t + p * 32 * RS + r * RS)[lc];
+            }
+        }
+        __syncwarp();  // this buffer is refilled two blocks on
+    }
+    cp_wait<0>();
+}
+
 // -------------------------------------------------------------------- trsm
 // 128 rows per CTA pass staged in smem (coalesced), one thread per row does
 // the forward substitution of trsm_right_inv (densela.hpp:137-146) from smem.
@@ -1677,6 +1801,28 @@ void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
 
 void trsm(Ctx* ctx, double* w0, double* w1, const double* R, int nb, std::int64_t n, Status* st, int skip_if_rank,
           int skip_if_notpd, cudaStream_t s) {
+    static const bool trsm_r_on = [] {
+        const char* e = std::getenv("BE_TRSM_R");
+        return !(e && e[0] == '0');
+    }();
+    if (trsm_r_on && (nb == 8 || nb == 16) && n > 0) {  // warp-independent kernel
+        const int np = w1 ? 2 : 1;
+        const std::size_t sm = static_cast<std::size_t>(kTrsmWarps) * 2 * np * 32 * (nb + 2) * sizeof(double);
+        const int per_sm = static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(6, (220u * 1024) / (sm + 2048))));
+        const std::int64_t nblk = (n + 31) / 32;
+        const int grid = static_cast<int>(std::max<std::int64_t>(
+            1, std::min<std::int64_t>(static_cast<std::int64_t>(per_sm) * ctx->num_sms, (nblk + kTrsmWarps - 1) / kTrsmWarps)));
+        if (nb == 8) {
+            ensure_dyn_smem(k_trsm_r<8>, sm);
+            k_trsm_r<8><<<grid, kTrsmWarps * 32, sm, s>>>(w0, w1, R, n, st, skip_if_rank, skip_if_notpd);
+        } else {
+            ensure_dyn_smem(k_trsm_r<16>, sm);
+            k_trsm_r<16><<<grid, kTrsmWarps * 32, sm, s>>>(w0, w1, R, n, st, skip_if_rank, skip_if_notpd);
+        }
+        BE_CUDA(cudaGetLastError());
+        ++ctx->launches;
+        return;
+    }
     if (nb % 2 == 0 && nb <= 32 && n > 0) {  // streamed
         const int np = w1 ? 2 : 1;
         const int Rr = 256 / np;
