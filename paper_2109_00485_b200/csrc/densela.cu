@@ -384,6 +384,85 @@ __global__ void __launch_bounds__(256, BE_GRAM_CTAS) k_gram_m(GramDev g, GramM q
     for (int e = tid; e < g.npairs * nb * nb; e += blockDim.x) out[e] = red[e];
 }
 
+// Register-direct Gram (nb = 8 NBB, NBB = 1 or 2; <= 2 pairs over <= 2
+// panels): no staging, no CTA barrier in the row loop. The CTA takes a
+// contiguous range of 32-row groups, its warps interleave over them; per
+// group a lane (g, t) loads, for k-step kk, row 4 kk + t at columns NBB g ..
+// NBB g + NBB - 1 of each panel (one 16- or 8-byte load; a warp load is four
+// whole rows) -- the m / n index of the m8n8k4 fragments is permuted so that
+// fragment element ib of lane g is column NBB g + ib: block (ib, jb) of the
+// accumulators holds output entries (NBB g + ib, NBB (2 t + h) + jb). Warps
+// are summed in order through shared memory into the CTA partial
+// (k_gram_reduce_m sums the CTAs in a fixed order: deterministic).
+template <int NBB, int ND, int NPR>
+__global__ void __launch_bounds__(512, ND == 2 ? 1 : 2) k_gram_r(GramDev g, std::int64_t n, double* __restrict__ partial) {
+    constexpr int NB = 8 * NBB, U = 8;  // 8 k-steps = 32 rows per group
+    extern __shared__ __align__(16) double red[];  // [warp][pair][NB][NB]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int gq = lane >> 2, t = lane & 3;
+    const std::int64_t nq = (n + 31) / 32;
+    const std::int64_t q0 = nq * blockIdx.x / gridDim.x, q1 = nq * (blockIdx.x + 1) / gridDim.x;
+    int ia[NPR], ib[NPR];
+#pragma unroll
+    for (int a = 0; a < NPR; ++a) {
+        ia[a] = g.ia[a];
+        ib[a] = g.ib[a];
+    }
+    double acc[NPR][NBB][NBB][2];
+#pragma unroll
+    for (int a = 0; a < NPR; ++a)
+#pragma unroll
+        for (int i = 0; i < NBB; ++i)
+#pragma unroll
+            for (int j = 0; j < NBB; ++j) acc[a][i][j][0] = acc[a][i][j][1] = 0.0;
+    for (std::int64_t q = q0 + warp; q < q1; q += nw) {
+        double x[ND][U][NBB];
+#pragma unroll
+        for (int d = 0; d < ND; ++d)
+#pragma unroll
+            for (int kk = 0; kk < U; ++kk) {
+                const std::int64_t row = q * 32 + 4 * kk + t;
+                const double* p = g.panel[d] + row * NB + NBB * gq;
+                if constexpr (NBB == 2) {
+                    const double2 v = row < n ? *reinterpret_cast<const double2*>(p) : make_double2(0.0, 0.0);
+                    x[d][kk][0] = v.x;
+                    x[d][kk][1] = v.y;
+                } else {
+                    x[d][kk][0] = row < n ? *p : 0.0;
+                }
+            }
+#pragma unroll
+        for (int kk = 0; kk < U; ++kk)
+#pragma unroll
+            for (int a = 0; a < NPR; ++a)
+#pragma unroll
+                for (int i = 0; i < NBB; ++i)
+#pragma unroll
+                    for (int j = 0; j < NBB; ++j) {
+                        const double fa = ND == 1 || ia[a] == 0 ? x[0][kk][i] : x[ND - 1][kk][i];
+                        const double fb = ND == 1 || ib[a] == 0 ? x[0][kk][j] : x[ND - 1][kk][j];
+                        dmma884(acc[a][i][j][0], acc[a][i][j][1], fa, fb);
+                    }
+    }
+    // this warp's sums -> red[warp], then the warps in order -> the CTA partial (row-major i, j)
+    double* mine = red + static_cast<std::size_t>(warp) * NPR * NB * NB;
+#pragma unroll
+    for (int a = 0; a < NPR; ++a)
+#pragma unroll
+        for (int i = 0; i < NBB; ++i)
+#pragma unroll
+            for (int j = 0; j < NBB; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    mine[(a * NB + NBB * gq + i) * NB + NBB * (2 * t + h) + j] = acc[a][i][j][h];
+    __syncthreads();
+    for (int e = tid; e < NPR * NB * NB; e += blockDim.x) {
+        double s = red[e];
+        for (int w = 1; w < nw; ++w) s += red[static_cast<std::size_t>(w) * NPR * NB * NB + e];
+        partial[static_cast<std::int64_t>(blockIdx.x) * NPR * NB * NB + e] = s;
+    }
+}
+
 // out_p(i, j) = sum over CTAs (lane-strided + butterfly, fixed order);
 // symmetrised pairs average both halves (gram, densela.hpp:90-97)
 __global__ void k_gram_reduce_m(GramDev g, GramOut o, int nparts, const double* __restrict__ partial) {
@@ -1563,6 +1642,40 @@ void gram(Ctx* ctx, const GramJob& job, std::int64_t n, double* partials, std::i
         g.ib[p] = idx_of(job.b[p]);
         o.out[p] = job.out[p];
         o.sym[p] = job.sym[p];
+    }
+    static const bool gram_r_on = [] {
+        const char* e = std::getenv("BE_GRAM_R");
+        return !(e && e[0] == '0');
+    }();
+    if (gram_r_on && (job.nb == 8 || job.nb == 16) && job.npairs <= 2 && g.nd <= 2 && n > 0) {  // register-direct
+        const int grid = static_cast<int>(std::max<std::int64_t>(
+            1, std::min<std::int64_t>((g.nd == 2 ? 1 : 2) * ctx->num_sms, (n + 31) / 32)));
+        const std::size_t sm = static_cast<std::size_t>(16) * job.npairs * job.nb * job.nb * sizeof(double);
+        if (static_cast<std::int64_t>(grid) * job.npairs * job.nb * job.nb <= partials_len) {
+#define BE_GRAMR(NBB, ND, NPR)                                                \
+    do {                                                                      \
+        ensure_dyn_smem(k_gram_r<NBB, ND, NPR>, sm);                          \
+        k_gram_r<NBB, ND, NPR><<<grid, 512, sm, s>>>(g, n, partials);         \
+    } while (0)
+#define BE_GRAMR_NB(NBB)                                                      \
+    if (g.nd == 1) {                                                          \
+        if (job.npairs == 1) BE_GRAMR(NBB, 1, 1); else BE_GRAMR(NBB, 1, 2);   \
+    } else {                                                                  \
+        if (job.npairs == 1) BE_GRAMR(NBB, 2, 1); else BE_GRAMR(NBB, 2, 2);   \
+    }
+            if (job.nb == 8) {
+                BE_GRAMR_NB(1)
+            } else {
+                BE_GRAMR_NB(2)
+            }
+#undef BE_GRAMR_NB
+#undef BE_GRAMR
+            const int total = job.npairs * job.nb * job.nb;
+            k_gram_reduce_m<<<(total * 32 + 255) / 256, 256, 0, s>>>(g, o, grid, partials);
+            BE_CUDA(cudaGetLastError());
+            ctx->launches += 2;
+            return;
+        }
     }
     if (job.nb % 8 == 0 && job.nb <= 32 && n > 0) {  // tensor-core kernel
         GramM q{};

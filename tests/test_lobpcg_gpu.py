@@ -300,15 +300,21 @@ def test_sygv_pivot_floor(ctx):
         abi.sygv_lowest(ctx, np.eye(2), b, 1, 1e-10)
 
 
-def test_gram_matches_numpy(ctx):
+@pytest.mark.parametrize("rows", [12345, 7])
+@pytest.mark.parametrize("nb", [8, 16, 24])
+def test_gram_matches_numpy(ctx, nb, rows):
+    """gram (densela.hpp:80-97): the register-direct kernel (nb 8, 16: one or two panels, a partial
+    last 32-row group) and the staged tensor-core kernel (nb 24), f64 against numpy; symmetrised
+    pairs are exactly symmetric."""
     torch = pytest.importorskip("torch")
-    a = torch.rand(12345, 16, dtype=torch.float64, device="cuda")
-    b = torch.rand(12345, 16, dtype=torch.float64, device="cuda")
-    g = abi.gram_dev(ctx, a.data_ptr(), b.data_ptr(), 16, 12345)
+    a = torch.rand(rows, nb, dtype=torch.float64, device="cuda")
+    b = torch.rand(rows, nb, dtype=torch.float64, device="cuda")
+    g = abi.gram_dev(ctx, a.data_ptr(), b.data_ptr(), nb, rows)
     want = a.cpu().numpy().T @ b.cpu().numpy()
     assert np.allclose(g, want, rtol=1e-12, atol=1e-10)
-    gs = abi.gram_dev(ctx, a.data_ptr(), a.data_ptr(), 16, 12345)
+    gs = abi.gram_dev(ctx, a.data_ptr(), a.data_ptr(), nb, rows)
     assert np.array_equal(gs, gs.T)
+    assert np.allclose(gs, a.cpu().numpy().T @ a.cpu().numpy(), rtol=1e-12, atol=1e-10)
 
 
 @pytest.mark.parametrize("rows", [5000, 4997])
