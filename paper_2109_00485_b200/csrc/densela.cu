@@ -1130,7 +1130,10 @@ __global__ void __launch_bounds__(256, 2) k_trsm_s(double* __restrict__ w0, doub
 // to NB + 2 doubles: the row-major copies and the row-per-lane reads are both
 // conflict-free), lane l substitutes row l in registers exactly as k_trsm_s,
 // the results go back with coalesced 16-byte stores. No CTA barrier after the
-// setup.
+// setup. gpart (one panel): the Gram W'^T W' of the result is formed on the
+// way -- DMMA over each solved tile in shared memory, warps summed in order
+// into the CTA partial [i][j] (k_gram_reduce_m) -- so CholQR's second pass
+// needs no separate read of W'.
 constexpr int kTrsmWarps = 4;
 // shared-memory loads the compiler may not hoist out of the row loop (the
 // 120 factor entries would otherwise be kept in registers and spill)
@@ -1147,7 +1150,9 @@ __device__ __forceinline__ double lds_nohoist(const double* p) {
 template <int NB>
 __global__ void __launch_bounds__(kTrsmWarps * 32) k_trsm_r(double* __restrict__ w0, double* __restrict__ w1,
                                                            const double* __restrict__ Rg, std::int64_t n, Status* st,
-                                                           int skip_if_rank, int skip_if_notpd) {
+                                                           int skip_if_rank, int skip_if_notpd,
+                                                           double* __restrict__ gpart) {
+    constexpr int NBB = NB / 8;
     constexpr int RS = NB + 2, PR = NB / 2;  // padded row stride (doubles), 16-byte pieces per row
     constexpr int RPI = 32 / PR;             // rows per coalesced warp copy
     constexpr int LPP = NB / 2;              // 16-byte pieces per lane per panel block
@@ -1197,6 +1202,11 @@ __global__ void __launch_bounds__(kTrsmWarps * 32) k_trsm_r(double* __restrict__
         cp_commit();
     };
     std::int64_t b = static_cast<std::int64_t>(blockIdx.x) * kTrsmWarps + warp;
+    double gacc[NBB][NBB][2];
+#pragma unroll
+    for (int i = 0; i < NBB; ++i)
+#pragma unroll
+        for (int j = 0; j < NBB; ++j) gacc[i][j][0] = gacc[i][j][1] = 0.0;
     issue(b, tiles);
     for (int it = 0; b < nblk; b += wstride, ++it) {
         double* t = tiles + (it & 1) * tstride;
@@ -1232,6 +1242,21 @@ __global__ void __launch_bounds__(kTrsmWarps * 32) k_trsm_r(double* __restrict__
             for (int k = 0; k < NB / 2; ++k) reinterpret_cast<double2*>(xr)[k] = make_double2(x[2 * k], x[2 * k + 1]);
         }
         __syncwarp();
+        if (gpart) {  // Gram of the solved tile (rows past n masked: their tile rows were never loaded)
+            const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const int r = 4 * kk + tq;
+                const bool ok = r0 + r < n;
+                double f[NBB];
+#pragma unroll
+                for (int i = 0; i < NBB; ++i) f[i] = ok ? t[r * RS + 8 * i + gq] : 0.0;
+#pragma unroll
+                for (int i = 0; i < NBB; ++i)
+#pragma unroll
+                    for (int j = 0; j < NBB; ++j) dmma884(gacc[i][j][0], gacc[i][j][1], f[i], f[j]);
+            }
+        }
         for (int p = 0; p < np; ++p) {
             double* w = (p == 0 ? w0 : w1) + r0 * NB;
 #pragma unroll
@@ -1245,6 +1270,23 @@ __global__ void __launch_bounds__(kTrsmWarps * 32) k_trsm_r(double* __restrict__
         __syncwarp();  // this buffer is refilled two blocks on
     }
     cp_wait<0>();
+    if (gpart) {  // warps in order -> the CTA partial (row-major i, j)
+        __syncthreads();
+        double* red = sbuf;  // [warp][NB][NB]
+        const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+        for (int i = 0; i < NBB; ++i)
+#pragma unroll
+            for (int j = 0; j < NBB; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) red[(warp * NB + 8 * i + gq) * NB + 8 * j + 2 * tq + h] = gacc[i][j][h];
+        __syncthreads();
+        for (int e = tid; e < NB * NB; e += blockDim.x) {
+            double sum = red[e];
+            for (int w = 1; w < kTrsmWarps; ++w) sum += red[w * NB * NB + e];
+            gpart[static_cast<std::int64_t>(blockIdx.x) * NB * NB + e] = sum;
+        }
+    }
 }
 
 // -------------------------------------------------------------------- trsm
@@ -1927,10 +1969,10 @@ void trsm(Ctx* ctx, double* w0, double* w1, const double* R, int nb, std::int64_
             1, std::min<std::int64_t>(static_cast<std::int64_t>(per_sm) * ctx->num_sms, (nblk + kTrsmWarps - 1) / kTrsmWarps)));
         if (nb == 8) {
             ensure_dyn_smem(k_trsm_r<8>, sm);
-            k_trsm_r<8><<<grid, kTrsmWarps * 32, sm, s>>>(w0, w1, R, n, st, skip_if_rank, skip_if_notpd);
+            k_trsm_r<8><<<grid, kTrsmWarps * 32, sm, s>>>(w0, w1, R, n, st, skip_if_rank, skip_if_notpd, nullptr);
         } else {
             ensure_dyn_smem(k_trsm_r<16>, sm);
-            k_trsm_r<16><<<grid, kTrsmWarps * 32, sm, s>>>(w0, w1, R, n, st, skip_if_rank, skip_if_notpd);
+            k_trsm_r<16><<<grid, kTrsmWarps * 32, sm, s>>>(w0, w1, R, n, st, skip_if_rank, skip_if_notpd, nullptr);
         }
         BE_CUDA(cudaGetLastError());
         ++ctx->launches;
@@ -1973,6 +2015,39 @@ void trsm(Ctx* ctx, double* w0, double* w1, const double* R, int nb, std::int64_
 #undef BE_TRSM
     BE_CUDA(cudaGetLastError());
     ++ctx->launches;
+}
+
+bool trsm_gram(Ctx* ctx, double* w, const double* R, int nb, std::int64_t n, Status* st, double* gram_out,
+               double* partials, std::int64_t partials_len, cudaStream_t s) {
+    static const bool on = [] {
+        const char* e1 = std::getenv("BE_TRSM_R");
+        const char* e2 = std::getenv("BE_TRSM_GRAM");
+        return !(e1 && e1[0] == '0') && !(e2 && e2[0] == '0');
+    }();
+    if (!on || !(nb == 8 || nb == 16) || n <= 0) return false;
+    const std::size_t sm = static_cast<std::size_t>(kTrsmWarps) * 2 * 32 * (nb + 2) * sizeof(double);
+    const int per_sm = static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(6, (220u * 1024) / (sm + 2048))));
+    const std::int64_t nblk = (n + 31) / 32;
+    const int grid = static_cast<int>(std::max<std::int64_t>(
+        1, std::min<std::int64_t>(static_cast<std::int64_t>(per_sm) * ctx->num_sms, (nblk + kTrsmWarps - 1) / kTrsmWarps)));
+    if (static_cast<std::int64_t>(grid) * nb * nb > partials_len) return false;
+    if (nb == 8) {
+        ensure_dyn_smem(k_trsm_r<8>, sm);
+        k_trsm_r<8><<<grid, kTrsmWarps * 32, sm, s>>>(w, nullptr, R, n, st, 1, 0, partials);
+    } else {
+        ensure_dyn_smem(k_trsm_r<16>, sm);
+        k_trsm_r<16><<<grid, kTrsmWarps * 32, sm, s>>>(w, nullptr, R, n, st, 1, 0, partials);
+    }
+    GramDev g{};
+    g.npairs = 1;
+    g.nb = nb;
+    GramOut o{};
+    o.out[0] = gram_out;
+    o.sym[0] = 1;
+    k_gram_reduce_m<<<(nb * nb * 32 + 255) / 256, 256, 0, s>>>(g, o, grid, partials);
+    BE_CUDA(cudaGetLastError());
+    ctx->launches += 2;
+    return true;
 }
 
 void qr_chol(Ctx* ctx, double* B, double* R, int nb, Status* st, cudaStream_t s) {

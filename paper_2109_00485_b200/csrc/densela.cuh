@@ -65,6 +65,11 @@ void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s);
 // skipped when st->rank_deficient (skip_if_rank) / st->not_pd (skip_if_notpd).
 void trsm(Ctx* ctx, double* w0, double* w1, const double* R, int nb, std::int64_t n, Status* st, int skip_if_rank,
           int skip_if_notpd, cudaStream_t s);
+// trsm of one panel (skip_if_rank) that also forms gram_out = W'^T W' of the
+// result on the way (CholQR's next pass); false when the fused kernel does
+// not apply (nb other than 8 / 16) -- then nothing was launched.
+bool trsm_gram(Ctx* ctx, double* w, const double* R, int nb, std::int64_t n, Status* st, double* gram_out,
+               double* partials, std::int64_t partials_len, cudaStream_t s);
 
 // Floored Cholesky with the qr_of_transpose retry logic (densela.hpp:412-445):
 // B (nb x nb) -> R; updates st->qr_failures / st->rank_deficient.

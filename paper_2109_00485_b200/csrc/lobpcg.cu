@@ -247,10 +247,13 @@ struct Solver {
     // qr_of_transpose (densela.hpp:412-445); returns false on RankDeficient
     bool qr(double* A, bool check) {
         reset_qr_flags();
+        bool have_gram = false;  // the first pass's trsm formed the second pass's Gram
         for (int pass = 0; pass < 2; ++pass) {
-            gram1(A, A, 1, Bq);
+            if (!have_gram) gram1(A, A, 1, Bq);
             dla::qr_chol(ctx, Bq, Rq, nb, st.get(), s);
-            dla::trsm(ctx, A, nullptr, Rq, nb, n, st.get(), 1, 0, s);
+            have_gram = pass == 0 && dla::trsm_gram(ctx, A, Rq, nb, n, st.get(), Bq, partials.get(), partials_len, s);
+            if (have_gram) allreduce(Bq, nb * nb);
+            else dla::trsm(ctx, A, nullptr, Rq, nb, n, st.get(), 1, 0, s);
         }
         if (!check) return true;
         sync_status();
