@@ -80,6 +80,8 @@ def args_parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gate", action="store_true", help="skip the correctness gate against the reference SpMM")
     ap.add_argument("--dist", action="store_true", help="run the distributed (NCCL) path even on one rank")
+    ap.add_argument("--partition", choices=["2d", "slabs"], default="2d",
+                    help="multi-GPU SpMM partition: nnz-balanced 2-D tiles (default) or block-row slabs")
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--values", choices=["f32", "f64"], default="f32",
@@ -374,9 +376,13 @@ def run_dist(a, rank, world, local):
         return t.cpu().numpy()
 
     t0 = time.time()
-    rp = weak.rank_problem(ctx, comm, p, rank, world, precond, allreduce_sum)
+    rp = weak.rank_problem(ctx, comm, p, rank, world, precond, allreduce_sum, partition=a.partition)
     t_setup = time.time() - t0
-    op, tiles, cuts, slabs, lo, hi = rp["op"], rp["tiles"], rp["cuts"], rp["slabs"], rp["lo"], rp["hi"]
+    op, tiles, cuts, lo, hi = rp["op"], rp["tiles"], rp["cuts"], rp["lo"], rp["hi"]
+    # this rank's share of the matrix: its 2-D tile (r0, r1, c0, c1) or its block-row slab
+    share = rp["rect"] if rp["rect"] is not None else rp["slabs"]
+    shares = allreduce_sum(np.eye(world)[rank][:, None] * np.asarray(share, np.float64)[None, :len(share)]) \
+        if rp["rect"] is not None else np.asarray(rp["slabs"])
     nnz_local = rp["nnz_local"]
     stats = allreduce_sum(np.array([float(nnz_local), float(rp["tile_entries"])]))
     nnz_tot, ent_tot = int(stats[0]), int(stats[1])
@@ -455,7 +461,8 @@ def run_dist(a, rank, world, local):
         "config": {"workload": f"t1 weak-scaled x{world}: n={n}, half-nnz={nnz_tot}, nev={a.nev}, block k={a.nb}, "
                                f"precond {a.precond}", "n": n, "nnz": nnz_tot, "nb": a.nb, "nev": a.nev,
                    "precond": precond, "generator": cfg, "parallelism": f"dist{world} (row panels + nnz-balanced "
-                   "SpMM slabs, NCCL allgather/reduce-scatter/allreduce)",
+                   f"SpMM {'2-D tiles' if a.partition == '2d' else 'slabs'}, segment-wise NCCL send/recv exchange, "
+                   "allreduce)",
                    "l2": "inputs larger than L2 (matrix stream 8 B/nnz >> 126 MB)", "values": "f32", "panels": "f64"},
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                      "traffic": None, "kernel": "distributed sym_spmm apply on rank 0 (slab SpMM + exchange)",
@@ -472,7 +479,8 @@ def run_dist(a, rank, world, local):
                    "precond_ms": 1e3 * float(np.mean(rec[:, 1])) if len(rec) else None,
                    "setup_s": {"generate_and_upload": t_setup}, "parallelism": f"dist{world}",
                    "comm": {"backend": info["backend"], "calls": info["calls"], "bytes_rank0": info["bytes"]},
-                   "cuts": [int(c) for c in cuts], "slabs": [int(c) for c in slabs]},
+                   "cuts": [int(c) for c in cuts], "partition": a.partition,
+                   "shares": np.asarray(shares).astype(np.int64).tolist()},
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

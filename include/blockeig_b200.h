@@ -202,6 +202,14 @@ be_status be_clustered_diag(const be_cluster_params* p, const double* rowabs, in
                             double* diag);
 /* expected stored nonzeros per CSB block row (the slab weights, no generation) */
 be_status be_clustered_weights(const be_cluster_params* p, int64_t* weights, int64_t* nblk);
+/* Expected stored entries of every lower block (row-major nblk x nblk; weights NULL: nblk only) --
+ * the weights of be_dist_tiles2d -- and one 2-D tile of the clustered matrix: block rows
+ * [brow_begin, brow_end) x block columns [bcol_begin, bcol_end), exactly the whole-matrix
+ * generator's entries there; rowabs / tile offsets as be_generate_clustered_part. */
+be_status be_clustered_block_weights(const be_cluster_params* p, int64_t* weights, int64_t* nblk);
+be_status be_generate_clustered_tile(const be_cluster_params* p, int64_t brow_begin, int64_t brow_end,
+                                     int64_t bcol_begin, int64_t bcol_end, be_csb** out, double** rowabs,
+                                     int64_t** tile_offsets, int64_t* n_tile_offsets);
 
 /* ------------------------------------------------------------------------- */
 /* Device context and the symmetric operator (SymmetricOperator,             */
@@ -409,6 +417,13 @@ be_status be_dist_rows(const int64_t* bounds, int64_t nbounds, int world, int64_
 be_status be_dist_touched(const be_csb_view* L_slab, const int64_t* cuts, const int* owner, int world,
                           uint8_t* touched);
 be_status be_dist_balance(const int64_t* weights, int64_t nitems, int world, int64_t* cuts);
+/* nnz-balanced 2-D tiles (north_star; replaces partition_matrix's fixed triangular layout,
+ * dist.hpp:113-198, for any rank count): recursive coordinate bisection of the lower block grid.
+ * weights[bi * nblk + bj] = stored entries of block (bi, bj), bi >= bj; bounds the nblk + 1 block
+ * boundaries (the cut side is the longer one in matrix rows). rects: world x (r0, r1, c0, c1),
+ * rank r owns the stored blocks with r0 <= bi < r1, c0 <= bj < c1 (empty: all zero). The
+ * rectangles are disjoint and cover every non-empty block; see DESIGN.md §6 for the rule. */
+be_status be_dist_tiles2d(const int64_t* weights, int64_t nblk, const int64_t* bounds, int world, int64_t* rects);
 
 /* Distributed symmetric operator: L_slab is this rank's share of the global
  * strictly-lower CSB (global coordinates and blocks; the ranks' slabs are

@@ -224,6 +224,30 @@ class Csb:
         sl._parent = self  # keeps a library-owned parent alive
         return sl
 
+    def block_weights(self) -> np.ndarray:
+        """Stored nonzeros per CSB block, (nrowblks, ncolblks) (the 2-D tile weights)."""
+        return self.block_nnz.reshape(self.nrowblks, self.ncolblks).copy()
+
+    def rect(self, r0: int, r1: int, c0: int, c1: int) -> "Csb":
+        """The blocks (bi, bj) with r0 <= bi < r1 and c0 <= bj < c1 (one rank's 2-D tile) as a CSB
+        of the same global shape and blocks (entries elsewhere absent)."""
+        nb = self.ncolblks
+        bn = self.block_nnz.reshape(self.nrowblks, nb)
+        keep = np.zeros_like(bn)
+        keep[r0:r1, c0:c1] = bn[r0:r1, c0:c1]
+        parts = []
+        for bi in range(r0, r1):
+            if c1 > c0:
+                lo = int(self.block_nnz_offsets[bi * nb + c0])
+                hi = lo + int(bn[bi, c0:c1].sum())
+                if hi > lo:
+                    parts.append(np.arange(lo, hi))
+        idx = np.concatenate(parts) if parts else np.zeros(0, np.int64)
+        off = np.zeros(keep.size, np.int64)
+        np.cumsum(keep.ravel()[:-1], out=off[1:])
+        return Csb(self.nrows, self.ncols, self.row_offsets, self.col_offsets, keep.ravel(), off,
+                   self.local_rows[idx], self.local_cols[idx], self.values[idx])
+
     def to_triples(self) -> np.ndarray:
         out = np.zeros(self.nnz, dtype=TRIPLE_DTYPE)
         v = self.view()
@@ -409,6 +433,33 @@ def generate_clustered_part(params: ClusterParams, brow_begin: int, brow_end: in
     return Csb._from_handle(h), rowabs, toff
 
 
+def generate_clustered_tile(params: ClusterParams, rows, cols):
+    """One 2-D tile of the clustered matrix: block rows [rows[0], rows[1]) x block columns
+    [cols[0], cols[1]) (global shape; exactly the whole-matrix generator's entries there):
+    (csb, rowabs contribution over all n rows, tile offsets)."""
+    h = C.c_void_p()
+    rp = C.POINTER(C.c_double)()
+    tp = C.POINTER(C.c_int64)()
+    nt = C.c_int64()
+    check(lib().be_generate_clustered_tile(C.byref(params), C.c_int64(rows[0]), C.c_int64(rows[1]),
+                                           C.c_int64(cols[0]), C.c_int64(cols[1]), C.byref(h), C.byref(rp),
+                                           C.byref(tp), C.byref(nt)))
+    rowabs = np.ctypeslib.as_array(rp, shape=(params.n,)).copy()
+    toff = np.ctypeslib.as_array(tp, shape=(nt.value,)).copy()
+    lib().be_free_buffer(rp)
+    lib().be_free_buffer(tp)
+    return Csb._from_handle(h), rowabs, toff
+
+
+def clustered_block_weights(params: ClusterParams) -> np.ndarray:
+    """Expected stored entries of every lower block, (nblk, nblk) (the 2-D tile weights)."""
+    nb = C.c_int64()
+    check(lib().be_clustered_block_weights(C.byref(params), None, C.byref(nb)))
+    w = np.zeros(nb.value * nb.value, np.int64)
+    check(lib().be_clustered_block_weights(C.byref(params), _p(w), C.byref(nb)))
+    return w.reshape(nb.value, nb.value)
+
+
 def clustered_diag(params: ClusterParams, rowabs, row_begin: int, row_end: int) -> np.ndarray:
     r = np.ascontiguousarray(rowabs, dtype=np.float64)
     out = np.zeros(row_end - row_begin)
@@ -550,6 +601,19 @@ def dist_balance(weights, world: int) -> np.ndarray:
     w = np.ascontiguousarray(weights, dtype=np.int64)
     out = np.zeros(world + 1, np.int64)
     check(lib().be_dist_balance(_p(w), C.c_int64(len(w)), C.c_int(world), _p(out)))
+    return out
+
+
+def dist_tiles2d(block_weights, bounds, world: int) -> np.ndarray:
+    """nnz-balanced 2-D tiles (be_dist_tiles2d): (world, 4) rectangles (r0, r1, c0, c1) of CSB
+    blocks, rank r owning the stored blocks r0 <= bi < r1, c0 <= bj < c1."""
+    w = np.ascontiguousarray(block_weights, dtype=np.int64)
+    nblk = w.shape[0]
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    if w.shape != (nblk, nblk) or len(b) != nblk + 1:
+        raise DimensionMismatch("dist_tiles2d: weights must be (nblk, nblk) with nblk + 1 bounds")
+    out = np.zeros((world, 4), np.int64)
+    check(lib().be_dist_tiles2d(_p(w), C.c_int64(nblk), _p(b), C.c_int(world), _p(out)))
     return out
 
 

@@ -6,6 +6,10 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <csignal>
+#include <cstdlib>
+#include <execinfo.h>
+#include <unistd.h>
 #include <cstring>
 #include <sstream>
 #include <tuple>
@@ -288,6 +292,33 @@ be_status be_generate_clustered_part(const be_cluster_params* p, int64_t brow_be
     });
 }
 
+be_status be_generate_clustered_tile(const be_cluster_params* p, int64_t brow_begin, int64_t brow_end,
+                                     int64_t bcol_begin, int64_t bcol_end, be_csb** out, double** rowabs,
+                                     int64_t** tile_offsets, int64_t* n_tile_offsets) {
+    return guard([&] {
+        if (!p || !out || !rowabs || !tile_offsets || !n_tile_offsets) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        std::vector<double> r;
+        std::vector<int64_t> t;
+        auto m = be::generate_clustered_part(*p, brow_begin, brow_end, false, r, t, bcol_begin, bcol_end);
+        *rowabs = static_cast<double*>(std::malloc(r.size() * sizeof(double)));
+        std::memcpy(*rowabs, r.data(), r.size() * sizeof(double));
+        *tile_offsets = static_cast<int64_t*>(std::malloc(t.size() * sizeof(int64_t)));
+        std::memcpy(*tile_offsets, t.data(), t.size() * sizeof(int64_t));
+        *n_tile_offsets = static_cast<int64_t>(t.size());
+        *out = new be_csb{std::move(m)};
+    });
+}
+
+be_status be_clustered_block_weights(const be_cluster_params* p, int64_t* weights, int64_t* nblk) {
+    return guard([&] {
+        if (!p || !nblk) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        int64_t nb = 0;
+        const auto w = be::clustered_block_weights(*p, nb);
+        *nblk = nb;
+        if (weights) std::memcpy(weights, w.data(), w.size() * sizeof(int64_t));
+    });
+}
+
 be_status be_clustered_diag(const be_cluster_params* p, const double* rowabs, int64_t row_begin, int64_t row_end,
                             double* diag) {
     return guard([&] {
@@ -305,6 +336,27 @@ be_status be_clustered_weights(const be_cluster_params* p, int64_t* weights, int
         if (weights) std::memcpy(weights, w.data(), w.size() * sizeof(int64_t));
     });
 }
+
+// BE_SEGV_TRACE=1: native backtrace on SIGSEGV/SIGABRT (addresses resolve with addr2line -e the .so)
+namespace {
+void be_segv_handler(int sig) {
+    void* frames[64];
+    const int n = backtrace(frames, 64);
+    const char msg[] = "blockeig_b200: native backtrace\n";
+    (void)!write(2, msg, sizeof(msg) - 1);
+    backtrace_symbols_fd(frames, n, 2);
+    std::signal(sig, SIG_DFL);
+    std::raise(sig);
+}
+struct SegvTrace {
+    SegvTrace() {
+        if (std::getenv("BE_SEGV_TRACE")) {
+            std::signal(SIGSEGV, be_segv_handler);
+            std::signal(SIGABRT, be_segv_handler);
+        }
+    }
+} g_segv_trace;
+}  // namespace
 
 // ------------------------------------------------------------------ context
 be_status be_ctx_create(int device, be_ctx** out) {
@@ -623,6 +675,16 @@ be_status be_dist_balance(const int64_t* weights, int64_t nitems, int world, int
         if ((!weights && nitems > 0) || !cuts || nitems < 0) be::fail(BE_ERR_BAD_PARAMS, "be_dist_balance: bad arguments");
         const auto c = be::dist_balance(weights, nitems, world);
         std::memcpy(cuts, c.data(), c.size() * sizeof(int64_t));
+    });
+}
+
+be_status be_dist_tiles2d(const int64_t* weights, int64_t nblk, const int64_t* bounds, int world, int64_t* rects) {
+    return guard([&] {
+        if (!weights || !bounds || !rects || nblk < 1) be::fail(BE_ERR_BAD_PARAMS, "be_dist_tiles2d: bad arguments");
+        for (int64_t i = 1; i <= nblk; ++i)
+            if (bounds[i] <= bounds[i - 1]) be::fail(BE_ERR_BAD_PARAMS, "be_dist_tiles2d: boundaries must be strictly increasing");
+        const auto r = be::dist_tiles2d(weights, nblk, bounds, world);
+        std::memcpy(rects, r.data(), r.size() * sizeof(int64_t));
     });
 }
 

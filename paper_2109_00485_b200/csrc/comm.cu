@@ -279,7 +279,7 @@ class LocalComm final : public Comm {
 
   private:
     // publish -> barrier -> wait peers' ready -> body -> record done ->
-    // barrier -> wait peers' done (so no rank reuses a buffer a peer still reads)
+    // barrier -> wait peers' done (so no rank reuses a buffer a peer still reads) -> barrier
     template <class F>
     void run(const void* send, void* recv, cudaStream_t s, F&& body) {
         if (world > kMaxLocalRanks) fail(BE_ERR_BAD_PARAMS, "local comm: more than 16 ranks");
@@ -304,6 +304,10 @@ class LocalComm final : public Comm {
         g_->barrier();
         for (int q = 0; q < world; ++q)
             if (q != rank) BE_CUDA(cudaStreamWaitEvent(s, sl[static_cast<std::size_t>(q)].done, 0));
+        // every rank has enqueued its waits on the peers' events before any rank leaves: a rank
+        // that returned first could otherwise destroy its events (comm close) or re-record them
+        // while a slower peer is still about to wait on them
+        g_->barrier();
         ++calls;
     }
 

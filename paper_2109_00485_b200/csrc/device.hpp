@@ -184,6 +184,7 @@ std::unique_ptr<Op> op_create_dist(Ctx* ctx, Comm* comm, const be_csb_view& L, c
 // equal-rows ownership on block boundaries / contiguous weight balance
 std::vector<index_t> dist_rows(const index_t* bounds, index_t nbounds, int world);
 std::vector<index_t> dist_balance(const index_t* weights, index_t nitems, int world);
+std::vector<index_t> dist_tiles2d(const index_t* w, index_t nblk, const index_t* bounds, int world);
 void op_apply(Op* op, const void* X, void* Y, index_t nrows, int nb, int panel_prec, int mode, cudaStream_t s);
 
 }  // namespace be

@@ -662,7 +662,9 @@ static ClusterPlan make_plan(const be_cluster_params& p) {
 // Block rows [b0, b1) of the clustered matrix as a CSB of the global shape;
 // diag_only keeps only the diagonal blocks (a rank's preconditioner tiles).
 // The entries are exactly those of the whole-matrix generator.
-static std::unique_ptr<CsbHost> clustered_rows(const ClusterPlan& plan, index_t b0, index_t b1, bool diag_only, int nw) {
+static std::unique_ptr<CsbHost> clustered_rows(const ClusterPlan& plan, index_t b0, index_t b1, bool diag_only, int nw,
+                                               index_t c0 = 0, index_t c1 = -1) {
+    if (c1 < 0) c1 = plan.nblk;
     const auto& p = plan.p;
     const index_t nblk = plan.nblk;
     const auto& B = plan.bounds;
@@ -674,7 +676,9 @@ static std::unique_ptr<CsbHost> clustered_rows(const ClusterPlan& plan, index_t 
     m->col_offsets = B;
     m->block_nnz.assign(static_cast<std::size_t>(nblk * nblk), 0);
     m->block_nnz_offsets.assign(static_cast<std::size_t>(nblk * nblk), 0);
-    auto wanted = [&](index_t bi, index_t bj) { return plan.block_on(bi, bj) && (!diag_only || bi == bj); };
+    auto wanted = [&](index_t bi, index_t bj) {
+        return bj >= c0 && bj < c1 && plan.block_on(bi, bj) && (!diag_only || bi == bj);
+    };
     // pass 1: counts per block (gap stream only)
     parallel_for_dynamic(nw, b1 - b0, [&](index_t q, int) {
         const index_t bi = b0 + q;
@@ -765,11 +769,14 @@ std::unique_ptr<CsbHost> generate_clustered(const be_cluster_params& p, std::vec
 }
 
 std::unique_ptr<CsbHost> generate_clustered_part(const be_cluster_params& p, index_t b0, index_t b1, bool diag_only,
-                                                 std::vector<double>& rowabs, std::vector<index_t>& tile_offsets) {
+                                                 std::vector<double>& rowabs, std::vector<index_t>& tile_offsets,
+                                                 index_t c0, index_t c1) {
     const int nw = p.threads > 0 ? p.threads : hw_threads();
     const ClusterPlan plan = make_plan(p);
     if (b0 < 0 || b1 < b0 || b1 > plan.nblk) fail(BE_ERR_BAD_PARAMS, "generate_clustered_part: bad block-row range");
-    auto m = clustered_rows(plan, b0, b1, diag_only, nw);
+    if (c1 < 0) c1 = plan.nblk;
+    if (c0 < 0 || c1 < c0 || c1 > plan.nblk) fail(BE_ERR_BAD_PARAMS, "generate_clustered_part: bad block-column range");
+    auto m = clustered_rows(plan, b0, b1, diag_only, nw, c0, c1);
     std::vector<double> rsum, csum;
     abs_sums(*m, b0, b1, rsum, csum, nw);
     rowabs.resize(static_cast<std::size_t>(p.n));
@@ -777,6 +784,32 @@ std::unique_ptr<CsbHost> generate_clustered_part(const be_cluster_params& p, ind
     std::mt19937_64 trng(p.seed + 0x7157);
     tile_offsets = draw_tile_offsets(p.n, p.block_extent, p.tile_min, p.tile_max, trng);
     return m;
+}
+
+// Expected stored entries of every lower block (bi, bj), row-major nblk x nblk (the 2-D tile
+// weights; the block-row weights below are their row sums up to rounding).
+std::vector<index_t> clustered_block_weights(const be_cluster_params& p, index_t& nblk_out) {
+    const ClusterPlan plan = make_plan(p);
+    const auto& B = plan.bounds;
+    const index_t nblk = plan.nblk;
+    nblk_out = nblk;
+    std::vector<index_t> w(static_cast<std::size_t>(nblk * nblk), 0);
+    auto ntiles_of = [&](index_t len) { return (len + p.tile - 1) / p.tile; };
+    for (index_t bi = 0; bi < nblk; ++bi) {
+        const index_t br = B[bi + 1] - B[bi];
+        double e = 0.0;  // the diagonal block
+        for (index_t a = 0; a < ntiles_of(br); ++a) {
+            const double t = static_cast<double>(std::min(p.tile, br - a * p.tile));
+            e += t * (t - 1) / 2 * p.fill;
+            for (index_t b = 0; b < a; ++b) e += t * static_cast<double>(std::min(p.tile, br - b * p.tile)) * p.fill * plan.p_tile;
+        }
+        w[static_cast<std::size_t>(bi * nblk + bi)] = static_cast<index_t>(std::llround(e));
+        for (index_t bj = 0; bj < bi; ++bj)
+            if (plan.block_on(bi, bj))
+                w[static_cast<std::size_t>(bi * nblk + bj)] = static_cast<index_t>(
+                    std::llround(static_cast<double>(br) * static_cast<double>(B[bj + 1] - B[bj]) * p.fill * plan.p_tile));
+    }
+    return w;
 }
 
 std::vector<index_t> clustered_block_row_weights(const be_cluster_params& p) {

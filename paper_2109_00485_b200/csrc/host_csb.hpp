@@ -76,9 +76,12 @@ std::unique_ptr<CsbHost> generate_clustered(const be_cluster_params& p, std::vec
                                             std::vector<index_t>& tile_offsets);
 // block rows [b0, b1) only (diag_only: their diagonal blocks only); rowabs
 // (n) receives this part's contribution to sum |row| of every row
+// [c0, c1): block columns kept (default: all; a 2-D tile of the lower triangle)
 std::unique_ptr<CsbHost> generate_clustered_part(const be_cluster_params& p, index_t b0, index_t b1, bool diag_only,
-                                                 std::vector<double>& rowabs, std::vector<index_t>& tile_offsets);
+                                                 std::vector<double>& rowabs, std::vector<index_t>& tile_offsets,
+                                                 index_t c0 = 0, index_t c1 = -1);
 double clustered_diag_value(const be_cluster_params& p, index_t i, double rowabs);
 std::vector<index_t> clustered_block_row_weights(const be_cluster_params& p);
+std::vector<index_t> clustered_block_weights(const be_cluster_params& p, index_t& nblk);
 
 }  // namespace be

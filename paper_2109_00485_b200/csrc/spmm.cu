@@ -44,6 +44,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <type_traits>
 #include <cmath>
 #include <cstdlib>
@@ -1913,6 +1914,72 @@ std::vector<index_t> dist_rows(const index_t* b, index_t nbounds, int world) {
     std::vector<index_t> cuts(static_cast<std::size_t>(world) + 1);
     for (int p = 0; p <= world; ++p) cuts[static_cast<std::size_t>(p)] = b[k[static_cast<std::size_t>(p)]];
     return cuts;
+}
+
+// nnz-balanced 2-D tiles (north_star's partition): recursive coordinate bisection of the lower
+// block grid. w[bi * nblk + bj] = stored entries of CSB block (bi, bj) (bi >= bj; the upper part
+// is ignored). A rectangle of block rows [r0, r1) x block columns [c0, c1) is first shrunk to the
+// bounding box of its non-empty blocks; holding p > 1 ranks it is cut in two -- the first part
+// (lower rows or columns) gets p / 2 ranks with the lower rank numbers, the second p - p / 2 --
+// across its longer side in matrix rows (rows on ties; a side of one block is never cut) at the
+// line k in [1, L - 1] minimising |W(first k lines) * p - W(rect) * (p / 2)| (the smaller k on
+// ties). An empty rectangle, or a single block, goes whole to its first rank; the other ranks get
+// empty rectangles (0, 0, 0, 0). A rank's tiles touch only the panel segments of its own row and
+// column ranges instead of the whole prefix a block-row slab reaches into. out: world x (r0, r1,
+// c0, c1).
+std::vector<index_t> dist_tiles2d(const index_t* w, index_t nblk, const index_t* bounds, int world) {
+    if (world < 1) fail(BE_ERR_BAD_PARAMS, "dist_tiles2d: world must be positive");
+    if (nblk < 1) fail(BE_ERR_BAD_PARAMS, "dist_tiles2d: empty block grid");
+    for (index_t i = 0; i < nblk * nblk; ++i)
+        if (w[i] < 0) fail(BE_ERR_BAD_PARAMS, "dist_tiles2d: negative weight");
+    std::vector<index_t> out(static_cast<std::size_t>(world) * 4, 0);
+    auto W = [&](index_t bi, index_t bj) { return bj <= bi ? w[bi * nblk + bj] : index_t{0}; };
+    std::function<void(index_t, index_t, index_t, index_t, int, int)> rec =
+        [&](index_t r0, index_t r1, index_t c0, index_t c1, int p, int rank0) {
+            index_t rl = r1, rh = r0, cl = c1, ch = c0;
+            for (index_t bi = r0; bi < r1; ++bi)
+                for (index_t bj = c0; bj < c1; ++bj)
+                    if (W(bi, bj) > 0) {
+                        rl = std::min(rl, bi), rh = std::max(rh, bi + 1);
+                        cl = std::min(cl, bj), ch = std::max(ch, bj + 1);
+                    }
+            if (rl >= rh) return;  // empty: every rank of it keeps (0, 0, 0, 0)
+            r0 = rl, r1 = rh, c0 = cl, c1 = ch;
+            if (p == 1 || (r1 - r0 < 2 && c1 - c0 < 2)) {
+                auto* o = out.data() + static_cast<std::size_t>(rank0) * 4;
+                o[0] = r0, o[1] = r1, o[2] = c0, o[3] = c1;
+                return;
+            }
+            const bool by_rows = c1 - c0 < 2 || (r1 - r0 >= 2 && bounds[r1] - bounds[r0] >= bounds[c1] - bounds[c0]);
+            const index_t L = by_rows ? r1 - r0 : c1 - c0;
+            std::vector<__int128> line(static_cast<std::size_t>(L), 0);
+            __int128 tot = 0;
+            for (index_t bi = r0; bi < r1; ++bi)
+                for (index_t bj = c0; bj < c1; ++bj) {
+                    const index_t x = W(bi, bj);
+                    line[static_cast<std::size_t>(by_rows ? bi - r0 : bj - c0)] += x;
+                    tot += x;
+                }
+            const int pl = p / 2;
+            const __int128 target = tot * pl;
+            __int128 pre = 0, bestd = -1;
+            index_t best = 1;
+            for (index_t k = 1; k < L; ++k) {
+                pre += line[static_cast<std::size_t>(k - 1)];
+                __int128 d = pre * p - target;
+                if (d < 0) d = -d;
+                if (bestd < 0 || d < bestd) bestd = d, best = k;
+            }
+            if (by_rows) {
+                rec(r0, r0 + best, c0, c1, pl, rank0);
+                rec(r0 + best, r1, c0, c1, p - pl, rank0 + pl);
+            } else {
+                rec(r0, r1, c0, c0 + best, pl, rank0);
+                rec(r0, r1, c0 + best, c1, p - pl, rank0 + pl);
+            }
+        };
+    rec(0, nblk, 0, nblk, world, 0);
+    return out;
 }
 
 // Contiguous weight balance: cut p = first item index whose prefix weight

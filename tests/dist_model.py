@@ -70,3 +70,57 @@ def slab_partial_spmm(rows, cols, vals, x_full_padded, cuts, nb):
     np.add.at(y, pr, vals[:, None] * x[pc])
     np.add.at(y, pc, vals[:, None] * x[pr])
     return y
+
+
+def dist_tiles2d(w, bounds, world):
+    """Recursive coordinate bisection of the lower block grid (be_dist_tiles2d), restated:
+    shrink to the bounding box of the non-empty blocks; p > 1 ranks: cut the longer side
+    (matrix rows, rows on ties, a one-block side never) at the line k in [1, L-1] minimising
+    |W(first k lines) p - W(rect) (p // 2)| (smaller k on ties), first part p // 2 ranks."""
+    w = np.tril(np.asarray(w, dtype=np.int64))
+    b = [int(x) for x in bounds]
+    out = np.zeros((world, 4), np.int64)
+
+    def rec(r0, r1, c0, c1, p, rank0):
+        sub = w[r0:r1, c0:c1]
+        nzr, nzc = np.nonzero(sub.sum(axis=1))[0], np.nonzero(sub.sum(axis=0))[0]
+        nz = np.nonzero(sub)
+        if len(nz[0]) == 0:
+            return
+        r0, r1 = r0 + int(nz[0].min()), r0 + int(nz[0].max()) + 1
+        c0, c1 = c0 + int(nz[1].min()), c0 + int(nz[1].max()) + 1
+        del nzr, nzc
+        if p == 1 or (r1 - r0 < 2 and c1 - c0 < 2):
+            out[rank0] = (r0, r1, c0, c1)
+            return
+        by_rows = c1 - c0 < 2 or (r1 - r0 >= 2 and b[r1] - b[r0] >= b[c1] - b[c0])
+        sub = w[r0:r1, c0:c1]
+        line = [int(x) for x in (sub.sum(axis=1) if by_rows else sub.sum(axis=0))]
+        tot, pl = sum(line), p // 2
+        pre, best, bestd = 0, 1, None
+        for k in range(1, len(line)):
+            pre += line[k - 1]
+            d = abs(pre * p - tot * pl)
+            if bestd is None or d < bestd:
+                best, bestd = k, d
+        if by_rows:
+            rec(r0, r0 + best, c0, c1, pl, rank0)
+            rec(r0 + best, r1, c0, c1, p - pl, rank0 + pl)
+        else:
+            rec(r0, r1, c0, c0 + best, pl, rank0)
+            rec(r0, r1, c0 + best, c1, p - pl, rank0 + pl)
+
+    rec(0, w.shape[0], 0, w.shape[0], world, 0)
+    return out
+
+
+def touched_segments(w, bounds, cuts, rect):
+    """Panel segments (cuts) whose rows a rectangle's non-empty blocks read or write."""
+    r0, r1, c0, c1 = (int(x) for x in rect)
+    q = set()
+    for bi in range(r0, r1):
+        for bj in range(c0, min(c1, bi + 1)):
+            if w[bi][bj] > 0:
+                q.add(int(np.searchsorted(cuts, bounds[bi], side="right") - 1))
+                q.add(int(np.searchsorted(cuts, bounds[bj], side="right") - 1))
+    return q

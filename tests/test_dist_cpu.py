@@ -244,3 +244,73 @@ def test_csb1_slab_loader(tmp_path):
         lo, hi = int(b[b0]), int(b[b1])
         if hi > lo:
             assert np.array_equal(d, s.diag[lo:hi])
+
+
+# ---- nnz-balanced 2-D tiles (be_dist_tiles2d) -----------------------------------------------
+def _lower_weights(rng, nblk, kind):
+    if kind == "uniform":
+        w = np.full((nblk, nblk), 100, np.int64)
+    elif kind == "random":
+        w = rng.integers(0, 1000, (nblk, nblk))
+    else:  # sparse: most blocks empty
+        w = rng.integers(0, 1000, (nblk, nblk)) * (rng.random((nblk, nblk)) < 0.15)
+    return np.tril(w).astype(np.int64)
+
+
+def test_tiles2d_matches_restatement_and_covers():
+    rng = np.random.default_rng(3)
+    for trial in range(120):
+        nblk = int(rng.integers(1, 24))
+        w = _lower_weights(rng, nblk, ("uniform", "random", "sparse")[trial % 3])
+        bounds = np.concatenate([[0], np.cumsum(rng.integers(1, 3000, nblk))])
+        for world in (1, 2, 3, 4, 5, 8, 16):
+            got = abi.dist_tiles2d(w, bounds, world)
+            assert np.array_equal(got, dm.dist_tiles2d(w, bounds, world)), (trial, world)
+            owner = -np.ones((nblk, nblk), np.int64)
+            for r, (r0, r1, c0, c1) in enumerate(got):
+                blk = owner[r0:r1, c0:c1]
+                assert np.all((blk == -1) | (np.tril(w)[r0:r1, c0:c1] == 0)), "rectangles overlap"
+                blk[np.tril(w)[r0:r1, c0:c1] > 0] = r
+            assert np.all(owner[w > 0] >= 0), "a non-empty block has no rank"
+
+
+def test_tiles2d_balance_and_exchange_volume():
+    """On the clustered generator's T1-shaped block weights (scaled down): every rank's tile is
+    within 2 % of the ideal nnz share, and the panel segments a rank's SpMM exchanges (rows or
+    columns it touches) are fewer than with block-row slabs for the heaviest rank."""
+    p = abi.clustered_params(n=290_000, target_nnz=110_000_000, block_extent=1000, seed=1)
+    w = abi.clustered_block_weights(p)
+    bounds = abi.uniform_boundaries(p.n, p.block_extent)
+    assert abs(np.tril(w).sum() - abi.clustered_weights(p).sum()) / w.sum() < 1e-3
+    for world in (2, 4, 8):
+        rects = abi.dist_tiles2d(w, bounds, world)
+        share = np.array([np.tril(w)[r0:r1, c0:c1].sum() for r0, r1, c0, c1 in rects])
+        assert share.sum() == np.tril(w).sum()
+        assert share.max() <= 1.02 * share.sum() / world, (world, share)
+        cuts = abi.dist_rows(bounds, world)
+        t2d = [len(dm.touched_segments(w, bounds, cuts, r)) for r in rects]
+        slabs = abi.dist_balance(w.sum(axis=1), world)
+        t1d = [len(dm.touched_segments(w, bounds, cuts, (slabs[r], slabs[r + 1], 0, len(w)))) for r in range(world)]
+        assert sum(t2d) <= sum(t1d) and max(t2d) <= max(t1d), (world, t2d, t1d)
+
+
+def test_clustered_tiles_reassemble_the_matrix():
+    """Each rank generates only its 2-D tile: the tiles are exactly the whole-matrix generator's
+    entries and the summed |row| parts give its diagonal."""
+    kw = dict(n=9000, target_nnz=2_000_000, block_extent=1000, seed=5)
+    p = abi.clustered_params(**kw)
+    whole, diag, toff = abi.generate_clustered(**kw)
+    bounds = abi.uniform_boundaries(9000, 1000)
+    rects = abi.dist_tiles2d(abi.clustered_block_weights(p), bounds, 4)
+    trip, absum = [], np.zeros(9000)
+    for r0, r1, c0, c1 in rects:
+        m, rowabs, t = abi.generate_clustered_tile(p, (int(r0), int(r1)), (int(c0), int(c1)))
+        assert np.array_equal(t, toff)
+        assert np.array_equal(m.to_triples(), whole.rect(int(r0), int(r1), int(c0), int(c1)).to_triples())
+        trip.append(m.to_triples())
+        absum += rowabs
+    t = np.concatenate(trip)
+    want = whole.to_triples()
+    assert len(t) == len(want)
+    assert np.array_equal(np.sort(t, order=["row", "col"]), np.sort(want, order=["row", "col"]))
+    assert np.allclose(abi.clustered_diag(p, absum, 0, 9000), diag, rtol=1e-13, atol=0)

@@ -102,6 +102,39 @@ def test_dist_spmm_matches_single_and_oracle(ctx, world):
         assert sum(i["bytes"] for _, _, i, *_ in res) < world * full
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_dist_spmm_2d_tiles_match_single_and_oracle(ctx, world):
+    """North_star's partition: every rank holds an nnz-balanced 2-D tile of blocks
+    (be_dist_tiles2d) instead of a block-row slab; the panels stay equal-row segments. The
+    distributed SpMM equals the single-GPU SpMM and the oracle, each rank's exchange plan is the
+    host rule on its tile, and no rank exchanges more segments than with slabs."""
+    m, diag, _ = problem(extent=500 if world > 4 else 1000)
+    n, nb = m.nrows, 16
+    x = np.random.default_rng(6).uniform(-1, 1, (n, nb))
+    cuts, slabs = partition(m, world)
+    rects = abi.dist_tiles2d(m.block_weights(), m.row_offsets, world)
+
+    def rank(r, c, comm):
+        tile = m.rect(*(int(v) for v in rects[r]))
+        op = abi.DistOperator(c, comm, tile, cuts, diag[cuts[r]:cuts[r + 1]])
+        y = op.apply_host(x[cuts[r]:cuts[r + 1]])
+        need = op.need()
+        op.close()
+        return y, need, abi.dist_touched(tile, cuts, world), tile.nnz
+
+    res = run_ranks(world, rank)
+    y = np.vstack([a[0] for a in res])
+    assert sum(a[3] for a in res) == m.nnz
+    want = ol.Impl("orc").spmm(m, diag, x)
+    single = abi.Operator(ctx, m, diag).apply_host(x)
+    assert np.linalg.norm(y - want) / np.linalg.norm(want) <= 1e-5
+    assert np.linalg.norm(y - single) / np.linalg.norm(single) <= 1e-6
+    need = np.array([a[2] for a in res])
+    assert all(np.array_equal(a[1], need) for a in res)
+    need1d = np.array([abi.dist_touched(m.slab(int(slabs[p]), int(slabs[p + 1])), cuts, world) for p in range(world)])
+    assert need.sum() <= need1d.sum()
+
+
 def test_dist_decode_is_the_slab(ctx):
     m, diag, _ = problem(n=3000, extent=500)
     world = 3
@@ -238,8 +271,9 @@ def test_nccl_world1(ctx):
     comm.close()
 
 
+@pytest.mark.parametrize("partition", ["2d", "slabs"])
 @pytest.mark.parametrize("world", [2, 3])
-def test_weak_scaling_glue_matches_whole_matrix(ctx, world):
+def test_weak_scaling_glue_matches_whole_matrix(ctx, world, partition):
     """The bench's per-rank problem construction (weak.rank_problem: slab and
     diagonal-block generation, the summed |row| diagonal, rank-range tiles)
     solves the same problem as the whole matrix on one GPU."""
@@ -265,7 +299,7 @@ def test_weak_scaling_glue_matches_whole_matrix(ctx, world):
             bar.wait()
             return out
 
-        rp = weak.rank_problem(c, comm, p, r, world, True, allreduce_sum)
+        rp = weak.rank_problem(c, comm, p, r, world, True, allreduce_sum, partition=partition)
         assert np.allclose(rp["diag"], diag[rp["lo"]:rp["hi"]], rtol=1e-13, atol=0)
         res = abi.lobpcg(c, rp["op"], tiles=rp["tiles"], k=8, nb=16, tol=3e-5, maxiter=300, seed=1)
         rp["op"].close()
