@@ -69,7 +69,7 @@ def _free_port():
         return sk.getsockname()[1]
 
 
-def _gloo_rank(rank, world, port, n, nb):
+def _gloo_rank(rank, world, port, n, nb, partition="slabs"):
     """One rank of the segment-wise exchange of the distributed operator on CPU
     with gloo: the C++ rule (be_dist_touched) decides which X segments travel where and which
     partial Y segments go to which owner; the partial SpMM of the slab is the restated model
@@ -85,7 +85,10 @@ def _gloo_rank(rank, world, port, n, nb):
     slabs = abi.dist_balance(m.block_row_nnz(), world)
     lmax = int(np.max(np.diff(cuts)))
     x = np.random.default_rng(1).uniform(-1, 1, (n, nb))
-    slab = m.slab(int(slabs[rank]), int(slabs[rank + 1]))
+    if partition == "2d":  # this rank's nnz-balanced 2-D tile (be_dist_tiles2d)
+        slab = m.rect(*(int(v) for v in abi.dist_tiles2d(m.block_weights(), m.row_offsets, world)[rank]))
+    else:
+        slab = m.slab(int(slabs[rank]), int(slabs[rank + 1]))
     mine = abi.dist_touched(slab, cuts, world)
     allt = [None] * world
     dist.all_gather_object(allt, mine.tolist())
@@ -143,10 +146,11 @@ def _gloo_rank(rank, world, port, n, nb):
         assert err < 1e-13, err
 
 
-@pytest.mark.parametrize("world", [2])
-def test_gloo_exchange_matches_oracle(world):
+@pytest.mark.parametrize("partition", ["slabs", "2d"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_exchange_matches_oracle(world, partition):
     import torch.multiprocessing as mp
-    mp.spawn(_gloo_rank, args=(world, _free_port(), 1500, 8), nprocs=world, join=True)
+    mp.spawn(_gloo_rank, args=(world, _free_port(), 1500, 8, partition), nprocs=world, join=True)
 
 
 def test_clustered_parts_reassemble_the_matrix():
