@@ -1519,11 +1519,8 @@ __global__ void k_sign_fix(double* C, const double* w, double* d, int n, int k, 
 // per-column partial sums of squares over this CTA's rows (2 panels max)
 __global__ void __launch_bounds__(kT) k_residual(const double* __restrict__ hx, const double* __restrict__ x,
                                                  const double* __restrict__ theta, double* __restrict__ r, int nb,
-                                                 std::int64_t n, double* __restrict__ partial, int mode,
-                                                 const Status* gate = nullptr) {
+                                                 std::int64_t n, double* __restrict__ partial, int mode) {
     // mode 0: r = hx - x*theta, sums of r^2 and x^2; mode 1: sums of x^2 only
-    // gate: run only when gate->not_pd is set (the device-side column-scaling fallback)
-    if (gate && !gate->not_pd) return;
     __shared__ double red[2][kT];
     const int tid = threadIdx.x;
     if (nb == 16) {  // 16-byte accesses: thread = (row, column pair)
@@ -1603,9 +1600,7 @@ __global__ void __launch_bounds__(kT) k_residual(const double* __restrict__ hx, 
 
 // column sums of the per-CTA partials: 256 threads = (column, part) with the
 // parts summed in a fixed order (deterministic)
-__global__ void k_norm_reduce(const double* __restrict__ partial, int nparts, int nb, double* out_r, double* out_x,
-                              const Status* gate = nullptr) {
-    if (gate && !gate->not_pd) return;
+__global__ void k_norm_reduce(const double* __restrict__ partial, int nparts, int nb, double* out_r, double* out_x) {
     __shared__ double red[2][256];
     const int tid = threadIdx.x;
     const int P = blockDim.x / nb;  // parts
@@ -2077,11 +2072,10 @@ void residual(Ctx* ctx, const double* hx, const double* x, const double* theta, 
     ctx->launches += 2;
 }
 
-void colnorm2(Ctx* ctx, const double* a, int nb, std::int64_t n, double* partials, double* out, cudaStream_t s,
-              const Status* gate) {
+void colnorm2(Ctx* ctx, const double* a, int nb, std::int64_t n, double* partials, double* out, cudaStream_t s) {
     const int grid = grid_rows(ctx, n, kT / nb * 64);
-    k_residual<<<grid, kT, 0, s>>>(nullptr, a, nullptr, nullptr, nb, n, partials, 1, gate);
-    k_norm_reduce<<<1, 256, 0, s>>>(partials, grid, nb, nullptr, out, gate);
+    k_residual<<<grid, kT, 0, s>>>(nullptr, a, nullptr, nullptr, nb, n, partials, 1);
+    k_norm_reduce<<<1, 256, 0, s>>>(partials, grid, nb, nullptr, out);
     BE_CUDA(cudaGetLastError());
     ctx->launches += 2;
 }

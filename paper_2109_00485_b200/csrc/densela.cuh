@@ -82,9 +82,7 @@ void chol_floored(Ctx* ctx, const double* B, double* R, int n, double rel_floor,
 void residual(Ctx* ctx, const double* hx, const double* x, const double* theta, double* r, int nb, std::int64_t n,
               double* partials, double* rnorm2, double* xnorm2, cudaStream_t s);
 // column sums of squares of one panel
-// gate: when non-null, the kernels run only if gate->not_pd is set (out left untouched otherwise)
-void colnorm2(Ctx* ctx, const double* a, int nb, std::int64_t n, double* partials, double* out, cudaStream_t s,
-              const Status* gate = nullptr);
+void colnorm2(Ctx* ctx, const double* a, int nb, std::int64_t n, double* partials, double* out, cudaStream_t s);
 // orthonormalize_pair fallback (lobpcg.hpp:263-269): scale columns of a, ha
 // by 1 / sqrt(norm2) when st->ortho_fallback.
 void scale_columns(Ctx* ctx, double* a, double* ha, const double* norm2, int nb, std::int64_t n, const Status* st,

@@ -187,12 +187,6 @@ struct Solver {
         sygv.ensure(ctx, dim);
     }
     ~Solver() {
-        if (s2) {
-            cudaStreamSynchronize(s2);
-            cudaStreamDestroy(s2);
-            cudaEventDestroy(ev_fork);
-            cudaEventDestroy(ev_join);
-        }
         if (cudaStreamSynchronize(s) != cudaSuccess) {  // queued work may still use the buffers: plain release
             if (hm) cudaFreeHost(hm);
             return;
@@ -380,51 +374,12 @@ struct Solver {
         allreduce(rn2, 2 * nb);  // rn2, xn2 are adjacent
     }
 
-    // P hygiene (lobpcg.hpp:412-417) + orthonormalize_pair (:254-270). device_fallback: the
-    // column-scaling branch runs gated on the device flag (no host round trip) and clears it.
-    void p_hygiene(bool device_fallback) {
-        gram1(X.get(), P.get(), 0, xtp);
-        dla::MixJob m{};
-        m.nb = nb;
-        m.nout = 2;
-        m.out[0] = dla::MixOut{P.get(), 1, 1, {{X.get(), xtp, 1, 0}}, -1};
-        m.out[1] = dla::MixOut{HP.get(), 1, 1, {{HX.get(), xtp, 1, 0}}, -1};
-        dla::mix(ctx, m, n, s);
-        gram1(P.get(), P.get(), 1, Bp);
-        dla::chol_floored(ctx, Bp, Rp, nb, 1e-8, st.get(), s);
-        dla::trsm(ctx, P.get(), HP.get(), Rp, nb, n, st.get(), 0, 1, s);
-        if (device_fallback) {
-            dla::colnorm2(ctx, P.get(), nb, n, partials.get(), pn2, s, st.get());
-            dla::scale_columns(ctx, P.get(), HP.get(), pn2, nb, n, st.get(), s);
-            BE_CUDA(cudaMemsetAsync(&st.get()->not_pd, 0, sizeof(int), s));
-        }
-    }
-    // a deferred P hygiene still owed when control returns to the caller
-    void flush_p() {
-        if (!p_pending) return;
-        p_pending = false;
-        BE_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(dla::Status), s));
-        p_hygiene(true);
-        sync_status();
-        if (hm->st.singular_tri) fail(BE_ERR_SINGULAR_TRIANGULAR, "trsm_right_inv: triangular factor is numerically singular");
-    }
-
     // One iteration of lobpcg_solve (lobpcg.hpp:338-441) from the preconditioner
     // on. With the fused Rayleigh-Ritz eigensolve the device takes every
     // decision of the iteration itself (the drop-P retry inside rr_eig, the
     // W restart deferred, see iterate) and the host synchronises once, at the
     // end, to read the status, the Ritz values and the residual norms.
     void iteration_body(bool w_restart) {
-        const bool overlap = p_pending;
-        if (overlap) {  // the previous iteration's P hygiene, on the side stream
-            BE_CUDA(cudaEventRecord(ev_fork, s));
-            BE_CUDA(cudaStreamWaitEvent(s2, ev_fork, 0));
-            std::swap(s, s2);
-            p_hygiene(true);
-            std::swap(s, s2);
-            BE_CUDA(cudaEventRecord(ev_join, s2));
-            p_pending = false;
-        }
         nv.to("precond");
         BE_CUDA(cudaEventRecord(ev.e[0], s));
         if (!w_restart) {
@@ -438,7 +393,6 @@ struct Solver {
                 BE_CUDA(cudaMemcpyAsync(W.get(), R.get(), static_cast<std::size_t>(n * nb) * 8, cudaMemcpyDeviceToDevice, s));
             }
         }
-        if (overlap) BE_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
         nv.to("w-hygiene");
         BE_CUDA(cudaEventRecord(ev.e[1], s));
         // W hygiene (lobpcg.hpp:358-373)
@@ -499,11 +453,18 @@ struct Solver {
         }
         nv.to("p-hygiene");
         BE_CUDA(cudaEventRecord(ev.e[6], s));
-        // P hygiene reads X and HX and writes only P and HP; the residual reads only X, HX and
-        // theta. Deferred, it runs on the side stream next to the next iteration's
-        // preconditioner (which reads R alone), joined before W hygiene projects W against P.
-        if (defer_p) p_pending = true;
-        else p_hygiene(false);
+        {  // P hygiene (lobpcg.hpp:412-417) + orthonormalize_pair (:254-270)
+            gram1(X.get(), P.get(), 0, xtp);
+            dla::MixJob m{};
+            m.nb = nb;
+            m.nout = 2;
+            m.out[0] = dla::MixOut{P.get(), 1, 1, {{X.get(), xtp, 1, 0}}, -1};
+            m.out[1] = dla::MixOut{HP.get(), 1, 1, {{HX.get(), xtp, 1, 0}}, -1};
+            dla::mix(ctx, m, n, s);
+            gram1(P.get(), P.get(), 1, Bp);
+            dla::chol_floored(ctx, Bp, Rp, nb, 1e-8, st.get(), s);
+            dla::trsm(ctx, P.get(), HP.get(), Rp, nb, n, st.get(), 0, 1, s);
+        }
         nv.to("residual");
         BE_CUDA(cudaEventRecord(ev.e[7], s));
         dla::residual(ctx, HX.get(), X.get(), theta, R.get(), nb, n, partials.get(), rn2, xn2, s);
@@ -520,7 +481,6 @@ struct Solver {
     // run up to `count` further iterations (never past maxiter); returns the
     // number executed. Stops at convergence.
     int iterate(int count) {
-        enable_overlap();
         int done = 0;
         while (done < count && !converged && iter < cfg.maxiter) {
             ++iter;
@@ -538,7 +498,6 @@ struct Solver {
                 std::swap(P, Pn);
                 std::swap(HP, HPn);
                 p_active = p_was;
-                p_pending = false;  // the rolled-back P already had its hygiene (deferred or not)
                 --res.operator_calls;
                 BE_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(dla::Status), s));
                 iteration_body(true);
@@ -547,7 +506,7 @@ struct Solver {
             if (hm->st.rr_dropped == 1 || dropped_host) ++res.restarts;
             th.assign(hm->theta, hm->theta + nb);
             p_active = true;
-            if (hm->st.not_pd && !p_pending) {  // column-scaling fallback of orthonormalize_pair
+            if (hm->st.not_pd) {  // column-scaling fallback of orthonormalize_pair
                 dla::colnorm2(ctx, P.get(), nb, n, partials.get(), pn2, s);
                 allreduce(pn2, nb);
                 dla::scale_columns(ctx, P.get(), HP.get(), pn2, nb, n, st.get(), s);
@@ -595,7 +554,6 @@ struct Solver {
             }
             if (nconv >= k) converged = true;
         }
-        flush_p();
         return done;
     }
 
@@ -618,18 +576,6 @@ struct Solver {
 
     be_observer_fn observer = nullptr;
     void* observer_user = nullptr;
-    // deferred P hygiene (single device, no observer: the observer sees P after its hygiene)
-    cudaStream_t s2 = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    bool p_pending = false;
-    bool defer_p = false;
-    void enable_overlap() {
-        defer_p = !comm && !observer && tiles && std::getenv("BE_NO_P_OVERLAP") == nullptr;
-        if (!defer_p || s2) return;
-        BE_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
-        BE_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-        BE_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-    }
 };
 
 }  // namespace

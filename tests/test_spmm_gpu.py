@@ -290,31 +290,3 @@ def test_auto_format_choice(ctx):
     mc, dc, _ = abi.generate_clustered(n=200000, target_nnz=1 << 23, seed=2)
     assert abi.Operator(ctx, mc, dc).info().ntiles > 0
 
-
-@pytest.mark.parametrize("stepped", [False, True])
-def test_deferred_p_hygiene_is_bit_identical(ctx, stepped, monkeypatch):
-    """P hygiene of iteration i overlapped with the preconditioner of iteration i + 1 on a side
-    stream (lobpcg.cu Solver::p_hygiene) performs the same operations in the same order per
-    panel: with the deterministic operator the solve history is bit-identical to the serial
-    order (BE_NO_P_OVERLAP=1), also across IncrementalSolve step() calls (flushed per call)."""
-    m, diag = sym_problem(3000, 30000, 500, 17)
-    toff = abi.uniform_boundaries(3000, 60)
-    tiles = abi.Tiles(ctx, m, diag, toff)
-    op = abi.Operator(ctx, m, diag, values_prec=abi.BE_F64, deterministic=True)
-
-    def solve():
-        if not stepped:
-            return abi.lobpcg(ctx, op, tiles=tiles, k=4, nb=8, tol=1e-9, maxiter=40, seed=5)
-        s = abi.IncrementalSolve(ctx, op, tiles=tiles, k=4, nb=8, tol=1e-9, maxiter=40, seed=5)
-        while s.step(3) == 3:
-            pass
-        return s.end()
-
-    monkeypatch.setenv("BE_NO_P_OVERLAP", "1")
-    serial = solve()
-    monkeypatch.delenv("BE_NO_P_OVERLAP")
-    over = solve()
-    assert serial["iterations"] == over["iterations"] and serial["iterations"] > 3
-    for key in ("lambda_", "x", "theta", "residual_norms"):
-        if key in serial:
-            assert np.array_equal(serial[key], over[key]), key
