@@ -506,13 +506,22 @@ def main():
     precond = a.precond == "on"
     vprec, sv = (abi.BE_F32, 4) if a.values == "f32" else (abi.BE_F64, 8)
     inp = ensure_cache(a.config, a.seed)  # the same bytes the reference arm reads
+    ctx = abi.Context(local)
+    # the tile-format configuration (T1) is streamed from the file (be_op_create_csb1); the sparse
+    # ones (c1, t1random) get the row-list format, which the in-memory build chooses
+    stream_build = a.config == "t1"
+    t_stream = None
+    if stream_build:
+        t0 = time.time()
+        op, _ = abi.Operator.from_csb1(ctx, inp["file"], values_prec=vprec)
+        t_stream = time.time() - t0
     t0 = time.time()
-    m, diag = abi.Csb.load(inp["file"])
+    m, diag = abi.Csb.load(inp["file"])  # the preconditioner tiles and the correctness gate
     toff = np.fromfile(inp["tiles"], dtype=np.int64)[1:]
     t_load = time.time() - t0
-    ctx = abi.Context(local)
     t0 = time.time()
-    op = abi.Operator(ctx, m, diag, values_prec=vprec)
+    if not stream_build:
+        op = abi.Operator(ctx, m, diag, values_prec=vprec)
     tiles = abi.Tiles(ctx, m, diag, toff) if precond else None
     t_up = time.time() - t0
     n, nnz = m.nrows, m.nnz
@@ -612,7 +621,8 @@ def main():
         "time_to_solution": tts,
         "input": dict(inp, our_load_s=round(t_load, 1), loaded_with="be_csb_load"),
         "lobpcg": {"iter_ms": ms_step, "spmm_ms": spmm_ms, "precond_ms": 1e3 * float(np.mean(rec[:, 1])),
-                   "setup_s": {"load": t_load, "upload": t_up}, "parallelism": "1 GPU"},
+                   "setup_s": {"operator_streamed_from_file": t_stream, "load": t_load, "upload": t_up},
+                   "parallelism": "1 GPU"},
     }
     print(json.dumps(line), flush=True)
 

@@ -246,6 +246,14 @@ enum { BE_OP_SYMMETRIC = 1, BE_OP_DETERMINISTIC = 2, BE_OP_FORMAT_TILES = 4, BE_
  * entries and fewer than 384 per occupied 128 x 128 sub-tile). */
 be_status be_op_create(be_ctx* ctx, const be_csb_view* L, const double* diag, int values_prec,
                        int flags, be_op** out);
+/* The symmetric operator streamed from a CSB1 cache file (be_csb_save with its diagonal section;
+ * the bytes load_csb, csb.hpp:264-290, and the driver's diagonal section, driver.hpp:136-161,
+ * read): batches of about batch_entries stored entries (whole block rows; <= 0: 2^26) are read by
+ * a loader thread while the previous batch is cut into tiles and uploaded, so the whole matrix is
+ * never resident on the host. flags must hold BE_OP_SYMMETRIC; the tile format is built (the same
+ * tiles as be_op_create with BE_OP_FORMAT_TILES). diag (optional, be_free_buffer): the diagonal. */
+be_status be_op_create_csb1(be_ctx* ctx, const char* path, int values_prec, int flags, int64_t batch_entries,
+                           double** diag, int64_t* ndiag, be_op** out);
 be_status be_op_destroy(be_op* op);
 
 /* Y = op(X) on device panels of type panel_prec (BE_F32 / BE_F64),

@@ -526,6 +526,22 @@ class Operator:
                                  C.byref(self._h)))
         self._csb = None
 
+    @classmethod
+    def from_csb1(cls, ctx: Context, path, values_prec=BE_F32, batch_entries=0):
+        """The symmetric tile-format operator streamed from a CSB1 cache file (be_op_create_csb1):
+        (operator, diagonal)."""
+        op = cls.__new__(cls)
+        op.ctx = ctx
+        op._csb = None
+        op._h = C.c_void_p()
+        dp = C.POINTER(C.c_double)()
+        nd = C.c_int64(0)
+        check(lib().be_op_create_csb1(ctx.handle, str(path).encode(), C.c_int(values_prec), C.c_int(BE_OP_SYMMETRIC),
+                                      C.c_int64(batch_entries), C.byref(dp), C.byref(nd), C.byref(op._h)))
+        diag = np.ctypeslib.as_array(dp, shape=(nd.value,)).copy() if nd.value > 0 else np.zeros(0)
+        lib().be_free_buffer(dp)
+        return op, diag
+
     @property
     def handle(self):
         return self._h

@@ -422,6 +422,22 @@ be_status be_op_create(be_ctx* ctx, const be_csb_view* L, const double* diag, in
     });
 }
 
+be_status be_op_create_csb1(be_ctx* ctx, const char* path, int values_prec, int flags, int64_t batch_entries,
+                           double** diag, int64_t* ndiag, be_op** out) {
+    return guard([&] {
+        if (!ctx || !path || !out) be::fail(BE_ERR_BAD_PARAMS, "null argument");
+        BE_CUDA(cudaSetDevice(ctx->impl->device));
+        std::vector<double> d;
+        auto op = be::op_create_csb1(ctx->impl.get(), path, values_prec, flags, diag ? &d : nullptr, batch_entries);
+        if (diag) {
+            *diag = static_cast<double*>(std::malloc(std::max<std::size_t>(d.size(), 1) * sizeof(double)));
+            std::memcpy(*diag, d.data(), d.size() * sizeof(double));
+        }
+        if (ndiag) *ndiag = static_cast<int64_t>(d.size());
+        *out = new be_op{std::move(op)};
+    });
+}
+
 be_status be_op_destroy(be_op* op) {
     return guard([&] { delete op; });
 }

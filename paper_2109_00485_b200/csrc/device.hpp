@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <memory>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "host_csb.hpp"
@@ -175,6 +176,9 @@ struct Op {
 };
 
 std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag, int values_prec, int flags);
+// the symmetric tile-format operator streamed from a CSB1 file (its diagonal section required)
+std::unique_ptr<Op> op_create_csb1(Ctx* ctx, const std::string& path, int values_prec, int flags,
+                                   std::vector<double>* diag_out, index_t batch_entries);
 // Distributed operator (row e): L holds this rank's slab of the global
 // strictly-lower matrix (global coordinates), cuts (world + 1 entries, on L's
 // block boundaries) the panel-row ownership, diag_local the diagonal of this

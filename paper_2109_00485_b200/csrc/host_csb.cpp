@@ -300,6 +300,26 @@ void save_csb1(std::ostream& os, const be_csb_view& v, const double* diag, index
 // contiguous ranges of the index and value sections (a multi-GPU rank loads
 // its own slab of a Test-3-sized cache without reading the rest). diag, when
 // given, receives the cached diagonal of those block rows' rows.
+// Header of a CSB1 file only: dimension, block rows and the stored entries per block row.
+std::vector<index_t> csb1_block_row_nnz(const std::string& path, index_t& nrows, index_t& nrowblks) {
+    std::ifstream is(path, std::ios::binary);
+    if (!is) fail(BE_ERR_PARSE, "cannot open " + path);
+    char magic[4];
+    is.read(magic, 4);
+    if (!is || std::memcmp(magic, "CSB1", 4) != 0) fail(BE_ERR_PARSE, "CSB1 cache: bad magic");
+    nrows = static_cast<index_t>(get<std::uint64_t>(is));
+    get<std::uint64_t>(is);  // ncols
+    nrowblks = static_cast<index_t>(get<std::uint64_t>(is));
+    const index_t ncolblks = static_cast<index_t>(get<std::uint64_t>(is));
+    if (nrowblks < 1 || ncolblks < 1 || nrowblks > (1 << 24) || ncolblks > (1 << 24))
+        fail(BE_ERR_PARSE, "CSB1 cache: implausible block counts");
+    for (index_t i = 0; i < nrowblks + 1 + ncolblks + 1; ++i) get<std::uint64_t>(is);
+    std::vector<index_t> brn(static_cast<std::size_t>(nrowblks), 0);
+    for (index_t b = 0; b < nrowblks * ncolblks; ++b) brn[static_cast<std::size_t>(b / ncolblks)] += static_cast<index_t>(get<std::uint64_t>(is));
+    if (!is) fail(BE_ERR_PARSE, "CSB1 cache: truncated header");
+    return brn;
+}
+
 std::unique_ptr<CsbHost> load_csb1_rows(const std::string& path, index_t b0, index_t b1, std::vector<double>* diag) {
     std::ifstream is(path, std::ios::binary);
     if (!is) fail(BE_ERR_PARSE, "cannot open " + path);

@@ -69,6 +69,7 @@ std::unique_ptr<CsbHost> load_csb1(const std::string& path, std::vector<double>*
 void save_csb1(std::ostream& os, const be_csb_view& v, const double* diag, index_t ndiag);
 std::unique_ptr<CsbHost> load_csb1(std::istream& is, std::vector<double>* diag);
 std::unique_ptr<CsbHost> load_csb1_rows(const std::string& path, index_t b0, index_t b1, std::vector<double>* diag);
+std::vector<index_t> csb1_block_row_nnz(const std::string& path, index_t& nrows, index_t& nrowblks);
 std::vector<index_t> draw_tile_offsets(index_t n, index_t block_extent, index_t tile_min, index_t tile_max,
                                        std::mt19937_64& rng);
 std::unique_ptr<Synth> generate_synthetic(const be_synth_params& p);

@@ -45,6 +45,7 @@
 
 #include <algorithm>
 #include <functional>
+#include <future>
 #include <type_traits>
 #include <cmath>
 #include <cstdlib>
@@ -58,6 +59,7 @@
 #include "comm.hpp"
 #include "device.hpp"
 #include "hostcopy.hpp"
+#include "host_csb.hpp"
 #include "stream.cuh"
 
 namespace be {
@@ -1313,6 +1315,8 @@ void build_block_row(const be_csb_view& L, index_t bi, int max_nnz, bool keep_sr
 }  // namespace
 
 static void op_build(Op* op, const be_csb_view& L, const RowMap* map);
+static void op_finish_tiles(Op* op, const std::vector<TileHdr>& all_hdr, const std::vector<unsigned char>& all_cls,
+                            const RowMap* map);
 
 Ctx::~Ctx() {}
 
@@ -1457,6 +1461,113 @@ std::unique_ptr<Op> op_create(Ctx* ctx, const be_csb_view& L, const double* diag
     return op;
 }
 
+#ifndef BE_SPMM_MAXNNZ
+#define BE_SPMM_MAXNNZ 2048  // f32 entries per tile piece (two CTAs per SM)
+#endif
+
+// Streamed build from a CSB1 file: batches of ~2^26 stored entries (whole block
+// rows) are read by a loader thread while the previous batch is cut into tiles on the host
+// workers and its blobs go up through the copy pool into a device buffer that grows by 1.5x
+// (first sized from the header's entry count). Host memory holds about two batches instead of
+// the whole matrix plus its tile format; file reading, tile building and the upload overlap.
+// Same tiles, headers and runs as op_build over the whole matrix (tile format; the decode index
+// is not kept).
+std::unique_ptr<Op> op_create_csb1(Ctx* ctx, const std::string& path, int values_prec, int flags,
+                                   std::vector<double>* diag_out, index_t batch_entries) {
+    if (values_prec != BE_F32 && values_prec != BE_F64) fail(BE_ERR_BAD_PARAMS, "values_prec must be BE_F32 or BE_F64");
+    if (!(flags & BE_OP_SYMMETRIC) || (flags & (BE_OP_DETERMINISTIC | BE_OP_FORMAT_ROWS)))
+        fail(BE_ERR_BAD_PARAMS, "be_op_create_csb1: builds the symmetric operator in the tile format");
+    index_t n = 0, nblk = 0;
+    const std::vector<index_t> brn = csb1_block_row_nnz(path, n, nblk);
+    if (n >= (index_t{1} << 31)) fail(BE_ERR_BAD_PARAMS, "sym_spmm: dimension exceeds 2^31 rows per device");
+    const index_t nnz = std::accumulate(brn.begin(), brn.end(), index_t{0});
+    if (batch_entries <= 0) batch_entries = index_t{1} << 26;
+    std::vector<index_t> cut{0};
+    for (index_t b = 0, acc = 0; b < nblk; ++b) {
+        acc += brn[static_cast<std::size_t>(b)];
+        if (acc >= batch_entries || b + 1 == nblk) {
+            cut.push_back(b + 1);
+            acc = 0;
+        }
+    }
+    auto op = std::make_unique<Op>();
+    op->ctx = ctx;
+    op->nrows = op->ncols = n;
+    op->nnz = nnz;
+    op->values_prec = values_prec;
+    op->symmetric = true;
+    op->max_nnz = values_prec == BE_F32 ? BE_SPMM_MAXNNZ : 1024;
+    op->blob_max = static_cast<int>(values_prec == BE_F32 ? blob_bytes<float>(op->max_nnz) : blob_bytes<double>(op->max_nnz));
+    op->counter.reset(2);
+    BE_CUDA(cudaMemset(op->counter.get(), 0, 2 * sizeof(int)));
+    const std::size_t per_entry = values_prec == BE_F32 ? 2 * sizeof(float) + 2 : 2 * sizeof(double) + 2;
+    index_t cap = std::max<index_t>(16, static_cast<index_t>(static_cast<double>(nnz) * per_entry * 1.25) + (index_t{1} << 24));
+    op->blobs.reset(cap);
+    std::vector<double> diag;
+    diag.reserve(static_cast<std::size_t>(n));
+    std::vector<TileHdr> all_hdr;
+    std::vector<unsigned char> all_cls;
+    index_t b_off = 0;
+    cudaStream_t s = ctx->stream;
+    struct Part {
+        std::unique_ptr<CsbHost> m;
+        std::vector<double> d;
+    };
+    auto load = [&path, &cut](std::size_t i) {
+        Part p;
+        p.m = load_csb1_rows(path, cut[i], cut[i + 1], &p.d);
+        return p;
+    };
+    std::future<Part> next = std::async(std::launch::async, load, std::size_t{0});
+    for (std::size_t i = 0; i + 1 < cut.size(); ++i) {
+        Part part = next.get();
+        if (i + 2 < cut.size()) next = std::async(std::launch::async, load, i + 1);
+        const be_csb_view L = part.m->view();
+        if (!is_strictly_lower(L)) fail(BE_ERR_NOT_STRICTLY_LOWER, "SymmetricOperator: stored entry with row <= col");
+        if (part.d.size() != static_cast<std::size_t>(L.row_offsets[cut[i + 1]] - L.row_offsets[cut[i]]))
+            fail(BE_ERR_DIMENSION_MISMATCH, "SymmetricOperator: diagonal length mismatch (CSB1 file without its diagonal)");
+        diag.insert(diag.end(), part.d.begin(), part.d.end());
+        const index_t b0 = cut[i], nb = cut[i + 1] - cut[i];
+        std::vector<RowOut> rows(static_cast<std::size_t>(nb));
+        parallel_for_dynamic(hw_threads(), nb, [&](index_t q, int) {
+            if (values_prec == BE_F32)
+                build_block_row<float>(L, b0 + q, op->max_nnz, false, nullptr, rows[static_cast<std::size_t>(q)]);
+            else
+                build_block_row<double>(L, b0 + q, op->max_nnz, false, nullptr, rows[static_cast<std::size_t>(q)]);
+        });
+        part.m.reset();
+        index_t add = 0;
+        for (const auto& r : rows) add += static_cast<index_t>(r.blob.size());
+        if (b_off + add > cap) {  // grow by 1.5x, keeping the blobs already up
+            const index_t nc = std::max(b_off + add, cap + cap / 2);
+            DBuf<unsigned char> nbuf(nc);
+            BE_CUDA(cudaStreamSynchronize(s));
+            if (b_off) BE_CUDA(cudaMemcpyAsync(nbuf.get(), op->blobs.get(), static_cast<std::size_t>(b_off), cudaMemcpyDeviceToDevice, s));
+            BE_CUDA(cudaStreamSynchronize(s));
+            op->blobs = std::move(nbuf);
+            cap = nc;
+        }
+        for (auto& r : rows) {
+            if (r.hdr.empty()) continue;
+            for (auto& h : r.hdr) h.begin16 += static_cast<std::uint32_t>(b_off / 16);
+            all_hdr.insert(all_hdr.end(), r.hdr.begin(), r.hdr.end());
+            all_cls.insert(all_cls.end(), r.cls.begin(), r.cls.end());
+            h2d_large(op->blobs.get() + b_off, r.blob.data(), r.blob.size(), s);
+            b_off += static_cast<index_t>(r.blob.size());
+            if (b_off / 16 >= (index_t{1} << 32)) fail(BE_ERR_BAD_PARAMS, "sym_spmm: tile blobs exceed 64 GB on one device");
+            r = RowOut();
+        }
+        BE_CUDA(cudaStreamSynchronize(s));  // the batch's pageable sources are released next round
+    }
+    op->blob_total = b_off;
+    op->padded = 0;
+    op_finish_tiles(op.get(), all_hdr, all_cls, nullptr);
+    op->diag.reset(std::max<index_t>(n, 1));
+    if (n > 0) BE_CUDA(cudaMemcpy(op->diag.get(), diag.data(), static_cast<std::size_t>(n) * 8, cudaMemcpyHostToDevice));
+    if (diag_out) *diag_out = std::move(diag);
+    return op;
+}
+
 // Rows of one L2 column band: the f32 X_J and Y_J rows of a band at nb = 16
 // (2 x 64 B per row) take about half of the 126 MB L2.
 #ifndef BE_SPMM_BAND_ROWS
@@ -1487,10 +1598,8 @@ static void op_build(Op* op, const be_csb_view& L, const RowMap* map) {
         padded += static_cast<index_t>(r.src.size());
     }
     if (bytes / 16 >= (index_t{1} << 32)) fail(BE_ERR_BAD_PARAMS, "sym_spmm: tile blobs exceed 64 GB on one device");
-    op->ntiles = ntiles;
     op->blob_total = bytes;
     op->padded = keep_src ? padded : 0;
-    op->tiles.reset(std::max<index_t>(ntiles, 1));
     op->blobs.reset(std::max<index_t>(bytes, 16));
     op->counter.reset(2);
     BE_CUDA(cudaMemset(op->counter.get(), 0, 2 * sizeof(int)));
@@ -1513,6 +1622,15 @@ static void op_build(Op* op, const be_csb_view& L, const RowMap* map) {
         r = RowOut();
     }
     BE_CUDA(cudaStreamSynchronize(op->ctx->stream));
+    op_finish_tiles(op, all_hdr, all_cls, map);
+}
+
+// Tile headers + run lists (shared by the in-memory and the streamed builds).
+static void op_finish_tiles(Op* op, const std::vector<TileHdr>& all_hdr, const std::vector<unsigned char>& all_cls,
+                            const RowMap* map) {
+    const index_t ntiles = static_cast<index_t>(all_hdr.size());
+    op->ntiles = ntiles;
+    op->tiles.reset(std::max<index_t>(ntiles, 1));
     if (ntiles > 0)
         BE_CUDA(cudaMemcpy(op->tiles.get(), all_hdr.data(), all_hdr.size() * sizeof(TileHdr), cudaMemcpyHostToDevice));
     if (map) {  // padded slots (ranks) whose rows the tiles read or write: tiles never straddle a segment
