@@ -928,6 +928,10 @@ struct MixR {
     int qo[4], last[4];  // output of each slot, slot ends its output
     int accl[4], addl[4];  // per output: load index of the old value / the added panel, or -1
     double* y[4];
+    // Gram epilogue (GR): A = output ga, B = output gbo or (gbo < 0) load gbl (accumulator
+    // layout); per-CTA partial [a][b] into gpart
+    int ga, gbo, gbl;
+    double* gpart;
 };
 
 template <int L, int KS>
@@ -939,10 +943,19 @@ __device__ __forceinline__ double pick_load(const double (&x)[L][KS], int l, int
     return v;
 }
 
-template <int NBB, int L>
-__global__ void __launch_bounds__(256, 4) k_mix_r(MixDev m, MixR r, std::int64_t n) {
+// GR: the Gram A^T B of two of the row blocks the warp holds -- an output and an output or an
+// added panel -- formed on the way (the accumulator-layout values moved into DMMA operand
+// fragments by shuffles), so the next Gram needs no read of the panels it just wrote.
+template <int NBB, int L, bool GR = false>
+__global__ void __launch_bounds__(256, GR ? 2 : 4) k_mix_r(MixDev m, MixR r, std::int64_t n) {
     constexpr int NB = 8 * NBB, KS = NB / 4;
+    constexpr int GB = GR ? NBB : 1;
     __shared__ __align__(16) double bsm[4 * KS * NBB * 32];  // [slot][kk][cb][lane]
+    double gacc[GB][GB][2];
+#pragma unroll
+    for (int i = 0; i < GB; ++i)
+#pragma unroll
+        for (int j = 0; j < GB; ++j) gacc[i][j][0] = gacc[i][j][1] = 0.0;
     for (int e = threadIdx.x; e < 4 * KS * NBB * 32; e += blockDim.x) {
         const int ln = e & 31, cb = (e >> 5) % NBB, kk = (e >> 5) / NBB % KS, q = (e >> 5) / (NBB * KS);
         double v = 0.0;
@@ -979,6 +992,7 @@ __global__ void __launch_bounds__(256, 4) k_mix_r(MixDev m, MixR r, std::int64_t
         double acc[NBB][2];
 #pragma unroll
         for (int cb = 0; cb < NBB; ++cb) acc[cb][0] = acc[cb][1] = 0.0;
+        double ka[GB][2], kb[GB][2];  // the Gram operands' row values (accumulator layout)
 #pragma unroll
         for (int q = 0; q < L; ++q) {
             if (q >= r.nq) break;
@@ -1002,9 +1016,54 @@ __global__ void __launch_bounds__(256, 4) k_mix_r(MixDev m, MixR r, std::int64_t
                         v1 += pick_load(x, dl, 2 * cb + 1);
                     }
                     if (ok) *reinterpret_cast<double2*>(y + 8 * cb) = make_double2(v0, v1);
+                    if constexpr (GR) {
+                        if (o == r.ga) ka[cb][0] = v0, ka[cb][1] = v1;
+                        if (o == r.gbo) kb[cb][0] = v0, kb[cb][1] = v1;
+                    }
                     acc[cb][0] = acc[cb][1] = 0.0;
                 }
             }
+        }
+        if constexpr (GR) {
+            if (r.gbo < 0)
+#pragma unroll
+                for (int cb = 0; cb < NBB; ++cb) {
+                    kb[cb][0] = pick_load(x, r.gbl, 2 * cb);
+                    kb[cb][1] = pick_load(x, r.gbl, 2 * cb + 1);
+                }
+            // rows past n hold zeros (their loads were zero-filled and nothing was added)
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+                const int src = (4 * ks + t) * 4 + (g >> 1);  // lane holding row 4 ks + t, columns 8 cb + g
+                double fa[GB], fb[GB];
+#pragma unroll
+                for (int cb = 0; cb < GB; ++cb) {
+                    const double a0 = __shfl_sync(0xffffffffu, ka[cb][0], src), a1 = __shfl_sync(0xffffffffu, ka[cb][1], src);
+                    const double b0 = __shfl_sync(0xffffffffu, kb[cb][0], src), b1 = __shfl_sync(0xffffffffu, kb[cb][1], src);
+                    fa[cb] = (g & 1) ? a1 : a0;
+                    fb[cb] = (g & 1) ? b1 : b0;
+                }
+#pragma unroll
+                for (int i = 0; i < GB; ++i)
+#pragma unroll
+                    for (int j = 0; j < GB; ++j) dmma884(gacc[i][j][0], gacc[i][j][1], fa[i], fb[j]);
+            }
+        }
+    }
+    if constexpr (GR) {  // warps in order -> the CTA partial (row-major a, b)
+        __shared__ double red[8][NB * NB];
+        const int warp = threadIdx.x >> 5;
+#pragma unroll
+        for (int i = 0; i < GB; ++i)
+#pragma unroll
+            for (int j = 0; j < GB; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) red[warp][(8 * i + g) * NB + 8 * j + 2 * t + h] = gacc[i][j][h];
+        __syncthreads();
+        for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+            double sum = red[0][e];
+            for (int w = 1; w < 8; ++w) sum += red[w][e];
+            r.gpart[static_cast<std::int64_t>(blockIdx.x) * NB * NB + e] = sum;
         }
     }
 }
@@ -1803,7 +1862,7 @@ void gram(Ctx* ctx, const GramJob& job, std::int64_t n, double* partials, std::i
     ctx->launches += 2;
 }
 
-void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
+bool mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
     if (job.nout < 1 || job.nout > 4 || job.nb < 1 || job.nb > 64) fail(BE_ERR_BAD_PARAMS, "mix: bad job");
     MixDev m{};
     m.nb = job.nb;
@@ -1887,9 +1946,55 @@ void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
                     else r.src[r.addl[o] = nl++] = ms.src[m.out[o].add_si];
                 }
             }
+            static const bool mix_gram_on = [] {
+                const char* e = std::getenv("BE_MIX_GRAM");
+                return !(e && e[0] == '0');
+            }();
+            bool gram = false;
+            if (fits && mix_gram_on && job.gram_out && job.gram_a >= 0 && job.gram_a < m.nout) {
+                r.ga = job.gram_a;
+                r.gbo = job.gram_b;
+                r.gbl = -1;
+                if (job.gram_b < 0)
+                    for (int o = 0; o < m.nout; ++o)
+                        if (r.addl[o] >= 0 && r.src[r.addl[o]] == job.gram_b_src) r.gbl = r.addl[o];
+                r.gpart = job.gram_partials;
+                gram = (r.gbo >= 0 && r.gbo < m.nout) || r.gbl >= 0;
+            }
             if (fits) {
                 const std::int64_t nblk = (n + 7) / 8;
-                const int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 4, (nblk + 7) / 8)));
+                int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 4, (nblk + 7) / 8)));
+                if (gram) {
+                    grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 2, (nblk + 7) / 8)));
+                    if (static_cast<std::int64_t>(grid) * job.nb * job.nb > job.gram_partials_len) gram = false;
+                }
+                if (gram) {
+                    if (job.nb == 8) {
+                        switch (nl) {
+                            case 1: k_mix_r<1, 1, true><<<grid, 256, 0, s>>>(m, r, n); break;
+                            case 2: k_mix_r<1, 2, true><<<grid, 256, 0, s>>>(m, r, n); break;
+                            case 3: k_mix_r<1, 3, true><<<grid, 256, 0, s>>>(m, r, n); break;
+                            default: k_mix_r<1, 4, true><<<grid, 256, 0, s>>>(m, r, n); break;
+                        }
+                    } else {
+                        switch (nl) {
+                            case 1: k_mix_r<2, 1, true><<<grid, 256, 0, s>>>(m, r, n); break;
+                            case 2: k_mix_r<2, 2, true><<<grid, 256, 0, s>>>(m, r, n); break;
+                            case 3: k_mix_r<2, 3, true><<<grid, 256, 0, s>>>(m, r, n); break;
+                            default: k_mix_r<2, 4, true><<<grid, 256, 0, s>>>(m, r, n); break;
+                        }
+                    }
+                    GramDev gd{};
+                    gd.npairs = 1;
+                    gd.nb = job.nb;
+                    GramOut go{};
+                    go.out[0] = job.gram_out;
+                    go.sym[0] = job.gram_sym;
+                    k_gram_reduce_m<<<(job.nb * job.nb * 32 + 255) / 256, 256, 0, s>>>(gd, go, grid, job.gram_partials);
+                    BE_CUDA(cudaGetLastError());
+                    ctx->launches += 2;
+                    return true;
+                }
 #define BE_MIXR(NBB, L) k_mix_r<NBB, L><<<grid, 256, 0, s>>>(m, r, n)
 #define BE_MIXR_L(NBB)                 \
     switch (nl) {                      \
@@ -1907,7 +2012,7 @@ void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
 #undef BE_MIXR
                 BE_CUDA(cudaGetLastError());
                 ++ctx->launches;
-                return;
+                return job.gram_out == nullptr;
             }
         }
         const bool bsm = job.nb > 16;
@@ -1931,7 +2036,7 @@ void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
             }
             BE_CUDA(cudaGetLastError());
             ++ctx->launches;
-            return;
+            return job.gram_out == nullptr;
         }
     }
     const std::size_t smp = (((static_cast<std::size_t>(m.ncoef) * job.nb * nblk * 4 + 1) & ~std::size_t{1}) +
@@ -1943,7 +2048,7 @@ void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
         k_mix_p<<<grid, kT, smp, s>>>(m, ms, n);
         BE_CUDA(cudaGetLastError());
         ++ctx->launches;
-        return;
+        return job.gram_out == nullptr;
     }
     const std::size_t sm = (static_cast<std::size_t>(m.ncoef) * job.nb * nblk * 4 +
                             static_cast<std::size_t>(ms.nsrc) * kMixRows * (job.nb + 1)) * sizeof(double);
@@ -1952,6 +2057,7 @@ void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
     k_mix<<<grid, kT, sm, s>>>(m, ms, nullptr, n);
     BE_CUDA(cudaGetLastError());
     ++ctx->launches;
+    return job.gram_out == nullptr;
 }
 
 void trsm(Ctx* ctx, double* w0, double* w1, const double* R, int nb, std::int64_t n, Status* st, int skip_if_rank,

@@ -58,8 +58,18 @@ struct MixJob {
     int nb;
     int nout;
     MixOut out[4];
+    // optional Gram epilogue: gram_out = A^T B with A = output gram_a and B = output gram_b, or
+    // (gram_b < 0) the panel gram_b_src, which must be one of the job's added panels; symmetrised
+    // when gram_sym (gram, densela.hpp:90-97). Formed only by the register-direct kernel.
+    double* gram_out = nullptr;
+    int gram_a = -1, gram_b = -1, gram_sym = 0;
+    const double* gram_b_src = nullptr;
+    double* gram_partials = nullptr;
+    std::int64_t gram_partials_len = 0;
 };
-void mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s);
+// returns whether the requested Gram epilogue was formed (false: nothing about it was launched,
+// the caller forms it separately; true when none was requested)
+bool mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s);
 
 // W <- W R^{-1} for up to two panels (trsm_right_inv, densela.hpp:125-147);
 // skipped when st->rank_deficient (skip_if_rank) / st->not_pd (skip_if_notpd).

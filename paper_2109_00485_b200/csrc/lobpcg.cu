@@ -445,7 +445,13 @@ struct Solver {
             m2.nout = 2;
             m2.out[0] = dla::MixOut{Xn.get(), 0, 1, {{X.get(), c1, 0, dim}}, -1, Pn.get()};
             m2.out[1] = dla::MixOut{HXn.get(), 0, 1, {{HX.get(), c1, 0, dim}}, -1, HPn.get()};
-            dla::mix(ctx, m2, n, s);
+            // P hygiene's first Gram X+^T P+ formed on the way (both are in the kernel's registers)
+            m2.gram_out = xtp;
+            m2.gram_a = 0;
+            m2.gram_b_src = Pn.get();
+            m2.gram_partials = partials.get();
+            m2.gram_partials_len = partials_len;
+            xtp_ready = dla::mix(ctx, m2, n, s);
             std::swap(X, Xn);
             std::swap(HX, HXn);
             std::swap(P, Pn);
@@ -454,14 +460,22 @@ struct Solver {
         nv.to("p-hygiene");
         BE_CUDA(cudaEventRecord(ev.e[6], s));
         {  // P hygiene (lobpcg.hpp:412-417) + orthonormalize_pair (:254-270)
-            gram1(X.get(), P.get(), 0, xtp);
+            if (xtp_ready) allreduce(xtp, nb * nb);
+            else gram1(X.get(), P.get(), 0, xtp);
             dla::MixJob m{};
             m.nb = nb;
             m.nout = 2;
             m.out[0] = dla::MixOut{P.get(), 1, 1, {{X.get(), xtp, 1, 0}}, -1};
             m.out[1] = dla::MixOut{HP.get(), 1, 1, {{HX.get(), xtp, 1, 0}}, -1};
-            dla::mix(ctx, m, n, s);
-            gram1(P.get(), P.get(), 1, Bp);
+            // orthonormalize_pair's Gram of the projected P, formed on the way
+            m.gram_out = Bp;
+            m.gram_a = 0;
+            m.gram_b = 0;
+            m.gram_sym = 1;
+            m.gram_partials = partials.get();
+            m.gram_partials_len = partials_len;
+            if (dla::mix(ctx, m, n, s)) allreduce(Bp, nb * nb);
+            else gram1(P.get(), P.get(), 1, Bp);
             dla::chol_floored(ctx, Bp, Rp, nb, 1e-8, st.get(), s);
             dla::trsm(ctx, P.get(), HP.get(), Rp, nb, n, st.get(), 0, 1, s);
         }
@@ -477,6 +491,7 @@ struct Solver {
         sync_status();
     }
     bool dropped_host = false;
+    bool xtp_ready = false;  // the update's mix formed X+^T P+
 
     // run up to `count` further iterations (never past maxiter); returns the
     // number executed. Stops at convergence.
