@@ -932,6 +932,12 @@ struct MixR {
     // layout); per-CTA partial [a][b] into gpart
     int ga, gbo, gbl;
     double* gpart;
+    // residual epilogue (RS): R = HX - X diag(theta) from the term-slot loads rx / rhx, per-CTA
+    // column sums of R^2 and X^2 into rpart[blk][2][nb] (k_residual's layout)
+    int rx, rhx;
+    const double* theta;
+    double* rout;
+    double* rpart;
 };
 
 template <int L, int KS>
@@ -946,11 +952,20 @@ __device__ __forceinline__ double pick_load(const double (&x)[L][KS], int l, int
 // GR: the Gram A^T B of two of the row blocks the warp holds -- an output and an output or an
 // added panel -- formed on the way (the accumulator-layout values moved into DMMA operand
 // fragments by shuffles), so the next Gram needs no read of the panels it just wrote.
-template <int NBB, int L, bool GR = false>
+// RS (with GR): the residual R = HX - X diag(theta) and its column norms from the X / HX term
+// loads (lobpcg.hpp:419: residual_block reads only X, HX and theta, which the mix does not change).
+template <int NBB, int L, bool GR = false, bool RS = false>
 __global__ void __launch_bounds__(256, GR ? 2 : 4) k_mix_r(MixDev m, MixR r, std::int64_t n) {
     constexpr int NB = 8 * NBB, KS = NB / 4;
     constexpr int GB = GR ? NBB : 1;
+    constexpr int RK = RS ? KS : 1;
     __shared__ __align__(16) double bsm[4 * KS * NBB * 32];  // [slot][kk][cb][lane]
+    __shared__ double s_theta[RS ? NB : 1];
+    if constexpr (RS)
+        if (threadIdx.x < NB) s_theta[threadIdx.x] = r.theta[threadIdx.x];
+    double rn[RK], xn[RK];
+#pragma unroll
+    for (int kk = 0; kk < RK; ++kk) rn[kk] = xn[kk] = 0.0;
     double gacc[GB][GB][2];
 #pragma unroll
     for (int i = 0; i < GB; ++i)
@@ -988,6 +1003,20 @@ __global__ void __launch_bounds__(256, GR ? 2 : 4) k_mix_r(MixDev m, MixR r, std
                 x[l][2 * h] = v.x;
                 x[l][2 * h + 1] = v.y;
             }
+        }
+        if constexpr (RS) {  // columns KS t .. KS t + KS - 1 of row `row` (the term-slot layout)
+            double rv[KS];
+#pragma unroll
+            for (int kk = 0; kk < KS; ++kk) {
+                const double xv = pick_load(x, r.rx, kk), hv = pick_load(x, r.rhx, kk);
+                rv[kk] = hv - xv * s_theta[KS * t + kk];
+                rn[kk] += rv[kk] * rv[kk];
+                xn[kk] += xv * xv;
+            }
+            if (ok)
+#pragma unroll
+                for (int h = 0; h < KS / 2; ++h)
+                    *reinterpret_cast<double2*>(r.rout + row * NB + KS * t + 2 * h) = make_double2(rv[2 * h], rv[2 * h + 1]);
         }
         double acc[NBB][2];
 #pragma unroll
@@ -1064,6 +1093,30 @@ __global__ void __launch_bounds__(256, GR ? 2 : 4) k_mix_r(MixDev m, MixR r, std
             double sum = red[0][e];
             for (int w = 1; w < 8; ++w) sum += red[w][e];
             r.gpart[static_cast<std::int64_t>(blockIdx.x) * NB * NB + e] = sum;
+        }
+    }
+    if constexpr (RS) {  // rows of a warp (lanes of equal t) by butterfly, then warps in order
+        __shared__ double rred[8][2][NB];
+        const int warp = threadIdx.x >> 5;
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                rn[kk] += __shfl_xor_sync(0xffffffffu, rn[kk], o);
+                xn[kk] += __shfl_xor_sync(0xffffffffu, xn[kk], o);
+            }
+        if (g == 0)
+#pragma unroll
+            for (int kk = 0; kk < KS; ++kk) {
+                rred[warp][0][KS * t + kk] = rn[kk];
+                rred[warp][1][KS * t + kk] = xn[kk];
+            }
+        __syncthreads();
+        if (threadIdx.x < 2 * NB) {
+            const int wh = threadIdx.x / NB, c = threadIdx.x % NB;
+            double sum = rred[0][wh][c];
+            for (int w = 1; w < 8; ++w) sum += rred[w][wh][c];
+            r.rpart[(static_cast<std::int64_t>(blockIdx.x) * 2 + wh) * NB + c] = sum;
         }
     }
 }
@@ -1961,28 +2014,46 @@ bool mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
                 r.gpart = job.gram_partials;
                 gram = (r.gbo >= 0 && r.gbo < m.nout) || r.gbl >= 0;
             }
+            bool res = false;  // the residual epilogue rides on the Gram kernel
+            if (gram && job.res_out) {
+                r.rx = r.rhx = -1;
+                for (int q = 0; q < r.nq; ++q) {
+                    if (r.src[q] == job.res_x) r.rx = q;
+                    if (r.src[q] == job.res_hx) r.rhx = q;
+                }
+                r.theta = job.res_theta;
+                r.rout = job.res_out;
+                res = r.rx >= 0 && r.rhx >= 0;
+                if (!res) gram = false;  // both or neither: the caller then forms them apart
+            } else if (job.res_out) {
+                gram = false;
+            }
             if (fits) {
                 const std::int64_t nblk = (n + 7) / 8;
                 int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 4, (nblk + 7) / 8)));
                 if (gram) {
                     grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 2, (nblk + 7) / 8)));
-                    if (static_cast<std::int64_t>(grid) * job.nb * job.nb > job.gram_partials_len) gram = false;
+                    const std::int64_t need = static_cast<std::int64_t>(grid) * job.nb * (job.nb + (res ? 2 : 0));
+                    if (need > job.gram_partials_len) gram = false;
+                    r.rpart = job.gram_partials + static_cast<std::int64_t>(grid) * job.nb * job.nb;
                 }
                 if (gram) {
+#define BE_MIXG(NBB, RSV)                                                        \
+    switch (nl) {                                                               \
+        case 1: k_mix_r<NBB, 1, true, RSV><<<grid, 256, 0, s>>>(m, r, n); break; \
+        case 2: k_mix_r<NBB, 2, true, RSV><<<grid, 256, 0, s>>>(m, r, n); break; \
+        case 3: k_mix_r<NBB, 3, true, RSV><<<grid, 256, 0, s>>>(m, r, n); break; \
+        default: k_mix_r<NBB, 4, true, RSV><<<grid, 256, 0, s>>>(m, r, n); break; \
+    }
                     if (job.nb == 8) {
-                        switch (nl) {
-                            case 1: k_mix_r<1, 1, true><<<grid, 256, 0, s>>>(m, r, n); break;
-                            case 2: k_mix_r<1, 2, true><<<grid, 256, 0, s>>>(m, r, n); break;
-                            case 3: k_mix_r<1, 3, true><<<grid, 256, 0, s>>>(m, r, n); break;
-                            default: k_mix_r<1, 4, true><<<grid, 256, 0, s>>>(m, r, n); break;
-                        }
+                        if (res) { BE_MIXG(1, true) } else { BE_MIXG(1, false) }
                     } else {
-                        switch (nl) {
-                            case 1: k_mix_r<2, 1, true><<<grid, 256, 0, s>>>(m, r, n); break;
-                            case 2: k_mix_r<2, 2, true><<<grid, 256, 0, s>>>(m, r, n); break;
-                            case 3: k_mix_r<2, 3, true><<<grid, 256, 0, s>>>(m, r, n); break;
-                            default: k_mix_r<2, 4, true><<<grid, 256, 0, s>>>(m, r, n); break;
-                        }
+                        if (res) { BE_MIXG(2, true) } else { BE_MIXG(2, false) }
+                    }
+#undef BE_MIXG
+                    if (res) {
+                        k_norm_reduce<<<1, 256, 0, s>>>(r.rpart, grid, job.nb, job.res_rn2, job.res_xn2);
+                        ++ctx->launches;
                     }
                     GramDev gd{};
                     gd.npairs = 1;

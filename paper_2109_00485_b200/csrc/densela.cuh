@@ -66,6 +66,15 @@ struct MixJob {
     const double* gram_b_src = nullptr;
     double* gram_partials = nullptr;
     std::int64_t gram_partials_len = 0;
+    // optional residual epilogue (with the Gram epilogue only; both or neither are formed):
+    // res_out = res_hx - res_x diag(res_theta), column sums of its squares and of res_x's squares
+    // into res_rn2 / res_xn2 (residual() below); res_x / res_hx must be term sources of the job
+    double* res_out = nullptr;
+    const double* res_x = nullptr;
+    const double* res_hx = nullptr;
+    const double* res_theta = nullptr;
+    double* res_rn2 = nullptr;
+    double* res_xn2 = nullptr;
 };
 // returns whether the requested Gram epilogue was formed (false: nothing about it was launched,
 // the caller forms it separately; true when none was requested)

@@ -245,9 +245,10 @@ struct Solver {
     }
 
     // qr_of_transpose (densela.hpp:412-445); returns false on RankDeficient
-    bool qr(double* A, bool check) {
+    bool qr(double* A, bool check, bool gram_given = false) {
         reset_qr_flags();
-        bool have_gram = false;  // the first pass's trsm formed the second pass's Gram
+        bool have_gram = gram_given;  // Bq already holds A^T A (the producer formed it) / the first
+                                      // pass's trsm formed the second pass's Gram
         for (int pass = 0; pass < 2; ++pass) {
             if (!have_gram) gram1(A, A, 1, Bq);
             dla::qr_chol(ctx, Bq, Rq, nb, st.get(), s);
@@ -268,13 +269,24 @@ struct Solver {
     }
 
     // project_out (lobpcg.hpp:243-246): w -= basis (basis^T w)
-    void project_out(double* w, const double* basis) {
+    // gram_next: the Gram of the projected w (the next qr_of_transpose's first pass) is formed
+    // into Bq on the way; returns whether it was
+    bool project_out(double* w, const double* basis, bool gram_next = false) {
         gram1(basis, w, 0, xtp);
         dla::MixJob m{};
         m.nb = nb;
         m.nout = 1;
         m.out[0] = dla::MixOut{w, 1, 1, {{basis, xtp, 1, 0}}, -1};
-        dla::mix(ctx, m, n, s);
+        if (gram_next) {
+            m.gram_out = Bq;
+            m.gram_a = m.gram_b = 0;
+            m.gram_sym = 1;
+            m.gram_partials = partials.get();
+            m.gram_partials_len = partials_len;
+        }
+        const bool g = dla::mix(ctx, m, n, s) && gram_next;
+        if (g) allreduce(Bq, nb * nb);
+        return g;
     }
 
     // rayleigh_ritz (lobpcg.hpp:113-157): false on BasisDegenerate
@@ -409,9 +421,9 @@ struct Solver {
             upload_random(W.get(), cfg.seed + static_cast<std::uint64_t>(iter) * 7919u);
             if (!qr(W.get(), true)) fail(BE_ERR_RANK_DEFICIENT, "qr_of_transpose: Gram Cholesky failed twice");
         }
-        project_out(W.get(), X.get());
-        if (p_active) project_out(W.get(), P.get());
-        qr(W.get(), false);  // RankDeficient swallowed: W keeps the completed passes
+        bool wg = project_out(W.get(), X.get(), !p_active);
+        if (p_active) wg = project_out(W.get(), P.get(), true);
+        qr(W.get(), false, wg);  // RankDeficient swallowed: W keeps the completed passes
         nv.to("spmm");
         BE_CUDA(cudaEventRecord(ev.e[2], s));
         apply_op(W.get(), HW.get());
@@ -474,14 +486,23 @@ struct Solver {
             m.gram_sym = 1;
             m.gram_partials = partials.get();
             m.gram_partials_len = partials_len;
-            if (dla::mix(ctx, m, n, s)) allreduce(Bp, nb * nb);
+            // residual_block (lobpcg.hpp:419) from the same X / HX loads: it reads only X, HX and
+            // theta, which P hygiene leaves alone
+            m.res_out = R.get();
+            m.res_x = X.get();
+            m.res_hx = HX.get();
+            m.res_theta = theta;
+            m.res_rn2 = rn2;
+            m.res_xn2 = xn2;
+            res_ready = dla::mix(ctx, m, n, s);
+            if (res_ready) allreduce(Bp, nb * nb);
             else gram1(P.get(), P.get(), 1, Bp);
             dla::chol_floored(ctx, Bp, Rp, nb, 1e-8, st.get(), s);
             dla::trsm(ctx, P.get(), HP.get(), Rp, nb, n, st.get(), 0, 1, s);
         }
         nv.to("residual");
         BE_CUDA(cudaEventRecord(ev.e[7], s));
-        dla::residual(ctx, HX.get(), X.get(), theta, R.get(), nb, n, partials.get(), rn2, xn2, s);
+        if (!res_ready) dla::residual(ctx, HX.get(), X.get(), theta, R.get(), nb, n, partials.get(), rn2, xn2, s);
         allreduce(rn2, 2 * nb);
         BE_CUDA(cudaMemcpyAsync(hm->theta, theta, nb * 8, cudaMemcpyDeviceToHost, s));
         BE_CUDA(cudaMemcpyAsync(hm->rn2, rn2, nb * 8, cudaMemcpyDeviceToHost, s));
@@ -492,6 +513,7 @@ struct Solver {
     }
     bool dropped_host = false;
     bool xtp_ready = false;  // the update's mix formed X+^T P+
+    bool res_ready = false;  // P hygiene's mix formed the residual and its norms
 
     // run up to `count` further iterations (never past maxiter); returns the
     // number executed. Stops at convergence.
