@@ -931,6 +931,7 @@ struct MixR {
     // Gram epilogue (GR): A = output ga, B = output gbo or (gbo < 0) load gbl (accumulator
     // layout); per-CTA partial [a][b] into gpart
     int ga, gbo, gbl;
+    int gal;  // ga < 0: A from load gal (accumulator layout)
     double* gpart;
     // residual epilogue (RS): R = HX - X diag(theta) from the term-slot loads rx / rhx, per-CTA
     // column sums of R^2 and X^2 into rpart[blk][2][nb] (k_residual's layout)
@@ -1059,6 +1060,12 @@ __global__ void __launch_bounds__(256, GR ? 2 : 4) k_mix_r(MixDev m, MixR r, std
                 for (int cb = 0; cb < NBB; ++cb) {
                     kb[cb][0] = pick_load(x, r.gbl, 2 * cb);
                     kb[cb][1] = pick_load(x, r.gbl, 2 * cb + 1);
+                }
+            if (r.ga < 0)
+#pragma unroll
+                for (int cb = 0; cb < NBB; ++cb) {
+                    ka[cb][0] = pick_load(x, r.gal, 2 * cb);
+                    ka[cb][1] = pick_load(x, r.gal, 2 * cb + 1);
                 }
             // rows past n hold zeros (their loads were zero-filled and nothing was added)
 #pragma unroll
@@ -2004,7 +2011,11 @@ bool mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
                 return !(e && e[0] == '0');
             }();
             bool gram = false;
-            if (fits && mix_gram_on && job.gram_out && job.gram_a >= 0 && job.gram_a < m.nout) {
+            r.gal = -1;
+            if (fits && mix_gram_on && job.gram_out && job.gram_a < 0 && job.gram_a_src) {
+                if (nl < 4) r.src[r.gal = nl++] = job.gram_a_src;  // else no room: no Gram
+            }
+            if (fits && mix_gram_on && job.gram_out && ((job.gram_a >= 0 && job.gram_a < m.nout) || r.gal >= 0)) {
                 r.ga = job.gram_a;
                 r.gbo = job.gram_b;
                 r.gbl = -1;

@@ -63,6 +63,7 @@ struct MixJob {
     // when gram_sym (gram, densela.hpp:90-97). Formed only by the register-direct kernel.
     double* gram_out = nullptr;
     int gram_a = -1, gram_b = -1, gram_sym = 0;
+    const double* gram_a_src = nullptr;  // A = this panel (gram_a < 0), loaded as one more panel
     const double* gram_b_src = nullptr;
     double* gram_partials = nullptr;
     std::int64_t gram_partials_len = 0;

@@ -119,7 +119,7 @@ struct Solver {
     dla::Sygv sygv;
     double* blocks = nullptr;  // 12 nb x nb
     double *G = nullptr, *O = nullptr, *C = nullptr, *theta = nullptr;
-    double *Bq = nullptr, *Rq = nullptr, *xtp = nullptr, *Bp = nullptr, *Rp = nullptr;
+    double *Bq = nullptr, *Rq = nullptr, *xtp = nullptr, *Bp = nullptr, *Rp = nullptr, *ptw = nullptr;
     double *rn2 = nullptr, *xn2 = nullptr, *shifts = nullptr, *pn2 = nullptr;
     std::int64_t partials_len = 0;
     // pinned host mirror of the small readbacks
@@ -172,6 +172,7 @@ struct Solver {
         xtp = p; p += nb2;
         Bp = p; p += nb2;
         Rp = p; p += nb2;
+        ptw = p;  // P^T W formed by the X projection's mix
         p += 3 * nb2;
         theta = p; p += nb;
         rn2 = p; p += nb;
@@ -271,21 +272,26 @@ struct Solver {
     // project_out (lobpcg.hpp:243-246): w -= basis (basis^T w)
     // gram_next: the Gram of the projected w (the next qr_of_transpose's first pass) is formed
     // into Bq on the way; returns whether it was
-    bool project_out(double* w, const double* basis, bool gram_next = false) {
-        gram1(basis, w, 0, xtp);
+    // next_basis: instead, the next projection's Gram next_basis^T w' goes into ptw (that basis
+    // loaded as one more panel of the mix); basis_gram: xtp already holds basis^T w.
+    bool project_out(double* w, const double* basis, bool gram_next = false, const double* next_basis = nullptr,
+                     bool basis_gram = false) {
+        if (!basis_gram) gram1(basis, w, 0, xtp);
         dla::MixJob m{};
         m.nb = nb;
         m.nout = 1;
         m.out[0] = dla::MixOut{w, 1, 1, {{basis, xtp, 1, 0}}, -1};
-        if (gram_next) {
-            m.gram_out = Bq;
-            m.gram_a = m.gram_b = 0;
-            m.gram_sym = 1;
+        if (gram_next || next_basis) {
+            m.gram_out = next_basis ? ptw : Bq;
+            m.gram_a = next_basis ? -1 : 0;
+            m.gram_a_src = next_basis;
+            m.gram_b = 0;
+            m.gram_sym = next_basis ? 0 : 1;
             m.gram_partials = partials.get();
             m.gram_partials_len = partials_len;
         }
-        const bool g = dla::mix(ctx, m, n, s) && gram_next;
-        if (g) allreduce(Bq, nb * nb);
+        const bool g = dla::mix(ctx, m, n, s) && (gram_next || next_basis);
+        if (g) allreduce(m.gram_out, nb * nb);
         return g;
     }
 
@@ -421,8 +427,11 @@ struct Solver {
             upload_random(W.get(), cfg.seed + static_cast<std::uint64_t>(iter) * 7919u);
             if (!qr(W.get(), true)) fail(BE_ERR_RANK_DEFICIENT, "qr_of_transpose: Gram Cholesky failed twice");
         }
-        bool wg = project_out(W.get(), X.get(), !p_active);
-        if (p_active) wg = project_out(W.get(), P.get(), true);
+        bool wg = project_out(W.get(), X.get(), !p_active, p_active ? P.get() : nullptr);
+        if (p_active) {
+            if (wg) std::swap(xtp, ptw);  // P^T W' is ready: the second projection's coefficients
+            wg = project_out(W.get(), P.get(), true, nullptr, wg);
+        }
         qr(W.get(), false, wg);  // RankDeficient swallowed: W keeps the completed passes
         nv.to("spmm");
         BE_CUDA(cudaEventRecord(ev.e[2], s));
