@@ -272,41 +272,6 @@ __device__ __forceinline__ void block_colsum4(double (&v)[kCW], double (*red)[16
     }
 }
 
-// block_colsum4 for Q column sets at once (one barrier pair): red holds [2 NW + 2][Q * 16].
-template <int C, int NT, int Q>
-__device__ __forceinline__ void block_colsumQ(double (&v)[Q][kCW], double (*red)[Q * 16], int& buf) {
-    constexpr int NW = NT / 32, CQ = C / kCW;
-#pragma unroll
-    for (int o = CQ; o < 32; o <<= 1)
-#pragma unroll
-        for (int q = 0; q < Q; ++q)
-#pragma unroll
-            for (int j = 0; j < kCW; ++j) v[q][j] += __shfl_xor_sync(0xffffffffu, v[q][j], o);
-    if constexpr (NW > 1) {
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        const int cq = threadIdx.x % CQ;
-        if (lane < CQ)
-#pragma unroll
-            for (int q = 0; q < Q; ++q)
-#pragma unroll
-                for (int j = 0; j < kCW; ++j) red[buf * NW + warp][q * 16 + cq * kCW + j] = v[q][j];
-        __syncthreads();
-        if (threadIdx.x < Q * C) {  // one thread per (set, column) sums the warps in order
-            const int q = threadIdx.x / C, c = threadIdx.x % C;
-            double t = red[buf * NW][q * 16 + c];
-#pragma unroll
-            for (int w = 1; w < NW; ++w) t += red[buf * NW + w][q * 16 + c];
-            red[2 * NW + buf][q * 16 + c] = t;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < Q; ++q)
-#pragma unroll
-            for (int j = 0; j < kCW; ++j) v[q][j] = red[2 * NW + buf][q * 16 + cq * kCW + j];
-        buf ^= 1;
-    }
-}
-
 template <int NT>
 __device__ __forceinline__ void block_sync() {
     if constexpr (NT == 32) __syncwarp(); else __syncthreads();
@@ -528,10 +493,6 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
     extern __shared__ __align__(16) double sV[];  // current basis vector [dmax][C], then the staged entries
     __shared__ __align__(16) double red[2 * (NT / 32) + 2][16];
     int rbuf = 0;
-#ifdef BE_FOM_CGS
-    __shared__ __align__(16) double redq[(MC == 4 && C == 16) ? 2 * (NT / 32) + 2 : 1][(MC - 1) * 16];
-    int rbufq = 0;
-#endif
 #ifdef BE_FOM_PROF
     long long prof_t = clock64();
 #endif
@@ -733,42 +694,6 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 8 : (NT >= 512 ? 1 : 2))
                 w[k][j] = x;
             }
         }
-#ifdef BE_FOM_CGS
-        if constexpr (MC == 4 && C == 16) {  // classical Gram-Schmidt: the s + 1 dots in one reduction
-            double cacc[MC - 1][kCW];
-#pragma unroll
-            for (int q = 0; q < MC - 1; ++q)
-#pragma unroll
-                for (int j = 0; j < kCW; ++j) cacc[q][j] = 0.0;
-#pragma unroll
-            for (int q = 0; q < MC - 1; ++q) {
-                if (q > s) break;
-#pragma unroll
-                for (int k = 0; k < RPT; ++k) {
-                    const int i = rl + k * RL;
-                    if (i < d) {
-                        const V4 v = (q == s ? ld4<H>(Vc + static_cast<std::size_t>(i) * C, hp) : ld4<H>(vg(q, i), hp));
-#pragma unroll
-                        for (int j = 0; j < kCW; ++j) cacc[q][j] += v.a[j] * w[k][j];
-                    }
-                }
-            }
-            block_colsumQ<C, NT, MC - 1>(cacc, redq, rbufq);
-#pragma unroll
-            for (int q = 0; q < MC - 1; ++q) {
-                if (q > s) break;
-#pragma unroll
-                for (int k = 0; k < RPT; ++k) {
-                    const int i = rl + k * RL;
-                    if (i < d) {
-                        const V4 v = (q == s ? ld4<H>(Vc + static_cast<std::size_t>(i) * C, hp) : ld4<H>(vg(q, i), hp));
-#pragma unroll
-                        for (int j = 0; j < kCW; ++j) w[k][j] -= cacc[q][j] * v.a[j];
-                    }
-                }
-            }
-        } else
-#endif
         for (int q = 0; q <= s; ++q) {  // one reorthogonalisation pass, in order
 #pragma unroll
             for (int j = 0; j < kCW; ++j) acc[j] = 0.0;
