@@ -956,7 +956,7 @@ __device__ __forceinline__ double pick_load(const double (&x)[L][KS], int l, int
 // RS (with GR): the residual R = HX - X diag(theta) and its column norms from the X / HX term
 // loads (lobpcg.hpp:419: residual_block reads only X, HX and theta, which the mix does not change).
 template <int NBB, int L, bool GR = false, bool RS = false>
-__global__ void __launch_bounds__(256, GR ? 2 : 4) k_mix_r(MixDev m, MixR r, std::int64_t n) {
+__global__ void __launch_bounds__(256, GR ? (L <= 2 && !RS ? 3 : 2) : 4) k_mix_r(MixDev m, MixR r, std::int64_t n) {
     constexpr int NB = 8 * NBB, KS = NB / 4;
     constexpr int GB = GR ? NBB : 1;
     constexpr int RK = RS ? KS : 1;
@@ -2043,7 +2043,8 @@ bool mix(Ctx* ctx, const MixJob& job, std::int64_t n, cudaStream_t s) {
                 const std::int64_t nblk = (n + 7) / 8;
                 int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 4, (nblk + 7) / 8)));
                 if (gram) {
-                    grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * 2, (nblk + 7) / 8)));
+                    const int per_sm = nl <= 2 && !res ? 3 : 2;  // the kernel's resident CTAs (launch bounds)
+                    grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ctx->num_sms * per_sm, (nblk + 7) / 8)));
                     const std::int64_t need = static_cast<std::int64_t>(grid) * job.nb * (job.nb + (res ? 2 : 0));
                     if (need > job.gram_partials_len) gram = false;
                     r.rpart = job.gram_partials + static_cast<std::int64_t>(grid) * job.nb * job.nb;
